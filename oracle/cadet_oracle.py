@@ -1,0 +1,523 @@
+"""CADET hot-path ORACLE — plain, slow, fp64 CPU reference.
+
+TEST INFRASTRUCTURE ONLY.  Only `tests/`, `__graft_entry__.smoke()` and
+`bench.py`'s cpu_baseline / `--impl reference` legs may import this module.
+It shares no code with the CUDA path (paper_2602_11410_b200/) and never
+imports it.  Every function follows PAPER.md (P:n) / SPEC.md (S:n) as cited,
+with the readings R1..R21 listed in DESIGN.md §3.
+
+Conventions: row-vector projections y = x.W, W[d_in][d_out] (R1); all math in
+float64 on bf16-valued inputs (R20); heads are per-head slices of width hd of
+the d-wide rows; RoPE pairs are adjacent (2i, 2i+1) (R4), per head (R5).
+Parity status: every function below is pinned by a `-m "not gpu"` test in
+tests/test_oracle_pins.py (no "parity unpinned" functions).
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+import numpy as np
+
+MASK_TIME = 1
+MASK_SESSION = 2
+MASK_PAIR_PREV = 4
+
+
+# ------------------------------------------------------------------ config
+@dataclass
+class AttnConfig:
+    d_model: int
+    n_heads: int
+    mask_flags: int = MASK_TIME
+    delta_delay_ms: int = 3_600_000          # P:561 "Delta_delay of one hour"
+    delta_cand_ms: int = 0                    # R11: candidates see all context
+    rope_dt_max_ms: int = 31_536_000_000      # P:627, R6
+    rope_phi_min: float = 1e-4
+    rope_base: float = 600000.0
+    use_rope: bool = True
+    use_rep_gate: bool = True
+    use_int_gate: bool = True
+    use_out_proj: bool = True
+
+    @property
+    def head_dim(self) -> int:
+        return self.d_model // self.n_heads
+
+
+# ------------------------------------------------------------------ numerics
+def sigmoid(x):
+    """sigma(x) = 1/(1+exp(-x)); evaluated without overflow."""
+    x = np.asarray(x, dtype=np.float64)
+    out = np.empty_like(x)
+    pos = x >= 0
+    out[pos] = 1.0 / (1.0 + np.exp(-x[pos]))
+    e = np.exp(x[~pos])
+    out[~pos] = e / (1.0 + e)
+    return out
+
+
+def softplus(x):
+    return np.logaddexp(0.0, np.asarray(x, dtype=np.float64))
+
+
+# ------------------------------------------------------------------ RoPE
+def rope_theta(head_dim: int, phi_min: float, base: float, dt_max_ms: int) -> np.ndarray:
+    """theta_i = (phi_min / dt_max) * base^(2i/d), i in [0, d/2)  (R5: d = head dim)."""
+    i = np.arange(head_dim // 2, dtype=np.float64)
+    return (phi_min / float(dt_max_ms)) * np.power(float(base), 2.0 * i / head_dim)
+
+
+def rope_rotate(x: np.ndarray, t_ms: np.ndarray, theta: np.ndarray, sign: float = 1.0) -> np.ndarray:
+    """Rotate adjacent pairs (x_2i, x_2i+1) of each row by alpha_i = t * theta_i.
+
+    x: [m, hd]; t_ms: int64 [m] absolute Unix ms, used as fp64 (R21).
+    sign=-1 applies R(-alpha) (the transpose), used by the backward.
+    """
+    alpha = sign * t_ms.astype(np.float64)[:, None] * theta[None, :]
+    c, s = np.cos(alpha), np.sin(alpha)
+    x0, x1 = x[:, 0::2], x[:, 1::2]
+    out = np.empty_like(x, dtype=np.float64)
+    out[:, 0::2] = x0 * c - x1 * s
+    out[:, 1::2] = x0 * s + x1 * c
+    return out
+
+
+# ------------------------------------------------------------------ mask (Fig. 3)
+def mask_dense(t_ms, n_cand: int, cfg: AttnConfig, session_ids=None, n_static: int = 0,
+               pair_flags=None) -> np.ndarray:
+    """Dense boolean mask A[i, j] (True = may attend) for ONE sequence (local indices).
+
+    - j == i always allowed (preserved diagonal, Fig. 3 caption P:383; R8).
+    - context query i < L (L = m - n_cand): j < i and
+        (TIME    => t_j <= t_i - Delta_delay)   (Eq. 6; tie allowed, R9)
+        (SESSION => sess_j < sess_i)            (R10, opt-in)
+      plus j < min(i, n_static) always (R13), plus j == i-1 if PAIR_PREV and flag_i (R12).
+    - candidate query i >= L: j < L and t_j <= t_i - Delta_cand (R11), never
+      another candidate.
+    """
+    t = np.asarray(t_ms, dtype=np.int64)
+    m = t.shape[0]
+    L = m - int(n_cand)
+    i = np.arange(m)[:, None]
+    j = np.arange(m)[None, :]
+    ctx_ok = j < i
+    if cfg.mask_flags & MASK_TIME:
+        ctx_ok = ctx_ok & (t[None, :] <= t[:, None] - np.int64(cfg.delta_delay_ms))
+    if cfg.mask_flags & MASK_SESSION:
+        s = np.asarray(session_ids, dtype=np.int64)
+        ctx_ok = ctx_ok & (s[None, :] < s[:, None])
+    if n_static:
+        ctx_ok = ctx_ok | (j < np.minimum(i, n_static))
+    if (cfg.mask_flags & MASK_PAIR_PREV) and pair_flags is not None:
+        pf = np.asarray(pair_flags).astype(bool)
+        ctx_ok = ctx_ok | ((j == i - 1) & pf[:, None])
+    cand_ok = (j < L) & (t[None, :] <= t[:, None] - np.int64(cfg.delta_cand_ms))
+    A = np.where(i < L, ctx_ok, cand_ok)
+    A = A | (i == j)
+    return A
+
+
+def kv_end_local(A: np.ndarray) -> np.ndarray:
+    """Exclusive end of the visible off-diagonal prefix of each row.
+
+    A must be built WITHOUT the PAIR_PREV exception (the canonical kv_end ignores
+    it).  Asserts every row is a prefix U {i}, which holds when timestamps and
+    session ids are non-decreasing within the sequence.
+    """
+    m = A.shape[0]
+    e = np.zeros(m, dtype=np.int64)
+    for i in range(m):
+        row = A[i, :i]
+        nz = np.nonzero(row)[0]
+        ei = 0 if nz.size == 0 else int(nz[-1]) + 1
+        assert row[:ei].all(), "mask row is not a prefix"
+        assert not A[i, i + 1:].any(), "mask row sees the future"
+        e[i] = ei
+    return e
+
+
+def tile_classes(A: np.ndarray, tile: int = 128) -> np.ndarray:
+    """Per (q-tile, k-tile), anchored at the sequence start, in-bounds cells only:
+    0 = SKIP (none allowed), 1 = PARTIAL, 2 = FULL (all allowed)."""
+    m = A.shape[0]
+    nq = (m + tile - 1) // tile
+    out = np.zeros((nq, nq), dtype=np.int8)
+    for a in range(nq):
+        for b in range(nq):
+            blk = A[a * tile:(a + 1) * tile, b * tile:(b + 1) * tile]
+            out[a, b] = 0 if not blk.any() else (2 if blk.all() else 1)
+    return out
+
+
+def count_pairs_inference(L: int, N: int) -> int:
+    """Closed form of the allowed-pair count for the candidate pattern: L(L+1)/2 + N(L+1)."""
+    return L * (L + 1) // 2 + N * (L + 1)
+
+
+# ------------------------------------------------------------------ batching
+def chunk_offsets(cu: np.ndarray, L_chunk: int) -> np.ndarray:
+    """Split each [a, e) at e - L_chunk, e - 2 L_chunk, ... (newest chunk full);
+    chunks emitted in buffer (time) order so they stay contiguous."""
+    out = [0]
+    for s in range(len(cu) - 1):
+        a, e = int(cu[s]), int(cu[s + 1])
+        bounds = []
+        k = 1
+        while True:
+            lo = max(a, e - k * L_chunk)
+            bounds.append(lo)
+            if lo == a:
+                break
+            k += 1
+        for b in reversed(bounds[:-1]):
+            out.append(b)
+        out.append(e)
+    return np.asarray(out, dtype=np.int64)
+
+
+def pack_greedy(lengths, budget: int):
+    """Greedy arrival-order packing into ONE fixed-budget buffer.
+    Returns (cu_seqlens, n_packed, pad)."""
+    cu = [0]
+    for m in lengths:
+        if cu[-1] + int(m) > budget:
+            break
+        cu.append(cu[-1] + int(m))
+    return np.asarray(cu, dtype=np.int64), len(cu) - 1, budget - cu[-1]
+
+
+# ------------------------------------------------------------------ attention core (Eq. 7)
+def attention_core_forward(Qr, Kr, V, A, n_heads: int):
+    """Per head: S = Q K^T / sqrt(hd); S[~A] = -inf; P = softmax_rows(S); O = P V.
+    Returns O [m, H*hd], LSE [H, m] (natural log of the masked row sum of exp(S)), P list."""
+    m, d = Qr.shape
+    hd = d // n_heads
+    O = np.zeros((m, d))
+    lse = np.zeros((n_heads, m))
+    Ps = []
+    for h in range(n_heads):
+        sl = slice(h * hd, (h + 1) * hd)
+        S = Qr[:, sl] @ Kr[:, sl].T / math.sqrt(hd)
+        S = np.where(A, S, -np.inf)
+        mx = S.max(axis=1, keepdims=True)
+        E = np.where(A, np.exp(S - mx), 0.0)
+        Z = E.sum(axis=1, keepdims=True)
+        P = E / Z
+        O[:, sl] = P @ V[:, sl]
+        lse[h] = (mx + np.log(Z))[:, 0]
+        Ps.append(P)
+    return O, lse, Ps
+
+
+def attention_core_backward(Qr, Kr, V, A, dO, n_heads: int):
+    """Adjoint of attention_core_forward (row A10): dV = P^T dO; dP = dO V^T;
+    dS = P * (dP - rowsum(dO*O)); dQ = dS K / sqrt(hd); dK = dS^T Q / sqrt(hd)."""
+    m, d = Qr.shape
+    hd = d // n_heads
+    O, _, Ps = attention_core_forward(Qr, Kr, V, A, n_heads)
+    dQ = np.zeros_like(Qr, dtype=np.float64)
+    dK = np.zeros_like(Kr, dtype=np.float64)
+    dV = np.zeros_like(V, dtype=np.float64)
+    for h in range(n_heads):
+        sl = slice(h * hd, (h + 1) * hd)
+        P = Ps[h]
+        dV[:, sl] = P.T @ dO[:, sl]
+        dP = dO[:, sl] @ V[:, sl].T
+        D = (dO[:, sl] * O[:, sl]).sum(axis=1, keepdims=True)
+        dS = P * (dP - D)
+        dQ[:, sl] = dS @ Kr[:, sl] / math.sqrt(hd)
+        dK[:, sl] = dS.T @ Qr[:, sl] / math.sqrt(hd)
+    return dQ, dK, dV
+
+
+# ------------------------------------------------------------------ full gated layer (Eqs. 3-7)
+def rope_heads(X, t_ms, cfg: AttnConfig, sign: float = 1.0):
+    hd = cfg.head_dim
+    th = rope_theta(hd, cfg.rope_phi_min, cfg.rope_base, cfg.rope_dt_max_ms)
+    out = np.empty_like(X, dtype=np.float64)
+    for h in range(cfg.n_heads):
+        sl = slice(h * hd, (h + 1) * hd)
+        out[:, sl] = rope_rotate(X[:, sl], t_ms, th, sign)
+    return out
+
+
+def layer_forward_seq(X, W, t_ms, A, cfg: AttnConfig):
+    """One sequence through the self-gated attention layer.
+
+    Gx = sigma(X W_xg), Xt = X * Gx                 (Eq. 4; R1)
+    Q, K, V = Xt W_q, Xt W_k, Xt W_v                (Eq. 3; R2)
+    Qt = Q * sigma(Q W_qg), Kt = K * sigma(K W_kg)  (Eq. 5)
+    Qr, Kr = RoPE_t(Qt), RoPE_t(Kt) per head        (R3-R5)
+    O = softmax(Qr Kr^T / sqrt(hd) + M) V           (Eq. 7; R16)
+    Y = O W_o                                       (R14)
+    """
+    X = np.asarray(X, dtype=np.float64)
+    Wxg, Wq, Wk, Wv, Wqg, Wkg, Wo = [np.asarray(w, dtype=np.float64) for w in W]
+    c = {}
+    c["X"] = X
+    if cfg.use_rep_gate:
+        c["Zx"] = X @ Wxg
+        c["Gx"] = sigmoid(c["Zx"])
+        Xt = X * c["Gx"]
+    else:
+        Xt = X
+    c["Xt"] = Xt
+    Q, K, V = Xt @ Wq, Xt @ Wk, Xt @ Wv
+    c["Q"], c["K"], c["V"] = Q, K, V
+    if cfg.use_int_gate:
+        c["Zq"], c["Zk"] = Q @ Wqg, K @ Wkg
+        c["Gq"], c["Gk"] = sigmoid(c["Zq"]), sigmoid(c["Zk"])
+        Qt, Kt = Q * c["Gq"], K * c["Gk"]
+    else:
+        Qt, Kt = Q, K
+    c["Qt"], c["Kt"] = Qt, Kt
+    if cfg.use_rope:
+        Qr, Kr = rope_heads(Qt, t_ms, cfg), rope_heads(Kt, t_ms, cfg)
+    else:
+        Qr, Kr = Qt, Kt
+    c["Qr"], c["Kr"] = Qr, Kr
+    O, lse, _ = attention_core_forward(Qr, Kr, V, A, cfg.n_heads)
+    c["O"], c["lse"] = O, lse
+    Y = O @ Wo if cfg.use_out_proj else O
+    c["Y"] = Y
+    return Y, c
+
+
+def layer_backward_seq(c, W, t_ms, A, dY, cfg: AttnConfig):
+    """Hand-derived adjoint of layer_forward_seq (rows A9, A10, A11, A12).
+    Returns dX and the list of 7 weight gradients in NAMES order."""
+    Wxg, Wq, Wk, Wv, Wqg, Wkg, Wo = [np.asarray(w, dtype=np.float64) for w in W]
+    dY = np.asarray(dY, dtype=np.float64)
+    d = Wq.shape[0]
+    g = {n: np.zeros((d, d)) for n in ["W_xg", "W_q", "W_k", "W_v", "W_qg", "W_kg", "W_o"]}
+    if cfg.use_out_proj:
+        dO = dY @ Wo.T
+        g["W_o"] = c["O"].T @ dY
+    else:
+        dO = dY
+    dQr, dKr, dV = attention_core_backward(c["Qr"], c["Kr"], c["V"], A, dO, cfg.n_heads)
+    if cfg.use_rope:
+        dQt, dKt = rope_heads(dQr, t_ms, cfg, -1.0), rope_heads(dKr, t_ms, cfg, -1.0)
+    else:
+        dQt, dKt = dQr, dKr
+    if cfg.use_int_gate:
+        uq = dQt * c["Q"] * c["Gq"] * (1.0 - c["Gq"])
+        uk = dKt * c["K"] * c["Gk"] * (1.0 - c["Gk"])
+        dQ = dQt * c["Gq"] + uq @ Wqg.T
+        dK = dKt * c["Gk"] + uk @ Wkg.T
+        g["W_qg"] = c["Q"].T @ uq
+        g["W_kg"] = c["K"].T @ uk
+    else:
+        dQ, dK = dQt, dKt
+    Xt = c["Xt"]
+    g["W_q"], g["W_k"], g["W_v"] = Xt.T @ dQ, Xt.T @ dK, Xt.T @ dV
+    dXt = dQ @ Wq.T + dK @ Wk.T + dV @ Wv.T
+    if cfg.use_rep_gate:
+        ux = dXt * c["X"] * c["Gx"] * (1.0 - c["Gx"])
+        dX = dXt * c["Gx"] + ux @ Wxg.T
+        g["W_xg"] = c["X"].T @ ux
+    else:
+        dX = dXt
+    inter = dict(dO=dO, dQr=dQr, dKr=dKr, dV=dV, dQt=dQt, dKt=dKt, dQ=dQ, dK=dK, dXt=dXt)
+    return dX, [g[n] for n in ["W_xg", "W_q", "W_k", "W_v", "W_qg", "W_kg", "W_o"]], inter
+
+
+# ------------------------------------------------------------------ packed batch drivers
+@dataclass
+class SeqMeta:
+    cu: np.ndarray             # [n+1] offsets into the packed buffer
+    t_ms: np.ndarray           # [T] int64
+    n_cand: np.ndarray         # [n]
+    session_ids: np.ndarray = None
+    n_static: np.ndarray = None
+    pair_flags: np.ndarray = None
+
+
+def seq_mask(meta: SeqMeta, s: int, cfg: AttnConfig) -> np.ndarray:
+    a, e = int(meta.cu[s]), int(meta.cu[s + 1])
+    return mask_dense(meta.t_ms[a:e], int(meta.n_cand[s]), cfg,
+                      None if meta.session_ids is None else meta.session_ids[a:e],
+                      0 if meta.n_static is None else int(meta.n_static[s]),
+                      None if meta.pair_flags is None else meta.pair_flags[a:e])
+
+
+def mask_artifacts(meta: SeqMeta, cfg: AttnConfig, T: int, tile: int = 128):
+    """Bit-exact targets: global kv_end [T], concatenated tile classes, pair count.
+
+    kv_end comes from the mask without the PAIR_PREV exception; the full mask
+    is asserted to equal prefix U {i} U {i-1 if flagged}."""
+    import dataclasses
+    cfg_nopp = dataclasses.replace(cfg, mask_flags=cfg.mask_flags & ~MASK_PAIR_PREV)
+    kv_end = np.arange(T, dtype=np.int64)          # pad rows: kv_end = i
+    tiles = []
+    pairs = 0
+    for s in range(len(meta.cu) - 1):
+        a, e = int(meta.cu[s]), int(meta.cu[s + 1])
+        A = seq_mask(meta, s, cfg)
+        e_loc = kv_end_local(seq_mask(meta, s, cfg_nopp))
+        m = e - a
+        L = m - int(meta.n_cand[s])
+        # structural assertion: A == prefix U diag U pair
+        R = np.arange(m)[None, :] < e_loc[:, None]
+        R |= np.eye(m, dtype=bool)
+        if (cfg.mask_flags & MASK_PAIR_PREV) and meta.pair_flags is not None:
+            pf = np.asarray(meta.pair_flags[a:e]).astype(bool)
+            for i in range(1, min(m, L)):
+                if pf[i]:
+                    R[i, i - 1] = True
+        assert (R == A).all(), "mask is not prefix U diag U pair"
+        kv_end[a:e] = a + e_loc
+        tiles.append(tile_classes(A, tile).reshape(-1))
+        pairs += int(A.sum())
+    tiles = np.concatenate(tiles) if tiles else np.zeros(0, np.int8)
+    return kv_end, tiles, pairs
+
+
+def batch_forward(X, W, meta: SeqMeta, cfg: AttnConfig):
+    """Unpacked per-sequence forward over a packed buffer; pad rows give 0 (R17)."""
+    T, d = X.shape
+    Y = np.zeros((T, d))
+    caches = []
+    lse = np.zeros((cfg.n_heads, T))
+    for s in range(len(meta.cu) - 1):
+        a, e = int(meta.cu[s]), int(meta.cu[s + 1])
+        A = seq_mask(meta, s, cfg)
+        Ys, c = layer_forward_seq(X[a:e], W, meta.t_ms[a:e], A, cfg)
+        Y[a:e] = Ys
+        lse[:, a:e] = c["lse"]
+        caches.append((a, e, A, c))
+    return Y, caches, lse
+
+
+def batch_backward(caches, W, meta: SeqMeta, dY, cfg: AttnConfig):
+    T, d = dY.shape
+    dX = np.zeros((T, d))
+    gs = [np.zeros((d, d)) for _ in range(7)]
+    inters = []
+    for (a, e, A, c) in caches:
+        dXs, g, inter = layer_backward_seq(c, W, meta.t_ms[a:e], A, dY[a:e], cfg)
+        dX[a:e] = dXs
+        for k in range(7):
+            gs[k] += g[k]
+        inters.append((a, e, inter))
+    return dX, gs, inters
+
+
+def packed_forward_blockdiag(X, W, meta: SeqMeta, cfg: AttnConfig, T: int):
+    """The SAME layer over the whole packed buffer with one T x T block-diagonal mask
+    (check 2: packed == unpacked).  Pad rows see only themselves."""
+    A = np.zeros((T, T), dtype=bool)
+    for s in range(len(meta.cu) - 1):
+        a, e = int(meta.cu[s]), int(meta.cu[s + 1])
+        A[a:e, a:e] = seq_mask(meta, s, cfg)
+    n_real = int(meta.cu[-1])
+    for i in range(n_real, T):
+        A[i, i] = True
+    Y, c = layer_forward_seq(X, W, meta.t_ms, A, cfg)
+    Y[n_real:] = 0.0
+    return Y
+
+
+# ------------------------------------------------------------------ heads (Eqs. 8-9)
+def heads_forward(H, rows, W1, b1, w2, b2):
+    """z_k = w2_k . ReLU(H_r W1_k + b1_k) + b2_k for all k in one pass (R14)."""
+    Hr = np.asarray(H, dtype=np.float64)[rows]
+    K = W1.shape[0]
+    pre = np.stack([Hr @ W1[k] + b1[k] for k in range(K)])          # [K, n, dh]
+    hid = np.maximum(pre, 0.0)
+    z = np.stack([hid[k] @ w2[k] + b2[k] for k in range(K)], axis=1)  # [n, K]
+    return z, pre, hid
+
+
+def heads_loss(z, bucket, label):
+    """L_ctx = sum_t CE(y_hat_{k_t}, y_t) with logits (Eq. 9; R15 sum)."""
+    zk = z[np.arange(z.shape[0]), bucket]
+    return float(np.sum(softplus(zk) - label * zk))
+
+
+def heads_loss_backward(H, rows, W1, b1, w2, b2, bucket, label):
+    """Routed BCE adjoint: dz_{k_t} = sigma(z_{k_t}) - y_t, 0 for other heads."""
+    z, pre, hid = heads_forward(H, rows, W1, b1, w2, b2)
+    n, K = z.shape
+    dz = np.zeros_like(z)
+    dz[np.arange(n), bucket] = sigmoid(z[np.arange(n), bucket]) - label
+    Hr = np.asarray(H, dtype=np.float64)[rows]
+    dW1 = np.zeros_like(W1, dtype=np.float64)
+    db1 = np.zeros_like(b1, dtype=np.float64)
+    dw2 = np.zeros_like(w2, dtype=np.float64)
+    db2 = dz.sum(axis=0)
+    dHr = np.zeros_like(Hr)
+    for k in range(K):
+        dhid = dz[:, k:k + 1] * w2[k][None, :] * (pre[k] > 0)
+        dW1[k] = Hr.T @ dhid
+        db1[k] = dhid.sum(axis=0)
+        dw2[k] = hid[k].T @ dz[:, k]
+        dHr += dhid @ np.asarray(W1[k], dtype=np.float64).T
+    dH = np.zeros_like(np.asarray(H, dtype=np.float64))
+    np.add.at(dH, rows, dHr)
+    return heads_loss(z, bucket, label), z, dH, dict(dW1=dW1, db1=db1, dw2=dw2, db2=db2)
+
+
+# ------------------------------------------------------------------ per-element loop (check 1)
+def layer_forward_loop(X, W, t_ms, n_cand, cfg: AttnConfig, session_ids=None):
+    """Independent evaluation for tiny inputs: pure-Python loops over (i, j) with
+    the mask predicate evaluated per pair (no dense mask, no matmul for attention)."""
+    X = np.asarray(X, dtype=np.float64)
+    Wxg, Wq, Wk, Wv, Wqg, Wkg, Wo = [np.asarray(w, dtype=np.float64) for w in W]
+    m, d = X.shape
+    H, hd = cfg.n_heads, cfg.head_dim
+    L = m - n_cand
+
+    def sig(v):
+        return 1.0 / (1.0 + math.exp(-v))
+
+    def allowed(i, j):
+        if i == j:
+            return True
+        if i < L:
+            ok = j < i
+            if cfg.mask_flags & MASK_TIME:
+                ok = ok and t_ms[j] <= t_ms[i] - cfg.delta_delay_ms
+            if cfg.mask_flags & MASK_SESSION:
+                ok = ok and session_ids[j] < session_ids[i]
+            return ok
+        return j < L and t_ms[j] <= t_ms[i] - cfg.delta_cand_ms
+
+    def vecmat(v, Wm):
+        return [sum(v[a] * Wm[a][b] for a in range(d)) for b in range(d)]
+
+    Xt, Qr, Kr, Vv = [], [], [], []
+    for i in range(m):
+        x = list(X[i])
+        if cfg.use_rep_gate:
+            z = vecmat(x, Wxg)
+            x = [x[a] * sig(z[a]) for a in range(d)]
+        q, k, v = vecmat(x, Wq), vecmat(x, Wk), vecmat(x, Wv)
+        if cfg.use_int_gate:
+            zq, zk = vecmat(q, Wqg), vecmat(k, Wkg)
+            q = [q[a] * sig(zq[a]) for a in range(d)]
+            k = [k[a] * sig(zk[a]) for a in range(d)]
+        if cfg.use_rope:
+            for h in range(H):
+                for p in range(hd // 2):
+                    th = (cfg.rope_phi_min / cfg.rope_dt_max_ms) * cfg.rope_base ** (2.0 * p / hd)
+                    al = float(t_ms[i]) * th
+                    for vec in (q, k):
+                        a0, a1 = vec[h * hd + 2 * p], vec[h * hd + 2 * p + 1]
+                        vec[h * hd + 2 * p] = a0 * math.cos(al) - a1 * math.sin(al)
+                        vec[h * hd + 2 * p + 1] = a0 * math.sin(al) + a1 * math.cos(al)
+        Qr.append(q); Kr.append(k); Vv.append(v)
+    Y = np.zeros((m, d))
+    for i in range(m):
+        o = [0.0] * d
+        for h in range(H):
+            js = [j for j in range(m) if allowed(i, j)]
+            sc = [sum(Qr[i][h * hd + a] * Kr[j][h * hd + a] for a in range(hd)) / math.sqrt(hd) for j in js]
+            mx = max(sc)
+            ex = [math.exp(s - mx) for s in sc]
+            Z = sum(ex)
+            for w, j in zip(ex, js):
+                for a in range(hd):
+                    o[h * hd + a] += (w / Z) * Vv[j][h * hd + a]
+        Y[i] = vecmat(o, Wo) if cfg.use_out_proj else o
+    return Y
