@@ -1,0 +1,235 @@
+/* cadet.h — C ABI of libcadet: the CADET (arXiv 2602.11410) data-parallel hot path on B200.
+ *
+ * The hot path is the packed (jagged) self-attention layer over user interaction
+ * sequences with timestamp RoPE, the session/delay + candidate mask, the
+ * representation- and interaction-level sigmoid self-gates, and the
+ * context-conditioned multi-tower heads.
+ * Citations: P:n = /root/reference/PAPER.md line n, S:n = SPEC.md line n.
+ *
+ * CONVENTIONS (apply to every call)
+ *  - Every pointer is a DEVICE pointer unless its name ends in _h (host).
+ *  - Every call enqueues work on `stream` and returns without synchronising; no call
+ *    allocates device memory.  The caller owns all buffers; scratch is passed as
+ *    `ws` (workspace) sized by the *_bytes queries, 256-byte aligned.
+ *  - Matrices are row-major.  Projections are row-vector: y = x . W with
+ *    W[d_in][d_out].  bf16 tensors are passed as void* (uint16 storage).
+ *  - Packed batch (Fig. 4): tokens of n sequences back to back in a buffer of
+ *    exactly T rows; sequence s owns rows [cu_seqlens[s], cu_seqlens[s+1]); rows
+ *    [cu_seqlens[n], T) are padding.  Pad rows produce 0 outputs and 0 gradients and
+ *    never attend or get attended.
+ *  - Return codes only; no exceptions cross the ABI.  cadet_last_error() returns a
+ *    thread-local message for the last non-OK status.  Host-detected errors (null
+ *    pointers, unsupported shapes, small workspace) return synchronously.
+ *    Device-detected input errors (offsets, ordering, n_candidates, bucket range,
+ *    NaN/Inf) are latched into the workspace error word and returned by the next
+ *    cadet_poll(ws); kernels stay memory-safe on invalid input (indices clamped,
+ *    invalid sequences skipped) and results are unspecified until cadet_poll
+ *    returns CADET_OK.
+ *  - Stateless and reentrant: concurrent calls on different streams with different
+ *    workspaces are allowed.
+ */
+#ifndef CADET_H
+#define CADET_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CADET_ABI_VERSION 1
+
+typedef struct CUstream_st* cadet_stream_t; /* == cudaStream_t; NULL = legacy default stream */
+
+typedef enum {
+  CADET_OK = 0,
+  CADET_E_ARG = 1,         /* null pointer / bad shape: d % H, odd head_dim, head_dim > 128, d % 32 ("dimension error") */
+  CADET_E_OFFSETS = 2,     /* cu_seqlens[0] != 0, empty or decreasing sequence, cu[n] > T          (device) */
+  CADET_E_ORDER = 3,       /* timestamps or session ids decrease inside a sequence ("ordering error") (device) */
+  CADET_E_TOO_LONG = 4,    /* a sequence longer than max_seqlen or the budget: chunk first          (device) */
+  CADET_E_CAND = 5,        /* n_candidates[s] > length of s                                                (device) */
+  CADET_E_BUCKET = 6,      /* bucket outside [0, K) ("routing error")                                (device) */
+  CADET_E_NONFINITE = 7,   /* NaN/Inf in a loss (fail-fast numerics)                                  (device) */
+  CADET_E_WORKSPACE = 8,   /* workspace / capacity too small                                                         */
+  CADET_E_UNSUPPORTED = 9, /* valid but not implemented in this build (e.g. dtype FP32)                               */
+  CADET_E_CUDA = 10        /* a CUDA runtime error; see cadet_last_error()                                          */
+} cadet_status;
+
+enum { CADET_BF16 = 0, CADET_FP32 = 1 };
+
+/* Mask rule bits (Fig. 3). */
+enum {
+  CADET_MASK_TIME = 1,     /* context query i sees j < i only if t_j <= t_i - delta_delay_ms (Eq. 6; tie allowed) */
+  CADET_MASK_SESSION = 2,  /* context query i sees j < i only if session_id_j < session_id_i (opt-in reading R10)  */
+  CADET_MASK_PAIR_PREV = 4 /* context query i also sees i-1 when token_flags[i] & 1 (SPEC S:310 exception, R12)     */
+};
+/* Always: the diagonal is visible (Fig. 3 "preserved diagonal", R8); candidate queries (the last
+ * n_candidates[s] rows of s) see context keys j with t_j <= t_i - delta_cand_ms and themselves only
+ * (P:285); j < n_static[s] is visible to every context query (R13). */
+
+typedef struct {
+  int32_t d_model;   /* d, multiple of 32 */
+  int32_t n_heads;   /* H; head_dim = d / H must be in {32, 64, 88, 96, 128} (even, <= 128) */
+  int32_t head_dim;  /* must equal d_model / n_heads */
+  int32_t dtype;     /* CADET_BF16 (bf16 operands, fp32 accumulation); CADET_FP32 -> CADET_E_UNSUPPORTED in v1 */
+  int32_t mask_flags;
+  int32_t out_f32;   /* core calls: 1 = write O / dQr / dKr / dV as fp32 (parity protocol, SURVEY 8(c) iii) */
+  int32_t use_rope, use_rep_gate, use_int_gate, use_out_proj; /* ablation switches (Table 1) */
+  int32_t deterministic; /* reserved, must be 0 (dQ uses fp32 atomics) */
+  int32_t reserved0;
+  int64_t delta_delay_ms;       /* Delta for context queries, Eq. 6; default 3,600,000 */
+  int64_t delta_cand_ms;        /* Delta for candidate queries; default 0 (R11) */
+  int64_t rope_delta_t_max_ms;  /* Delta t_max; default 31,536,000,000 = 1 year (R6) */
+  double rope_phi_min;          /* default 1e-4 */
+  double rope_base;             /* default 600000 */
+} cadet_attn_config;
+
+typedef struct {
+  int32_t n_seqs;       /* n (host scalar) */
+  int32_t total_tokens; /* T = budget rows of every [T, ...] buffer (host scalar) */
+  int32_t max_seqlen;   /* upper bound on any sequence length (host scalar) */
+  int32_t reserved0;
+  const int32_t* cu_seqlens;    /* [n+1] */
+  const int64_t* timestamps_ms; /* [T] Unix ms; non-decreasing within a sequence */
+  const int32_t* session_ids;   /* [T] or NULL (required with CADET_MASK_SESSION); non-decreasing within a sequence */
+  const int32_t* n_candidates;  /* [n] or NULL: the last n_candidates[s] tokens of s are candidates */
+  const int32_t* n_static;      /* [n] or NULL: always-visible static prefix length (R13) */
+  const uint8_t* token_flags;   /* [T] or NULL: bit0 = may see token i-1 under CADET_MASK_PAIR_PREV */
+} cadet_batch;
+
+/* Seven [d, d] bf16 matrices (Eqs. 3-5): rep gate, Q, K, V, Q gate, K gate, output. */
+typedef struct {
+  const void *W_xg, *W_q, *W_k, *W_v, *W_qg, *W_kg, *W_o;
+} cadet_attn_weights;
+/* fp32 [d, d] gradients, OVERWRITTEN (not accumulated) by cadet_attn_backward. */
+typedef struct {
+  float *dW_xg, *dW_q, *dW_k, *dW_v, *dW_qg, *dW_kg, *dW_o;
+} cadet_attn_grads;
+
+/* Context-conditioned towers (Eq. 8; R14): z_k = w2_k . ReLU(h W1_k + b1_k) + b2_k.
+ * W1 is stored as ONE [d, K*dh] bf16 matrix whose columns [k*dh, (k+1)*dh) are tower k. */
+typedef struct {
+  int32_t K;        /* towers (K = 2 at P:624) */
+  int32_t d_model;
+  int32_t d_hidden; /* dh, multiple of 32 (default d/2) */
+  int32_t dtype;    /* CADET_BF16 */
+} cadet_head_config;
+typedef struct {
+  const void* W1;   /* bf16 [d, K*dh] */
+  const float* b1;  /* [K*dh] */
+  const float* w2;  /* [K*dh] */
+  const float* b2;  /* [K] */
+} cadet_head_weights;
+typedef struct {
+  float *dW1 /*[d, K*dh]*/, *db1 /*[K*dh]*/, *dw2 /*[K*dh]*/, *db2 /*[K]*/; /* overwritten */
+} cadet_head_grads;
+
+/* ------------------------------------------------------------------ queries */
+int32_t cadet_abi_version(void);
+const char* cadet_last_error(void);
+const char* cadet_status_string(cadet_status s);
+void cadet_default_attn_config(cadet_attn_config* cfg_h, int32_t d_model, int32_t n_heads);
+void cadet_tile_shape(int32_t* bm_h, int32_t* bn_h); /* 128, 128: the tile of cadet_mask_export's tile classes */
+
+/* Workspace for cadet_mask_plan / the core calls (plan + error word), and for the full layer
+ * (plan + backward temporaries).  `saved` holds the forward activations needed by the backward:
+ * Zx, X~, Q, K, Zq, Zk, Qr, Kr, V, O (bf16 [T, d] each) and LSE (fp32 [H, T]). */
+size_t cadet_plan_workspace_bytes(int32_t n_seqs, int32_t total_tokens);
+size_t cadet_attn_workspace_bytes(const cadet_attn_config* cfg_h, int32_t n_seqs, int32_t total_tokens);
+size_t cadet_attn_saved_bytes(const cadet_attn_config* cfg_h, int32_t total_tokens);
+size_t cadet_heads_workspace_bytes(const cadet_head_config* h_h, int32_t n_rows);
+
+/* ------------------------------------------------------------------ A1: mask plan
+ * Validates the batch and builds, in ws: per row kv_end[i] (exclusive end of the visible
+ * off-diagonal prefix, global index), the row -> sequence map, per 128-row tile the visit
+ * bounds, and the cost-ordered (LPT) tile work lists.  The mask is never materialised. */
+cadet_status cadet_mask_plan(const cadet_attn_config* cfg_h, const cadet_batch* b_h, void* ws, size_t ws_bytes,
+                             cadet_stream_t stream);
+/* Test hook (bit-exact targets): kv_end [T] int32 (global; pad rows hold kv_end = i); tile_class int8,
+ * per sequence a row-major nq_s x nq_s block (nq_s = ceil(len_s/128), tiles anchored at the sequence
+ * start), blocks concatenated in sequence order, 0 = SKIP 1 = PARTIAL 2 = FULL; n_pairs [1] int64 =
+ * number of allowed (i, j) cells (head-independent).  tile_class_cap = capacity in entries
+ * (>= sum nq_s^2; excess entries are not written).  Requires a prior cadet_mask_plan on ws. */
+cadet_status cadet_mask_export(const cadet_attn_config* cfg_h, const cadet_batch* b_h, const void* ws,
+                               int32_t* kv_end, int8_t* tile_class, int64_t tile_class_cap, int64_t* n_pairs,
+                               cadet_stream_t stream);
+
+/* ------------------------------------------------------------------ A5 / A10: attention core (Eq. 7)
+ * Qr, Kr, V: bf16 [T, H*hd] (= [T, H, hd]); Qr/Kr already gated and rotated.
+ * O: [T, H*hd] bf16 (fp32 if cfg.out_f32); lse: fp32 [H, T] = ln sum_{j visible} exp(Qr_i.Kr_j / sqrt(hd)).
+ * Runs cadet_mask_plan internally. */
+cadet_status cadet_attn_core_forward(const cadet_attn_config* cfg_h, const cadet_batch* b_h, const void* Qr,
+                                     const void* Kr, const void* V, void* O, float* lse, void* ws, size_t ws_bytes,
+                                     cadet_stream_t stream);
+/* dO: bf16 [T, H*hd]; O must be the bf16 output of the forward.  Outputs: dQr fp32 [T, H*hd]
+ * (always fp32: atomically accumulated), dKr and dV [T, H*hd] bf16 (fp32 if cfg.out_f32). */
+cadet_status cadet_attn_core_backward(const cadet_attn_config* cfg_h, const cadet_batch* b_h, const void* Qr,
+                                      const void* Kr, const void* V, const void* O, const float* lse, const void* dO,
+                                      float* dQr, void* dKr, void* dV, void* ws, size_t ws_bytes,
+                                      cadet_stream_t stream);
+
+/* ------------------------------------------------------------------ A2-A6: full gated layer forward
+ * X: bf16 [T, d].  Y: bf16 [T, d] = O . W_o (+ resid if resid != NULL, bf16 [T, d]).
+ * saved: cadet_attn_saved_bytes; consumed by cadet_attn_backward.  Runs cadet_mask_plan. */
+cadet_status cadet_attn_forward(const cadet_attn_config* cfg_h, const cadet_batch* b_h, const cadet_attn_weights* w_h,
+                                const void* X, void* Y, const void* resid, void* saved, void* ws, size_t ws_bytes,
+                                cadet_stream_t stream);
+/* A9-A12: dY bf16 [T, d] -> dX bf16 [T, d] (+ dresid, bf16 [T, d], if non-NULL: the residual-path
+ * gradient is added, i.e. dX = dresid + dX_attn) and the 7 fp32 weight gradients (overwritten).
+ * ws must be the same workspace as the forward's (the plan is reused) or re-planned. */
+cadet_status cadet_attn_backward(const cadet_attn_config* cfg_h, const cadet_batch* b_h,
+                                 const cadet_attn_weights* w_h, const void* X, const void* saved, const void* dY,
+                                 void* dX, const void* dresid, const cadet_attn_grads* g_h, void* ws, size_t ws_bytes,
+                                 cadet_stream_t stream);
+
+/* ------------------------------------------------------------------ A7 / A8: towers + routed loss (Eqs. 8-9)
+ * Hs: bf16 [T, d] transformer output; rows: int32 [n] packed row index of each scored token
+ * (impression rows in training, candidate rows at serving).  logits: fp32 [n, K].
+ * pre_out (nullable): bf16 [n, K*dh] pre-activations kept for the backward. */
+cadet_status cadet_heads_forward(const cadet_head_config* h_h, const cadet_head_weights* w_h, const void* Hs,
+                                 const int32_t* rows, int32_t n, float* logits, void* pre_out, void* ws,
+                                 size_t ws_bytes, cadet_stream_t stream);
+/* Routed BCE with logits, summed (Eq. 9, R15): loss = sum_t softplus(z_{k_t}) - y_t z_{k_t};
+ * dz_{k_t} = sigma(z_{k_t}) - y_t, other towers 0.  bucket int32 [n] in [0, K) (else
+ * CADET_E_BUCKET via cadet_poll), label fp32 [n].  Writes loss_sum[1], dHs (bf16 [T, d], rows not
+ * in `rows` set to 0) and the head gradients.  pre must be the forward's pre_out. */
+cadet_status cadet_heads_loss_backward(const cadet_head_config* h_h, const cadet_head_weights* w_h, const void* Hs,
+                                       const int32_t* rows, int32_t n, int32_t T, const float* logits,
+                                       const void* pre, const int32_t* bucket, const float* label, float* loss_sum,
+                                       void* dHs, const cadet_head_grads* g_h, void* ws, size_t ws_bytes,
+                                       cadet_stream_t stream);
+
+/* ------------------------------------------------------------------ A0 / A13: chunk and pack
+ * Chunk: split each sequence [a, e) of cu_in at e - L, e - 2L, ... (newest chunk full, oldest may be
+ * short) and write the refined offsets in buffer order to cu_out (capacity cap entries);
+ * n_out[0] (device) = number of chunks.  Chunks stay contiguous: no data moves. */
+cadet_status cadet_chunk(const int32_t* cu_in, int32_t n_in, int32_t L_chunk, int32_t* cu_out, int32_t cap,
+                         int32_t* n_out, void* ws, cadet_stream_t stream); /* ws >= 256 B: error word (cadet_poll) */
+/* Pack: greedy arrival-order packing of padded sequences into one fixed budget:
+ * sequences 0..k-1 are copied while their running total fits `budget`; rows [total, budget) are
+ * zero-filled.  padded: bf16 [B, Lmax, d]; lens: int32 [B]; t_padded (nullable) int64 [B, Lmax] and
+ * s_padded (nullable) int32 [B, Lmax] are packed alongside into t_out / s_out ([budget]).
+ * Outputs: packed [budget, d], cu_out [B+1] (entries past n_packed repeat the total), n_packed[0].
+ * ws (>= cadet_pack_workspace_bytes) holds the error word read by cadet_poll. */
+cadet_status cadet_pack(const void* padded, const int32_t* lens, int32_t B, int32_t Lmax, int32_t d, int32_t budget,
+                        const int64_t* t_padded, const int32_t* s_padded, void* packed, int64_t* t_out,
+                        int32_t* s_out, int32_t* cu_out, int32_t* n_packed, void* ws, size_t ws_bytes,
+                        cadet_stream_t stream);
+size_t cadet_pack_workspace_bytes(int32_t B);
+
+/* ------------------------------------------------------------------ stage hook (tests / building block)
+ * C[M, N] = A . B (+ resid) with the tcgen05 GEMM.  A: bf16, storage [M, K] (a_mn = 0) or [K, M]
+ * (a_mn = 1); B: bf16, storage [N, K] (b_mn = 0) or [K, N] (b_mn = 1).  C fp32 (c_f32 = 1) or bf16,
+ * [M, N]; resid (nullable) same dtype as C.  N % 32 == 0, K % 8 == 0, M % 8 == 0 when MN-major. */
+cadet_status cadet_gemm(int32_t M, int32_t N, int32_t K, const void* A, int32_t a_mn, const void* B, int32_t b_mn,
+                        void* C, int32_t c_f32, const void* resid, cadet_stream_t stream);
+
+/* ------------------------------------------------------------------ errors
+ * Synchronises `stream`, then returns and clears the device-latched error word in ws. */
+cadet_status cadet_poll(void* ws, cadet_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CADET_H */

@@ -1,0 +1,64 @@
+// Shared geometry of the attention kernels (rows A5 / A10).
+#pragma once
+#include "plan.cuh"
+#include "ptx.cuh"
+#include "tma_host.cuh"
+
+namespace cadet {
+
+// Head-dim tiling: a [128 x HDP] operand tile is held as NB column blocks of CB bf16 columns,
+// each block a [128 rows x RB bytes] TMA box with RB-byte swizzle (RB = 128 when hd % 64 == 0,
+// else 64).  hd = 88 runs as HDP = 96: TMA zero-fills columns 88..95 of the 3-D [T][H][hd] map.
+template <int HD>
+struct HeadGeom {
+  static constexpr int HDP = (HD + 31) / 32 * 32;
+  static constexpr int RB = (HDP % 64 == 0) ? 128 : 64;  // row bytes per block = swizzle width
+  static constexpr int CB = RB / 2;                       // bf16 columns per block
+  static constexpr int NB = HDP / CB;
+  static constexpr int BLK = 128 * RB;                    // bytes per block
+  static constexpr int TILE_BYTES = NB * BLK;
+  static constexpr uint32_t SWZ = (RB == 128) ? SWZ_128B : SWZ_64B;
+};
+
+// K-major operand (rows x HDP) descriptor for k-step kk (16 columns).
+template <int HD>
+CADET_DEV uint64_t kmajor_desc(uint32_t base, int kk) {
+  using G = HeadGeom<HD>;
+  const int col = kk * 16;
+  const uint32_t addr = base + (col / G::CB) * G::BLK + (col % G::CB) * 2;
+  return smem_desc(addr, 16, 8 * G::RB, G::SWZ);
+}
+// MN-major operand: storage rows = K dimension (16 rows per k-step), columns = N (HDP).
+template <int HD>
+CADET_DEV uint64_t mnmajor_desc(uint32_t base, int kk) {
+  using G = HeadGeom<HD>;
+  return smem_desc(base + kk * 16 * G::RB, G::BLK, 8 * G::RB, G::SWZ);
+}
+
+// 128 x 128 bf16 tile written by threads (P, P^T, dS^T): 2 blocks of 64 columns, 128B swizzle.
+CADET_DEV uint32_t p_off(int row, int col) {  // byte offset of the 8-column chunk holding col
+  return (col >> 6) * 16384 + swz_off(row, (col & 63) >> 3, 128);
+}
+CADET_DEV uint64_t p_kmajor_desc(uint32_t base, int kk) {  // A operand, K = columns
+  return smem_desc(base + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024, SWZ_128B);
+}
+CADET_DEV uint64_t p_mnmajor_desc(uint32_t base, int kk) {  // A operand MN-major: M = columns, K = rows
+  return smem_desc(base + kk * 16 * 128, 16384, 1024, SWZ_128B);
+}
+
+struct AttnParams {
+  int32_t T, H, hd, d, n;
+  float scale_log2;  // log2(e) / sqrt(hd)
+  float scale;       // 1 / sqrt(hd)
+  int32_t out_f32;
+  const int32_t* cu;
+  PlanView plan;
+  void* O;           // fwd: O out;  bwd: (unused)
+  float* lse;        // fwd out / bwd in  [H, T]
+  const float* D;    // bwd: rowsum(dO * O) [H, T]
+  float* dQ;         // bwd: fp32 accumulator [T, d]
+  void* dK;          // bwd out
+  void* dV;          // bwd out
+};
+
+}  // namespace cadet

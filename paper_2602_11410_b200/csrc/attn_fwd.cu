@@ -1,0 +1,327 @@
+// A5: packed, session-masked attention forward (Eq. 7).
+//
+// One CTA per (128-row q-tile of one sequence, head), q-tiles taken in descending cost order
+// (LPT work list from the plan).  Only the visible k-tiles are visited: the front prefix
+// [0, nf) and the diagonal band [kt2, qt] ("skips compute_qk entirely for tiles
+// that are fully masked").  Per row, the mask predicate runs only when the row's visible
+// prefix does not cover the whole k-tile (PARTIAL rows); FULL rows skip it.
+//
+//   warp 0     : TMA producer: Q once, K/V tiles through a 2-stage ring (3-D [T][H][hd] maps)
+//   warp 1     : TMEM owner + tcgen05.mma issuer: S_j = Q K_j^T (TMEM, double-buffered),
+//                O += P_j V_j (TMEM accumulator, P_j from shared memory)
+//   warps 2..5 : softmax, thread = query row: tcgen05.ld S, mask, online softmax with
+//                conditional rescaling (threshold 2^8), P -> smem (bf16), O rescale in TMEM,
+//                final O / l and LSE.
+#include "attn_common.cuh"
+
+namespace cadet {
+
+template <int HD>
+struct FwdCfg {
+  using G = HeadGeom<HD>;
+  static constexpr int Q_OFF = 0;
+  static constexpr int K_OFF = Q_OFF + G::TILE_BYTES;
+  static constexpr int V_OFF = K_OFF + 2 * G::TILE_BYTES;
+  static constexpr int P_OFF = V_OFF + 2 * G::TILE_BYTES;
+  static constexpr int BAR_OFF = P_OFF + 32768;
+  static constexpr int USED = BAR_OFF + 256;
+  // >= 116 KB so that exactly one CTA (which owns all 512 TMEM columns) is resident per SM
+  static constexpr int SMEM = (USED + 1024 > 118784 ? USED + 1024 : 118784);
+  static constexpr int S_COL = 0;    // two 128-column S buffers
+  static constexpr int O_COL = 256;  // HDP columns
+};
+
+struct FwdBars {
+  uint64_t q_full, k_full[2], k_empty[2], v_full[2], v_empty[2], s_full[2], s_free[2], p_full, pv_done;
+  uint32_t tmem_base;
+};
+
+__device__ __forceinline__ int visit_tile(const QTileInfo& qi, int j) { return j < qi.nf ? j : qi.kt2 + (j - qi.nf); }
+
+template <int HD>
+__global__ void __launch_bounds__(192, 1)
+    attn_fwd_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constant__ CUtensorMap mK,
+                    const __grid_constant__ CUtensorMap mV, const AttnParams p) {
+  using G = HeadGeom<HD>;
+  using C = FwdCfg<HD>;
+  const int nq_total = p.plan.counters[0];
+  const int b = blockIdx.x / p.H;
+  const int h = blockIdx.x % p.H;
+  if (b >= nq_total) return;
+  const QTileInfo qi = p.plan.qinfo[p.plan.fwd_order[b]];
+  const int sa = p.cu[qi.seq], se = p.cu[qi.seq + 1];
+  const int q0 = sa + qi.qt * 128;
+  const int rows_valid = min(128, se - q0);
+  const int n_kv = qi.nf + (qi.qt + 1 - qi.kt2);
+
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  FwdBars* bars = reinterpret_cast<FwdBars*>(smem + C::BAR_OFF);
+  const uint32_t warp = warp_id(), lane = lane_id();
+
+  if (threadIdx.x == 0) {
+    mbar_init(&bars->q_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&bars->k_full[i], 1);
+      mbar_init(&bars->k_empty[i], 1);
+      mbar_init(&bars->v_full[i], 1);
+      mbar_init(&bars->v_empty[i], 1);
+      mbar_init(&bars->s_full[i], 1);
+      mbar_init(&bars->s_free[i], 128);
+    }
+    mbar_init(&bars->p_full, 128);
+    mbar_init(&bars->pv_done, 1);
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc<512>(&bars->tmem_base);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = bars->tmem_base;
+
+  if (warp == 0) {
+    // ============================ producer
+    if (elect_one()) {
+      tma_prefetch(&mQ);
+      tma_prefetch(&mK);
+      tma_prefetch(&mV);
+      mbar_expect_tx(&bars->q_full, G::TILE_BYTES);
+#pragma unroll
+      for (int blk = 0; blk < G::NB; ++blk)
+        tma_load_3d(smem + C::Q_OFF + blk * G::BLK, &mQ, &bars->q_full, blk * G::CB, h, q0);
+      for (int j = 0; j < n_kv; ++j) {
+        const int st = j & 1, use = j >> 1;
+        const int krow = sa + visit_tile(qi, j) * 128;
+        if (use > 0) mbar_wait(&bars->k_empty[st], (use - 1) & 1);
+        mbar_expect_tx(&bars->k_full[st], G::TILE_BYTES);
+#pragma unroll
+        for (int blk = 0; blk < G::NB; ++blk)
+          tma_load_3d(smem + C::K_OFF + st * G::TILE_BYTES + blk * G::BLK, &mK, &bars->k_full[st], blk * G::CB, h,
+                      krow);
+        if (use > 0) mbar_wait(&bars->v_empty[st], (use - 1) & 1);
+        mbar_expect_tx(&bars->v_full[st], G::TILE_BYTES);
+#pragma unroll
+        for (int blk = 0; blk < G::NB; ++blk)
+          tma_load_3d(smem + C::V_OFF + st * G::TILE_BYTES + blk * G::BLK, &mV, &bars->v_full[st], blk * G::CB, h,
+                      krow);
+      }
+    }
+  } else if (warp == 1) {
+    // ============================ MMA issuer
+    if (elect_one()) {
+      const uint32_t idesc_s = idesc_bf16(128, 128, 0, 0);
+      const uint32_t idesc_o = idesc_bf16(128, G::HDP, 0, 1);
+      const uint32_t sQ = smem_u32(smem + C::Q_OFF);
+      const uint32_t sP = smem_u32(smem + C::P_OFF);
+      mbar_wait(&bars->q_full, 0);
+      auto issue_s = [&](int j) {
+        const int st = j & 1, use = j >> 1;
+        if (use > 0) mbar_wait(&bars->s_free[st], (use - 1) & 1);
+        mbar_wait(&bars->k_full[st], use & 1);
+        tc_fence_after();
+        const uint32_t sK = smem_u32(smem + C::K_OFF + st * G::TILE_BYTES);
+#pragma unroll
+        for (int kk = 0; kk < G::HDP / 16; ++kk)
+          mma_bf16_ss(tmem + C::S_COL + st * 128, kmajor_desc<HD>(sQ, kk), kmajor_desc<HD>(sK, kk), idesc_s,
+                      kk > 0 ? 1u : 0u);
+        mma_commit(&bars->k_empty[st]);
+        mma_commit(&bars->s_full[st]);
+      };
+      if (n_kv > 0) issue_s(0);
+      for (int j = 0; j < n_kv; ++j) {
+        if (j + 1 < n_kv) issue_s(j + 1);
+        const int st = j & 1;
+        mbar_wait(&bars->p_full, j & 1);
+        mbar_wait(&bars->v_full[st], (j >> 1) & 1);
+        tc_fence_after();
+        const uint32_t sV = smem_u32(smem + C::V_OFF + st * G::TILE_BYTES);
+#pragma unroll
+        for (int kk = 0; kk < 128 / 16; ++kk)
+          mma_bf16_ss(tmem + C::O_COL, p_kmajor_desc(sP, kk), mnmajor_desc<HD>(sV, kk), idesc_o,
+                      (j > 0 || kk > 0) ? 1u : 0u);
+        mma_commit(&bars->v_empty[st]);
+        mma_commit(&bars->pv_done);
+      }
+    }
+  } else {
+    // ============================ softmax warps 2..5
+    const uint32_t quarter = warp & 3;
+    const int rt = quarter * 32 + lane;  // row in tile == TMEM lane
+    const int r = q0 + rt;
+    const bool valid = rt < rows_valid;
+    const int e_r = valid ? p.plan.kv_end[r] : 0;
+    const bool pp = valid ? (p.plan.row_pp[r] != 0) : false;
+    const float sl2 = p.scale_log2;
+    float m_used = -INFINITY;  // scaled (log2) running max actually used as the exp base
+    float l = 0.f;
+    uint8_t* sP = smem + C::P_OFF;
+    for (int j = 0; j < n_kv; ++j) {
+      const int st = j & 1, use = j >> 1;
+      const int k0 = sa + visit_tile(qi, j) * 128;
+      mbar_wait(&bars->s_full[st], use & 1);
+      tc_fence_after();
+      // pass 1: masked row max over the 128 columns (S read from TMEM in 32-column slices)
+      const bool partial = !valid || (e_r < k0 + 128);
+      auto load_masked = [&](int c, float (&x)[32]) {
+        uint32_t u[32];
+        tmem_ld32(tmem_addr(tmem, quarter, C::S_COL + st * 128 + c * 32), u);
+        tmem_ld_wait();
+#pragma unroll
+        for (int q = 0; q < 32; ++q) x[q] = __uint_as_float(u[q]);
+        if (partial) {
+#pragma unroll
+          for (int q = 0; q < 32; ++q) {
+            const int jj = k0 + c * 32 + q;
+            const bool ok = valid && ((jj < e_r) || (jj == r) || (pp && jj == r - 1));
+            if (!ok) x[q] = -INFINITY;
+          }
+        }
+      };
+      float mx = -INFINITY;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        float x[32];
+        load_masked(c, x);
+#pragma unroll
+        for (int q = 0; q < 32; ++q) mx = fmaxf(mx, x[q]);
+      }
+      const float mx_s = mx * sl2;
+      float factor = 1.f;
+      bool rescale = false;
+      if (mx_s > m_used + 8.f) {  // conditional rescale (also the first finite max)
+        factor = (m_used == -INFINITY) ? 0.f : fast_exp2(m_used - mx_s);
+        m_used = mx_s;
+        rescale = true;
+      }
+      // ---- previous PV must be done before touching O or overwriting P
+      if (j > 0) {
+        mbar_wait(&bars->pv_done, (j - 1) & 1);
+        tc_fence_after();
+        if (__any_sync(0xffffffffu, rescale)) {
+          const float f = rescale ? factor : 1.f;
+#pragma unroll
+          for (int c = 0; c < G::HDP / 32; ++c) {
+            uint32_t u[32];
+            const uint32_t ta = tmem_addr(tmem, quarter, C::O_COL + c * 32);
+            tmem_ld32(ta, u);
+            tmem_ld_wait();
+#pragma unroll
+            for (int q = 0; q < 32; ++q) u[q] = __float_as_uint(__uint_as_float(u[q]) * f);
+            tmem_st32(ta, u);
+          }
+          tmem_st_wait();
+        }
+      }
+      // pass 2: P = exp2(s*scale_log2 - m) -> bf16 -> shared memory (128B-swizzled K-major A operand)
+      const float base = (m_used == -INFINITY) ? 0.f : m_used;
+      float rs = 0.f;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        float x[32];
+        load_masked(c, x);
+#pragma unroll
+        for (int ch = 0; ch < 4; ++ch) {
+          uint32_t w[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int q = ch * 8 + e * 2;
+            const float p0 = fast_exp2(fmaf(x[q], sl2, -base));
+            const float p1 = fast_exp2(fmaf(x[q + 1], sl2, -base));
+            rs += p0 + p1;
+            w[e] = pack_bf16(p0, p1);
+          }
+          *reinterpret_cast<uint4*>(sP + p_off(rt, c * 32 + ch * 8)) = make_uint4(w[0], w[1], w[2], w[3]);
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&bars->s_free[st]);
+      l = l * factor + rs;
+      fence_proxy_async_smem();
+      tc_fence_before();
+      mbar_arrive(&bars->p_full);
+    }
+    // ---- epilogue: O / l, LSE
+    if (n_kv > 0) {
+      mbar_wait(&bars->pv_done, (n_kv - 1) & 1);
+      tc_fence_after();
+    }
+    const float inv_l = (l > 0.f) ? 1.f / l : 0.f;
+#pragma unroll
+    for (int c = 0; c < G::HDP / 32; ++c) {
+      uint32_t u[32];
+      tmem_ld32(tmem_addr(tmem, quarter, C::O_COL + c * 32), u);
+      tmem_ld_wait();
+      if (valid) {
+        const size_t off = (size_t)r * p.d + (size_t)h * p.hd + c * 32;
+        const int ncol = min(32, p.hd - c * 32);
+        if (p.out_f32) {
+          float* o = reinterpret_cast<float*>(p.O) + off;
+          for (int q = 0; q < ncol; q += 4)
+            *reinterpret_cast<float4*>(o + q) =
+                make_float4(__uint_as_float(u[q]) * inv_l, __uint_as_float(u[q + 1]) * inv_l,
+                            __uint_as_float(u[q + 2]) * inv_l, __uint_as_float(u[q + 3]) * inv_l);
+        } else {
+          __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(p.O) + off;
+          for (int q = 0; q < ncol; q += 8) {
+            uint4 v;
+            v.x = pack_bf16(__uint_as_float(u[q]) * inv_l, __uint_as_float(u[q + 1]) * inv_l);
+            v.y = pack_bf16(__uint_as_float(u[q + 2]) * inv_l, __uint_as_float(u[q + 3]) * inv_l);
+            v.z = pack_bf16(__uint_as_float(u[q + 4]) * inv_l, __uint_as_float(u[q + 5]) * inv_l);
+            v.w = pack_bf16(__uint_as_float(u[q + 6]) * inv_l, __uint_as_float(u[q + 7]) * inv_l);
+            *reinterpret_cast<uint4*>(o + q) = v;
+          }
+        }
+      }
+    }
+    if (valid) p.lse[(size_t)h * p.T + r] = (l > 0.f) ? (m_used + __log2f(l)) * 0.6931471805599453f : 0.f;
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 1) tmem_dealloc<512>(tmem);
+}
+
+// ---------------------------------------------------------------- host
+bool make_head_map(CUtensorMap* m, const void* ptr, int T, int H, int hd);  // attn_host (below)
+
+bool make_head_map(CUtensorMap* m, const void* ptr, int T, int H, int hd) {
+  const int HDP = (hd + 31) / 32 * 32;
+  const int RB = (HDP % 64 == 0) ? 128 : 64;
+  uint64_t dims[3] = {(uint64_t)hd, (uint64_t)H, (uint64_t)T};
+  uint64_t strides[2] = {(uint64_t)hd * 2, (uint64_t)H * hd * 2};
+  uint32_t box[3] = {(uint32_t)(RB / 2), 1, 128};
+  return encode_bf16_map(m, ptr, 3, dims, strides, box,
+                         RB == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B);
+}
+
+template <int HD>
+static cudaError_t fwd_hd(const CUtensorMap& mQ, const CUtensorMap& mK, const CUtensorMap& mV, const AttnParams& p,
+                          cudaStream_t st) {
+  using C = FwdCfg<HD>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(attn_fwd_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const int grid = p.plan.nq_cap * p.H;
+  if (grid == 0) return cudaSuccess;
+  attn_fwd_kernel<HD><<<grid, 192, C::SMEM, st>>>(mQ, mK, mV, p);
+  return cudaGetLastError();
+}
+
+cudaError_t attn_fwd_launch(const void* Qr, const void* Kr, const void* V, const AttnParams& p, cudaStream_t st) {
+  CUtensorMap mQ, mK, mV;
+  if (!make_head_map(&mQ, Qr, p.T, p.H, p.hd) || !make_head_map(&mK, Kr, p.T, p.H, p.hd) ||
+      !make_head_map(&mV, V, p.T, p.H, p.hd))
+    return cudaErrorInvalidValue;
+  switch ((p.hd + 31) / 32 * 32) {
+    case 32: return fwd_hd<32>(mQ, mK, mV, p, st);
+    case 64: return fwd_hd<64>(mQ, mK, mV, p, st);
+    case 96: return fwd_hd<96>(mQ, mK, mV, p, st);
+    case 128: return fwd_hd<128>(mQ, mK, mV, p, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace cadet

@@ -1,0 +1,438 @@
+// Persistent warp-specialised tcgen05 GEMM (bf16 in, fp32 accumulate in TMEM) with the
+// CADET epilogues fused (rows A2-A4, A6, A7, A9, A11, A12).
+//
+//   warp 0      : TMA producer (one elected lane), 128B-swizzled K- or MN-major tiles
+//   warp 1      : tcgen05.mma issuer (one elected lane), M=128 x N=BN x K=16 per instruction
+//   warp 2      : TMEM allocator (2 x BN fp32 columns: double-buffered accumulator)
+//   warps 4..7  : epilogue, thread = accumulator row (TMEM lane), tcgen05.ld 32 columns at a time
+//
+// C[M,N] = sum_seg A_seg[M,K_seg] . B_seg[K_seg,N], tiles 128 x BN x 64, split-K optional.
+#include "gemm.cuh"
+#include "ptx.cuh"
+#include "tma_host.cuh"
+#include <string.h>
+
+namespace cadet {
+
+constexpr int BM = 128;
+constexpr int BK = 64;
+constexpr int GEMM_THREADS = 256;
+
+struct KProb {
+  int32_t M, N, nseg, kb_total, split_k, m_tiles, n_tiles, unit_begin;
+  int32_t kb[GEMM_MAX_SEG];
+  int32_t a_mn[GEMM_MAX_SEG], b_mn[GEMM_MAX_SEG];
+  EpiParams epi;
+};
+
+struct GemmKParams {
+  CUtensorMap mA[GEMM_MAX_PROB][GEMM_MAX_SEG];
+  CUtensorMap mB[GEMM_MAX_PROB][GEMM_MAX_SEG];
+  KProb p[GEMM_MAX_PROB];
+  int32_t nprob, total_units;
+};
+
+template <int BN>
+struct GemmCfg {
+  static constexpr int STAGES = (BN == 256) ? 4 : 6;
+  static constexpr int A_BYTES = BM * BK * 2;  // 16 KB
+  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int TMEM_COLS = 2 * BN;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+};
+
+struct Unit {
+  int p, m0, n0, kb_lo, kb_hi;
+};
+
+__device__ __forceinline__ Unit decode_unit(const GemmKParams& P, int u) {
+  int p = 0;
+  while (p + 1 < P.nprob && u >= P.p[p + 1].unit_begin) ++p;
+  const KProb& q = P.p[p];
+  int local = u - q.unit_begin;
+  const int ks = local % q.split_k;
+  local /= q.split_k;
+  const int nt = local % q.n_tiles;
+  const int mt = local / q.n_tiles;
+  Unit r;
+  r.p = p;
+  r.m0 = mt * BM;
+  r.n0 = nt * 0;  // filled by caller with BN
+  r.n0 = nt;
+  r.kb_lo = (int)(((long long)ks * q.kb_total) / q.split_k);
+  r.kb_hi = (int)(((long long)(ks + 1) * q.kb_total) / q.split_k);
+  return r;
+}
+
+__device__ __forceinline__ void kb_to_seg(const KProb& q, int kb, int& seg, int& kk) {
+  seg = 0;
+  while (seg + 1 < q.nseg && kb >= q.kb[seg]) {
+    kb -= q.kb[seg];
+    ++seg;
+  }
+  kk = kb;
+}
+
+// ---------------------------------------------------------------- epilogue helpers
+__device__ __forceinline__ void load_bf16x32(const void* base, float (&x)[32]) {
+  const uint4* p = reinterpret_cast<const uint4*>(base);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    uint4 u = p[q];
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      float2 f = __bfloat1622float2(h[e]);
+      x[q * 8 + e * 2] = f.x;
+      x[q * 8 + e * 2 + 1] = f.y;
+    }
+  }
+}
+__device__ __forceinline__ void load_f32x32(const void* base, float (&x)[32]) {
+  const float4* p = reinterpret_cast<const float4*>(base);
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    float4 v = p[q];
+    x[q * 4] = v.x;
+    x[q * 4 + 1] = v.y;
+    x[q * 4 + 2] = v.z;
+    x[q * 4 + 3] = v.w;
+  }
+}
+__device__ __forceinline__ void load_any32(const void* base, int is_f32, size_t off, float (&x)[32]) {
+  if (is_f32)
+    load_f32x32(reinterpret_cast<const float*>(base) + off, x);
+  else
+    load_bf16x32(reinterpret_cast<const __nv_bfloat16*>(base) + off, x);
+}
+__device__ __forceinline__ void store_any32(void* base, int is_f32, size_t off, const float (&x)[32]) {
+  if (is_f32) {
+    float4* p = reinterpret_cast<float4*>(reinterpret_cast<float*>(base) + off);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) p[q] = make_float4(x[q * 4], x[q * 4 + 1], x[q * 4 + 2], x[q * 4 + 3]);
+  } else {
+    uint4* p = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(base) + off);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      uint4 u;
+      u.x = pack_bf16(x[q * 8 + 0], x[q * 8 + 1]);
+      u.y = pack_bf16(x[q * 8 + 2], x[q * 8 + 3]);
+      u.z = pack_bf16(x[q * 8 + 4], x[q * 8 + 5]);
+      u.w = pack_bf16(x[q * 8 + 6], x[q * 8 + 7]);
+      p[q] = u;
+    }
+  }
+}
+
+// Rotate adjacent pairs by alpha = dt * theta_i (timestamp RoPE).  Angle in fp64,
+// reduced mod 2*pi in fp64, then fp32 sincos (SURVEY hard part 6).
+__device__ __forceinline__ void rope_pair(float& a, float& b, double dt, double theta, float sign) {
+  const double TWO_PI_HI = 6.283185307179586;
+  const double TWO_PI_LO = 2.4492935982947064e-16;
+  double ang = dt * theta;
+  double k = rint(ang * 0.15915494309189535);
+  double r = fma(-k, TWO_PI_HI, ang);
+  r = fma(-k, TWO_PI_LO, r);
+  float s, c;
+  sincosf((float)r, &s, &c);
+  s *= sign;
+  const float x0 = a, x1 = b;
+  a = x0 * c - x1 * s;
+  b = x0 * s + x1 * c;
+}
+
+__device__ __forceinline__ void run_epilogue(const EpiParams& e, int row, int M, int n0c, float (&v)[32]) {
+  if (row >= M) return;
+  int orow = row;
+  if (e.row_map) {
+    orow = e.row_map[row];
+    if (orow < 0) return;
+  }
+  const size_t off = (size_t)orow * e.ldo + n0c;
+  const size_t in_off = (size_t)row * e.ldo + n0c;
+  switch (e.mode) {
+    case EPI_STORE: {
+      if (e.resid) {
+        float r[32];
+        load_any32(e.resid, e.resid_f32, in_off, r);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] += r[j];
+      }
+      store_any32(e.out, e.out_f32, off, v);
+    } break;
+    case EPI_GATE:
+    case EPI_GATE_ROPE: {
+      if (e.aux) store_any32(e.aux, e.aux_f32, in_off, v);
+      float x[32];
+      load_bf16x32(reinterpret_cast<const __nv_bfloat16*>(e.src) + in_off, x);
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] = x[j] * (1.0f / (1.0f + __expf(-v[j])));
+      if (e.mode == EPI_GATE_ROPE) {
+        const int s = e.row_seq[row];
+        const double dt = (s >= 0) ? (double)(e.t_ms[row] - e.t_ms[e.cu[s]]) : 0.0;
+#pragma unroll
+        for (int j = 0; j < 32; j += 2) {
+          const int i = ((n0c + j) % e.hd) >> 1;
+          rope_pair(v[j], v[j + 1], dt, e.theta[i], 1.0f);
+        }
+      }
+      store_any32(e.out, e.out_f32, off, v);
+    } break;
+    case EPI_GATE_BWD: {
+      float z[32], x[32];
+      load_any32(e.aux, e.aux_f32, in_off, z);
+      load_bf16x32(reinterpret_cast<const __nv_bfloat16*>(e.src) + in_off, x);
+      float r[32];
+      if (e.resid) {
+        load_any32(e.resid, e.resid_f32, in_off, r);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) r[j] = 0.f;
+      }
+      float u[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const float g = 1.0f / (1.0f + __expf(-z[j]));
+        u[j] = v[j] * x[j] * g * (1.0f - g);
+        r[j] += v[j] * g;
+      }
+      store_any32(e.out, e.out_f32, off, u);
+      store_any32(e.out2, 1, off, r);
+    } break;
+    case EPI_ATOMIC: {
+      float* o = reinterpret_cast<float*>(e.out) + off;
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        atomicAdd(reinterpret_cast<float4*>(o) + q, make_float4(v[q * 4], v[q * 4 + 1], v[q * 4 + 2], v[q * 4 + 3]));
+    } break;
+    case EPI_HEAD: {
+      float part = 0.f;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const float pre = v[j] + e.b1[n0c + j];
+        v[j] = pre;
+        part += fmaxf(pre, 0.f) * e.w2[n0c + j];
+      }
+      if (e.aux) store_any32(e.aux, e.aux_f32, in_off, v);
+      atomicAdd(e.logits + (size_t)row * e.n_towers + (n0c / e.hd), part);
+    } break;
+    default:
+      break;
+  }
+}
+
+// ---------------------------------------------------------------- kernel
+template <int BN>
+__global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_kernel(const __grid_constant__ GemmKParams P) {
+  using C = GemmCfg<BN>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
+  uint64_t* empty = full + C::STAGES;
+  uint64_t* tfull = empty + C::STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const uint32_t warp = warp_id(), lane = lane_id();
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < C::STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], 4);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc<C::TMEM_COLS>(tmem_slot);
+  if (warp == 0 && lane == 0) {
+    for (int p = 0; p < P.nprob; ++p)
+      for (int s = 0; s < P.p[p].nseg; ++s) {
+        tma_prefetch(&P.mA[p][s]);
+        tma_prefetch(&P.mB[p][s]);
+      }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ============================ TMA producer
+    if (elect_one()) {
+      uint32_t it = 0;
+      for (int u = blockIdx.x; u < P.total_units; u += gridDim.x) {
+        const Unit U = decode_unit(P, u);
+        const KProb& q = P.p[U.p];
+        const int n0 = U.n0 * BN;
+        for (int kb = U.kb_lo; kb < U.kb_hi; ++kb, ++it) {
+          const uint32_t stage = it % C::STAGES, use = it / C::STAGES;
+          if (use > 0) mbar_wait(&empty[stage], (use - 1) & 1);
+          int seg, kk;
+          kb_to_seg(q, kb, seg, kk);
+          const int k0 = kk * BK;
+          uint8_t* sA = smem + stage * C::STAGE_BYTES;
+          uint8_t* sB = sA + C::A_BYTES;
+          mbar_expect_tx(&full[stage], C::STAGE_BYTES);
+          if (!q.a_mn[seg]) {
+            tma_load_2d(sA, &P.mA[U.p][seg], &full[stage], k0, U.m0);
+          } else {
+#pragma unroll
+            for (int j = 0; j < BM / 64; ++j) tma_load_2d(sA + j * 8192, &P.mA[U.p][seg], &full[stage], U.m0 + 64 * j, k0);
+          }
+          if (!q.b_mn[seg]) {
+            tma_load_2d(sB, &P.mB[U.p][seg], &full[stage], k0, n0);
+          } else {
+#pragma unroll
+            for (int j = 0; j < BN / 64; ++j) tma_load_2d(sB + j * 8192, &P.mB[U.p][seg], &full[stage], n0 + 64 * j, k0);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ============================ MMA issuer
+    if (elect_one()) {
+      uint32_t it = 0, tc = 0;
+      for (int u = blockIdx.x; u < P.total_units; u += gridDim.x, ++tc) {
+        const Unit U = decode_unit(P, u);
+        const KProb& q = P.p[U.p];
+        const uint32_t buf = tc & 1, use = tc >> 1;
+        if (use > 0) mbar_wait(&tempty[buf], (use - 1) & 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + buf * BN;
+        for (int kb = U.kb_lo; kb < U.kb_hi; ++kb, ++it) {
+          const uint32_t stage = it % C::STAGES, suse = it / C::STAGES;
+          mbar_wait(&full[stage], suse & 1);
+          tc_fence_after();
+          int seg, kk;
+          kb_to_seg(q, kb, seg, kk);
+          const uint32_t a_mn = q.a_mn[seg], b_mn = q.b_mn[seg];
+          const uint32_t idesc = idesc_bf16(BM, BN, a_mn, b_mn);
+          const uint32_t sA = smem_u32(smem + stage * C::STAGE_BYTES);
+          const uint32_t sB = sA + C::A_BYTES;
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            const uint64_t ad = a_mn ? smem_desc(sA + k * 2048, 8192, 1024, SWZ_128B)
+                                     : smem_desc(sA + k * 32, 16, 1024, SWZ_128B);
+            const uint64_t bd = b_mn ? smem_desc(sB + k * 2048, 8192, 1024, SWZ_128B)
+                                     : smem_desc(sB + k * 32, 16, 1024, SWZ_128B);
+            mma_bf16_ss(d_tmem, ad, bd, idesc, (kb > U.kb_lo || k > 0) ? 1u : 0u);
+          }
+          mma_commit(&empty[stage]);
+        }
+        mma_commit(&tfull[buf]);
+      }
+    }
+  } else if (warp >= 4) {
+    // ============================ epilogue
+    const uint32_t quarter = warp & 3;
+    uint32_t tc = 0;
+    for (int u = blockIdx.x; u < P.total_units; u += gridDim.x, ++tc) {
+      const Unit U = decode_unit(P, u);
+      const KProb& q = P.p[U.p];
+      const uint32_t buf = tc & 1, use = tc >> 1;
+      mbar_wait(&tfull[buf], use & 1);
+      tc_fence_after();
+      const int row = U.m0 + quarter * 32 + lane;
+      const int n0 = U.n0 * BN;
+      for (int c = 0; c < BN / 32; ++c) {
+        const int n0c = n0 + c * 32;
+        if (n0c >= q.N) break;
+        uint32_t r[32];
+        tmem_ld32(tmem_addr(tmem_base, quarter, buf * BN + c * 32), r);
+        tmem_ld_wait();
+        float v[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+        run_epilogue(q.epi, row, q.M, n0c, v);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[buf]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc<C::TMEM_COLS>(tmem_base);
+}
+
+// ---------------------------------------------------------------- host
+static int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+static bool make_operand_map(CUtensorMap* m, const OperandDesc& o, int box_rows_kmajor) {
+  uint64_t dims[2] = {(uint64_t)o.cols, (uint64_t)o.rows};
+  uint64_t strides[1] = {(uint64_t)o.cols * 2};
+  uint32_t box[2];
+  if (!o.mn_major) {
+    box[0] = 64;
+    box[1] = (uint32_t)box_rows_kmajor;
+  } else {
+    box[0] = 64;
+    box[1] = 64;
+  }
+  return encode_bf16_map(m, o.ptr, 2, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B);
+}
+
+template <int BN>
+static cudaError_t launch_bn(const GemmKParams& P, cudaStream_t stream) {
+  using C = GemmCfg<BN>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(gemm_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const int grid = P.total_units < num_sms() ? P.total_units : num_sms();
+  gemm_kernel<BN><<<grid, GEMM_THREADS, C::SMEM, stream>>>(P);
+  return cudaGetLastError();
+}
+
+cudaError_t gemm_launch(const GemmProblem* probs, int nprob, int bn, cudaStream_t stream) {
+  if (nprob < 1 || nprob > GEMM_MAX_PROB || (bn != 128 && bn != 256)) return cudaErrorInvalidValue;
+  static GemmKParams P;  // large; filled per launch (host-side only)
+  memset(&P, 0, sizeof(P));
+  P.nprob = nprob;
+  int total = 0;
+  for (int p = 0; p < nprob; ++p) {
+    const GemmProblem& g = probs[p];
+    KProb& q = P.p[p];
+    if (g.M <= 0 || g.N <= 0 || g.N % 32 != 0 || g.nseg < 1 || g.nseg > GEMM_MAX_SEG) return cudaErrorInvalidValue;
+    q.M = g.M;
+    q.N = g.N;
+    q.nseg = g.nseg;
+    q.kb_total = 0;
+    for (int s = 0; s < g.nseg; ++s) {
+      const OperandDesc& A = g.A[s];
+      const OperandDesc& B = g.B[s];
+      if (A.cols % 8 || B.cols % 8 || g.K[s] <= 0) return cudaErrorInvalidValue;
+      if (!make_operand_map(&P.mA[p][s], A, BM)) return cudaErrorInvalidValue;
+      if (!make_operand_map(&P.mB[p][s], B, bn)) return cudaErrorInvalidValue;
+      q.a_mn[s] = A.mn_major;
+      q.b_mn[s] = B.mn_major;
+      q.kb[s] = (g.K[s] + BK - 1) / BK;
+      q.kb_total += q.kb[s];
+    }
+    q.split_k = g.split_k < 1 ? 1 : (g.split_k > q.kb_total ? q.kb_total : g.split_k);
+    q.m_tiles = (g.M + BM - 1) / BM;
+    q.n_tiles = (g.N + bn - 1) / bn;
+    q.unit_begin = total;
+    q.epi = g.epi;
+    total += q.m_tiles * q.n_tiles * q.split_k;
+  }
+  P.total_units = total;
+  return bn == 256 ? launch_bn<256>(P, stream) : launch_bn<128>(P, stream);
+}
+
+}  // namespace cadet

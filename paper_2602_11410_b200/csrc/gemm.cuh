@@ -1,0 +1,64 @@
+// Host/device interface of the tcgen05 GEMM with CADET fused epilogues.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace cadet {
+
+enum EpiMode : int32_t {
+  EPI_STORE = 0,      // out = acc (+ resid)                                        (A3, A6, A9, A12 ...)
+  EPI_GATE = 1,       // out = src * sigma(acc); aux = acc                          (Eq. 4)
+  EPI_GATE_ROPE = 2,  // out = RoPE_t(src * sigma(acc)); aux = acc                  (Eq. 5 + P:274)
+  EPI_GATE_BWD = 3,   // g = sigma(aux); out = acc*src*g*(1-g); out2 = acc*g + resid (A12)
+  EPI_ATOMIC = 4,     // out += acc (fp32 red.add; split-K weight gradients)
+  EPI_HEAD = 5,       // pre = acc + b1; aux = pre; logits[row, n/dh] += relu(pre).w2 (Eq. 8)
+};
+
+struct EpiParams {
+  int32_t mode;
+  int32_t out_f32;  // out dtype: 1 = fp32, 0 = bf16
+  int32_t ldo;      // leading dim of out / resid / src / aux (elements)
+  int32_t resid_f32;
+  int32_t aux_f32;
+  int32_t hd;       // RoPE head dim (EPI_GATE_ROPE) or head hidden width dh (EPI_HEAD)
+  int32_t n_towers; // EPI_HEAD: K
+  void* out;
+  const void* resid;
+  const void* src;   // bf16
+  void* aux;
+  float* out2;
+  const int32_t* row_map;  // optional output-row remap (scatter); < 0 = drop row
+  // RoPE (EPI_GATE_ROPE)
+  const int64_t* t_ms;
+  const int32_t* row_seq;
+  const int32_t* cu;
+  const double* theta;     // [hd/2]
+  // heads (EPI_HEAD)
+  const float* b1;
+  const float* w2;
+  float* logits;
+};
+
+struct OperandDesc {
+  const void* ptr;  // bf16, row-major storage [rows][cols]
+  int32_t rows, cols;
+  int32_t mn_major; // 0: storage is [MN][K] (K-major); 1: storage is [K][MN] (MN-major)
+};
+
+constexpr int GEMM_MAX_PROB = 3;
+constexpr int GEMM_MAX_SEG = 3;
+
+struct GemmProblem {
+  int32_t M, N;
+  int32_t nseg;
+  int32_t K[GEMM_MAX_SEG];
+  OperandDesc A[GEMM_MAX_SEG], B[GEMM_MAX_SEG];
+  int32_t split_k;   // > 1 only with EPI_ATOMIC
+  EpiParams epi;
+};
+
+// Enqueue: returns cudaError_t.  BN chosen by the host (128 or 256).
+cudaError_t gemm_launch(const GemmProblem* probs, int nprob, int bn, cudaStream_t stream);
+
+}  // namespace cadet

@@ -1,0 +1,57 @@
+// Plan data carved from the workspace.
+#pragma once
+#include <stdint.h>
+#include <cuda_runtime.h>
+
+namespace cadet {
+
+constexpr int TILE = 128;
+
+struct QTileInfo {  // one per (sequence, 128-row tile), anchored at the sequence start
+  int32_t seq;      // sequence index
+  int32_t qt;       // tile index inside the sequence
+  int32_t nf;       // front k-tiles [0, nf) are visited (prefix region, max_i kv_end)
+  int32_t kt2;      // then tiles [kt2, qt] (diagonal, and qt-1 for a PAIR_PREV first row); kt2 >= nf
+};
+
+struct PlanView {   // device pointers into the workspace
+  uint32_t* err;      // [1] latched error bits
+  int32_t* counters;  // [0] = nq_total, [1] = n (for checking)
+  unsigned long long* pairs;  // [1]
+  int32_t* kv_end;    // [T]
+  int32_t* row_seq;   // [T] (-1 for pad rows)
+  uint8_t* row_pp;    // [T] PAIR_PREV bit resolved for the row
+  int32_t* tile_off;  // [n+1] prefix sum of nq_s
+  int64_t* tc_off;    // [n+1] prefix sum of nq_s^2 (export)
+  QTileInfo* qinfo;   // [nq_cap]
+  int32_t* fwd_order; // [nq_cap] q-tiles by descending forward cost
+  int32_t* bwd_order; // [nq_cap] k-tiles by descending backward cost
+  int32_t* hist;      // [2 * hmax] histograms / cursors
+  int32_t nq_cap, hmax;
+};
+
+struct PlanArgs {
+  int32_t n, T, max_seqlen, mask_flags;
+  int64_t delta_ctx, delta_cand;
+  const int32_t* cu;
+  const int64_t* t;
+  const int32_t* sess;
+  const int32_t* ncand;
+  const int32_t* nstatic;
+  const uint8_t* flags;
+};
+
+size_t plan_bytes(int32_t n, int32_t T, int32_t max_seqlen);
+PlanView plan_carve(void* ws, int32_t n, int32_t T, int32_t max_seqlen);
+cudaError_t plan_launch(const PlanArgs& a, const PlanView& v, cudaStream_t st);
+cudaError_t plan_export_launch(const PlanArgs& a, const PlanView& v, int32_t* kv_end_out, int8_t* tc_out,
+                               int64_t tc_cap, int64_t* pairs_out, cudaStream_t st);
+cudaError_t chunk_launch(const int32_t* cu_in, int32_t n_in, int32_t L, int32_t* cu_out, int32_t cap,
+                         int32_t* n_out, uint32_t* err, cudaStream_t st);
+cudaError_t pack_launch(const void* padded, const int32_t* lens, int32_t B, int32_t Lmax, int32_t d, int32_t budget,
+                        const int64_t* tp, const int32_t* sp, void* packed, int64_t* t_out, int32_t* s_out,
+                        int32_t* cu_out, int32_t* n_packed, uint32_t* err, cudaStream_t st);
+cudaError_t zero_pad_rows_launch(void* buf, int32_t row_bytes, int32_t T, const int32_t* cu, int32_t n,
+                                 cudaStream_t st);
+
+}  // namespace cadet
