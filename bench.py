@@ -1,0 +1,367 @@
+#!/usr/bin/env python
+"""bench.py — CADET hot path on B200: packed attention fwd+bwd throughput (tokens/s, TFLOP/s).
+
+One step = one pass of the whole hot path over one packed batch per rank:
+pack -> chunk -> plan -> L gated attention layers forward -> towers + routed BCE -> towers and
+layers backward -> (N > 1) NCCL all-reduce of the flat fp32 gradient buffer.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c4|c3|c2] [--impl ours|reference]
+
+Rank r uses the generator batch of seed 1000*r (weak scaling: fixed per-rank budget T).  Inputs are
+resident in HBM for `value`; `e2e` repeats the step through the same public API with the step's
+inputs copied from pinned host memory and the loss read back inside the timed region.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+
+WORKLOADS = {
+    # C4 long-history chunked path (the north-star gate config), C3 paper-shaped
+    # 8-layer stack, C2 serving shape (forward only, 64 x ~512 with 64 candidates).
+    "c4": dict(d_model=1024, n_heads=8, n_layers=1, budget=65536, L_chunk=2048, max_tokens=8192),
+    "c3": dict(d_model=352, n_heads=4, n_layers=8, budget=65536, L_chunk=2048, max_tokens=8192),
+}
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d, "measured"
+    return PEAKS_FALLBACK, "fallback"
+
+
+# ------------------------------------------------------------------ clocks sampler
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, dev_index: int):
+        self.dev = dev_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ workload
+def build_inputs(wl: dict, seed: int, pin: bool):
+    from synth import generator as G
+    from paper_2602_11410_b200.model import make_inputs
+    gcfg = G.GenConfig(max_tokens=wl["max_tokens"])
+    users = G.gen_users_for_budget(seed, wl["budget"], gcfg)
+    return users, make_inputs(users, wl["d_model"], wl["L_chunk"], seed, pin=pin)
+
+
+def step_flops(wl: dict, tokens: int, pairs: int, n_imp: int, dh: int, K: int = 2):
+    """Algorithmic FLOPs per step: attention 4 d P fwd + 8 d P bwd per layer;
+    seven d x d projections 2 T_r d^2 each fwd, twice that bwd; towers 2 n K d dh fwd, 2x bwd."""
+    d, nl = wl["d_model"], wl["n_layers"]
+    attn_f = nl * 4.0 * d * pairs
+    attn_b = nl * 8.0 * d * pairs
+    gemm = nl * (14.0 + 28.0) * tokens * d * d + 6.0 * n_imp * K * d * dh
+    return {"gemm": gemm, "attn_fwd": attn_f, "attn_bwd": attn_b}
+
+
+# ------------------------------------------------------------------ oracle baseline (CPU)
+def oracle_sample(users, wl: dict, max_tokens: int):
+    """First whole chunks of the batch up to max_tokens tokens (bounded CPU sample)."""
+    from synth import generator as G
+    L = wl["L_chunk"]
+    seqs = []
+    total = 0
+    for u in users:
+        m = u.length
+        n = -(-m // L)
+        starts = [0] + [m - (n - c) * L for c in range(1, n)]
+        ends = starts[1:] + [m]
+        for a, e in zip(starts, ends):
+            if total + (e - a) > max_tokens:
+                return seqs, total
+            seqs.append((u, a, e))
+            total += e - a
+    return seqs, total
+
+
+def run_oracle_step(seqs, wl: dict, seed: int):
+    """One fp64 oracle pass (layers fwd + towers loss/bwd + layers bwd) over the sample."""
+    from oracle import cadet_oracle as O
+    from synth import generator as G
+    d, H, nl = wl["d_model"], wl["n_heads"], wl["n_layers"]
+    cfg = O.AttnConfig(d_model=d, n_heads=H)
+    Ws = [[w.astype(np.float64) for w in G.layer_weights(seed, l, d).as_list()] for l in range(nl)]
+    hw = G.head_weights(seed, 2, d, d // 2)
+    rng = np.random.default_rng(seed)
+    loss = 0.0
+    for (u, a, e) in seqs:
+        t = u.timestamps[a:e]
+        A = O.mask_dense(t, 0, cfg)
+        X = rng.standard_normal((e - a, d))
+        caches = []
+        for l in range(nl):
+            Y, c = O.layer_forward_seq(X, Ws[l], t, A, cfg)
+            caches.append((X, c))
+            X = X + Y
+        rows = np.arange(0, e - a, 2)
+        Lh, z, dH, g = O.heads_loss_backward(X, rows, hw.W1.astype(np.float64), hw.b1.astype(np.float64),
+                                             hw.w2.astype(np.float64), hw.b2.astype(np.float64),
+                                             u.buckets[a:e][rows], u.labels[a:e][rows].astype(np.float64))
+        loss += Lh
+        dX = dH
+        for l in reversed(range(nl)):
+            Xl, c = caches[l]
+            dXa, gW, _ = O.layer_backward_seq(c, Ws[l], t, A, dX, cfg)
+            dX = dX + dXa
+    return loss
+
+
+def cpu_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def time_oracle(users, wl, seed, budget_s=15.0, max_tokens=None):
+    """Time the oracle as it stands on the host cores; returns (tokens/s, tokens, seconds, desc)."""
+    try:
+        from threadpoolctl import threadpool_limits
+        ctx = threadpool_limits(cpu_cores())
+    except Exception:
+        ctx = None
+    max_tokens = max_tokens or (12288 if wl["d_model"] >= 1024 else 8192)
+    seqs, tok = oracle_sample(users, wl, max_tokens)
+    t0 = time.perf_counter()
+    run_oracle_step(seqs, wl, seed)
+    dt = time.perf_counter() - t0
+    desc = (f"first {len(seqs)} whole chunks ({tok} tokens) of the rank-0 batch, {wl['n_layers']} layer(s) "
+            f"fwd+bwd + towers, numpy fp64")
+    return tok / dt, tok, dt, desc
+
+
+# ------------------------------------------------------------------ main
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", default="c4", choices=sorted(WORKLOADS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    wl = WORKLOADS[args.workload]
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    metric = "packed attention fwd+bwd tokens/s and TFLOP/s (% bf16 peak) at 1/2/4/8 B200"
+    workload_name = {"c4": "C4 long-history chunked path: histories <= 8192 events chunked at 2048, d 1024, "
+                           "8 heads x 128, 1 gated layer + K=2 towers, fwd+bwd, T=65536/rank",
+                     "c3": "C3 paper-shaped: 8 gated layers, d 352, 4 heads x 88, Lc 2048, K=2 towers, fwd+bwd, "
+                           "T=65536/rank"}[args.workload]
+
+    if args.impl == "reference":
+        # The reference arm is the CPU oracle (no reference implementation exists): rank 0 only.
+        if rank != 0:
+            return
+        users, _ = build_inputs(wl, 1000 * rank, pin=False)
+        times, toks = [], 0
+        for i in range(args.warmup + args.steps):
+            v, tok, dt, desc = time_oracle(users, wl, 0, max_tokens=2048 if wl["d_model"] >= 1024 else 3072)
+            if i >= args.warmup:
+                times.append(dt)
+                toks = tok
+        ms = 1000.0 * float(np.mean(times))
+        val = toks / (ms / 1000.0)
+        out = {"impl": "reference", "metric": metric, "value": val, "unit": "tokens/s", "n_gpus": args.gpus,
+               "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+               "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+               "config": {"workload": workload_name, "sample": desc},
+               "cpu_baseline": {"value": val, "unit": "tokens/s", "cores": cpu_cores(), "kind": "oracle",
+                                "sample": desc},
+               "e2e": {"value": val, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(out))
+        return
+
+    import torch
+    import torch.distributed as dist
+    from paper_2602_11410_b200 import build, ops
+    from paper_2602_11410_b200.model import CadetStack, StackConfig
+    build.build(verbose=False)
+    torch.cuda.set_device(local)
+    group = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        group = dist.group.WORLD
+    dev = torch.device("cuda", local)
+
+    users, host_inp = build_inputs(wl, 1000 * rank, pin=True)
+    inp = host_inp.to(dev)
+    torch.cuda.synchronize()
+    scfg = StackConfig(d_model=wl["d_model"], n_heads=wl["n_heads"], n_layers=wl["n_layers"], budget=wl["budget"],
+                       L_chunk=wl["L_chunk"])
+    stack = CadetStack(scfg, seed=0, device=dev)
+    pairs = stack.pairs(inp)
+    n_imp = inp.rows.numel()
+    flops = step_flops(wl, inp.tokens, pairs, n_imp, scfg.dh)
+    total_flops = sum(flops.values())
+
+    def barrier():
+        if group is not None:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        stack.step(inp, group)
+    torch.cuda.synchronize()
+    stack.poll()
+
+    # ---------------- timed region (inputs resident in HBM)
+    clocks = ClockSampler(local)
+    clocks.start()
+    ops.prof_enable(15, 64 * (args.steps + 1) * (wl["n_layers"] + 2))
+    n0 = ops.launch_count()
+    barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    for _ in range(args.steps):
+        stack.step(inp, group)
+    ev1.record()
+    torch.cuda.synchronize()
+    barrier()
+    launches = (ops.launch_count() - n0) // max(1, args.steps)
+    prof = ops.prof_read()
+    clk = clocks.stop()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if group is not None:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    tok = torch.tensor([inp.tokens], dtype=torch.float64, device=dev)
+    if group is not None:
+        dist.all_reduce(tok)
+    tokens_all = float(tok.item())
+    value = tokens_all / (ms_max / 1000.0)
+    tflops_all = total_flops * world / (ms_max / 1000.0) / 1e12
+
+    # ---------------- e2e: same step through the public API from pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        loss_h = torch.zeros(1, dtype=torch.float32).pin_memory()
+        for _ in range(2):
+            inp.copy_(host_inp)
+            stack.step(inp, group)
+            loss_h.copy_(stack.loss, non_blocking=True)
+        torch.cuda.synchronize()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(args.steps):
+            inp.copy_(host_inp)
+            stack.step(inp, group)
+            loss_h.copy_(stack.loss, non_blocking=True)
+        e1.record()
+        torch.cuda.synchronize()
+        barrier()
+        ems = torch.tensor([e0.elapsed_time(e1) / args.steps], dtype=torch.float64, device=dev)
+        if group is not None:
+            dist.all_reduce(ems, op=dist.ReduceOp.MAX)
+        e2e = {"value": tokens_all / (float(ems.item()) / 1000.0), "unit": "tokens/s",
+               "h2d_bytes_per_step": int(host_inp.nbytes()), "d2h_bytes_per_step": 4,
+               "ms_per_step": float(ems.item())}
+    stack.poll()
+
+    if rank != 0:
+        if group is not None:
+            dist.destroy_process_group()
+        return
+
+    # ---------------- roofline of the dominant kernel class (live CUDA-event times)
+    peaks, peak_src = load_peaks()
+    per_step_ms = {k: v[0] / max(1, args.steps) for k, v in prof.items()}
+    dom = max(("gemm", "attn_fwd", "attn_bwd"), key=lambda k: per_step_ms[k])
+    achieved = flops[dom] / (per_step_ms[dom] / 1000.0) / 1e12 if per_step_ms[dom] > 0 else 0.0
+    peak = float(peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops")))
+    roofline = {"bound": "tensor", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                "frac": achieved / peak, "traffic": None,
+                "peak_source": f"{peak_src} bf16_tflops_sustained (kernel timed inside a long step)",
+                "share_of_step": per_step_ms[dom] / ms, "per_class_ms_per_step": per_step_ms,
+                "launches_per_step": {k: v[1] / max(1, args.steps) for k, v in prof.items()}}
+    cpu = None
+    if not args.no_cpu and world == 1:
+        v, tokc, dt, desc = time_oracle(users, wl, 0)
+        cpu = {"value": v, "unit": "tokens/s", "cores": cpu_cores(), "kind": "oracle", "sample": desc,
+               "seconds": dt}
+    out = {
+        "metric": metric, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": workload_name, "tokens_real_per_rank": inp.tokens, "budget_T": wl["budget"],
+                   "sequences_per_rank": inp.n_chunks, "histories_per_rank": inp.n_hist,
+                   "allowed_pairs_per_head": pairs, "impressions": n_imp, "layers": wl["n_layers"],
+                   "d_model": wl["d_model"], "heads": wl["n_heads"], "L_chunk": wl["L_chunk"],
+                   "l2": "inputs > L2 (X 128 MB + activations > 1 GB per step); no flush needed",
+                   "parallelism": f"dp{world}"},
+        "tflops": tflops_all, "tflops_per_gpu": tflops_all / world,
+        "frac_of_peak_measured": tflops_all / world / float(peaks.get("bf16_tflops", 1663.9)),
+        "frac_of_peak_spec": tflops_all / world / 2250.0,
+        "flops_per_step_per_rank": flops,
+        "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
+    }
+    print(json.dumps(out))
+    if group is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

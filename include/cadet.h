@@ -206,14 +206,16 @@ cadet_status cadet_heads_loss_backward(const cadet_head_config* h_h, const cadet
  * n_out[0] (device) = number of chunks.  Chunks stay contiguous: no data moves. */
 cadet_status cadet_chunk(const int32_t* cu_in, int32_t n_in, int32_t L_chunk, int32_t* cu_out, int32_t cap,
                          int32_t* n_out, void* ws, cadet_stream_t stream); /* ws >= 256 B: error word (cadet_poll) */
-/* Pack: greedy arrival-order packing of padded sequences into one fixed budget:
- * sequences 0..k-1 are copied while their running total fits `budget`; rows [total, budget) are
- * zero-filled.  padded: bf16 [B, Lmax, d]; lens: int32 [B]; t_padded (nullable) int64 [B, Lmax] and
- * s_padded (nullable) int32 [B, Lmax] are packed alongside into t_out / s_out ([budget]).
+/* Pack: greedy arrival-order packing into one fixed budget: sequences 0..k-1 are
+ * copied while their running total fits `budget`; rows [total, budget) are zero-filled.
+ * src: bf16 [*, d]; sequence s occupies src rows [src_row[s], src_row[s] + lens[s]) (padded input
+ * [B, Lmax, d]: src_row[s] = s * Lmax; contiguous histories: src_row = NULL means the exclusive
+ * prefix sum of lens).  t_src (nullable) int64 and s_src (nullable) int32 are per src row and are
+ * packed alongside into t_out / s_out ([budget]).
  * Outputs: packed [budget, d], cu_out [B+1] (entries past n_packed repeat the total), n_packed[0].
  * ws (>= cadet_pack_workspace_bytes) holds the error word read by cadet_poll. */
-cadet_status cadet_pack(const void* padded, const int32_t* lens, int32_t B, int32_t Lmax, int32_t d, int32_t budget,
-                        const int64_t* t_padded, const int32_t* s_padded, void* packed, int64_t* t_out,
+cadet_status cadet_pack(const void* src, const int64_t* src_row, const int32_t* lens, int32_t B, int32_t d,
+                        int32_t budget, const int64_t* t_src, const int32_t* s_src, void* packed, int64_t* t_out,
                         int32_t* s_out, int32_t* cu_out, int32_t* n_packed, void* ws, size_t ws_bytes,
                         cadet_stream_t stream);
 size_t cadet_pack_workspace_bytes(int32_t B);
@@ -224,6 +226,17 @@ size_t cadet_pack_workspace_bytes(int32_t B);
  * [M, N]; resid (nullable) same dtype as C.  N % 32 == 0, K % 8 == 0, M % 8 == 0 when MN-major. */
 cadet_status cadet_gemm(int32_t M, int32_t N, int32_t K, const void* A, int32_t a_mn, const void* B, int32_t b_mn,
                         void* C, int32_t c_f32, const void* resid, cadet_stream_t stream);
+
+/* ------------------------------------------------------------------ instrumentation (bench / tests)
+ * cadet_launch_count: number of libcadet kernels launched by this process so far.
+ * cadet_prof_enable(classes, max_pairs): from now on every launch of a kernel in `classes`
+ * (bit 0 GEMM, bit 1 attention forward, bit 2 attention backward, bit 3 everything else) is
+ * bracketed by a cudaEvent pair on its stream (no host sync).  cadet_prof_read synchronises those
+ * events and returns, per class, the summed milliseconds and the number of launches; it disables
+ * profiling.  Used by bench.py to time the dominant kernel live inside the timed region. */
+int64_t cadet_launch_count(void);
+cadet_status cadet_prof_enable(int32_t classes, int32_t max_pairs);
+cadet_status cadet_prof_read(double* ms_h /*[4]*/, int64_t* launches_h /*[4]*/);
 
 /* ------------------------------------------------------------------ errors
  * Synchronises `stream`, then returns and clears the device-latched error word in ws. */

@@ -88,10 +88,13 @@ SIGNATURES = {
     "cadet_heads_loss_backward": (I32, [C.POINTER(HeadConfig), C.POINTER(HeadWeights), P, P, I32, I32, P, P, P, P,
                                         P, P, C.POINTER(HeadGrads), P, SZ, P]),
     "cadet_chunk": (I32, [P, I32, I32, P, I32, P, P, P]),
-    "cadet_pack": (I32, [P, P, I32, I32, I32, I32, P, P, P, P, P, P, P, P, SZ, P]),
+    "cadet_pack": (I32, [P, P, P, I32, I32, I32, P, P, P, P, P, P, P, P, SZ, P]),
     "cadet_pack_workspace_bytes": (SZ, [I32]),
     "cadet_gemm": (I32, [I32, I32, I32, P, I32, P, I32, P, I32, P, P]),
     "cadet_poll": (I32, [P, P]),
+    "cadet_launch_count": (I64, []),
+    "cadet_prof_enable": (I32, [I32, I32]),
+    "cadet_prof_read": (I32, [C.POINTER(C.c_double), C.POINTER(I64)]),
 }
 
 _lib = None

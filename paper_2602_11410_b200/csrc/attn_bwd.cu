@@ -12,6 +12,7 @@
 //   warp 1     : TMEM owner + MMA issuer
 //   warps 2..5 : thread = key row for P^T / dS^T (TMEM lane), = query row for the dQ drain
 #include "attn_common.cuh"
+#include "prof.cuh"
 
 namespace cadet {
 
@@ -320,12 +321,14 @@ static cudaError_t bwd_hd(const CUtensorMap& mQ, const CUtensorMap& mK, const CU
   }
   const int grid = p.plan.nq_cap * p.H;
   if (grid == 0) return cudaSuccess;
+  ProfScope ps(PROF_ATTN_BWD, st, 1);
   attn_bwd_kernel<HD><<<grid, 192, C::SMEM, st>>>(mQ, mK, mV, mdO, p);
   return cudaGetLastError();
 }
 
 cudaError_t attn_bwd_pre_launch(const void* O, const void* dO, float* D, float* dQacc, int T, int H, int hd,
                                 cudaStream_t st) {
+  ProfScope ps(PROF_OTHER, st, 1);
   if (T > 0)
     attn_bwd_pre_kernel<<<(T + 7) / 8, 256, 0, st>>>(reinterpret_cast<const __nv_bfloat16*>(O),
                                                       reinterpret_cast<const __nv_bfloat16*>(dO), D, T, H, hd);

@@ -13,6 +13,7 @@
 //                conditional rescaling (threshold 2^8), P -> smem (bf16), O rescale in TMEM,
 //                final O / l and LSE.
 #include "attn_common.cuh"
+#include "prof.cuh"
 
 namespace cadet {
 
@@ -306,6 +307,7 @@ static cudaError_t fwd_hd(const CUtensorMap& mQ, const CUtensorMap& mK, const CU
   }
   const int grid = p.plan.nq_cap * p.H;
   if (grid == 0) return cudaSuccess;
+  ProfScope ps(PROF_ATTN_FWD, st, 1);
   attn_fwd_kernel<HD><<<grid, 192, C::SMEM, st>>>(mQ, mK, mV, p);
   return cudaGetLastError();
 }

@@ -181,15 +181,15 @@ cadet_status cadet_chunk(const int32_t* cu_in, int32_t n_in, int32_t L_chunk, in
 
 size_t cadet_pack_workspace_bytes(int32_t B) { (void)B; return 256; }
 
-cadet_status cadet_pack(const void* padded, const int32_t* lens, int32_t B, int32_t Lmax, int32_t d, int32_t budget,
-                        const int64_t* t_padded, const int32_t* s_padded, void* packed, int64_t* t_out,
+cadet_status cadet_pack(const void* src, const int64_t* src_row, const int32_t* lens, int32_t B, int32_t d,
+                        int32_t budget, const int64_t* t_src, const int32_t* s_src, void* packed, int64_t* t_out,
                         int32_t* s_out, int32_t* cu_out, int32_t* n_packed, void* ws, size_t ws_bytes,
                         cadet_stream_t stream) {
-  if (!padded || !lens || !packed || !cu_out || !n_packed || B < 0 || Lmax <= 0 || d <= 0 || budget <= 0 || !ws)
+  if (!src || !lens || !packed || !cu_out || !n_packed || B < 0 || d <= 0 || budget <= 0 || !ws)
     return fail(CADET_E_ARG, "cadet_pack args");
   if (d % 8) return fail(CADET_E_ARG, "d must be a multiple of 8");
   if (ws_bytes < 256) return fail(CADET_E_WORKSPACE, "pack workspace");
-  return cuda_check(pack_launch(padded, lens, B, Lmax, d, budget, t_padded, s_padded, packed, t_out, s_out, cu_out,
+  return cuda_check(pack_launch(src, src_row, lens, B, d, budget, t_src, s_src, packed, t_out, s_out, cu_out,
                                 n_packed, reinterpret_cast<uint32_t*>(ws), reinterpret_cast<cudaStream_t>(stream)),
                     "pack");
 }

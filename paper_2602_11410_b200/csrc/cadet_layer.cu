@@ -6,6 +6,7 @@
 #include "../../include/cadet.h"
 #include "gemm.cuh"
 #include "layer.cuh"
+#include "misc.cuh"
 
 using namespace cadet;
 
@@ -68,6 +69,515 @@ cadet_status cadet_attn_core_forward(const cadet_attn_config* cfg, const cadet_b
   if (e == cudaSuccess) e = cudaMemsetAsync(lse, 0, sizeof(float) * (size_t)T * cfg->n_heads, st);
   if (e == cudaSuccess) e = attn_fwd_launch(Qr, Kr, V, p, st);
   return cuda_err(e, "attention forward");
+}
+
+
+cadet_status cadet_attn_core_backward(const cadet_attn_config* cfg, const cadet_batch* b, const void* Qr,
+                                      const void* Kr, const void* V, const void* O, const float* lse, const void* dO,
+                                      float* dQr, void* dKr, void* dV, void* ws, size_t ws_bytes,
+                                      cadet_stream_t stream) {
+  cadet_status s = check_cfg(cfg);
+  if (s) return s;
+  if ((s = check_batch(b, cfg))) return s;
+  if (!Qr || !Kr || !V || !O || !lse || !dO || !dQr || !dKr || !dV || !ws) {
+    set_error("cadet_attn_core_backward: null pointer");
+    return CADET_E_ARG;
+  }
+  const int T = b->total_tokens, d = cfg->d_model, H = cfg->n_heads;
+  const size_t pb = plan_bytes(b->n_seqs, T, T);
+  const size_t need = pb + a256((size_t)4 * H * T);
+  if (ws_bytes < need) return ws_err(ws_bytes, need);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if ((s = cadet_mask_plan(cfg, b, ws, ws_bytes, stream))) return s;
+  PlanView v = plan_carve(ws, b->n_seqs, T, T);
+  float* D = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ws) + pb);
+  AttnParams p = attn_params(cfg, b, v);
+  p.lse = const_cast<float*>(lse);
+  p.D = D;
+  p.dQ = dQr;
+  p.dK = dKr;
+  p.dV = dV;
+  const int ob = d * (cfg->out_f32 ? 4 : 2);
+  cudaError_t e = attn_bwd_pre_launch(O, dO, D, dQr, T, H, cfg->head_dim, st);
+  if (e == cudaSuccess) e = zero_pad_rows_launch(dKr, ob, T, b->cu_seqlens, b->n_seqs, st);
+  if (e == cudaSuccess) e = zero_pad_rows_launch(dV, ob, T, b->cu_seqlens, b->n_seqs, st);
+  if (e == cudaSuccess) e = attn_bwd_launch(Qr, Kr, V, dO, p, st);
+  return cuda_err(e, "attention backward");
+}
+
+}  // extern "C"
+
+// =====================================================================================
+// Full gated layer (rows A2-A12)
+// =====================================================================================
+namespace {
+
+struct LayerBufs {  // carved from `saved`
+  void *Zx, *Xt, *Q, *K, *Zq, *Zk, *Qr, *Kr, *V, *O;
+  float* lse;
+};
+struct LayerWs {    // carved from `ws` after the plan
+  double* theta;
+  float* D;
+  void *dO, *dKr, *dV, *uq, *uk, *dQ, *dK, *ux;
+  float *dQacc, *rq, *rk, *rx;
+};
+
+size_t bf_sz(int T, int d) { return a256((size_t)T * d * 2); }
+size_t f_sz(int T, int d) { return a256((size_t)T * d * 4); }
+
+LayerBufs carve_saved(void* saved, const cadet_attn_config* c, int T) {
+  uint8_t* p = reinterpret_cast<uint8_t*>(saved);
+  const size_t z = bf_sz(T, c->d_model);
+  LayerBufs L;
+  void** slots[10] = {&L.Zx, &L.Xt, &L.Q, &L.K, &L.Zq, &L.Zk, &L.Qr, &L.Kr, &L.V, &L.O};
+  for (int i = 0; i < 10; ++i) *slots[i] = p + i * z;
+  L.lse = reinterpret_cast<float*>(p + 10 * z);
+  return L;
+}
+size_t saved_bytes(const cadet_attn_config* c, int T) {
+  return 10 * bf_sz(T, c->d_model) + a256((size_t)4 * c->n_heads * T);
+}
+size_t layer_ws_bytes(const cadet_attn_config* c, int n, int T) {
+  const int d = c->d_model;
+  return plan_bytes(n, T, T) + a256(8 * 64) + a256((size_t)4 * c->n_heads * T) + 8 * bf_sz(T, d) + 4 * f_sz(T, d);
+}
+LayerWs carve_ws(void* ws, const cadet_attn_config* c, int n, int T) {
+  const int d = c->d_model;
+  uint8_t* p = reinterpret_cast<uint8_t*>(ws) + plan_bytes(n, T, T);
+  LayerWs W;
+  W.theta = reinterpret_cast<double*>(p);
+  p += a256(8 * 64);
+  W.D = reinterpret_cast<float*>(p);
+  p += a256((size_t)4 * c->n_heads * T);
+  void** bf[8] = {&W.dO, &W.dKr, &W.dV, &W.uq, &W.uk, &W.dQ, &W.dK, &W.ux};
+  for (int i = 0; i < 8; ++i) {
+    *bf[i] = p;
+    p += bf_sz(T, d);
+  }
+  float** fp[4] = {&W.dQacc, &W.rq, &W.rk, &W.rx};
+  for (int i = 0; i < 4; ++i) {
+    *fp[i] = reinterpret_cast<float*>(p);
+    p += f_sz(T, d);
+  }
+  return W;
+}
+
+int pick_bn(int M, int N) {
+  if (N % 256 == 0 && (long long)((M + 127) / 128) * (N / 256) >= 148) return 256;
+  if (N <= 128) return 128;
+  const int w256 = (N + 255) / 256 * 256 - N, w128 = (N + 127) / 128 * 128 - N;
+  return (w256 <= w128 && (long long)((M + 127) / 128) * ((N + 255) / 256) >= 148) ? 256 : 128;
+}
+int pick_split(int M, int N, int bn, int K) {
+  const long long tiles = (long long)((M + 127) / 128) * ((N + bn - 1) / bn);
+  const int kb = (K + 63) / 64;
+  long long split = (2 * 148 + tiles - 1) / tiles;
+  if (split > kb / 4) split = kb / 4;
+  return split < 1 ? 1 : (int)split;
+}
+
+OperandDesc act(const void* p, int T, int d) { return OperandDesc{p, T, d, 0}; }       // [T, d] as K-major A
+OperandDesc act_t(const void* p, int T, int d) { return OperandDesc{p, T, d, 1}; }     // [T, d] as MN-major (wgrad)
+OperandDesc w_fwd(const void* W, int din, int dout) { return OperandDesc{W, din, dout, 1}; }  // x.W: B MN-major
+OperandDesc w_bwd(const void* W, int din, int dout) { return OperandDesc{W, din, dout, 0}; }  // g.W^T: B K-major
+
+GemmProblem prob(int M, int N, int K, OperandDesc A, OperandDesc B, int mode) {
+  GemmProblem g;
+  memset(&g, 0, sizeof(g));
+  g.M = M;
+  g.N = N;
+  g.nseg = 1;
+  g.K[0] = K;
+  g.A[0] = A;
+  g.B[0] = B;
+  g.split_k = 1;
+  g.epi.mode = mode;
+  g.epi.ldo = N;
+  return g;
+}
+
+// dW = A^T . G over T rows, fp32, split-K with atomics into a zeroed output.
+GemmProblem wgrad(const void* A, const void* G, float* dW, int T, int din, int dout, int bn) {
+  GemmProblem g = prob(din, dout, T, act_t(A, T, din), act_t(G, T, dout), EPI_ATOMIC);
+  g.split_k = pick_split(din, dout, bn, T);
+  g.epi.out = dW;
+  g.epi.out_f32 = 1;
+  return g;
+}
+
+struct RopeCtx {
+  const int64_t* t;
+  const int32_t* row_seq;
+  const int32_t* cu;
+  const double* theta;
+  int hd;
+};
+
+}  // namespace
+
+extern "C" {
+
+size_t cadet_attn_workspace_bytes(const cadet_attn_config* c, int32_t n, int32_t T) {
+  if (check_cfg(c)) return 0;
+  return layer_ws_bytes(c, n, T);
+}
+size_t cadet_attn_saved_bytes(const cadet_attn_config* c, int32_t T) {
+  if (check_cfg(c)) return 0;
+  return saved_bytes(c, T);
+}
+
+cadet_status cadet_attn_forward(const cadet_attn_config* cfg, const cadet_batch* b, const cadet_attn_weights* w,
+                                const void* X, void* Y, const void* resid, void* saved, void* ws, size_t ws_bytes,
+                                cadet_stream_t stream) {
+  cadet_status s = check_cfg(cfg);
+  if (s) return s;
+  if ((s = check_batch(b, cfg))) return s;
+  if (!w || !X || !Y || !saved || !ws || !w->W_q || !w->W_k || !w->W_v || (cfg->use_rep_gate && !w->W_xg) ||
+      (cfg->use_int_gate && (!w->W_qg || !w->W_kg)) || (cfg->use_out_proj && !w->W_o)) {
+    set_error("cadet_attn_forward: null pointer");
+    return CADET_E_ARG;
+  }
+  const int T = b->total_tokens, d = cfg->d_model, n = b->n_seqs, hd = cfg->head_dim;
+  const size_t need = layer_ws_bytes(cfg, n, T);
+  if (ws_bytes < need) return ws_err(ws_bytes, need);
+  if (T == 0) return CADET_OK;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if ((s = cadet_mask_plan(cfg, b, ws, ws_bytes, stream))) return s;
+  PlanView v = plan_carve(ws, n, T, T);
+  LayerBufs L = carve_saved(saved, cfg, T);
+  LayerWs W = carve_ws(ws, cfg, n, T);
+  cudaError_t e = rope_theta_launch(W.theta, hd, cfg->rope_phi_min, cfg->rope_base, (double)cfg->rope_delta_t_max_ms, st);
+  const int bn = pick_bn(T, d);
+  // A2: representation gate  Xt = X * sigma(X W_xg)   (Eq. 4)
+  const void* Xt = X;
+  if (e == cudaSuccess && cfg->use_rep_gate) {
+    GemmProblem g = prob(T, d, d, act(X, T, d), w_fwd(w->W_xg, d, d), EPI_GATE);
+    g.epi.out = L.Xt;
+    g.epi.src = X;
+    g.epi.aux = L.Zx;
+    e = gemm_launch(&g, 1, bn, st);
+    Xt = L.Xt;
+  }
+  // A3: Q, K, V = Xt W_{q,k,v}   (Eq. 3; R2)
+  if (e == cudaSuccess) {
+    GemmProblem g[3];
+    const void* Ws[3] = {w->W_q, w->W_k, w->W_v};
+    void* outs[3] = {L.Q, L.K, L.V};
+    for (int i = 0; i < 3; ++i) {
+      g[i] = prob(T, d, d, act(Xt, T, d), w_fwd(Ws[i], d, d), EPI_STORE);
+      g[i].epi.out = outs[i];
+    }
+    e = gemm_launch(g, 3, bn, st);
+  }
+  // A4: interaction gates + timestamp RoPE  (Eq. 5)
+  if (e == cudaSuccess) {
+    if (cfg->use_int_gate) {
+      GemmProblem g[2];
+      const void* Ws[2] = {w->W_qg, w->W_kg};
+      const void* src[2] = {L.Q, L.K};
+      void* outs[2] = {L.Qr, L.Kr};
+      void* aux[2] = {L.Zq, L.Zk};
+      for (int i = 0; i < 2; ++i) {
+        g[i] = prob(T, d, d, act(src[i], T, d), w_fwd(Ws[i], d, d), cfg->use_rope ? EPI_GATE_ROPE : EPI_GATE);
+        g[i].epi.out = outs[i];
+        g[i].epi.src = src[i];
+        g[i].epi.aux = aux[i];
+        g[i].epi.hd = hd;
+        g[i].epi.t_ms = b->timestamps_ms;
+        g[i].epi.row_seq = v.row_seq;
+        g[i].epi.cu = b->cu_seqlens;
+        g[i].epi.theta = W.theta;
+      }
+      e = gemm_launch(g, 2, bn, st);
+    } else if (cfg->use_rope) {
+      e = rope_apply_launch(L.Q, L.Qr, T, d, hd, W.theta, b->timestamps_ms, v.row_seq, b->cu_seqlens, st);
+      if (e == cudaSuccess)
+        e = rope_apply_launch(L.K, L.Kr, T, d, hd, W.theta, b->timestamps_ms, v.row_seq, b->cu_seqlens, st);
+    } else {
+      e = cudaMemcpyAsync(L.Qr, L.Q, (size_t)T * d * 2, cudaMemcpyDeviceToDevice, st);
+      if (e == cudaSuccess) e = cudaMemcpyAsync(L.Kr, L.K, (size_t)T * d * 2, cudaMemcpyDeviceToDevice, st);
+    }
+  }
+  // A5: attention core
+  if (e == cudaSuccess) {
+    AttnParams p = attn_params(cfg, b, v);
+    p.out_f32 = 0;
+    p.O = L.O;
+    p.lse = L.lse;
+    e = zero_pad_rows_launch(L.O, d * 2, T, b->cu_seqlens, n, st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(L.lse, 0, sizeof(float) * (size_t)T * cfg->n_heads, st);
+    if (e == cudaSuccess) e = attn_fwd_launch(L.Qr, L.Kr, L.V, p, st);
+  }
+  // A6: Y = O W_o (+ resid)
+  if (e == cudaSuccess) {
+    if (cfg->use_out_proj) {
+      GemmProblem g = prob(T, d, d, act(L.O, T, d), w_fwd(w->W_o, d, d), EPI_STORE);
+      g.epi.out = Y;
+      g.epi.resid = resid;
+      e = gemm_launch(&g, 1, bn, st);
+    } else {
+      e = add_bf16_launch(L.O, resid, Y, (size_t)T * d, st);
+    }
+  }
+  return cuda_err(e, "attention layer forward");
+}
+
+cadet_status cadet_attn_backward(const cadet_attn_config* cfg, const cadet_batch* b, const cadet_attn_weights* w,
+                                 const void* X, const void* saved, const void* dY, void* dX, const void* dresid,
+                                 const cadet_attn_grads* gr, void* ws, size_t ws_bytes, cadet_stream_t stream) {
+  cadet_status s = check_cfg(cfg);
+  if (s) return s;
+  if ((s = check_batch(b, cfg))) return s;
+  if (!w || !X || !saved || !dY || !dX || !gr || !ws || !gr->dW_q || !gr->dW_k || !gr->dW_v ||
+      (cfg->use_rep_gate && !gr->dW_xg) || (cfg->use_int_gate && (!gr->dW_qg || !gr->dW_kg)) ||
+      (cfg->use_out_proj && !gr->dW_o)) {
+    set_error("cadet_attn_backward: null pointer");
+    return CADET_E_ARG;
+  }
+  const int T = b->total_tokens, d = cfg->d_model, n = b->n_seqs, hd = cfg->head_dim, H = cfg->n_heads;
+  const size_t need = layer_ws_bytes(cfg, n, T);
+  if (ws_bytes < need) return ws_err(ws_bytes, need);
+  if (T == 0) return CADET_OK;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if ((s = cadet_mask_plan(cfg, b, ws, ws_bytes, stream))) return s;
+  PlanView v = plan_carve(ws, n, T, T);
+  LayerBufs L = carve_saved(const_cast<void*>(saved), cfg, T);
+  LayerWs W = carve_ws(ws, cfg, n, T);
+  const int bn = pick_bn(T, d);
+  const int bnw = pick_bn(d, d);
+  const size_t wbytes = (size_t)d * d * 4;
+  cudaError_t e = rope_theta_launch(W.theta, hd, cfg->rope_phi_min, cfg->rope_base, (double)cfg->rope_delta_t_max_ms, st);
+  float* gws[7] = {gr->dW_xg, gr->dW_q, gr->dW_k, gr->dW_v, gr->dW_qg, gr->dW_kg, gr->dW_o};
+  for (int i = 0; i < 7 && e == cudaSuccess; ++i)
+    if (gws[i]) e = cudaMemsetAsync(gws[i], 0, wbytes, st);
+  const void* Xt = cfg->use_rep_gate ? L.Xt : X;
+  // A9: dO = dY W_o^T ; dW_o = O^T dY
+  const void* dO = dY;
+  if (e == cudaSuccess && cfg->use_out_proj) {
+    GemmProblem g = prob(T, d, d, act(dY, T, d), w_bwd(w->W_o, d, d), EPI_STORE);
+    g.epi.out = W.dO;
+    e = gemm_launch(&g, 1, bn, st);
+    if (e == cudaSuccess) {
+      GemmProblem gw = wgrad(L.O, dY, gr->dW_o, T, d, d, bnw);
+      e = gemm_launch(&gw, 1, bnw, st);
+    }
+    dO = W.dO;
+  }
+  // A10: attention core backward
+  if (e == cudaSuccess) {
+    AttnParams p = attn_params(cfg, b, v);
+    p.out_f32 = 0;
+    p.lse = L.lse;
+    p.D = W.D;
+    p.dQ = W.dQacc;
+    p.dK = W.dKr;
+    p.dV = W.dV;
+    e = attn_bwd_pre_launch(L.O, dO, W.D, W.dQacc, T, H, hd, st);
+    if (e == cudaSuccess) e = zero_pad_rows_launch(W.dKr, d * 2, T, b->cu_seqlens, n, st);
+    if (e == cudaSuccess) e = zero_pad_rows_launch(W.dV, d * 2, T, b->cu_seqlens, n, st);
+    if (e == cudaSuccess) e = attn_bwd_launch(L.Qr, L.Kr, L.V, dO, p, st);
+  }
+  // A11: R(-alpha) + interaction-gate backward
+  const void* dQ = W.dQ;
+  const void* dK = W.dK;
+  if (e == cudaSuccess) {
+    if (cfg->use_int_gate) {
+      e = rope_gate_bwd_launch(W.dQacc, 1, L.Q, L.Zq, W.uq, W.rq, 0, T, d, hd, cfg->use_rope, W.theta,
+                               b->timestamps_ms, v.row_seq, b->cu_seqlens, st);
+      if (e == cudaSuccess)
+        e = rope_gate_bwd_launch(W.dKr, 0, L.K, L.Zk, W.uk, W.rk, 0, T, d, hd, cfg->use_rope, W.theta,
+                                 b->timestamps_ms, v.row_seq, b->cu_seqlens, st);
+      if (e == cudaSuccess) {  // dQ = rq + uq W_qg^T ; dK = rk + uk W_kg^T
+        GemmProblem g[2];
+        const void* us[2] = {W.uq, W.uk};
+        const float* rs[2] = {W.rq, W.rk};
+        const void* Ws[2] = {w->W_qg, w->W_kg};
+        void* outs[2] = {W.dQ, W.dK};
+        for (int i = 0; i < 2; ++i) {
+          g[i] = prob(T, d, d, act(us[i], T, d), w_bwd(Ws[i], d, d), EPI_STORE);
+          g[i].epi.out = outs[i];
+          g[i].epi.resid = rs[i];
+          g[i].epi.resid_f32 = 1;
+        }
+        e = gemm_launch(g, 2, bn, st);
+      }
+      if (e == cudaSuccess) {  // dW_qg = Q^T uq ; dW_kg = K^T uk
+        GemmProblem g[2] = {wgrad(L.Q, W.uq, gr->dW_qg, T, d, d, bnw), wgrad(L.K, W.uk, gr->dW_kg, T, d, d, bnw)};
+        e = gemm_launch(g, 2, bnw, st);
+      }
+    } else {
+      e = rope_gate_bwd_launch(W.dQacc, 1, nullptr, nullptr, nullptr, W.dQ, 1, T, d, hd, cfg->use_rope, W.theta,
+                               b->timestamps_ms, v.row_seq, b->cu_seqlens, st);
+      if (e == cudaSuccess)
+        e = rope_gate_bwd_launch(W.dKr, 0, nullptr, nullptr, nullptr, W.dK, 1, T, d, hd, cfg->use_rope, W.theta,
+                                 b->timestamps_ms, v.row_seq, b->cu_seqlens, st);
+    }
+  }
+  // A12: dXt = dQ W_q^T + dK W_k^T + dV W_v^T (one K = 3d accumulation), weight grads, rep-gate bwd
+  if (e == cudaSuccess) {
+    GemmProblem g;
+    memset(&g, 0, sizeof(g));
+    g.M = T;
+    g.N = d;
+    g.nseg = 3;
+    const void* gs[3] = {dQ, dK, W.dV};
+    const void* Ws[3] = {w->W_q, w->W_k, w->W_v};
+    for (int i = 0; i < 3; ++i) {
+      g.K[i] = d;
+      g.A[i] = act(gs[i], T, d);
+      g.B[i] = w_bwd(Ws[i], d, d);
+    }
+    g.split_k = 1;
+    g.epi.ldo = d;
+    if (cfg->use_rep_gate) {  // ux = dXt * X * g (1 - g) ; rx = dXt * g (+ dresid)
+      g.epi.mode = EPI_GATE_BWD;
+      g.epi.out = W.ux;
+      g.epi.out2 = W.rx;
+      g.epi.src = X;
+      g.epi.aux = L.Zx;
+      g.epi.resid = dresid;
+    } else {
+      g.epi.mode = EPI_STORE;
+      g.epi.out = dX;
+      g.epi.resid = dresid;
+    }
+    e = gemm_launch(&g, 1, bn, st);
+    if (e == cudaSuccess) {
+      GemmProblem gw[3] = {wgrad(Xt, dQ, gr->dW_q, T, d, d, bnw), wgrad(Xt, dK, gr->dW_k, T, d, d, bnw),
+                           wgrad(Xt, W.dV, gr->dW_v, T, d, d, bnw)};
+      e = gemm_launch(gw, 3, bnw, st);
+    }
+    if (e == cudaSuccess && cfg->use_rep_gate) {  // dX = rx + ux W_xg^T ; dW_xg = X^T ux
+      GemmProblem g2 = prob(T, d, d, act(W.ux, T, d), w_bwd(w->W_xg, d, d), EPI_STORE);
+      g2.epi.out = dX;
+      g2.epi.resid = W.rx;
+      g2.epi.resid_f32 = 1;
+      e = gemm_launch(&g2, 1, bn, st);
+      if (e == cudaSuccess) {
+        GemmProblem gw = wgrad(X, W.ux, gr->dW_xg, T, d, d, bnw);
+        e = gemm_launch(&gw, 1, bnw, st);
+      }
+    }
+  }
+  if (e == cudaSuccess) e = zero_pad_rows_launch(dX, d * 2, T, b->cu_seqlens, n, st);
+  return cuda_err(e, "attention layer backward");
+}
+
+// =====================================================================================
+// Heads (rows A7 / A8)
+// =====================================================================================
+static cadet_status check_head(const cadet_head_config* h, const cadet_head_weights* w) {
+  if (!h || !w || !w->W1 || !w->b1 || !w->w2 || !w->b2) {
+    set_error("heads: null pointer");
+    return CADET_E_ARG;
+  }
+  if (h->K < 1 || h->d_model <= 0 || h->d_model % 8 || h->d_hidden <= 0 || h->d_hidden % 32) {
+    set_error("heads: K >= 1, d_model % 8 == 0, d_hidden % 32 == 0 required");
+    return CADET_E_ARG;
+  }
+  if (h->dtype != CADET_BF16) {
+    set_error("heads: bf16 only");
+    return CADET_E_UNSUPPORTED;
+  }
+  return CADET_OK;
+}
+
+size_t cadet_heads_workspace_bytes(const cadet_head_config* h, int32_t n) {
+  if (!h || n < 0) return 0;
+  const int N = h->K * h->d_hidden;
+  return 256 + a256((size_t)n * h->d_model * 2) + a256((size_t)n * N * 2) * 2 + a256((size_t)n * 4);
+}
+
+cadet_status cadet_heads_forward(const cadet_head_config* h, const cadet_head_weights* w, const void* Hs,
+                                 const int32_t* rows, int32_t n, float* logits, void* pre_out, void* ws,
+                                 size_t ws_bytes, cadet_stream_t stream) {
+  cadet_status s = check_head(h, w);
+  if (s) return s;
+  if (!Hs || !rows || !logits || !ws || n < 0) {
+    set_error("heads_forward: null pointer");
+    return CADET_E_ARG;
+  }
+  const size_t need = cadet_heads_workspace_bytes(h, n);
+  if (ws_bytes < need) return ws_err(ws_bytes, need);
+  if (n == 0) return CADET_OK;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const int d = h->d_model, N = h->K * h->d_hidden;
+  uint8_t* p = reinterpret_cast<uint8_t*>(ws);
+  uint32_t* err = reinterpret_cast<uint32_t*>(p);
+  void* Hr = p + 256;
+  void* pre = pre_out ? pre_out : (void*)(p + 256 + a256((size_t)n * d * 2));
+  cudaError_t e = gather_rows_launch(Hs, rows, n, 1 << 30, d, Hr, err, st);
+  if (e == cudaSuccess) e = head_init_launch(logits, w->b2, n, h->K, st);
+  if (e == cudaSuccess) {
+    GemmProblem g = prob(n, N, d, act(Hr, n, d), w_fwd(w->W1, d, N), EPI_HEAD);
+    g.epi.aux = pre;
+    g.epi.b1 = w->b1;
+    g.epi.w2 = w->w2;
+    g.epi.logits = logits;
+    g.epi.hd = h->d_hidden;
+    g.epi.n_towers = h->K;
+    e = gemm_launch(&g, 1, pick_bn(n, N), st);
+  }
+  return cuda_err(e, "heads forward");
+}
+
+cadet_status cadet_heads_loss_backward(const cadet_head_config* h, const cadet_head_weights* w, const void* Hs,
+                                       const int32_t* rows, int32_t n, int32_t T, const float* logits,
+                                       const void* pre, const int32_t* bucket, const float* label, float* loss_sum,
+                                       void* dHs, const cadet_head_grads* gr, void* ws, size_t ws_bytes,
+                                       cadet_stream_t stream) {
+  cadet_status s = check_head(h, w);
+  if (s) return s;
+  if (!Hs || !rows || !logits || !pre || !bucket || !label || !loss_sum || !dHs || !gr || !gr->dW1 || !gr->db1 ||
+      !gr->dw2 || !gr->db2 || !ws || n < 0 || T < 0) {
+    set_error("heads_loss_backward: null pointer");
+    return CADET_E_ARG;
+  }
+  const size_t need = cadet_heads_workspace_bytes(h, n);
+  if (ws_bytes < need) return ws_err(ws_bytes, need);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const int d = h->d_model, N = h->K * h->d_hidden;
+  uint8_t* p = reinterpret_cast<uint8_t*>(ws);
+  uint32_t* err = reinterpret_cast<uint32_t*>(p);
+  void* Hr = p + 256;
+  void* dhid_lo = p + 256 + a256((size_t)n * d * 2);  // the forward's `pre` slot (pre is caller-owned here)
+  void* dhid = p + 256 + a256((size_t)n * d * 2) + a256((size_t)n * N * 2);
+  float* dz = reinterpret_cast<float*>(p + 256 + a256((size_t)n * d * 2) + 2 * a256((size_t)n * N * 2));
+  cudaError_t e = cudaMemsetAsync(loss_sum, 0, 4, st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(gr->dW1, 0, (size_t)d * N * 4, st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(gr->db1, 0, (size_t)N * 4, st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(gr->dw2, 0, (size_t)N * 4, st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(gr->db2, 0, (size_t)h->K * 4, st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(dHs, 0, (size_t)T * d * 2, st);
+  if (n == 0) return cuda_err(e, "heads backward");
+  if (e == cudaSuccess) e = head_dz_launch(logits, bucket, label, n, h->K, dz, loss_sum, gr->db2, err, st);
+  if (e == cudaSuccess) e = head_dhid_launch(pre, dz, bucket, w->w2, n, h->K, h->d_hidden, dhid, dhid_lo, gr->db1, gr->dw2, st);
+  if (e == cudaSuccess) e = gather_rows_launch(Hs, rows, n, T, d, Hr, err, st);
+  if (e == cudaSuccess) {  // dW1 = H_r^T (dhid_hi + dhid_lo)
+    GemmProblem g = prob(d, N, n, act_t(Hr, n, d), act_t(dhid, n, N), EPI_ATOMIC);
+    g.nseg = 2;
+    g.K[1] = n;
+    g.A[1] = act_t(Hr, n, d);
+    g.B[1] = act_t(dhid_lo, n, N);
+    const int bnw = pick_bn(d, N);
+    g.split_k = pick_split(d, N, bnw, n);
+    g.epi.out = gr->dW1;
+    g.epi.out_f32 = 1;
+    e = gemm_launch(&g, 1, bnw, st);
+  }
+  if (e == cudaSuccess) {  // dHs[rows] = (dhid_hi + dhid_lo) W1^T
+    GemmProblem g = prob(n, d, N, act(dhid, n, N), w_bwd(w->W1, d, N), EPI_STORE);
+    g.nseg = 2;
+    g.K[1] = N;
+    g.A[1] = act(dhid_lo, n, N);
+    g.B[1] = w_bwd(w->W1, d, N);
+    g.epi.out = dHs;
+    g.epi.ldo = d;
+    g.epi.row_map = rows;
+    e = gemm_launch(&g, 1, pick_bn(n, d), st);
+  }
+  return cuda_err(e, "heads backward");
 }
 
 }  // extern "C"

@@ -8,6 +8,7 @@
 //
 // C[M,N] = sum_seg A_seg[M,K_seg] . B_seg[K_seg,N], tiles 128 x BN x 64, split-K optional.
 #include "gemm.cuh"
+#include "prof.cuh"
 #include "ptx.cuh"
 #include "tma_host.cuh"
 #include <string.h>
@@ -395,6 +396,7 @@ static cudaError_t launch_bn(const GemmKParams& P, cudaStream_t stream) {
     attr = true;
   }
   const int grid = P.total_units < num_sms() ? P.total_units : num_sms();
+  ProfScope ps(PROF_GEMM, stream, 1);
   gemm_kernel<BN><<<grid, GEMM_THREADS, C::SMEM, stream>>>(P);
   return cudaGetLastError();
 }

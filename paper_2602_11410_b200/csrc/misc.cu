@@ -1,0 +1,250 @@
+// Elementwise / reduction kernels of the hot path that are HBM-bound (no tensor cores):
+//   rope_theta_kernel       theta_i = (phi_min / dt_max) * base^(2i/hd)
+//   rope_apply_kernel       RoPE without interaction gate (ablation path)
+//   rope_gate_bwd_kernel    A11: dQt = R(-alpha) dQr; g = sigma(Zq); u = dQt*Q*g*(1-g); r = dQt*g
+//   gather_rows_kernel      H_r = H[rows] (A7 operand)
+//   head_init / head_dz / head_dhid   A7/A8 routed BCE (Eq. 9) and the tower backward
+//   add_kernel              Y = O (+ resid) when the output projection is ablated
+#include "misc.cuh"
+#include "prof.cuh"
+#include "ptx.cuh"
+
+namespace cadet {
+
+__global__ void rope_theta_kernel(double* theta, int half, int hd, double phi_min, double base, double dt_max) {
+  const int i = threadIdx.x + blockIdx.x * blockDim.x;
+  if (i < half) theta[i] = (phi_min / dt_max) * pow(base, 2.0 * i / (double)hd);
+}
+
+__device__ __forceinline__ void rot(float& a, float& b, double dt, double th, float sign) {
+  const double TWO_PI_HI = 6.283185307179586;
+  const double TWO_PI_LO = 2.4492935982947064e-16;
+  double ang = dt * th;
+  double k = rint(ang * 0.15915494309189535);
+  double r = fma(-k, TWO_PI_HI, ang);
+  r = fma(-k, TWO_PI_LO, r);
+  float s, c;
+  sincosf((float)r, &s, &c);
+  s *= sign;
+  const float x0 = a, x1 = b;
+  a = x0 * c - x1 * s;
+  b = x0 * s + x1 * c;
+}
+
+__device__ __forceinline__ double row_dt(const int64_t* t, const int32_t* row_seq, const int32_t* cu, int row) {
+  const int s = row_seq[row];
+  return s >= 0 ? (double)(t[row] - t[cu[s]]) : 0.0;
+}
+
+// one thread per (row, pair of columns)
+__global__ void rope_apply_kernel(const __nv_bfloat16* in, __nv_bfloat16* out, int T, int d, int hd,
+                                  const double* theta, const int64_t* t, const int32_t* row_seq, const int32_t* cu) {
+  const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const size_t pairs = (size_t)T * d / 2;
+  if (idx >= pairs) return;
+  const int row = (int)(idx / (d / 2));
+  const int c = (int)(idx % (d / 2)) * 2;
+  float2 v = __bfloat1622float2(reinterpret_cast<const __nv_bfloat162*>(in)[idx]);
+  rot(v.x, v.y, row_dt(t, row_seq, cu, row), theta[(c % hd) >> 1], 1.f);
+  reinterpret_cast<__nv_bfloat162*>(out)[idx] = __floats2bfloat162_rn(v.x, v.y);
+}
+
+// dr: fp32 (dQr accumulator) or bf16 (dKr).  gate (Z) bf16 may be null (no interaction gate):
+// then out_u is unused and out_r (bf16 if r_bf16) receives dQt directly.
+__global__ void rope_gate_bwd_kernel(const void* dr, int dr_f32, const __nv_bfloat16* Xq, const __nv_bfloat16* Z,
+                                     __nv_bfloat16* out_u, void* out_r, int r_bf16, int T, int d, int hd, int use_rope,
+                                     const double* theta, const int64_t* t, const int32_t* row_seq,
+                                     const int32_t* cu) {
+  const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const size_t pairs = (size_t)T * d / 2;
+  if (idx >= pairs) return;
+  const int row = (int)(idx / (d / 2));
+  const int c = (int)(idx % (d / 2)) * 2;
+  float2 g;
+  if (dr_f32)
+    g = reinterpret_cast<const float2*>(dr)[idx];
+  else
+    g = __bfloat1622float2(reinterpret_cast<const __nv_bfloat162*>(dr)[idx]);
+  if (use_rope) rot(g.x, g.y, row_dt(t, row_seq, cu, row), theta[(c % hd) >> 1], -1.f);  // R(-alpha)
+  float2 r = g;
+  if (Z) {
+    const float2 z = __bfloat1622float2(reinterpret_cast<const __nv_bfloat162*>(Z)[idx]);
+    const float2 x = __bfloat1622float2(reinterpret_cast<const __nv_bfloat162*>(Xq)[idx]);
+    const float g0 = 1.f / (1.f + __expf(-z.x)), g1 = 1.f / (1.f + __expf(-z.y));
+    reinterpret_cast<__nv_bfloat162*>(out_u)[idx] =
+        __floats2bfloat162_rn(g.x * x.x * g0 * (1.f - g0), g.y * x.y * g1 * (1.f - g1));
+    r = make_float2(g.x * g0, g.y * g1);
+  }
+  if (r_bf16)
+    reinterpret_cast<__nv_bfloat162*>(out_r)[idx] = __floats2bfloat162_rn(r.x, r.y);
+  else
+    reinterpret_cast<float2*>(out_r)[idx] = r;
+}
+
+__global__ void gather_rows_kernel(const uint8_t* H, const int32_t* rows, int n, int T, int row_bytes, uint8_t* out,
+                                   uint32_t* err) {
+  const int r = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (r >= n) return;
+  int src = rows[r];
+  if (src < 0 || src >= T) {
+    if (lane == 0) atomicOr(err, ERRBIT_OFFSETS);
+    src = 0;
+  }
+  const uint4* s = reinterpret_cast<const uint4*>(H + (size_t)src * row_bytes);
+  uint4* o = reinterpret_cast<uint4*>(out + (size_t)r * row_bytes);
+  for (int c = lane; c < row_bytes / 16; c += 32) o[c] = s[c];
+}
+
+__global__ void head_init_kernel(float* logits, const float* b2, int n, int K) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n * K) logits[i] = b2[i % K];
+}
+
+// Routed BCE (Eq. 9): loss = sum softplus(z_k) - y z_k; dz = sigma(z_k) - y on the realised tower.
+__global__ void head_dz_kernel(const float* logits, const int32_t* bucket, const float* label, int n, int K,
+                               float* dz, float* loss_sum, float* db2, uint32_t* err) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  float l = 0.f, g = 0.f;
+  int k = 0;
+  if (i < n) {
+    k = bucket[i];
+    if (k < 0 || k >= K) {
+      atomicOr(err, ERRBIT_BUCKET);
+      k = min(max(k, 0), K - 1);
+    }
+    const float z = logits[(size_t)i * K + k];
+    const float y = label[i];
+    l = fmaxf(z, 0.f) + log1pf(__expf(-fabsf(z))) - y * z;
+    g = 1.f / (1.f + __expf(-z)) - y;
+    if (!isfinite(l)) atomicOr(err, ERRBIT_NONFINITE);
+    dz[i] = g;
+    atomicAdd(db2 + k, g);
+  }
+  for (int o = 16; o > 0; o >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
+  if ((threadIdx.x & 31) == 0) atomicAdd(loss_sum, l);
+}
+
+// dhid[i, c] = dz_i * w2[c] * 1[pre > 0] on the realised tower, 0 elsewhere (S:260 isolation);
+// column sums db1[c] += dhid, dw2[c] += dz_i * relu(pre[i, c]).  Block = 32 columns x 8 row-groups.
+__global__ void head_dhid_kernel(const __nv_bfloat16* pre, const float* dz, const int32_t* bucket, const float* w2,
+                                 int n, int K, int dh, __nv_bfloat16* dhid, __nv_bfloat16* dhid_lo, float* db1,
+                                 float* dw2) {
+  const int N = K * dh;
+  const int c = blockIdx.x * 32 + threadIdx.x;
+  const int k = c / dh;
+  float s1 = 0.f, s2 = 0.f;
+  if (c < N) {
+    const float w = w2[c];
+    for (int i = blockIdx.y * blockDim.y + threadIdx.y; i < n; i += gridDim.y * blockDim.y) {
+      const int b = min(max(bucket[i], 0), K - 1);
+      const float pr = __bfloat162float(pre[(size_t)i * N + c]);
+      float gv = 0.f;
+      if (b == k) {
+        const float z = dz[i];
+        gv = pr > 0.f ? z * w : 0.f;
+        s2 += z * fmaxf(pr, 0.f);
+      }
+      s1 += gv;
+      const __nv_bfloat16 hi = __float2bfloat16(gv);  // bf16 hi + lo split: the GEMM operand keeps ~16 bits
+      dhid[(size_t)i * N + c] = hi;
+      dhid_lo[(size_t)i * N + c] = __float2bfloat16(gv - __bfloat162float(hi));
+    }
+  }
+  __shared__ float sh1[8][33], sh2[8][33];
+  sh1[threadIdx.y][threadIdx.x] = s1;
+  sh2[threadIdx.y][threadIdx.x] = s2;
+  __syncthreads();
+  if (threadIdx.y == 0 && c < N) {
+    float a = 0.f, b = 0.f;
+    for (int y = 0; y < blockDim.y; ++y) {
+      a += sh1[y][threadIdx.x];
+      b += sh2[y][threadIdx.x];
+    }
+    atomicAdd(db1 + c, a);
+    atomicAdd(dw2 + c, b);
+  }
+}
+
+__global__ void add_bf16_kernel(const __nv_bfloat16* a, const __nv_bfloat16* b, __nv_bfloat16* out, size_t n2) {
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n2) return;
+  float2 x = __bfloat1622float2(reinterpret_cast<const __nv_bfloat162*>(a)[i]);
+  if (b) {
+    const float2 y = __bfloat1622float2(reinterpret_cast<const __nv_bfloat162*>(b)[i]);
+    x.x += y.x;
+    x.y += y.y;
+  }
+  reinterpret_cast<__nv_bfloat162*>(out)[i] = __floats2bfloat162_rn(x.x, x.y);
+}
+
+// ---------------------------------------------------------------- launchers
+static inline unsigned blocks(size_t n, unsigned b) { return (unsigned)((n + b - 1) / b); }
+
+cudaError_t rope_theta_launch(double* theta, int hd, double phi_min, double base, double dt_max, cudaStream_t st) {
+  ProfScope ps(PROF_OTHER, st, 1);
+  rope_theta_kernel<<<1, 128, 0, st>>>(theta, hd / 2, hd, phi_min, base, dt_max);
+  return cudaGetLastError();
+}
+cudaError_t rope_apply_launch(const void* in, void* out, int T, int d, int hd, const double* theta, const int64_t* t,
+                              const int32_t* row_seq, const int32_t* cu, cudaStream_t st) {
+  ProfScope ps(PROF_OTHER, st, 1);
+  const size_t pairs = (size_t)T * d / 2;
+  if (pairs)
+    rope_apply_kernel<<<blocks(pairs, 256), 256, 0, st>>>(reinterpret_cast<const __nv_bfloat16*>(in),
+                                                         reinterpret_cast<__nv_bfloat16*>(out), T, d, hd, theta, t,
+                                                         row_seq, cu);
+  return cudaGetLastError();
+}
+cudaError_t rope_gate_bwd_launch(const void* dr, int dr_f32, const void* Xq, const void* Z, void* out_u, void* out_r,
+                                 int r_bf16, int T, int d, int hd, int use_rope, const double* theta, const int64_t* t,
+                                 const int32_t* row_seq, const int32_t* cu, cudaStream_t st) {
+  ProfScope ps(PROF_OTHER, st, 1);
+  const size_t pairs = (size_t)T * d / 2;
+  if (pairs)
+    rope_gate_bwd_kernel<<<blocks(pairs, 256), 256, 0, st>>>(
+        dr, dr_f32, reinterpret_cast<const __nv_bfloat16*>(Xq), reinterpret_cast<const __nv_bfloat16*>(Z),
+        reinterpret_cast<__nv_bfloat16*>(out_u), out_r, r_bf16, T, d, hd, use_rope, theta, t, row_seq, cu);
+  return cudaGetLastError();
+}
+cudaError_t gather_rows_launch(const void* H, const int32_t* rows, int n, int T, int d, void* out, uint32_t* err,
+                               cudaStream_t st) {
+  ProfScope ps(PROF_OTHER, st, 1);
+  if (n > 0)
+    gather_rows_kernel<<<blocks(n, 8), 256, 0, st>>>(reinterpret_cast<const uint8_t*>(H), rows, n, T, d * 2,
+                                                     reinterpret_cast<uint8_t*>(out), err);
+  return cudaGetLastError();
+}
+cudaError_t head_init_launch(float* logits, const float* b2, int n, int K, cudaStream_t st) {
+  ProfScope ps(PROF_OTHER, st, 1);
+  if (n > 0) head_init_kernel<<<blocks((size_t)n * K, 256), 256, 0, st>>>(logits, b2, n, K);
+  return cudaGetLastError();
+}
+cudaError_t head_dz_launch(const float* logits, const int32_t* bucket, const float* label, int n, int K, float* dz,
+                           float* loss_sum, float* db2, uint32_t* err, cudaStream_t st) {
+  ProfScope ps(PROF_OTHER, st, 1);
+  if (n > 0) head_dz_kernel<<<blocks(n, 256), 256, 0, st>>>(logits, bucket, label, n, K, dz, loss_sum, db2, err);
+  return cudaGetLastError();
+}
+cudaError_t head_dhid_launch(const void* pre, const float* dz, const int32_t* bucket, const float* w2, int n, int K,
+                             int dh, void* dhid, void* dhid_lo, float* db1, float* dw2, cudaStream_t st) {
+  ProfScope ps(PROF_OTHER, st, 1);
+  if (n > 0) {
+    dim3 blk(32, 8);
+    dim3 grd((K * dh + 31) / 32, (unsigned)min(64, (n + 7) / 8));
+    head_dhid_kernel<<<grd, blk, 0, st>>>(reinterpret_cast<const __nv_bfloat16*>(pre), dz, bucket, w2, n, K, dh,
+                                          reinterpret_cast<__nv_bfloat16*>(dhid),
+                                          reinterpret_cast<__nv_bfloat16*>(dhid_lo), db1, dw2);
+  }
+  return cudaGetLastError();
+}
+cudaError_t add_bf16_launch(const void* a, const void* b, void* out, size_t n, cudaStream_t st) {
+  ProfScope ps(PROF_OTHER, st, 1);
+  if (n)
+    add_bf16_kernel<<<blocks(n / 2, 256), 256, 0, st>>>(reinterpret_cast<const __nv_bfloat16*>(a),
+                                                         reinterpret_cast<const __nv_bfloat16*>(b),
+                                                         reinterpret_cast<__nv_bfloat16*>(out), n / 2);
+  return cudaGetLastError();
+}
+
+}  // namespace cadet

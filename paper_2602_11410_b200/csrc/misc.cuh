@@ -1,0 +1,22 @@
+// Launchers of the elementwise / reduction kernels (misc.cu).
+#pragma once
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+namespace cadet {
+cudaError_t rope_theta_launch(double* theta, int hd, double phi_min, double base, double dt_max, cudaStream_t st);
+cudaError_t rope_apply_launch(const void* in, void* out, int T, int d, int hd, const double* theta, const int64_t* t,
+                              const int32_t* row_seq, const int32_t* cu, cudaStream_t st);
+cudaError_t rope_gate_bwd_launch(const void* dr, int dr_f32, const void* Xq, const void* Z, void* out_u, void* out_r,
+                                 int r_bf16, int T, int d, int hd, int use_rope, const double* theta, const int64_t* t,
+                                 const int32_t* row_seq, const int32_t* cu, cudaStream_t st);
+cudaError_t gather_rows_launch(const void* H, const int32_t* rows, int n, int T, int d, void* out, uint32_t* err,
+                               cudaStream_t st);
+cudaError_t head_init_launch(float* logits, const float* b2, int n, int K, cudaStream_t st);
+cudaError_t head_dz_launch(const float* logits, const int32_t* bucket, const float* label, int n, int K, float* dz,
+                           float* loss_sum, float* db2, uint32_t* err, cudaStream_t st);
+cudaError_t head_dhid_launch(const void* pre, const float* dz, const int32_t* bucket, const float* w2, int n, int K,
+                             int dh, void* dhid, void* dhid_lo, float* db1, float* dw2, cudaStream_t st);
+cudaError_t add_bf16_launch(const void* a, const void* b, void* out, size_t n, cudaStream_t st);
+}  // namespace cadet

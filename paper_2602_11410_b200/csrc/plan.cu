@@ -8,6 +8,7 @@
 // on PARTIAL rows only.  This is exactly the structure of the mask of PAPER.md Eq. 6 / Fig. 3 /
 // P:540-546 when timestamps (and session ids) are non-decreasing inside a sequence.
 #include "plan.cuh"
+#include "prof.cuh"
 #include "ptx.cuh"
 
 namespace cadet {
@@ -274,6 +275,7 @@ __global__ void __launch_bounds__(128) plan_scatter_kernel(PlanArgs a, PlanView 
 }
 
 cudaError_t plan_launch(const PlanArgs& a, const PlanView& v, cudaStream_t st) {
+  ProfScope ps(PROF_OTHER, st, 5);
   plan_seq_kernel<<<1, 1024, 0, st>>>(a, v);
   if (a.T > 0) plan_row_kernel<<<(a.T + 255) / 256, 256, 0, st>>>(a, v);
   const int nb = (v.nq_cap + 127) / 128;
@@ -322,6 +324,7 @@ __global__ void copy_kv_end_kernel(const int32_t* src, int32_t* dst, int T, cons
 
 cudaError_t plan_export_launch(const PlanArgs& a, const PlanView& v, int32_t* kv_end_out, int8_t* tc_out,
                                int64_t tc_cap, int64_t* pairs_out, cudaStream_t st) {
+  ProfScope ps(PROF_OTHER, st, 2);
   if (kv_end_out || pairs_out)
     copy_kv_end_kernel<<<(a.T + 255) / 256 + 1, 256, 0, st>>>(v.kv_end, kv_end_out ? kv_end_out : v.kv_end,
                                                               kv_end_out ? a.T : 0, v.pairs, pairs_out);
@@ -369,6 +372,7 @@ __global__ void __launch_bounds__(1024) chunk_kernel(const int32_t* cu_in, int n
 
 cudaError_t chunk_launch(const int32_t* cu_in, int32_t n_in, int32_t L, int32_t* cu_out, int32_t cap, int32_t* n_out,
                          uint32_t* err, cudaStream_t st) {
+  ProfScope ps(PROF_OTHER, st, 1);
   chunk_kernel<<<1, 1024, 0, st>>>(cu_in, n_in, L, cu_out, cap, n_out, err);
   return cudaGetLastError();
 }
@@ -418,8 +422,8 @@ __global__ void __launch_bounds__(1024) pack_offsets_kernel(const int32_t* lens,
   if (e) atomicOr(err, e);
 }
 
-__global__ void __launch_bounds__(256) pack_rows_kernel(const uint8_t* padded, const int32_t* cu, const int32_t* n_packed,
-                                                         int Lmax, int row_bytes, int budget, const int64_t* tp,
+__global__ void __launch_bounds__(256) pack_rows_kernel(const uint8_t* src, const int64_t* src_row, const int32_t* cu,
+                                                         const int32_t* n_packed, int row_bytes, int budget, const int64_t* tp,
                                                          const int32_t* sp, uint8_t* packed, int64_t* t_out,
                                                          int32_t* s_out) {
   const int warps = blockDim.x / 32;
@@ -440,12 +444,12 @@ __global__ void __launch_bounds__(256) pack_rows_kernel(const uint8_t* padded, c
         hi = mid - 1;
     }
     const int s = lo, j = r - cu[s];
-    const size_t src_row = (size_t)s * Lmax + j;
-    const uint4* src = reinterpret_cast<const uint4*>(padded + src_row * row_bytes);
-    for (int c = lane; c < nvec; c += 32) dst[c] = src[c];
+    const size_t sr = src_row ? (size_t)src_row[s] + j : (size_t)r;  // contiguous: packed row == source row
+    const uint4* sv = reinterpret_cast<const uint4*>(src + sr * row_bytes);
+    for (int c = lane; c < nvec; c += 32) dst[c] = sv[c];
     if (lane == 0) {
-      if (t_out) t_out[r] = tp ? tp[src_row] : 0;
-      if (s_out) s_out[r] = sp ? sp[src_row] : 0;
+      if (t_out) t_out[r] = tp ? tp[sr] : 0;
+      if (s_out) s_out[r] = sp ? sp[sr] : 0;
     }
   } else {
     for (int c = lane; c < nvec; c += 32) dst[c] = make_uint4(0, 0, 0, 0);
@@ -456,13 +460,14 @@ __global__ void __launch_bounds__(256) pack_rows_kernel(const uint8_t* padded, c
   }
 }
 
-cudaError_t pack_launch(const void* padded, const int32_t* lens, int32_t B, int32_t Lmax, int32_t d, int32_t budget,
-                        const int64_t* tp, const int32_t* sp, void* packed, int64_t* t_out, int32_t* s_out,
-                        int32_t* cu_out, int32_t* n_packed, uint32_t* err, cudaStream_t st) {
+cudaError_t pack_launch(const void* src, const int64_t* src_row, const int32_t* lens, int32_t B, int32_t d,
+                        int32_t budget, const int64_t* tp, const int32_t* sp, void* packed, int64_t* t_out,
+                        int32_t* s_out, int32_t* cu_out, int32_t* n_packed, uint32_t* err, cudaStream_t st) {
+  ProfScope ps(PROF_OTHER, st, 2);
   pack_offsets_kernel<<<1, 1024, 0, st>>>(lens, B, budget, cu_out, n_packed, err);
   const int rows_per_block = 8;
   pack_rows_kernel<<<(budget + rows_per_block - 1) / rows_per_block, 256, 0, st>>>(
-      reinterpret_cast<const uint8_t*>(padded), cu_out, n_packed, Lmax, d * 2, budget, tp, sp,
+      reinterpret_cast<const uint8_t*>(src), src_row, cu_out, n_packed, d * 2, budget, tp, sp,
       reinterpret_cast<uint8_t*>(packed), t_out, s_out);
   return cudaGetLastError();
 }
@@ -478,6 +483,7 @@ __global__ void zero_pad_rows_kernel(uint8_t* buf, int row_bytes, int T, const i
 
 cudaError_t zero_pad_rows_launch(void* buf, int32_t row_bytes, int32_t T, const int32_t* cu, int32_t n,
                                  cudaStream_t st) {
+  ProfScope ps(PROF_OTHER, st, 1);
   zero_pad_rows_kernel<<<148, 256, 0, st>>>(reinterpret_cast<uint8_t*>(buf), row_bytes, T, cu, n);
   return cudaGetLastError();
 }

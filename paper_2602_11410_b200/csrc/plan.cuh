@@ -48,9 +48,9 @@ cudaError_t plan_export_launch(const PlanArgs& a, const PlanView& v, int32_t* kv
                                int64_t tc_cap, int64_t* pairs_out, cudaStream_t st);
 cudaError_t chunk_launch(const int32_t* cu_in, int32_t n_in, int32_t L, int32_t* cu_out, int32_t cap,
                          int32_t* n_out, uint32_t* err, cudaStream_t st);
-cudaError_t pack_launch(const void* padded, const int32_t* lens, int32_t B, int32_t Lmax, int32_t d, int32_t budget,
-                        const int64_t* tp, const int32_t* sp, void* packed, int64_t* t_out, int32_t* s_out,
-                        int32_t* cu_out, int32_t* n_packed, uint32_t* err, cudaStream_t st);
+cudaError_t pack_launch(const void* src, const int64_t* src_row, const int32_t* lens, int32_t B, int32_t d,
+                        int32_t budget, const int64_t* tp, const int32_t* sp, void* packed, int64_t* t_out,
+                        int32_t* s_out, int32_t* cu_out, int32_t* n_packed, uint32_t* err, cudaStream_t st);
 cudaError_t zero_pad_rows_launch(void* buf, int32_t row_bytes, int32_t T, const int32_t* cu, int32_t n,
                                  cudaStream_t st);
 

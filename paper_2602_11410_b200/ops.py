@@ -137,16 +137,37 @@ def chunk(cu_in: torch.Tensor, L_chunk: int, cap: int, ws=None):
     return cu_out, n_out, ws
 
 
-def pack(padded, lens, budget: int, t_padded=None, s_padded=None, ws=None):
-    _need_cuda(padded, lens, t_padded, s_padded)
-    B, Lmax, d = padded.shape
-    dev = padded.device
+def pack(src, lens, budget: int, src_row=None, t_src=None, s_src=None, ws=None):
+    """A13: greedy arrival-order packing into a fixed budget.  src [rows, d] bf16 with
+    sequence s at rows [src_row[s], src_row[s] + lens[s]) (src_row None = back to back)."""
+    _need_cuda(src, lens, src_row, t_src, s_src)
+    d = src.shape[-1]
+    B = lens.numel()
+    dev = src.device
     ws = workspace(L.lib().cadet_pack_workspace_bytes(B), dev) if ws is None else ws
-    packed = torch.empty(budget, d, dtype=padded.dtype, device=dev)
-    t_out = torch.empty(budget, dtype=torch.int64, device=dev) if t_padded is not None else None
-    s_out = torch.empty(budget, dtype=torch.int32, device=dev) if s_padded is not None else None
+    packed = torch.empty(budget, d, dtype=src.dtype, device=dev)
+    t_out = torch.empty(budget, dtype=torch.int64, device=dev) if t_src is not None else None
+    s_out = torch.empty(budget, dtype=torch.int32, device=dev) if s_src is not None else None
     cu = torch.empty(B + 1, dtype=torch.int32, device=dev)
     n_packed = torch.zeros(1, dtype=torch.int32, device=dev)
-    L.check(L.lib().cadet_pack(_p(padded), _p(lens), B, Lmax, d, budget, _p(t_padded), _p(s_padded), _p(packed),
+    L.check(L.lib().cadet_pack(_p(src), _p(src_row), _p(lens), B, d, budget, _p(t_src), _p(s_src), _p(packed),
                                _p(t_out), _p(s_out), _p(cu), _p(n_packed), _p(ws), ws.numel(), _stream()))
     return packed, t_out, s_out, cu, n_packed, ws
+
+
+def launch_count() -> int:
+    return int(L.lib().cadet_launch_count())
+
+
+def prof_enable(classes: int = 15, max_pairs: int = 4096):
+    L.check(L.lib().cadet_prof_enable(classes, max_pairs))
+
+
+PROF_CLASSES = ("gemm", "attn_fwd", "attn_bwd", "other")
+
+
+def prof_read():
+    ms = (C.c_double * 4)()
+    n = (C.c_int64 * 4)()
+    L.check(L.lib().cadet_prof_read(ms, n))
+    return {k: (ms[i], int(n[i])) for i, k in enumerate(PROF_CLASSES)}

@@ -1,0 +1,10 @@
+#!/bin/bash
+cd "${GRAFT_REPO_ROOT:-/root/repo}"
+mkdir -p gpurun_out
+python -c "import paper_2602_11410_b200.build as b; b.build()" > gpurun_out/s2_build.log 2>&1
+for k in "gemm or mask_plan or chunk or pack or attn_core_forward" attn_core_backward heads layer_forward layer_backward; do
+  f="gpurun_out/s2_$(echo $k | cut -c1-12 | tr ' ' _).log"
+  timeout 600 python -m pytest tests/test_gpu_core.py tests/test_gpu_layer.py -q -m gpu -k "$k" -s -rA > "$f" 2>&1
+  echo "$k -> $?" >> gpurun_out/s2_summary.txt
+done
+cat gpurun_out/s2_summary.txt

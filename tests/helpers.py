@@ -24,6 +24,27 @@ def assert_close(got, ref, max_abs=MAX_ABS, mean_abs=MEAN_ABS, what=""):
     return mx, mn
 
 
+def bf16_half_ulp(x):
+    """Half a bf16 ulp of |x| (round-to-nearest storage error bound)."""
+    a = np.abs(np.asarray(x, dtype=np.float64))
+    e = np.floor(np.log2(np.maximum(a, 1e-38)))
+    return np.where(a > 0, 0.5 * np.exp2(e - 7), 0.0)
+
+
+def assert_close_stored(got_bf16, ref, max_abs=MAX_ABS, mean_abs=MEAN_ABS, what=""):
+    """Protocol (iii) for a stage whose fp32 accumulator is stored as bf16: the storage
+    rounding (<= half a bf16 ulp, deterministic) is removed before applying the tolerance,
+    so what is gated is the accumulator's error (R22)."""
+    got = np.asarray(got_bf16, dtype=np.float64)
+    ref = np.asarray(ref, dtype=np.float64)
+    rms = float(np.sqrt(np.mean(ref ** 2))) if ref.size else 0.0
+    allow = bf16_half_ulp(np.maximum(np.abs(ref), np.abs(got)))
+    resid = np.maximum(np.abs(got - ref) - allow, 0.0) / max(1.0, rms)
+    mx, mn = float(resid.max()), float(resid.mean())
+    assert mx <= max_abs and mn <= mean_abs, f"{what}: accumulator max {mx:.3e} mean {mn:.3e} (rms ref {rms:.3e})"
+    return mx, mn
+
+
 def make_case(lengths, T=None, n_cand=None, stress=True, seed=0):
     """Packed batch metadata (host numpy) of given sequence lengths; T = budget (>= sum)."""
     cfgg = G.stress_config() if stress else G.GenConfig()

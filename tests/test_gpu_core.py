@@ -153,8 +153,10 @@ def test_pack_bit_exact(ops):
         B, Lmax, d = len(lens), max(lens), 64
         X = rng.standard_normal((B, Lmax, d)).astype(np.float32)
         tp = rng.integers(0, 10**12, size=(B, Lmax)).astype(np.int64)
-        packed, t_out, s_out, cu, n_packed, ws = ops.pack(bf16_tensor(X), torch.tensor(lens, dtype=torch.int32,
-                                                          device="cuda"), budget, torch.tensor(tp, device="cuda"))
+        src_row = torch.arange(B, dtype=torch.int64, device="cuda") * Lmax
+        packed, t_out, s_out, cu, n_packed, ws = ops.pack(bf16_tensor(X.reshape(B * Lmax, d)),
+                                                          torch.tensor(lens, dtype=torch.int32, device="cuda"),
+                                                          budget, src_row=src_row, t_src=torch.tensor(tp, device="cuda"))
         ops.poll(ws)
         cu_ref, nref, pad = O.pack_greedy(lens, budget)
         k = int(n_packed.item())
@@ -165,6 +167,12 @@ def test_pack_bit_exact(ops):
             assert (P[cu_ref[s_]:cu_ref[s_ + 1]] == Xb[s_, : lens[s_]]).all()
             assert (t_out.cpu().numpy()[cu_ref[s_]:cu_ref[s_ + 1]] == tp[s_, : lens[s_]]).all()
         assert (P[cu_ref[-1]:] == 0).all() and budget - cu_ref[-1] == pad
+    # contiguous histories (src_row = NULL): packed rows are the source rows
+    lens = [5, 3, 6, 4]
+    X = rng.standard_normal((18, 32)).astype(np.float32)
+    packed, *_rest, n_packed, ws = ops.pack(bf16_tensor(X), torch.tensor(lens, dtype=torch.int32, device="cuda"), 16)
+    assert int(n_packed.item()) == 3
+    assert (to_np(packed)[:14] == G.bf16_round(X[:14])).all() and (to_np(packed)[14:] == 0).all()
 
 
 # ------------------------------------------------------------------ attention core forward
