@@ -28,7 +28,7 @@ class AttnConfig(C.Structure):
     _fields_ = [("d_model", C.c_int32), ("n_heads", C.c_int32), ("head_dim", C.c_int32), ("dtype", C.c_int32),
                 ("mask_flags", C.c_int32), ("out_f32", C.c_int32), ("use_rope", C.c_int32),
                 ("use_rep_gate", C.c_int32), ("use_int_gate", C.c_int32), ("use_out_proj", C.c_int32),
-                ("deterministic", C.c_int32), ("reserved0", C.c_int32), ("delta_delay_ms", C.c_int64),
+                ("deterministic", C.c_int32), ("plan_ready", C.c_int32), ("delta_delay_ms", C.c_int64),
                 ("delta_cand_ms", C.c_int64), ("rope_delta_t_max_ms", C.c_int64), ("rope_phi_min", C.c_double),
                 ("rope_base", C.c_double)]
 

@@ -6,12 +6,13 @@
 // that are fully masked").  Per row, the mask predicate runs only when the row's visible
 // prefix does not cover the whole k-tile (PARTIAL rows); FULL rows skip it.
 //
-//   warp 0     : TMA producer: Q once, K/V tiles through a 2-stage ring (3-D [T][H][hd] maps)
-//   warp 1     : TMEM owner + tcgen05.mma issuer: S_j = Q K_j^T (TMEM, double-buffered),
-//                O += P_j V_j (TMEM accumulator, P_j from shared memory)
+//   warp 0     : TMA producer: Q once, then K_j / V_j (single-buffered, 3-D [T][H][hd] maps)
+//   warp 1     : TMEM owner + tcgen05.mma issuer: S_j = Q K_j^T into TMEM; O += P_j V_j with
+//                P_j read from TMEM (TS form: P overwrites the consumed S columns as packed bf16)
 //   warps 2..5 : softmax, thread = query row: tcgen05.ld S, mask, online softmax with
-//                conditional rescaling (threshold 2^8), P -> smem (bf16), O rescale in TMEM,
-//                final O / l and LSE.
+//                conditional rescaling (threshold 2^8), tcgen05.st P, O rescale, final O / l, LSE.
+// ~96 KB of shared memory and 256 TMEM columns per CTA, so two CTAs share an SM and one CTA's
+// softmax overlaps the other's MMAs (the role FA4's two softmax warpgroups play).
 #include "attn_common.cuh"
 #include "prof.cuh"
 
@@ -22,25 +23,23 @@ struct FwdCfg {
   using G = HeadGeom<HD>;
   static constexpr int Q_OFF = 0;
   static constexpr int K_OFF = Q_OFF + G::TILE_BYTES;
-  static constexpr int V_OFF = K_OFF + 2 * G::TILE_BYTES;
-  static constexpr int P_OFF = V_OFF + 2 * G::TILE_BYTES;
-  static constexpr int BAR_OFF = P_OFF + 32768;
-  static constexpr int USED = BAR_OFF + 256;
-  // >= 116 KB so that exactly one CTA (which owns all 512 TMEM columns) is resident per SM
-  static constexpr int SMEM = (USED + 1024 > 118784 ? USED + 1024 : 118784);
-  static constexpr int S_COL = 0;    // two 128-column S buffers
-  static constexpr int O_COL = 256;  // HDP columns
+  static constexpr int V_OFF = K_OFF + G::TILE_BYTES;
+  static constexpr int BAR_OFF = V_OFF + G::TILE_BYTES;
+  static constexpr int SMEM = BAR_OFF + 256 + 1024;
+  static constexpr int S_COL = 0;    // S (fp32, 128 columns); P (bf16 pairs) reuses columns [0, 64)
+  static constexpr int O_COL = 128;  // HDP fp32 columns
+  static constexpr uint32_t TMEM_COLS = 256;
 };
 
 struct FwdBars {
-  uint64_t q_full, k_full[2], k_empty[2], v_full[2], v_empty[2], s_full[2], s_free[2], p_full, pv_done;
+  uint64_t q_full, k_full, k_empty, v_full, v_empty, s_full, p_full, pv_done;
   uint32_t tmem_base;
 };
 
 __device__ __forceinline__ int visit_tile(const QTileInfo& qi, int j) { return j < qi.nf ? j : qi.kt2 + (j - qi.nf); }
 
 template <int HD>
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(192, 2)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constant__ CUtensorMap mK,
                     const __grid_constant__ CUtensorMap mV, const AttnParams p) {
   using G = HeadGeom<HD>;
@@ -62,19 +61,16 @@ __global__ void __launch_bounds__(192, 1)
 
   if (threadIdx.x == 0) {
     mbar_init(&bars->q_full, 1);
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&bars->k_full[i], 1);
-      mbar_init(&bars->k_empty[i], 1);
-      mbar_init(&bars->v_full[i], 1);
-      mbar_init(&bars->v_empty[i], 1);
-      mbar_init(&bars->s_full[i], 1);
-      mbar_init(&bars->s_free[i], 128);
-    }
+    mbar_init(&bars->k_full, 1);
+    mbar_init(&bars->k_empty, 1);
+    mbar_init(&bars->v_full, 1);
+    mbar_init(&bars->v_empty, 1);
+    mbar_init(&bars->s_full, 1);
     mbar_init(&bars->p_full, 128);
     mbar_init(&bars->pv_done, 1);
     fence_mbar_init();
   }
-  if (warp == 1) tmem_alloc<512>(&bars->tmem_base);
+  if (warp == 1) tmem_alloc<C::TMEM_COLS>(&bars->tmem_base);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -83,28 +79,22 @@ __global__ void __launch_bounds__(192, 1)
   if (warp == 0) {
     // ============================ producer
     if (elect_one()) {
-      tma_prefetch(&mQ);
-      tma_prefetch(&mK);
-      tma_prefetch(&mV);
       mbar_expect_tx(&bars->q_full, G::TILE_BYTES);
 #pragma unroll
       for (int blk = 0; blk < G::NB; ++blk)
         tma_load_3d(smem + C::Q_OFF + blk * G::BLK, &mQ, &bars->q_full, blk * G::CB, h, q0);
       for (int j = 0; j < n_kv; ++j) {
-        const int st = j & 1, use = j >> 1;
         const int krow = sa + visit_tile(qi, j) * 128;
-        if (use > 0) mbar_wait(&bars->k_empty[st], (use - 1) & 1);
-        mbar_expect_tx(&bars->k_full[st], G::TILE_BYTES);
+        if (j > 0) mbar_wait(&bars->k_empty, (j - 1) & 1);
+        mbar_expect_tx(&bars->k_full, G::TILE_BYTES);
 #pragma unroll
         for (int blk = 0; blk < G::NB; ++blk)
-          tma_load_3d(smem + C::K_OFF + st * G::TILE_BYTES + blk * G::BLK, &mK, &bars->k_full[st], blk * G::CB, h,
-                      krow);
-        if (use > 0) mbar_wait(&bars->v_empty[st], (use - 1) & 1);
-        mbar_expect_tx(&bars->v_full[st], G::TILE_BYTES);
+          tma_load_3d(smem + C::K_OFF + blk * G::BLK, &mK, &bars->k_full, blk * G::CB, h, krow);
+        if (j > 0) mbar_wait(&bars->v_empty, (j - 1) & 1);
+        mbar_expect_tx(&bars->v_full, G::TILE_BYTES);
 #pragma unroll
         for (int blk = 0; blk < G::NB; ++blk)
-          tma_load_3d(smem + C::V_OFF + st * G::TILE_BYTES + blk * G::BLK, &mV, &bars->v_full[st], blk * G::CB, h,
-                      krow);
+          tma_load_3d(smem + C::V_OFF + blk * G::BLK, &mV, &bars->v_full, blk * G::CB, h, krow);
       }
     }
   } else if (warp == 1) {
@@ -113,34 +103,27 @@ __global__ void __launch_bounds__(192, 1)
       const uint32_t idesc_s = idesc_bf16(128, 128, 0, 0);
       const uint32_t idesc_o = idesc_bf16(128, G::HDP, 0, 1);
       const uint32_t sQ = smem_u32(smem + C::Q_OFF);
-      const uint32_t sP = smem_u32(smem + C::P_OFF);
+      const uint32_t sK = smem_u32(smem + C::K_OFF);
+      const uint32_t sV = smem_u32(smem + C::V_OFF);
       mbar_wait(&bars->q_full, 0);
-      auto issue_s = [&](int j) {
-        const int st = j & 1, use = j >> 1;
-        if (use > 0) mbar_wait(&bars->s_free[st], (use - 1) & 1);
-        mbar_wait(&bars->k_full[st], use & 1);
+      for (int j = 0; j < n_kv; ++j) {
+        // S_j: the tensor pipe executes in issue order, so S_j overwrites P_{j-1} only after PV_{j-1}
+        // has read it; p_full(j-1) (waited below) guarantees the softmax finished with S_{j-1}.
+        mbar_wait(&bars->k_full, j & 1);
         tc_fence_after();
-        const uint32_t sK = smem_u32(smem + C::K_OFF + st * G::TILE_BYTES);
 #pragma unroll
         for (int kk = 0; kk < G::HDP / 16; ++kk)
-          mma_bf16_ss(tmem + C::S_COL + st * 128, kmajor_desc<HD>(sQ, kk), kmajor_desc<HD>(sK, kk), idesc_s,
-                      kk > 0 ? 1u : 0u);
-        mma_commit(&bars->k_empty[st]);
-        mma_commit(&bars->s_full[st]);
-      };
-      if (n_kv > 0) issue_s(0);
-      for (int j = 0; j < n_kv; ++j) {
-        if (j + 1 < n_kv) issue_s(j + 1);
-        const int st = j & 1;
+          mma_bf16_ss(tmem + C::S_COL, kmajor_desc<HD>(sQ, kk), kmajor_desc<HD>(sK, kk), idesc_s, kk > 0 ? 1u : 0u);
+        mma_commit(&bars->k_empty);
+        mma_commit(&bars->s_full);
         mbar_wait(&bars->p_full, j & 1);
-        mbar_wait(&bars->v_full[st], (j >> 1) & 1);
+        mbar_wait(&bars->v_full, j & 1);
         tc_fence_after();
-        const uint32_t sV = smem_u32(smem + C::V_OFF + st * G::TILE_BYTES);
 #pragma unroll
         for (int kk = 0; kk < 128 / 16; ++kk)
-          mma_bf16_ss(tmem + C::O_COL, p_kmajor_desc(sP, kk), mnmajor_desc<HD>(sV, kk), idesc_o,
+          mma_bf16_ts(tmem + C::O_COL, tmem + C::S_COL + kk * 8, mnmajor_desc<HD>(sV, kk), idesc_o,
                       (j > 0 || kk > 0) ? 1u : 0u);
-        mma_commit(&bars->v_empty[st]);
+        mma_commit(&bars->v_empty);
         mma_commit(&bars->pv_done);
       }
     }
@@ -155,17 +138,15 @@ __global__ void __launch_bounds__(192, 1)
     const float sl2 = p.scale_log2;
     float m_used = -INFINITY;  // scaled (log2) running max actually used as the exp base
     float l = 0.f;
-    uint8_t* sP = smem + C::P_OFF;
     for (int j = 0; j < n_kv; ++j) {
-      const int st = j & 1, use = j >> 1;
       const int k0 = sa + visit_tile(qi, j) * 128;
-      mbar_wait(&bars->s_full[st], use & 1);
+      // s_full(j) also implies PV_{j-1} completed (commit tracks all prior tcgen05 ops)
+      mbar_wait(&bars->s_full, j & 1);
       tc_fence_after();
-      // pass 1: masked row max over the 128 columns (S read from TMEM in 32-column slices)
       const bool partial = !valid || (e_r < k0 + 128);
       auto load_masked = [&](int c, float (&x)[32]) {
         uint32_t u[32];
-        tmem_ld32(tmem_addr(tmem, quarter, C::S_COL + st * 128 + c * 32), u);
+        tmem_ld32(tmem_addr(tmem, quarter, C::S_COL + c * 32), u);
         tmem_ld_wait();
 #pragma unroll
         for (int q = 0; q < 32; ++q) x[q] = __uint_as_float(u[q]);
@@ -178,8 +159,9 @@ __global__ void __launch_bounds__(192, 1)
           }
         }
       };
+      // pass 1: masked row max
       float mx = -INFINITY;
-#pragma unroll
+#pragma unroll 1
       for (int c = 0; c < 4; ++c) {
         float x[32];
         load_masked(c, x);
@@ -194,52 +176,41 @@ __global__ void __launch_bounds__(192, 1)
         m_used = mx_s;
         rescale = true;
       }
-      // ---- previous PV must be done before touching O or overwriting P
-      if (j > 0) {
-        mbar_wait(&bars->pv_done, (j - 1) & 1);
-        tc_fence_after();
-        if (__any_sync(0xffffffffu, rescale)) {
-          const float f = rescale ? factor : 1.f;
+      if (j > 0 && __any_sync(0xffffffffu, rescale)) {
+        const float f = rescale ? factor : 1.f;
 #pragma unroll
-          for (int c = 0; c < G::HDP / 32; ++c) {
-            uint32_t u[32];
-            const uint32_t ta = tmem_addr(tmem, quarter, C::O_COL + c * 32);
-            tmem_ld32(ta, u);
-            tmem_ld_wait();
+        for (int c = 0; c < G::HDP / 32; ++c) {
+          uint32_t u[32];
+          const uint32_t ta = tmem_addr(tmem, quarter, C::O_COL + c * 32);
+          tmem_ld32(ta, u);
+          tmem_ld_wait();
 #pragma unroll
-            for (int q = 0; q < 32; ++q) u[q] = __float_as_uint(__uint_as_float(u[q]) * f);
-            tmem_st32(ta, u);
-          }
-          tmem_st_wait();
+          for (int q = 0; q < 32; ++q) u[q] = __float_as_uint(__uint_as_float(u[q]) * f);
+          tmem_st32(ta, u);
         }
       }
-      // pass 2: P = exp2(s*scale_log2 - m) -> bf16 -> shared memory (128B-swizzled K-major A operand)
+      // pass 2: P = exp2(s * scale_log2 - m) as packed bf16 into TMEM columns [16c, 16c + 16),
+      // which only overlap S columns already consumed (chunk c/2 <= c).
       const float base = (m_used == -INFINITY) ? 0.f : m_used;
       float rs = 0.f;
-#pragma unroll
+#pragma unroll 1
       for (int c = 0; c < 4; ++c) {
         float x[32];
         load_masked(c, x);
+        uint32_t w[16];
 #pragma unroll
-        for (int ch = 0; ch < 4; ++ch) {
-          uint32_t w[4];
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const int q = ch * 8 + e * 2;
-            const float p0 = fast_exp2(fmaf(x[q], sl2, -base));
-            const float p1 = fast_exp2(fmaf(x[q + 1], sl2, -base));
-            rs += p0 + p1;
-            w[e] = pack_bf16(p0, p1);
-          }
-          *reinterpret_cast<uint4*>(sP + p_off(rt, c * 32 + ch * 8)) = make_uint4(w[0], w[1], w[2], w[3]);
+        for (int q = 0; q < 32; q += 2) {
+          const float p0 = fast_exp2(fmaf(x[q], sl2, -base));
+          const float p1 = fast_exp2(fmaf(x[q + 1], sl2, -base));
+          rs += p0 + p1;
+          w[q >> 1] = pack_bf16(p0, p1);
         }
+        tmem_st16(tmem_addr(tmem, quarter, C::S_COL + c * 16), w);
       }
-      tc_fence_before();
-      mbar_arrive(&bars->s_free[st]);
-      l = l * factor + rs;
-      fence_proxy_async_smem();
+      tmem_st_wait();
       tc_fence_before();
       mbar_arrive(&bars->p_full);
+      l = l * factor + rs;
     }
     // ---- epilogue: O / l, LSE
     if (n_kv > 0) {
@@ -279,7 +250,7 @@ __global__ void __launch_bounds__(192, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if (warp == 1) tmem_dealloc<512>(tmem);
+  if (warp == 1) tmem_dealloc<C::TMEM_COLS>(tmem);
 }
 
 // ---------------------------------------------------------------- host

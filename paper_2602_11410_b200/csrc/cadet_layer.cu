@@ -58,7 +58,7 @@ cadet_status cadet_attn_core_forward(const cadet_attn_config* cfg, const cadet_b
   const size_t need = plan_bytes(b->n_seqs, b->total_tokens, b->total_tokens);
   if (ws_bytes < need) return ws_err(ws_bytes, need);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  if ((s = cadet_mask_plan(cfg, b, ws, ws_bytes, stream))) return s;
+  if (!cfg->plan_ready && (s = cadet_mask_plan(cfg, b, ws, ws_bytes, stream))) return s;
   PlanView v = plan_carve(ws, b->n_seqs, b->total_tokens, b->total_tokens);
   AttnParams p = attn_params(cfg, b, v);
   p.O = O;
@@ -88,7 +88,7 @@ cadet_status cadet_attn_core_backward(const cadet_attn_config* cfg, const cadet_
   const size_t need = pb + a256((size_t)4 * H * T);
   if (ws_bytes < need) return ws_err(ws_bytes, need);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  if ((s = cadet_mask_plan(cfg, b, ws, ws_bytes, stream))) return s;
+  if (!cfg->plan_ready && (s = cadet_mask_plan(cfg, b, ws, ws_bytes, stream))) return s;
   PlanView v = plan_carve(ws, b->n_seqs, T, T);
   float* D = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ws) + pb);
   AttnParams p = attn_params(cfg, b, v);
@@ -243,7 +243,7 @@ cadet_status cadet_attn_forward(const cadet_attn_config* cfg, const cadet_batch*
   if (ws_bytes < need) return ws_err(ws_bytes, need);
   if (T == 0) return CADET_OK;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  if ((s = cadet_mask_plan(cfg, b, ws, ws_bytes, stream))) return s;
+  if (!cfg->plan_ready && (s = cadet_mask_plan(cfg, b, ws, ws_bytes, stream))) return s;
   PlanView v = plan_carve(ws, n, T, T);
   LayerBufs L = carve_saved(saved, cfg, T);
   LayerWs W = carve_ws(ws, cfg, n, T);
@@ -340,7 +340,7 @@ cadet_status cadet_attn_backward(const cadet_attn_config* cfg, const cadet_batch
   if (ws_bytes < need) return ws_err(ws_bytes, need);
   if (T == 0) return CADET_OK;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  if ((s = cadet_mask_plan(cfg, b, ws, ws_bytes, stream))) return s;
+  if (!cfg->plan_ready && (s = cadet_mask_plan(cfg, b, ws, ws_bytes, stream))) return s;
   PlanView v = plan_carve(ws, n, T, T);
   LayerBufs L = carve_saved(const_cast<void*>(saved), cfg, T);
   LayerWs W = carve_ws(ws, cfg, n, T);

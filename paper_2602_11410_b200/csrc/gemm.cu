@@ -4,7 +4,8 @@
 //   warp 0      : TMA producer (one elected lane), 128B-swizzled K- or MN-major tiles
 //   warp 1      : tcgen05.mma issuer (one elected lane), M=128 x N=BN x K=16 per instruction
 //   warp 2      : TMEM allocator (2 x BN fp32 columns: double-buffered accumulator)
-//   warps 4..7  : epilogue, thread = accumulator row (TMEM lane), tcgen05.ld 32 columns at a time
+//   warps 4..11 : epilogue, thread = accumulator row (TMEM lane), tcgen05.ld 32 columns at a time;
+//                 two warps per TMEM lane quarter split the 32-column slices
 //
 // C[M,N] = sum_seg A_seg[M,K_seg] . B_seg[K_seg,N], tiles 128 x BN x 64, split-K optional.
 #include "gemm.cuh"
@@ -17,7 +18,7 @@ namespace cadet {
 
 constexpr int BM = 128;
 constexpr int BK = 64;
-constexpr int GEMM_THREADS = 256;
+constexpr int GEMM_THREADS = 384;  // 4 non-epilogue warps + 8 epilogue warps
 
 struct KProb {
   int32_t M, N, nseg, kb_total, split_k, m_tiles, n_tiles, unit_begin;
@@ -129,14 +130,13 @@ __device__ __forceinline__ void store_any32(void* base, int is_f32, size_t off, 
 // Rotate adjacent pairs by alpha = dt * theta_i (timestamp RoPE).  Angle in fp64,
 // reduced mod 2*pi in fp64, then fp32 sincos (SURVEY hard part 6).
 __device__ __forceinline__ void rope_pair(float& a, float& b, double dt, double theta, float sign) {
-  const double TWO_PI_HI = 6.283185307179586;
-  const double TWO_PI_LO = 2.4492935982947064e-16;
-  double ang = dt * theta;
-  double k = rint(ang * 0.15915494309189535);
-  double r = fma(-k, TWO_PI_HI, ang);
-  r = fma(-k, TWO_PI_LO, r);
+  // alpha = dt * theta in fp64, reduced mod 2 pi in fp64 (|k| <= ~1e3: the 2 pi rounding error
+  // k * 2.4e-16 is negligible), then MUFU sincos on r in [-pi, pi] (abs err ~5e-7).
+  const double ang = dt * theta;
+  const double k = rint(ang * 0.15915494309189535);
+  const float r = (float)fma(-k, 6.283185307179586, ang);
   float s, c;
-  sincosf((float)r, &s, &c);
+  __sincosf(r, &s, &c);
   s *= sign;
   const float x0 = a, x1 = b;
   a = x0 * c - x1 * s;
@@ -168,14 +168,16 @@ __device__ __forceinline__ void run_epilogue(const EpiParams& e, int row, int M,
       float x[32];
       load_bf16x32(reinterpret_cast<const __nv_bfloat16*>(e.src) + in_off, x);
 #pragma unroll
-      for (int j = 0; j < 32; ++j) v[j] = x[j] * (1.0f / (1.0f + __expf(-v[j])));
+      for (int j = 0; j < 32; ++j) v[j] = x[j] * __fdividef(1.0f, 1.0f + __expf(-v[j]));
       if (e.mode == EPI_GATE_ROPE) {
         const int s = e.row_seq[row];
         const double dt = (s >= 0) ? (double)(e.t_ms[row] - e.t_ms[e.cu[s]]) : 0.0;
+        int hc = n0c % e.hd;  // head-local column of v[0]; a 32-column slice crosses at most one head edge
 #pragma unroll
         for (int j = 0; j < 32; j += 2) {
-          const int i = ((n0c + j) % e.hd) >> 1;
-          rope_pair(v[j], v[j + 1], dt, e.theta[i], 1.0f);
+          rope_pair(v[j], v[j + 1], dt, e.theta[hc >> 1], 1.0f);
+          hc += 2;
+          if (hc >= e.hd) hc -= e.hd;
         }
       }
       store_any32(e.out, e.out_f32, off, v);
@@ -194,7 +196,7 @@ __device__ __forceinline__ void run_epilogue(const EpiParams& e, int row, int M,
       float u[32];
 #pragma unroll
       for (int j = 0; j < 32; ++j) {
-        const float g = 1.0f / (1.0f + __expf(-z[j]));
+        const float g = __fdividef(1.0f, 1.0f + __expf(-z[j]));
         u[j] = v[j] * x[j] * g * (1.0f - g);
         r[j] += v[j] * g;
       }
@@ -243,7 +245,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_kernel(const __grid_cons
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
-      mbar_init(&tempty[b], 4);
+      mbar_init(&tempty[b], 8);
     }
     fence_mbar_init();
   }
@@ -329,6 +331,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_kernel(const __grid_cons
   } else if (warp >= 4) {
     // ============================ epilogue
     const uint32_t quarter = warp & 3;
+    const int half = (warp - 4) >> 2;  // warps 4-7 take even 32-column slices, 8-11 odd ones
     uint32_t tc = 0;
     for (int u = blockIdx.x; u < P.total_units; u += gridDim.x, ++tc) {
       const Unit U = decode_unit(P, u);
@@ -338,7 +341,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_kernel(const __grid_cons
       tc_fence_after();
       const int row = U.m0 + quarter * 32 + lane;
       const int n0 = U.n0 * BN;
-      for (int c = 0; c < BN / 32; ++c) {
+      for (int c = half; c < BN / 32; c += 2) {
         const int n0c = n0 + c * 32;
         if (n0c >= q.N) break;
         uint32_t r[32];

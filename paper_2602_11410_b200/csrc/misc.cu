@@ -17,14 +17,13 @@ __global__ void rope_theta_kernel(double* theta, int half, int hd, double phi_mi
 }
 
 __device__ __forceinline__ void rot(float& a, float& b, double dt, double th, float sign) {
-  const double TWO_PI_HI = 6.283185307179586;
-  const double TWO_PI_LO = 2.4492935982947064e-16;
-  double ang = dt * th;
-  double k = rint(ang * 0.15915494309189535);
-  double r = fma(-k, TWO_PI_HI, ang);
-  r = fma(-k, TWO_PI_LO, r);
+  // alpha = dt * theta in fp64, reduced mod 2 pi in fp64 (|k| <= ~1e3: the 2 pi rounding error
+  // k * 2.4e-16 is negligible), then MUFU sincos on r in [-pi, pi] (abs err ~5e-7).
+  const double ang = dt * th;
+  const double k = rint(ang * 0.15915494309189535);
+  const float r = (float)fma(-k, 6.283185307179586, ang);
   float s, c;
-  sincosf((float)r, &s, &c);
+  __sincosf(r, &s, &c);
   s *= sign;
   const float x0 = a, x1 = b;
   a = x0 * c - x1 * s;
@@ -70,7 +69,7 @@ __global__ void rope_gate_bwd_kernel(const void* dr, int dr_f32, const __nv_bflo
   if (Z) {
     const float2 z = __bfloat1622float2(reinterpret_cast<const __nv_bfloat162*>(Z)[idx]);
     const float2 x = __bfloat1622float2(reinterpret_cast<const __nv_bfloat162*>(Xq)[idx]);
-    const float g0 = 1.f / (1.f + __expf(-z.x)), g1 = 1.f / (1.f + __expf(-z.y));
+    const float g0 = __fdividef(1.f, 1.f + __expf(-z.x)), g1 = __fdividef(1.f, 1.f + __expf(-z.y));
     reinterpret_cast<__nv_bfloat162*>(out_u)[idx] =
         __floats2bfloat162_rn(g.x * x.x * g0 * (1.f - g0), g.y * x.y * g1 * (1.f - g1));
     r = make_float2(g.x * g0, g.y * g1);
@@ -119,10 +118,14 @@ __global__ void head_dz_kernel(const float* logits, const int32_t* bucket, const
     g = 1.f / (1.f + __expf(-z)) - y;
     if (!isfinite(l)) atomicOr(err, ERRBIT_NONFINITE);
     dz[i] = g;
-    atomicAdd(db2 + k, g);
   }
   for (int o = 16; o > 0; o >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
   if ((threadIdx.x & 31) == 0) atomicAdd(loss_sum, l);
+  for (int kk = 0; kk < K; ++kk) {  // db2[k] = sum of dz over rows routed to tower k (warp-reduced)
+    float gk = (i < n && k == kk) ? g : 0.f;
+    for (int o = 16; o > 0; o >>= 1) gk += __shfl_xor_sync(0xffffffffu, gk, o);
+    if ((threadIdx.x & 31) == 0 && gk != 0.f) atomicAdd(db2 + kk, gk);
+  }
 }
 
 // dhid[i, c] = dz_i * w2[c] * 1[pre > 0] on the realised tower, 0 elsewhere (S:260 isolation);

@@ -247,17 +247,27 @@ __global__ void __launch_bounds__(128) plan_tile_kernel(PlanArgs a, PlanView v) 
 }
 
 // ---------------------------------------------------------------- K4 / K5
-__global__ void plan_order_kernel(PlanView v) {
-  if (threadIdx.x == 0) {
-    for (int which = 0; which < 2; ++which) {
-      int* h = v.hist + which * v.hmax;
-      int acc = 0;
-      for (int c = v.hmax - 1; c >= 0; --c) {  // descending cost first (LPT)
-        const int k = h[c];
-        h[c] = acc;
-        acc += k;
-      }
+// Exclusive scan of the cost histograms in DESCENDING cost order (LPT: most expensive first).
+__global__ void __launch_bounds__(1024) plan_order_kernel(PlanView v) {
+  __shared__ long long sh[1024];
+  const int tid = threadIdx.x, nt = blockDim.x;
+  for (int which = 0; which < 2; ++which) {
+    int* h = v.hist + which * v.hmax;
+    const int per = (v.hmax + nt - 1) / nt;
+    // thread t owns reversed positions [t*per, (t+1)*per): cost c = hmax-1-pos
+    long long local = 0;
+    for (int q = tid * per; q < min((tid + 1) * per, v.hmax); ++q) local += h[v.hmax - 1 - q];
+    long long total;
+    long long pre = block_exclusive_scan<long long>(local, sh, total);
+    int vals[64];
+    const int cnt = max(0, min((tid + 1) * per, v.hmax) - tid * per);
+    for (int q = 0; q < cnt && q < 64; ++q) vals[q] = h[v.hmax - 1 - (tid * per + q)];
+    __syncthreads();
+    for (int q = 0; q < cnt && q < 64; ++q) {
+      h[v.hmax - 1 - (tid * per + q)] = (int)pre;
+      pre += vals[q];
     }
+    __syncthreads();
   }
 }
 
@@ -281,7 +291,7 @@ cudaError_t plan_launch(const PlanArgs& a, const PlanView& v, cudaStream_t st) {
   const int nb = (v.nq_cap + 127) / 128;
   if (nb > 0) {
     plan_tile_kernel<<<nb, 128, 0, st>>>(a, v);
-    plan_order_kernel<<<1, 32, 0, st>>>(v);
+    plan_order_kernel<<<1, 1024, 0, st>>>(v);
     plan_scatter_kernel<<<nb, 128, 0, st>>>(a, v);
   }
   return cudaGetLastError();

@@ -181,6 +181,10 @@ class CadetStack:
                             _vp(self.n_out), C.c_void_p(self.small_ws.data_ptr() + 256), st))
         b = self.batch(inp).struct()
         ws, wsn = _vp(self._ws), self._ws.numel()
+        # A1: one mask plan per step, shared by every layer's forward and backward
+        self.acfg.plan_ready = 0
+        chk(lib.cadet_mask_plan(C.byref(self.acfg), C.byref(b), ws, wsn, st))
+        self.acfg.plan_ready = 1
         # A1-A6: residual layers  H[l+1] = H[l] + Attn(H[l])
         for l in range(cfg.n_layers):
             w = L.AttnWeights(*[x.data_ptr() for x in self.W[l]])
@@ -214,6 +218,7 @@ class CadetStack:
     def pairs(self, inp: StepInputs) -> int:
         """Allowed (i, j) pairs of the planned mask (head-independent), from the plan's export hook."""
         self.step(inp, backward=False)
+        self.acfg.plan_ready = 0
         kv, tc, pairs = ops.mask_export(self.acfg, self.batch(inp), self._ws, 0)
         return int(pairs.item())
 
