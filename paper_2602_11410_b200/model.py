@@ -90,6 +90,16 @@ def make_inputs(users, d: int, L_chunk: int, seed: int, pin: bool = False) -> St
     return inp
 
 
+def dp_reduce(grads: torch.Tensor, loss: torch.Tensor, group=None):
+    """the routed loss is a SUM over impressions (Eq. 9, R15), so summing the ranks'
+    flat fp32 gradient buffers (one NCCL all-reduce bucket) gives exactly the union-batch gradient."""
+    if group is None:
+        return grads, loss
+    torch.distributed.all_reduce(grads, group=group)
+    torch.distributed.all_reduce(loss, group=group)
+    return grads, loss
+
+
 def _vp(t):
     return C.c_void_p(t.data_ptr()) if t is not None else None
 
@@ -209,10 +219,7 @@ class CadetStack:
             chk(lib.cadet_attn_backward(C.byref(self.acfg), C.byref(b), C.byref(w), _vp(self.Hs[l]),
                                         _vp(self.saved[l]), _vp(self.dHs[l + 1]), _vp(self.dHs[l]),
                                         _vp(self.dHs[l + 1]), C.byref(g), ws, wsn, st))
-        if group is not None:
-            # DP: the loss is a sum (R15) -> SUM all-reduce is the union-batch gradient
-            torch.distributed.all_reduce(self.grads, group=group)
-            torch.distributed.all_reduce(self.loss, group=group)
+        dp_reduce(self.grads, self.loss, group)
         return self.loss
 
     def pairs(self, inp: StepInputs) -> int:

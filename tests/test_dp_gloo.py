@@ -1,0 +1,76 @@
+"""Multi-rank (N > 1) host logic on CPU with 2 gloo ranks: sharding whole sequences across ranks
+and SUM-all-reducing the flat gradient buffer (model.dp_reduce) equals the gradient of the union
+batch (Eq. 9 is a sum, R15).  Gradients come from the fp64 oracle."""
+import os
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+import torch.distributed as dist  # noqa: E402
+import torch.multiprocessing as mp  # noqa: E402
+
+
+def _case():
+    from oracle import cadet_oracle as O
+    from synth import generator as G
+    lens = [13, 9, 1, 11, 6, 7]
+    b = G.fixed_lengths_batch(lens, seed=4, cfg=G.stress_config())
+    cu = np.concatenate([[0], np.cumsum(b.lengths)])
+    d, H = 8, 2
+    rng = np.random.default_rng(5)
+    X = rng.standard_normal((cu[-1], d))
+    dY = rng.standard_normal((cu[-1], d))
+    W = [rng.standard_normal((d, d)) / np.sqrt(d) for _ in range(7)]
+    cfg = O.AttnConfig(d_model=d, n_heads=H, delta_delay_ms=120_000, rope_phi_min=0.5, rope_base=1e4,
+                       rope_dt_max_ms=86_400_000)
+    return O, b, cu, X, dY, W, cfg
+
+
+def _grads(O, cu, ts, X, dY, W, cfg, seqs):
+    """Oracle flat gradient (7 d x d) of the given whole sequences."""
+    flat = []
+    g = None
+    for s in seqs:
+        a, e = int(cu[s]), int(cu[s + 1])
+        meta = O.SeqMeta(cu=np.array([0, e - a]), t_ms=ts[a:e], n_cand=np.zeros(1, np.int64))
+        _, caches, _ = O.batch_forward(X[a:e], W, meta, cfg)
+        _, gW, _ = O.batch_backward(caches, W, meta, dY[a:e], cfg)
+        g = gW if g is None else [x + y for x, y in zip(g, gW)]
+    return np.concatenate([x.reshape(-1) for x in g])
+
+
+def _worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2602_11410_b200.model import dp_reduce
+    O, b, cu, X, dY, W, cfg = _case()
+    mine = [s for s in range(len(cu) - 1) if s % world == rank]     # whole sequences per rank
+    flat = torch.tensor(_grads(O, cu, b.timestamps, X, dY, W, cfg, mine))
+    loss = torch.tensor([float(len(mine))], dtype=torch.float64)
+    dp_reduce(flat, loss, dist.group.WORLD)
+    if rank == 0:
+        q.put((flat.numpy(), float(loss.item())))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_dp_sum_allreduce_equals_union_gradient():
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got, loss = q.get(timeout=240)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    O, b, cu, X, dY, W, cfg = _case()
+    ref = _grads(O, cu, b.timestamps, X, dY, W, cfg, range(len(cu) - 1))
+    assert np.abs(got - ref).max() <= 1e-12 * max(1.0, np.abs(ref).max())
+    assert loss == len(cu) - 1
