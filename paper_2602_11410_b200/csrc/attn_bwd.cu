@@ -1,16 +1,21 @@
 // A10: attention backward (adjoint of PAPER.md Eq. 7) for the packed, session-masked layout.
 //
 // One CTA per (128-key tile of one sequence, head), k-tiles in descending cost order.  K_j, V_j
-// stay in shared memory; the CTA walks the q-tiles that see k-tile j (the transpose of the
-// forward visit rule: q-tile i visits j iff j < nf_i or kt2_i <= j <= i), and per q-tile:
-//   S^T  = K_j Q_i^T,  dP^T = V_j dO_i^T            (tcgen05, TMEM cols [0,128) and [128,256))
-//   P^T  = exp2(S^T scale log2e - LSE_i log2e) on visible cells, dS^T = P^T (dP^T - D_i) * scale
-//   dV  += P^T dO_i,  dK += dS^T Q_i                   (TMEM accumulators [256,384), [384,512))
-//   dQ_i = dS K_j  (TMEM [128, 128+HDP), reusing dP^T) -> fp32 atomics into the dQ accumulator
+// stay in shared memory; the CTA walks the q-tiles that see k-tile j (transpose of the forward
+// visit rule: q-tile i visits j iff j < nf_i or kt2_i <= j <= i; list built once in smem), and per
+// q-tile i:
+//   S^T  = K_j Q_i^T           -> TMEM [0,128)        dP^T = V_j dO_i^T -> TMEM [128,256)
+//   P^T  = exp2(S^T scale log2e - LSE_i log2e) on visible cells (predicate only on non-FULL pairs)
+//   dS^T = P^T (dP^T - D_i) scale
+//   P^T, dS^T are written back as packed bf16 over the consumed S^T / dP^T columns and feed
+//   dV += P^T dO_i and dK += dS^T Q_i as TMEM-A (TS) MMAs into TMEM [256,384) / [384,512);
+//   dS^T also goes to shared memory for dQ_i = dS K_j (MN-major A), written over [128,256) and
+//   drained by four dedicated warps with fp32 vector atomics while the next S^T is computed.
 //
-//   warp 0     : TMA producer (K_j, V_j once; Q_i, dO_i per q-tile)
-//   warp 1     : TMEM owner + MMA issuer
-//   warps 2..5 : thread = key row for P^T / dS^T (TMEM lane), = query row for the dQ drain
+//   warp 0      : TMA producer (K_j, V_j once; Q_i, dO_i per q-tile)
+//   warp 1      : TMEM owner + MMA issuer
+//   warps 2..5  : thread = key row (TMEM lane): P^T, dS^T
+//   warps 6..9  : thread = query row: dQ drain; final dK, dV epilogue
 #include "attn_common.cuh"
 #include "prof.cuh"
 
@@ -23,18 +28,20 @@ struct BwdCfg {
   static constexpr int V_OFF = K_OFF + G::TILE_BYTES;
   static constexpr int Q_OFF = V_OFF + G::TILE_BYTES;
   static constexpr int DO_OFF = Q_OFF + G::TILE_BYTES;
-  static constexpr int PT_OFF = DO_OFF + G::TILE_BYTES;
-  static constexpr int DS_OFF = PT_OFF + 32768;
-  static constexpr int VEC_OFF = DS_OFF + 32768;      // [2][4][128] x 4 B
-  static constexpr int BAR_OFF = VEC_OFF + 2 * 4 * 128 * 4;
-  static constexpr int USED = BAR_OFF + 256;
-  static constexpr int SMEM = (USED + 1024 > 118784 ? USED + 1024 : 118784);
+  static constexpr int DS_OFF = DO_OFF + G::TILE_BYTES;  // dS^T bf16 [128 keys x 128 q], 128B swizzle
+  static constexpr int VEC_OFF = DS_OFF + 32768;          // [2][4][128] x 4 B: lse2, D, e, q|pp
+  static constexpr int LIST_OFF = VEC_OFF + 2 * 4 * 128 * 4;
+  static constexpr int MAX_LIST = 512;                    // visited q-tiles per k-tile (T/128 bound)
+  static constexpr int BAR_OFF = LIST_OFF + MAX_LIST * 4;
+  static constexpr int SMEM = BAR_OFF + 256 + 1024;
   static constexpr int S_COL = 0, DP_COL = 128, DV_COL = 256, DK_COL = 384;
+  static constexpr int THREADS = 320;
 };
 
 struct BwdBars {
-  uint64_t kv_full, qd_full, qd_empty, sdp_full, pds_full, mma2_done, dq_free;
+  uint64_t kv_full, qd_full, qd_empty, s_full, dp_full, pds_ready, dq_full, dq_free;
   uint32_t tmem_base;
+  int32_t n_it;
 };
 
 __device__ __forceinline__ bool q_sees_k(const QTileInfo& qi, int kt) {
@@ -42,7 +49,7 @@ __device__ __forceinline__ bool q_sees_k(const QTileInfo& qi, int kt) {
 }
 
 template <int HD>
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(320, 1)
     attn_bwd_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constant__ CUtensorMap mK,
                     const __grid_constant__ CUtensorMap mV, const __grid_constant__ CUtensorMap mdO,
                     const AttnParams p) {
@@ -64,51 +71,66 @@ __global__ void __launch_bounds__(192, 1)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   BwdBars* bars = reinterpret_cast<BwdBars*>(smem + C::BAR_OFF);
-  float* vec = reinterpret_cast<float*>(smem + C::VEC_OFF);  // [2][4][128]: lse2, D, e (int), q|pp (int)
+  float* vec = reinterpret_cast<float*>(smem + C::VEC_OFF);
+  int* list = reinterpret_cast<int*>(smem + C::LIST_OFF);
   const uint32_t warp = warp_id(), lane = lane_id();
 
-  if (threadIdx.x == 0) {
-    mbar_init(&bars->kv_full, 1);
-    mbar_init(&bars->qd_full, 1);
-    mbar_init(&bars->qd_empty, 1);
-    mbar_init(&bars->sdp_full, 1);
-    mbar_init(&bars->pds_full, 128);
-    mbar_init(&bars->mma2_done, 1);
-    mbar_init(&bars->dq_free, 128);
-    fence_mbar_init();
+  if (warp == 0) {
+    // visited q-tiles (and whether the (q-tile, k-tile) pair is FULL) -> smem list
+    int n = 0;
+    for (int base = kt; base < nq_s; base += 32) {
+      const int qt = base + (int)lane;
+      int entry = -1;
+      if (qt < nq_s) {
+        const QTileInfo qi = p.plan.qinfo[tile0 + qt];
+        if (q_sees_k(qi, kt)) {
+          const bool full = qi.rows == 128 && qi.emin >= (kt + 1) * 128;
+          entry = qt | (full ? (1 << 30) : 0);
+        }
+      }
+      const uint32_t m = __ballot_sync(0xffffffffu, entry >= 0);
+      const int pos = n + __popc(m & ((1u << lane) - 1u));
+      if (entry >= 0 && pos < C::MAX_LIST) list[pos] = entry;
+      n += __popc(m);
+    }
+    if (lane == 0) {
+      bars->n_it = min(n, C::MAX_LIST);
+      mbar_init(&bars->kv_full, 1);
+      mbar_init(&bars->qd_full, 1);
+      mbar_init(&bars->qd_empty, 1);
+      mbar_init(&bars->s_full, 1);
+      mbar_init(&bars->dp_full, 1);
+      mbar_init(&bars->pds_ready, 128);
+      mbar_init(&bars->dq_full, 1);
+      mbar_init(&bars->dq_free, 128);
+      fence_mbar_init();
+    }
   }
   if (warp == 1) tmem_alloc<512>(&bars->tmem_base);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = bars->tmem_base;
+  const int n_it = bars->n_it;
 
   if (warp == 0) {
     // ============================ producer
     if (elect_one()) {
-      tma_prefetch(&mQ);
-      tma_prefetch(&mK);
-      tma_prefetch(&mV);
-      tma_prefetch(&mdO);
       mbar_expect_tx(&bars->kv_full, 2 * G::TILE_BYTES);
 #pragma unroll
       for (int blk = 0; blk < G::NB; ++blk) {
         tma_load_3d(smem + C::K_OFF + blk * G::BLK, &mK, &bars->kv_full, blk * G::CB, h, k0);
         tma_load_3d(smem + C::V_OFF + blk * G::BLK, &mV, &bars->kv_full, blk * G::CB, h, k0);
       }
-      int it = 0;
-      for (int qt = kt; qt < nq_s; ++qt) {
-        const QTileInfo qi = p.plan.qinfo[tile0 + qt];
-        if (!q_sees_k(qi, kt)) continue;
+      for (int it = 0; it < n_it; ++it) {
+        const int q0 = sa + (list[it] & 0xFFFF) * 128;
         if (it > 0) mbar_wait(&bars->qd_empty, (it - 1) & 1);
-        const int q0 = sa + qt * 128;
         mbar_expect_tx(&bars->qd_full, 2 * G::TILE_BYTES);
 #pragma unroll
         for (int blk = 0; blk < G::NB; ++blk) {
           tma_load_3d(smem + C::Q_OFF + blk * G::BLK, &mQ, &bars->qd_full, blk * G::CB, h, q0);
           tma_load_3d(smem + C::DO_OFF + blk * G::BLK, &mdO, &bars->qd_full, blk * G::CB, h, q0);
         }
-        ++it;
       }
     }
   } else if (warp == 1) {
@@ -119,60 +141,60 @@ __global__ void __launch_bounds__(192, 1)
       const uint32_t id_q = idesc_bf16(128, G::HDP, 1, 1);
       const uint32_t sK = smem_u32(smem + C::K_OFF), sV = smem_u32(smem + C::V_OFF);
       const uint32_t sQ = smem_u32(smem + C::Q_OFF), sdO = smem_u32(smem + C::DO_OFF);
-      const uint32_t sPT = smem_u32(smem + C::PT_OFF), sDS = smem_u32(smem + C::DS_OFF);
+      const uint32_t sDS = smem_u32(smem + C::DS_OFF);
       mbar_wait(&bars->kv_full, 0);
-      int it = 0;
-      for (int qt = kt; qt < nq_s; ++qt) {
-        const QTileInfo qi = p.plan.qinfo[tile0 + qt];
-        if (!q_sees_k(qi, kt)) continue;
+      for (int it = 0; it < n_it; ++it) {
         mbar_wait(&bars->qd_full, it & 1);
-        if (it > 0) mbar_wait(&bars->dq_free, (it - 1) & 1);  // dQ_{i-1} drained from the dP region
         tc_fence_after();
+        // S^T_i over the P^T_{i-1} columns: in-order after dV_{i-1}, which read them.
 #pragma unroll
         for (int kk = 0; kk < G::HDP / 16; ++kk)
           mma_bf16_ss(tmem + C::S_COL, kmajor_desc<HD>(sK, kk), kmajor_desc<HD>(sQ, kk), id_s, kk > 0 ? 1u : 0u);
+        mma_commit(&bars->s_full);
+        if (it > 0) {
+          mbar_wait(&bars->dq_free, (it - 1) & 1);  // dQ_{i-1} drained from [128, 256)
+          tc_fence_after();
+        }
 #pragma unroll
         for (int kk = 0; kk < G::HDP / 16; ++kk)
           mma_bf16_ss(tmem + C::DP_COL, kmajor_desc<HD>(sV, kk), kmajor_desc<HD>(sdO, kk), id_s, kk > 0 ? 1u : 0u);
-        mma_commit(&bars->sdp_full);
-        mbar_wait(&bars->pds_full, it & 1);
+        mma_commit(&bars->dp_full);
+        mbar_wait(&bars->pds_ready, it & 1);
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < 128 / 16; ++kk)
-          mma_bf16_ss(tmem + C::DV_COL, p_kmajor_desc(sPT, kk), mnmajor_desc<HD>(sdO, kk), id_kv,
+          mma_bf16_ts(tmem + C::DV_COL, tmem + C::S_COL + kk * 8, mnmajor_desc<HD>(sdO, kk), id_kv,
                       (it > 0 || kk > 0) ? 1u : 0u);
 #pragma unroll
         for (int kk = 0; kk < 128 / 16; ++kk)
-          mma_bf16_ss(tmem + C::DK_COL, p_kmajor_desc(sDS, kk), mnmajor_desc<HD>(sQ, kk), id_kv,
+          mma_bf16_ts(tmem + C::DK_COL, tmem + C::DP_COL + kk * 8, mnmajor_desc<HD>(sQ, kk), id_kv,
                       (it > 0 || kk > 0) ? 1u : 0u);
+        mma_commit(&bars->qd_empty);
+        // dQ_i = dS K_j over the dS^T columns: in-order after dK_i, which read them.
 #pragma unroll
         for (int kk = 0; kk < 128 / 16; ++kk)
           mma_bf16_ss(tmem + C::DP_COL, p_mnmajor_desc(sDS, kk), mnmajor_desc<HD>(sK, kk), id_q, kk > 0 ? 1u : 0u);
-        mma_commit(&bars->qd_empty);
-        mma_commit(&bars->mma2_done);
-        ++it;
+        mma_commit(&bars->dq_full);
       }
     }
-  } else {
-    // ============================ compute warps 2..5
+  } else if (warp < 6) {
+    // ============================ P^T / dS^T warps (thread = key row)
     const uint32_t quarter = warp & 3;
-    const int tr = quarter * 32 + lane;      // TMEM lane = key row (P^T) = query row (dQ drain)
-    const int ct = threadIdx.x - 64;         // 0..127 loader index
+    const int tr = quarter * 32 + lane;
+    const int ct = threadIdx.x - 64;  // 0..127 vector-loader index
     const int key = k0 + tr;
     const bool key_valid = tr < keys_valid;
     const float sl2 = p.scale_log2;
     const float LOG2E = 1.4426950408889634f;
-    uint8_t* sPT = smem + C::PT_OFF;
     uint8_t* sDS = smem + C::DS_OFF;
-    int it = 0;
-    for (int qt = kt; qt < nq_s; ++qt) {
-      const QTileInfo qi = p.plan.qinfo[tile0 + qt];
-      if (!q_sees_k(qi, kt)) continue;
-      const int q0 = sa + qt * 128;
+    for (int it = 0; it < n_it; ++it) {
+      const int ent = list[it];
+      const bool full = (ent >> 30) & 1;
+      const int q0 = sa + (ent & 0xFFFF) * 128;
       const int qvalid = min(128, se - q0);
       float* vb = vec + (it & 1) * 512;
       int* vbi = reinterpret_cast<int*>(vb);
-      {  // per-query vectors of this q-tile
+      {
         const int q = q0 + ct;
         const bool v = ct < qvalid;
         vb[ct] = v ? p.lse[(size_t)h * p.T + q] * LOG2E : INFINITY;
@@ -181,75 +203,109 @@ __global__ void __launch_bounds__(192, 1)
         vbi[384 + ct] = v ? (q | (p.plan.row_pp[q] ? (1 << 30) : 0)) : -2;
       }
       named_bar_sync(1, 128);
-      mbar_wait(&bars->sdp_full, it & 1);
+      mbar_wait(&bars->s_full, it & 1);
       tc_fence_after();
-      if (it > 0) {  // PT / DST shared buffers are free once the previous MMAs completed
-        mbar_wait(&bars->mma2_done, (it - 1) & 1);
-      }
-#pragma unroll 1
+      float pr[128];
+#pragma unroll
       for (int c = 0; c < 4; ++c) {
-        uint32_t us[32], ud[32];
+        uint32_t us[32];
         tmem_ld32(tmem_addr(tmem, quarter, C::S_COL + c * 32), us);
+        tmem_ld_wait();
+#pragma unroll
+        for (int q4 = 0; q4 < 32; q4 += 4) {
+          const float4 l4 = *reinterpret_cast<const float4*>(vb + c * 32 + q4);  // broadcast LDS.128
+          const float lv[4] = {l4.x, l4.y, l4.z, l4.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) pr[c * 32 + q4 + e] = fast_exp2(fmaf(__uint_as_float(us[q4 + e]), sl2, -lv[e]));
+        }
+        if (!full) {
+#pragma unroll
+          for (int q4 = 0; q4 < 32; q4 += 4) {
+            const int4 e4 = *reinterpret_cast<const int4*>(vbi + 256 + c * 32 + q4);
+            const int4 w4 = *reinterpret_cast<const int4*>(vbi + 384 + c * 32 + q4);
+            const int ev[4] = {e4.x, e4.y, e4.z, e4.w}, wv[4] = {w4.x, w4.y, w4.z, w4.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const int qw = wv[e];
+              const int qq = qw & ~(1 << 30);
+              const bool ppq = (qw >= 0) && (qw & (1 << 30));
+              const bool ok = key_valid && qw >= 0 && ((key < ev[e]) || (key == qq) || (ppq && key == qq - 1));
+              if (!ok) pr[c * 32 + q4 + e] = 0.f;
+            }
+          }
+        }
+      }
+      // P^T (bf16) over the consumed S^T columns [0, 64)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        uint32_t w[16];
+#pragma unroll
+        for (int q = 0; q < 32; q += 2) w[q >> 1] = pack_bf16(pr[c * 32 + q], pr[c * 32 + q + 1]);
+        tmem_st16(tmem_addr(tmem, quarter, C::S_COL + c * 16), w);
+      }
+      mbar_wait(&bars->dp_full, it & 1);
+      tc_fence_after();
+      if (it > 0) mbar_wait(&bars->dq_full, (it - 1) & 1);  // dQ_{i-1} MMA has finished reading dS smem
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        uint32_t ud[32];
         tmem_ld32(tmem_addr(tmem, quarter, C::DP_COL + c * 32), ud);
         tmem_ld_wait();
-        uint32_t wp[16], wd[16];
+        uint32_t w[16];
 #pragma unroll
-        for (int q2 = 0; q2 < 32; q2 += 2) {
-          float pv[2], dv[2];
+        for (int q4 = 0; q4 < 32; q4 += 4) {
+          const float4 d4 = *reinterpret_cast<const float4*>(vb + 128 + c * 32 + q4);
+          const float dv[4] = {d4.x, d4.y, d4.z, d4.w};
+          float ds[4];
 #pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const int col = c * 32 + q2 + e;
-            const int qe = vbi[256 + col];
-            const int qw = vbi[384 + col];
-            const int qq = qw & ~(1 << 30);
-            const bool ppq = (qw >= 0) && (qw & (1 << 30));
-            const bool ok = key_valid && qw >= 0 && ((key < qe) || (key == qq) || (ppq && key == qq - 1));
-            const float s = __uint_as_float(us[q2 + e]);
-            const float pr = ok ? fast_exp2(fmaf(s, sl2, -vb[col])) : 0.f;
-            pv[e] = pr;
-            dv[e] = pr * (__uint_as_float(ud[q2 + e]) - vb[128 + col]) * p.scale;
-          }
-          wp[q2 >> 1] = pack_bf16(pv[0], pv[1]);
-          wd[q2 >> 1] = pack_bf16(dv[0], dv[1]);
+          for (int e = 0; e < 4; ++e) ds[e] = pr[c * 32 + q4 + e] * (__uint_as_float(ud[q4 + e]) - dv[e]) * p.scale;
+          w[q4 >> 1] = pack_bf16(ds[0], ds[1]);
+          w[(q4 >> 1) + 1] = pack_bf16(ds[2], ds[3]);
         }
+        tmem_st16(tmem_addr(tmem, quarter, C::DP_COL + c * 16), w);
 #pragma unroll
-        for (int ch = 0; ch < 4; ++ch) {
-          *reinterpret_cast<uint4*>(sPT + p_off(tr, c * 32 + ch * 8)) =
-              make_uint4(wp[ch * 4], wp[ch * 4 + 1], wp[ch * 4 + 2], wp[ch * 4 + 3]);
+        for (int ch = 0; ch < 4; ++ch)
           *reinterpret_cast<uint4*>(sDS + p_off(tr, c * 32 + ch * 8)) =
-              make_uint4(wd[ch * 4], wd[ch * 4 + 1], wd[ch * 4 + 2], wd[ch * 4 + 3]);
-        }
+              make_uint4(w[ch * 4], w[ch * 4 + 1], w[ch * 4 + 2], w[ch * 4 + 3]);
       }
+      tmem_st_wait();
       fence_proxy_async_smem();
       tc_fence_before();
-      mbar_arrive(&bars->pds_full);
-      // ---- dQ_i drain: thread = query row
-      mbar_wait(&bars->mma2_done, it & 1);
+      mbar_arrive(&bars->pds_ready);
+    }
+  } else {
+    // ============================ dQ drain warps (thread = query row), then dK / dV epilogue
+    const uint32_t quarter = warp & 3;
+    const int tr = quarter * 32 + lane;
+    for (int it = 0; it < n_it; ++it) {
+      const int q0 = sa + (list[it] & 0xFFFF) * 128;
+      const int q = q0 + tr;
+      const bool qv = q < se;
+      mbar_wait(&bars->dq_full, it & 1);
       tc_fence_after();
-      {
-        const int q = q0 + tr;
-        const bool qv = tr < qvalid;
 #pragma unroll 1
-        for (int c = 0; c < G::HDP / 32; ++c) {
-          uint32_t u[32];
-          tmem_ld32(tmem_addr(tmem, quarter, C::DP_COL + c * 32), u);
-          tmem_ld_wait();
-          if (qv) {
-            float* dst = p.dQ + (size_t)q * p.d + (size_t)h * p.hd + c * 32;
-            const int ncol = min(32, p.hd - c * 32);
-            for (int j = 0; j < ncol; j += 4)
+      for (int c = 0; c < G::HDP / 32; ++c) {
+        uint32_t u[32];
+        tmem_ld32(tmem_addr(tmem, quarter, C::DP_COL + c * 32), u);
+        tmem_ld_wait();
+        if (qv) {
+          float* dst = p.dQ + (size_t)q * p.d + (size_t)h * p.hd + c * 32;
+          const int ncol = min(32, p.hd - c * 32);
+#pragma unroll
+          for (int j = 0; j < 32; j += 4)
+            if (j < ncol)
               atomicAdd(reinterpret_cast<float4*>(dst + j),
                         make_float4(__uint_as_float(u[j]), __uint_as_float(u[j + 1]), __uint_as_float(u[j + 2]),
                                     __uint_as_float(u[j + 3])));
-          }
         }
       }
       tc_fence_before();
       mbar_arrive(&bars->dq_free);
-      ++it;
     }
-    // ---- dK, dV epilogue (thread = key row)
-    if (it > 0) {
+    // dK, dV (thread = key row): all MMAs completed (the last dq_full tracks every prior MMA)
+    const int key = k0 + tr;
+    const bool key_valid = tr < keys_valid;
+    if (n_it > 0) {
       tc_fence_after();
 #pragma unroll 1
       for (int which = 0; which < 2; ++which) {
@@ -322,7 +378,7 @@ static cudaError_t bwd_hd(const CUtensorMap& mQ, const CUtensorMap& mK, const CU
   const int grid = p.plan.nq_cap * p.H;
   if (grid == 0) return cudaSuccess;
   ProfScope ps(PROF_ATTN_BWD, st, 1);
-  attn_bwd_kernel<HD><<<grid, 192, C::SMEM, st>>>(mQ, mK, mV, mdO, p);
+  attn_bwd_kernel<HD><<<grid, C::THREADS, C::SMEM, st>>>(mQ, mK, mV, mdO, p);
   return cudaGetLastError();
 }
 

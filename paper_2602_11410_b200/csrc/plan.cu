@@ -229,8 +229,12 @@ __global__ void __launch_bounds__(128) plan_tile_kernel(PlanArgs a, PlanView v) 
   const int len = min(seq_len_safe(a.cu, s, a.T), a.max_seqlen);
   const int nq_s = (len + TILE - 1) / TILE;
   const int r0 = sa + qt * TILE, r1 = min(sa + len, r0 + TILE);
-  int emax = 0;
-  for (int r = r0; r < r1; ++r) emax = max(emax, v.kv_end[r] - sa);
+  int emax = 0, emin = 1 << 30;
+  for (int r = r0; r < r1; ++r) {
+    const int e = v.kv_end[r] - sa;
+    emax = max(emax, e);
+    emin = min(emin, e);
+  }
   const int nf = min((emax + TILE - 1) / TILE, qt + 1);
   const int kt_pp = (qt > 0 && v.row_pp[r0]) ? qt - 1 : qt;
   const int kt2 = max(nf, kt_pp);
@@ -239,6 +243,9 @@ __global__ void __launch_bounds__(128) plan_tile_kernel(PlanArgs a, PlanView v) 
   info.qt = qt;
   info.nf = nf;
   info.kt2 = kt2;
+  info.emin = (r1 > r0) ? emin : 0;
+  info.rows = r1 - r0;
+  info.pad0 = info.pad1 = 0;
   v.qinfo[g] = info;
   const int cost_f = min(nf + (qt + 1 - kt2), v.hmax - 1);
   const int cost_b = min(nq_s - qt, v.hmax - 1);

@@ -12,6 +12,9 @@ struct QTileInfo {  // one per (sequence, 128-row tile), anchored at the sequenc
   int32_t qt;       // tile index inside the sequence
   int32_t nf;       // front k-tiles [0, nf) are visited (prefix region, max_i kv_end)
   int32_t kt2;      // then tiles [kt2, qt] (diagonal, and qt-1 for a PAIR_PREV first row); kt2 >= nf
+  int32_t emin;     // min over the tile's rows of the local visible-prefix end (k-tiles below emin/128 are FULL)
+  int32_t rows;     // rows of this tile inside the sequence (<= 128)
+  int32_t pad0, pad1;
 };
 
 struct PlanView {   // device pointers into the workspace
