@@ -213,7 +213,7 @@ cadet_status cadet_gemm(int32_t M, int32_t N, int32_t K, const void* A, int32_t 
   g.epi.ldo = N;
   g.epi.resid = resid;
   g.epi.resid_f32 = c_f32;
-  const int bn = (N % 256 == 0 && (long long)((M + 127) / 128) * (N / 256) >= 120) ? 256 : 128;
+  const int bn = (N % 256 == 0 && M >= 256) ? 256 : 128;  // 256 -> CTA-pair (cta_group::2) kernel
   return cuda_check(gemm_launch(&g, 1, bn, reinterpret_cast<cudaStream_t>(stream)), "gemm");
 }
 

@@ -169,6 +169,9 @@ int pick_bn(int M, int N) {
   const int w256 = (N + 255) / 256 * 256 - N, w128 = (N + 127) / 128 * 128 - N;
   return (w256 <= w128 && (long long)((M + 127) / 128) * ((N + 255) / 256) >= 148) ? 256 : 128;
 }
+// Weight gradients are split-K, so tile count is never the limit: prefer BN = 256 (BN = 128 with
+// both operands from smem needs 128 B/clk of smem bandwidth per SM, the whole budget).
+int pick_bn_wgrad(int N) { return (N >= 256 && ((N + 255) / 256 * 256 - N) <= ((N + 127) / 128 * 128 - N) + 64) ? 256 : 128; }
 int pick_split(int M, int N, int bn, int K) {
   const long long tiles = (long long)((M + 127) / 128) * ((N + bn - 1) / bn);
   const int kb = (K + 63) / 64;
@@ -345,7 +348,7 @@ cadet_status cadet_attn_backward(const cadet_attn_config* cfg, const cadet_batch
   LayerBufs L = carve_saved(const_cast<void*>(saved), cfg, T);
   LayerWs W = carve_ws(ws, cfg, n, T);
   const int bn = pick_bn(T, d);
-  const int bnw = pick_bn(d, d);
+  const int bnw = pick_bn_wgrad(d);
   const size_t wbytes = (size_t)d * d * 4;
   cudaError_t e = rope_theta_launch(W.theta, hd, cfg->rope_phi_min, cfg->rope_base, (double)cfg->rope_delta_t_max_ms, st);
   float* gws[7] = {gr->dW_xg, gr->dW_q, gr->dW_k, gr->dW_v, gr->dW_qg, gr->dW_kg, gr->dW_o};
@@ -555,12 +558,12 @@ cadet_status cadet_heads_loss_backward(const cadet_head_config* h, const cadet_h
   if (e == cudaSuccess) e = head_dhid_launch(pre, dz, bucket, w->w2, n, h->K, h->d_hidden, dhid, dhid_lo, gr->db1, gr->dw2, st);
   if (e == cudaSuccess) e = gather_rows_launch(Hs, rows, n, T, d, Hr, err, st);
   if (e == cudaSuccess) {  // dW1 = H_r^T (dhid_hi + dhid_lo)
+    const int bnw = pick_bn_wgrad(N);
     GemmProblem g = prob(d, N, n, act_t(Hr, n, d), act_t(dhid, n, N), EPI_ATOMIC);
     g.nseg = 2;
     g.K[1] = n;
     g.A[1] = act_t(Hr, n, d);
     g.B[1] = act_t(dhid_lo, n, N);
-    const int bnw = pick_bn(d, N);
     g.split_k = pick_split(d, N, bnw, n);
     g.epi.out = gr->dW1;
     g.epi.out_f32 = 1;

@@ -32,6 +32,7 @@ struct GemmKParams {
   CUtensorMap mB[GEMM_MAX_PROB][GEMM_MAX_SEG];
   KProb p[GEMM_MAX_PROB];
   int32_t nprob, total_units;
+  int32_t bm;  // M tile of a unit: 128 (one CTA) or 256 (CTA pair, cta_group::2)
 };
 
 template <int BN>
@@ -59,9 +60,8 @@ __device__ __forceinline__ Unit decode_unit(const GemmKParams& P, int u) {
   const int mt = local / q.n_tiles;
   Unit r;
   r.p = p;
-  r.m0 = mt * BM;
-  r.n0 = nt * 0;  // filled by caller with BN
-  r.n0 = nt;
+  r.m0 = mt * P.bm;
+  r.n0 = nt;  // tile index; callers multiply by BN
   r.kb_lo = (int)(((long long)ks * q.kb_total) / q.split_k);
   r.kb_hi = (int)(((long long)(ks + 1) * q.kb_total) / q.split_k);
   return r;
@@ -363,6 +363,172 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_kernel(const __grid_cons
   if (warp == 2) tmem_dealloc<C::TMEM_COLS>(tmem_base);
 }
 
+// ---------------------------------------------------------------- CTA-pair kernel (cta_group::2)
+// Two CTAs of a cluster compute one 256 x 256 tile: CTA r holds A rows [128 r, 128 r + 128) and B
+// columns [128 r, 128 r + 128) of the tile in its shared memory; the leader issues M=256 N=256
+// tcgen05.mma.cta_group::2, each CTA's TMEM receives its 128 rows x 256 columns.  Per SM and
+// k-block this streams 32 KB (vs 48 KB for a 128 x 256 one-CTA tile): half the B traffic, which
+// is what bounds the d x d projections through L2.
+struct PairCfg {
+  static constexpr int STAGES = 6;
+  static constexpr int A_BYTES = 128 * BK * 2;
+  static constexpr int B_BYTES = 128 * BK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int TMEM_COLS = 512;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+};
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
+    gemm_pair_kernel(const __grid_constant__ GemmKParams P) {
+  using C = PairCfg;
+  constexpr int BN = 256;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
+  uint64_t* empty = full + C::STAGES;
+  uint64_t* tfull = empty + C::STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const uint32_t warp = warp_id(), lane = lane_id();
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < C::STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], 16);  // 8 epilogue warps in each CTA of the pair
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc_pair<C::TMEM_COLS>(tmem_slot);
+  if (warp == 0 && lane == 0) {
+    for (int p = 0; p < P.nprob; ++p)
+      for (int s = 0; s < P.p[p].nseg; ++s) {
+        tma_prefetch(&P.mA[p][s]);
+        tma_prefetch(&P.mB[p][s]);
+      }
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+
+  if (warp == 0) {
+    // ============================ TMA producer (both CTAs; bytes land on the leader's barrier)
+    if (elect_one()) {
+      uint32_t it = 0;
+      for (int u = cid; u < P.total_units; u += ncl) {
+        const Unit U = decode_unit(P, u);
+        const KProb& q = P.p[U.p];
+        const int n0 = U.n0 * BN + 128 * (int)rank;
+        const int m0 = U.m0 + 128 * (int)rank;
+        for (int kb = U.kb_lo; kb < U.kb_hi; ++kb, ++it) {
+          const uint32_t stage = it % C::STAGES, use = it / C::STAGES;
+          if (use > 0) mbar_wait(&empty[stage], (use - 1) & 1);
+          int seg, kk;
+          kb_to_seg(q, kb, seg, kk);
+          const int k0 = kk * BK;
+          uint8_t* sA = smem + stage * C::STAGE_BYTES;
+          uint8_t* sB = sA + C::A_BYTES;
+          const uint32_t fb = mapa_shared(smem_u32(&full[stage]), 0);
+          if (leader) mbar_expect_tx(&full[stage], 2 * C::STAGE_BYTES);
+          if (!q.a_mn[seg]) {
+            tma_load_2d_pair(sA, &P.mA[U.p][seg], fb, k0, m0);
+          } else {
+            tma_load_2d_pair(sA, &P.mA[U.p][seg], fb, m0, k0);
+            tma_load_2d_pair(sA + 8192, &P.mA[U.p][seg], fb, m0 + 64, k0);
+          }
+          if (!q.b_mn[seg]) {
+            tma_load_2d_pair(sB, &P.mB[U.p][seg], fb, k0, n0);
+          } else {
+            tma_load_2d_pair(sB, &P.mB[U.p][seg], fb, n0, k0);
+            tma_load_2d_pair(sB + 8192, &P.mB[U.p][seg], fb, n0 + 64, k0);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ============================ MMA issuer (leader CTA only)
+    if (leader && elect_one()) {
+      uint32_t it = 0, tc = 0;
+      for (int u = cid; u < P.total_units; u += ncl, ++tc) {
+        const Unit U = decode_unit(P, u);
+        const KProb& q = P.p[U.p];
+        const uint32_t buf = tc & 1, use = tc >> 1;
+        if (use > 0) mbar_wait(&tempty[buf], (use - 1) & 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + buf * BN;
+        for (int kb = U.kb_lo; kb < U.kb_hi; ++kb, ++it) {
+          const uint32_t stage = it % C::STAGES, suse = it / C::STAGES;
+          mbar_wait(&full[stage], suse & 1);
+          tc_fence_after();
+          int seg, kk;
+          kb_to_seg(q, kb, seg, kk);
+          const uint32_t a_mn = q.a_mn[seg], b_mn = q.b_mn[seg];
+          const uint32_t idesc = idesc_bf16(256, BN, a_mn, b_mn);
+          const uint32_t sA = smem_u32(smem + stage * C::STAGE_BYTES);
+          const uint32_t sB = sA + C::A_BYTES;
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            const uint64_t ad = a_mn ? smem_desc(sA + k * 2048, 8192, 1024, SWZ_128B)
+                                     : smem_desc(sA + k * 32, 16, 1024, SWZ_128B);
+            const uint64_t bd = b_mn ? smem_desc(sB + k * 2048, 8192, 1024, SWZ_128B)
+                                     : smem_desc(sB + k * 32, 16, 1024, SWZ_128B);
+            mma_bf16_ss_pair(d_tmem, ad, bd, idesc, (kb > U.kb_lo || k > 0) ? 1u : 0u);
+          }
+          mma_commit_pair_mc(&empty[stage], 0x3);
+        }
+        mma_commit_pair_mc(&tfull[buf], 0x3);
+      }
+    }
+  } else if (warp >= 4) {
+    // ============================ epilogue (both CTAs: 128 rows x 256 columns each)
+    const uint32_t quarter = warp & 3;
+    const int half = (warp - 4) >> 2;
+    const uint32_t te_remote = mapa_shared(smem_u32(&tempty[0]), 0);
+    uint32_t tc = 0;
+    for (int u = cid; u < P.total_units; u += ncl, ++tc) {
+      const Unit U = decode_unit(P, u);
+      const KProb& q = P.p[U.p];
+      const uint32_t buf = tc & 1, use = tc >> 1;
+      mbar_wait(&tfull[buf], use & 1);
+      tc_fence_after();
+      const int row = U.m0 + 128 * (int)rank + quarter * 32 + lane;
+      const int n0 = U.n0 * BN;
+      for (int c = half; c < BN / 32; c += 2) {
+        const int n0c = n0 + c * 32;
+        if (n0c >= q.N) break;
+        uint32_t r[32];
+        tmem_ld32(tmem_addr(tmem_base, quarter, buf * BN + c * 32), r);
+        tmem_ld_wait();
+        float v[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+        run_epilogue(q.epi, row, q.M, n0c, v);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        if (leader)
+          mbar_arrive(&tempty[buf]);
+        else
+          mbar_arrive_cluster(te_remote + buf * 8);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();
+  tc_fence_after();
+  if (warp == 1) tmem_dealloc_pair<C::TMEM_COLS>(tmem_base);
+}
+
 // ---------------------------------------------------------------- host
 static int num_sms() {
   static int n = 0;
@@ -389,6 +555,20 @@ static bool make_operand_map(CUtensorMap* m, const OperandDesc& o, int box_rows_
   return encode_bf16_map(m, o.ptr, 2, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B);
 }
 
+static cudaError_t launch_pair(const GemmKParams& P, cudaStream_t stream) {
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(gemm_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, PairCfg::SMEM);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  int pairs = num_sms() / 2;
+  if (P.total_units < pairs) pairs = P.total_units;
+  ProfScope ps(PROF_GEMM, stream, 1);
+  gemm_pair_kernel<<<2 * pairs, GEMM_THREADS, PairCfg::SMEM, stream>>>(P);
+  return cudaGetLastError();
+}
+
 template <int BN>
 static cudaError_t launch_bn(const GemmKParams& P, cudaStream_t stream) {
   using C = GemmCfg<BN>;
@@ -409,6 +589,10 @@ cudaError_t gemm_launch(const GemmProblem* probs, int nprob, int bn, cudaStream_
   static GemmKParams P;  // large; filled per launch (host-side only)
   memset(&P, 0, sizeof(P));
   P.nprob = nprob;
+  // CTA pairs (cta_group::2, 256 x 256 tiles) whenever the N tile is 256 and every M spans a pair tile
+  bool pair = bn == 256;
+  for (int p = 0; p < nprob; ++p) pair = pair && probs[p].M >= 256;
+  P.bm = pair ? 256 : BM;
   int total = 0;
   for (int p = 0; p < nprob; ++p) {
     const GemmProblem& g = probs[p];
@@ -423,20 +607,21 @@ cudaError_t gemm_launch(const GemmProblem* probs, int nprob, int bn, cudaStream_
       const OperandDesc& B = g.B[s];
       if (A.cols % 8 || B.cols % 8 || g.K[s] <= 0) return cudaErrorInvalidValue;
       if (!make_operand_map(&P.mA[p][s], A, BM)) return cudaErrorInvalidValue;
-      if (!make_operand_map(&P.mB[p][s], B, bn)) return cudaErrorInvalidValue;
+      if (!make_operand_map(&P.mB[p][s], B, pair ? 128 : bn)) return cudaErrorInvalidValue;
       q.a_mn[s] = A.mn_major;
       q.b_mn[s] = B.mn_major;
       q.kb[s] = (g.K[s] + BK - 1) / BK;
       q.kb_total += q.kb[s];
     }
     q.split_k = g.split_k < 1 ? 1 : (g.split_k > q.kb_total ? q.kb_total : g.split_k);
-    q.m_tiles = (g.M + BM - 1) / BM;
+    q.m_tiles = (g.M + P.bm - 1) / P.bm;
     q.n_tiles = (g.N + bn - 1) / bn;
     q.unit_begin = total;
     q.epi = g.epi;
     total += q.m_tiles * q.n_tiles * q.split_k;
   }
   P.total_units = total;
+  if (pair) return launch_pair(P, stream);
   return bn == 256 ? launch_bn<256>(P, stream) : launch_bn<128>(P, stream);
 }
 

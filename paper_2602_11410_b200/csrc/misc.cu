@@ -50,34 +50,82 @@ __global__ void rope_apply_kernel(const __nv_bfloat16* in, __nv_bfloat16* out, i
 
 // dr: fp32 (dQr accumulator) or bf16 (dKr).  gate (Z) bf16 may be null (no interaction gate):
 // then out_u is unused and out_r (bf16 if r_bf16) receives dQt directly.
-__global__ void rope_gate_bwd_kernel(const void* dr, int dr_f32, const __nv_bfloat16* Xq, const __nv_bfloat16* Z,
-                                     __nv_bfloat16* out_u, void* out_r, int r_bf16, int T, int d, int hd, int use_rope,
-                                     const double* theta, const int64_t* t, const int32_t* row_seq,
-                                     const int32_t* cu) {
+// One thread = 8 consecutive columns (4 pairs) of one row: one dt per thread, 16-byte accesses,
+// the theta table in shared memory.
+__global__ void __launch_bounds__(256) rope_gate_bwd_kernel(const void* dr, int dr_f32, const __nv_bfloat16* Xq,
+                                                            const __nv_bfloat16* Z, __nv_bfloat16* out_u,
+                                                            void* out_r, int r_bf16, int T, int d, int hd,
+                                                            int use_rope, const double* theta, const int64_t* t,
+                                                            const int32_t* row_seq, const int32_t* cu) {
+  __shared__ double th[64];
+  if (threadIdx.x < hd / 2) th[threadIdx.x] = theta[threadIdx.x];
+  __syncthreads();
+  const int per_row = d / 8;
   const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const size_t pairs = (size_t)T * d / 2;
-  if (idx >= pairs) return;
-  const int row = (int)(idx / (d / 2));
-  const int c = (int)(idx % (d / 2)) * 2;
-  float2 g;
-  if (dr_f32)
-    g = reinterpret_cast<const float2*>(dr)[idx];
-  else
-    g = __bfloat1622float2(reinterpret_cast<const __nv_bfloat162*>(dr)[idx]);
-  if (use_rope) rot(g.x, g.y, row_dt(t, row_seq, cu, row), theta[(c % hd) >> 1], -1.f);  // R(-alpha)
-  float2 r = g;
-  if (Z) {
-    const float2 z = __bfloat1622float2(reinterpret_cast<const __nv_bfloat162*>(Z)[idx]);
-    const float2 x = __bfloat1622float2(reinterpret_cast<const __nv_bfloat162*>(Xq)[idx]);
-    const float g0 = __fdividef(1.f, 1.f + __expf(-z.x)), g1 = __fdividef(1.f, 1.f + __expf(-z.y));
-    reinterpret_cast<__nv_bfloat162*>(out_u)[idx] =
-        __floats2bfloat162_rn(g.x * x.x * g0 * (1.f - g0), g.y * x.y * g1 * (1.f - g1));
-    r = make_float2(g.x * g0, g.y * g1);
+  if (idx >= (size_t)T * per_row) return;
+  const int row = (int)(idx / per_row);
+  const int c0 = (int)(idx % per_row) * 8;
+  const size_t off = (size_t)row * d + c0;
+  float g[8];
+  if (dr_f32) {
+    const float4 a = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(dr) + off)[0];
+    const float4 b = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(dr) + off)[1];
+    g[0] = a.x; g[1] = a.y; g[2] = a.z; g[3] = a.w; g[4] = b.x; g[5] = b.y; g[6] = b.z; g[7] = b.w;
+  } else {
+    const uint4 u = *reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(dr) + off);
+    const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float2 f = __bfloat1622float2(h2[e]);
+      g[2 * e] = f.x;
+      g[2 * e + 1] = f.y;
+    }
   }
-  if (r_bf16)
-    reinterpret_cast<__nv_bfloat162*>(out_r)[idx] = __floats2bfloat162_rn(r.x, r.y);
-  else
-    reinterpret_cast<float2*>(out_r)[idx] = r;
+  if (use_rope) {
+    const double dt = row_dt(t, row_seq, cu, row);
+    int hc = c0 % hd;
+#pragma unroll
+    for (int e = 0; e < 8; e += 2) {
+      rot(g[e], g[e + 1], dt, th[hc >> 1], -1.f);  // R(-alpha)
+      hc += 2;
+      if (hc >= hd) hc -= hd;
+    }
+  }
+  float r[8];
+  if (Z) {
+    const uint4 zu = *reinterpret_cast<const uint4*>(Z + off);
+    const uint4 xu = *reinterpret_cast<const uint4*>(Xq + off);
+    const __nv_bfloat162* z2 = reinterpret_cast<const __nv_bfloat162*>(&zu);
+    const __nv_bfloat162* x2 = reinterpret_cast<const __nv_bfloat162*>(&xu);
+    uint32_t uo[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float2 z = __bfloat1622float2(z2[e]);
+      const float2 x = __bfloat1622float2(x2[e]);
+      const float g0 = __fdividef(1.f, 1.f + __expf(-z.x)), g1 = __fdividef(1.f, 1.f + __expf(-z.y));
+      __nv_bfloat162 v = __floats2bfloat162_rn(g[2 * e] * x.x * g0 * (1.f - g0), g[2 * e + 1] * x.y * g1 * (1.f - g1));
+      uo[e] = *reinterpret_cast<uint32_t*>(&v);
+      r[2 * e] = g[2 * e] * g0;
+      r[2 * e + 1] = g[2 * e + 1] * g1;
+    }
+    *reinterpret_cast<uint4*>(out_u + off) = make_uint4(uo[0], uo[1], uo[2], uo[3]);
+  } else {
+#pragma unroll
+    for (int e = 0; e < 8; ++e) r[e] = g[e];
+  }
+  if (r_bf16) {
+    uint32_t ro[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      __nv_bfloat162 v = __floats2bfloat162_rn(r[2 * e], r[2 * e + 1]);
+      ro[e] = *reinterpret_cast<uint32_t*>(&v);
+    }
+    *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(out_r) + off) = make_uint4(ro[0], ro[1], ro[2], ro[3]);
+  } else {
+    float4* o = reinterpret_cast<float4*>(reinterpret_cast<float*>(out_r) + off);
+    o[0] = make_float4(r[0], r[1], r[2], r[3]);
+    o[1] = make_float4(r[4], r[5], r[6], r[7]);
+  }
 }
 
 __global__ void gather_rows_kernel(const uint8_t* H, const int32_t* rows, int n, int T, int row_bytes, uint8_t* out,
@@ -203,9 +251,9 @@ cudaError_t rope_gate_bwd_launch(const void* dr, int dr_f32, const void* Xq, con
                                  int r_bf16, int T, int d, int hd, int use_rope, const double* theta, const int64_t* t,
                                  const int32_t* row_seq, const int32_t* cu, cudaStream_t st) {
   ProfScope ps(PROF_OTHER, st, 1);
-  const size_t pairs = (size_t)T * d / 2;
-  if (pairs)
-    rope_gate_bwd_kernel<<<blocks(pairs, 256), 256, 0, st>>>(
+  const size_t work = (size_t)T * d / 8;
+  if (work)
+    rope_gate_bwd_kernel<<<blocks(work, 256), 256, 0, st>>>(
         dr, dr_f32, reinterpret_cast<const __nv_bfloat16*>(Xq), reinterpret_cast<const __nv_bfloat16*>(Z),
         reinterpret_cast<__nv_bfloat16*>(out_u), out_r, r_bf16, T, d, hd, use_rope, theta, t, row_seq, cu);
   return cudaGetLastError();
