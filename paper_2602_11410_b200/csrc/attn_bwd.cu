@@ -1,60 +1,251 @@
-// A10: attention backward (adjoint of PAPER.md Eq. 7) for the packed, session-masked layout.
+// A10: attention backward (adjoint of PAPER.md Eq. 7) for the packed, session-masked layout,
+// as two atomic-free kernels (deterministic; no fp32 reductions through L2):
 //
-// One CTA per (128-key tile of one sequence, head), k-tiles in descending cost order.  K_j, V_j
-// stay in shared memory; the CTA walks the q-tiles that see k-tile j (transpose of the forward
-// visit rule: q-tile i visits j iff j < nf_i or kt2_i <= j <= i; list built once in smem), and per
-// q-tile i:
-//   S^T  = K_j Q_i^T           -> TMEM [0,128)        dP^T = V_j dO_i^T -> TMEM [128,256)
-//   P^T  = exp2(S^T scale log2e - LSE_i log2e) on visible cells (predicate only on non-FULL pairs)
-//   dS^T = P^T (dP^T - D_i) scale
-//   P^T, dS^T are written back as packed bf16 over the consumed S^T / dP^T columns and feed
-//   dV += P^T dO_i and dK += dS^T Q_i as TMEM-A (TS) MMAs into TMEM [256,384) / [384,512);
-//   dS^T also goes to shared memory for dQ_i = dS K_j (MN-major A), written over [128,256) and
-//   drained by four dedicated warps with fp32 vector atomics while the next S^T is computed.
-//
-//   warp 0      : TMA producer (K_j, V_j once; Q_i, dO_i per q-tile)
-//   warp 1      : TMEM owner + MMA issuer
-//   warps 2..5  : thread = key row (TMEM lane): P^T, dS^T
-//   warps 6..9  : thread = query row: dQ drain; final dK, dV epilogue
+// attn_bwd_dq_kernel  — one CTA per (q-tile, head), k-tiles visited exactly as in the forward:
+//   S_j = Q K_j^T (TMEM, double-buffered), dP_j = dO V_j^T (TMEM);  thread = query row:
+//   P = exp2(S log2e/sqrt(hd) - LSE log2e) on visible cells, dS = P (dP - D) / sqrt(hd) written
+//   as packed bf16 over the consumed dP columns;  dQ += dS K_j as a TMEM-A (TS) MMA; dQ leaves
+//   TMEM once, at the end.
+// attn_bwd_dkv_kernel — one CTA per (k-tile, head), walking the q-tiles that see it (transpose of
+//   the visit rule, list built once in smem):  S^T = K Q_i^T, dP^T = V dO_i^T;  thread = key row
+//   (two warps per TMEM lane quarter, 64 q columns each): P^T, dS^T as packed bf16 over the
+//   consumed columns;  dV += P^T dO_i, dK += dS^T Q_i as TS MMAs; Q_i / dO_i double-buffered.
+// The extra S/dP recompute (7 MMAs per tile pair instead of 5) buys the removal of 1.1 GB of dQ
+// atomics per C4 step and of the drain -> dP dependency.
 #include "attn_common.cuh"
 #include "prof.cuh"
 
 namespace cadet {
 
-template <int HD>
-struct BwdCfg {
-  using G = HeadGeom<HD>;
-  static constexpr int K_OFF = 0;
-  static constexpr int V_OFF = K_OFF + G::TILE_BYTES;
-  static constexpr int Q_OFF = V_OFF + G::TILE_BYTES;
-  static constexpr int DO_OFF = Q_OFF + G::TILE_BYTES;
-  static constexpr int DS_OFF = DO_OFF + G::TILE_BYTES;  // dS^T bf16 [128 keys x 128 q], 128B swizzle
-  static constexpr int VEC_OFF = DS_OFF + 32768;          // [2][4][128] x 4 B: lse2, D, e, q|pp
-  static constexpr int LIST_OFF = VEC_OFF + 2 * 4 * 128 * 4;
-  static constexpr int MAX_LIST = 512;                    // visited q-tiles per k-tile (T/128 bound)
-  static constexpr int BAR_OFF = LIST_OFF + MAX_LIST * 4;
-  static constexpr int SMEM = BAR_OFF + 256 + 1024;
-  static constexpr int S_COL = 0, DP_COL = 128, DV_COL = 256, DK_COL = 384;
-  static constexpr int THREADS = 320;
-};
-
-struct BwdBars {
-  uint64_t kv_full, qd_full, qd_empty, s_full, dp_full, pds_ready, dq_full, dq_free;
-  uint32_t tmem_base;
-  int32_t n_it;
-};
-
+__device__ __forceinline__ int visit_tile_b(const QTileInfo& qi, int j) { return j < qi.nf ? j : qi.kt2 + (j - qi.nf); }
 __device__ __forceinline__ bool q_sees_k(const QTileInfo& qi, int kt) {
   return kt < qi.nf || (kt >= qi.kt2 && kt <= qi.qt);
 }
 
+// ============================================================================ dQ kernel
+template <int HD>
+struct DqCfg {
+  using G = HeadGeom<HD>;
+  static constexpr int Q_OFF = 0;
+  static constexpr int DO_OFF = Q_OFF + G::TILE_BYTES;
+  static constexpr int K_OFF = DO_OFF + G::TILE_BYTES;        // two stages
+  static constexpr int V_OFF = K_OFF + 2 * G::TILE_BYTES;     // two stages
+  static constexpr int BAR_OFF = V_OFF + 2 * G::TILE_BYTES;
+  static constexpr int SMEM = BAR_OFF + 256 + 1024;
+  static constexpr int S_COL = 0, DP_COL = 256, DQ_COL = 384;  // S double-buffered
+};
+
+struct DqBars {
+  uint64_t qd_full, k_full[2], k_empty[2], v_full[2], v_empty[2], s_full[2], s_free[2], dp_full, ds_ready, dq_done;
+  uint32_t tmem_base;
+};
+
+template <int HD>
+__global__ void __launch_bounds__(192, 1)
+    attn_bwd_dq_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constant__ CUtensorMap mK,
+                       const __grid_constant__ CUtensorMap mV, const __grid_constant__ CUtensorMap mdO,
+                       const AttnParams p) {
+  using G = HeadGeom<HD>;
+  using C = DqCfg<HD>;
+  const int nq_total = p.plan.counters[0];
+  const int b = blockIdx.x / p.H;
+  const int h = blockIdx.x % p.H;
+  if (b >= nq_total) return;
+  const QTileInfo qi = p.plan.qinfo[p.plan.fwd_order[b]];
+  const int sa = p.cu[qi.seq], se = p.cu[qi.seq + 1];
+  const int q0 = sa + qi.qt * 128;
+  const int rows_valid = min(128, se - q0);
+  const int n_kv = qi.nf + (qi.qt + 1 - qi.kt2);
+
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  DqBars* bars = reinterpret_cast<DqBars*>(smem + C::BAR_OFF);
+  const uint32_t warp = warp_id(), lane = lane_id();
+  if (threadIdx.x == 0) {
+    mbar_init(&bars->qd_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&bars->k_full[i], 1);
+      mbar_init(&bars->k_empty[i], 1);
+      mbar_init(&bars->v_full[i], 1);
+      mbar_init(&bars->v_empty[i], 1);
+      mbar_init(&bars->s_full[i], 1);
+      mbar_init(&bars->s_free[i], 128);
+    }
+    mbar_init(&bars->dp_full, 1);
+    mbar_init(&bars->ds_ready, 128);
+    mbar_init(&bars->dq_done, 1);
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc<512>(&bars->tmem_base);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = bars->tmem_base;
+
+  if (warp == 0) {
+    if (elect_one()) {
+      mbar_expect_tx(&bars->qd_full, 2 * G::TILE_BYTES);
+#pragma unroll
+      for (int blk = 0; blk < G::NB; ++blk) {
+        tma_load_3d(smem + C::Q_OFF + blk * G::BLK, &mQ, &bars->qd_full, blk * G::CB, h, q0);
+        tma_load_3d(smem + C::DO_OFF + blk * G::BLK, &mdO, &bars->qd_full, blk * G::CB, h, q0);
+      }
+      for (int j = 0; j < n_kv; ++j) {
+        const int st = j & 1, use = j >> 1;
+        const int krow = sa + visit_tile_b(qi, j) * 128;
+        if (use > 0) mbar_wait(&bars->k_empty[st], (use - 1) & 1);
+        mbar_expect_tx(&bars->k_full[st], G::TILE_BYTES);
+#pragma unroll
+        for (int blk = 0; blk < G::NB; ++blk)
+          tma_load_3d(smem + C::K_OFF + st * G::TILE_BYTES + blk * G::BLK, &mK, &bars->k_full[st], blk * G::CB, h,
+                      krow);
+        if (use > 0) mbar_wait(&bars->v_empty[st], (use - 1) & 1);
+        mbar_expect_tx(&bars->v_full[st], G::TILE_BYTES);
+#pragma unroll
+        for (int blk = 0; blk < G::NB; ++blk)
+          tma_load_3d(smem + C::V_OFF + st * G::TILE_BYTES + blk * G::BLK, &mV, &bars->v_full[st], blk * G::CB, h,
+                      krow);
+      }
+    }
+  } else if (warp == 1) {
+    if (elect_one()) {
+      const uint32_t id_s = idesc_bf16(128, 128, 0, 0);
+      const uint32_t id_q = idesc_bf16(128, G::HDP, 0, 1);
+      const uint32_t sQ = smem_u32(smem + C::Q_OFF), sdO = smem_u32(smem + C::DO_OFF);
+      mbar_wait(&bars->qd_full, 0);
+      auto issue_s = [&](int j) {
+        const int st = j & 1, use = j >> 1;
+        if (use > 0) mbar_wait(&bars->s_free[st], (use - 1) & 1);
+        mbar_wait(&bars->k_full[st], use & 1);
+        tc_fence_after();
+        const uint32_t sK = smem_u32(smem + C::K_OFF + st * G::TILE_BYTES);
+#pragma unroll
+        for (int kk = 0; kk < G::HDP / 16; ++kk)
+          mma_bf16_ss(tmem + C::S_COL + st * 128, kmajor_desc<HD>(sQ, kk), kmajor_desc<HD>(sK, kk), id_s,
+                      kk > 0 ? 1u : 0u);
+        mma_commit(&bars->s_full[st]);
+      };
+      if (n_kv > 0) issue_s(0);
+      for (int j = 0; j < n_kv; ++j) {
+        const int st = j & 1, use = j >> 1;
+        // dP_j over dS_{j-1}: in-order after dQ_{j-1}, which read it
+        mbar_wait(&bars->v_full[st], use & 1);
+        tc_fence_after();
+        const uint32_t sV = smem_u32(smem + C::V_OFF + st * G::TILE_BYTES);
+#pragma unroll
+        for (int kk = 0; kk < G::HDP / 16; ++kk)
+          mma_bf16_ss(tmem + C::DP_COL, kmajor_desc<HD>(sdO, kk), kmajor_desc<HD>(sV, kk), id_s, kk > 0 ? 1u : 0u);
+        mma_commit(&bars->dp_full);
+        mma_commit(&bars->v_empty[st]);
+        if (j + 1 < n_kv) issue_s(j + 1);
+        mbar_wait(&bars->ds_ready, j & 1);
+        tc_fence_after();
+        const uint32_t sK = smem_u32(smem + C::K_OFF + st * G::TILE_BYTES);
+#pragma unroll
+        for (int kk = 0; kk < 128 / 16; ++kk)
+          mma_bf16_ts(tmem + C::DQ_COL, tmem + C::DP_COL + kk * 8, mnmajor_desc<HD>(sK, kk), id_q,
+                      (j > 0 || kk > 0) ? 1u : 0u);
+        mma_commit(&bars->k_empty[st]);
+      }
+      mma_commit(&bars->dq_done);
+    }
+  } else {
+    const uint32_t quarter = warp & 3;
+    const int rt = quarter * 32 + lane;
+    const int r = q0 + rt;
+    const bool valid = rt < rows_valid;
+    const int e_r = valid ? p.plan.kv_end[r] : 0;
+    const bool pp = valid ? (p.plan.row_pp[r] != 0) : false;
+    const float lse2 = valid ? p.lse[(size_t)h * p.T + r] * 1.4426950408889634f : 0.f;
+    const float Dr = valid ? p.D[(size_t)h * p.T + r] : 0.f;
+    const float sl2 = p.scale_log2;
+    for (int j = 0; j < n_kv; ++j) {
+      const int st = j & 1, use = j >> 1;
+      const int k0 = sa + visit_tile_b(qi, j) * 128;
+      const bool partial = !valid || (e_r < k0 + 128);
+      mbar_wait(&bars->s_full[st], use & 1);
+      mbar_wait(&bars->dp_full, j & 1);
+      tc_fence_after();
+#pragma unroll 1
+      for (int c = 0; c < 4; ++c) {
+        uint32_t us[32], ud[32];
+        tmem_ld32(tmem_addr(tmem, quarter, C::S_COL + st * 128 + c * 32), us);
+        tmem_ld32(tmem_addr(tmem, quarter, C::DP_COL + c * 32), ud);
+        tmem_ld_wait();
+        uint32_t w[16];
+        const uint32_t m = !partial ? 0xFFFFFFFFu : (valid ? row_mask32(e_r, r, pp, k0 + c * 32) : 0u);
+#pragma unroll
+        for (int q = 0; q < 32; q += 2) {
+          float ds[2];
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            float pr = fast_exp2(fmaf(__uint_as_float(us[q + e]), sl2, -lse2));
+            if (!((m >> (q + e)) & 1u)) pr = 0.f;
+            ds[e] = pr * (__uint_as_float(ud[q + e]) - Dr) * p.scale;
+          }
+          w[q >> 1] = pack_bf16(ds[0], ds[1]);
+        }
+        tmem_st16(tmem_addr(tmem, quarter, C::DP_COL + c * 16), w);  // over dP chunk c/2 (consumed)
+      }
+      tmem_st_wait();
+      tc_fence_before();
+      mbar_arrive(&bars->s_free[st]);
+      mbar_arrive(&bars->ds_ready);
+    }
+    if (n_kv > 0) {
+      mbar_wait(&bars->dq_done, 0);
+      tc_fence_after();
+    }
+#pragma unroll 1
+    for (int c = 0; c < G::HDP / 32; ++c) {
+      uint32_t u[32];
+      tmem_ld32(tmem_addr(tmem, quarter, C::DQ_COL + c * 32), u);
+      tmem_ld_wait();
+      if (valid) {
+        float* o = p.dQ + (size_t)r * p.d + (size_t)h * p.hd + c * 32;
+        const int ncol = min(32, p.hd - c * 32);
+        for (int q = 0; q < ncol; q += 4)
+          *reinterpret_cast<float4*>(o + q) = make_float4(__uint_as_float(u[q]), __uint_as_float(u[q + 1]),
+                                                          __uint_as_float(u[q + 2]), __uint_as_float(u[q + 3]));
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 1) tmem_dealloc<512>(tmem);
+}
+
+// ============================================================================ dK / dV kernel
+template <int HD>
+struct DkvCfg {
+  using G = HeadGeom<HD>;
+  static constexpr int K_OFF = 0;
+  static constexpr int V_OFF = K_OFF + G::TILE_BYTES;
+  static constexpr int Q_OFF = V_OFF + G::TILE_BYTES;          // two stages
+  static constexpr int DO_OFF = Q_OFF + 2 * G::TILE_BYTES;     // two stages
+  static constexpr int VEC_OFF = DO_OFF + 2 * G::TILE_BYTES;   // [2][4][128] x 4 B: lse2, D, e, q|pp
+  static constexpr int LIST_OFF = VEC_OFF + 2 * 4 * 128 * 4;
+  static constexpr int MAX_LIST = 512;
+  static constexpr int BAR_OFF = LIST_OFF + MAX_LIST * 4;
+  static constexpr int SMEM = BAR_OFF + 256 + 1024;
+  static constexpr int S_COL = 0, DP_COL = 128, DV_COL = 256, DK_COL = 384;
+  static constexpr int THREADS = 320;  // producer, MMA, 8 compute warps (two per TMEM lane quarter)
+};
+
+struct DkvBars {
+  uint64_t kv_full, q_full[2], q_empty[2], do_full[2], do_empty[2], s_full, dp_full, pds_ready, mma_done;
+  uint32_t tmem_base;
+  int32_t n_it;
+};
+
 template <int HD>
 __global__ void __launch_bounds__(320, 1)
-    attn_bwd_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constant__ CUtensorMap mK,
-                    const __grid_constant__ CUtensorMap mV, const __grid_constant__ CUtensorMap mdO,
-                    const AttnParams p) {
+    attn_bwd_dkv_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constant__ CUtensorMap mK,
+                        const __grid_constant__ CUtensorMap mV, const __grid_constant__ CUtensorMap mdO,
+                        const AttnParams p) {
   using G = HeadGeom<HD>;
-  using C = BwdCfg<HD>;
+  using C = DkvCfg<HD>;
   const int nq_total = p.plan.counters[0];
   const int b = blockIdx.x / p.H;
   const int h = blockIdx.x % p.H;
@@ -63,20 +254,19 @@ __global__ void __launch_bounds__(320, 1)
   const QTileInfo ki = p.plan.qinfo[g];
   const int kt = ki.qt;
   const int sa = p.cu[ki.seq], se = p.cu[ki.seq + 1];
-  const int tile0 = g - kt;  // tile index of q-tile 0 of this sequence
+  const int tile0 = g - kt;
   const int nq_s = (se - sa + 127) / 128;
   const int k0 = sa + kt * 128;
   const int keys_valid = min(128, se - k0);
 
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  BwdBars* bars = reinterpret_cast<BwdBars*>(smem + C::BAR_OFF);
+  DkvBars* bars = reinterpret_cast<DkvBars*>(smem + C::BAR_OFF);
   float* vec = reinterpret_cast<float*>(smem + C::VEC_OFF);
   int* list = reinterpret_cast<int*>(smem + C::LIST_OFF);
   const uint32_t warp = warp_id(), lane = lane_id();
 
   if (warp == 0) {
-    // visited q-tiles (and whether the (q-tile, k-tile) pair is FULL) -> smem list
     int n = 0;
     for (int base = kt; base < nq_s; base += 32) {
       const int qt = base + (int)lane;
@@ -85,7 +275,8 @@ __global__ void __launch_bounds__(320, 1)
         const QTileInfo qi = p.plan.qinfo[tile0 + qt];
         if (q_sees_k(qi, kt)) {
           const bool full = qi.rows == 128 && qi.emin >= (kt + 1) * 128;
-          entry = qt | (full ? (1 << 30) : 0);
+          const bool near = qt - kt <= 1;  // diagonal / pair-prev cells can only occur here
+          entry = qt | (full ? (1 << 30) : 0) | (near ? (1 << 29) : 0);
         }
       }
       const uint32_t m = __ballot_sync(0xffffffffu, entry >= 0);
@@ -96,13 +287,16 @@ __global__ void __launch_bounds__(320, 1)
     if (lane == 0) {
       bars->n_it = min(n, C::MAX_LIST);
       mbar_init(&bars->kv_full, 1);
-      mbar_init(&bars->qd_full, 1);
-      mbar_init(&bars->qd_empty, 1);
+      for (int i = 0; i < 2; ++i) {
+        mbar_init(&bars->q_full[i], 1);
+        mbar_init(&bars->q_empty[i], 1);
+        mbar_init(&bars->do_full[i], 1);
+        mbar_init(&bars->do_empty[i], 1);
+      }
       mbar_init(&bars->s_full, 1);
       mbar_init(&bars->dp_full, 1);
-      mbar_init(&bars->pds_ready, 128);
-      mbar_init(&bars->dq_full, 1);
-      mbar_init(&bars->dq_free, 128);
+      mbar_init(&bars->pds_ready, 256);
+      mbar_init(&bars->mma_done, 1);
       fence_mbar_init();
     }
   }
@@ -114,7 +308,6 @@ __global__ void __launch_bounds__(320, 1)
   const int n_it = bars->n_it;
 
   if (warp == 0) {
-    // ============================ producer
     if (elect_one()) {
       mbar_expect_tx(&bars->kv_full, 2 * G::TILE_BYTES);
 #pragma unroll
@@ -123,38 +316,40 @@ __global__ void __launch_bounds__(320, 1)
         tma_load_3d(smem + C::V_OFF + blk * G::BLK, &mV, &bars->kv_full, blk * G::CB, h, k0);
       }
       for (int it = 0; it < n_it; ++it) {
+        const int st = it & 1, use = it >> 1;
         const int q0 = sa + (list[it] & 0xFFFF) * 128;
-        if (it > 0) mbar_wait(&bars->qd_empty, (it - 1) & 1);
-        mbar_expect_tx(&bars->qd_full, 2 * G::TILE_BYTES);
+        if (use > 0) mbar_wait(&bars->q_empty[st], (use - 1) & 1);  // list entry: qt | full<<30 | near<<29
+        mbar_expect_tx(&bars->q_full[st], G::TILE_BYTES);
 #pragma unroll
-        for (int blk = 0; blk < G::NB; ++blk) {
-          tma_load_3d(smem + C::Q_OFF + blk * G::BLK, &mQ, &bars->qd_full, blk * G::CB, h, q0);
-          tma_load_3d(smem + C::DO_OFF + blk * G::BLK, &mdO, &bars->qd_full, blk * G::CB, h, q0);
-        }
+        for (int blk = 0; blk < G::NB; ++blk)
+          tma_load_3d(smem + C::Q_OFF + st * G::TILE_BYTES + blk * G::BLK, &mQ, &bars->q_full[st], blk * G::CB, h, q0);
+        if (use > 0) mbar_wait(&bars->do_empty[st], (use - 1) & 1);
+        mbar_expect_tx(&bars->do_full[st], G::TILE_BYTES);
+#pragma unroll
+        for (int blk = 0; blk < G::NB; ++blk)
+          tma_load_3d(smem + C::DO_OFF + st * G::TILE_BYTES + blk * G::BLK, &mdO, &bars->do_full[st], blk * G::CB, h,
+                      q0);
       }
     }
   } else if (warp == 1) {
-    // ============================ MMA issuer
     if (elect_one()) {
       const uint32_t id_s = idesc_bf16(128, 128, 0, 0);
       const uint32_t id_kv = idesc_bf16(128, G::HDP, 0, 1);
-      const uint32_t id_q = idesc_bf16(128, G::HDP, 1, 1);
       const uint32_t sK = smem_u32(smem + C::K_OFF), sV = smem_u32(smem + C::V_OFF);
-      const uint32_t sQ = smem_u32(smem + C::Q_OFF), sdO = smem_u32(smem + C::DO_OFF);
-      const uint32_t sDS = smem_u32(smem + C::DS_OFF);
       mbar_wait(&bars->kv_full, 0);
       for (int it = 0; it < n_it; ++it) {
-        mbar_wait(&bars->qd_full, it & 1);
+        const int st = it & 1, use = it >> 1;
+        const uint32_t sQ = smem_u32(smem + C::Q_OFF + st * G::TILE_BYTES);
+        const uint32_t sdO = smem_u32(smem + C::DO_OFF + st * G::TILE_BYTES);
+        // S^T_i over P^T_{i-1} and dP^T_i over dS^T_{i-1}: in-order after dV_{i-1} / dK_{i-1}
+        mbar_wait(&bars->q_full[st], use & 1);
         tc_fence_after();
-        // S^T_i over the P^T_{i-1} columns: in-order after dV_{i-1}, which read them.
 #pragma unroll
         for (int kk = 0; kk < G::HDP / 16; ++kk)
           mma_bf16_ss(tmem + C::S_COL, kmajor_desc<HD>(sK, kk), kmajor_desc<HD>(sQ, kk), id_s, kk > 0 ? 1u : 0u);
         mma_commit(&bars->s_full);
-        if (it > 0) {
-          mbar_wait(&bars->dq_free, (it - 1) & 1);  // dQ_{i-1} drained from [128, 256)
-          tc_fence_after();
-        }
+        mbar_wait(&bars->do_full[st], use & 1);
+        tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < G::HDP / 16; ++kk)
           mma_bf16_ss(tmem + C::DP_COL, kmajor_desc<HD>(sV, kk), kmajor_desc<HD>(sdO, kk), id_s, kk > 0 ? 1u : 0u);
@@ -165,174 +360,141 @@ __global__ void __launch_bounds__(320, 1)
         for (int kk = 0; kk < 128 / 16; ++kk)
           mma_bf16_ts(tmem + C::DV_COL, tmem + C::S_COL + kk * 8, mnmajor_desc<HD>(sdO, kk), id_kv,
                       (it > 0 || kk > 0) ? 1u : 0u);
+        mma_commit(&bars->do_empty[st]);
 #pragma unroll
         for (int kk = 0; kk < 128 / 16; ++kk)
           mma_bf16_ts(tmem + C::DK_COL, tmem + C::DP_COL + kk * 8, mnmajor_desc<HD>(sQ, kk), id_kv,
                       (it > 0 || kk > 0) ? 1u : 0u);
-        mma_commit(&bars->qd_empty);
-        // dQ_i = dS K_j over the dS^T columns: in-order after dK_i, which read them.
-#pragma unroll
-        for (int kk = 0; kk < 128 / 16; ++kk)
-          mma_bf16_ss(tmem + C::DP_COL, p_mnmajor_desc(sDS, kk), mnmajor_desc<HD>(sK, kk), id_q, kk > 0 ? 1u : 0u);
-        mma_commit(&bars->dq_full);
+        mma_commit(&bars->q_empty[st]);
       }
+      mma_commit(&bars->mma_done);
     }
-  } else if (warp < 6) {
-    // ============================ P^T / dS^T warps (thread = key row)
+  } else {
+    // thread = key row; warps 2..5 take q columns [0, 64), warps 6..9 columns [64, 128)
     const uint32_t quarter = warp & 3;
+    const int half = (warp - 2) >> 2;
     const int tr = quarter * 32 + lane;
-    const int ct = threadIdx.x - 64;  // 0..127 vector-loader index
+    const int ct = threadIdx.x - 64;  // 0..255; the first 128 load the per-query vectors
     const int key = k0 + tr;
     const bool key_valid = tr < keys_valid;
     const float sl2 = p.scale_log2;
     const float LOG2E = 1.4426950408889634f;
-    uint8_t* sDS = smem + C::DS_OFF;
+    float nl = 0.f, nd = 0.f;
+    int ne = -1, nw = -2;
+    auto fetch = [&](int it) {
+      if (ct >= 128) return;
+      const int q = sa + (list[it] & 0xFFFF) * 128 + ct;
+      const bool v = q < se;
+      nl = v ? p.lse[(size_t)h * p.T + q] * LOG2E : INFINITY;
+      nd = v ? p.D[(size_t)h * p.T + q] : 0.f;
+      ne = v ? p.plan.kv_end[q] : -1;
+      nw = v ? (q | (p.plan.row_pp[q] ? (1 << 30) : 0)) : -2;
+    };
+    if (n_it > 0) fetch(0);
     for (int it = 0; it < n_it; ++it) {
-      const int ent = list[it];
-      const bool full = (ent >> 30) & 1;
-      const int q0 = sa + (ent & 0xFFFF) * 128;
-      const int qvalid = min(128, se - q0);
+      const bool full = (list[it] >> 30) & 1;
+      const bool near = (list[it] >> 29) & 1;
       float* vb = vec + (it & 1) * 512;
       int* vbi = reinterpret_cast<int*>(vb);
-      {
-        const int q = q0 + ct;
-        const bool v = ct < qvalid;
-        vb[ct] = v ? p.lse[(size_t)h * p.T + q] * LOG2E : INFINITY;
-        vb[128 + ct] = v ? p.D[(size_t)h * p.T + q] : 0.f;
-        vbi[256 + ct] = v ? p.plan.kv_end[q] : -1;
-        vbi[384 + ct] = v ? (q | (p.plan.row_pp[q] ? (1 << 30) : 0)) : -2;
+      if (ct < 128) {
+        vb[ct] = nl;
+        vb[128 + ct] = nd;
+        vbi[256 + ct] = ne;
+        vbi[384 + ct] = nw;
       }
-      named_bar_sync(1, 128);
+      if (it + 1 < n_it) fetch(it + 1);
+      named_bar_sync(1, 256);
       mbar_wait(&bars->s_full, it & 1);
-      tc_fence_after();
-      float pr[128];
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        uint32_t us[32];
-        tmem_ld32(tmem_addr(tmem, quarter, C::S_COL + c * 32), us);
-        tmem_ld_wait();
-#pragma unroll
-        for (int q4 = 0; q4 < 32; q4 += 4) {
-          const float4 l4 = *reinterpret_cast<const float4*>(vb + c * 32 + q4);  // broadcast LDS.128
-          const float lv[4] = {l4.x, l4.y, l4.z, l4.w};
-#pragma unroll
-          for (int e = 0; e < 4; ++e) pr[c * 32 + q4 + e] = fast_exp2(fmaf(__uint_as_float(us[q4 + e]), sl2, -lv[e]));
-        }
-        if (!full) {
-#pragma unroll
-          for (int q4 = 0; q4 < 32; q4 += 4) {
-            const int4 e4 = *reinterpret_cast<const int4*>(vbi + 256 + c * 32 + q4);
-            const int4 w4 = *reinterpret_cast<const int4*>(vbi + 384 + c * 32 + q4);
-            const int ev[4] = {e4.x, e4.y, e4.z, e4.w}, wv[4] = {w4.x, w4.y, w4.z, w4.w};
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const int qw = wv[e];
-              const int qq = qw & ~(1 << 30);
-              const bool ppq = (qw >= 0) && (qw & (1 << 30));
-              const bool ok = key_valid && qw >= 0 && ((key < ev[e]) || (key == qq) || (ppq && key == qq - 1));
-              if (!ok) pr[c * 32 + q4 + e] = 0.f;
-            }
-          }
-        }
-      }
-      // P^T (bf16) over the consumed S^T columns [0, 64)
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        uint32_t w[16];
-#pragma unroll
-        for (int q = 0; q < 32; q += 2) w[q >> 1] = pack_bf16(pr[c * 32 + q], pr[c * 32 + q + 1]);
-        tmem_st16(tmem_addr(tmem, quarter, C::S_COL + c * 16), w);
-      }
       mbar_wait(&bars->dp_full, it & 1);
       tc_fence_after();
-      if (it > 0) mbar_wait(&bars->dq_full, (it - 1) & 1);  // dQ_{i-1} MMA has finished reading dS smem
+      uint32_t wp[2][16], wd[2][16];
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        uint32_t ud[32];
+      for (int cc = 0; cc < 2; ++cc) {
+        const int c = half * 2 + cc;
+        uint32_t us[32], ud[32];
+        tmem_ld32(tmem_addr(tmem, quarter, C::S_COL + c * 32), us);
         tmem_ld32(tmem_addr(tmem, quarter, C::DP_COL + c * 32), ud);
         tmem_ld_wait();
-        uint32_t w[16];
 #pragma unroll
         for (int q4 = 0; q4 < 32; q4 += 4) {
+          const float4 l4 = *reinterpret_cast<const float4*>(vb + c * 32 + q4);
           const float4 d4 = *reinterpret_cast<const float4*>(vb + 128 + c * 32 + q4);
-          const float dv[4] = {d4.x, d4.y, d4.z, d4.w};
-          float ds[4];
+          const float lv[4] = {l4.x, l4.y, l4.z, l4.w}, dv[4] = {d4.x, d4.y, d4.z, d4.w};
+          float pv[4], sv[4];
 #pragma unroll
-          for (int e = 0; e < 4; ++e) ds[e] = pr[c * 32 + q4 + e] * (__uint_as_float(ud[q4 + e]) - dv[e]) * p.scale;
-          w[q4 >> 1] = pack_bf16(ds[0], ds[1]);
-          w[(q4 >> 1) + 1] = pack_bf16(ds[2], ds[3]);
+          for (int e = 0; e < 4; ++e) pv[e] = fast_exp2(fmaf(__uint_as_float(us[q4 + e]), sl2, -lv[e]));
+          if (!full) {
+            const int4 e4 = *reinterpret_cast<const int4*>(vbi + 256 + c * 32 + q4);
+            const int ev[4] = {e4.x, e4.y, e4.z, e4.w};  // -1 for query rows outside the sequence
+            if (!near) {  // far pair: only the visible prefix can admit this key
+#pragma unroll
+              for (int e = 0; e < 4; ++e)
+                if (!(key_valid && key < ev[e])) pv[e] = 0.f;
+            } else {
+              const int4 w4 = *reinterpret_cast<const int4*>(vbi + 384 + c * 32 + q4);
+              const int wv[4] = {w4.x, w4.y, w4.z, w4.w};
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const int qw = wv[e];
+                const int qq = qw & ~(1 << 30);
+                const bool ppq = (qw >= 0) && (qw & (1 << 30));
+                const bool ok = key_valid && qw >= 0 && ((key < ev[e]) || (key == qq) || (ppq && key == qq - 1));
+                if (!ok) pv[e] = 0.f;
+              }
+            }
+          }
+#pragma unroll
+          for (int e = 0; e < 4; ++e) sv[e] = pv[e] * (__uint_as_float(ud[q4 + e]) - dv[e]) * p.scale;
+          wp[cc][q4 >> 1] = pack_bf16(pv[0], pv[1]);
+          wp[cc][(q4 >> 1) + 1] = pack_bf16(pv[2], pv[3]);
+          wd[cc][q4 >> 1] = pack_bf16(sv[0], sv[1]);
+          wd[cc][(q4 >> 1) + 1] = pack_bf16(sv[2], sv[3]);
         }
-        tmem_st16(tmem_addr(tmem, quarter, C::DP_COL + c * 16), w);
+      }
+      // every S^T / dP^T column is in registers before any P^T / dS^T column overwrites them
+      tc_fence_before();
+      named_bar_sync(2, 256);
+      tc_fence_after();
 #pragma unroll
-        for (int ch = 0; ch < 4; ++ch)
-          *reinterpret_cast<uint4*>(sDS + p_off(tr, c * 32 + ch * 8)) =
-              make_uint4(w[ch * 4], w[ch * 4 + 1], w[ch * 4 + 2], w[ch * 4 + 3]);
+      for (int cc = 0; cc < 2; ++cc) {
+        const int c = half * 2 + cc;
+        tmem_st16(tmem_addr(tmem, quarter, C::S_COL + c * 16), wp[cc]);
+        tmem_st16(tmem_addr(tmem, quarter, C::DP_COL + c * 16), wd[cc]);
       }
       tmem_st_wait();
-      fence_proxy_async_smem();
       tc_fence_before();
       mbar_arrive(&bars->pds_ready);
     }
-  } else {
-    // ============================ dQ drain warps (thread = query row), then dK / dV epilogue
-    const uint32_t quarter = warp & 3;
-    const int tr = quarter * 32 + lane;
-    for (int it = 0; it < n_it; ++it) {
-      const int q0 = sa + (list[it] & 0xFFFF) * 128;
-      const int q = q0 + tr;
-      const bool qv = q < se;
-      mbar_wait(&bars->dq_full, it & 1);
-      tc_fence_after();
-#pragma unroll 1
-      for (int c = 0; c < G::HDP / 32; ++c) {
-        uint32_t u[32];
-        tmem_ld32(tmem_addr(tmem, quarter, C::DP_COL + c * 32), u);
-        tmem_ld_wait();
-        if (qv) {
-          float* dst = p.dQ + (size_t)q * p.d + (size_t)h * p.hd + c * 32;
-          const int ncol = min(32, p.hd - c * 32);
-#pragma unroll
-          for (int j = 0; j < 32; j += 4)
-            if (j < ncol)
-              atomicAdd(reinterpret_cast<float4*>(dst + j),
-                        make_float4(__uint_as_float(u[j]), __uint_as_float(u[j + 1]), __uint_as_float(u[j + 2]),
-                                    __uint_as_float(u[j + 3])));
-        }
-      }
-      tc_fence_before();
-      mbar_arrive(&bars->dq_free);
-    }
-    // dK, dV (thread = key row): all MMAs completed (the last dq_full tracks every prior MMA)
-    const int key = k0 + tr;
-    const bool key_valid = tr < keys_valid;
+    // dK, dV (thread = key row; each half writes half of the hd columns)
     if (n_it > 0) {
+      mbar_wait(&bars->mma_done, 0);
       tc_fence_after();
+    }
 #pragma unroll 1
-      for (int which = 0; which < 2; ++which) {
-        void* out = which == 0 ? p.dK : p.dV;
-        const int col0 = which == 0 ? C::DK_COL : C::DV_COL;
+    for (int which = 0; which < 2; ++which) {
+      void* out = which == 0 ? p.dK : p.dV;
+      const int col0 = which == 0 ? C::DK_COL : C::DV_COL;
 #pragma unroll 1
-        for (int c = 0; c < G::HDP / 32; ++c) {
-          uint32_t u[32];
-          tmem_ld32(tmem_addr(tmem, quarter, col0 + c * 32), u);
-          tmem_ld_wait();
-          if (key_valid) {
-            const size_t off = (size_t)key * p.d + (size_t)h * p.hd + c * 32;
-            const int ncol = min(32, p.hd - c * 32);
-            if (p.out_f32) {
-              float* o = reinterpret_cast<float*>(out) + off;
-              for (int j = 0; j < ncol; j += 4)
-                *reinterpret_cast<float4*>(o + j) = make_float4(__uint_as_float(u[j]), __uint_as_float(u[j + 1]),
-                                                                __uint_as_float(u[j + 2]), __uint_as_float(u[j + 3]));
-            } else {
-              __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(out) + off;
-              for (int j = 0; j < ncol; j += 8)
-                *reinterpret_cast<uint4*>(o + j) =
-                    make_uint4(pack_bf16(__uint_as_float(u[j]), __uint_as_float(u[j + 1])),
-                               pack_bf16(__uint_as_float(u[j + 2]), __uint_as_float(u[j + 3])),
-                               pack_bf16(__uint_as_float(u[j + 4]), __uint_as_float(u[j + 5])),
-                               pack_bf16(__uint_as_float(u[j + 6]), __uint_as_float(u[j + 7])));
-            }
+      for (int c = half; c < G::HDP / 32; c += 2) {
+        uint32_t u[32];
+        tmem_ld32(tmem_addr(tmem, quarter, col0 + c * 32), u);
+        tmem_ld_wait();
+        if (key_valid && n_it > 0) {
+          const size_t off = (size_t)key * p.d + (size_t)h * p.hd + c * 32;
+          const int ncol = min(32, p.hd - c * 32);
+          if (p.out_f32) {
+            float* o = reinterpret_cast<float*>(out) + off;
+            for (int j = 0; j < ncol; j += 4)
+              *reinterpret_cast<float4*>(o + j) = make_float4(__uint_as_float(u[j]), __uint_as_float(u[j + 1]),
+                                                              __uint_as_float(u[j + 2]), __uint_as_float(u[j + 3]));
+          } else {
+            __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(out) + off;
+            for (int j = 0; j < ncol; j += 8)
+              *reinterpret_cast<uint4*>(o + j) =
+                  make_uint4(pack_bf16(__uint_as_float(u[j]), __uint_as_float(u[j + 1])),
+                             pack_bf16(__uint_as_float(u[j + 2]), __uint_as_float(u[j + 3])),
+                             pack_bf16(__uint_as_float(u[j + 4]), __uint_as_float(u[j + 5])),
+                             pack_bf16(__uint_as_float(u[j + 6]), __uint_as_float(u[j + 7])));
           }
         }
       }
@@ -368,17 +530,23 @@ bool make_head_map(CUtensorMap* m, const void* ptr, int T, int H, int hd);
 template <int HD>
 static cudaError_t bwd_hd(const CUtensorMap& mQ, const CUtensorMap& mK, const CUtensorMap& mV, const CUtensorMap& mdO,
                           const AttnParams& p, cudaStream_t st) {
-  using C = BwdCfg<HD>;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(attn_bwd_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    cudaError_t e = cudaFuncSetAttribute(attn_bwd_dq_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         DqCfg<HD>::SMEM);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(attn_bwd_dkv_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               DkvCfg<HD>::SMEM);
     if (e != cudaSuccess) return e;
     attr = true;
   }
   const int grid = p.plan.nq_cap * p.H;
   if (grid == 0) return cudaSuccess;
-  ProfScope ps(PROF_ATTN_BWD, st, 1);
-  attn_bwd_kernel<HD><<<grid, C::THREADS, C::SMEM, st>>>(mQ, mK, mV, mdO, p);
+  {
+    ProfScope ps(PROF_ATTN_BWD, st, 2);
+    attn_bwd_dq_kernel<HD><<<grid, 192, DqCfg<HD>::SMEM, st>>>(mQ, mK, mV, mdO, p);
+    attn_bwd_dkv_kernel<HD><<<grid, DkvCfg<HD>::THREADS, DkvCfg<HD>::SMEM, st>>>(mQ, mK, mV, mdO, p);
+  }
   return cudaGetLastError();
 }
 
@@ -388,9 +556,8 @@ cudaError_t attn_bwd_pre_launch(const void* O, const void* dO, float* D, float* 
   if (T > 0)
     attn_bwd_pre_kernel<<<(T + 7) / 8, 256, 0, st>>>(reinterpret_cast<const __nv_bfloat16*>(O),
                                                       reinterpret_cast<const __nv_bfloat16*>(dO), D, T, H, hd);
-  cudaError_t e = cudaGetLastError();
-  if (e == cudaSuccess && dQacc) e = cudaMemsetAsync(dQacc, 0, sizeof(float) * (size_t)T * H * hd, st);
-  return e;
+  (void)dQacc;  // dQ is written exactly once per row by attn_bwd_dq_kernel (pad rows zeroed by the caller)
+  return cudaGetLastError();
 }
 
 cudaError_t attn_bwd_launch(const void* Qr, const void* Kr, const void* V, const void* dO, const AttnParams& p,

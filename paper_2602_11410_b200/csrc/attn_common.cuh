@@ -46,6 +46,17 @@ CADET_DEV uint64_t p_mnmajor_desc(uint32_t base, int kk) {  // A operand MN-majo
   return smem_desc(base + kk * 16 * 128, 16384, 1024, SWZ_128B);
 }
 
+// Visible-key bitmask of query row r over the 32 keys [kc, kc + 32): the prefix [.., e_r), the
+// diagonal r and, with the PAIR_PREV bit, r - 1 (SURVEY 8(c) mask structure; Fig. 3).
+CADET_DEV uint32_t row_mask32(int e_r, int r, bool pp, int kc) {
+  const int lim = e_r - kc;
+  uint32_t m = lim >= 32 ? 0xFFFFFFFFu : (lim <= 0 ? 0u : ((1u << lim) - 1u));
+  const int dd = r - kc;
+  if (dd >= 0 && dd < 32) m |= 1u << dd;
+  if (pp && dd - 1 >= 0 && dd - 1 < 32) m |= 1u << (dd - 1);
+  return m;
+}
+
 struct AttnParams {
   int32_t T, H, hd, d, n;
   float scale_log2;  // log2(e) / sqrt(hd)

@@ -151,12 +151,10 @@ __global__ void __launch_bounds__(192, 2)
 #pragma unroll
         for (int q = 0; q < 32; ++q) x[q] = __uint_as_float(u[q]);
         if (partial) {
+          const uint32_t m = valid ? row_mask32(e_r, r, pp, k0 + c * 32) : 0u;
 #pragma unroll
-          for (int q = 0; q < 32; ++q) {
-            const int jj = k0 + c * 32 + q;
-            const bool ok = valid && ((jj < e_r) || (jj == r) || (pp && jj == r - 1));
-            if (!ok) x[q] = -INFINITY;
-          }
+          for (int q = 0; q < 32; ++q)
+            if (!((m >> q) & 1u)) x[q] = -INFINITY;
         }
       };
       // pass 1: masked row max

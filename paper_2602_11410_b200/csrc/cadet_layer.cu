@@ -99,6 +99,7 @@ cadet_status cadet_attn_core_backward(const cadet_attn_config* cfg, const cadet_
   p.dV = dV;
   const int ob = d * (cfg->out_f32 ? 4 : 2);
   cudaError_t e = attn_bwd_pre_launch(O, dO, D, dQr, T, H, cfg->head_dim, st);
+  if (e == cudaSuccess) e = zero_pad_rows_launch(dQr, d * 4, T, b->cu_seqlens, b->n_seqs, st);
   if (e == cudaSuccess) e = zero_pad_rows_launch(dKr, ob, T, b->cu_seqlens, b->n_seqs, st);
   if (e == cudaSuccess) e = zero_pad_rows_launch(dV, ob, T, b->cu_seqlens, b->n_seqs, st);
   if (e == cudaSuccess) e = attn_bwd_launch(Qr, Kr, V, dO, p, st);
@@ -377,6 +378,7 @@ cadet_status cadet_attn_backward(const cadet_attn_config* cfg, const cadet_batch
     p.dK = W.dKr;
     p.dV = W.dV;
     e = attn_bwd_pre_launch(L.O, dO, W.D, W.dQacc, T, H, hd, st);
+    if (e == cudaSuccess) e = zero_pad_rows_launch(W.dQacc, d * 4, T, b->cu_seqlens, n, st);
     if (e == cudaSuccess) e = zero_pad_rows_launch(W.dKr, d * 2, T, b->cu_seqlens, n, st);
     if (e == cudaSuccess) e = zero_pad_rows_launch(W.dV, d * 2, T, b->cu_seqlens, n, st);
     if (e == cudaSuccess) e = attn_bwd_launch(L.Qr, L.Kr, L.V, dO, p, st);
