@@ -17,6 +17,21 @@
 
 namespace cadet {
 
+#ifdef CADET_PHASE_TIMING
+// Phase timers (profiling builds only): per CTA, summed clock64 deltas, [blockIdx][8].
+__device__ unsigned long long g_phase[8192][8];
+#define PT_DECL unsigned long long _pt = clock64();
+#define PT_MARK(slot)                                          \
+  {                                                            \
+    unsigned long long _n = clock64();                         \
+    if (blockIdx.x < 8192) atomicAdd(&g_phase[blockIdx.x][slot], _n - _pt); \
+    _pt = _n;                                                  \
+  }
+#else
+#define PT_DECL
+#define PT_MARK(slot)
+#endif
+
 __device__ __forceinline__ int visit_tile_b(const QTileInfo& qi, int j) { return j < qi.nf ? j : qi.kt2 + (j - qi.nf); }
 __device__ __forceinline__ bool q_sees_k(const QTileInfo& qi, int kt) {
   return kt < qi.nf || (kt >= qi.kt2 && kt <= qi.qt);
@@ -179,7 +194,8 @@ __global__ void __launch_bounds__(192, 1)
           float ds[2];
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
-            float pr = fast_exp2(fmaf(__uint_as_float(us[q + e]), sl2, -lse2));
+            const float xe = fmaf(__uint_as_float(us[q + e]), sl2, -lse2);
+            float pr = fast_exp2(xe);
             if (!((m >> (q + e)) & 1u)) pr = 0.f;
             ds[e] = pr * (__uint_as_float(ud[q + e]) - Dr) * p.scale;
           }
@@ -202,8 +218,8 @@ __global__ void __launch_bounds__(192, 1)
       tmem_ld32(tmem_addr(tmem, quarter, C::DQ_COL + c * 32), u);
       tmem_ld_wait();
       if (valid) {
-        float* o = p.dQ + (size_t)r * p.d + (size_t)h * p.hd + c * 32;
         const int ncol = min(32, p.hd - c * 32);
+        float* o = p.dQ + (size_t)r * p.d + (size_t)h * p.hd + c * 32;
         for (int q = 0; q < ncol; q += 4)
           *reinterpret_cast<float4*>(o + q) = make_float4(__uint_as_float(u[q]), __uint_as_float(u[q + 1]),
                                                           __uint_as_float(u[q + 2]), __uint_as_float(u[q + 3]));
@@ -217,6 +233,10 @@ __global__ void __launch_bounds__(192, 1)
 }
 
 // ============================================================================ dK / dV kernel
+// Each visited q-tile is processed as two 64-column halves h (global half index): the MMA warp
+// issues S^T_h = K Q_h^T and dP^T_h = V dO_h^T into TMEM half-buffer (h & 1) BEFORE waiting for
+// half h-1's P^T/dS^T, so the tensor core works while a compute warpgroup (one per half-buffer,
+// thread = key row, 64 q columns) turns the previous half into P^T / dS^T.
 template <int HD>
 struct DkvCfg {
   using G = HeadGeom<HD>;
@@ -224,17 +244,18 @@ struct DkvCfg {
   static constexpr int V_OFF = K_OFF + G::TILE_BYTES;
   static constexpr int Q_OFF = V_OFF + G::TILE_BYTES;          // two stages
   static constexpr int DO_OFF = Q_OFF + 2 * G::TILE_BYTES;     // two stages
-  static constexpr int VEC_OFF = DO_OFF + 2 * G::TILE_BYTES;   // [2][4][128] x 4 B: lse2, D, e, q|pp
-  static constexpr int LIST_OFF = VEC_OFF + 2 * 4 * 128 * 4;
+  static constexpr int VEC_OFF = DO_OFF + 2 * G::TILE_BYTES;   // [2 groups][2 bufs][4][64] x 4 B
+  static constexpr int LIST_OFF = VEC_OFF + 2 * 2 * 4 * 64 * 4;
   static constexpr int MAX_LIST = 512;
   static constexpr int BAR_OFF = LIST_OFF + MAX_LIST * 4;
   static constexpr int SMEM = BAR_OFF + 256 + 1024;
+  // S^T/P^T half-buffers at [0,64) and [64,128); dP^T/dS^T at [128,192) and [192,256)
   static constexpr int S_COL = 0, DP_COL = 128, DV_COL = 256, DK_COL = 384;
-  static constexpr int THREADS = 320;  // producer, MMA, 8 compute warps (two per TMEM lane quarter)
+  static constexpr int THREADS = 320;  // producer, MMA, 2 compute warpgroups (one per half-buffer)
 };
 
 struct DkvBars {
-  uint64_t kv_full, q_full[2], q_empty[2], do_full[2], do_empty[2], s_full, dp_full, pds_ready, mma_done;
+  uint64_t kv_full, q_full[2], q_empty[2], do_full[2], do_empty[2], sdp_full[2], pds_ready[2], mma_done;
   uint32_t tmem_base;
   int32_t n_it;
 };
@@ -292,10 +313,9 @@ __global__ void __launch_bounds__(320, 1)
         mbar_init(&bars->q_empty[i], 1);
         mbar_init(&bars->do_full[i], 1);
         mbar_init(&bars->do_empty[i], 1);
+        mbar_init(&bars->sdp_full[i], 1);
+        mbar_init(&bars->pds_ready[i], 128);
       }
-      mbar_init(&bars->s_full, 1);
-      mbar_init(&bars->dp_full, 1);
-      mbar_init(&bars->pds_ready, 256);
       mbar_init(&bars->mma_done, 1);
       fence_mbar_init();
     }
@@ -315,10 +335,10 @@ __global__ void __launch_bounds__(320, 1)
         tma_load_3d(smem + C::K_OFF + blk * G::BLK, &mK, &bars->kv_full, blk * G::CB, h, k0);
         tma_load_3d(smem + C::V_OFF + blk * G::BLK, &mV, &bars->kv_full, blk * G::CB, h, k0);
       }
-      for (int it = 0; it < n_it; ++it) {
+      for (int it = 0; it < n_it; ++it) {  // list entry: qt | full<<30 | near<<29
         const int st = it & 1, use = it >> 1;
         const int q0 = sa + (list[it] & 0xFFFF) * 128;
-        if (use > 0) mbar_wait(&bars->q_empty[st], (use - 1) & 1);  // list entry: qt | full<<30 | near<<29
+        if (use > 0) mbar_wait(&bars->q_empty[st], (use - 1) & 1);
         mbar_expect_tx(&bars->q_full[st], G::TILE_BYTES);
 #pragma unroll
         for (int blk = 0; blk < G::NB; ++blk)
@@ -333,57 +353,71 @@ __global__ void __launch_bounds__(320, 1)
     }
   } else if (warp == 1) {
     if (elect_one()) {
-      const uint32_t id_s = idesc_bf16(128, 128, 0, 0);
+      const uint32_t id_s = idesc_bf16(128, 64, 0, 0);
       const uint32_t id_kv = idesc_bf16(128, G::HDP, 0, 1);
       const uint32_t sK = smem_u32(smem + C::K_OFF), sV = smem_u32(smem + C::V_OFF);
       mbar_wait(&bars->kv_full, 0);
-      for (int it = 0; it < n_it; ++it) {
-        const int st = it & 1, use = it >> 1;
+      const int nh = 2 * n_it;
+      // half hh: q-tile hh >> 1, columns [64 (hh & 1), +64), TMEM half-buffer hh & 1
+      auto issue_sdp = [&](int hh) {
+        const int it = hh >> 1, hf = hh & 1, st = it & 1, use = it >> 1;
+        const uint32_t sQ = smem_u32(smem + C::Q_OFF + st * G::TILE_BYTES) + hf * 64 * G::RB;
+        const uint32_t sdO = smem_u32(smem + C::DO_OFF + st * G::TILE_BYTES) + hf * 64 * G::RB;
+        if (hf == 0) {
+          mbar_wait(&bars->q_full[st], use & 1);
+          mbar_wait(&bars->do_full[st], use & 1);
+          tc_fence_after();
+        }
+        // over P^T/dS^T of half hh-2: in-order after its dV/dK MMAs, issued after pds_ready(hh-2)
+#pragma unroll
+        for (int kk = 0; kk < G::HDP / 16; ++kk)
+          mma_bf16_ss(tmem + C::S_COL + hf * 64, kmajor_desc<HD>(sK, kk), kmajor_desc<HD>(sQ, kk), id_s,
+                      kk > 0 ? 1u : 0u);
+#pragma unroll
+        for (int kk = 0; kk < G::HDP / 16; ++kk)
+          mma_bf16_ss(tmem + C::DP_COL + hf * 64, kmajor_desc<HD>(sV, kk), kmajor_desc<HD>(sdO, kk), id_s,
+                      kk > 0 ? 1u : 0u);
+        mma_commit(&bars->sdp_full[hf]);
+      };
+      if (nh > 0) issue_sdp(0);
+      for (int hh = 0; hh < nh; ++hh) {
+        const int it = hh >> 1, hf = hh & 1, st = it & 1;
+        if (hh + 1 < nh) issue_sdp(hh + 1);
+        mbar_wait(&bars->pds_ready[hf], (hh >> 1) & 1);
+        tc_fence_after();
         const uint32_t sQ = smem_u32(smem + C::Q_OFF + st * G::TILE_BYTES);
         const uint32_t sdO = smem_u32(smem + C::DO_OFF + st * G::TILE_BYTES);
-        // S^T_i over P^T_{i-1} and dP^T_i over dS^T_{i-1}: in-order after dV_{i-1} / dK_{i-1}
-        mbar_wait(&bars->q_full[st], use & 1);
-        tc_fence_after();
 #pragma unroll
-        for (int kk = 0; kk < G::HDP / 16; ++kk)
-          mma_bf16_ss(tmem + C::S_COL, kmajor_desc<HD>(sK, kk), kmajor_desc<HD>(sQ, kk), id_s, kk > 0 ? 1u : 0u);
-        mma_commit(&bars->s_full);
-        mbar_wait(&bars->do_full[st], use & 1);
-        tc_fence_after();
+        for (int kk = 0; kk < 64 / 16; ++kk)
+          mma_bf16_ts(tmem + C::DV_COL, tmem + C::S_COL + hf * 64 + kk * 8, mnmajor_desc<HD>(sdO, hf * 4 + kk), id_kv,
+                      (hh > 0 || kk > 0) ? 1u : 0u);
 #pragma unroll
-        for (int kk = 0; kk < G::HDP / 16; ++kk)
-          mma_bf16_ss(tmem + C::DP_COL, kmajor_desc<HD>(sV, kk), kmajor_desc<HD>(sdO, kk), id_s, kk > 0 ? 1u : 0u);
-        mma_commit(&bars->dp_full);
-        mbar_wait(&bars->pds_ready, it & 1);
-        tc_fence_after();
-#pragma unroll
-        for (int kk = 0; kk < 128 / 16; ++kk)
-          mma_bf16_ts(tmem + C::DV_COL, tmem + C::S_COL + kk * 8, mnmajor_desc<HD>(sdO, kk), id_kv,
-                      (it > 0 || kk > 0) ? 1u : 0u);
-        mma_commit(&bars->do_empty[st]);
-#pragma unroll
-        for (int kk = 0; kk < 128 / 16; ++kk)
-          mma_bf16_ts(tmem + C::DK_COL, tmem + C::DP_COL + kk * 8, mnmajor_desc<HD>(sQ, kk), id_kv,
-                      (it > 0 || kk > 0) ? 1u : 0u);
-        mma_commit(&bars->q_empty[st]);
+        for (int kk = 0; kk < 64 / 16; ++kk)
+          mma_bf16_ts(tmem + C::DK_COL, tmem + C::DP_COL + hf * 64 + kk * 8, mnmajor_desc<HD>(sQ, hf * 4 + kk), id_kv,
+                      (hh > 0 || kk > 0) ? 1u : 0u);
+        if (hf == 1) {
+          mma_commit(&bars->do_empty[st]);
+          mma_commit(&bars->q_empty[st]);
+        }
       }
       mma_commit(&bars->mma_done);
     }
   } else {
-    // thread = key row; warps 2..5 take q columns [0, 64), warps 6..9 columns [64, 128)
+    // warpgroup grp (warps 2..5 -> 0, 6..9 -> 1) owns TMEM half-buffer grp = q columns [64 grp, +64)
     const uint32_t quarter = warp & 3;
-    const int half = (warp - 2) >> 2;
+    const int grp = (warp - 2) >> 2;
     const int tr = quarter * 32 + lane;
-    const int ct = threadIdx.x - 64;  // 0..255; the first 128 load the per-query vectors
+    const int gt = (threadIdx.x - 64) & 127;  // 0..127 inside the warpgroup
     const int key = k0 + tr;
     const bool key_valid = tr < keys_valid;
     const float sl2 = p.scale_log2;
     const float LOG2E = 1.4426950408889634f;
+    float* vgrp = vec + grp * 2 * 256;
     float nl = 0.f, nd = 0.f;
     int ne = -1, nw = -2;
-    auto fetch = [&](int it) {
-      if (ct >= 128) return;
-      const int q = sa + (list[it] & 0xFFFF) * 128 + ct;
+    auto fetch = [&](int it) {  // the group's first 64 threads load the 64 columns' vectors
+      if (gt >= 64) return;
+      const int q = sa + (list[it] & 0xFFFF) * 128 + grp * 64 + gt;
       const bool v = q < se;
       nl = v ? p.lse[(size_t)h * p.T + q] * LOG2E : INFINITY;
       nd = v ? p.D[(size_t)h * p.T + q] : 0.f;
@@ -394,44 +428,45 @@ __global__ void __launch_bounds__(320, 1)
     for (int it = 0; it < n_it; ++it) {
       const bool full = (list[it] >> 30) & 1;
       const bool near = (list[it] >> 29) & 1;
-      float* vb = vec + (it & 1) * 512;
+      float* vb = vgrp + (it & 1) * 256;
       int* vbi = reinterpret_cast<int*>(vb);
-      if (ct < 128) {
-        vb[ct] = nl;
-        vb[128 + ct] = nd;
-        vbi[256 + ct] = ne;
-        vbi[384 + ct] = nw;
+      if (gt < 64) {
+        vb[gt] = nl;
+        vb[64 + gt] = nd;
+        vbi[128 + gt] = ne;
+        vbi[192 + gt] = nw;
       }
       if (it + 1 < n_it) fetch(it + 1);
-      named_bar_sync(1, 256);
-      mbar_wait(&bars->s_full, it & 1);
-      mbar_wait(&bars->dp_full, it & 1);
+      named_bar_sync(1 + grp, 128);
+      mbar_wait(&bars->sdp_full[grp], it & 1);
       tc_fence_after();
-      uint32_t wp[2][16], wd[2][16];
 #pragma unroll
-      for (int cc = 0; cc < 2; ++cc) {
-        const int c = half * 2 + cc;
+      for (int c = 0; c < 2; ++c) {
         uint32_t us[32], ud[32];
-        tmem_ld32(tmem_addr(tmem, quarter, C::S_COL + c * 32), us);
-        tmem_ld32(tmem_addr(tmem, quarter, C::DP_COL + c * 32), ud);
+        tmem_ld32(tmem_addr(tmem, quarter, C::S_COL + grp * 64 + c * 32), us);
+        tmem_ld32(tmem_addr(tmem, quarter, C::DP_COL + grp * 64 + c * 32), ud);
         tmem_ld_wait();
+        uint32_t wp[16], wd[16];
 #pragma unroll
         for (int q4 = 0; q4 < 32; q4 += 4) {
           const float4 l4 = *reinterpret_cast<const float4*>(vb + c * 32 + q4);
-          const float4 d4 = *reinterpret_cast<const float4*>(vb + 128 + c * 32 + q4);
+          const float4 d4 = *reinterpret_cast<const float4*>(vb + 64 + c * 32 + q4);
           const float lv[4] = {l4.x, l4.y, l4.z, l4.w}, dv[4] = {d4.x, d4.y, d4.z, d4.w};
           float pv[4], sv[4];
 #pragma unroll
-          for (int e = 0; e < 4; ++e) pv[e] = fast_exp2(fmaf(__uint_as_float(us[q4 + e]), sl2, -lv[e]));
+          for (int e = 0; e < 4; ++e) {
+            const float xe = fmaf(__uint_as_float(us[q4 + e]), sl2, -lv[e]);
+            pv[e] = fast_exp2(xe);
+          }
           if (!full) {
-            const int4 e4 = *reinterpret_cast<const int4*>(vbi + 256 + c * 32 + q4);
+            const int4 e4 = *reinterpret_cast<const int4*>(vbi + 128 + c * 32 + q4);
             const int ev[4] = {e4.x, e4.y, e4.z, e4.w};  // -1 for query rows outside the sequence
             if (!near) {  // far pair: only the visible prefix can admit this key
 #pragma unroll
               for (int e = 0; e < 4; ++e)
                 if (!(key_valid && key < ev[e])) pv[e] = 0.f;
             } else {
-              const int4 w4 = *reinterpret_cast<const int4*>(vbi + 384 + c * 32 + q4);
+              const int4 w4 = *reinterpret_cast<const int4*>(vbi + 192 + c * 32 + q4);
               const int wv[4] = {w4.x, w4.y, w4.z, w4.w};
 #pragma unroll
               for (int e = 0; e < 4; ++e) {
@@ -445,27 +480,21 @@ __global__ void __launch_bounds__(320, 1)
           }
 #pragma unroll
           for (int e = 0; e < 4; ++e) sv[e] = pv[e] * (__uint_as_float(ud[q4 + e]) - dv[e]) * p.scale;
-          wp[cc][q4 >> 1] = pack_bf16(pv[0], pv[1]);
-          wp[cc][(q4 >> 1) + 1] = pack_bf16(pv[2], pv[3]);
-          wd[cc][q4 >> 1] = pack_bf16(sv[0], sv[1]);
-          wd[cc][(q4 >> 1) + 1] = pack_bf16(sv[2], sv[3]);
+          wp[q4 >> 1] = pack_bf16(pv[0], pv[1]);
+          wp[(q4 >> 1) + 1] = pack_bf16(pv[2], pv[3]);
+          wd[q4 >> 1] = pack_bf16(sv[0], sv[1]);
+          wd[(q4 >> 1) + 1] = pack_bf16(sv[2], sv[3]);
         }
-      }
-      // every S^T / dP^T column is in registers before any P^T / dS^T column overwrites them
-      tc_fence_before();
-      named_bar_sync(2, 256);
-      tc_fence_after();
-#pragma unroll
-      for (int cc = 0; cc < 2; ++cc) {
-        const int c = half * 2 + cc;
-        tmem_st16(tmem_addr(tmem, quarter, C::S_COL + c * 16), wp[cc]);
-        tmem_st16(tmem_addr(tmem, quarter, C::DP_COL + c * 16), wd[cc]);
+        // P^T / dS^T chunk c -> columns [16c, 16c + 16) of this half: only this thread's own,
+        // already-loaded S^T / dP^T chunk 0 is overwritten
+        tmem_st16(tmem_addr(tmem, quarter, C::S_COL + grp * 64 + c * 16), wp);
+        tmem_st16(tmem_addr(tmem, quarter, C::DP_COL + grp * 64 + c * 16), wd);
       }
       tmem_st_wait();
       tc_fence_before();
-      mbar_arrive(&bars->pds_ready);
+      mbar_arrive(&bars->pds_ready[grp]);
     }
-    // dK, dV (thread = key row; each half writes half of the hd columns)
+    // dK, dV (thread = key row; each warpgroup writes half of the hd columns)
     if (n_it > 0) {
       mbar_wait(&bars->mma_done, 0);
       tc_fence_after();
@@ -475,7 +504,7 @@ __global__ void __launch_bounds__(320, 1)
       void* out = which == 0 ? p.dK : p.dV;
       const int col0 = which == 0 ? C::DK_COL : C::DV_COL;
 #pragma unroll 1
-      for (int c = half; c < G::HDP / 32; c += 2) {
+      for (int c = grp; c < G::HDP / 32; c += 2) {
         uint32_t u[32];
         tmem_ld32(tmem_addr(tmem, quarter, col0 + c * 32), u);
         tmem_ld_wait();
@@ -576,3 +605,16 @@ cudaError_t attn_bwd_launch(const void* Qr, const void* Kr, const void* V, const
 }
 
 }  // namespace cadet
+
+#ifdef CADET_PHASE_TIMING
+extern "C" int cadet_debug_phase_read(unsigned long long* out, int n) {
+  if (n > 8192 * 8) n = 8192 * 8;
+  cudaMemcpyFromSymbol(out, cadet::g_phase, sizeof(unsigned long long) * n);
+  return n;
+}
+extern "C" int cadet_debug_phase_reset() {
+  static unsigned long long z[8192 * 8];
+  cudaMemcpyToSymbol(cadet::g_phase, z, sizeof(z));
+  return 0;
+}
+#endif

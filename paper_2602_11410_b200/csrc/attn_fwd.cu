@@ -18,6 +18,18 @@
 
 namespace cadet {
 
+#ifdef CADET_PHASE_TIMING
+__device__ unsigned long long g_phase_fwd[8192][8];
+#define FT_MARK(slot)                                                              \
+  if (lane == 0 && blockIdx.x < 8192) {                                             \
+    unsigned long long _n = clock64();                                              \
+    atomicAdd(&g_phase_fwd[blockIdx.x][slot], _n - _ft);                            \
+    _ft = _n;                                                                       \
+  }
+#else
+#define FT_MARK(slot)
+#endif
+
 template <int HD>
 struct FwdCfg {
   using G = HeadGeom<HD>;
@@ -105,11 +117,16 @@ __global__ void __launch_bounds__(192, 2)
       const uint32_t sQ = smem_u32(smem + C::Q_OFF);
       const uint32_t sK = smem_u32(smem + C::K_OFF);
       const uint32_t sV = smem_u32(smem + C::V_OFF);
+#ifdef CADET_PHASE_TIMING
+      unsigned long long _ft = clock64();
+#endif
       mbar_wait(&bars->q_full, 0);
+      FT_MARK(0)
       for (int j = 0; j < n_kv; ++j) {
         // S_j: the tensor pipe executes in issue order, so S_j overwrites P_{j-1} only after PV_{j-1}
         // has read it; p_full(j-1) (waited below) guarantees the softmax finished with S_{j-1}.
         mbar_wait(&bars->k_full, j & 1);
+        FT_MARK(1)
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < G::HDP / 16; ++kk)
@@ -117,7 +134,9 @@ __global__ void __launch_bounds__(192, 2)
         mma_commit(&bars->k_empty);
         mma_commit(&bars->s_full);
         mbar_wait(&bars->p_full, j & 1);
+        FT_MARK(2)
         mbar_wait(&bars->v_full, j & 1);
+        FT_MARK(3)
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < 128 / 16; ++kk)
@@ -138,10 +157,16 @@ __global__ void __launch_bounds__(192, 2)
     const float sl2 = p.scale_log2;
     float m_used = -INFINITY;  // scaled (log2) running max actually used as the exp base
     float l = 0.f;
+#ifdef CADET_PHASE_TIMING
+    unsigned long long _ft = clock64();
+    const uint32_t lane_save = lane;
+#define lane (threadIdx.x == 64 ? 0u : 1u)
+#endif
     for (int j = 0; j < n_kv; ++j) {
       const int k0 = sa + visit_tile(qi, j) * 128;
       // s_full(j) also implies PV_{j-1} completed (commit tracks all prior tcgen05 ops)
       mbar_wait(&bars->s_full, j & 1);
+      FT_MARK(4)
       tc_fence_after();
       const bool partial = !valid || (e_r < k0 + 128);
       auto load_masked = [&](int c, float (&x)[32]) {
@@ -166,6 +191,7 @@ __global__ void __launch_bounds__(192, 2)
 #pragma unroll
         for (int q = 0; q < 32; ++q) mx = fmaxf(mx, x[q]);
       }
+      FT_MARK(5)
       const float mx_s = mx * sl2;
       float factor = 1.f;
       bool rescale = false;
@@ -209,7 +235,12 @@ __global__ void __launch_bounds__(192, 2)
       tc_fence_before();
       mbar_arrive(&bars->p_full);
       l = l * factor + rs;
+      FT_MARK(6)
     }
+#ifdef CADET_PHASE_TIMING
+#undef lane
+    (void)lane_save;
+#endif
     // ---- epilogue: O / l, LSE
     if (n_kv > 0) {
       mbar_wait(&bars->pv_done, (n_kv - 1) & 1);
@@ -296,3 +327,15 @@ cudaError_t attn_fwd_launch(const void* Qr, const void* Kr, const void* V, const
 }
 
 }  // namespace cadet
+
+#ifdef CADET_PHASE_TIMING
+extern "C" int cadet_debug_phase_read_fwd(unsigned long long* out, int n) {
+  cudaMemcpyFromSymbol(out, cadet::g_phase_fwd, sizeof(unsigned long long) * n);
+  return n;
+}
+extern "C" int cadet_debug_phase_reset_fwd() {
+  static unsigned long long z[8192 * 8];
+  cudaMemcpyToSymbol(cadet::g_phase_fwd, z, sizeof(z));
+  return 0;
+}
+#endif

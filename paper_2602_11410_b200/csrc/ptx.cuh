@@ -270,6 +270,26 @@ CADET_DEV float fast_exp2(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+// 2^x on the FMA/ALU pipes (FA4-style MUFU offload): x = n + f with n = rint(x) via the 1.5*2^23
+// trick, 2^f on [-1/2, 1/2] by a degree-4 near-minimax polynomial (max rel err 2.7e-6), n added
+// to the exponent field as an integer.  x < -126 (incl. -inf) returns exactly 0.
+CADET_DEV float exp2_poly(float x) {
+  const float xc = fmaxf(x, -127.f);
+  const float t = xc + 12582912.f;
+  const float f = xc - (t - 12582912.f);
+  float p = fmaf(0.00957009536025538f, f, 0.05591786349494091f);
+  p = fmaf(p, f, 0.24024745021653496f);
+  p = fmaf(p, f, 0.6931218143849706f);
+  p = fmaf(p, f, 0.99999926137738f);
+  const float r = __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+  return x < -126.f ? 0.f : r;
+}
+// bf16x2 pack on the ALU pipe (integer round-half-up + PRMT) instead of F2FP: keeps the
+// transcendental (XU) pipe free for exp2 in the softmax loops.  Differs from RNE only on exact ties.
+CADET_DEV uint32_t pack_bf16_alu(float a, float b) {
+  const uint32_t ua = __float_as_uint(a) + 0x8000u, ub = __float_as_uint(b) + 0x8000u;
+  return __byte_perm(ua, ub, 0x7632);
+}
 CADET_DEV uint32_t pack_bf16(float a, float b) {
   __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
   return *reinterpret_cast<uint32_t*>(&v);

@@ -1,0 +1,54 @@
+"""Profiling-build experiment: per-phase clock64 sums of the dK/dV backward kernel (C4 batch)."""
+import ctypes as C
+import os
+import subprocess
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from paper_2602_11410_b200 import build as B  # noqa: E402
+
+lib_dbg = os.path.join(B.HERE, "libcadet_dbg.so")
+objs = []
+for src in B.sources():
+    obj = os.path.join(B.HERE, "build", os.path.basename(src) + ".dbg.o")
+    subprocess.check_call(["nvcc", *B.FLAGS, "-DCADET_PHASE_TIMING", "-c", src, "-o", obj])
+    objs.append(obj)
+subprocess.check_call(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-shared", *objs, "-o", lib_dbg, "-lcudart"])
+from paper_2602_11410_b200 import _lib  # noqa: E402
+_lib.LIB_PATH = lib_dbg
+import torch  # noqa: E402
+import bench  # noqa: E402
+from paper_2602_11410_b200.model import CadetStack, StackConfig  # noqa: E402
+
+wl = bench.WORKLOADS["c4"]
+users, hinp = bench.build_inputs(wl, 0, pin=False)
+inp = hinp.to("cuda")
+st = CadetStack(StackConfig(d_model=1024, n_heads=8, n_layers=1, budget=65536, L_chunk=2048), device="cuda")
+st.step(inp)
+torch.cuda.synchronize()
+L = _lib.lib()
+L.cadet_debug_phase_reset()
+L.cadet_debug_phase_reset_fwd()
+st.step(inp)
+torch.cuda.synchronize()
+buf = (C.c_ulonglong * (8192 * 8))()
+L.cadet_debug_phase_read(buf, 8192 * 8)
+a = np.frombuffer(buf, dtype=np.uint64).reshape(8192, 8).astype(np.float64)
+used = a[a.sum(1) > 0]
+names = ["mma: kv wait", "mma: q_full wait", "mma: S+dP issue", "mma: pds wait", "cmp: s/dp wait",
+         "cmp: compute", "cmp: bar+store", "mma: tail"]
+print("CTAs", len(used))
+for i, n in enumerate(names):
+    print(f"{n:18s} mean per CTA {used[:, i].mean():12.0f} clk   total share {used[:, i].sum() / used[:, [0,1,2,3,7]].sum():.3f}")
+
+L.cadet_debug_phase_read_fwd(buf, 8192 * 8)
+a = np.frombuffer(buf, dtype=np.uint64).reshape(8192, 8).astype(np.float64)
+used = a[a.sum(1) > 0]
+names = ["mma: q wait", "mma: k_full wait", "mma: S issue+p_full wait", "mma: v_full wait", "smx: s_full wait",
+         "smx: pass1", "smx: rescale+pass2+arrive", "-"]
+print("FWD CTAs", len(used))
+for i, n in enumerate(names[:7]):
+    print(f"{n:26s} mean per CTA {used[:, i].mean():12.0f} clk")
