@@ -7,7 +7,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libcadet.so")
+LIB_PATH = os.environ.get("CADET_LIB") or os.path.join(HERE, "libcadet.so")  # CADET_LIB: A/B builds
 
 CADET_MASK_TIME = 1
 CADET_MASK_SESSION = 2

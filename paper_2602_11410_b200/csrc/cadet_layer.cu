@@ -388,22 +388,22 @@ cadet_status cadet_attn_backward(const cadet_attn_config* cfg, const cadet_batch
   const void* dK = W.dK;
   if (e == cudaSuccess) {
     if (cfg->use_int_gate) {
-      e = rope_gate_bwd_launch(W.dQacc, 1, L.Q, L.Zq, W.uq, W.rq, 0, T, d, hd, cfg->use_rope, W.theta,
+      e = rope_gate_bwd_launch(W.dQacc, 1, L.Q, L.Zq, W.uq, W.rq, 1, T, d, hd, cfg->use_rope, W.theta,
                                b->timestamps_ms, v.row_seq, b->cu_seqlens, st);
       if (e == cudaSuccess)
-        e = rope_gate_bwd_launch(W.dKr, 0, L.K, L.Zk, W.uk, W.rk, 0, T, d, hd, cfg->use_rope, W.theta,
+        e = rope_gate_bwd_launch(W.dKr, 0, L.K, L.Zk, W.uk, W.rk, 1, T, d, hd, cfg->use_rope, W.theta,
                                  b->timestamps_ms, v.row_seq, b->cu_seqlens, st);
       if (e == cudaSuccess) {  // dQ = rq + uq W_qg^T ; dK = rk + uk W_kg^T
         GemmProblem g[2];
         const void* us[2] = {W.uq, W.uk};
-        const float* rs[2] = {W.rq, W.rk};
+        const void* rs[2] = {W.rq, W.rk};  // bf16
         const void* Ws[2] = {w->W_qg, w->W_kg};
         void* outs[2] = {W.dQ, W.dK};
         for (int i = 0; i < 2; ++i) {
           g[i] = prob(T, d, d, act(us[i], T, d), w_bwd(Ws[i], d, d), EPI_STORE);
           g[i].epi.out = outs[i];
           g[i].epi.resid = rs[i];
-          g[i].epi.resid_f32 = 1;
+          g[i].epi.resid_f32 = 0;
         }
         e = gemm_launch(g, 2, bn, st);
       }
