@@ -237,12 +237,14 @@ def main():
     import torch.distributed as dist
     from paper_2602_11410_b200 import build, ops
     from paper_2602_11410_b200.model import CadetStack, StackConfig
-    build.build(verbose=False)
+    if local == 0:
+        build.build(verbose=False)  # no-op when the shipped libcadet.so is current
     torch.cuda.set_device(local)
     group = None
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         group = dist.group.WORLD
+        dist.barrier()  # local rank 0 finished any rebuild before the others load the library
     dev = torch.device("cuda", local)
 
     users, host_inp = build_inputs(wl, 1000 * rank, pin=True)
@@ -292,7 +294,10 @@ def main():
         dist.all_reduce(tok)
     tokens_all = float(tok.item())
     value = tokens_all / (ms_max / 1000.0)
-    tflops_all = total_flops * world / (ms_max / 1000.0) / 1e12
+    fl = torch.tensor([total_flops], dtype=torch.float64, device=dev)
+    if group is not None:
+        dist.all_reduce(fl)  # ranks hold different batches: sum their algorithmic FLOPs
+    tflops_all = float(fl.item()) / (ms_max / 1000.0) / 1e12
 
     # ---------------- e2e: same step through the public API from pinned host buffers
     e2e = None

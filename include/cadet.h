@@ -113,7 +113,7 @@ typedef struct {
 typedef struct {
   int32_t K;        /* towers (K = 2 at P:624) */
   int32_t d_model;
-  int32_t d_hidden; /* dh, multiple of 32 (default d/2) */
+  int32_t d_hidden; /* dh >= 32, multiple of 8, K*dh multiple of 32 (default d/2) */
   int32_t dtype;    /* CADET_BF16 */
 } cadet_head_config;
 typedef struct {

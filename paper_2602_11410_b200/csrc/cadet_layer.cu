@@ -477,8 +477,9 @@ static cadet_status check_head(const cadet_head_config* h, const cadet_head_weig
     set_error("heads: null pointer");
     return CADET_E_ARG;
   }
-  if (h->K < 1 || h->d_model <= 0 || h->d_model % 8 || h->d_hidden <= 0 || h->d_hidden % 32) {
-    set_error("heads: K >= 1, d_model % 8 == 0, d_hidden % 32 == 0 required");
+  if (h->K < 1 || h->d_model <= 0 || h->d_model % 8 || h->d_hidden < 32 || h->d_hidden % 8 ||
+      (h->K * h->d_hidden) % 32) {
+    set_error("heads: K >= 1, d_model % 8 == 0, d_hidden % 8 == 0 and >= 32, K*d_hidden % 32 == 0 required");
     return CADET_E_ARG;
   }
   if (h->dtype != CADET_BF16) {

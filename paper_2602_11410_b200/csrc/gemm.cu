@@ -210,15 +210,23 @@ __device__ __forceinline__ void run_epilogue(const EpiParams& e, int row, int M,
         atomicAdd(reinterpret_cast<float4*>(o) + q, make_float4(v[q * 4], v[q * 4 + 1], v[q * 4 + 2], v[q * 4 + 3]));
     } break;
     case EPI_HEAD: {
-      float part = 0.f;
+      // a 32-column slice covers at most two towers when dh % 32 != 0 (dh >= 32)
+      const int k0 = n0c / e.hd;
+      const int split = (k0 + 1) * e.hd - n0c;  // first column of tower k0 + 1 inside the slice
+      float part0 = 0.f, part1 = 0.f;
 #pragma unroll
       for (int j = 0; j < 32; ++j) {
         const float pre = v[j] + e.b1[n0c + j];
         v[j] = pre;
-        part += fmaxf(pre, 0.f) * e.w2[n0c + j];
+        const float c = fmaxf(pre, 0.f) * e.w2[n0c + j];
+        if (j < split)
+          part0 += c;
+        else
+          part1 += c;
       }
       if (e.aux) store_any32(e.aux, e.aux_f32, in_off, v);
-      atomicAdd(e.logits + (size_t)row * e.n_towers + (n0c / e.hd), part);
+      atomicAdd(e.logits + (size_t)row * e.n_towers + k0, part0);
+      if (split < 32) atomicAdd(e.logits + (size_t)row * e.n_towers + k0 + 1, part1);
     } break;
     default:
       break;

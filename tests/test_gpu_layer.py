@@ -214,7 +214,8 @@ def head_case(n_rows, T, d, K, dh, seed=0):
     return Hs, rows, hw, W1cat, bucket, label
 
 
-@pytest.mark.parametrize("n_rows,T,d,K,dh", [(37, 100, 64, 2, 32), (700, 1500, 256, 2, 128), (2000, 4000, 352, 3, 160)])
+@pytest.mark.parametrize("n_rows,T,d,K,dh", [(37, 100, 64, 2, 32), (700, 1500, 256, 2, 128), (2000, 4000, 352, 3, 160),
+                                            (999, 2100, 352, 2, 176)])
 def test_heads_forward_backward(ops, n_rows, T, d, K, dh):
     from paper_2602_11410_b200 import _lib as L
     Hs, rows, hw, W1cat, bucket, label = head_case(n_rows, T, d, K, dh)
