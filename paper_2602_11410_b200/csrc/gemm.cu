@@ -54,8 +54,11 @@ __device__ __forceinline__ Unit decode_unit(const GemmKParams& P, int u) {
   while (p + 1 < P.nprob && u >= P.p[p + 1].unit_begin) ++p;
   const KProb& q = P.p[p];
   int local = u - q.unit_begin;
-  const int ks = local % q.split_k;
-  local /= q.split_k;
+  // split-K: K-slice outermost, so the m x n tiles of one K-slice run together and that slice of
+  // both operands stays L2-resident (weight gradients read each activation row block once)
+  const int mn = q.m_tiles * q.n_tiles;
+  const int ks = local / mn;
+  local -= ks * mn;
   const int nt = local % q.n_tiles;
   const int mt = local / q.n_tiles;
   Unit r;
