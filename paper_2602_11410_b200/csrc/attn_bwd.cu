@@ -20,6 +20,20 @@ namespace cadet {
 #ifdef CADET_PHASE_TIMING
 // Phase timers (profiling builds only): per CTA, summed clock64 deltas, [blockIdx][8].
 __device__ unsigned long long g_phase[8192][8];
+// CTA timeline: [blockIdx][kernel 0=dq 1=dkv] {entry, first MMA result, all MMAs done, exit, smid, n}
+__device__ unsigned long long g_trace[8192][2][6];
+CADET_DEV unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+CADET_DEV uint32_t smid() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %smid;" : "=r"(r));
+  return r;
+}
+#define TR(k, slot, v) \
+  if (blockIdx.x < 8192) g_trace[blockIdx.x][k][slot] = (v);
 #define PT_DECL unsigned long long _pt = clock64();
 #define PT_MARK(slot)                                          \
   {                                                            \
@@ -30,7 +44,10 @@ __device__ unsigned long long g_phase[8192][8];
 #else
 #define PT_DECL
 #define PT_MARK(slot)
+#define TR(k, slot, v)
 #endif
+#define PTM(cond, slot) \
+  if (cond) { PT_MARK(slot) }
 
 __device__ __forceinline__ int visit_tile_b(const QTileInfo& qi, int j) { return j < qi.nf ? j : qi.kt2 + (j - qi.nf); }
 __device__ __forceinline__ bool q_sees_k(const QTileInfo& qi, int kt) {
@@ -71,6 +88,7 @@ __global__ void __launch_bounds__(192, 1)
   const int q0 = sa + qi.qt * 128;
   const int rows_valid = min(128, se - q0);
   const int n_kv = qi.nf + (qi.qt + 1 - qi.kt2);
+  if (threadIdx.x == 0) { TR(0, 0, gtime()); TR(0, 4, smid()); TR(0, 5, n_kv); }
 
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -181,6 +199,7 @@ __global__ void __launch_bounds__(192, 1)
       mbar_wait(&bars->s_full[st], use & 1);
       mbar_wait(&bars->dp_full, j & 1);
       tc_fence_after();
+      if (j == 0 && rt == 0) { TR(0, 1, gtime()); }
 #pragma unroll 1
       for (int c = 0; c < 4; ++c) {
         uint32_t us[32], ud[32];
@@ -212,6 +231,7 @@ __global__ void __launch_bounds__(192, 1)
       mbar_wait(&bars->dq_done, 0);
       tc_fence_after();
     }
+    if (rt == 0) { TR(0, 2, gtime()); }
 #pragma unroll 1
     for (int c = 0; c < G::HDP / 32; ++c) {
       uint32_t u[32];
@@ -230,6 +250,7 @@ __global__ void __launch_bounds__(192, 1)
   __syncthreads();
   tc_fence_after();
   if (warp == 1) tmem_dealloc<512>(tmem);
+  if (threadIdx.x == 0) { TR(0, 3, gtime()); }
 }
 
 // ============================================================================ dK / dV kernel
@@ -260,6 +281,41 @@ struct DkvBars {
   int32_t n_it;
 };
 
+// One 32-column chunk of P^T / dS^T for key row `key` (thread): straight-line, with the
+// per-column vectors (LSE*log2e, D, visible-prefix end) read from shared memory at vaddr,
+// vaddr + 256 and vaddr + 512.  MASKED: column i is visible iff key < e_i or bit i of extra.
+// dS^T is left unscaled (the dK epilogue applies 1/sqrt(hd)).
+template <bool MASKED>
+CADET_DEV void dkv_chunk(const uint32_t (&us)[32], const uint32_t (&ud)[32], uint32_t vaddr, int key, uint32_t extra,
+                         float sl2, uint32_t (&wp)[16], uint32_t (&wd)[16]) {
+#pragma unroll
+  for (int i = 0; i < 32; i += 4) {
+    const float4 l4 = lds_f4(vaddr + i * 4);
+    const float4 d4 = lds_f4(vaddr + 256 + i * 4);
+    const float lv[4] = {l4.x, l4.y, l4.z, l4.w}, dv[4] = {d4.x, d4.y, d4.z, d4.w};
+    int ev[4] = {0, 0, 0, 0};
+    if (MASKED) {
+      const int4 e4 = lds_i4(vaddr + 512 + i * 4);
+      ev[0] = e4.x, ev[1] = e4.y, ev[2] = e4.z, ev[3] = e4.w;
+    }
+    float pv[4], sv[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      float x = fmaf(__uint_as_float(us[i + e]), sl2, -lv[e]);
+      if (MASKED) {
+        const bool vis = (key < ev[e]) | (((extra >> (i + e)) & 1u) != 0u);
+        x = vis ? x : -INFINITY;
+      }
+      pv[e] = fast_exp2(x);
+      sv[e] = pv[e] * (__uint_as_float(ud[i + e]) - dv[e]);
+    }
+    wp[i >> 1] = pack_bf16(pv[0], pv[1]);
+    wp[(i >> 1) + 1] = pack_bf16(pv[2], pv[3]);
+    wd[i >> 1] = pack_bf16(sv[0], sv[1]);
+    wd[(i >> 1) + 1] = pack_bf16(sv[2], sv[3]);
+  }
+}
+
 template <int HD>
 __global__ void __launch_bounds__(320, 1)
     attn_bwd_dkv_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constant__ CUtensorMap mK,
@@ -279,6 +335,7 @@ __global__ void __launch_bounds__(320, 1)
   const int nq_s = (se - sa + 127) / 128;
   const int k0 = sa + kt * 128;
   const int keys_valid = min(128, se - k0);
+  if (threadIdx.x == 0) { TR(1, 0, gtime()); TR(1, 4, smid()); }
 
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -380,11 +437,14 @@ __global__ void __launch_bounds__(320, 1)
         mma_commit(&bars->sdp_full[hf]);
       };
       if (nh > 0) issue_sdp(0);
+      PT_DECL
       for (int hh = 0; hh < nh; ++hh) {
         const int it = hh >> 1, hf = hh & 1, st = it & 1;
         if (hh + 1 < nh) issue_sdp(hh + 1);
+        PT_MARK(5)
         mbar_wait(&bars->pds_ready[hf], (hh >> 1) & 1);
         tc_fence_after();
+        PT_MARK(6)
         const uint32_t sQ = smem_u32(smem + C::Q_OFF + st * G::TILE_BYTES);
         const uint32_t sdO = smem_u32(smem + C::DO_OFF + st * G::TILE_BYTES);
 #pragma unroll
@@ -414,7 +474,9 @@ __global__ void __launch_bounds__(320, 1)
     const float LOG2E = 1.4426950408889634f;
     float* vgrp = vec + grp * 2 * 256;
     float nl = 0.f, nd = 0.f;
-    int ne = -1, nw = -2;
+    int ne = -1;
+    // query row key+1 carries the PAIR_PREV bit: then it sees this key (the transposed pair cell)
+    const bool ppn = key_valid && key + 1 < se && p.plan.row_pp[key + 1] != 0;
     auto fetch = [&](int it) {  // the group's first 64 threads load the 64 columns' vectors
       if (gt >= 64) return;
       const int q = sa + (list[it] & 0xFFFF) * 128 + grp * 64 + gt;
@@ -422,73 +484,51 @@ __global__ void __launch_bounds__(320, 1)
       nl = v ? p.lse[(size_t)h * p.T + q] * LOG2E : INFINITY;
       nd = v ? p.D[(size_t)h * p.T + q] : 0.f;
       ne = v ? p.plan.kv_end[q] : -1;
-      nw = v ? (q | (p.plan.row_pp[q] ? (1 << 30) : 0)) : -2;
     };
     if (n_it > 0) fetch(0);
+    const bool tracer = gt == 0;
+    PT_DECL
     for (int it = 0; it < n_it; ++it) {
+      PTM(tracer, 4)
       const bool full = (list[it] >> 30) & 1;
-      const bool near = (list[it] >> 29) & 1;
+      const int qbase = sa + (list[it] & 0xFFFF) * 128 + grp * 64;
       float* vb = vgrp + (it & 1) * 256;
-      int* vbi = reinterpret_cast<int*>(vb);
       if (gt < 64) {
         vb[gt] = nl;
         vb[64 + gt] = nd;
-        vbi[128 + gt] = ne;
-        vbi[192 + gt] = nw;
+        reinterpret_cast<int*>(vb)[128 + gt] = ne;
       }
       if (it + 1 < n_it) fetch(it + 1);
       named_bar_sync(1 + grp, 128);
+      PTM(tracer, 0)
       mbar_wait(&bars->sdp_full[grp], it & 1);
       tc_fence_after();
+      PTM(tracer, 1)
+      if (it == 0 && gt == 0 && grp == 0) { TR(1, 1, gtime()); TR(1, 5, n_it); }
+      const uint32_t vs = smem_u32(vb);
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
         uint32_t us[32], ud[32];
         tmem_ld32(tmem_addr(tmem, quarter, C::S_COL + grp * 64 + c * 32), us);
         tmem_ld32(tmem_addr(tmem, quarter, C::DP_COL + grp * 64 + c * 32), ud);
         tmem_ld_wait();
+        PTM(tracer, 2)
         uint32_t wp[16], wd[16];
-#pragma unroll
-        for (int q4 = 0; q4 < 32; q4 += 4) {
-          const float4 l4 = *reinterpret_cast<const float4*>(vb + c * 32 + q4);
-          const float4 d4 = *reinterpret_cast<const float4*>(vb + 64 + c * 32 + q4);
-          const float lv[4] = {l4.x, l4.y, l4.z, l4.w}, dv[4] = {d4.x, d4.y, d4.z, d4.w};
-          float pv[4], sv[4];
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const float xe = fmaf(__uint_as_float(us[q4 + e]), sl2, -lv[e]);
-            pv[e] = fast_exp2(xe);
-          }
-          if (!full) {
-            const int4 e4 = *reinterpret_cast<const int4*>(vbi + 128 + c * 32 + q4);
-            const int ev[4] = {e4.x, e4.y, e4.z, e4.w};  // -1 for query rows outside the sequence
-            if (!near) {  // far pair: only the visible prefix can admit this key
-#pragma unroll
-              for (int e = 0; e < 4; ++e)
-                if (!(key_valid && key < ev[e])) pv[e] = 0.f;
-            } else {
-              const int4 w4 = *reinterpret_cast<const int4*>(vbi + 192 + c * 32 + q4);
-              const int wv[4] = {w4.x, w4.y, w4.z, w4.w};
-#pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                const int qw = wv[e];
-                const int qq = qw & ~(1 << 30);
-                const bool ppq = (qw >= 0) && (qw & (1 << 30));
-                const bool ok = key_valid && qw >= 0 && ((key < ev[e]) || (key == qq) || (ppq && key == qq - 1));
-                if (!ok) pv[e] = 0.f;
-              }
-            }
-          }
-#pragma unroll
-          for (int e = 0; e < 4; ++e) sv[e] = pv[e] * (__uint_as_float(ud[q4 + e]) - dv[e]) * p.scale;
-          wp[q4 >> 1] = pack_bf16(pv[0], pv[1]);
-          wp[(q4 >> 1) + 1] = pack_bf16(pv[2], pv[3]);
-          wd[q4 >> 1] = pack_bf16(sv[0], sv[1]);
-          wd[(q4 >> 1) + 1] = pack_bf16(sv[2], sv[3]);
+        if (full) {
+          dkv_chunk<false>(us, ud, vs + c * 128, key, 0u, sl2, wp, wd);
+        } else {
+          // diagonal (key == q) and transposed pair (q == key + 1 with PAIR_PREV) columns of the chunk
+          const int dd = key - (qbase + c * 32);
+          uint32_t extra = 0;
+          if (key_valid && dd >= 0 && dd < 32) extra |= 1u << dd;
+          if (ppn && dd + 1 >= 0 && dd + 1 < 32) extra |= 1u << (dd + 1);
+          dkv_chunk<true>(us, ud, vs + c * 128, key, extra, sl2, wp, wd);
         }
         // P^T / dS^T chunk c -> columns [16c, 16c + 16) of this half: only this thread's own,
         // already-loaded S^T / dP^T chunk 0 is overwritten
         tmem_st16(tmem_addr(tmem, quarter, C::S_COL + grp * 64 + c * 16), wp);
         tmem_st16(tmem_addr(tmem, quarter, C::DP_COL + grp * 64 + c * 16), wd);
+        PTM(tracer, 3)
       }
       tmem_st_wait();
       tc_fence_before();
@@ -499,10 +539,12 @@ __global__ void __launch_bounds__(320, 1)
       mbar_wait(&bars->mma_done, 0);
       tc_fence_after();
     }
+    if (gt == 0 && grp == 0) { TR(1, 2, gtime()); }
 #pragma unroll 1
     for (int which = 0; which < 2; ++which) {
       void* out = which == 0 ? p.dK : p.dV;
       const int col0 = which == 0 ? C::DK_COL : C::DV_COL;
+      const float f = which == 0 ? p.scale : 1.f;  // dS^T was accumulated without 1/sqrt(hd)
 #pragma unroll 1
       for (int c = grp; c < G::HDP / 32; c += 2) {
         uint32_t u[32];
@@ -514,16 +556,17 @@ __global__ void __launch_bounds__(320, 1)
           if (p.out_f32) {
             float* o = reinterpret_cast<float*>(out) + off;
             for (int j = 0; j < ncol; j += 4)
-              *reinterpret_cast<float4*>(o + j) = make_float4(__uint_as_float(u[j]), __uint_as_float(u[j + 1]),
-                                                              __uint_as_float(u[j + 2]), __uint_as_float(u[j + 3]));
+              *reinterpret_cast<float4*>(o + j) =
+                  make_float4(f * __uint_as_float(u[j]), f * __uint_as_float(u[j + 1]),
+                              f * __uint_as_float(u[j + 2]), f * __uint_as_float(u[j + 3]));
           } else {
             __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(out) + off;
             for (int j = 0; j < ncol; j += 8)
               *reinterpret_cast<uint4*>(o + j) =
-                  make_uint4(pack_bf16(__uint_as_float(u[j]), __uint_as_float(u[j + 1])),
-                             pack_bf16(__uint_as_float(u[j + 2]), __uint_as_float(u[j + 3])),
-                             pack_bf16(__uint_as_float(u[j + 4]), __uint_as_float(u[j + 5])),
-                             pack_bf16(__uint_as_float(u[j + 6]), __uint_as_float(u[j + 7])));
+                  make_uint4(pack_bf16(f * __uint_as_float(u[j]), f * __uint_as_float(u[j + 1])),
+                             pack_bf16(f * __uint_as_float(u[j + 2]), f * __uint_as_float(u[j + 3])),
+                             pack_bf16(f * __uint_as_float(u[j + 4]), f * __uint_as_float(u[j + 5])),
+                             pack_bf16(f * __uint_as_float(u[j + 6]), f * __uint_as_float(u[j + 7])));
           }
         }
       }
@@ -533,6 +576,7 @@ __global__ void __launch_bounds__(320, 1)
   __syncthreads();
   tc_fence_after();
   if (warp == 1) tmem_dealloc<512>(tmem);
+  if (threadIdx.x == 0) { TR(1, 3, gtime()); }
 }
 
 // D_i = rowsum(dO_i * O_i) per head (FlashAttention preprocess), bf16 inputs, fp32 out [H, T].
@@ -610,6 +654,11 @@ cudaError_t attn_bwd_launch(const void* Qr, const void* Kr, const void* V, const
 extern "C" int cadet_debug_phase_read(unsigned long long* out, int n) {
   if (n > 8192 * 8) n = 8192 * 8;
   cudaMemcpyFromSymbol(out, cadet::g_phase, sizeof(unsigned long long) * n);
+  return n;
+}
+extern "C" int cadet_debug_trace_read(unsigned long long* out, int n) {
+  if (n > 8192 * 12) n = 8192 * 12;
+  cudaMemcpyFromSymbol(out, cadet::g_trace, sizeof(unsigned long long) * n);
   return n;
 }
 extern "C" int cadet_debug_phase_reset() {
