@@ -12,6 +12,8 @@
 //   consumed columns;  dV += P^T dO_i, dK += dS^T Q_i as TS MMAs; Q_i / dO_i double-buffered.
 // The extra S/dP recompute (7 MMAs per tile pair instead of 5) buys the removal of 1.1 GB of dQ
 // atomics per C4 step and of the drain -> dP dependency.
+#include <algorithm>
+
 #include "attn_common.cuh"
 #include "prof.cuh"
 
@@ -55,6 +57,11 @@ __device__ __forceinline__ bool q_sees_k(const QTileInfo& qi, int kt) {
 }
 
 // ============================================================================ dQ kernel
+// Persistent: CTA c takes work items w = c, c + gridDim.x, ... of the (q-tile in fwd_order, head)
+// list (LPT order preserved per stride).  Barrier phases count globally across items; Q/dO are
+// released (qd_empty) once the item's last S / dP MMA is issued and the dQ accumulator once the
+// compute warps have drained it (dq_free), so the next item's loads and first MMAs overlap the
+// current item's tail and dQ store.
 template <int HD>
 struct DqCfg {
   using G = HeadGeom<HD>;
@@ -65,30 +72,40 @@ struct DqCfg {
   static constexpr int BAR_OFF = V_OFF + 2 * G::TILE_BYTES;
   static constexpr int SMEM = BAR_OFF + 256 + 1024;
   static constexpr int S_COL = 0, DP_COL = 256, DQ_COL = 384;  // S double-buffered
+  static constexpr int THREADS = 320;  // producer, MMA, 2 compute warpgroups (64 S/dP columns each)
 };
 
 struct DqBars {
-  uint64_t qd_full, k_full[2], k_empty[2], v_full[2], v_empty[2], s_full[2], s_free[2], dp_full, ds_ready, dq_done;
+  uint64_t qd_full, qd_empty, k_full[2], k_empty[2], v_full[2], v_empty[2], s_full[2], s_free[2], dp_full, ds_ready,
+      dq_done, dq_free;
   uint32_t tmem_base;
 };
 
+struct DqWork {
+  QTileInfo qi;
+  int h, sa, se, q0, rows_valid, n_kv;
+};
+CADET_DEV DqWork dq_work(const AttnParams& p, int w) {
+  DqWork t;
+  t.h = w % p.H;
+  t.qi = p.plan.qinfo[p.plan.fwd_order[w / p.H]];
+  t.sa = p.cu[t.qi.seq];
+  t.se = p.cu[t.qi.seq + 1];
+  t.q0 = t.sa + t.qi.qt * 128;
+  t.rows_valid = min(128, t.se - t.q0);
+  t.n_kv = t.qi.nf + (t.qi.qt + 1 - t.qi.kt2);
+  return t;
+}
+
 template <int HD>
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(320, 1)
     attn_bwd_dq_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constant__ CUtensorMap mK,
                        const __grid_constant__ CUtensorMap mV, const __grid_constant__ CUtensorMap mdO,
                        const AttnParams p) {
   using G = HeadGeom<HD>;
   using C = DqCfg<HD>;
-  const int nq_total = p.plan.counters[0];
-  const int b = blockIdx.x / p.H;
-  const int h = blockIdx.x % p.H;
-  if (b >= nq_total) return;
-  const QTileInfo qi = p.plan.qinfo[p.plan.fwd_order[b]];
-  const int sa = p.cu[qi.seq], se = p.cu[qi.seq + 1];
-  const int q0 = sa + qi.qt * 128;
-  const int rows_valid = min(128, se - q0);
-  const int n_kv = qi.nf + (qi.qt + 1 - qi.kt2);
-  if (threadIdx.x == 0) { TR(0, 0, gtime()); TR(0, 4, smid()); TR(0, 5, n_kv); }
+  const int n_work = p.plan.counters[0] * p.H;
+  if (threadIdx.x == 0) { TR(0, 0, gtime()); TR(0, 4, smid()); }
 
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -96,17 +113,19 @@ __global__ void __launch_bounds__(192, 1)
   const uint32_t warp = warp_id(), lane = lane_id();
   if (threadIdx.x == 0) {
     mbar_init(&bars->qd_full, 1);
+    mbar_init(&bars->qd_empty, 1);
     for (int i = 0; i < 2; ++i) {
       mbar_init(&bars->k_full[i], 1);
       mbar_init(&bars->k_empty[i], 1);
       mbar_init(&bars->v_full[i], 1);
       mbar_init(&bars->v_empty[i], 1);
       mbar_init(&bars->s_full[i], 1);
-      mbar_init(&bars->s_free[i], 128);
+      mbar_init(&bars->s_free[i], 256);
     }
     mbar_init(&bars->dp_full, 1);
-    mbar_init(&bars->ds_ready, 128);
+    mbar_init(&bars->ds_ready, 256);
     mbar_init(&bars->dq_done, 1);
+    mbar_init(&bars->dq_free, 256);
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc<512>(&bars->tmem_base);
@@ -117,27 +136,32 @@ __global__ void __launch_bounds__(192, 1)
 
   if (warp == 0) {
     if (elect_one()) {
-      mbar_expect_tx(&bars->qd_full, 2 * G::TILE_BYTES);
+      int gk = 0;  // global k-tile counter: stage gk & 1, use gk >> 1
+      for (int w = blockIdx.x, wi = 0; w < n_work; w += gridDim.x, ++wi) {
+        const DqWork t = dq_work(p, w);
+        if (wi > 0) mbar_wait(&bars->qd_empty, (wi - 1) & 1);
+        mbar_expect_tx(&bars->qd_full, 2 * G::TILE_BYTES);
 #pragma unroll
-      for (int blk = 0; blk < G::NB; ++blk) {
-        tma_load_3d(smem + C::Q_OFF + blk * G::BLK, &mQ, &bars->qd_full, blk * G::CB, h, q0);
-        tma_load_3d(smem + C::DO_OFF + blk * G::BLK, &mdO, &bars->qd_full, blk * G::CB, h, q0);
-      }
-      for (int j = 0; j < n_kv; ++j) {
-        const int st = j & 1, use = j >> 1;
-        const int krow = sa + visit_tile_b(qi, j) * 128;
-        if (use > 0) mbar_wait(&bars->k_empty[st], (use - 1) & 1);
-        mbar_expect_tx(&bars->k_full[st], G::TILE_BYTES);
+        for (int blk = 0; blk < G::NB; ++blk) {
+          tma_load_3d(smem + C::Q_OFF + blk * G::BLK, &mQ, &bars->qd_full, blk * G::CB, t.h, t.q0);
+          tma_load_3d(smem + C::DO_OFF + blk * G::BLK, &mdO, &bars->qd_full, blk * G::CB, t.h, t.q0);
+        }
+        for (int j = 0; j < t.n_kv; ++j, ++gk) {
+          const int st = gk & 1, use = gk >> 1;
+          const int krow = t.sa + visit_tile_b(t.qi, j) * 128;
+          if (use > 0) mbar_wait(&bars->k_empty[st], (use - 1) & 1);
+          mbar_expect_tx(&bars->k_full[st], G::TILE_BYTES);
 #pragma unroll
-        for (int blk = 0; blk < G::NB; ++blk)
-          tma_load_3d(smem + C::K_OFF + st * G::TILE_BYTES + blk * G::BLK, &mK, &bars->k_full[st], blk * G::CB, h,
-                      krow);
-        if (use > 0) mbar_wait(&bars->v_empty[st], (use - 1) & 1);
-        mbar_expect_tx(&bars->v_full[st], G::TILE_BYTES);
+          for (int blk = 0; blk < G::NB; ++blk)
+            tma_load_3d(smem + C::K_OFF + st * G::TILE_BYTES + blk * G::BLK, &mK, &bars->k_full[st], blk * G::CB, t.h,
+                        krow);
+          if (use > 0) mbar_wait(&bars->v_empty[st], (use - 1) & 1);
+          mbar_expect_tx(&bars->v_full[st], G::TILE_BYTES);
 #pragma unroll
-        for (int blk = 0; blk < G::NB; ++blk)
-          tma_load_3d(smem + C::V_OFF + st * G::TILE_BYTES + blk * G::BLK, &mV, &bars->v_full[st], blk * G::CB, h,
-                      krow);
+          for (int blk = 0; blk < G::NB; ++blk)
+            tma_load_3d(smem + C::V_OFF + st * G::TILE_BYTES + blk * G::BLK, &mV, &bars->v_full[st], blk * G::CB, t.h,
+                        krow);
+        }
       }
     }
   } else if (warp == 1) {
@@ -145,105 +169,131 @@ __global__ void __launch_bounds__(192, 1)
       const uint32_t id_s = idesc_bf16(128, 128, 0, 0);
       const uint32_t id_q = idesc_bf16(128, G::HDP, 0, 1);
       const uint32_t sQ = smem_u32(smem + C::Q_OFF), sdO = smem_u32(smem + C::DO_OFF);
-      mbar_wait(&bars->qd_full, 0);
-      auto issue_s = [&](int j) {
-        const int st = j & 1, use = j >> 1;
-        if (use > 0) mbar_wait(&bars->s_free[st], (use - 1) & 1);
-        mbar_wait(&bars->k_full[st], use & 1);
+      int gs = 0;  // global k-tile counter (S buffer, K/V stage)
+      for (int w = blockIdx.x, wi = 0; w < n_work; w += gridDim.x, ++wi) {
+        const int n_kv = dq_work(p, w).n_kv;
+        mbar_wait(&bars->qd_full, wi & 1);
         tc_fence_after();
-        const uint32_t sK = smem_u32(smem + C::K_OFF + st * G::TILE_BYTES);
+        auto issue_s = [&](int j) {
+          const int g = gs + j, st = g & 1, use = g >> 1;
+          if (use > 0) mbar_wait(&bars->s_free[st], (use - 1) & 1);
+          mbar_wait(&bars->k_full[st], use & 1);
+          tc_fence_after();
+          const uint32_t sK = smem_u32(smem + C::K_OFF + st * G::TILE_BYTES);
 #pragma unroll
-        for (int kk = 0; kk < G::HDP / 16; ++kk)
-          mma_bf16_ss(tmem + C::S_COL + st * 128, kmajor_desc<HD>(sQ, kk), kmajor_desc<HD>(sK, kk), id_s,
-                      kk > 0 ? 1u : 0u);
-        mma_commit(&bars->s_full[st]);
-      };
-      if (n_kv > 0) issue_s(0);
-      for (int j = 0; j < n_kv; ++j) {
-        const int st = j & 1, use = j >> 1;
-        // dP_j over dS_{j-1}: in-order after dQ_{j-1}, which read it
-        mbar_wait(&bars->v_full[st], use & 1);
-        tc_fence_after();
-        const uint32_t sV = smem_u32(smem + C::V_OFF + st * G::TILE_BYTES);
+          for (int kk = 0; kk < G::HDP / 16; ++kk)
+            mma_bf16_ss(tmem + C::S_COL + st * 128, kmajor_desc<HD>(sQ, kk), kmajor_desc<HD>(sK, kk), id_s,
+                        kk > 0 ? 1u : 0u);
+          mma_commit(&bars->s_full[st]);
+        };
+        if (n_kv > 0) issue_s(0);
+        for (int j = 0; j < n_kv; ++j) {
+          const int g = gs + j, st = g & 1, use = g >> 1;
+          // dP_j over dS_{j-1}: in-order after dQ_{j-1}, which read it
+          mbar_wait(&bars->v_full[st], use & 1);
+          tc_fence_after();
+          const uint32_t sV = smem_u32(smem + C::V_OFF + st * G::TILE_BYTES);
 #pragma unroll
-        for (int kk = 0; kk < G::HDP / 16; ++kk)
-          mma_bf16_ss(tmem + C::DP_COL, kmajor_desc<HD>(sdO, kk), kmajor_desc<HD>(sV, kk), id_s, kk > 0 ? 1u : 0u);
-        mma_commit(&bars->dp_full);
-        mma_commit(&bars->v_empty[st]);
-        if (j + 1 < n_kv) issue_s(j + 1);
-        mbar_wait(&bars->ds_ready, j & 1);
-        tc_fence_after();
-        const uint32_t sK = smem_u32(smem + C::K_OFF + st * G::TILE_BYTES);
+          for (int kk = 0; kk < G::HDP / 16; ++kk)
+            mma_bf16_ss(tmem + C::DP_COL, kmajor_desc<HD>(sdO, kk), kmajor_desc<HD>(sV, kk), id_s, kk > 0 ? 1u : 0u);
+          mma_commit(&bars->dp_full);
+          mma_commit(&bars->v_empty[st]);
+          if (j + 1 < n_kv)
+            issue_s(j + 1);
+          else
+            mma_commit(&bars->qd_empty);  // the item's last reads of Q (S) and dO (dP) are issued
+          mbar_wait(&bars->ds_ready, g & 1);
+          tc_fence_after();
+          if (j == 0 && wi > 0) {
+            mbar_wait(&bars->dq_free, (wi - 1) & 1);
+            tc_fence_after();
+          }
+          const uint32_t sK = smem_u32(smem + C::K_OFF + st * G::TILE_BYTES);
 #pragma unroll
-        for (int kk = 0; kk < 128 / 16; ++kk)
-          mma_bf16_ts(tmem + C::DQ_COL, tmem + C::DP_COL + kk * 8, mnmajor_desc<HD>(sK, kk), id_q,
-                      (j > 0 || kk > 0) ? 1u : 0u);
-        mma_commit(&bars->k_empty[st]);
+          for (int kk = 0; kk < 128 / 16; ++kk)
+            mma_bf16_ts(tmem + C::DQ_COL, tmem + C::DP_COL + (kk >> 1) * 32 + (kk & 1) * 8, mnmajor_desc<HD>(sK, kk),
+                        id_q, (j > 0 || kk > 0) ? 1u : 0u);
+          mma_commit(&bars->k_empty[st]);
+        }
+        if (n_kv == 0) {
+          mma_commit(&bars->qd_empty);
+          if (wi > 0) mbar_wait(&bars->dq_free, (wi - 1) & 1);
+        }
+        mma_commit(&bars->dq_done);
+        gs += n_kv;
       }
-      mma_commit(&bars->dq_done);
     }
   } else {
+    // thread = query row; warpgroup grp (warps 2..5 -> 0, 6..9 -> 1) owns S/dP columns [64 grp, +64)
     const uint32_t quarter = warp & 3;
+    const int grp = (warp - 2) >> 2;
     const int rt = quarter * 32 + lane;
-    const int r = q0 + rt;
-    const bool valid = rt < rows_valid;
-    const int e_r = valid ? p.plan.kv_end[r] : 0;
-    const bool pp = valid ? (p.plan.row_pp[r] != 0) : false;
-    const float lse2 = valid ? p.lse[(size_t)h * p.T + r] * 1.4426950408889634f : 0.f;
-    const float Dr = valid ? p.D[(size_t)h * p.T + r] : 0.f;
     const float sl2 = p.scale_log2;
-    for (int j = 0; j < n_kv; ++j) {
-      const int st = j & 1, use = j >> 1;
-      const int k0 = sa + visit_tile_b(qi, j) * 128;
-      const bool partial = !valid || (e_r < k0 + 128);
-      mbar_wait(&bars->s_full[st], use & 1);
-      mbar_wait(&bars->dp_full, j & 1);
-      tc_fence_after();
-      if (j == 0 && rt == 0) { TR(0, 1, gtime()); }
-#pragma unroll 1
-      for (int c = 0; c < 4; ++c) {
-        uint32_t us[32], ud[32];
-        tmem_ld32(tmem_addr(tmem, quarter, C::S_COL + st * 128 + c * 32), us);
-        tmem_ld32(tmem_addr(tmem, quarter, C::DP_COL + c * 32), ud);
-        tmem_ld_wait();
-        uint32_t w[16];
-        const uint32_t m = !partial ? 0xFFFFFFFFu : (valid ? row_mask32(e_r, r, pp, k0 + c * 32) : 0u);
+    int gs = 0;
+    for (int w = blockIdx.x, wi = 0; w < n_work; w += gridDim.x, ++wi) {
+      const DqWork t = dq_work(p, w);
+      const int r = t.q0 + rt;
+      const bool valid = rt < t.rows_valid;
+      const int e_r = valid ? p.plan.kv_end[r] : 0;
+      const bool pp = valid ? (p.plan.row_pp[r] != 0) : false;
+      const float lse2 = valid ? p.lse[(size_t)t.h * p.T + r] * 1.4426950408889634f : 0.f;
+      const float Dr = valid ? p.D[(size_t)t.h * p.T + r] : 0.f;
+      for (int j = 0; j < t.n_kv; ++j) {
+        const int g = gs + j, st = g & 1, use = g >> 1;
+        const int k0 = t.sa + visit_tile_b(t.qi, j) * 128;
+        const bool partial = !valid || (e_r < k0 + 128);
+        mbar_wait(&bars->s_full[st], use & 1);
+        mbar_wait(&bars->dp_full, g & 1);
+        tc_fence_after();
 #pragma unroll
-        for (int q = 0; q < 32; q += 2) {
-          float ds[2];
+        for (int cc = 0; cc < 2; ++cc) {
+          const int c = 2 * grp + cc;
+          uint32_t us[32], ud[32];
+          tmem_ld32(tmem_addr(tmem, quarter, C::S_COL + st * 128 + c * 32), us);
+          tmem_ld32(tmem_addr(tmem, quarter, C::DP_COL + c * 32), ud);
+          tmem_ld_wait();
+          uint32_t wv[16];
+          const uint32_t m = !partial ? 0xFFFFFFFFu : (valid ? row_mask32(e_r, r, pp, k0 + c * 32) : 0u);
 #pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const float xe = fmaf(__uint_as_float(us[q + e]), sl2, -lse2);
-            float pr = fast_exp2(xe);
-            if (!((m >> (q + e)) & 1u)) pr = 0.f;
-            ds[e] = pr * (__uint_as_float(ud[q + e]) - Dr) * p.scale;
+          for (int q = 0; q < 32; q += 2) {
+            float ds[2];
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              float xe = fmaf(__uint_as_float(us[q + e]), sl2, -lse2);
+              xe = ((m >> (q + e)) & 1u) ? xe : -INFINITY;
+              const float pr = fast_exp2(xe);
+              ds[e] = pr * (__uint_as_float(ud[q + e]) - Dr);  // 1/sqrt(hd) applied in the dQ epilogue
+            }
+            wv[q >> 1] = pack_bf16(ds[0], ds[1]);
           }
-          w[q >> 1] = pack_bf16(ds[0], ds[1]);
+          // packed dS of keys [32c, 32c + 32) -> dP columns [32c, 32c + 16): this thread's own, loaded chunk
+          tmem_st16(tmem_addr(tmem, quarter, C::DP_COL + c * 32), wv);
         }
-        tmem_st16(tmem_addr(tmem, quarter, C::DP_COL + c * 16), w);  // over dP chunk c/2 (consumed)
+        tmem_st_wait();
+        tc_fence_before();
+        mbar_arrive(&bars->s_free[st]);
+        mbar_arrive(&bars->ds_ready);
       }
-      tmem_st_wait();
-      tc_fence_before();
-      mbar_arrive(&bars->s_free[st]);
-      mbar_arrive(&bars->ds_ready);
-    }
-    if (n_kv > 0) {
-      mbar_wait(&bars->dq_done, 0);
+      mbar_wait(&bars->dq_done, wi & 1);
       tc_fence_after();
-    }
-    if (rt == 0) { TR(0, 2, gtime()); }
 #pragma unroll 1
-    for (int c = 0; c < G::HDP / 32; ++c) {
-      uint32_t u[32];
-      tmem_ld32(tmem_addr(tmem, quarter, C::DQ_COL + c * 32), u);
-      tmem_ld_wait();
-      if (valid) {
-        const int ncol = min(32, p.hd - c * 32);
-        float* o = p.dQ + (size_t)r * p.d + (size_t)h * p.hd + c * 32;
-        for (int q = 0; q < ncol; q += 4)
-          *reinterpret_cast<float4*>(o + q) = make_float4(__uint_as_float(u[q]), __uint_as_float(u[q + 1]),
-                                                          __uint_as_float(u[q + 2]), __uint_as_float(u[q + 3]));
+      for (int c = grp; c < G::HDP / 32; c += 2) {
+        uint32_t u[32];
+        tmem_ld32(tmem_addr(tmem, quarter, C::DQ_COL + c * 32), u);
+        tmem_ld_wait();
+        if (valid) {
+          const float f = t.n_kv > 0 ? p.scale : 0.f;
+          const int ncol = min(32, p.hd - c * 32);
+          float* o = p.dQ + (size_t)r * p.d + (size_t)t.h * p.hd + c * 32;
+          for (int q = 0; q < ncol; q += 4)
+            *reinterpret_cast<float4*>(o + q) =
+                make_float4(f * __uint_as_float(u[q]), f * __uint_as_float(u[q + 1]), f * __uint_as_float(u[q + 2]),
+                            f * __uint_as_float(u[q + 3]));
+        }
       }
+      tc_fence_before();
+      mbar_arrive(&bars->dq_free);
+      gs += t.n_kv;
     }
   }
   tc_fence_before();
@@ -254,33 +304,13 @@ __global__ void __launch_bounds__(192, 1)
 }
 
 // ============================================================================ dK / dV kernel
-// Each visited q-tile is processed as two 64-column halves h (global half index): the MMA warp
-// issues S^T_h = K Q_h^T and dP^T_h = V dO_h^T into TMEM half-buffer (h & 1) BEFORE waiting for
-// half h-1's P^T/dS^T, so the tensor core works while a compute warpgroup (one per half-buffer,
-// thread = key row, 64 q columns) turns the previous half into P^T / dS^T.
-template <int HD>
-struct DkvCfg {
-  using G = HeadGeom<HD>;
-  static constexpr int K_OFF = 0;
-  static constexpr int V_OFF = K_OFF + G::TILE_BYTES;
-  static constexpr int Q_OFF = V_OFF + G::TILE_BYTES;          // two stages
-  static constexpr int DO_OFF = Q_OFF + 2 * G::TILE_BYTES;     // two stages
-  static constexpr int VEC_OFF = DO_OFF + 2 * G::TILE_BYTES;   // [2 groups][2 bufs][4][64] x 4 B
-  static constexpr int LIST_OFF = VEC_OFF + 2 * 2 * 4 * 64 * 4;
-  static constexpr int MAX_LIST = 512;
-  static constexpr int BAR_OFF = LIST_OFF + MAX_LIST * 4;
-  static constexpr int SMEM = BAR_OFF + 256 + 1024;
-  // S^T/P^T half-buffers at [0,64) and [64,128); dP^T/dS^T at [128,192) and [192,256)
-  static constexpr int S_COL = 0, DP_COL = 128, DV_COL = 256, DK_COL = 384;
-  static constexpr int THREADS = 320;  // producer, MMA, 2 compute warpgroups (one per half-buffer)
-};
-
-struct DkvBars {
-  uint64_t kv_full, q_full[2], q_empty[2], do_full[2], do_empty[2], sdp_full[2], pds_ready[2], mma_done;
-  uint32_t tmem_base;
-  int32_t n_it;
-};
-
+// Persistent like the dQ kernel, over (k-tile in bwd_order, head) items; each item walks the
+// q-tiles of its plan visit list (bwd_list).  Each visited q-tile is processed as two 64-column
+// halves: the MMA warp issues S^T_h = K Q_h^T and dP^T_h = V dO_h^T into TMEM half-buffer
+// (h & 1) BEFORE waiting for half h-1's P^T/dS^T, so the tensor core works while a compute
+// warpgroup (one per half-buffer, thread = key row, 64 q columns) turns the previous half into
+// P^T / dS^T.  K/V are released (kv_empty) after the item's last S^T/dP^T, the dK/dV
+// accumulators after the compute warps drained them (acc_free).
 // One 32-column chunk of P^T / dS^T for key row `key` (thread): straight-line, with the
 // per-column vectors (LSE*log2e, D, visible-prefix end) read from shared memory at vaddr,
 // vaddr + 256 and vaddr + 512.  MASKED: column i is visible iff key < e_i or bit i of extra.
@@ -317,95 +347,110 @@ CADET_DEV void dkv_chunk(const uint32_t (&us)[32], const uint32_t (&ud)[32], uin
 }
 
 template <int HD>
+struct DkvCfg {
+  using G = HeadGeom<HD>;
+  static constexpr int K_OFF = 0;
+  static constexpr int V_OFF = K_OFF + G::TILE_BYTES;
+  static constexpr int Q_OFF = V_OFF + G::TILE_BYTES;          // two stages
+  static constexpr int DO_OFF = Q_OFF + 2 * G::TILE_BYTES;     // two stages
+  static constexpr int VEC_OFF = DO_OFF + 2 * G::TILE_BYTES;   // [2 groups][2 bufs][256] x 4 B
+  static constexpr int BAR_OFF = VEC_OFF + 2 * 2 * 256 * 4;
+  static constexpr int SMEM = BAR_OFF + 256 + 1024;
+  // S^T/P^T half-buffers at [0,64) and [64,128); dP^T/dS^T at [128,192) and [192,256)
+  static constexpr int S_COL = 0, DP_COL = 128, DV_COL = 256, DK_COL = 384;
+  static constexpr int THREADS = 320;  // producer, MMA, 2 compute warpgroups (one per half-buffer)
+};
+
+struct DkvBars {
+  uint64_t kv_full, kv_empty, q_full[2], q_empty[2], do_full[2], do_empty[2], sdp_full[2], pds_ready[2], mma_done,
+      acc_free;
+  uint32_t tmem_base;
+};
+
+struct DkvWork {
+  int h, seq, kt, sa, se, k0, keys_valid, off, n_it;
+};
+CADET_DEV DkvWork dkv_work(const AttnParams& p, int w) {
+  DkvWork t;
+  t.h = w % p.H;
+  const int g = p.plan.bwd_order[w / p.H];
+  const QTileInfo ki = p.plan.qinfo[g];
+  t.seq = ki.seq;
+  t.kt = ki.qt;
+  t.sa = p.cu[ki.seq];
+  t.se = p.cu[ki.seq + 1];
+  t.k0 = t.sa + t.kt * 128;
+  t.keys_valid = min(128, t.se - t.k0);
+  t.off = p.plan.bwd_off[g];
+  t.n_it = p.plan.bwd_cnt[g];
+  return t;
+}
+
+template <int HD>
 __global__ void __launch_bounds__(320, 1)
     attn_bwd_dkv_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constant__ CUtensorMap mK,
                         const __grid_constant__ CUtensorMap mV, const __grid_constant__ CUtensorMap mdO,
                         const AttnParams p) {
   using G = HeadGeom<HD>;
   using C = DkvCfg<HD>;
-  const int nq_total = p.plan.counters[0];
-  const int b = blockIdx.x / p.H;
-  const int h = blockIdx.x % p.H;
-  if (b >= nq_total) return;
-  const int g = p.plan.bwd_order[b];
-  const QTileInfo ki = p.plan.qinfo[g];
-  const int kt = ki.qt;
-  const int sa = p.cu[ki.seq], se = p.cu[ki.seq + 1];
-  const int tile0 = g - kt;
-  const int nq_s = (se - sa + 127) / 128;
-  const int k0 = sa + kt * 128;
-  const int keys_valid = min(128, se - k0);
+  const int n_work = p.plan.counters[0] * p.H;
   if (threadIdx.x == 0) { TR(1, 0, gtime()); TR(1, 4, smid()); }
 
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   DkvBars* bars = reinterpret_cast<DkvBars*>(smem + C::BAR_OFF);
   float* vec = reinterpret_cast<float*>(smem + C::VEC_OFF);
-  int* list = reinterpret_cast<int*>(smem + C::LIST_OFF);
   const uint32_t warp = warp_id(), lane = lane_id();
-
-  if (warp == 0) {
-    int n = 0;
-    for (int base = kt; base < nq_s; base += 32) {
-      const int qt = base + (int)lane;
-      int entry = -1;
-      if (qt < nq_s) {
-        const QTileInfo qi = p.plan.qinfo[tile0 + qt];
-        if (q_sees_k(qi, kt)) {
-          const bool full = qi.rows == 128 && qi.emin >= (kt + 1) * 128;
-          const bool near = qt - kt <= 1;  // diagonal / pair-prev cells can only occur here
-          entry = qt | (full ? (1 << 30) : 0) | (near ? (1 << 29) : 0);
-        }
-      }
-      const uint32_t m = __ballot_sync(0xffffffffu, entry >= 0);
-      const int pos = n + __popc(m & ((1u << lane) - 1u));
-      if (entry >= 0 && pos < C::MAX_LIST) list[pos] = entry;
-      n += __popc(m);
+  if (threadIdx.x == 0) {
+    mbar_init(&bars->kv_full, 1);
+    mbar_init(&bars->kv_empty, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&bars->q_full[i], 1);
+      mbar_init(&bars->q_empty[i], 1);
+      mbar_init(&bars->do_full[i], 1);
+      mbar_init(&bars->do_empty[i], 1);
+      mbar_init(&bars->sdp_full[i], 1);
+      mbar_init(&bars->pds_ready[i], 128);
     }
-    if (lane == 0) {
-      bars->n_it = min(n, C::MAX_LIST);
-      mbar_init(&bars->kv_full, 1);
-      for (int i = 0; i < 2; ++i) {
-        mbar_init(&bars->q_full[i], 1);
-        mbar_init(&bars->q_empty[i], 1);
-        mbar_init(&bars->do_full[i], 1);
-        mbar_init(&bars->do_empty[i], 1);
-        mbar_init(&bars->sdp_full[i], 1);
-        mbar_init(&bars->pds_ready[i], 128);
-      }
-      mbar_init(&bars->mma_done, 1);
-      fence_mbar_init();
-    }
+    mbar_init(&bars->mma_done, 1);
+    mbar_init(&bars->acc_free, 256);
+    fence_mbar_init();
   }
   if (warp == 1) tmem_alloc<512>(&bars->tmem_base);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = bars->tmem_base;
-  const int n_it = bars->n_it;
+  const int32_t* list = p.plan.bwd_list;
 
   if (warp == 0) {
     if (elect_one()) {
-      mbar_expect_tx(&bars->kv_full, 2 * G::TILE_BYTES);
+      int gq = 0;  // global q-tile counter: stage gq & 1, use gq >> 1
+      for (int w = blockIdx.x, wi = 0; w < n_work; w += gridDim.x, ++wi) {
+        const DkvWork t = dkv_work(p, w);
+        if (wi > 0) mbar_wait(&bars->kv_empty, (wi - 1) & 1);
+        mbar_expect_tx(&bars->kv_full, 2 * G::TILE_BYTES);
 #pragma unroll
-      for (int blk = 0; blk < G::NB; ++blk) {
-        tma_load_3d(smem + C::K_OFF + blk * G::BLK, &mK, &bars->kv_full, blk * G::CB, h, k0);
-        tma_load_3d(smem + C::V_OFF + blk * G::BLK, &mV, &bars->kv_full, blk * G::CB, h, k0);
-      }
-      for (int it = 0; it < n_it; ++it) {  // list entry: qt | full<<30 | near<<29
-        const int st = it & 1, use = it >> 1;
-        const int q0 = sa + (list[it] & 0xFFFF) * 128;
-        if (use > 0) mbar_wait(&bars->q_empty[st], (use - 1) & 1);
-        mbar_expect_tx(&bars->q_full[st], G::TILE_BYTES);
+        for (int blk = 0; blk < G::NB; ++blk) {
+          tma_load_3d(smem + C::K_OFF + blk * G::BLK, &mK, &bars->kv_full, blk * G::CB, t.h, t.k0);
+          tma_load_3d(smem + C::V_OFF + blk * G::BLK, &mV, &bars->kv_full, blk * G::CB, t.h, t.k0);
+        }
+        for (int it = 0; it < t.n_it; ++it, ++gq) {  // list entry: qt | full << 30
+          const int st = gq & 1, use = gq >> 1;
+          const int q0 = t.sa + (list[t.off + it] & 0xFFFF) * 128;
+          if (use > 0) mbar_wait(&bars->q_empty[st], (use - 1) & 1);
+          mbar_expect_tx(&bars->q_full[st], G::TILE_BYTES);
 #pragma unroll
-        for (int blk = 0; blk < G::NB; ++blk)
-          tma_load_3d(smem + C::Q_OFF + st * G::TILE_BYTES + blk * G::BLK, &mQ, &bars->q_full[st], blk * G::CB, h, q0);
-        if (use > 0) mbar_wait(&bars->do_empty[st], (use - 1) & 1);
-        mbar_expect_tx(&bars->do_full[st], G::TILE_BYTES);
+          for (int blk = 0; blk < G::NB; ++blk)
+            tma_load_3d(smem + C::Q_OFF + st * G::TILE_BYTES + blk * G::BLK, &mQ, &bars->q_full[st], blk * G::CB, t.h,
+                        q0);
+          if (use > 0) mbar_wait(&bars->do_empty[st], (use - 1) & 1);
+          mbar_expect_tx(&bars->do_full[st], G::TILE_BYTES);
 #pragma unroll
-        for (int blk = 0; blk < G::NB; ++blk)
-          tma_load_3d(smem + C::DO_OFF + st * G::TILE_BYTES + blk * G::BLK, &mdO, &bars->do_full[st], blk * G::CB, h,
-                      q0);
+          for (int blk = 0; blk < G::NB; ++blk)
+            tma_load_3d(smem + C::DO_OFF + st * G::TILE_BYTES + blk * G::BLK, &mdO, &bars->do_full[st], blk * G::CB,
+                        t.h, q0);
+        }
       }
     }
   } else if (warp == 1) {
@@ -413,54 +458,69 @@ __global__ void __launch_bounds__(320, 1)
       const uint32_t id_s = idesc_bf16(128, 64, 0, 0);
       const uint32_t id_kv = idesc_bf16(128, G::HDP, 0, 1);
       const uint32_t sK = smem_u32(smem + C::K_OFF), sV = smem_u32(smem + C::V_OFF);
-      mbar_wait(&bars->kv_full, 0);
-      const int nh = 2 * n_it;
-      // half hh: q-tile hh >> 1, columns [64 (hh & 1), +64), TMEM half-buffer hh & 1
-      auto issue_sdp = [&](int hh) {
-        const int it = hh >> 1, hf = hh & 1, st = it & 1, use = it >> 1;
-        const uint32_t sQ = smem_u32(smem + C::Q_OFF + st * G::TILE_BYTES) + hf * 64 * G::RB;
-        const uint32_t sdO = smem_u32(smem + C::DO_OFF + st * G::TILE_BYTES) + hf * 64 * G::RB;
-        if (hf == 0) {
-          mbar_wait(&bars->q_full[st], use & 1);
-          mbar_wait(&bars->do_full[st], use & 1);
-          tc_fence_after();
-        }
-        // over P^T/dS^T of half hh-2: in-order after its dV/dK MMAs, issued after pds_ready(hh-2)
-#pragma unroll
-        for (int kk = 0; kk < G::HDP / 16; ++kk)
-          mma_bf16_ss(tmem + C::S_COL + hf * 64, kmajor_desc<HD>(sK, kk), kmajor_desc<HD>(sQ, kk), id_s,
-                      kk > 0 ? 1u : 0u);
-#pragma unroll
-        for (int kk = 0; kk < G::HDP / 16; ++kk)
-          mma_bf16_ss(tmem + C::DP_COL + hf * 64, kmajor_desc<HD>(sV, kk), kmajor_desc<HD>(sdO, kk), id_s,
-                      kk > 0 ? 1u : 0u);
-        mma_commit(&bars->sdp_full[hf]);
-      };
-      if (nh > 0) issue_sdp(0);
-      PT_DECL
-      for (int hh = 0; hh < nh; ++hh) {
-        const int it = hh >> 1, hf = hh & 1, st = it & 1;
-        if (hh + 1 < nh) issue_sdp(hh + 1);
-        PT_MARK(5)
-        mbar_wait(&bars->pds_ready[hf], (hh >> 1) & 1);
+      int gq = 0;  // global q-tile counter; global half index 2 gq + hh
+      for (int w = blockIdx.x, wi = 0; w < n_work; w += gridDim.x, ++wi) {
+        const int n_it = dkv_work(p, w).n_it;
+        mbar_wait(&bars->kv_full, wi & 1);
         tc_fence_after();
-        PT_MARK(6)
-        const uint32_t sQ = smem_u32(smem + C::Q_OFF + st * G::TILE_BYTES);
-        const uint32_t sdO = smem_u32(smem + C::DO_OFF + st * G::TILE_BYTES);
+        const int nh = 2 * n_it;
+        // half hh: q-tile hh >> 1, columns [64 (hh & 1), +64), TMEM half-buffer hh & 1
+        auto issue_sdp = [&](int hh) {
+          const int hf = hh & 1, g = gq + (hh >> 1), st = g & 1, use = g >> 1;
+          const uint32_t sQ = smem_u32(smem + C::Q_OFF + st * G::TILE_BYTES) + hf * 64 * G::RB;
+          const uint32_t sdO = smem_u32(smem + C::DO_OFF + st * G::TILE_BYTES) + hf * 64 * G::RB;
+          if (hf == 0) {
+            mbar_wait(&bars->q_full[st], use & 1);
+            mbar_wait(&bars->do_full[st], use & 1);
+            tc_fence_after();
+          }
+          // over P^T/dS^T of half hh-2: in-order after its dV/dK MMAs, issued after pds_ready(hh-2)
 #pragma unroll
-        for (int kk = 0; kk < 64 / 16; ++kk)
-          mma_bf16_ts(tmem + C::DV_COL, tmem + C::S_COL + hf * 64 + kk * 8, mnmajor_desc<HD>(sdO, hf * 4 + kk), id_kv,
-                      (hh > 0 || kk > 0) ? 1u : 0u);
+          for (int kk = 0; kk < G::HDP / 16; ++kk)
+            mma_bf16_ss(tmem + C::S_COL + hf * 64, kmajor_desc<HD>(sK, kk), kmajor_desc<HD>(sQ, kk), id_s,
+                        kk > 0 ? 1u : 0u);
 #pragma unroll
-        for (int kk = 0; kk < 64 / 16; ++kk)
-          mma_bf16_ts(tmem + C::DK_COL, tmem + C::DP_COL + hf * 64 + kk * 8, mnmajor_desc<HD>(sQ, hf * 4 + kk), id_kv,
-                      (hh > 0 || kk > 0) ? 1u : 0u);
-        if (hf == 1) {
-          mma_commit(&bars->do_empty[st]);
-          mma_commit(&bars->q_empty[st]);
+          for (int kk = 0; kk < G::HDP / 16; ++kk)
+            mma_bf16_ss(tmem + C::DP_COL + hf * 64, kmajor_desc<HD>(sV, kk), kmajor_desc<HD>(sdO, kk), id_s,
+                        kk > 0 ? 1u : 0u);
+          mma_commit(&bars->sdp_full[hf]);
+        };
+        if (nh > 0) issue_sdp(0);
+        PT_DECL
+        for (int hh = 0; hh < nh; ++hh) {
+          const int hf = hh & 1, g = gq + (hh >> 1), st = g & 1;
+          if (hh + 1 < nh) issue_sdp(hh + 1);
+          if (hh + 1 == nh - 1) mma_commit(&bars->kv_empty);  // the item's last reads of K / V are issued
+          PT_MARK(5)
+          mbar_wait(&bars->pds_ready[hf], g & 1);
+          tc_fence_after();
+          PT_MARK(6)
+          if (hh == 0 && wi > 0) {
+            mbar_wait(&bars->acc_free, (wi - 1) & 1);
+            tc_fence_after();
+          }
+          const uint32_t sQ = smem_u32(smem + C::Q_OFF + st * G::TILE_BYTES);
+          const uint32_t sdO = smem_u32(smem + C::DO_OFF + st * G::TILE_BYTES);
+#pragma unroll
+          for (int kk = 0; kk < 64 / 16; ++kk)
+            mma_bf16_ts(tmem + C::DV_COL, tmem + C::S_COL + hf * 64 + kk * 8, mnmajor_desc<HD>(sdO, hf * 4 + kk),
+                        id_kv, (hh > 0 || kk > 0) ? 1u : 0u);
+#pragma unroll
+          for (int kk = 0; kk < 64 / 16; ++kk)
+            mma_bf16_ts(tmem + C::DK_COL, tmem + C::DP_COL + hf * 64 + kk * 8, mnmajor_desc<HD>(sQ, hf * 4 + kk),
+                        id_kv, (hh > 0 || kk > 0) ? 1u : 0u);
+          if (hf == 1) {
+            mma_commit(&bars->do_empty[st]);
+            mma_commit(&bars->q_empty[st]);
+          }
         }
+        if (nh == 0) {
+          mma_commit(&bars->kv_empty);
+          if (wi > 0) mbar_wait(&bars->acc_free, (wi - 1) & 1);
+        }
+        mma_commit(&bars->mma_done);
+        gq += n_it;
       }
-      mma_commit(&bars->mma_done);
     }
   } else {
     // warpgroup grp (warps 2..5 -> 0, 6..9 -> 1) owns TMEM half-buffer grp = q columns [64 grp, +64)
@@ -468,108 +528,116 @@ __global__ void __launch_bounds__(320, 1)
     const int grp = (warp - 2) >> 2;
     const int tr = quarter * 32 + lane;
     const int gt = (threadIdx.x - 64) & 127;  // 0..127 inside the warpgroup
-    const int key = k0 + tr;
-    const bool key_valid = tr < keys_valid;
     const float sl2 = p.scale_log2;
     const float LOG2E = 1.4426950408889634f;
     float* vgrp = vec + grp * 2 * 256;
-    float nl = 0.f, nd = 0.f;
-    int ne = -1;
-    // query row key+1 carries the PAIR_PREV bit: then it sees this key (the transposed pair cell)
-    const bool ppn = key_valid && key + 1 < se && p.plan.row_pp[key + 1] != 0;
-    auto fetch = [&](int it) {  // the group's first 64 threads load the 64 columns' vectors
-      if (gt >= 64) return;
-      const int q = sa + (list[it] & 0xFFFF) * 128 + grp * 64 + gt;
-      const bool v = q < se;
-      nl = v ? p.lse[(size_t)h * p.T + q] * LOG2E : INFINITY;
-      nd = v ? p.D[(size_t)h * p.T + q] : 0.f;
-      ne = v ? p.plan.kv_end[q] : -1;
-    };
-    if (n_it > 0) fetch(0);
     const bool tracer = gt == 0;
-    PT_DECL
-    for (int it = 0; it < n_it; ++it) {
-      PTM(tracer, 4)
-      const bool full = (list[it] >> 30) & 1;
-      const int qbase = sa + (list[it] & 0xFFFF) * 128 + grp * 64;
-      float* vb = vgrp + (it & 1) * 256;
-      if (gt < 64) {
-        vb[gt] = nl;
-        vb[64 + gt] = nd;
-        reinterpret_cast<int*>(vb)[128 + gt] = ne;
-      }
-      if (it + 1 < n_it) fetch(it + 1);
-      named_bar_sync(1 + grp, 128);
-      PTM(tracer, 0)
-      mbar_wait(&bars->sdp_full[grp], it & 1);
-      tc_fence_after();
-      PTM(tracer, 1)
-      if (it == 0 && gt == 0 && grp == 0) { TR(1, 1, gtime()); TR(1, 5, n_it); }
-      const uint32_t vs = smem_u32(vb);
-#pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        uint32_t us[32], ud[32];
-        tmem_ld32(tmem_addr(tmem, quarter, C::S_COL + grp * 64 + c * 32), us);
-        tmem_ld32(tmem_addr(tmem, quarter, C::DP_COL + grp * 64 + c * 32), ud);
-        tmem_ld_wait();
-        PTM(tracer, 2)
-        uint32_t wp[16], wd[16];
-        if (full) {
-          dkv_chunk<false>(us, ud, vs + c * 128, key, 0u, sl2, wp, wd);
-        } else {
-          // diagonal (key == q) and transposed pair (q == key + 1 with PAIR_PREV) columns of the chunk
-          const int dd = key - (qbase + c * 32);
-          uint32_t extra = 0;
-          if (key_valid && dd >= 0 && dd < 32) extra |= 1u << dd;
-          if (ppn && dd + 1 >= 0 && dd + 1 < 32) extra |= 1u << (dd + 1);
-          dkv_chunk<true>(us, ud, vs + c * 128, key, extra, sl2, wp, wd);
+    int gq = 0;
+    for (int w = blockIdx.x, wi = 0; w < n_work; w += gridDim.x, ++wi) {
+      const DkvWork t = dkv_work(p, w);
+      const int key = t.k0 + tr;
+      const bool key_valid = tr < t.keys_valid;
+      // query row key+1 carries the PAIR_PREV bit: then it sees this key (the transposed pair cell)
+      const bool ppn = key_valid && key + 1 < t.se && p.plan.row_pp[key + 1] != 0;
+      float nl = 0.f, nd = 0.f;
+      int ne = -1, nent = 0;
+      auto fetch = [&](int it) {  // the group's first 64 threads load the 64 columns' vectors
+        if (gt >= 64) return;
+        const int entry = list[t.off + it];
+        const int q = t.sa + (entry & 0xFFFF) * 128 + grp * 64 + gt;
+        const bool v = q < t.se;
+        nl = v ? p.lse[(size_t)t.h * p.T + q] * LOG2E : INFINITY;
+        nd = v ? p.D[(size_t)t.h * p.T + q] : 0.f;
+        ne = v ? p.plan.kv_end[q] : -1;
+        nent = entry;
+      };
+      if (t.n_it > 0) fetch(0);
+      PT_DECL
+      for (int it = 0; it < t.n_it; ++it) {
+        const int g = gq + it;
+        PTM(tracer, 4)
+        float* vb = vgrp + (g & 1) * 256;
+        if (gt < 64) {
+          vb[gt] = nl;
+          vb[64 + gt] = nd;
+          reinterpret_cast<int*>(vb)[128 + gt] = ne;
+          if (gt == 0) reinterpret_cast<int*>(vb)[192] = nent;
         }
-        // P^T / dS^T chunk c -> columns [16c, 16c + 16) of this half: only this thread's own,
-        // already-loaded S^T / dP^T chunk 0 is overwritten
-        tmem_st16(tmem_addr(tmem, quarter, C::S_COL + grp * 64 + c * 16), wp);
-        tmem_st16(tmem_addr(tmem, quarter, C::DP_COL + grp * 64 + c * 16), wd);
-        PTM(tracer, 3)
-      }
-      tmem_st_wait();
-      tc_fence_before();
-      mbar_arrive(&bars->pds_ready[grp]);
-    }
-    // dK, dV (thread = key row; each warpgroup writes half of the hd columns)
-    if (n_it > 0) {
-      mbar_wait(&bars->mma_done, 0);
-      tc_fence_after();
-    }
-    if (gt == 0 && grp == 0) { TR(1, 2, gtime()); }
-#pragma unroll 1
-    for (int which = 0; which < 2; ++which) {
-      void* out = which == 0 ? p.dK : p.dV;
-      const int col0 = which == 0 ? C::DK_COL : C::DV_COL;
-      const float f = which == 0 ? p.scale : 1.f;  // dS^T was accumulated without 1/sqrt(hd)
-#pragma unroll 1
-      for (int c = grp; c < G::HDP / 32; c += 2) {
-        uint32_t u[32];
-        tmem_ld32(tmem_addr(tmem, quarter, col0 + c * 32), u);
-        tmem_ld_wait();
-        if (key_valid && n_it > 0) {
-          const size_t off = (size_t)key * p.d + (size_t)h * p.hd + c * 32;
-          const int ncol = min(32, p.hd - c * 32);
-          if (p.out_f32) {
-            float* o = reinterpret_cast<float*>(out) + off;
-            for (int j = 0; j < ncol; j += 4)
-              *reinterpret_cast<float4*>(o + j) =
-                  make_float4(f * __uint_as_float(u[j]), f * __uint_as_float(u[j + 1]),
-                              f * __uint_as_float(u[j + 2]), f * __uint_as_float(u[j + 3]));
+        if (it + 1 < t.n_it) fetch(it + 1);
+        named_bar_sync(1 + grp, 128);
+        const int entry = reinterpret_cast<const int*>(vb)[192];
+        const bool full = (entry >> 30) & 1;
+        const int qbase = t.sa + (entry & 0xFFFF) * 128 + grp * 64;
+        PTM(tracer, 0)
+        mbar_wait(&bars->sdp_full[grp], g & 1);
+        tc_fence_after();
+        PTM(tracer, 1)
+        const uint32_t vs = smem_u32(vb);
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          uint32_t us[32], ud[32];
+          tmem_ld32(tmem_addr(tmem, quarter, C::S_COL + grp * 64 + c * 32), us);
+          tmem_ld32(tmem_addr(tmem, quarter, C::DP_COL + grp * 64 + c * 32), ud);
+          tmem_ld_wait();
+          PTM(tracer, 2)
+          uint32_t wp[16], wd[16];
+          if (full) {
+            dkv_chunk<false>(us, ud, vs + c * 128, key, 0u, sl2, wp, wd);
           } else {
-            __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(out) + off;
-            for (int j = 0; j < ncol; j += 8)
-              *reinterpret_cast<uint4*>(o + j) =
-                  make_uint4(pack_bf16(f * __uint_as_float(u[j]), f * __uint_as_float(u[j + 1])),
-                             pack_bf16(f * __uint_as_float(u[j + 2]), f * __uint_as_float(u[j + 3])),
-                             pack_bf16(f * __uint_as_float(u[j + 4]), f * __uint_as_float(u[j + 5])),
-                             pack_bf16(f * __uint_as_float(u[j + 6]), f * __uint_as_float(u[j + 7])));
+            // diagonal (key == q) and transposed pair (q == key + 1 with PAIR_PREV) columns of the chunk
+            const int dd = key - (qbase + c * 32);
+            uint32_t extra = 0;
+            if (key_valid && dd >= 0 && dd < 32) extra |= 1u << dd;
+            if (ppn && dd + 1 >= 0 && dd + 1 < 32) extra |= 1u << (dd + 1);
+            dkv_chunk<true>(us, ud, vs + c * 128, key, extra, sl2, wp, wd);
+          }
+          // P^T / dS^T chunk c -> columns [16c, 16c + 16) of this half: only this thread's own,
+          // already-loaded S^T / dP^T chunk 0 is overwritten
+          tmem_st16(tmem_addr(tmem, quarter, C::S_COL + grp * 64 + c * 16), wp);
+          tmem_st16(tmem_addr(tmem, quarter, C::DP_COL + grp * 64 + c * 16), wd);
+          PTM(tracer, 3)
+        }
+        tmem_st_wait();
+        tc_fence_before();
+        mbar_arrive(&bars->pds_ready[grp]);
+      }
+      // dK, dV (thread = key row; each warpgroup writes half of the hd columns)
+      mbar_wait(&bars->mma_done, wi & 1);
+      tc_fence_after();
+#pragma unroll 1
+      for (int which = 0; which < 2; ++which) {
+        void* out = which == 0 ? p.dK : p.dV;
+        const int col0 = which == 0 ? C::DK_COL : C::DV_COL;
+        const float f = t.n_it == 0 ? 0.f : (which == 0 ? p.scale : 1.f);  // dS^T was accumulated without 1/sqrt(hd)
+#pragma unroll 1
+        for (int c = grp; c < G::HDP / 32; c += 2) {
+          uint32_t u[32];
+          tmem_ld32(tmem_addr(tmem, quarter, col0 + c * 32), u);
+          tmem_ld_wait();
+          if (key_valid) {
+            const size_t off = (size_t)key * p.d + (size_t)t.h * p.hd + c * 32;
+            const int ncol = min(32, p.hd - c * 32);
+            if (p.out_f32) {
+              float* o = reinterpret_cast<float*>(out) + off;
+              for (int j = 0; j < ncol; j += 4)
+                *reinterpret_cast<float4*>(o + j) =
+                    make_float4(f * __uint_as_float(u[j]), f * __uint_as_float(u[j + 1]),
+                                f * __uint_as_float(u[j + 2]), f * __uint_as_float(u[j + 3]));
+            } else {
+              __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(out) + off;
+              for (int j = 0; j < ncol; j += 8)
+                *reinterpret_cast<uint4*>(o + j) =
+                    make_uint4(pack_bf16(f * __uint_as_float(u[j]), f * __uint_as_float(u[j + 1])),
+                               pack_bf16(f * __uint_as_float(u[j + 2]), f * __uint_as_float(u[j + 3])),
+                               pack_bf16(f * __uint_as_float(u[j + 4]), f * __uint_as_float(u[j + 5])),
+                               pack_bf16(f * __uint_as_float(u[j + 6]), f * __uint_as_float(u[j + 7])));
+            }
           }
         }
       }
+      tc_fence_before();
+      mbar_arrive(&bars->acc_free);
+      gq += t.n_it;
     }
   }
   tc_fence_before();
@@ -600,6 +668,17 @@ __global__ void __launch_bounds__(256) attn_bwd_pre_kernel(const __nv_bfloat16* 
 
 bool make_head_map(CUtensorMap* m, const void* ptr, int T, int H, int hd);
 
+static int num_sms_attn() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
 template <int HD>
 static cudaError_t bwd_hd(const CUtensorMap& mQ, const CUtensorMap& mK, const CUtensorMap& mV, const CUtensorMap& mdO,
                           const AttnParams& p, cudaStream_t st) {
@@ -613,11 +692,12 @@ static cudaError_t bwd_hd(const CUtensorMap& mQ, const CUtensorMap& mK, const CU
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  const int grid = p.plan.nq_cap * p.H;
+  // persistent: one CTA per SM (smem-limited), never more CTAs than work items
+  const int grid = std::min(p.plan.nq_cap * p.H, num_sms_attn());
   if (grid == 0) return cudaSuccess;
   {
     ProfScope ps(PROF_ATTN_BWD, st, 2);
-    attn_bwd_dq_kernel<HD><<<grid, 192, DqCfg<HD>::SMEM, st>>>(mQ, mK, mV, mdO, p);
+    attn_bwd_dq_kernel<HD><<<grid, DqCfg<HD>::THREADS, DqCfg<HD>::SMEM, st>>>(mQ, mK, mV, mdO, p);
     attn_bwd_dkv_kernel<HD><<<grid, DkvCfg<HD>::THREADS, DkvCfg<HD>::SMEM, st>>>(mQ, mK, mV, mdO, p);
   }
   return cudaGetLastError();

@@ -17,6 +17,8 @@ static inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 static int32_t nq_cap_of(int32_t n, int32_t T) { return (T + TILE - 1) / TILE + n; }
 static int32_t hmax_of(int32_t max_seqlen) { return (max_seqlen + TILE - 1) / TILE + 3; }
+// sum_s nq_s (nq_s + 1) / 2 with sum_s nq_s <= nq_cap and nq_s <= hmax
+static size_t list_cap_of(size_t nq, size_t hm) { return nq * (hm + 1) / 2 + hm; }
 
 size_t plan_bytes(int32_t n, int32_t T, int32_t max_seqlen) {
   const size_t nq = nq_cap_of(n, T), hm = hmax_of(max_seqlen);
@@ -31,6 +33,9 @@ size_t plan_bytes(int32_t n, int32_t T, int32_t max_seqlen) {
   b += align256(nq * sizeof(QTileInfo));
   b += align256(nq * 4) * 2;
   b += align256(hm * 2 * 4);
+  b += align256((size_t)(n + 1) * 4);
+  b += align256(nq * 4) * 2;
+  b += align256(list_cap_of(nq, hm) * 4);
   return b;
 }
 
@@ -38,6 +43,7 @@ PlanView plan_carve(void* ws, int32_t n, int32_t T, int32_t max_seqlen) {
   PlanView v;
   v.nq_cap = nq_cap_of(n, T);
   v.hmax = hmax_of(max_seqlen);
+  v.list_cap = (int32_t)list_cap_of(v.nq_cap, v.hmax);
   uint8_t* p = reinterpret_cast<uint8_t*>(ws);
   auto take = [&](size_t bytes) {
     uint8_t* r = p;
@@ -56,6 +62,10 @@ PlanView plan_carve(void* ws, int32_t n, int32_t T, int32_t max_seqlen) {
   v.fwd_order = reinterpret_cast<int32_t*>(take((size_t)v.nq_cap * 4));
   v.bwd_order = reinterpret_cast<int32_t*>(take((size_t)v.nq_cap * 4));
   v.hist = reinterpret_cast<int32_t*>(take((size_t)v.hmax * 2 * 4));
+  v.tri_off = reinterpret_cast<int32_t*>(take((size_t)(n + 1) * 4));
+  v.bwd_off = reinterpret_cast<int32_t*>(take((size_t)v.nq_cap * 4));
+  v.bwd_cnt = reinterpret_cast<int32_t*>(take((size_t)v.nq_cap * 4));
+  v.bwd_list = reinterpret_cast<int32_t*>(take(list_cap_of(v.nq_cap, v.hmax) * 4));
   return v;
 }
 
@@ -95,7 +105,7 @@ __global__ void __launch_bounds__(1024) plan_seq_kernel(PlanArgs a, PlanView v) 
     if (a.n > 0 && a.cu[0] != 0) err |= ERRBIT_OFFSETS;
     if (a.n > 0 && a.cu[a.n] > a.T) err |= ERRBIT_OFFSETS;
   }
-  long long nq_sum = 0, tc_sum = 0;
+  long long nq_sum = 0, tc_sum = 0, tri_sum = 0;
   for (int s = s0; s < s1; ++s) {
     const int ra = a.cu[s], re = a.cu[s + 1];
     if (re <= ra) err |= ERRBIT_OFFSETS;
@@ -105,17 +115,21 @@ __global__ void __launch_bounds__(1024) plan_seq_kernel(PlanArgs a, PlanView v) 
     const long long nq = (min(len, a.max_seqlen) + TILE - 1) / TILE;
     nq_sum += nq;
     tc_sum += nq * nq;
+    tri_sum += nq * (nq + 1) / 2;
   }
-  long long tot_nq, tot_tc;
+  long long tot_nq, tot_tc, tot_tri;
   long long pre_nq = block_exclusive_scan<long long>(nq_sum, sh, tot_nq);
   long long pre_tc = block_exclusive_scan<long long>(tc_sum, sh, tot_tc);
+  long long pre_tri = block_exclusive_scan<long long>(tri_sum, sh, tot_tri);
   for (int s = s0; s < s1; ++s) {
     v.tile_off[s] = (int32_t)pre_nq;
     v.tc_off[s] = pre_tc;
+    v.tri_off[s] = (int32_t)pre_tri;
     const int len = min(seq_len_safe(a.cu, s, a.T), a.max_seqlen);
     const long long nq = (len + TILE - 1) / TILE;
     pre_nq += nq;
     pre_tc += nq * nq;
+    pre_tri += nq * (nq + 1) / 2;
   }
   if (tid == 0) {
     v.tile_off[a.n] = (int32_t)min(tot_nq, (long long)v.nq_cap);
@@ -289,6 +303,22 @@ __global__ void __launch_bounds__(128) plan_scatter_kernel(PlanArgs a, PlanView 
   const int cost_b = min(nq_s - info.qt, v.hmax - 1);
   v.fwd_order[atomicAdd(&v.hist[cost_f], 1)] = g;
   v.bwd_order[atomicAdd(&v.hist[v.hmax + cost_b], 1)] = g;
+  // visit list of g as a k-tile (transpose of the forward visit rule): q-tiles qt >= kt of the
+  // sequence with kt < nf(qt) or kt2(qt) <= kt <= qt; slots [base, base + nq_s - kt) of the
+  // sequence's triangle
+  const int kt = info.qt, tile0 = g - kt;
+  const int base = v.tri_off[info.seq] + kt * nq_s - kt * (kt - 1) / 2;
+  int n = 0;
+  for (int qt = kt; qt < nq_s && tile0 + qt < nq_total; ++qt) {
+    const QTileInfo qi = v.qinfo[tile0 + qt];
+    if (kt < qi.nf || (kt >= qi.kt2 && kt <= qi.qt)) {
+      const bool full = qi.rows == TILE && qi.emin >= (kt + 1) * TILE;
+      if (base + n < v.list_cap) v.bwd_list[base + n] = qt | (full ? (1 << 30) : 0);  // (invalid offsets latch E_OFFSETS)
+      ++n;
+    }
+  }
+  v.bwd_off[g] = base;
+  v.bwd_cnt[g] = base + n <= v.list_cap ? n : 0;
 }
 
 cudaError_t plan_launch(const PlanArgs& a, const PlanView& v, cudaStream_t st) {

@@ -38,29 +38,11 @@ a = np.frombuffer(buf, dtype=np.uint64).reshape(8192, 2, 6).astype(np.float64)
 for k, name in enumerate(["dq", "dkv"]):
     t = a[:, k, :]
     t = t[t[:, 0] > 0]
-    t0 = t[:, 0].min()
-    ent, first, done, ext, sm, n = [t[:, i] for i in range(6)]
-    span = ext.max() - t0
-    print(f"== {name}: CTAs {len(t)}  span {span / 1e3:.1f} us  mean n {n.mean():.2f}")
-    print(f"  setup (entry->first MMA result) mean {np.mean(first - ent) / 1e3:.2f} us")
-    print(f"  loop  (first->all MMAs done)    mean {np.mean(done - first) / 1e3:.2f} us "
-          f" per item {np.sum(done - first) / max(n.sum(), 1) / 1e3:.3f} us")
-    print(f"  epilogue (done->exit)           mean {np.mean(ext - done) / 1e3:.2f} us")
-    busy = np.zeros(148)
-    gaps = []
-    for s in range(148):
-        m = sm == s
-        if not m.any():
-            continue
-        e, x = ent[m], ext[m]
-        o = np.argsort(e)
-        e, x = e[o], x[o]
-        busy[s] = np.sum(x - e)
-        gaps += list(e[1:] - x[:-1])
-    print(f"  SM busy frac mean {busy.mean() / span:.3f}  min {busy.min() / span:.3f}  "
-          f"inter-CTA gap mean {np.mean(gaps) / 1e3:.2f} us  CTAs/SM {len(t) / 148:.1f}")
-    last = np.sort(ext - t0)[-148:]
-    print(f"  tail: last-SM-finish spread {(last[-1] - last[0]) / 1e3:.1f} us")
+    ent, ext = t[:, 0], t[:, 3]
+    span = ext.max() - ent.min()
+    print(f"== {name}: CTAs {len(t)}  span {span / 1e3:.1f} us  CTA time mean {np.mean(ext - ent) / 1e3:.1f} "
+          f"min {np.min(ext - ent) / 1e3:.1f} max {np.max(ext - ent) / 1e3:.1f} us  "
+          f"start spread {(ent.max() - ent.min()) / 1e3:.1f} us")
 buf2 = (C.c_ulonglong * (8192 * 8))()
 L.cadet_debug_phase_reset()
 st.step(inp)
@@ -68,7 +50,7 @@ torch.cuda.synchronize()
 L.cadet_debug_phase_read(buf2, 8192 * 8)
 ph = np.frombuffer(buf2, dtype=np.uint64).reshape(8192, 8).astype(np.float64)
 used = ph[ph.sum(1) > 0]
-items = a[:, 1, 5][a[:, 1, 0] > 0].sum()
+items = 4840  # C4 dkv work items (k-tiles x heads)
 names = ["cmp: vec st+bar", "cmp: sdp wait", "cmp: tmem ld", "cmp: math+st", "cmp: st_wait+arrive+loop",
          "mma: issue sdp", "mma: pds wait", "mma: dVdK issue"]
 for i, nm in enumerate(names):
