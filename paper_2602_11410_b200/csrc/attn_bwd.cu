@@ -69,7 +69,8 @@ struct DqCfg {
   static constexpr int DO_OFF = Q_OFF + G::TILE_BYTES;
   static constexpr int K_OFF = DO_OFF + G::TILE_BYTES;        // two stages
   static constexpr int V_OFF = K_OFF + 2 * G::TILE_BYTES;     // two stages
-  static constexpr int BAR_OFF = V_OFF + 2 * G::TILE_BYTES;
+  static constexpr int STG_OFF = V_OFF + 2 * G::TILE_BYTES;   // [8 compute warps][4 KB] store transpose
+  static constexpr int BAR_OFF = STG_OFF + 8 * 4096;
   static constexpr int SMEM = BAR_OFF + 256 + 1024;
   static constexpr int S_COL = 0, DP_COL = 256, DQ_COL = 384;  // S double-buffered
   static constexpr int THREADS = 320;  // producer, MMA, 2 compute warpgroups (64 S/dP columns each)
@@ -230,8 +231,10 @@ __global__ void __launch_bounds__(320, 1)
     const int rt = quarter * 32 + lane;
     const float sl2 = p.scale_log2;
     int gs = 0;
+    // items decoded one ahead: the row loads below depend on no global-load chain
+    DqWork t = dq_work(p, blockIdx.x < n_work ? blockIdx.x : 0);
+    DqWork tn = dq_work(p, blockIdx.x + gridDim.x < n_work ? blockIdx.x + gridDim.x : 0);
     for (int w = blockIdx.x, wi = 0; w < n_work; w += gridDim.x, ++wi) {
-      const DqWork t = dq_work(p, w);
       const int r = t.q0 + rt;
       const bool valid = rt < t.rows_valid;
       const int e_r = valid ? p.plan.kv_end[r] : 0;
@@ -276,24 +279,21 @@ __global__ void __launch_bounds__(320, 1)
       }
       mbar_wait(&bars->dq_done, wi & 1);
       tc_fence_after();
+      const uint32_t stg = smem_u32(smem + C::STG_OFF + (warp - 2) * 4096);
 #pragma unroll 1
       for (int c = grp; c < G::HDP / 32; c += 2) {
         uint32_t u[32];
         tmem_ld32(tmem_addr(tmem, quarter, C::DQ_COL + c * 32), u);
         tmem_ld_wait();
-        if (valid) {
-          const float f = t.n_kv > 0 ? p.scale : 0.f;
-          const int ncol = min(32, p.hd - c * 32);
-          float* o = p.dQ + (size_t)r * p.d + (size_t)t.h * p.hd + c * 32;
-          for (int q = 0; q < ncol; q += 4)
-            *reinterpret_cast<float4*>(o + q) =
-                make_float4(f * __uint_as_float(u[q]), f * __uint_as_float(u[q + 1]), f * __uint_as_float(u[q + 2]),
-                            f * __uint_as_float(u[q + 3]));
-        }
+        const float f = t.n_kv > 0 ? p.scale : 0.f;
+        warp_store_rows_f32(stg, u, f, p.dQ + (size_t)(t.q0 + quarter * 32) * p.d + (size_t)t.h * p.hd + c * 32,
+                            p.d, t.rows_valid - (int)quarter * 32, min(32, p.hd - c * 32));
       }
       tc_fence_before();
       mbar_arrive(&bars->dq_free);
       gs += t.n_kv;
+      t = tn;
+      if (w + 2 * gridDim.x < n_work) tn = dq_work(p, w + 2 * gridDim.x);
     }
   }
   tc_fence_before();
@@ -354,7 +354,8 @@ struct DkvCfg {
   static constexpr int Q_OFF = V_OFF + G::TILE_BYTES;          // two stages
   static constexpr int DO_OFF = Q_OFF + 2 * G::TILE_BYTES;     // two stages
   static constexpr int VEC_OFF = DO_OFF + 2 * G::TILE_BYTES;   // [2 groups][2 bufs][256] x 4 B
-  static constexpr int BAR_OFF = VEC_OFF + 2 * 2 * 256 * 4;
+  static constexpr int STG_OFF = VEC_OFF + 2 * 2 * 256 * 4;    // [8 compute warps][2 KB] store transpose
+  static constexpr int BAR_OFF = STG_OFF + 8 * 2048;
   static constexpr int SMEM = BAR_OFF + 256 + 1024;
   // S^T/P^T half-buffers at [0,64) and [64,128); dP^T/dS^T at [128,192) and [192,256)
   static constexpr int S_COL = 0, DP_COL = 128, DV_COL = 256, DK_COL = 384;
@@ -459,10 +460,13 @@ __global__ void __launch_bounds__(320, 1)
       const uint32_t id_kv = idesc_bf16(128, G::HDP, 0, 1);
       const uint32_t sK = smem_u32(smem + C::K_OFF), sV = smem_u32(smem + C::V_OFF);
       int gq = 0;  // global q-tile counter; global half index 2 gq + hh
+      PT_DECL
       for (int w = blockIdx.x, wi = 0; w < n_work; w += gridDim.x, ++wi) {
         const int n_it = dkv_work(p, w).n_it;
+        PT_MARK(3)
         mbar_wait(&bars->kv_full, wi & 1);
         tc_fence_after();
+        PT_MARK(0)
         const int nh = 2 * n_it;
         // half hh: q-tile hh >> 1, columns [64 (hh & 1), +64), TMEM half-buffer hh & 1
         auto issue_sdp = [&](int hh) {
@@ -486,19 +490,19 @@ __global__ void __launch_bounds__(320, 1)
           mma_commit(&bars->sdp_full[hf]);
         };
         if (nh > 0) issue_sdp(0);
-        PT_DECL
         for (int hh = 0; hh < nh; ++hh) {
           const int hf = hh & 1, g = gq + (hh >> 1), st = g & 1;
           if (hh + 1 < nh) issue_sdp(hh + 1);
           if (hh + 1 == nh - 1) mma_commit(&bars->kv_empty);  // the item's last reads of K / V are issued
-          PT_MARK(5)
+          PT_MARK(3)
           mbar_wait(&bars->pds_ready[hf], g & 1);
           tc_fence_after();
-          PT_MARK(6)
+          PT_MARK(2)
           if (hh == 0 && wi > 0) {
             mbar_wait(&bars->acc_free, (wi - 1) & 1);
             tc_fence_after();
           }
+          PT_MARK(1)
           const uint32_t sQ = smem_u32(smem + C::Q_OFF + st * G::TILE_BYTES);
           const uint32_t sdO = smem_u32(smem + C::DO_OFF + st * G::TILE_BYTES);
 #pragma unroll
@@ -532,30 +536,34 @@ __global__ void __launch_bounds__(320, 1)
     const float LOG2E = 1.4426950408889634f;
     float* vgrp = vec + grp * 2 * 256;
     const bool tracer = gt == 0;
+    float nl = 0.f, nd = 0.f;
+    int ne = -1, nent = 0;
+    // the group's first 64 threads load the 64 columns' vectors of iteration it of item u
+    auto fetch = [&](const DkvWork& u, int it) {
+      if (gt >= 64) return;
+      const int entry = list[u.off + it];
+      const int q = u.sa + (entry & 0xFFFF) * 128 + grp * 64 + gt;
+      const bool v = q < u.se;
+      nl = v ? p.lse[(size_t)u.h * p.T + q] * LOG2E : INFINITY;
+      nd = v ? p.D[(size_t)u.h * p.T + q] : 0.f;
+      ne = v ? p.plan.kv_end[q] : -1;
+      nent = entry;
+    };
+    // items are decoded one ahead and the first iteration's vectors fetched during the previous
+    // item, so no dependent global-load chain sits at an item boundary
+    DkvWork t = dkv_work(p, blockIdx.x < n_work ? blockIdx.x : 0);
+    DkvWork tn = dkv_work(p, blockIdx.x + gridDim.x < n_work ? blockIdx.x + gridDim.x : 0);
+    if (blockIdx.x < n_work && t.n_it > 0) fetch(t, 0);
     int gq = 0;
+    PT_DECL
     for (int w = blockIdx.x, wi = 0; w < n_work; w += gridDim.x, ++wi) {
-      const DkvWork t = dkv_work(p, w);
+      const bool has_next = w + gridDim.x < n_work;
       const int key = t.k0 + tr;
       const bool key_valid = tr < t.keys_valid;
       // query row key+1 carries the PAIR_PREV bit: then it sees this key (the transposed pair cell)
       const bool ppn = key_valid && key + 1 < t.se && p.plan.row_pp[key + 1] != 0;
-      float nl = 0.f, nd = 0.f;
-      int ne = -1, nent = 0;
-      auto fetch = [&](int it) {  // the group's first 64 threads load the 64 columns' vectors
-        if (gt >= 64) return;
-        const int entry = list[t.off + it];
-        const int q = t.sa + (entry & 0xFFFF) * 128 + grp * 64 + gt;
-        const bool v = q < t.se;
-        nl = v ? p.lse[(size_t)t.h * p.T + q] * LOG2E : INFINITY;
-        nd = v ? p.D[(size_t)t.h * p.T + q] : 0.f;
-        ne = v ? p.plan.kv_end[q] : -1;
-        nent = entry;
-      };
-      if (t.n_it > 0) fetch(0);
-      PT_DECL
       for (int it = 0; it < t.n_it; ++it) {
         const int g = gq + it;
-        PTM(tracer, 4)
         float* vb = vgrp + (g & 1) * 256;
         if (gt < 64) {
           vb[gt] = nl;
@@ -563,15 +571,18 @@ __global__ void __launch_bounds__(320, 1)
           reinterpret_cast<int*>(vb)[128 + gt] = ne;
           if (gt == 0) reinterpret_cast<int*>(vb)[192] = nent;
         }
-        if (it + 1 < t.n_it) fetch(it + 1);
+        if (it + 1 < t.n_it)
+          fetch(t, it + 1);
+        else if (has_next && tn.n_it > 0)
+          fetch(tn, 0);
         named_bar_sync(1 + grp, 128);
         const int entry = reinterpret_cast<const int*>(vb)[192];
         const bool full = (entry >> 30) & 1;
         const int qbase = t.sa + (entry & 0xFFFF) * 128 + grp * 64;
-        PTM(tracer, 0)
+        PTM(tracer, 7)
         mbar_wait(&bars->sdp_full[grp], g & 1);
         tc_fence_after();
-        PTM(tracer, 1)
+        PTM(tracer, 6)
         const uint32_t vs = smem_u32(vb);
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
@@ -579,7 +590,6 @@ __global__ void __launch_bounds__(320, 1)
           tmem_ld32(tmem_addr(tmem, quarter, C::S_COL + grp * 64 + c * 32), us);
           tmem_ld32(tmem_addr(tmem, quarter, C::DP_COL + grp * 64 + c * 32), ud);
           tmem_ld_wait();
-          PTM(tracer, 2)
           uint32_t wp[16], wd[16];
           if (full) {
             dkv_chunk<false>(us, ud, vs + c * 128, key, 0u, sl2, wp, wd);
@@ -595,15 +605,16 @@ __global__ void __launch_bounds__(320, 1)
           // already-loaded S^T / dP^T chunk 0 is overwritten
           tmem_st16(tmem_addr(tmem, quarter, C::S_COL + grp * 64 + c * 16), wp);
           tmem_st16(tmem_addr(tmem, quarter, C::DP_COL + grp * 64 + c * 16), wd);
-          PTM(tracer, 3)
         }
         tmem_st_wait();
         tc_fence_before();
         mbar_arrive(&bars->pds_ready[grp]);
       }
       // dK, dV (thread = key row; each warpgroup writes half of the hd columns)
+      PTM(tracer, 7)
       mbar_wait(&bars->mma_done, wi & 1);
       tc_fence_after();
+      PTM(tracer, 4)
 #pragma unroll 1
       for (int which = 0; which < 2; ++which) {
         void* out = which == 0 ? p.dK : p.dV;
@@ -614,30 +625,31 @@ __global__ void __launch_bounds__(320, 1)
           uint32_t u[32];
           tmem_ld32(tmem_addr(tmem, quarter, col0 + c * 32), u);
           tmem_ld_wait();
-          if (key_valid) {
-            const size_t off = (size_t)key * p.d + (size_t)t.h * p.hd + c * 32;
-            const int ncol = min(32, p.hd - c * 32);
-            if (p.out_f32) {
-              float* o = reinterpret_cast<float*>(out) + off;
-              for (int j = 0; j < ncol; j += 4)
-                *reinterpret_cast<float4*>(o + j) =
-                    make_float4(f * __uint_as_float(u[j]), f * __uint_as_float(u[j + 1]),
-                                f * __uint_as_float(u[j + 2]), f * __uint_as_float(u[j + 3]));
-            } else {
-              __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(out) + off;
-              for (int j = 0; j < ncol; j += 8)
-                *reinterpret_cast<uint4*>(o + j) =
-                    make_uint4(pack_bf16(f * __uint_as_float(u[j]), f * __uint_as_float(u[j + 1])),
-                               pack_bf16(f * __uint_as_float(u[j + 2]), f * __uint_as_float(u[j + 3])),
-                               pack_bf16(f * __uint_as_float(u[j + 4]), f * __uint_as_float(u[j + 5])),
-                               pack_bf16(f * __uint_as_float(u[j + 6]), f * __uint_as_float(u[j + 7])));
-            }
+          const int ncol = min(32, p.hd - c * 32);
+          if (!p.out_f32) {
+            uint32_t wv[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) wv[j] = pack_bf16(f * __uint_as_float(u[2 * j]), f * __uint_as_float(u[2 * j + 1]));
+            warp_store_rows_bf16(smem_u32(smem + C::STG_OFF + (warp - 2) * 2048), wv,
+                                 reinterpret_cast<__nv_bfloat16*>(out) + (size_t)(t.k0 + quarter * 32) * p.d +
+                                     (size_t)t.h * p.hd + c * 32,
+                                 p.d, t.keys_valid - (int)quarter * 32, ncol);
+          } else if (key_valid) {  // fp32 outputs (exactness mode): direct row stores
+            float* o = reinterpret_cast<float*>(out) + (size_t)key * p.d + (size_t)t.h * p.hd + c * 32;
+            for (int j = 0; j < ncol; j += 4)
+              *reinterpret_cast<float4*>(o + j) = make_float4(f * __uint_as_float(u[j]), f * __uint_as_float(u[j + 1]),
+                                                              f * __uint_as_float(u[j + 2]), f * __uint_as_float(u[j + 3]));
           }
         }
       }
       tc_fence_before();
       mbar_arrive(&bars->acc_free);
+      PTM(tracer, 5)
       gq += t.n_it;
+      if (has_next && t.n_it == 0 && tn.n_it > 0) fetch(tn, 0);
+      t = tn;
+      const int w2 = w + 2 * gridDim.x;
+      if (w2 < n_work) tn = dkv_work(p, w2);
     }
   }
   tc_fence_before();

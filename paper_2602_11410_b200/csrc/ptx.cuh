@@ -275,6 +275,54 @@ CADET_DEV int4 lds_i4(uint32_t saddr) {
   asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(saddr));
   return v;
 }
+CADET_DEV void sts_u4(uint32_t saddr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(saddr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
+}
+CADET_DEV uint4 lds_u4(uint32_t saddr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(saddr) : "memory");
+  return v;
+}
+
+// Row-per-lane results (lane = row of a 32-row block, as tcgen05.ld 32x32b delivers them) written
+// to global memory through a per-warp shared-memory transpose, so that each store instruction
+// covers whole row segments instead of 32 different lines.  XOR-swizzled 16-byte slots keep both
+// shared-memory phases conflict-free.
+// bf16: w = this lane's 32 columns packed (16 words); stage = 2 KB; g0 = &row0[col0], ld = row stride.
+CADET_DEV void warp_store_rows_bf16(uint32_t stage, const uint32_t (&w)[16], __nv_bfloat16* g0, size_t ld,
+                                    int rows_valid, int ncol) {
+  const uint32_t lane = threadIdx.x & 31;
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+    sts_u4(stage + lane * 64 + ((j ^ ((lane >> 1) & 3)) << 4), w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
+  __syncwarp();
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int row = i * 8 + (lane >> 2), j = lane & 3;
+    const uint4 v = lds_u4(stage + row * 64 + ((j ^ ((row >> 1) & 3)) << 4));
+    if (row < rows_valid && j * 8 < ncol) *reinterpret_cast<uint4*>(g0 + (size_t)row * ld + j * 8) = v;
+  }
+  __syncwarp();
+}
+// fp32: u = this lane's 32 columns (scaled by f); stage = 4 KB.
+CADET_DEV void warp_store_rows_f32(uint32_t stage, const uint32_t (&u)[32], float f, float* g0, size_t ld,
+                                   int rows_valid, int ncol) {
+  const uint32_t lane = threadIdx.x & 31;
+#pragma unroll
+  for (int j = 0; j < 8; ++j)
+    sts_u4(stage + lane * 128 + ((j ^ (lane & 7)) << 4), __float_as_uint(f * __uint_as_float(u[4 * j])),
+           __float_as_uint(f * __uint_as_float(u[4 * j + 1])), __float_as_uint(f * __uint_as_float(u[4 * j + 2])),
+           __float_as_uint(f * __uint_as_float(u[4 * j + 3])));
+  __syncwarp();
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int row = i * 4 + (lane >> 3), j = lane & 7;
+    const uint4 v = lds_u4(stage + row * 128 + ((j ^ (row & 7)) << 4));
+    if (row < rows_valid && j * 4 < ncol) *reinterpret_cast<uint4*>(g0 + (size_t)row * ld + j * 4) = v;
+  }
+  __syncwarp();
+}
+
 CADET_DEV float fast_exp2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
