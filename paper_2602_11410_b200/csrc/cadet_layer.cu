@@ -119,6 +119,7 @@ struct LayerBufs {  // carved from `saved`
 };
 struct LayerWs {    // carved from `ws` after the plan
   double* theta;
+  float* rope_cs;   // [T][hd + 32] (cos, sin) table
   float* D;
   void *dO, *dKr, *dV, *uq, *uk, *dQ, *dK, *ux;
   float *dQacc, *rq, *rk, *rx;
@@ -141,7 +142,8 @@ size_t saved_bytes(const cadet_attn_config* c, int T) {
 }
 size_t layer_ws_bytes(const cadet_attn_config* c, int n, int T) {
   const int d = c->d_model;
-  return plan_bytes(n, T, T) + a256(8 * 64) + a256((size_t)4 * c->n_heads * T) + 8 * bf_sz(T, d) + 4 * f_sz(T, d);
+  return plan_bytes(n, T, T) + a256(8 * 64) + a256((size_t)4 * T * (c->head_dim + 32)) +
+         a256((size_t)4 * c->n_heads * T) + 8 * bf_sz(T, d) + 4 * f_sz(T, d);
 }
 LayerWs carve_ws(void* ws, const cadet_attn_config* c, int n, int T) {
   const int d = c->d_model;
@@ -149,6 +151,8 @@ LayerWs carve_ws(void* ws, const cadet_attn_config* c, int n, int T) {
   LayerWs W;
   W.theta = reinterpret_cast<double*>(p);
   p += a256(8 * 64);
+  W.rope_cs = reinterpret_cast<float*>(p);
+  p += a256((size_t)4 * T * (c->head_dim + 32));
   W.D = reinterpret_cast<float*>(p);
   p += a256((size_t)4 * c->n_heads * T);
   void** bf[8] = {&W.dO, &W.dKr, &W.dV, &W.uq, &W.uk, &W.dQ, &W.dK, &W.ux};
@@ -210,14 +214,6 @@ GemmProblem wgrad(const void* A, const void* G, float* dW, int T, int din, int d
   return g;
 }
 
-struct RopeCtx {
-  const int64_t* t;
-  const int32_t* row_seq;
-  const int32_t* cu;
-  const double* theta;
-  int hd;
-};
-
 }  // namespace
 
 extern "C" {
@@ -252,6 +248,8 @@ cadet_status cadet_attn_forward(const cadet_attn_config* cfg, const cadet_batch*
   LayerBufs L = carve_saved(saved, cfg, T);
   LayerWs W = carve_ws(ws, cfg, n, T);
   cudaError_t e = rope_theta_launch(W.theta, hd, cfg->rope_phi_min, cfg->rope_base, (double)cfg->rope_delta_t_max_ms, st);
+  if (e == cudaSuccess && cfg->use_rope)
+    e = rope_table_launch(W.rope_cs, T, hd, W.theta, b->timestamps_ms, v.row_seq, b->cu_seqlens, st);
   const int bn = pick_bn(T, d);
   // A2: representation gate  Xt = X * sigma(X W_xg)   (Eq. 4)
   const void* Xt = X;
@@ -288,16 +286,12 @@ cadet_status cadet_attn_forward(const cadet_attn_config* cfg, const cadet_batch*
         g[i].epi.src = src[i];
         g[i].epi.aux = aux[i];
         g[i].epi.hd = hd;
-        g[i].epi.t_ms = b->timestamps_ms;
-        g[i].epi.row_seq = v.row_seq;
-        g[i].epi.cu = b->cu_seqlens;
-        g[i].epi.theta = W.theta;
+        g[i].epi.rope_cs = W.rope_cs;
       }
       e = gemm_launch(g, 2, bn, st);
     } else if (cfg->use_rope) {
-      e = rope_apply_launch(L.Q, L.Qr, T, d, hd, W.theta, b->timestamps_ms, v.row_seq, b->cu_seqlens, st);
-      if (e == cudaSuccess)
-        e = rope_apply_launch(L.K, L.Kr, T, d, hd, W.theta, b->timestamps_ms, v.row_seq, b->cu_seqlens, st);
+      e = rope_apply_launch(L.Q, L.Qr, T, d, hd, W.rope_cs, st);
+      if (e == cudaSuccess) e = rope_apply_launch(L.K, L.Kr, T, d, hd, W.rope_cs, st);
     } else {
       e = cudaMemcpyAsync(L.Qr, L.Q, (size_t)T * d * 2, cudaMemcpyDeviceToDevice, st);
       if (e == cudaSuccess) e = cudaMemcpyAsync(L.Kr, L.K, (size_t)T * d * 2, cudaMemcpyDeviceToDevice, st);
@@ -352,6 +346,9 @@ cadet_status cadet_attn_backward(const cadet_attn_config* cfg, const cadet_batch
   const int bnw = pick_bn_wgrad(d);
   const size_t wbytes = (size_t)d * d * 4;
   cudaError_t e = rope_theta_launch(W.theta, hd, cfg->rope_phi_min, cfg->rope_base, (double)cfg->rope_delta_t_max_ms, st);
+  if (e == cudaSuccess && cfg->use_rope)
+    e = rope_table_launch(W.rope_cs, T, hd, W.theta, b->timestamps_ms, v.row_seq, b->cu_seqlens, st);
+  const float* cs = cfg->use_rope ? W.rope_cs : nullptr;
   float* gws[7] = {gr->dW_xg, gr->dW_q, gr->dW_k, gr->dW_v, gr->dW_qg, gr->dW_kg, gr->dW_o};
   for (int i = 0; i < 7 && e == cudaSuccess; ++i)
     if (gws[i]) e = cudaMemsetAsync(gws[i], 0, wbytes, st);
@@ -388,11 +385,9 @@ cadet_status cadet_attn_backward(const cadet_attn_config* cfg, const cadet_batch
   const void* dK = W.dK;
   if (e == cudaSuccess) {
     if (cfg->use_int_gate) {
-      e = rope_gate_bwd_launch(W.dQacc, 1, L.Q, L.Zq, W.uq, W.rq, 1, T, d, hd, cfg->use_rope, W.theta,
-                               b->timestamps_ms, v.row_seq, b->cu_seqlens, st);
+      e = rope_gate_bwd_launch(W.dQacc, 1, L.Q, L.Zq, W.uq, W.rq, 1, T, d, hd, cs, st);
       if (e == cudaSuccess)
-        e = rope_gate_bwd_launch(W.dKr, 0, L.K, L.Zk, W.uk, W.rk, 1, T, d, hd, cfg->use_rope, W.theta,
-                                 b->timestamps_ms, v.row_seq, b->cu_seqlens, st);
+        e = rope_gate_bwd_launch(W.dKr, 0, L.K, L.Zk, W.uk, W.rk, 1, T, d, hd, cs, st);
       if (e == cudaSuccess) {  // dQ = rq + uq W_qg^T ; dK = rk + uk W_kg^T
         GemmProblem g[2];
         const void* us[2] = {W.uq, W.uk};
@@ -412,11 +407,9 @@ cadet_status cadet_attn_backward(const cadet_attn_config* cfg, const cadet_batch
         e = gemm_launch(g, 2, bnw, st);
       }
     } else {
-      e = rope_gate_bwd_launch(W.dQacc, 1, nullptr, nullptr, nullptr, W.dQ, 1, T, d, hd, cfg->use_rope, W.theta,
-                               b->timestamps_ms, v.row_seq, b->cu_seqlens, st);
+      e = rope_gate_bwd_launch(W.dQacc, 1, nullptr, nullptr, nullptr, W.dQ, 1, T, d, hd, cs, st);
       if (e == cudaSuccess)
-        e = rope_gate_bwd_launch(W.dKr, 0, nullptr, nullptr, nullptr, W.dK, 1, T, d, hd, cfg->use_rope, W.theta,
-                                 b->timestamps_ms, v.row_seq, b->cu_seqlens, st);
+        e = rope_gate_bwd_launch(W.dKr, 0, nullptr, nullptr, nullptr, W.dK, 1, T, d, hd, cs, st);
     }
   }
   // A12: dXt = dQ W_q^T + dK W_k^T + dV W_v^T (one K = 3d accumulation), weight grads, rep-gate bwd

@@ -42,7 +42,9 @@ struct GemmCfg {
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int TMEM_COLS = 2 * BN;
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+  static constexpr int STG_OFF = STAGES * STAGE_BYTES;        // [8 epilogue warps][4 KB] row transposes
+  static constexpr int BAR_OFF = STG_OFF + 8 * 4096;
+  static constexpr int SMEM = BAR_OFF + 1024 + 256;
 };
 
 struct Unit {
@@ -130,20 +132,14 @@ __device__ __forceinline__ void store_any32(void* base, int is_f32, size_t off, 
   }
 }
 
-// Rotate adjacent pairs by alpha = dt * theta_i (timestamp RoPE).  Angle in fp64,
-// reduced mod 2*pi in fp64, then fp32 sincos (SURVEY hard part 6).
-__device__ __forceinline__ void rope_pair(float& a, float& b, double dt, double theta, float sign) {
-  // alpha = dt * theta in fp64, reduced mod 2 pi in fp64 (|k| <= ~1e3: the 2 pi rounding error
-  // k * 2.4e-16 is negligible), then MUFU sincos on r in [-pi, pi] (abs err ~5e-7).
-  const double ang = dt * theta;
-  const double k = rint(ang * 0.15915494309189535);
-  const float r = (float)fma(-k, 6.283185307179586, ang);
-  float s, c;
-  __sincosf(r, &s, &c);
-  s *= sign;
-  const float x0 = a, x1 = b;
-  a = x0 * c - x1 * s;
-  b = x0 * s + x1 * c;
+// Rotate adjacent pairs (v[2j], v[2j+1]) by alpha_j: cs = (cos, sin) interleaved.
+__device__ __forceinline__ void rope_rotate32(float (&v)[32], const float (&cs)[32]) {
+#pragma unroll
+  for (int j = 0; j < 32; j += 2) {
+    const float x0 = v[j], x1 = v[j + 1], c = cs[j], s = cs[j + 1];
+    v[j] = x0 * c - x1 * s;
+    v[j + 1] = x0 * s + x1 * c;
+  }
 }
 
 __device__ __forceinline__ void run_epilogue(const EpiParams& e, int row, int M, int n0c, float (&v)[32]) {
@@ -173,15 +169,9 @@ __device__ __forceinline__ void run_epilogue(const EpiParams& e, int row, int M,
 #pragma unroll
       for (int j = 0; j < 32; ++j) v[j] = x[j] * __fdividef(1.0f, 1.0f + __expf(-v[j]));
       if (e.mode == EPI_GATE_ROPE) {
-        const int s = e.row_seq[row];
-        const double dt = (s >= 0) ? (double)(e.t_ms[row] - e.t_ms[e.cu[s]]) : 0.0;
-        int hc = n0c % e.hd;  // head-local column of v[0]; a 32-column slice crosses at most one head edge
-#pragma unroll
-        for (int j = 0; j < 32; j += 2) {
-          rope_pair(v[j], v[j + 1], dt, e.theta[hc >> 1], 1.0f);
-          hc += 2;
-          if (hc >= e.hd) hc -= e.hd;
-        }
+        float cs[32];
+        load_f32x32(e.rope_cs + (size_t)row * (e.hd + 32) + (n0c % e.hd), cs);
+        rope_rotate32(v, cs);
       }
       store_any32(e.out, e.out_f32, off, v);
     } break;
@@ -236,13 +226,143 @@ __device__ __forceinline__ void run_epilogue(const EpiParams& e, int row, int M,
   }
 }
 
+// Warp-cooperative variants: the 32 lanes hold rows row0 .. row0 + 31 of the same 32 columns
+// (tcgen05.ld 32x32b layout).  Global traffic goes through a per-warp 4 KB swizzled transpose
+// (ptx.cuh) so each load / store instruction covers whole row segments instead of 32 lines.
+__device__ __forceinline__ void warp_load_rows(uint32_t stg, const void* base, int is_f32, size_t off0, size_t ld,
+                                               int rows_valid, float (&x)[32]) {
+  const uint32_t lane = threadIdx.x & 31;
+  if (!is_f32) {
+    const __nv_bfloat16* b = reinterpret_cast<const __nv_bfloat16*>(base) + off0;
+    uint4 g[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int row = i * 8 + (lane >> 2), j = lane & 3;
+      g[i] = row < rows_valid ? *reinterpret_cast<const uint4*>(b + (size_t)row * ld + j * 8) : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int row = i * 8 + (lane >> 2), j = lane & 3;
+      sts_u4(stg + row * 64 + ((j ^ ((row >> 1) & 3)) << 4), g[i].x, g[i].y, g[i].z, g[i].w);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const uint4 u = lds_u4(stg + lane * 64 + ((j ^ ((lane >> 1) & 3)) << 4));
+      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float2 f = __bfloat1622float2(h[e]);
+        x[j * 8 + e * 2] = f.x;
+        x[j * 8 + e * 2 + 1] = f.y;
+      }
+    }
+  } else {
+    const float* b = reinterpret_cast<const float*>(base) + off0;
+    uint4 g[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int row = i * 4 + (lane >> 3), j = lane & 7;
+      g[i] = row < rows_valid ? *reinterpret_cast<const uint4*>(b + (size_t)row * ld + j * 4) : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int row = i * 4 + (lane >> 3), j = lane & 7;
+      sts_u4(stg + row * 128 + ((j ^ (row & 7)) << 4), g[i].x, g[i].y, g[i].z, g[i].w);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const uint4 u = lds_u4(stg + lane * 128 + ((j ^ (lane & 7)) << 4));
+      x[j * 4] = __uint_as_float(u.x);
+      x[j * 4 + 1] = __uint_as_float(u.y);
+      x[j * 4 + 2] = __uint_as_float(u.z);
+      x[j * 4 + 3] = __uint_as_float(u.w);
+    }
+  }
+  __syncwarp();
+}
+__device__ __forceinline__ void warp_store_rows(uint32_t stg, void* base, int is_f32, size_t off0, size_t ld,
+                                                int rows_valid, const float (&v)[32]) {
+  if (!is_f32) {
+    uint32_t w[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) w[j] = pack_bf16(v[2 * j], v[2 * j + 1]);
+    warp_store_rows_bf16(stg, w, reinterpret_cast<__nv_bfloat16*>(base) + off0, ld, rows_valid, 32);
+  } else {
+    uint32_t u[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) u[j] = __float_as_uint(v[j]);
+    warp_store_rows_f32(stg, u, 1.0f, reinterpret_cast<float*>(base) + off0, ld, rows_valid, 32);
+  }
+}
+
+__device__ __forceinline__ void run_epilogue_warp(const EpiParams& e, int row0, int M, int n0c, float (&v)[32],
+                                                  uint32_t stg) {
+  const int lane = threadIdx.x & 31;
+  if (e.row_map || e.mode == EPI_ATOMIC || e.mode == EPI_HEAD) {
+    run_epilogue(e, row0 + lane, M, n0c, v);
+    return;
+  }
+  const int rows_valid = M - row0;
+  if (rows_valid <= 0) return;
+  const size_t off0 = (size_t)row0 * e.ldo + n0c;
+  switch (e.mode) {
+    case EPI_STORE: {
+      if (e.resid) {
+        float r[32];
+        warp_load_rows(stg, e.resid, e.resid_f32, off0, e.ldo, rows_valid, r);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] += r[j];
+      }
+      warp_store_rows(stg, e.out, e.out_f32, off0, e.ldo, rows_valid, v);
+    } break;
+    case EPI_GATE:
+    case EPI_GATE_ROPE: {
+      if (e.aux) warp_store_rows(stg, e.aux, e.aux_f32, off0, e.ldo, rows_valid, v);
+      float x[32];
+      warp_load_rows(stg, e.src, 0, off0, e.ldo, rows_valid, x);
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] = x[j] * __fdividef(1.0f, 1.0f + __expf(-v[j]));
+      if (e.mode == EPI_GATE_ROPE) {  // head-local window [n0c % hd, + 32) of the rope table rows
+        float cs[32];
+        warp_load_rows(stg, e.rope_cs, 1, (size_t)row0 * (e.hd + 32) + (n0c % e.hd), e.hd + 32, rows_valid, cs);
+        rope_rotate32(v, cs);
+      }
+      warp_store_rows(stg, e.out, e.out_f32, off0, e.ldo, rows_valid, v);
+    } break;
+    case EPI_GATE_BWD: {
+      float z[32], x[32], r[32];
+      warp_load_rows(stg, e.aux, e.aux_f32, off0, e.ldo, rows_valid, z);
+      warp_load_rows(stg, e.src, 0, off0, e.ldo, rows_valid, x);
+      if (e.resid) {
+        warp_load_rows(stg, e.resid, e.resid_f32, off0, e.ldo, rows_valid, r);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) r[j] = 0.f;
+      }
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const float g = __fdividef(1.0f, 1.0f + __expf(-z[j]));
+        const float vj = v[j];
+        v[j] = vj * x[j] * g * (1.0f - g);
+        r[j] += vj * g;
+      }
+      warp_store_rows(stg, e.out, e.out_f32, off0, e.ldo, rows_valid, v);
+      warp_store_rows(stg, e.out2, 1, off0, e.ldo, rows_valid, r);
+    } break;
+    default:
+      break;
+  }
+}
+
 // ---------------------------------------------------------------- kernel
 template <int BN>
 __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_kernel(const __grid_constant__ GemmKParams P) {
   using C = GemmCfg<BN>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::BAR_OFF);
   uint64_t* empty = full + C::STAGES;
   uint64_t* tfull = empty + C::STAGES;
   uint64_t* tempty = tfull + 2;
@@ -343,6 +463,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_kernel(const __grid_cons
     // ============================ epilogue
     const uint32_t quarter = warp & 3;
     const int half = (warp - 4) >> 2;  // warps 4-7 take even 32-column slices, 8-11 odd ones
+    const uint32_t stg = smem_u32(smem + C::STG_OFF) + (warp - 4) * 4096;
     uint32_t tc = 0;
     for (int u = blockIdx.x; u < P.total_units; u += gridDim.x, ++tc) {
       const Unit U = decode_unit(P, u);
@@ -350,7 +471,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_kernel(const __grid_cons
       const uint32_t buf = tc & 1, use = tc >> 1;
       mbar_wait(&tfull[buf], use & 1);
       tc_fence_after();
-      const int row = U.m0 + quarter * 32 + lane;
+      const int row0 = U.m0 + quarter * 32;
       const int n0 = U.n0 * BN;
       for (int c = half; c < BN / 32; c += 2) {
         const int n0c = n0 + c * 32;
@@ -361,7 +482,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_kernel(const __grid_cons
         float v[32];
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-        run_epilogue(q.epi, row, q.M, n0c, v);
+        run_epilogue_warp(q.epi, row0, q.M, n0c, v, stg);
       }
       tc_fence_before();
       __syncwarp();
@@ -386,7 +507,9 @@ struct PairCfg {
   static constexpr int B_BYTES = 128 * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int TMEM_COLS = 512;
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+  static constexpr int STG_OFF = STAGES * STAGE_BYTES;
+  static constexpr int BAR_OFF = STG_OFF + 8 * 4096;
+  static constexpr int SMEM = BAR_OFF + 1024 + 256;
 };
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
@@ -395,7 +518,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
   constexpr int BN = 256;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::BAR_OFF);
   uint64_t* empty = full + C::STAGES;
   uint64_t* tfull = empty + C::STAGES;
   uint64_t* tempty = tfull + 2;
@@ -502,6 +625,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
     // ============================ epilogue (both CTAs: 128 rows x 256 columns each)
     const uint32_t quarter = warp & 3;
     const int half = (warp - 4) >> 2;
+    const uint32_t stg = smem_u32(smem + C::STG_OFF) + (warp - 4) * 4096;
     const uint32_t te_remote = mapa_shared(smem_u32(&tempty[0]), 0);
     uint32_t tc = 0;
     for (int u = cid; u < P.total_units; u += ncl, ++tc) {
@@ -510,7 +634,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
       const uint32_t buf = tc & 1, use = tc >> 1;
       mbar_wait(&tfull[buf], use & 1);
       tc_fence_after();
-      const int row = U.m0 + 128 * (int)rank + quarter * 32 + lane;
+      const int row0 = U.m0 + 128 * (int)rank + quarter * 32;
       const int n0 = U.n0 * BN;
       for (int c = half; c < BN / 32; c += 2) {
         const int n0c = n0 + c * 32;
@@ -521,7 +645,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
         float v[32];
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-        run_epilogue(q.epi, row, q.M, n0c, v);
+        run_epilogue_warp(q.epi, row0, q.M, n0c, v, stg);
       }
       tc_fence_before();
       __syncwarp();

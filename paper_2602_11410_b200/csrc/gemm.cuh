@@ -29,11 +29,8 @@ struct EpiParams {
   void* aux;
   float* out2;
   const int32_t* row_map;  // optional output-row remap (scatter); < 0 = drop row
-  // RoPE (EPI_GATE_ROPE)
-  const int64_t* t_ms;
-  const int32_t* row_seq;
-  const int32_t* cu;
-  const double* theta;     // [hd/2]
+  // RoPE (EPI_GATE_ROPE): (cos, sin) table [M][hd + 32] floats, interleaved per frequency
+  const float* rope_cs;
   // heads (EPI_HEAD)
   const float* b1;
   const float* w2;

@@ -1,5 +1,7 @@
 // Elementwise / reduction kernels of the hot path that are HBM-bound (no tensor cores):
 //   rope_theta_kernel       theta_i = (phi_min / dt_max) * base^(2i/hd)
+//   rope_table_kernel       (cos, sin)(dt_row theta_i) per (row, frequency), shared by every head
+//                           and by Q and K (forward epilogue and backward)
 //   rope_apply_kernel       RoPE without interaction gate (ablation path)
 //   rope_gate_bwd_kernel    A11: dQt = R(-alpha) dQr; g = sigma(Zq); u = dQt*Q*g*(1-g); r = dQt*g
 //   gather_rows_kernel      H_r = H[rows] (A7 operand)
@@ -16,50 +18,54 @@ __global__ void rope_theta_kernel(double* theta, int half, int hd, double phi_mi
   if (i < half) theta[i] = (phi_min / dt_max) * pow(base, 2.0 * i / (double)hd);
 }
 
-__device__ __forceinline__ void rot(float& a, float& b, double dt, double th, float sign) {
-  // alpha = dt * theta in fp64, reduced mod 2 pi in fp64 (|k| <= ~1e3: the 2 pi rounding error
-  // k * 2.4e-16 is negligible), then MUFU sincos on r in [-pi, pi] (abs err ~5e-7).
+// alpha = dt * theta in fp64, reduced mod 2 pi in fp64 (|k| <= ~1e3: the 2 pi rounding error
+// k * 2.4e-16 is negligible), then MUFU sincos on r in [-pi, pi] (abs err ~5e-7).
+__device__ __forceinline__ void rope_cs(double dt, double th, float& c, float& s) {
   const double ang = dt * th;
   const double k = rint(ang * 0.15915494309189535);
   const float r = (float)fma(-k, 6.283185307179586, ang);
-  float s, c;
   __sincosf(r, &s, &c);
-  s *= sign;
-  const float x0 = a, x1 = b;
-  a = x0 * c - x1 * s;
-  b = x0 * s + x1 * c;
 }
 
-__device__ __forceinline__ double row_dt(const int64_t* t, const int32_t* row_seq, const int32_t* cu, int row) {
+// cs[row][2i] = cos(alpha_i), cs[row][2i + 1] = sin(alpha_i), alpha_i = dt_row theta_i with
+// dt_row = t_row - t_(sequence start); row stride hd + 32 floats, the first 32 entries
+// repeated at [hd, hd + 32) so that any 32-float window starting at an even head-local column
+// is contiguous (a GEMM epilogue slice may cross one head edge when hd % 32 != 0).
+__global__ void rope_table_kernel(float* cs, int T, int hd, const double* theta, const int64_t* t,
+                                  const int32_t* row_seq, const int32_t* cu) {
+  const int half = hd / 2, w = half + 16;
+  const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (size_t)T * w) return;
+  const int row = (int)(idx / w), i = (int)(idx % w);
+  const int pr = i < half ? i : i - half;
   const int s = row_seq[row];
-  return s >= 0 ? (double)(t[row] - t[cu[s]]) : 0.0;
+  const double dt = s >= 0 ? (double)(t[row] - t[cu[s]]) : 0.0;
+  float c, sn;
+  rope_cs(dt, theta[pr], c, sn);
+  reinterpret_cast<float2*>(cs + (size_t)row * (hd + 32))[i] = make_float2(c, sn);
 }
 
 // one thread per (row, pair of columns)
 __global__ void rope_apply_kernel(const __nv_bfloat16* in, __nv_bfloat16* out, int T, int d, int hd,
-                                  const double* theta, const int64_t* t, const int32_t* row_seq, const int32_t* cu) {
+                                  const float* cs) {
   const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   const size_t pairs = (size_t)T * d / 2;
   if (idx >= pairs) return;
   const int row = (int)(idx / (d / 2));
   const int c = (int)(idx % (d / 2)) * 2;
-  float2 v = __bfloat1622float2(reinterpret_cast<const __nv_bfloat162*>(in)[idx]);
-  rot(v.x, v.y, row_dt(t, row_seq, cu, row), theta[(c % hd) >> 1], 1.f);
-  reinterpret_cast<__nv_bfloat162*>(out)[idx] = __floats2bfloat162_rn(v.x, v.y);
+  const float2 v = __bfloat1622float2(reinterpret_cast<const __nv_bfloat162*>(in)[idx]);
+  const float2 r = *reinterpret_cast<const float2*>(cs + (size_t)row * (hd + 32) + (c % hd));
+  reinterpret_cast<__nv_bfloat162*>(out)[idx] = __floats2bfloat162_rn(v.x * r.x - v.y * r.y, v.x * r.y + v.y * r.x);
 }
 
 // dr: fp32 (dQr accumulator) or bf16 (dKr).  gate (Z) bf16 may be null (no interaction gate):
 // then out_u is unused and out_r (bf16 if r_bf16) receives dQt directly.
-// One thread = 8 consecutive columns (4 pairs) of one row: one dt per thread, 16-byte accesses,
-// the theta table in shared memory.
+// One thread = 8 consecutive columns (4 pairs) of one row: 16-byte accesses, (cos, sin) from the
+// rope table (cs, row stride hd + 32; null without RoPE).
 __global__ void __launch_bounds__(256) rope_gate_bwd_kernel(const void* dr, int dr_f32, const __nv_bfloat16* Xq,
                                                             const __nv_bfloat16* Z, __nv_bfloat16* out_u,
                                                             void* out_r, int r_bf16, int T, int d, int hd,
-                                                            int use_rope, const double* theta, const int64_t* t,
-                                                            const int32_t* row_seq, const int32_t* cu) {
-  __shared__ double th[64];
-  if (threadIdx.x < hd / 2) th[threadIdx.x] = theta[threadIdx.x];
-  __syncthreads();
+                                                            const float* cs) {
   const int per_row = d / 8;
   const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= (size_t)T * per_row) return;
@@ -81,14 +87,15 @@ __global__ void __launch_bounds__(256) rope_gate_bwd_kernel(const void* dr, int 
       g[2 * e + 1] = f.y;
     }
   }
-  if (use_rope) {
-    const double dt = row_dt(t, row_seq, cu, row);
-    int hc = c0 % hd;
+  if (cs) {  // R(-alpha): the 8-column group never crosses a head edge (hd % 8 == 0)
+    const float4* q = reinterpret_cast<const float4*>(cs + (size_t)row * (hd + 32) + (c0 % hd));
+    const float4 a = q[0], b = q[1];
+    const float cv[4] = {a.x, a.z, b.x, b.z}, sv[4] = {a.y, a.w, b.y, b.w};
 #pragma unroll
-    for (int e = 0; e < 8; e += 2) {
-      rot(g[e], g[e + 1], dt, th[hc >> 1], -1.f);  // R(-alpha)
-      hc += 2;
-      if (hc >= hd) hc -= hd;
+    for (int e = 0; e < 4; ++e) {
+      const float x0 = g[2 * e], x1 = g[2 * e + 1];
+      g[2 * e] = x0 * cv[e] + x1 * sv[e];
+      g[2 * e + 1] = x1 * cv[e] - x0 * sv[e];
     }
   }
   float r[8];
@@ -237,25 +244,29 @@ cudaError_t rope_theta_launch(double* theta, int hd, double phi_min, double base
   rope_theta_kernel<<<1, 128, 0, st>>>(theta, hd / 2, hd, phi_min, base, dt_max);
   return cudaGetLastError();
 }
-cudaError_t rope_apply_launch(const void* in, void* out, int T, int d, int hd, const double* theta, const int64_t* t,
-                              const int32_t* row_seq, const int32_t* cu, cudaStream_t st) {
+cudaError_t rope_table_launch(float* cs, int T, int hd, const double* theta, const int64_t* t, const int32_t* row_seq,
+                              const int32_t* cu, cudaStream_t st) {
+  ProfScope ps(PROF_OTHER, st, 1);
+  const size_t work = (size_t)T * (hd / 2 + 16);
+  if (work) rope_table_kernel<<<blocks(work, 256), 256, 0, st>>>(cs, T, hd, theta, t, row_seq, cu);
+  return cudaGetLastError();
+}
+cudaError_t rope_apply_launch(const void* in, void* out, int T, int d, int hd, const float* cs, cudaStream_t st) {
   ProfScope ps(PROF_OTHER, st, 1);
   const size_t pairs = (size_t)T * d / 2;
   if (pairs)
     rope_apply_kernel<<<blocks(pairs, 256), 256, 0, st>>>(reinterpret_cast<const __nv_bfloat16*>(in),
-                                                         reinterpret_cast<__nv_bfloat16*>(out), T, d, hd, theta, t,
-                                                         row_seq, cu);
+                                                         reinterpret_cast<__nv_bfloat16*>(out), T, d, hd, cs);
   return cudaGetLastError();
 }
 cudaError_t rope_gate_bwd_launch(const void* dr, int dr_f32, const void* Xq, const void* Z, void* out_u, void* out_r,
-                                 int r_bf16, int T, int d, int hd, int use_rope, const double* theta, const int64_t* t,
-                                 const int32_t* row_seq, const int32_t* cu, cudaStream_t st) {
+                                 int r_bf16, int T, int d, int hd, const float* cs, cudaStream_t st) {
   ProfScope ps(PROF_OTHER, st, 1);
   const size_t work = (size_t)T * d / 8;
   if (work)
     rope_gate_bwd_kernel<<<blocks(work, 256), 256, 0, st>>>(
         dr, dr_f32, reinterpret_cast<const __nv_bfloat16*>(Xq), reinterpret_cast<const __nv_bfloat16*>(Z),
-        reinterpret_cast<__nv_bfloat16*>(out_u), out_r, r_bf16, T, d, hd, use_rope, theta, t, row_seq, cu);
+        reinterpret_cast<__nv_bfloat16*>(out_u), out_r, r_bf16, T, d, hd, cs);
   return cudaGetLastError();
 }
 cudaError_t gather_rows_launch(const void* H, const int32_t* rows, int n, int T, int d, void* out, uint32_t* err,

@@ -6,11 +6,12 @@
 
 namespace cadet {
 cudaError_t rope_theta_launch(double* theta, int hd, double phi_min, double base, double dt_max, cudaStream_t st);
-cudaError_t rope_apply_launch(const void* in, void* out, int T, int d, int hd, const double* theta, const int64_t* t,
-                              const int32_t* row_seq, const int32_t* cu, cudaStream_t st);
+// (cos, sin) table [T][hd + 32] floats (see rope_table_kernel); cs = null means no RoPE
+cudaError_t rope_table_launch(float* cs, int T, int hd, const double* theta, const int64_t* t, const int32_t* row_seq,
+                              const int32_t* cu, cudaStream_t st);
+cudaError_t rope_apply_launch(const void* in, void* out, int T, int d, int hd, const float* cs, cudaStream_t st);
 cudaError_t rope_gate_bwd_launch(const void* dr, int dr_f32, const void* Xq, const void* Z, void* out_u, void* out_r,
-                                 int r_bf16, int T, int d, int hd, int use_rope, const double* theta, const int64_t* t,
-                                 const int32_t* row_seq, const int32_t* cu, cudaStream_t st);
+                                 int r_bf16, int T, int d, int hd, const float* cs, cudaStream_t st);
 cudaError_t gather_rows_launch(const void* H, const int32_t* rows, int n, int T, int d, void* out, uint32_t* err,
                                cudaStream_t st);
 cudaError_t head_init_launch(float* logits, const float* b2, int n, int K, cudaStream_t st);
