@@ -24,6 +24,7 @@ import time
 import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
+TRAFFIC_PROFILE = "r01_dram_traffic.json"  # per-class DRAM bytes per launch (scripts/traffic_summary.py)
 sys.path.insert(0, ROOT)
 
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
@@ -95,12 +96,25 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ workload
-def build_inputs(wl: dict, seed: int, pin: bool):
+def build_inputs(wl: dict, seed: int, pin: bool, rank: int = 0, world: int = 1):
+    """One rank's batch.  N = 1: users drawn in arrival order up to the budget.  N > 1:
+    every rank draws the same global user stream for world x budget tokens and keeps its share of
+    the LPT partition (whole users, balanced on estimated cost, each rank under its budget)."""
     from synth import generator as G
-    from paper_2602_11410_b200.model import make_inputs
+    from paper_2602_11410_b200.model import make_inputs, partition_lpt
     gcfg = G.GenConfig(max_tokens=wl["max_tokens"])
-    users = G.gen_users_for_budget(seed, wl["budget"], gcfg)
-    return users, make_inputs(users, wl["d_model"], wl["L_chunk"], seed, pin=pin)
+    if world == 1:
+        users = G.gen_users_for_budget(seed, wl["budget"], gcfg)
+    else:
+        allu = G.gen_users_for_budget(seed, world * wl["budget"], gcfg)
+        while True:
+            try:
+                parts = partition_lpt([u.length for u in allu], world, wl["budget"], wl["L_chunk"], wl["d_model"])
+                break
+            except ValueError:
+                allu = allu[:-1]
+        users = [allu[i] for i in parts[rank]]
+    return users, make_inputs(users, wl["d_model"], wl["L_chunk"], seed + 1000 * rank, pin=pin)
 
 
 def step_flops(wl: dict, tokens: int, pairs: int, n_imp: int, dh: int, K: int = 2):
@@ -247,7 +261,7 @@ def main():
         dist.barrier()  # local rank 0 finished any rebuild before the others load the library
     dev = torch.device("cuda", local)
 
-    users, host_inp = build_inputs(wl, 1000 * rank, pin=True)
+    users, host_inp = build_inputs(wl, 0, pin=True, rank=rank, world=world)
     inp = host_inp.to(dev)
     torch.cuda.synchronize()
     scfg = StackConfig(d_model=wl["d_model"], n_heads=wl["n_heads"], n_layers=wl["n_layers"], budget=wl["budget"],
@@ -337,8 +351,15 @@ def main():
     dom = max(("gemm", "attn_fwd", "attn_bwd"), key=lambda k: per_step_ms[k])
     achieved = flops[dom] / (per_step_ms[dom] / 1000.0) / 1e12 if per_step_ms[dom] > 0 else 0.0
     peak = float(peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops")))
+    traffic, traffic_src = None, None
+    tpath = os.path.join(ROOT, "profiles", TRAFFIC_PROFILE)
+    if os.path.exists(tpath) and workload_name == "c4":
+        tj = json.load(open(tpath))
+        if dom in tj:
+            traffic, traffic_src = tj[dom]["dram_bytes_per_launch"], f"profiles/{TRAFFIC_PROFILE} ({tj.get('method', '')})"
     roofline = {"bound": "tensor", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                "frac": achieved / peak, "traffic": None,
+                "frac": achieved / peak, "traffic": traffic, "traffic_unit": "DRAM bytes per launch",
+                "traffic_source": traffic_src,
                 "peak_source": f"{peak_src} bf16_tflops_sustained (kernel timed inside a long step)",
                 "share_of_step": per_step_ms[dom] / ms, "per_class_ms_per_step": per_step_ms,
                 "launches_per_step": {k: v[1] / max(1, args.steps) for k, v in prof.items()}}
@@ -356,7 +377,8 @@ def main():
                    "allowed_pairs_per_head": pairs, "impressions": n_imp, "layers": wl["n_layers"],
                    "d_model": wl["d_model"], "heads": wl["n_heads"], "L_chunk": wl["L_chunk"],
                    "l2": "inputs > L2 (X 128 MB + activations > 1 GB per step); no flush needed",
-                   "parallelism": f"dp{world}"},
+                   "parallelism": f"dp{world}",
+                   "partition": "N>1: LPT of one global user stream (world x budget tokens) over ranks"},
         "tflops": tflops_all, "tflops_per_gpu": tflops_all / world,
         "frac_of_peak_measured": tflops_all / world / float(peaks.get("bf16_tflops", 1663.9)),
         "frac_of_peak_spec": tflops_all / world / 2250.0,

@@ -6,7 +6,10 @@ A step (in order):
   A1-A6      L residual layers of self-gated attention forward (cadet_attn_forward; plan inside)
   A7-A8      context-conditioned towers + routed BCE + tower backward (cadet_heads_*)
   A9-A12     layers backward (cadet_attn_backward), weight gradients into one flat fp32 buffer
-  DP         torch.distributed all_reduce(SUM) of the flat gradient buffer (NCCL) when world > 1
+  DP         SURVEY 8(e), NCCL through torch.distributed when world > 1: per-layer gradient buckets
+             all-reduced (SUM) asynchronously as soon as each layer's backward is enqueued, loss and
+             impression count all-reduced, logits + labels all-gathered (dp_gather_scores); whole
+             users are assigned to ranks by LPT on estimated cost (partition_lpt)
 Every computation is a libcadet kernel; PyTorch only allocates memory, provides the stream and
 runs the NCCL collective.
 """
@@ -98,6 +101,97 @@ def dp_reduce(grads: torch.Tensor, loss: torch.Tensor, group=None):
     torch.distributed.all_reduce(grads, group=group)
     torch.distributed.all_reduce(loss, group=group)
     return grads, loss
+
+
+class GradBuckets:
+    """gradient buckets all-reduced (SUM) as soon as their producer is enqueued.
+
+    `launch(i)` starts an async all_reduce of bucket i (NCCL orders it after the work already on
+    the current stream, so it overlaps the backward of earlier layers); `wait()` joins them all.
+    Summation is exact for the union batch because the loss is a sum (Eq. 9, R15)."""
+
+    def __init__(self, buckets, group=None):
+        self.buckets = list(buckets)
+        self.group = group
+        self.handles = []
+
+    def launch(self, i: int):
+        if self.group is not None:
+            self.handles.append(torch.distributed.all_reduce(self.buckets[i], group=self.group, async_op=True))
+
+    def wait(self):
+        for h in self.handles:
+            h.wait()
+        self.handles = []
+
+
+def dp_reduce_stats(loss: torch.Tensor, n_imp: int, group=None):
+    """global loss sum and impression count (one all_reduce of a 2-vector)."""
+    v = torch.stack([loss.reshape(-1)[0].to(torch.float64), torch.tensor(float(n_imp), dtype=torch.float64,
+                                                                        device=loss.device)])
+    if group is not None:
+        torch.distributed.all_reduce(v, group=group)
+    return float(v[0].item()), int(round(float(v[1].item())))
+
+
+def dp_gather_scores(logits: torch.Tensor, labels: torch.Tensor, group=None):
+    """all_gather of the ranks' logits [n_r, K] and labels [n_r] (evaluation and
+    the cross-user pairwise loss of NEXT-2).  n_r differs per rank: gather the counts first, pad to
+    the maximum, gather, then drop the padding.  Returns rank-ordered concatenations."""
+    if group is None:
+        return logits, labels
+    world = torch.distributed.get_world_size(group)
+    n = torch.tensor([logits.shape[0]], dtype=torch.int64, device=logits.device)
+    counts = [torch.zeros_like(n) for _ in range(world)]
+    torch.distributed.all_gather(counts, n, group=group)
+    counts = [int(c.item()) for c in counts]
+    m = max(counts)
+    lp = torch.zeros((m,) + tuple(logits.shape[1:]), dtype=logits.dtype, device=logits.device)
+    yp = torch.zeros((m,), dtype=labels.dtype, device=labels.device)
+    lp[: logits.shape[0]] = logits
+    yp[: labels.shape[0]] = labels
+    gl = [torch.empty_like(lp) for _ in range(world)]
+    gy = [torch.empty_like(yp) for _ in range(world)]
+    torch.distributed.all_gather(gl, lp, group=group)
+    torch.distributed.all_gather(gy, yp, group=group)
+    return (torch.cat([g[:c] for g, c in zip(gl, counts)]), torch.cat([g[:c] for g, c in zip(gy, counts)]))
+
+
+def chunk_lengths(length: int, L_chunk: int):
+    """A0 split of one history (newest chunk full, oldest may be short)."""
+    n = -(-int(length) // L_chunk)
+    return [int(length) - (n - 1) * L_chunk] + [L_chunk] * (n - 1) if n > 0 else []
+
+
+def user_cost(length: int, L_chunk: int, d_model: int) -> float:
+    """Estimated step cost of one user: per chunk c1 len + c2 len^2 with c1 = 7 d, c2 = 1, i.e. the
+    42 d^2 projection flops per token against ~6 d len attention flops per token (len / 2 visible
+    keys, 12 d flops per pair fwd + bwd), in units of 6 d flops."""
+    return float(sum(7.0 * d_model * c + float(c) * c for c in chunk_lengths(length, L_chunk)))
+
+
+def partition_lpt(lens, world: int, budget: int, L_chunk: int, d_model: int):
+    """SURVEY 8(e) partitioning: whole users (their chunks stay together, chunking runs on device)
+    to ranks by longest-processing-time-first on user_cost, each rank under its token budget.
+    Deterministic (ties by user index, then rank).  Returns per-rank sorted user-index arrays
+    (arrival order is kept inside a rank).  Raises if a user cannot be placed."""
+    lens = [int(x) for x in lens]
+    cost = [user_cost(m, L_chunk, d_model) for m in lens]
+    order = sorted(range(len(lens)), key=lambda i: (-cost[i], i))
+    load = [0.0] * world
+    tokens = [0] * world
+    out = [[] for _ in range(world)]
+    for i in order:
+        best = None
+        for r in range(world):
+            if tokens[r] + lens[i] <= budget and (best is None or load[r] < load[best]):
+                best = r
+        if best is None:
+            raise ValueError(f"user {i} ({lens[i]} tokens) fits no rank under budget {budget}")
+        out[best].append(i)
+        load[best] += cost[i]
+        tokens[best] += lens[i]
+    return [np.array(sorted(o), dtype=np.int64) for o in out]
 
 
 def _vp(t):
@@ -207,11 +301,17 @@ class CadetStack:
                                     _vp(self.logits), _vp(self.pre), _vp(self._hws), self._hws.numel(), st))
         if not backward:
             return self.logits
+        # gradient buckets: [towers] then one per layer (in backward order), each all-reduced as soon
+        # as its backward is enqueued (overlapped with the backward of earlier layers)
+        nl, dd = cfg.n_layers, d * d
+        buckets = GradBuckets([self.grads[nl * 7 * dd:]] +
+                              [self.grads[l * 7 * dd:(l + 1) * 7 * dd] for l in reversed(range(nl))], group)
         hg = L.HeadGrads(self.gW1.data_ptr(), self.gb1.data_ptr(), self.gw2.data_ptr(), self.gb2.data_ptr())
         chk(lib.cadet_heads_loss_backward(C.byref(hc), C.byref(hw), _vp(self.Hs[-1]), _vp(inp.rows), n_imp, T,
                                           _vp(self.logits), _vp(self.pre), _vp(inp.bucket), _vp(inp.label),
                                           _vp(self.loss), _vp(self.dHs[-1]), C.byref(hg), _vp(self._hws),
                                           self._hws.numel(), st))
+        buckets.launch(0)
         # A9-A12: layers backward; dX_l = dX_{l+1} (residual) + Attn_l^T(dX_{l+1})
         for l in reversed(range(cfg.n_layers)):
             w = L.AttnWeights(*[x.data_ptr() for x in self.W[l]])
@@ -219,7 +319,10 @@ class CadetStack:
             chk(lib.cadet_attn_backward(C.byref(self.acfg), C.byref(b), C.byref(w), _vp(self.Hs[l]),
                                         _vp(self.saved[l]), _vp(self.dHs[l + 1]), _vp(self.dHs[l]),
                                         _vp(self.dHs[l + 1]), C.byref(g), ws, wsn, st))
-        dp_reduce(self.grads, self.loss, group)
+            buckets.launch(nl - l)
+        buckets.wait()
+        if group is not None:
+            torch.distributed.all_reduce(self.loss, group=group)
         return self.loss
 
     def pairs(self, inp: StepInputs) -> int:

@@ -51,7 +51,7 @@ L.cadet_debug_phase_read(buf2, 8192 * 8)
 ph = np.frombuffer(buf2, dtype=np.uint64).reshape(8192, 8).astype(np.float64)
 used = ph[ph.sum(1) > 0]
 items = 4840  # C4 dkv work items (k-tiles x heads)
-names = ["mma: kv_full wait", "mma: acc_free wait", "mma: pds wait", "mma: issue", "cmp: mma_done wait",
-         "cmp: drain", "cmp: sdp wait", "cmp: math etc"]
+names = ["mma: kv_full wait", "mma: acc_free wait", "mma: pds wait", "mma: issue", "mma: q/dO full wait",
+         "cmp: vec st+fetch+bar", "cmp: sdp wait", "cmp: math+st+arrive (+drain at item end)"]
 for i, nm in enumerate(names):
     print(f"{nm:26s} per item {used[:, i].sum() / items:10.0f} clk  per CTA {used[:, i].mean() / 1.9e3:8.1f} us")

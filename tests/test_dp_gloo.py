@@ -44,14 +44,28 @@ def _worker(rank, world, port, q):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    from paper_2602_11410_b200.model import dp_reduce
+    from paper_2602_11410_b200.model import GradBuckets, dp_gather_scores, dp_reduce, dp_reduce_stats
     O, b, cu, X, dY, W, cfg = _case()
     mine = [s for s in range(len(cu) - 1) if s % world == rank]     # whole sequences per rank
-    flat = torch.tensor(_grads(O, cu, b.timestamps, X, dY, W, cfg, mine))
+    g = _grads(O, cu, b.timestamps, X, dY, W, cfg, mine)
+    flat = torch.tensor(g)
     loss = torch.tensor([float(len(mine))], dtype=torch.float64)
     dp_reduce(flat, loss, dist.group.WORLD)
+    # the same gradient through per-layer-style async buckets (three uneven slices of one buffer)
+    flat2 = torch.tensor(g)
+    n = flat2.numel()
+    bk = GradBuckets([flat2[2 * n // 3:], flat2[n // 3:2 * n // 3], flat2[:n // 3]], dist.group.WORLD)
+    for i in range(3):
+        bk.launch(i)
+    bk.wait()
+    # loss / impression counts, and variable-count logits + labels (rank r holds r + 2 rows)
+    tot_loss, tot_imp = dp_reduce_stats(torch.tensor([1.5 * (rank + 1)]), 10 * (rank + 1), dist.group.WORLD)
+    m = rank + 2
+    lg = torch.arange(m * 2, dtype=torch.float32).reshape(m, 2) + 100 * rank
+    lb = torch.full((m,), float(rank))
+    gl, gy = dp_gather_scores(lg, lb, dist.group.WORLD)
     if rank == 0:
-        q.put((flat.numpy(), float(loss.item())))
+        q.put((flat.numpy(), float(loss.item()), flat2.numpy(), tot_loss, tot_imp, gl.numpy(), gy.numpy()))
     dist.barrier()
     dist.destroy_process_group()
 
@@ -66,11 +80,37 @@ def test_dp_sum_allreduce_equals_union_gradient():
     procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
     for p in procs:
         p.start()
-    got, loss = q.get(timeout=240)
+    got, loss, got2, tot_loss, tot_imp, gl, gy = q.get(timeout=240)
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
     O, b, cu, X, dY, W, cfg = _case()
     ref = _grads(O, cu, b.timestamps, X, dY, W, cfg, range(len(cu) - 1))
     assert np.abs(got - ref).max() <= 1e-12 * max(1.0, np.abs(ref).max())
+    assert np.abs(got2 - ref).max() <= 1e-12 * max(1.0, np.abs(ref).max())
     assert loss == len(cu) - 1
+    assert tot_loss == pytest.approx(1.5 + 3.0) and tot_imp == 30
+    exp_l = np.concatenate([np.arange(4, dtype=np.float32).reshape(2, 2),
+                            np.arange(6, dtype=np.float32).reshape(3, 2) + 100])
+    assert np.array_equal(gl, exp_l) and np.array_equal(gy, np.array([0, 0, 1, 1, 1], np.float32))
+
+
+def test_partition_lpt_balances_under_budget():
+    """SURVEY 8(e) host packer: every user placed exactly once, per-rank tokens within the budget,
+    users kept in arrival order inside a rank, LPT spread (max - min load <= largest user cost)."""
+    from paper_2602_11410_b200.model import chunk_lengths, partition_lpt, user_cost
+    from synth import generator as G
+    assert chunk_lengths(5000, 2048) == [904, 2048, 2048] and chunk_lengths(2048, 2048) == [2048]
+    assert sum(chunk_lengths(8191, 2048)) == 8191
+    users = G.gen_users_for_budget(3, 4 * 16384, G.GenConfig())
+    lens = [u.length for u in users]
+    for world in (1, 2, 3, 4):
+        parts = partition_lpt(lens, world, 16384 * 4 // world + 8192, 2048, 352)
+        flat = np.sort(np.concatenate(parts))
+        assert np.array_equal(flat, np.arange(len(lens)))
+        loads = [sum(user_cost(lens[i], 2048, 352) for i in p) for p in parts]
+        assert all(sum(lens[i] for i in p) <= 16384 * 4 // world + 8192 for p in parts)
+        assert all(np.all(np.diff(p) > 0) for p in parts)
+        assert max(loads) - min(loads) <= max(user_cost(m, 2048, 352) for m in lens) + 1e-6
+    with pytest.raises(ValueError):
+        partition_lpt([10, 20, 30], 2, 25, 2048, 64)
