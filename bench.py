@@ -47,15 +47,40 @@ def load_peaks():
 
 # ------------------------------------------------------------------ clocks sampler
 class ClockSampler:
+    """SM clock and clock-event (throttle) reasons sampled DURING the timed region: NVML every
+    5 ms from a background thread (nvidia-smi as fallback, ~200 ms per sample)."""
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    BITS = {"sw_power_cap": 0x4, "hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40}
 
-    def __init__(self, dev_index: int):
+    def __init__(self, dev_index: int, pci_bus_id: str | None = None):
         self.dev = dev_index
+        self.pci = pci_bus_id
         self.proc = None
+        self.nv = None
         self.lines = []
+        self.sm, self.mx, self.reasons = [], None, set()
 
     def start(self):
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            h = None
+            if self.pci:
+                try:
+                    h = nv.nvmlDeviceGetHandleByPciBusId(self.pci)
+                except Exception:
+                    h = None
+            if h is None:
+                h = nv.nvmlDeviceGetHandleByIndex(self.dev)
+            self.nv, self.h = nv, h
+            self.mx = float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
+            self.running = True
+            self.t = threading.Thread(target=self._poll, daemon=True)
+            self.t.start()
+            return
+        except Exception:
+            self.nv = None
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.FIELDS}",
                                           "--format=csv,noheader,nounits", "-lms", "200"],
@@ -65,11 +90,30 @@ class ClockSampler:
         except Exception:
             self.proc = None
 
+    def _poll(self):
+        nv, h = self.nv, self.h
+        get_r = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or nv.nvmlDeviceGetCurrentClocksThrottleReasons
+        while self.running:
+            try:
+                self.sm.append(float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)))
+                r = int(get_r(h))
+                for n, bit in self.BITS.items():
+                    if r & bit:
+                        self.reasons.add(n)
+            except Exception:
+                pass
+            time.sleep(0.005)
+
     def _read(self):
         for line in self.proc.stdout:
             self.lines.append(line.strip())
 
     def stop(self):
+        if self.nv is not None:
+            self.running = False
+            self.t.join(timeout=2)
+            return {"sm_mhz": float(np.median(self.sm)) if self.sm else None, "sm_max_mhz": self.mx,
+                    "reasons": sorted(self.reasons), "samples": len(self.sm), "source": "nvml"}
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         self.proc.terminate()
@@ -92,7 +136,7 @@ class ClockSampler:
                 if v.lower().startswith("active"):
                     reasons.add(n)
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "source": "nvidia-smi"}
 
 
 # ------------------------------------------------------------------ workload
@@ -282,7 +326,11 @@ def main():
     stack.poll()
 
     # ---------------- timed region (inputs resident in HBM)
-    clocks = ClockSampler(local)
+    pp = torch.cuda.get_device_properties(local)
+    pci = None
+    if hasattr(pp, "pci_bus_id"):
+        pci = f"{getattr(pp, 'pci_domain_id', 0):08x}:{pp.pci_bus_id:02x}:{getattr(pp, 'pci_device_id', 0):02x}.0"
+    clocks = ClockSampler(local, pci)
     clocks.start()
     ops.prof_enable(15, 64 * (args.steps + 1) * (wl["n_layers"] + 2))
     n0 = ops.launch_count()
