@@ -257,6 +257,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--graph", action="store_true",
+                    help="replay the step as one CUDA graph (measured: no gain over eager launches on C4)")
     args = ap.parse_args()
     wl = WORKLOADS[args.workload]
     rank = int(os.environ.get("RANK", "0"))
@@ -330,21 +332,43 @@ def main():
     pci = None
     if hasattr(pp, "pci_bus_id"):
         pci = f"{getattr(pp, 'pci_domain_id', 0):08x}:{pp.pci_bus_id:02x}:{getattr(pp, 'pci_device_id', 0):02x}.0"
+    # --graph: the step as one CUDA graph; the per-class CUDA events are nodes of the graph, so after
+    # the timed replays they hold the last timed step.  Eager fallback if capture fails.
+    graph, graph_err = None, None
+    if args.graph:
+        try:
+            ops.prof_enable(15, 64 * (wl["n_layers"] + 2))
+            n0 = ops.launch_count()
+            graph = stack.capture(inp, group)
+            launches = ops.launch_count() - n0
+            for _ in range(2):
+                graph.replay()
+            torch.cuda.synchronize()
+        except Exception as ex:  # noqa: BLE001
+            graph, graph_err = None, f"{type(ex).__name__}: {ex}"[:200]
+            torch.cuda.synchronize()
+            ops.prof_read()
     clocks = ClockSampler(local, pci)
     clocks.start()
-    ops.prof_enable(15, 64 * (args.steps + 1) * (wl["n_layers"] + 2))
-    n0 = ops.launch_count()
+    if graph is None:
+        ops.prof_enable(15, 64 * (args.steps + 1) * (wl["n_layers"] + 2))
+        n0 = ops.launch_count()
     barrier()
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record()
     for _ in range(args.steps):
-        stack.step(inp, group)
+        if graph is not None:
+            graph.replay()
+        else:
+            stack.step(inp, group)
     ev1.record()
     torch.cuda.synchronize()
     barrier()
-    launches = (ops.launch_count() - n0) // max(1, args.steps)
+    if graph is None:
+        launches = (ops.launch_count() - n0) // max(1, args.steps)
     prof = ops.prof_read()
+    prof_steps = 1 if graph is not None else max(1, args.steps)
     clk = clocks.stop()
     ms = ev0.elapsed_time(ev1) / args.steps
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
@@ -365,18 +389,28 @@ def main():
     e2e = None
     if not args.no_e2e:
         loss_h = torch.zeros(1, dtype=torch.float32).pin_memory()
+        egraph = None
+        if graph is not None:  # H2D of the inputs + step + D2H of the loss, one graph
+            try:
+                egraph = stack.capture(inp, group, host_inp=host_inp, loss_h=loss_h)
+            except Exception:  # noqa: BLE001
+                egraph = None
+
+        def e2e_step():
+            if egraph is not None:
+                egraph.replay()
+            else:
+                inp.copy_(host_inp)
+                stack.step(inp, group)
+                loss_h.copy_(stack.loss, non_blocking=True)
         for _ in range(2):
-            inp.copy_(host_inp)
-            stack.step(inp, group)
-            loss_h.copy_(stack.loss, non_blocking=True)
+            e2e_step()
         torch.cuda.synchronize()
         barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         for _ in range(args.steps):
-            inp.copy_(host_inp)
-            stack.step(inp, group)
-            loss_h.copy_(stack.loss, non_blocking=True)
+            e2e_step()
         e1.record()
         torch.cuda.synchronize()
         barrier()
@@ -395,7 +429,7 @@ def main():
 
     # ---------------- roofline of the dominant kernel class (live CUDA-event times)
     peaks, peak_src = load_peaks()
-    per_step_ms = {k: v[0] / max(1, args.steps) for k, v in prof.items()}
+    per_step_ms = {k: v[0] / prof_steps for k, v in prof.items()}
     dom = max(("gemm", "attn_fwd", "attn_bwd"), key=lambda k: per_step_ms[k])
     achieved = flops[dom] / (per_step_ms[dom] / 1000.0) / 1e12 if per_step_ms[dom] > 0 else 0.0
     peak = float(peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops")))
@@ -410,7 +444,7 @@ def main():
                 "traffic_source": traffic_src,
                 "peak_source": f"{peak_src} bf16_tflops_sustained (kernel timed inside a long step)",
                 "share_of_step": per_step_ms[dom] / ms, "per_class_ms_per_step": per_step_ms,
-                "launches_per_step": {k: v[1] / max(1, args.steps) for k, v in prof.items()}}
+                "launches_per_step": {k: v[1] / prof_steps for k, v in prof.items()}}
     cpu = None
     if not args.no_cpu and world == 1:
         v, tokc, dt, desc = time_oracle(users, wl, 0)
@@ -432,6 +466,7 @@ def main():
         "frac_of_peak_spec": tflops_all / world / 2250.0,
         "flops_per_step_per_rank": flops,
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
+        "cuda_graph": graph is not None, "cuda_graph_error": graph_err,
     }
     print(json.dumps(out))
     if group is not None:

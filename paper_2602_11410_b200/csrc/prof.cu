@@ -18,19 +18,30 @@ int g_used = 0;
 
 void note_launches(int n) { g_launches += n; }
 
+// Inside stream capture a plain cudaEventRecord only adds a capture dependency; an external
+// event-record node is needed for the event to be re-recorded by every graph replay.
+static void record(cudaEvent_t ev, cudaStream_t st) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(st, &cs);
+  if (cs == cudaStreamCaptureStatusActive)
+    cudaEventRecordWithFlags(ev, st, cudaEventRecordExternal);
+  else
+    cudaEventRecord(ev, st);
+}
+
 int prof_begin(int cls, cudaStream_t st) {
   if (!g_classes) return -1;
   std::lock_guard<std::mutex> lk(g_mu);
   if (!(g_classes & (1 << cls)) || g_used >= g_max) return -1;
   const int slot = g_used++;
   g_cls[slot] = cls;
-  cudaEventRecord(g_ev[2 * slot], st);
+  record(g_ev[2 * slot], st);
   return slot;
 }
 
 void prof_end(int slot, cudaStream_t st) {
   if (slot < 0) return;
-  cudaEventRecord(g_ev[2 * slot + 1], st);
+  record(g_ev[2 * slot + 1], st);
 }
 }  // namespace cadet
 

@@ -325,6 +325,21 @@ class CadetStack:
             torch.distributed.all_reduce(self.loss, group=group)
         return self.loss
 
+    def capture(self, inp: StepInputs, group=None, host_inp: StepInputs | None = None, loss_h=None):
+        """CUDA graph of one whole step: every libcadet launch (and, with host_inp / loss_h, the H2D
+        copy of the step's inputs from pinned memory and the D2H of the loss) becomes a graph node,
+        replayed with no host work.  Kernel arguments, TMA descriptors included, are copied into
+        the nodes at capture, so replays see the same buffers; call step() once first so that
+        every buffer is sized."""
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            if host_inp is not None:
+                inp.copy_(host_inp)
+            self.step(inp, group)
+            if loss_h is not None:
+                loss_h.copy_(self.loss, non_blocking=True)
+        return g
+
     def pairs(self, inp: StepInputs) -> int:
         """Allowed (i, j) pairs of the planned mask (head-independent), from the plan's export hook."""
         self.step(inp, backward=False)
