@@ -1,0 +1,179 @@
+"""Full-size parity in the launch configuration bench.py times (BASELINE.json configs[3] = C4, the
+bench workload, through CadetStack exactly as bench.py steps it; configs[1] = C2 serving, forward
+only with candidate rows).  Sequences are independent (no attention crosses cu_seqlens),
+so the fp64 oracle checks whole sampled sequences one at a time: the layer output, the input
+gradient dX and the tower logits of those sequences (C2: every sequence).  Weight gradients sum
+over all sequences and are covered at oracle-sized shapes in test_gpu_layer.py."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+from oracle import cadet_oracle as O
+from synth import generator as G
+from tests.helpers import (assert_close, assert_close_stored, bf16_half_ulp, bf16_tensor, err_stats, make_case,
+                           to_dev_batch, to_np)
+from tests.test_gpu_core import meta_of, oracle_cfg
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def c4():
+    import bench
+    from paper_2602_11410_b200 import build
+    from paper_2602_11410_b200.model import CadetStack, StackConfig
+    build.build()
+    wl = bench.WORKLOADS["c4"]
+    users, hinp = bench.build_inputs(wl, 0, pin=False)
+    inp = hinp.to("cuda")
+    st = CadetStack(StackConfig(d_model=wl["d_model"], n_heads=wl["n_heads"], n_layers=wl["n_layers"],
+                                budget=wl["budget"], L_chunk=wl["L_chunk"]), seed=0, device="cuda")
+    st.step(inp)
+    torch.cuda.synchronize()
+    st.poll()
+    cu = st.cu[: inp.n_chunks + 1].cpu().numpy().astype(np.int64)
+    lens = np.diff(cu)
+    order = np.argsort(lens, kind="stable")
+    picks = sorted({int(order[-1]), int(order[0]), int(order[len(order) // 2]), int(order[(3 * len(order)) // 4])})
+    return st, inp, cu, picks
+
+
+def _unit_scale(ref):
+    """Power-of-two factor bringing rms(ref) to ~1 (exact on bf16 values, so the storage-rounding
+    allowance of assert_close_stored scales with it)."""
+    rms = float(np.sqrt(np.mean(np.asarray(ref, np.float64) ** 2)))
+    return 2.0 ** -round(np.log2(rms)) if rms > 0 else 1.0
+
+
+def test_c4_sampled_sequences_forward_backward(c4):
+    """Sampled whole chunks of the C4 bench step vs the fp64 oracle: every forward stage fed the
+    GPU's own previous stage (protocol iii: Zx, Xt, Q, K, V, Zq, Zk, Qr, Kr, O, LSE, the layer
+    output), the attention contribution H1 - H0 end to end from the packed input, and the input
+    gradient dH0 = dH1 + Attn^T(dH1) end to end (flat-regime e2e gates of test_gpu_layer.py; values
+    rescaled to unit rms by a power of two, storage rounding removed)."""
+    from tests.test_gpu_layer import saved_views
+    st, inp, cu, picks = c4
+    T, d, H = st.cfg.budget, st.cfg.d_model, st.cfg.n_heads
+    t = st.t_p.cpu().numpy()
+    s = st.s_p.cpu().numpy()
+    H0, H1 = to_np(st.Hs[0]), to_np(st.Hs[1])
+    dH1, dH0 = to_np(st.dHs[1]), to_np(st.dHs[0])
+    Wl = [to_np(w) for w in st.W[0]]
+    sv = saved_views(st.saved[0], T, d, H)
+    ocfg = oracle_cfg(st.acfg)
+    assert (H1[cu[-1]:] == 0).all() and (dH0[cu[-1]:] == 0).all()
+    for k in picks:
+        a, e = int(cu[k]), int(cu[k + 1])
+        tag = f"seq {k} len {e - a}"
+        meta = meta_of(np.array([0, e - a]), t[a:e], s[a:e], np.zeros(1, np.int64))
+        A = O.seq_mask(meta, 0, ocfg)
+        # stages, each fed the GPU's previous stage
+        Zx = H0[a:e] @ Wl[0]
+        assert_close_stored(sv["Zx"][a:e], Zx, what=f"Zx {tag}")
+        assert_close_stored(sv["Xt"][a:e], H0[a:e] * O.sigmoid(Zx), what=f"Xt {tag}")
+        for nm, Wi in (("Q", Wl[1]), ("K", Wl[2]), ("V", Wl[3])):
+            assert_close_stored(sv[nm][a:e], sv["Xt"][a:e] @ Wi, what=f"{nm} {tag}")
+        for nm, src, Wg, zn in (("Qr", "Q", Wl[4], "Zq"), ("Kr", "K", Wl[5], "Zk")):
+            Z = sv[src][a:e] @ Wg
+            assert_close_stored(sv[zn][a:e], Z, what=f"{zn} {tag}")
+            # the stored Qr / Kr are rotated by times rebased to the sequence start (R21:
+            # scores depend only on differences); the oracle stage gets the same rebased times
+            assert_close_stored(sv[nm][a:e], O.rope_heads(sv[src][a:e] * O.sigmoid(Z), t[a:e] - t[a], ocfg),
+                                what=f"{nm} {tag}")
+        o, l, _ = O.attention_core_forward(sv["Qr"][a:e], sv["Kr"][a:e], sv["V"][a:e], A, H)
+        assert_close_stored(sv["O"][a:e], o, what=f"O {tag}")
+        assert_close(sv["lse"][:, a:e], l, what=f"LSE {tag}")
+        assert_close_stored(H1[a:e], H0[a:e] + sv["O"][a:e] @ Wl[6], what=f"H1 stage {tag}")
+        # end to end from the packed input: the north-star absolute gates (max 1e-2, mean 1e-3) on the
+        # attention contribution H1 - H0, H1's storage rounding removed (unit-rms figure printed)
+        Y, caches, _ = O.batch_forward(H0[a:e], Wl, meta, ocfg)
+        resid = np.maximum(np.abs((H1[a:e] - H0[a:e]) - Y) - bf16_half_ulp(np.abs(H1[a:e])), 0)
+        mx, mn = float(resid.max()), float(resid.mean())
+        rms = float(np.sqrt(np.mean(Y ** 2)))
+        print(f"C4 {tag}: Attn(H0) e2e abs max {mx:.3e} mean {mn:.3e} (rms {rms:.3e}: rel max {mx / rms:.3e})")
+        assert mx <= 1e-2 and mn <= 1e-3, (tag, mx, mn)
+        dX, _, _ = O.batch_backward(caches, Wl, meta, dH1[a:e], ocfg)
+        ref = dH1[a:e] + dX
+        f = _unit_scale(ref)
+        mx, mn = assert_close_stored(dH0[a:e] * f, ref * f, max_abs=5e-2, mean_abs=5e-3, what=f"dH0 {tag}")
+        print(f"C4 {tag}: dH0 e2e (unit rms) max {mx:.3e} mean {mn:.3e}")
+
+
+def test_c4_tower_logits_sampled(c4):
+    """Towers (A7) at full size: logits of the impression rows of the sampled chunks, oracle fed the
+    GPU's layer output."""
+    st, inp, cu, picks = c4
+    rows = inp.rows.cpu().numpy().astype(np.int64)
+    sel = np.zeros(rows.shape, bool)
+    for k in picks:
+        sel |= (rows >= cu[k]) & (rows < cu[k + 1])
+    assert sel.sum() > 0
+    K, dh = st.cfg.K, st.cfg.dh
+    W1 = to_np(st.W1)
+    W1k = np.stack([W1[:, k * dh:(k + 1) * dh] for k in range(K)])
+    b1 = st.b1.cpu().numpy().astype(np.float64).reshape(K, dh)
+    w2 = st.w2.cpu().numpy().astype(np.float64).reshape(K, dh)
+    b2 = st.b2.cpu().numpy().astype(np.float64)
+    z, _, _ = O.heads_forward(to_np(st.Hs[-1]), rows[sel], W1k, b1, w2, b2)
+    assert_close(st.logits.cpu().numpy()[sel], z, what="C4 logits")
+
+
+def test_c2_serving_forward_all_sequences():
+    """configs[1] (C2 serving): 64 histories of U{448..576} tokens, the last 64 of each are
+    candidates (see all context, Delta_cand = 0; context causal, Delta_ctx = 0: P:533),
+    d 512, 8 heads x 64, one layer forward + towers on the 4,096 candidate rows; every sequence
+    checked against the oracle."""
+    from paper_2602_11410_b200 import _lib as L
+    from paper_2602_11410_b200 import build, ops
+    build.build()
+    rng = np.random.default_rng(2)
+    lens = rng.integers(448, 577, size=64)
+    nc = np.full(64, 64)
+    cu, t, s, ncv, T = make_case(list(lens), n_cand=list(nc), seed=2, stress=False)
+    d, H, K, dh = 512, 8, 2, 256
+    X = G.normal_bf16(2, 1, (T, d))
+    X[cu[-1]:] = 0
+    W = G.layer_weights(2, 0, d)
+    cfg = ops.config(d, H, delta_delay_ms=0, delta_cand_ms=0)
+    b = to_dev_batch(cu, t, s, ncv, T)
+    Xd = bf16_tensor(X)
+    Wd = [bf16_tensor(w) for w in W.as_list()]
+    w = L.AttnWeights(*[x.data_ptr() for x in Wd])
+    lib = L.lib()
+    saved = torch.zeros(lib.cadet_attn_saved_bytes(C.byref(cfg), T), dtype=torch.uint8, device="cuda")
+    ws = ops.workspace(lib.cadet_attn_workspace_bytes(C.byref(cfg), b.n_seqs, T))
+    Y = torch.empty(T, d, dtype=torch.bfloat16, device="cuda")
+    stream = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    L.check(lib.cadet_attn_forward(C.byref(cfg), C.byref(b.struct()), C.byref(w), C.c_void_p(Xd.data_ptr()),
+                                   C.c_void_p(Y.data_ptr()), None, C.c_void_p(saved.data_ptr()),
+                                   C.c_void_p(ws.data_ptr()), ws.numel(), stream))
+    rows = np.concatenate([np.arange(cu[i + 1] - 64, cu[i + 1]) for i in range(64)]).astype(np.int32)
+    hw = G.head_weights(2, K, d, dh)
+    W1cat = np.concatenate([hw.W1[k] for k in range(K)], axis=1)
+    hc = L.HeadConfig(K, d, dh, 0)
+    W1d = bf16_tensor(W1cat)
+    tens = {k: torch.tensor(v, device="cuda") for k, v in dict(b1=hw.b1.reshape(-1), w2=hw.w2.reshape(-1),
+                                                                b2=hw.b2, rows=rows).items()}
+    hwst = L.HeadWeights(W1d.data_ptr(), tens["b1"].data_ptr(), tens["w2"].data_ptr(), tens["b2"].data_ptr())
+    hws = ops.workspace(lib.cadet_heads_workspace_bytes(C.byref(hc), len(rows)))
+    logits = torch.empty(len(rows), K, dtype=torch.float32, device="cuda")
+    pre = torch.empty(len(rows), K * dh, dtype=torch.bfloat16, device="cuda")
+    L.check(lib.cadet_heads_forward(C.byref(hc), C.byref(hwst), C.c_void_p(Y.data_ptr()),
+                                    C.c_void_p(tens["rows"].data_ptr()), len(rows), C.c_void_p(logits.data_ptr()),
+                                    C.c_void_p(pre.data_ptr()), C.c_void_p(hws.data_ptr()), hws.numel(), stream))
+    torch.cuda.synchronize()
+    ops.poll(ws)
+    ops.poll(hws)
+    ocfg = oracle_cfg(cfg)
+    meta = meta_of(cu, t, s, ncv)
+    Yref, _, _ = O.batch_forward(X.astype(np.float64), [x.astype(np.float64) for x in W.as_list()], meta, ocfg)
+    Yg = to_np(Y)
+    mx, mn, rms = err_stats(Yg, Yref)
+    print(f"C2 Y e2e: max {mx:.3e} mean {mn:.3e} rms {rms:.3f}")
+    assert_close_stored(Yg, Yref, what="C2 Y")
+    assert (Yg[cu[-1]:] == 0).all()
+    z, _, _ = O.heads_forward(Yg, rows.astype(np.int64), hw.W1.astype(np.float64), hw.b1.astype(np.float64),
+                              hw.w2.astype(np.float64), hw.b2.astype(np.float64))
+    assert_close(logits.cpu().numpy(), z, what="C2 logits")
