@@ -229,34 +229,48 @@ __device__ __forceinline__ void run_epilogue(const EpiParams& e, int row, int M,
 // Warp-cooperative variants: the 32 lanes hold rows row0 .. row0 + 31 of the same 32 columns
 // (tcgen05.ld 32x32b layout).  Global traffic goes through a per-warp 4 KB swizzled transpose
 // (ptx.cuh) so each load / store instruction covers whole row segments instead of 32 lines.
+// bf16 32 x 32 slice in two phases, so the global loads of a later slice can be issued early:
+// (1) coalesced loads (8 rows x 64 B per instruction) into registers, (2) transpose to this lane's row.
+__device__ __forceinline__ void warp_ldg_rows_bf16(const void* base, size_t off0, size_t ld, int rows_valid,
+                                                   uint4 (&g)[4]) {
+  const uint32_t lane = threadIdx.x & 31;
+  const __nv_bfloat16* b = reinterpret_cast<const __nv_bfloat16*>(base) + off0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int row = i * 8 + (lane >> 2), j = lane & 3;
+    g[i] = row < rows_valid ? *reinterpret_cast<const uint4*>(b + (size_t)row * ld + j * 8) : make_uint4(0, 0, 0, 0);
+  }
+}
+__device__ __forceinline__ void warp_sts_rows_bf16(uint32_t stg, const uint4 (&g)[4], float (&x)[32]) {
+  const uint32_t lane = threadIdx.x & 31;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int row = i * 8 + (lane >> 2), j = lane & 3;
+    sts_u4(stg + row * 64 + ((j ^ ((row >> 1) & 3)) << 4), g[i].x, g[i].y, g[i].z, g[i].w);
+  }
+  __syncwarp();
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const uint4 u = lds_u4(stg + lane * 64 + ((j ^ ((lane >> 1) & 3)) << 4));
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float2 f = __bfloat1622float2(h[e]);
+      x[j * 8 + e * 2] = f.x;
+      x[j * 8 + e * 2 + 1] = f.y;
+    }
+  }
+  __syncwarp();
+}
+
 __device__ __forceinline__ void warp_load_rows(uint32_t stg, const void* base, int is_f32, size_t off0, size_t ld,
                                                int rows_valid, float (&x)[32]) {
   const uint32_t lane = threadIdx.x & 31;
   if (!is_f32) {
-    const __nv_bfloat16* b = reinterpret_cast<const __nv_bfloat16*>(base) + off0;
     uint4 g[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int row = i * 8 + (lane >> 2), j = lane & 3;
-      g[i] = row < rows_valid ? *reinterpret_cast<const uint4*>(b + (size_t)row * ld + j * 8) : make_uint4(0, 0, 0, 0);
-    }
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int row = i * 8 + (lane >> 2), j = lane & 3;
-      sts_u4(stg + row * 64 + ((j ^ ((row >> 1) & 3)) << 4), g[i].x, g[i].y, g[i].z, g[i].w);
-    }
-    __syncwarp();
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const uint4 u = lds_u4(stg + lane * 64 + ((j ^ ((lane >> 1) & 3)) << 4));
-      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const float2 f = __bfloat1622float2(h[e]);
-        x[j * 8 + e * 2] = f.x;
-        x[j * 8 + e * 2 + 1] = f.y;
-      }
-    }
+    warp_ldg_rows_bf16(base, off0, ld, rows_valid, g);
+    warp_sts_rows_bf16(stg, g, x);
+    return;
   } else {
     const float* b = reinterpret_cast<const float*>(base) + off0;
     uint4 g[8];
@@ -297,8 +311,25 @@ __device__ __forceinline__ void warp_store_rows(uint32_t stg, void* base, int is
   }
 }
 
+// Primary epilogue input (bf16 only), loaded one slice ahead by the epilogue loop: src for the
+// gates, resid for a store, aux (the saved pre-activation) for the gate backward.
+__device__ __forceinline__ const void* epi_primary(const EpiParams& e) {
+  if (e.row_map) return nullptr;
+  switch (e.mode) {
+    case EPI_GATE:
+    case EPI_GATE_ROPE:
+      return e.src;
+    case EPI_STORE:
+      return e.resid_f32 ? nullptr : e.resid;
+    case EPI_GATE_BWD:
+      return e.aux_f32 ? nullptr : e.aux;
+    default:
+      return nullptr;
+  }
+}
+
 __device__ __forceinline__ void run_epilogue_warp(const EpiParams& e, int row0, int M, int n0c, float (&v)[32],
-                                                  uint32_t stg) {
+                                                  uint32_t stg, const uint4* pre = nullptr) {
   const int lane = threadIdx.x & 31;
   if (e.row_map || e.mode == EPI_ATOMIC || e.mode == EPI_HEAD) {
     run_epilogue(e, row0 + lane, M, n0c, v);
@@ -311,7 +342,10 @@ __device__ __forceinline__ void run_epilogue_warp(const EpiParams& e, int row0, 
     case EPI_STORE: {
       if (e.resid) {
         float r[32];
-        warp_load_rows(stg, e.resid, e.resid_f32, off0, e.ldo, rows_valid, r);
+        if (pre)
+          warp_sts_rows_bf16(stg, *reinterpret_cast<const uint4(*)[4]>(pre), r);
+        else
+          warp_load_rows(stg, e.resid, e.resid_f32, off0, e.ldo, rows_valid, r);
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] += r[j];
       }
@@ -321,7 +355,10 @@ __device__ __forceinline__ void run_epilogue_warp(const EpiParams& e, int row0, 
     case EPI_GATE_ROPE: {
       if (e.aux) warp_store_rows(stg, e.aux, e.aux_f32, off0, e.ldo, rows_valid, v);
       float x[32];
-      warp_load_rows(stg, e.src, 0, off0, e.ldo, rows_valid, x);
+      if (pre)
+        warp_sts_rows_bf16(stg, *reinterpret_cast<const uint4(*)[4]>(pre), x);
+      else
+        warp_load_rows(stg, e.src, 0, off0, e.ldo, rows_valid, x);
 #pragma unroll
       for (int j = 0; j < 32; ++j) v[j] = x[j] * __fdividef(1.0f, 1.0f + __expf(-v[j]));
       if (e.mode == EPI_GATE_ROPE) {  // head-local window [n0c % hd, + 32) of the rope table rows
@@ -333,7 +370,10 @@ __device__ __forceinline__ void run_epilogue_warp(const EpiParams& e, int row0, 
     } break;
     case EPI_GATE_BWD: {
       float z[32], x[32], r[32];
-      warp_load_rows(stg, e.aux, e.aux_f32, off0, e.ldo, rows_valid, z);
+      if (pre)
+        warp_sts_rows_bf16(stg, *reinterpret_cast<const uint4(*)[4]>(pre), z);
+      else
+        warp_load_rows(stg, e.aux, e.aux_f32, off0, e.ldo, rows_valid, z);
       warp_load_rows(stg, e.src, 0, off0, e.ldo, rows_valid, x);
       if (e.resid) {
         warp_load_rows(stg, e.resid, e.resid_f32, off0, e.ldo, rows_valid, r);
@@ -393,8 +433,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_kernel(const __grid_cons
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
+  // registers: warpgroup 0 (TMA, MMA, allocator, idle) gives 104 per thread to the epilogue warpgroups
   if (warp == 0) {
     // ============================ TMA producer
+    setmaxnreg_dec<64>();
     if (elect_one()) {
       uint32_t it = 0;
       for (int u = blockIdx.x; u < P.total_units; u += gridDim.x) {
@@ -427,6 +469,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_kernel(const __grid_cons
     }
   } else if (warp == 1) {
     // ============================ MMA issuer
+    setmaxnreg_dec<64>();
     if (elect_one()) {
       uint32_t it = 0, tc = 0;
       for (int u = blockIdx.x; u < P.total_units; u += gridDim.x, ++tc) {
@@ -459,8 +502,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_kernel(const __grid_cons
         mma_commit(&tfull[buf]);
       }
     }
-  } else if (warp >= 4) {
+  } else if (warp < 4) {
+    setmaxnreg_dec<64>();
+  } else {
     // ============================ epilogue
+    setmaxnreg_inc<216>();
     const uint32_t quarter = warp & 3;
     const int half = (warp - 4) >> 2;  // warps 4-7 take even 32-column slices, 8-11 odd ones
     const uint32_t stg = smem_u32(smem + C::STG_OFF) + (warp - 4) * 4096;
@@ -473,16 +519,27 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_kernel(const __grid_cons
       tc_fence_after();
       const int row0 = U.m0 + quarter * 32;
       const int n0 = U.n0 * BN;
+      // the primary epilogue input of slice c + 2 is requested before slice c is processed
+      const void* pb = epi_primary(q.epi);
+      uint4 g[4];
+      auto issue = [&](int c) {
+        const int n0c = n0 + c * 32;
+        if (pb && c < BN / 32 && n0c < q.N && row0 < q.M)
+          warp_ldg_rows_bf16(pb, (size_t)row0 * q.epi.ldo + n0c, q.epi.ldo, q.M - row0, g);
+      };
+      issue(half);
       for (int c = half; c < BN / 32; c += 2) {
         const int n0c = n0 + c * 32;
         if (n0c >= q.N) break;
+        uint4 cur[4] = {g[0], g[1], g[2], g[3]};
+        issue(c + 2);
         uint32_t r[32];
         tmem_ld32(tmem_addr(tmem_base, quarter, buf * BN + c * 32), r);
         tmem_ld_wait();
         float v[32];
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-        run_epilogue_warp(q.epi, row0, q.M, n0c, v, stg);
+        run_epilogue_warp(q.epi, row0, q.M, n0c, v, stg, pb ? cur : nullptr);
       }
       tc_fence_before();
       __syncwarp();
@@ -555,6 +612,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
 
   if (warp == 0) {
     // ============================ TMA producer (both CTAs; bytes land on the leader's barrier)
+    setmaxnreg_dec<64>();
     if (elect_one()) {
       uint32_t it = 0;
       for (int u = cid; u < P.total_units; u += ncl) {
@@ -589,6 +647,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
     }
   } else if (warp == 1) {
     // ============================ MMA issuer (leader CTA only)
+    setmaxnreg_dec<64>();
     if (leader && elect_one()) {
       uint32_t it = 0, tc = 0;
       for (int u = cid; u < P.total_units; u += ncl, ++tc) {
@@ -621,8 +680,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
         mma_commit_pair_mc(&tfull[buf], 0x3);
       }
     }
-  } else if (warp >= 4) {
+  } else if (warp < 4) {
+    setmaxnreg_dec<64>();
+  } else {
     // ============================ epilogue (both CTAs: 128 rows x 256 columns each)
+    setmaxnreg_inc<216>();
     const uint32_t quarter = warp & 3;
     const int half = (warp - 4) >> 2;
     const uint32_t stg = smem_u32(smem + C::STG_OFF) + (warp - 4) * 4096;
@@ -636,16 +698,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
       tc_fence_after();
       const int row0 = U.m0 + 128 * (int)rank + quarter * 32;
       const int n0 = U.n0 * BN;
+      // the primary epilogue input of slice c + 2 is requested before slice c is processed
+      const void* pb = epi_primary(q.epi);
+      uint4 g[4];
+      auto issue = [&](int c) {
+        const int n0c = n0 + c * 32;
+        if (pb && c < BN / 32 && n0c < q.N && row0 < q.M)
+          warp_ldg_rows_bf16(pb, (size_t)row0 * q.epi.ldo + n0c, q.epi.ldo, q.M - row0, g);
+      };
+      issue(half);
       for (int c = half; c < BN / 32; c += 2) {
         const int n0c = n0 + c * 32;
         if (n0c >= q.N) break;
+        uint4 cur[4] = {g[0], g[1], g[2], g[3]};
+        issue(c + 2);
         uint32_t r[32];
         tmem_ld32(tmem_addr(tmem_base, quarter, buf * BN + c * 32), r);
         tmem_ld_wait();
         float v[32];
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-        run_epilogue_warp(q.epi, row0, q.M, n0c, v, stg);
+        run_epilogue_warp(q.epi, row0, q.M, n0c, v, stg, pb ? cur : nullptr);
       }
       tc_fence_before();
       __syncwarp();

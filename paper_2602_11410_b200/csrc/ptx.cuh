@@ -265,6 +265,16 @@ CADET_DEV uint32_t swz_off(uint32_t row, uint32_t chunk, uint32_t row_bytes) {
 }
 
 // ------------------------------------------------------------------ small math
+// Warpgroup register reallocation (all 4 warps of a warpgroup execute it).
+template <uint32_t N>
+CADET_DEV void setmaxnreg_dec() {
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(N));
+}
+template <uint32_t N>
+CADET_DEV void setmaxnreg_inc() {
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(N));
+}
+
 CADET_DEV float4 lds_f4(uint32_t saddr) {
   float4 v;
   asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(saddr));
