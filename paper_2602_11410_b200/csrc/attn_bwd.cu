@@ -286,8 +286,17 @@ __global__ void __launch_bounds__(320, 1)
         tmem_ld32(tmem_addr(tmem, quarter, C::DQ_COL + c * 32), u);
         tmem_ld_wait();
         const float f = t.n_kv > 0 ? p.scale : 0.f;
-        warp_store_rows_f32(stg, u, f, p.dQ + (size_t)(t.q0 + quarter * 32) * p.d + (size_t)t.h * p.hd + c * 32,
-                            p.d, t.rows_valid - (int)quarter * 32, min(32, p.hd - c * 32));
+        const size_t off = (size_t)(t.q0 + quarter * 32) * p.d + (size_t)t.h * p.hd + c * 32;
+        if (p.dq_bf16) {
+          uint32_t wv[16];
+#pragma unroll
+          for (int jj = 0; jj < 16; ++jj) wv[jj] = pack_bf16(f * __uint_as_float(u[2 * jj]), f * __uint_as_float(u[2 * jj + 1]));
+          warp_store_rows_bf16(stg, wv, reinterpret_cast<__nv_bfloat16*>(p.dQ) + off, p.d, t.rows_valid - (int)quarter * 32,
+                               min(32, p.hd - c * 32));
+        } else {
+          warp_store_rows_f32(stg, u, f, reinterpret_cast<float*>(p.dQ) + off, p.d, t.rows_valid - (int)quarter * 32,
+                              min(32, p.hd - c * 32));
+        }
       }
       tc_fence_before();
       mbar_arrive(&bars->dq_free);

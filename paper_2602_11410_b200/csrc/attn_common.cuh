@@ -67,7 +67,8 @@ struct AttnParams {
   void* O;           // fwd: O out;  bwd: (unused)
   float* lse;        // fwd out / bwd in  [H, T]
   const float* D;    // bwd: rowsum(dO * O) [H, T]
-  float* dQ;         // bwd: fp32 accumulator [T, d]
+  void* dQ;          // bwd: dQ [T, d], fp32 (core ABI) or bf16 (dq_bf16: the layer path)
+  int32_t dq_bf16;
   void* dK;          // bwd out
   void* dV;          // bwd out
 };

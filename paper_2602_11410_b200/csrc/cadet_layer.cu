@@ -372,10 +372,11 @@ cadet_status cadet_attn_backward(const cadet_attn_config* cfg, const cadet_batch
     p.lse = L.lse;
     p.D = W.D;
     p.dQ = W.dQacc;
+    p.dq_bf16 = 1;  // dQ_r rounded to bf16 like dK_r before R(-alpha) and the gate backward
     p.dK = W.dKr;
     p.dV = W.dV;
     e = attn_bwd_pre_launch(L.O, dO, W.D, W.dQacc, T, H, hd, st);
-    if (e == cudaSuccess) e = zero_pad_rows_launch(W.dQacc, d * 4, T, b->cu_seqlens, n, st);
+    if (e == cudaSuccess) e = zero_pad_rows_launch(W.dQacc, d * 2, T, b->cu_seqlens, n, st);
     if (e == cudaSuccess) e = zero_pad_rows_launch(W.dKr, d * 2, T, b->cu_seqlens, n, st);
     if (e == cudaSuccess) e = zero_pad_rows_launch(W.dV, d * 2, T, b->cu_seqlens, n, st);
     if (e == cudaSuccess) e = attn_bwd_launch(L.Qr, L.Kr, L.V, dO, p, st);
@@ -385,7 +386,7 @@ cadet_status cadet_attn_backward(const cadet_attn_config* cfg, const cadet_batch
   const void* dK = W.dK;
   if (e == cudaSuccess) {
     if (cfg->use_int_gate) {
-      e = rope_gate_bwd_launch(W.dQacc, 1, L.Q, L.Zq, W.uq, W.rq, 1, T, d, hd, cs, st);
+      e = rope_gate_bwd_launch(W.dQacc, 0, L.Q, L.Zq, W.uq, W.rq, 1, T, d, hd, cs, st);
       if (e == cudaSuccess)
         e = rope_gate_bwd_launch(W.dKr, 0, L.K, L.Zk, W.uk, W.rk, 1, T, d, hd, cs, st);
       if (e == cudaSuccess) {  // dQ = rq + uq W_qg^T ; dK = rk + uk W_kg^T
@@ -407,7 +408,7 @@ cadet_status cadet_attn_backward(const cadet_attn_config* cfg, const cadet_batch
         e = gemm_launch(g, 2, bnw, st);
       }
     } else {
-      e = rope_gate_bwd_launch(W.dQacc, 1, nullptr, nullptr, nullptr, W.dQ, 1, T, d, hd, cs, st);
+      e = rope_gate_bwd_launch(W.dQacc, 0, nullptr, nullptr, nullptr, W.dQ, 1, T, d, hd, cs, st);
       if (e == cudaSuccess)
         e = rope_gate_bwd_launch(W.dKr, 0, nullptr, nullptr, nullptr, W.dK, 1, T, d, hd, cs, st);
     }
@@ -431,7 +432,8 @@ cadet_status cadet_attn_backward(const cadet_attn_config* cfg, const cadet_batch
     if (cfg->use_rep_gate) {  // ux = dXt * X * g (1 - g) ; rx = dXt * g (+ dresid)
       g.epi.mode = EPI_GATE_BWD;
       g.epi.out = W.ux;
-      g.epi.out2 = W.rx;
+      g.epi.out2 = W.rx;  // bf16 (like r_q, r_k): rounded once before the bf16 dX it feeds
+      g.epi.out2_f32 = 0;
       g.epi.src = X;
       g.epi.aux = L.Zx;
       g.epi.resid = dresid;
@@ -450,7 +452,7 @@ cadet_status cadet_attn_backward(const cadet_attn_config* cfg, const cadet_batch
       GemmProblem g2 = prob(T, d, d, act(W.ux, T, d), w_bwd(w->W_xg, d, d), EPI_STORE);
       g2.epi.out = dX;
       g2.epi.resid = W.rx;
-      g2.epi.resid_f32 = 1;
+      g2.epi.resid_f32 = 0;
       e = gemm_launch(&g2, 1, bn, st);
       if (e == cudaSuccess) {
         GemmProblem gw = wgrad(X, W.ux, gr->dW_xg, T, d, d, bnw);

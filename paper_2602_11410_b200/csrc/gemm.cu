@@ -194,7 +194,7 @@ __device__ __forceinline__ void run_epilogue(const EpiParams& e, int row, int M,
         r[j] += v[j] * g;
       }
       store_any32(e.out, e.out_f32, off, u);
-      store_any32(e.out2, 1, off, r);
+      store_any32(e.out2, e.out2_f32, off, r);
     } break;
     case EPI_ATOMIC: {
       float* o = reinterpret_cast<float*>(e.out) + off;
@@ -389,7 +389,7 @@ __device__ __forceinline__ void run_epilogue_warp(const EpiParams& e, int row0, 
         r[j] += vj * g;
       }
       warp_store_rows(stg, e.out, e.out_f32, off0, e.ldo, rows_valid, v);
-      warp_store_rows(stg, e.out2, 1, off0, e.ldo, rows_valid, r);
+      warp_store_rows(stg, e.out2, e.out2_f32, off0, e.ldo, rows_valid, r);
     } break;
     default:
       break;

@@ -27,7 +27,8 @@ struct EpiParams {
   const void* resid;
   const void* src;   // bf16
   void* aux;
-  float* out2;
+  void* out2;        // EPI_GATE_BWD second output: fp32 if out2_f32 else bf16
+  int32_t out2_f32;
   const int32_t* row_map;  // optional output-row remap (scatter); < 0 = drop row
   // RoPE (EPI_GATE_ROPE): (cos, sin) table [M][hd + 32] floats, interleaved per frequency
   const float* rope_cs;
