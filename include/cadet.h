@@ -76,9 +76,13 @@ typedef struct {
   int32_t mask_flags;
   int32_t out_f32;   /* core calls: 1 = write O / dQr / dKr / dV as fp32 (parity protocol, SURVEY 8(c) iii) */
   int32_t use_rope, use_rep_gate, use_int_gate, use_out_proj; /* ablation switches (Table 1) */
-  int32_t deterministic; /* reserved, must be 0 (dQ uses fp32 atomics) */
-  int32_t plan_ready;    /* 1 = ws already holds cadet_mask_plan's plan for this batch (same ws, same batch):
-                            the layer/core calls skip re-planning (one plan per step for all layers) */
+  int32_t deterministic; /* reserved, must be 0 (attention fwd/bwd are atomic-free and deterministic; split-K
+                            weight gradients accumulate with fp32 atomics) */
+  int32_t plan_ready;    /* 0 = plan inside the call; 1 = ws already holds cadet_mask_plan's plan for this batch
+                            (same ws, same batch): the layer/core calls skip re-planning (one plan per step for
+                            all layers); 2 = as 1 and ws also holds the RoPE (cos, sin) table, which
+                            cadet_mask_plan builds when given >= cadet_attn_workspace_bytes with use_rope
+                            (one table per step instead of one per layer call) */
   int64_t delta_delay_ms;       /* Delta for context queries, Eq. 6; default 3,600,000 */
   int64_t delta_cand_ms;        /* Delta for candidate queries; default 0 (R11) */
   int64_t rope_delta_t_max_ms;  /* Delta t_max; default 31,536,000,000 = 1 year (R6) */

@@ -669,22 +669,44 @@ __global__ void __launch_bounds__(320, 1)
 }
 
 // D_i = rowsum(dO_i * O_i) per head (FlashAttention preprocess), bf16 inputs, fp32 out [H, T].
+// One warp per row, 16-byte loads (8 columns per lane per 256-column pass); per-head sums by
+// segmented shuffles when hd / 8 lanes is a power of two dividing the pass, else shared atomics.
 __global__ void __launch_bounds__(256) attn_bwd_pre_kernel(const __nv_bfloat16* O, const __nv_bfloat16* dO, float* D,
                                                             int T, int H, int hd) {
-  const int row = blockIdx.x * 8 + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
-  if (row >= T) return;
-  const int d = H * hd;
-  for (int h = 0; h < H; ++h) {
-    float acc = 0.f;
-    for (int c = lane * 2; c < hd; c += 64) {
-      const float2 o = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(O + (size_t)row * d + h * hd + c));
-      const float2 g = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(dO + (size_t)row * d + h * hd + c));
-      acc = fmaf(o.x, g.x, fmaf(o.y, g.y, acc));
+  __shared__ float acc[8][128];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int row = blockIdx.x * 8 + w;
+  const int d = H * hd, lpg = hd / 8;  // lanes per head
+  const bool seg = (lpg & (lpg - 1)) == 0 && lpg <= 32;
+  for (int h = lane; h < H; h += 32) acc[w][h] = 0.f;
+  __syncwarp();
+  if (row < T) {  // warp-uniform: every lane runs every pass (shuffles), lanes past d contribute 0
+    for (int c0 = 0; c0 < d; c0 += 256) {
+      const int c = c0 + lane * 8;
+      const bool valid = c < d;
+      float p = 0.f;
+      if (valid) {
+        const uint4 o = *reinterpret_cast<const uint4*>(O + (size_t)row * d + c);
+        const uint4 g = *reinterpret_cast<const uint4*>(dO + (size_t)row * d + c);
+        const __nv_bfloat162* o2 = reinterpret_cast<const __nv_bfloat162*>(&o);
+        const __nv_bfloat162* g2 = reinterpret_cast<const __nv_bfloat162*>(&g);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float2 a = __bfloat1622float2(o2[e]), b = __bfloat1622float2(g2[e]);
+          p = fmaf(a.x, b.x, fmaf(a.y, b.y, p));
+        }
+      }
+      if (seg) {
+        for (int off = lpg >> 1; off > 0; off >>= 1) p += __shfl_xor_sync(0xffffffffu, p, off);
+        if (valid && (lane & (lpg - 1)) == 0) acc[w][c / hd] += p;  // one lane per head segment
+      } else if (valid) {
+        atomicAdd(&acc[w][c / hd], p);
+      }
     }
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if (lane == 0) D[(size_t)h * T + row] = acc;
   }
+  __syncwarp();
+  if (row < T)
+    for (int h = lane; h < H; h += 32) D[(size_t)h * T + row] = acc[w][h];
 }
 
 bool make_head_map(CUtensorMap* m, const void* ptr, int T, int H, int hd);

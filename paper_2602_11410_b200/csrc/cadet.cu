@@ -135,7 +135,9 @@ cadet_status cadet_mask_plan(const cadet_attn_config* cfg, const cadet_batch* b,
     return fail(CADET_E_WORKSPACE, "workspace %zu < %zu", ws_bytes, plan_bytes(b->n_seqs, b->total_tokens, b->total_tokens));
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   PlanView v = plan_carve(ws, b->n_seqs, b->total_tokens, b->total_tokens);
-  return cuda_check(plan_launch(plan_args(cfg, b), v, st), "mask plan");
+  cudaError_t e = plan_launch(plan_args(cfg, b), v, st);
+  if (e == cudaSuccess) e = layer_plan_extras(cfg, b, ws, ws_bytes, st);  // RoPE table (plan_ready = 2)
+  return cuda_check(e, "mask plan");
 }
 
 cadet_status cadet_mask_export(const cadet_attn_config* cfg, const cadet_batch* b, const void* ws, int32_t* kv_end,

@@ -168,6 +168,16 @@ LayerWs carve_ws(void* ws, const cadet_attn_config* c, int n, int T) {
   return W;
 }
 
+// theta_i and the per-step (cos, sin) table (rope_table_kernel) into the layer workspace.
+cudaError_t rope_prepare(const cadet_attn_config* cfg, const cadet_batch* b, const LayerWs& W, const PlanView& v,
+                         cudaStream_t st) {
+  const int hd = cfg->head_dim;
+  cudaError_t e = rope_theta_launch(W.theta, hd, cfg->rope_phi_min, cfg->rope_base, (double)cfg->rope_delta_t_max_ms, st);
+  if (e == cudaSuccess && cfg->use_rope)
+    e = rope_table_launch(W.rope_cs, b->total_tokens, hd, W.theta, b->timestamps_ms, v.row_seq, b->cu_seqlens, st);
+  return e;
+}
+
 int pick_bn(int M, int N) {
   if (N % 256 == 0 && (long long)((M + 127) / 128) * (N / 256) >= 148) return 256;
   if (N <= 128) return 128;
@@ -247,9 +257,7 @@ cadet_status cadet_attn_forward(const cadet_attn_config* cfg, const cadet_batch*
   PlanView v = plan_carve(ws, n, T, T);
   LayerBufs L = carve_saved(saved, cfg, T);
   LayerWs W = carve_ws(ws, cfg, n, T);
-  cudaError_t e = rope_theta_launch(W.theta, hd, cfg->rope_phi_min, cfg->rope_base, (double)cfg->rope_delta_t_max_ms, st);
-  if (e == cudaSuccess && cfg->use_rope)
-    e = rope_table_launch(W.rope_cs, T, hd, W.theta, b->timestamps_ms, v.row_seq, b->cu_seqlens, st);
+  cudaError_t e = cfg->plan_ready >= 2 ? cudaSuccess : rope_prepare(cfg, b, W, v, st);
   const int bn = pick_bn(T, d);
   // A2: representation gate  Xt = X * sigma(X W_xg)   (Eq. 4)
   const void* Xt = X;
@@ -345,9 +353,7 @@ cadet_status cadet_attn_backward(const cadet_attn_config* cfg, const cadet_batch
   const int bn = pick_bn(T, d);
   const int bnw = pick_bn_wgrad(d);
   const size_t wbytes = (size_t)d * d * 4;
-  cudaError_t e = rope_theta_launch(W.theta, hd, cfg->rope_phi_min, cfg->rope_base, (double)cfg->rope_delta_t_max_ms, st);
-  if (e == cudaSuccess && cfg->use_rope)
-    e = rope_table_launch(W.rope_cs, T, hd, W.theta, b->timestamps_ms, v.row_seq, b->cu_seqlens, st);
+  cudaError_t e = cfg->plan_ready >= 2 ? cudaSuccess : rope_prepare(cfg, b, W, v, st);
   const float* cs = cfg->use_rope ? W.rope_cs : nullptr;
   float* gws[7] = {gr->dW_xg, gr->dW_q, gr->dW_k, gr->dW_v, gr->dW_qg, gr->dW_kg, gr->dW_o};
   for (int i = 0; i < 7 && e == cudaSuccess; ++i)
@@ -582,3 +588,16 @@ cadet_status cadet_heads_loss_backward(const cadet_head_config* h, const cadet_h
 }
 
 }  // extern "C"
+
+namespace cadet {
+// cadet_mask_plan's extension (plan_ready = 2): with a layer-sized workspace also build the
+// per-step RoPE table, so the layer calls of the step skip it.
+cudaError_t layer_plan_extras(const cadet_attn_config* cfg, const cadet_batch* b, void* ws, size_t ws_bytes,
+                              cudaStream_t st) {
+  if (!cfg->use_rope || ws_bytes < layer_ws_bytes(cfg, b->n_seqs, b->total_tokens) || b->total_tokens == 0)
+    return cudaSuccess;
+  PlanView v = plan_carve(ws, b->n_seqs, b->total_tokens, b->total_tokens);
+  LayerWs W = carve_ws(ws, cfg, b->n_seqs, b->total_tokens);
+  return rope_prepare(cfg, b, W, v, st);
+}
+}  // namespace cadet

@@ -16,4 +16,6 @@ cudaError_t attn_bwd_launch(const void* Qr, const void* Kr, const void* V, const
                             cudaStream_t st);
 cudaError_t attn_bwd_pre_launch(const void* O, const void* dO, float* D, float* dQacc, int T, int H, int hd,
                                 cudaStream_t st);
+cudaError_t layer_plan_extras(const cadet_attn_config* cfg, const cadet_batch* b, void* ws, size_t ws_bytes,
+                              cudaStream_t st);
 }  // namespace cadet

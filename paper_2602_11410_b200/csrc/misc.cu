@@ -184,40 +184,64 @@ __global__ void head_dz_kernel(const float* logits, const int32_t* bucket, const
 }
 
 // dhid[i, c] = dz_i * w2[c] * 1[pre > 0] on the realised tower, 0 elsewhere (S:260 isolation);
-// column sums db1[c] += dhid, dw2[c] += dz_i * relu(pre[i, c]).  Block = 32 columns x 8 row-groups.
-__global__ void head_dhid_kernel(const __nv_bfloat16* pre, const float* dz, const int32_t* bucket, const float* w2,
-                                 int n, int K, int dh, __nv_bfloat16* dhid, __nv_bfloat16* dhid_lo, float* db1,
-                                 float* dw2) {
+// column sums db1[c] += dhid, dw2[c] += dz_i * relu(pre[i, c]).  Thread = 8 consecutive columns
+// (one tower: dh % 8 == 0) with 16-byte accesses; block = 32 x 8 threads (256 columns x 8 row
+// groups), rows strided over blockIdx.y.
+__global__ void __launch_bounds__(256) head_dhid_kernel(const __nv_bfloat16* pre, const float* dz, const int32_t* bucket,
+                                                        const float* w2, int n, int K, int dh, __nv_bfloat16* dhid,
+                                                        __nv_bfloat16* dhid_lo, float* db1, float* dw2) {
   const int N = K * dh;
-  const int c = blockIdx.x * 32 + threadIdx.x;
-  const int k = c / dh;
-  float s1 = 0.f, s2 = 0.f;
-  if (c < N) {
-    const float w = w2[c];
+  const int c0 = (blockIdx.x * 32 + threadIdx.x) * 8;
+  float s1[8], s2[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) s1[e] = s2[e] = 0.f;
+  if (c0 < N) {
+    const int k = c0 / dh;
+    float w[8];
+    const float4 wa = *reinterpret_cast<const float4*>(w2 + c0), wb = *reinterpret_cast<const float4*>(w2 + c0 + 4);
+    w[0] = wa.x, w[1] = wa.y, w[2] = wa.z, w[3] = wa.w, w[4] = wb.x, w[5] = wb.y, w[6] = wb.z, w[7] = wb.w;
     for (int i = blockIdx.y * blockDim.y + threadIdx.y; i < n; i += gridDim.y * blockDim.y) {
       const int b = min(max(bucket[i], 0), K - 1);
-      const float pr = __bfloat162float(pre[(size_t)i * N + c]);
-      float gv = 0.f;
+      uint32_t hi[4] = {0, 0, 0, 0}, lo[4] = {0, 0, 0, 0};
       if (b == k) {
         const float z = dz[i];
-        gv = pr > 0.f ? z * w : 0.f;
-        s2 += z * fmaxf(pr, 0.f);
+        const uint4 pu = *reinterpret_cast<const uint4*>(pre + (size_t)i * N + c0);
+        const __nv_bfloat162* p2 = reinterpret_cast<const __nv_bfloat162*>(&pu);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float2 pr = __bfloat1622float2(p2[e]);
+          const float g0 = pr.x > 0.f ? z * w[2 * e] : 0.f, g1 = pr.y > 0.f ? z * w[2 * e + 1] : 0.f;
+          s1[2 * e] += g0;
+          s1[2 * e + 1] += g1;
+          s2[2 * e] += z * fmaxf(pr.x, 0.f);
+          s2[2 * e + 1] += z * fmaxf(pr.y, 0.f);
+          // bf16 hi + lo split: the GEMM operand keeps ~16 bits (R27)
+          const __nv_bfloat162 h = __floats2bfloat162_rn(g0, g1);
+          const float2 hf = __bfloat1622float2(h);
+          const __nv_bfloat162 l = __floats2bfloat162_rn(g0 - hf.x, g1 - hf.y);
+          hi[e] = *reinterpret_cast<const uint32_t*>(&h);
+          lo[e] = *reinterpret_cast<const uint32_t*>(&l);
+        }
       }
-      s1 += gv;
-      const __nv_bfloat16 hi = __float2bfloat16(gv);  // bf16 hi + lo split: the GEMM operand keeps ~16 bits
-      dhid[(size_t)i * N + c] = hi;
-      dhid_lo[(size_t)i * N + c] = __float2bfloat16(gv - __bfloat162float(hi));
+      *reinterpret_cast<uint4*>(dhid + (size_t)i * N + c0) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+      *reinterpret_cast<uint4*>(dhid_lo + (size_t)i * N + c0) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
     }
   }
-  __shared__ float sh1[8][33], sh2[8][33];
-  sh1[threadIdx.y][threadIdx.x] = s1;
-  sh2[threadIdx.y][threadIdx.x] = s2;
+  __shared__ float sh1[8][257], sh2[8][257];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    sh1[threadIdx.y][threadIdx.x * 8 + e] = s1[e];
+    sh2[threadIdx.y][threadIdx.x * 8 + e] = s2[e];
+  }
   __syncthreads();
-  if (threadIdx.y == 0 && c < N) {
+  // 256 threads reduce the 256 columns over the 8 row groups
+  const int t = threadIdx.y * 32 + threadIdx.x;
+  const int c = blockIdx.x * 256 + t;
+  if (c < N) {
     float a = 0.f, b = 0.f;
-    for (int y = 0; y < blockDim.y; ++y) {
-      a += sh1[y][threadIdx.x];
-      b += sh2[y][threadIdx.x];
+    for (int y = 0; y < 8; ++y) {
+      a += sh1[y][t];
+      b += sh2[y][t];
     }
     atomicAdd(db1 + c, a);
     atomicAdd(dw2 + c, b);
@@ -293,7 +317,7 @@ cudaError_t head_dhid_launch(const void* pre, const float* dz, const int32_t* bu
   ProfScope ps(PROF_OTHER, st, 1);
   if (n > 0) {
     dim3 blk(32, 8);
-    dim3 grd((K * dh + 31) / 32, (unsigned)min(64, (n + 7) / 8));
+    dim3 grd((K * dh + 255) / 256, (unsigned)min(128, (n + 7) / 8));
     head_dhid_kernel<<<grd, blk, 0, st>>>(reinterpret_cast<const __nv_bfloat16*>(pre), dz, bucket, w2, n, K, dh,
                                           reinterpret_cast<__nv_bfloat16*>(dhid),
                                           reinterpret_cast<__nv_bfloat16*>(dhid_lo), db1, dw2);

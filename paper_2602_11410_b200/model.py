@@ -285,10 +285,11 @@ class CadetStack:
                             _vp(self.n_out), C.c_void_p(self.small_ws.data_ptr() + 256), st))
         b = self.batch(inp).struct()
         ws, wsn = _vp(self._ws), self._ws.numel()
-        # A1: one mask plan per step, shared by every layer's forward and backward
+        # A1: one mask plan per step, shared by every layer's forward and backward; with the layer-sized
+        # workspace the plan call also builds the step's RoPE (cos, sin) table (plan_ready = 2)
         self.acfg.plan_ready = 0
         chk(lib.cadet_mask_plan(C.byref(self.acfg), C.byref(b), ws, wsn, st))
-        self.acfg.plan_ready = 1
+        self.acfg.plan_ready = 2
         # A1-A6: residual layers  H[l+1] = H[l] + Attn(H[l])
         for l in range(cfg.n_layers):
             w = L.AttnWeights(*[x.data_ptr() for x in self.W[l]])
