@@ -224,6 +224,20 @@ GemmProblem wgrad(const void* A, const void* G, float* dW, int T, int din, int d
   return g;
 }
 
+// Two independent groups of GEMMs (e.g. an input gradient and the weight gradient that shares its
+// operand) as ONE persistent launch when they use the same N tile: one ramp-up / tail instead of two.
+cudaError_t gemm_launch2(const GemmProblem* a, int na, int bna, const GemmProblem* b, int nb, int bnb,
+                         cudaStream_t st) {
+  if (bna == bnb && na + nb <= GEMM_MAX_PROB) {
+    GemmProblem g[GEMM_MAX_PROB];
+    for (int i = 0; i < na; ++i) g[i] = a[i];
+    for (int i = 0; i < nb; ++i) g[na + i] = b[i];
+    return gemm_launch(g, na + nb, bna, st);
+  }
+  cudaError_t e = gemm_launch(a, na, bna, st);
+  return e == cudaSuccess ? gemm_launch(b, nb, bnb, st) : e;
+}
+
 }  // namespace
 
 extern "C" {
@@ -364,11 +378,8 @@ cadet_status cadet_attn_backward(const cadet_attn_config* cfg, const cadet_batch
   if (e == cudaSuccess && cfg->use_out_proj) {
     GemmProblem g = prob(T, d, d, act(dY, T, d), w_bwd(w->W_o, d, d), EPI_STORE);
     g.epi.out = W.dO;
-    e = gemm_launch(&g, 1, bn, st);
-    if (e == cudaSuccess) {
-      GemmProblem gw = wgrad(L.O, dY, gr->dW_o, T, d, d, bnw);
-      e = gemm_launch(&gw, 1, bnw, st);
-    }
+    GemmProblem gw = wgrad(L.O, dY, gr->dW_o, T, d, d, bnw);
+    e = gemm_launch2(&g, 1, bn, &gw, 1, bnw, st);
     dO = W.dO;
   }
   // A10: attention core backward
@@ -407,11 +418,9 @@ cadet_status cadet_attn_backward(const cadet_attn_config* cfg, const cadet_batch
           g[i].epi.resid = rs[i];
           g[i].epi.resid_f32 = 0;
         }
-        e = gemm_launch(g, 2, bn, st);
-      }
-      if (e == cudaSuccess) {  // dW_qg = Q^T uq ; dW_kg = K^T uk
-        GemmProblem g[2] = {wgrad(L.Q, W.uq, gr->dW_qg, T, d, d, bnw), wgrad(L.K, W.uk, gr->dW_kg, T, d, d, bnw)};
-        e = gemm_launch(g, 2, bnw, st);
+        // dW_qg = Q^T uq ; dW_kg = K^T uk share the u operands: same launch
+        GemmProblem gw[2] = {wgrad(L.Q, W.uq, gr->dW_qg, T, d, d, bnw), wgrad(L.K, W.uk, gr->dW_kg, T, d, d, bnw)};
+        e = gemm_launch2(g, 2, bn, gw, 2, bnw, st);
       }
     } else {
       e = rope_gate_bwd_launch(W.dQacc, 0, nullptr, nullptr, nullptr, W.dQ, 1, T, d, hd, cs, st);
@@ -448,22 +457,18 @@ cadet_status cadet_attn_backward(const cadet_attn_config* cfg, const cadet_batch
       g.epi.out = dX;
       g.epi.resid = dresid;
     }
-    e = gemm_launch(&g, 1, bn, st);
-    if (e == cudaSuccess) {
+    {  // with the weight gradients of W_q, W_k, W_v (same dQ, dK, dV operands) in one launch
       GemmProblem gw[3] = {wgrad(Xt, dQ, gr->dW_q, T, d, d, bnw), wgrad(Xt, dK, gr->dW_k, T, d, d, bnw),
                            wgrad(Xt, W.dV, gr->dW_v, T, d, d, bnw)};
-      e = gemm_launch(gw, 3, bnw, st);
+      e = gemm_launch2(&g, 1, bn, gw, 3, bnw, st);
     }
     if (e == cudaSuccess && cfg->use_rep_gate) {  // dX = rx + ux W_xg^T ; dW_xg = X^T ux
       GemmProblem g2 = prob(T, d, d, act(W.ux, T, d), w_bwd(w->W_xg, d, d), EPI_STORE);
       g2.epi.out = dX;
       g2.epi.resid = W.rx;
       g2.epi.resid_f32 = 0;
-      e = gemm_launch(&g2, 1, bn, st);
-      if (e == cudaSuccess) {
-        GemmProblem gw = wgrad(X, W.ux, gr->dW_xg, T, d, d, bnw);
-        e = gemm_launch(&gw, 1, bnw, st);
-      }
+      GemmProblem gw = wgrad(X, W.ux, gr->dW_xg, T, d, d, bnw);
+      e = gemm_launch2(&g2, 1, bn, &gw, 1, bnw, st);
     }
   }
   if (e == cudaSuccess) e = zero_pad_rows_launch(dX, d * 2, T, b->cu_seqlens, n, st);
@@ -561,19 +566,16 @@ cadet_status cadet_heads_loss_backward(const cadet_head_config* h, const cadet_h
   if (e == cudaSuccess) e = head_dz_launch(logits, bucket, label, n, h->K, dz, loss_sum, gr->db2, err, st);
   if (e == cudaSuccess) e = head_dhid_launch(pre, dz, bucket, w->w2, n, h->K, h->d_hidden, dhid, dhid_lo, gr->db1, gr->dw2, st);
   if (e == cudaSuccess) e = gather_rows_launch(Hs, rows, n, T, d, Hr, err, st);
-  if (e == cudaSuccess) {  // dW1 = H_r^T (dhid_hi + dhid_lo)
+  if (e == cudaSuccess) {  // dW1 = H_r^T (dhid_hi + dhid_lo) and dHs[rows] = (dhid_hi + dhid_lo) W1^T: one launch
     const int bnw = pick_bn_wgrad(N);
-    GemmProblem g = prob(d, N, n, act_t(Hr, n, d), act_t(dhid, n, N), EPI_ATOMIC);
-    g.nseg = 2;
-    g.K[1] = n;
-    g.A[1] = act_t(Hr, n, d);
-    g.B[1] = act_t(dhid_lo, n, N);
-    g.split_k = pick_split(d, N, bnw, n);
-    g.epi.out = gr->dW1;
-    g.epi.out_f32 = 1;
-    e = gemm_launch(&g, 1, bnw, st);
-  }
-  if (e == cudaSuccess) {  // dHs[rows] = (dhid_hi + dhid_lo) W1^T
+    GemmProblem gw = prob(d, N, n, act_t(Hr, n, d), act_t(dhid, n, N), EPI_ATOMIC);
+    gw.nseg = 2;
+    gw.K[1] = n;
+    gw.A[1] = act_t(Hr, n, d);
+    gw.B[1] = act_t(dhid_lo, n, N);
+    gw.split_k = pick_split(d, N, bnw, n);
+    gw.epi.out = gr->dW1;
+    gw.epi.out_f32 = 1;
     GemmProblem g = prob(n, d, N, act(dhid, n, N), w_bwd(w->W1, d, N), EPI_STORE);
     g.nseg = 2;
     g.K[1] = N;
@@ -582,7 +584,7 @@ cadet_status cadet_heads_loss_backward(const cadet_head_config* h, const cadet_h
     g.epi.out = dHs;
     g.epi.ldo = d;
     g.epi.row_map = rows;
-    e = gemm_launch(&g, 1, pick_bn(n, d), st);
+    e = gemm_launch2(&g, 1, pick_bn(n, d), &gw, 1, bnw, st);
   }
   return cuda_err(e, "heads backward");
 }

@@ -44,7 +44,7 @@ struct OperandDesc {
   int32_t mn_major; // 0: storage is [MN][K] (K-major); 1: storage is [K][MN] (MN-major)
 };
 
-constexpr int GEMM_MAX_PROB = 3;
+constexpr int GEMM_MAX_PROB = 4;
 constexpr int GEMM_MAX_SEG = 3;
 
 struct GemmProblem {
