@@ -82,6 +82,12 @@ __device__ __forceinline__ void kb_to_seg(const KProb& q, int kb, int& seg, int&
 }
 
 // ---------------------------------------------------------------- epilogue helpers
+// Epilogue mode sets (compile time): each GEMM launch instantiates only the epilogues of its
+// problems, so e.g. a plain store does not carry the gate + RoPE epilogue's registers.
+__host__ __device__ constexpr uint32_t MB(int m) { return 1u << m; }
+constexpr uint32_t MODES_ALL = MB(EPI_STORE) | MB(EPI_GATE) | MB(EPI_GATE_ROPE) | MB(EPI_GATE_BWD) | MB(EPI_ATOMIC) |
+                               MB(EPI_HEAD);
+#define HAS_MODE(m) ((MODES & MB(m)) != 0u)
 __device__ __forceinline__ void load_bf16x32(const void* base, float (&x)[32]) {
   const uint4* p = reinterpret_cast<const uint4*>(base);
 #pragma unroll
@@ -142,6 +148,7 @@ __device__ __forceinline__ void rope_rotate32(float (&v)[32], const float (&cs)[
   }
 }
 
+template <uint32_t MODES>
 __device__ __forceinline__ void run_epilogue(const EpiParams& e, int row, int M, int n0c, float (&v)[32]) {
   if (row >= M) return;
   int orow = row;
@@ -152,7 +159,7 @@ __device__ __forceinline__ void run_epilogue(const EpiParams& e, int row, int M,
   const size_t off = (size_t)orow * e.ldo + n0c;
   const size_t in_off = (size_t)row * e.ldo + n0c;
   switch (e.mode) {
-    case EPI_STORE: {
+    case EPI_STORE: if constexpr (HAS_MODE(EPI_STORE)) {
       if (e.resid) {
         float r[32];
         load_any32(e.resid, e.resid_f32, in_off, r);
@@ -162,20 +169,20 @@ __device__ __forceinline__ void run_epilogue(const EpiParams& e, int row, int M,
       store_any32(e.out, e.out_f32, off, v);
     } break;
     case EPI_GATE:
-    case EPI_GATE_ROPE: {
+    case EPI_GATE_ROPE: if constexpr (HAS_MODE(EPI_GATE) || HAS_MODE(EPI_GATE_ROPE)) {
       if (e.aux) store_any32(e.aux, e.aux_f32, in_off, v);
       float x[32];
       load_bf16x32(reinterpret_cast<const __nv_bfloat16*>(e.src) + in_off, x);
 #pragma unroll
       for (int j = 0; j < 32; ++j) v[j] = x[j] * __fdividef(1.0f, 1.0f + __expf(-v[j]));
-      if (e.mode == EPI_GATE_ROPE) {
+      if (HAS_MODE(EPI_GATE_ROPE) && e.mode == EPI_GATE_ROPE) {
         float cs[32];
         load_f32x32(e.rope_cs + (size_t)row * (e.hd + 32) + (n0c % e.hd), cs);
         rope_rotate32(v, cs);
       }
       store_any32(e.out, e.out_f32, off, v);
     } break;
-    case EPI_GATE_BWD: {
+    case EPI_GATE_BWD: if constexpr (HAS_MODE(EPI_GATE_BWD)) {
       float z[32], x[32];
       load_any32(e.aux, e.aux_f32, in_off, z);
       load_bf16x32(reinterpret_cast<const __nv_bfloat16*>(e.src) + in_off, x);
@@ -196,13 +203,13 @@ __device__ __forceinline__ void run_epilogue(const EpiParams& e, int row, int M,
       store_any32(e.out, e.out_f32, off, u);
       store_any32(e.out2, e.out2_f32, off, r);
     } break;
-    case EPI_ATOMIC: {
+    case EPI_ATOMIC: if constexpr (HAS_MODE(EPI_ATOMIC)) {
       float* o = reinterpret_cast<float*>(e.out) + off;
 #pragma unroll
       for (int q = 0; q < 8; ++q)
         atomicAdd(reinterpret_cast<float4*>(o) + q, make_float4(v[q * 4], v[q * 4 + 1], v[q * 4 + 2], v[q * 4 + 3]));
     } break;
-    case EPI_HEAD: {
+    case EPI_HEAD: if constexpr (HAS_MODE(EPI_HEAD)) {
       // a 32-column slice covers at most two towers when dh % 32 != 0 (dh >= 32)
       const int k0 = n0c / e.hd;
       const int split = (k0 + 1) * e.hd - n0c;  // first column of tower k0 + 1 inside the slice
@@ -263,6 +270,36 @@ __device__ __forceinline__ void warp_sts_rows_bf16(uint32_t stg, const uint4 (&g
   __syncwarp();
 }
 
+// fp32 32 x 32 slice in the same two phases (4 rows x 128 B per load instruction).
+__device__ __forceinline__ void warp_ldg_rows_f32(const void* base, size_t off0, size_t ld, int rows_valid,
+                                                  uint4 (&g)[8]) {
+  const uint32_t lane = threadIdx.x & 31;
+  const float* b = reinterpret_cast<const float*>(base) + off0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int row = i * 4 + (lane >> 3), j = lane & 7;
+    g[i] = row < rows_valid ? *reinterpret_cast<const uint4*>(b + (size_t)row * ld + j * 4) : make_uint4(0, 0, 0, 0);
+  }
+}
+__device__ __forceinline__ void warp_sts_rows_f32(uint32_t stg, const uint4 (&g)[8], float (&x)[32]) {
+  const uint32_t lane = threadIdx.x & 31;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int row = i * 4 + (lane >> 3), j = lane & 7;
+    sts_u4(stg + row * 128 + ((j ^ (row & 7)) << 4), g[i].x, g[i].y, g[i].z, g[i].w);
+  }
+  __syncwarp();
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const uint4 u = lds_u4(stg + lane * 128 + ((j ^ (lane & 7)) << 4));
+    x[j * 4] = __uint_as_float(u.x);
+    x[j * 4 + 1] = __uint_as_float(u.y);
+    x[j * 4 + 2] = __uint_as_float(u.z);
+    x[j * 4 + 3] = __uint_as_float(u.w);
+  }
+  __syncwarp();
+}
+
 __device__ __forceinline__ void warp_load_rows(uint32_t stg, const void* base, int is_f32, size_t off0, size_t ld,
                                                int rows_valid, float (&x)[32]) {
   const uint32_t lane = threadIdx.x & 31;
@@ -272,29 +309,10 @@ __device__ __forceinline__ void warp_load_rows(uint32_t stg, const void* base, i
     warp_sts_rows_bf16(stg, g, x);
     return;
   } else {
-    const float* b = reinterpret_cast<const float*>(base) + off0;
     uint4 g[8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int row = i * 4 + (lane >> 3), j = lane & 7;
-      g[i] = row < rows_valid ? *reinterpret_cast<const uint4*>(b + (size_t)row * ld + j * 4) : make_uint4(0, 0, 0, 0);
-    }
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int row = i * 4 + (lane >> 3), j = lane & 7;
-      sts_u4(stg + row * 128 + ((j ^ (row & 7)) << 4), g[i].x, g[i].y, g[i].z, g[i].w);
-    }
-    __syncwarp();
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const uint4 u = lds_u4(stg + lane * 128 + ((j ^ (lane & 7)) << 4));
-      x[j * 4] = __uint_as_float(u.x);
-      x[j * 4 + 1] = __uint_as_float(u.y);
-      x[j * 4 + 2] = __uint_as_float(u.z);
-      x[j * 4 + 3] = __uint_as_float(u.w);
-    }
+    warp_ldg_rows_f32(base, off0, ld, rows_valid, g);
+    warp_sts_rows_f32(stg, g, x);
   }
-  __syncwarp();
 }
 __device__ __forceinline__ void warp_store_rows(uint32_t stg, void* base, int is_f32, size_t off0, size_t ld,
                                                 int rows_valid, const float (&v)[32]) {
@@ -328,18 +346,20 @@ __device__ __forceinline__ const void* epi_primary(const EpiParams& e) {
   }
 }
 
+template <uint32_t MODES>
 __device__ __forceinline__ void run_epilogue_warp(const EpiParams& e, int row0, int M, int n0c, float (&v)[32],
-                                                  uint32_t stg, const uint4* pre = nullptr) {
+                                                  uint32_t stg, const uint4* pre = nullptr,
+                                                  const uint4* pre_cs = nullptr) {
   const int lane = threadIdx.x & 31;
   if (e.row_map || e.mode == EPI_ATOMIC || e.mode == EPI_HEAD) {
-    run_epilogue(e, row0 + lane, M, n0c, v);
+    run_epilogue<MODES>(e, row0 + lane, M, n0c, v);
     return;
   }
   const int rows_valid = M - row0;
   if (rows_valid <= 0) return;
   const size_t off0 = (size_t)row0 * e.ldo + n0c;
   switch (e.mode) {
-    case EPI_STORE: {
+    case EPI_STORE: if constexpr (HAS_MODE(EPI_STORE)) {
       if (e.resid) {
         float r[32];
         if (pre)
@@ -352,7 +372,7 @@ __device__ __forceinline__ void run_epilogue_warp(const EpiParams& e, int row0, 
       warp_store_rows(stg, e.out, e.out_f32, off0, e.ldo, rows_valid, v);
     } break;
     case EPI_GATE:
-    case EPI_GATE_ROPE: {
+    case EPI_GATE_ROPE: if constexpr (HAS_MODE(EPI_GATE) || HAS_MODE(EPI_GATE_ROPE)) {
       if (e.aux) warp_store_rows(stg, e.aux, e.aux_f32, off0, e.ldo, rows_valid, v);
       float x[32];
       if (pre)
@@ -361,14 +381,17 @@ __device__ __forceinline__ void run_epilogue_warp(const EpiParams& e, int row0, 
         warp_load_rows(stg, e.src, 0, off0, e.ldo, rows_valid, x);
 #pragma unroll
       for (int j = 0; j < 32; ++j) v[j] = x[j] * __fdividef(1.0f, 1.0f + __expf(-v[j]));
-      if (e.mode == EPI_GATE_ROPE) {  // head-local window [n0c % hd, + 32) of the rope table rows
+      if (HAS_MODE(EPI_GATE_ROPE) && e.mode == EPI_GATE_ROPE) {  // head-local window [n0c % hd, + 32) of the table
         float cs[32];
-        warp_load_rows(stg, e.rope_cs, 1, (size_t)row0 * (e.hd + 32) + (n0c % e.hd), e.hd + 32, rows_valid, cs);
+        if (pre_cs)
+          warp_sts_rows_f32(stg, *reinterpret_cast<const uint4(*)[8]>(pre_cs), cs);
+        else
+          warp_load_rows(stg, e.rope_cs, 1, (size_t)row0 * (e.hd + 32) + (n0c % e.hd), e.hd + 32, rows_valid, cs);
         rope_rotate32(v, cs);
       }
       warp_store_rows(stg, e.out, e.out_f32, off0, e.ldo, rows_valid, v);
     } break;
-    case EPI_GATE_BWD: {
+    case EPI_GATE_BWD: if constexpr (HAS_MODE(EPI_GATE_BWD)) {
       float z[32], x[32], r[32];
       if (pre)
         warp_sts_rows_bf16(stg, *reinterpret_cast<const uint4(*)[4]>(pre), z);
@@ -397,7 +420,7 @@ __device__ __forceinline__ void run_epilogue_warp(const EpiParams& e, int row0, 
 }
 
 // ---------------------------------------------------------------- kernel
-template <int BN>
+template <int BN, uint32_t MODES>
 __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_kernel(const __grid_constant__ GemmKParams P) {
   using C = GemmCfg<BN>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -521,17 +544,29 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_kernel(const __grid_cons
       const int n0 = U.n0 * BN;
       // the primary epilogue input of slice c + 2 is requested before slice c is processed
       const void* pb = epi_primary(q.epi);
-      uint4 g[4];
+      // gate + RoPE launches also request the slice's RoPE table window a slice ahead
+      constexpr bool RPM = MODES == MB(EPI_GATE_ROPE);
+      const bool rp = RPM && q.epi.mode == EPI_GATE_ROPE && !q.epi.row_map;
+      uint4 g[4], gc[RPM ? 8 : 1];
       auto issue = [&](int c) {
         const int n0c = n0 + c * 32;
-        if (pb && c < BN / 32 && n0c < q.N && row0 < q.M)
-          warp_ldg_rows_bf16(pb, (size_t)row0 * q.epi.ldo + n0c, q.epi.ldo, q.M - row0, g);
+        if (c < BN / 32 && n0c < q.N && row0 < q.M) {
+          if (pb) warp_ldg_rows_bf16(pb, (size_t)row0 * q.epi.ldo + n0c, q.epi.ldo, q.M - row0, g);
+          if constexpr (RPM) {
+            if (rp)
+              warp_ldg_rows_f32(q.epi.rope_cs, (size_t)row0 * (q.epi.hd + 32) + (n0c % q.epi.hd), q.epi.hd + 32,
+                                q.M - row0, gc);
+          }
+        }
       };
       issue(half);
       for (int c = half; c < BN / 32; c += 2) {
         const int n0c = n0 + c * 32;
         if (n0c >= q.N) break;
         uint4 cur[4] = {g[0], g[1], g[2], g[3]};
+        uint4 curc[RPM ? 8 : 1];
+#pragma unroll
+        for (int i = 0; i < (RPM ? 8 : 1); ++i) curc[i] = gc[i];
         issue(c + 2);
         uint32_t r[32];
         tmem_ld32(tmem_addr(tmem_base, quarter, buf * BN + c * 32), r);
@@ -539,7 +574,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_kernel(const __grid_cons
         float v[32];
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-        run_epilogue_warp(q.epi, row0, q.M, n0c, v, stg, pb ? cur : nullptr);
+        run_epilogue_warp<MODES>(q.epi, row0, q.M, n0c, v, stg, pb ? cur : nullptr, rp ? curc : nullptr);
       }
       tc_fence_before();
       __syncwarp();
@@ -569,6 +604,7 @@ struct PairCfg {
   static constexpr int SMEM = BAR_OFF + 1024 + 256;
 };
 
+template <uint32_t MODES>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
     gemm_pair_kernel(const __grid_constant__ GemmKParams P) {
   using C = PairCfg;
@@ -700,17 +736,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
       const int n0 = U.n0 * BN;
       // the primary epilogue input of slice c + 2 is requested before slice c is processed
       const void* pb = epi_primary(q.epi);
-      uint4 g[4];
+      // gate + RoPE launches also request the slice's RoPE table window a slice ahead
+      constexpr bool RPM = MODES == MB(EPI_GATE_ROPE);
+      const bool rp = RPM && q.epi.mode == EPI_GATE_ROPE && !q.epi.row_map;
+      uint4 g[4], gc[RPM ? 8 : 1];
       auto issue = [&](int c) {
         const int n0c = n0 + c * 32;
-        if (pb && c < BN / 32 && n0c < q.N && row0 < q.M)
-          warp_ldg_rows_bf16(pb, (size_t)row0 * q.epi.ldo + n0c, q.epi.ldo, q.M - row0, g);
+        if (c < BN / 32 && n0c < q.N && row0 < q.M) {
+          if (pb) warp_ldg_rows_bf16(pb, (size_t)row0 * q.epi.ldo + n0c, q.epi.ldo, q.M - row0, g);
+          if constexpr (RPM) {
+            if (rp)
+              warp_ldg_rows_f32(q.epi.rope_cs, (size_t)row0 * (q.epi.hd + 32) + (n0c % q.epi.hd), q.epi.hd + 32,
+                                q.M - row0, gc);
+          }
+        }
       };
       issue(half);
       for (int c = half; c < BN / 32; c += 2) {
         const int n0c = n0 + c * 32;
         if (n0c >= q.N) break;
         uint4 cur[4] = {g[0], g[1], g[2], g[3]};
+        uint4 curc[RPM ? 8 : 1];
+#pragma unroll
+        for (int i = 0; i < (RPM ? 8 : 1); ++i) curc[i] = gc[i];
         issue(c + 2);
         uint32_t r[32];
         tmem_ld32(tmem_addr(tmem_base, quarter, buf * BN + c * 32), r);
@@ -718,7 +766,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
         float v[32];
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-        run_epilogue_warp(q.epi, row0, q.M, n0c, v, stg, pb ? cur : nullptr);
+        run_epilogue_warp<MODES>(q.epi, row0, q.M, n0c, v, stg, pb ? cur : nullptr, rp ? curc : nullptr);
       }
       tc_fence_before();
       __syncwarp();
@@ -763,18 +811,34 @@ static bool make_operand_map(CUtensorMap* m, const OperandDesc& o, int box_rows_
   return encode_bf16_map(m, o.ptr, 2, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B);
 }
 
+template <uint32_t MODES>
 static cudaError_t launch_pair(const GemmKParams& P, cudaStream_t stream) {
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, PairCfg::SMEM);
+    cudaError_t e =
+        cudaFuncSetAttribute(gemm_pair_kernel<MODES>, cudaFuncAttributeMaxDynamicSharedMemorySize, PairCfg::SMEM);
     if (e != cudaSuccess) return e;
     attr = true;
   }
   int pairs = num_sms() / 2;
   if (P.total_units < pairs) pairs = P.total_units;
   ProfScope ps(PROF_GEMM, stream, 1);
-  gemm_pair_kernel<<<2 * pairs, GEMM_THREADS, PairCfg::SMEM, stream>>>(P);
+  gemm_pair_kernel<MODES><<<2 * pairs, GEMM_THREADS, PairCfg::SMEM, stream>>>(P);
   return cudaGetLastError();
+}
+
+// the mode sets the layer launches get their own instantiation; anything else runs the all-modes one
+static cudaError_t launch_pair_modes(const GemmKParams& P, uint32_t modes, cudaStream_t stream) {
+  switch (modes) {
+    case MB(EPI_STORE): return launch_pair<MB(EPI_STORE)>(P, stream);
+    case MB(EPI_GATE): return launch_pair<MB(EPI_GATE)>(P, stream);
+    case MB(EPI_GATE_ROPE): return launch_pair<MB(EPI_GATE_ROPE)>(P, stream);
+    case MB(EPI_STORE) | MB(EPI_ATOMIC): return launch_pair<MB(EPI_STORE) | MB(EPI_ATOMIC)>(P, stream);
+    case MB(EPI_GATE_BWD) | MB(EPI_ATOMIC): return launch_pair<MB(EPI_GATE_BWD) | MB(EPI_ATOMIC)>(P, stream);
+    case MB(EPI_ATOMIC): return launch_pair<MB(EPI_ATOMIC)>(P, stream);
+    case MB(EPI_HEAD): return launch_pair<MB(EPI_HEAD)>(P, stream);
+    default: return launch_pair<MODES_ALL>(P, stream);
+  }
 }
 
 template <int BN>
@@ -782,13 +846,14 @@ static cudaError_t launch_bn(const GemmKParams& P, cudaStream_t stream) {
   using C = GemmCfg<BN>;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    cudaError_t e =
+        cudaFuncSetAttribute(gemm_kernel<BN, MODES_ALL>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     if (e != cudaSuccess) return e;
     attr = true;
   }
   const int grid = P.total_units < num_sms() ? P.total_units : num_sms();
   ProfScope ps(PROF_GEMM, stream, 1);
-  gemm_kernel<BN><<<grid, GEMM_THREADS, C::SMEM, stream>>>(P);
+  gemm_kernel<BN, MODES_ALL><<<grid, GEMM_THREADS, C::SMEM, stream>>>(P);
   return cudaGetLastError();
 }
 
@@ -829,7 +894,9 @@ cudaError_t gemm_launch(const GemmProblem* probs, int nprob, int bn, cudaStream_
     total += q.m_tiles * q.n_tiles * q.split_k;
   }
   P.total_units = total;
-  if (pair) return launch_pair(P, stream);
+  uint32_t modes = 0;
+  for (int p = 0; p < nprob; ++p) modes |= MB(probs[p].epi.mode);
+  if (pair) return launch_pair_modes(P, modes, stream);
   return bn == 256 ? launch_bn<256>(P, stream) : launch_bn<128>(P, stream);
 }
 
