@@ -53,24 +53,32 @@ CADET_DEV void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
 CADET_DEV void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+// try_wait with a suspend-time hint: a waiting thread is parked by the hardware until the phase
+// completes (or the hint expires) instead of re-polling, so waiting warps stop stealing issue
+// slots from the working warps on their SM sub-partition.
 CADET_DEV bool mbar_try_wait(uint32_t addr, uint32_t parity) {
   uint32_t ok;
   asm volatile(
       "{\n .reg .pred p;\n"
-      " mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n"
       " selp.u32 %0, 1, 0, p;\n}\n"
       : "=r"(ok)
-      : "r"(addr), "r"(parity)
+      : "r"(addr), "r"(parity), "r"(0x989680u)
       : "memory");
   return ok != 0;
 }
-// Bounded wait: a phase that never completes (a bug) traps after ~seconds instead
-// of hanging the GPU.
+CADET_DEV uint64_t global_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// Bounded wait: a phase that never completes (a bug) traps after ~20 s instead of hanging the GPU.
 CADET_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t a = smem_u32(bar);
-  uint32_t n = 0;
+  if (mbar_try_wait(a, parity)) return;
+  const uint64_t t0 = global_ns();
   while (!mbar_try_wait(a, parity)) {
-    if (++n > (1u << 26)) {
+    if (global_ns() - t0 > 20000000000ull) {
       printf("cadet: mbarrier timeout block %d thread %d\n", blockIdx.x, threadIdx.x);
       __trap();
     }
