@@ -139,9 +139,9 @@ __global__ void __launch_bounds__(192, 2)
         FT_MARK(3)
         tc_fence_after();
 #pragma unroll
-        for (int kk = 0; kk < 128 / 16; ++kk)
-          mma_bf16_ts(tmem + C::O_COL, tmem + C::S_COL + kk * 8, mnmajor_desc<HD>(sV, kk), idesc_o,
-                      (j > 0 || kk > 0) ? 1u : 0u);
+        for (int kk = 0; kk < 128 / 16; ++kk)  // packed P of keys [32c, 32c + 32) at columns [32c, 32c + 16)
+          mma_bf16_ts(tmem + C::O_COL, tmem + C::S_COL + (kk >> 1) * 32 + (kk & 1) * 8, mnmajor_desc<HD>(sV, kk),
+                      idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
         mma_commit(&bars->v_empty);
         mma_commit(&bars->pv_done);
       }
@@ -169,28 +169,35 @@ __global__ void __launch_bounds__(192, 2)
       FT_MARK(4)
       tc_fence_after();
       const bool partial = !valid || (e_r < k0 + 128);
-      auto load_masked = [&](int c, float (&x)[32]) {
-        uint32_t u[32];
-        tmem_ld32(tmem_addr(tmem, quarter, C::S_COL + c * 32), u);
-        tmem_ld_wait();
-#pragma unroll
-        for (int q = 0; q < 32; ++q) x[q] = __uint_as_float(u[q]);
+      auto mask32 = [&](int c, uint32_t (&u)[32]) {
         if (partial) {
           const uint32_t m = valid ? row_mask32(e_r, r, pp, k0 + c * 32) : 0u;
 #pragma unroll
           for (int q = 0; q < 32; ++q)
-            if (!((m >> q) & 1u)) x[q] = -INFINITY;
+            if (!((m >> q) & 1u)) u[q] = __float_as_uint(-INFINITY);
         }
       };
-      // pass 1: masked row max
+      // pass 1: row max over two batches of two chunks (two loads in flight per wait); chunks 2, 3
+      // stay in registers for pass 2
       float mx = -INFINITY;
-#pragma unroll 1
-      for (int c = 0; c < 4; ++c) {
-        float x[32];
-        load_masked(c, x);
+      uint32_t s2[32], s3[32];
+      {
+        uint32_t s0[32], s1[32];
+        tmem_ld32(tmem_addr(tmem, quarter, C::S_COL), s0);
+        tmem_ld32(tmem_addr(tmem, quarter, C::S_COL + 32), s1);
+        tmem_ld_wait();
+        mask32(0, s0);
+        mask32(1, s1);
 #pragma unroll
-        for (int q = 0; q < 32; ++q) mx = fmaxf(mx, x[q]);
+        for (int q = 0; q < 32; ++q) mx = fmaxf(mx, fmaxf(__uint_as_float(s0[q]), __uint_as_float(s1[q])));
       }
+      tmem_ld32(tmem_addr(tmem, quarter, C::S_COL + 64), s2);
+      tmem_ld32(tmem_addr(tmem, quarter, C::S_COL + 96), s3);
+      tmem_ld_wait();
+      mask32(2, s2);
+      mask32(3, s3);
+#pragma unroll
+      for (int q = 0; q < 32; ++q) mx = fmaxf(mx, fmaxf(__uint_as_float(s2[q]), __uint_as_float(s3[q])));
       FT_MARK(5)
       const float mx_s = mx * sl2;
       float factor = 1.f;
@@ -213,23 +220,32 @@ __global__ void __launch_bounds__(192, 2)
           tmem_st32(ta, u);
         }
       }
-      // pass 2: P = exp2(s * scale_log2 - m) as packed bf16 into TMEM columns [16c, 16c + 16),
-      // which only overlap S columns already consumed (chunk c/2 <= c).
+      // pass 2: P = exp2(s * scale_log2 - m) as packed bf16; chunk c's P lands in the first 16 of its
+      // own 32 columns (chunks 2, 3 from registers first, then chunks 0, 1 reloaded)
       const float base = (m_used == -INFINITY) ? 0.f : m_used;
       float rs = 0.f;
-#pragma unroll 1
-      for (int c = 0; c < 4; ++c) {
-        float x[32];
-        load_masked(c, x);
+      auto exp_store = [&](int c, const uint32_t (&u)[32]) {
         uint32_t w[16];
 #pragma unroll
         for (int q = 0; q < 32; q += 2) {
-          const float p0 = fast_exp2(fmaf(x[q], sl2, -base));
-          const float p1 = fast_exp2(fmaf(x[q + 1], sl2, -base));
+          const float p0 = fast_exp2(fmaf(__uint_as_float(u[q]), sl2, -base));
+          const float p1 = fast_exp2(fmaf(__uint_as_float(u[q + 1]), sl2, -base));
           rs += p0 + p1;
           w[q >> 1] = pack_bf16(p0, p1);
         }
-        tmem_st16(tmem_addr(tmem, quarter, C::S_COL + c * 16), w);
+        tmem_st16(tmem_addr(tmem, quarter, C::S_COL + c * 32), w);
+      };
+      exp_store(2, s2);
+      exp_store(3, s3);
+      {
+        uint32_t s0[32], s1[32];
+        tmem_ld32(tmem_addr(tmem, quarter, C::S_COL), s0);
+        tmem_ld32(tmem_addr(tmem, quarter, C::S_COL + 32), s1);
+        tmem_ld_wait();
+        mask32(0, s0);
+        mask32(1, s1);
+        exp_store(0, s0);
+        exp_store(1, s1);
       }
       tmem_st_wait();
       tc_fence_before();
