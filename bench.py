@@ -140,24 +140,26 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ workload
+SHARDS = 8  # the largest scaling run: every N <= 8 takes its ranks' shards from the same 8-way partition
+
+
 def build_inputs(wl: dict, seed: int, pin: bool, rank: int = 0, world: int = 1):
-    """One rank's batch.  N = 1: users drawn in arrival order up to the budget.  N > 1:
-    every rank draws the same global user stream for world x budget tokens and keeps its share of
-    the LPT partition (whole users, balanced on estimated cost, each rank under its budget)."""
+    """One rank's batch: one global user stream of max(8, world) x budget tokens is
+    partitioned by LPT (whole users, balanced on estimated cost, each shard under the budget) and
+    rank r takes shard r.  Every N <= 8 therefore runs shards of equal estimated cost, so the weak
+    scaling series compares like with like (N = 1 runs shard 0)."""
     from synth import generator as G
     from paper_2602_11410_b200.model import make_inputs, partition_lpt
     gcfg = G.GenConfig(max_tokens=wl["max_tokens"])
-    if world == 1:
-        users = G.gen_users_for_budget(seed, wl["budget"], gcfg)
-    else:
-        allu = G.gen_users_for_budget(seed, world * wl["budget"], gcfg)
-        while True:
-            try:
-                parts = partition_lpt([u.length for u in allu], world, wl["budget"], wl["L_chunk"], wl["d_model"])
-                break
-            except ValueError:
-                allu = allu[:-1]
-        users = [allu[i] for i in parts[rank]]
+    shards = max(SHARDS, world)
+    allu = G.gen_users_for_budget(seed, shards * wl["budget"], gcfg)
+    while True:
+        try:
+            parts = partition_lpt([u.length for u in allu], shards, wl["budget"], wl["L_chunk"], wl["d_model"])
+            break
+        except ValueError:
+            allu = allu[:-1]
+    users = [allu[i] for i in parts[rank]]
     return users, make_inputs(users, wl["d_model"], wl["L_chunk"], seed + 1000 * rank, pin=pin)
 
 
@@ -322,8 +324,10 @@ def main():
         if group is not None:
             dist.barrier()
 
+    # diagnostic: CADET_BENCH_NO_COLLECTIVE=1 steps without the gradient all-reduce (rank imbalance only)
+    step_group = None if os.environ.get("CADET_BENCH_NO_COLLECTIVE") == "1" else group
     for _ in range(args.warmup):
-        stack.step(inp, group)
+        stack.step(inp, step_group)
     torch.cuda.synchronize()
     stack.poll()
 
@@ -339,7 +343,7 @@ def main():
         try:
             ops.prof_enable(15, 64 * (wl["n_layers"] + 2))
             n0 = ops.launch_count()
-            graph = stack.capture(inp, group)
+            graph = stack.capture(inp, step_group)
             launches = ops.launch_count() - n0
             for _ in range(2):
                 graph.replay()
@@ -361,7 +365,7 @@ def main():
         if graph is not None:
             graph.replay()
         else:
-            stack.step(inp, group)
+            stack.step(inp, step_group)
     ev1.record()
     torch.cuda.synchronize()
     barrier()
@@ -392,7 +396,7 @@ def main():
         egraph = None
         if graph is not None:  # H2D of the inputs + step + D2H of the loss, one graph
             try:
-                egraph = stack.capture(inp, group, host_inp=host_inp, loss_h=loss_h)
+                egraph = stack.capture(inp, step_group, host_inp=host_inp, loss_h=loss_h)
             except Exception:  # noqa: BLE001
                 egraph = None
 
@@ -401,7 +405,7 @@ def main():
                 egraph.replay()
             else:
                 inp.copy_(host_inp)
-                stack.step(inp, group)
+                stack.step(inp, step_group)
                 loss_h.copy_(stack.loss, non_blocking=True)
         for _ in range(2):
             e2e_step()
@@ -460,7 +464,7 @@ def main():
                    "d_model": wl["d_model"], "heads": wl["n_heads"], "L_chunk": wl["L_chunk"],
                    "l2": "inputs > L2 (X 128 MB + activations > 1 GB per step); no flush needed",
                    "parallelism": f"dp{world}",
-                   "partition": "N>1: LPT of one global user stream (world x budget tokens) over ranks"},
+                   "partition": "rank r = shard r of an LPT partition of one user stream into 8 budgets"},
         "tflops": tflops_all, "tflops_per_gpu": tflops_all / world,
         "frac_of_peak_measured": tflops_all / world / float(peaks.get("bf16_tflops", 1663.9)),
         "frac_of_peak_spec": tflops_all / world / 2250.0,

@@ -187,6 +187,15 @@ cadet_status cadet_attn_backward(const cadet_attn_config* cfg_h, const cadet_bat
                                  const cadet_attn_weights* w_h, const void* X, const void* saved, const void* dY,
                                  void* dX, const void* dresid, const cadet_attn_grads* g_h, void* ws, size_t ws_bytes,
                                  cadet_stream_t stream);
+/* As cadet_attn_backward, and (grad_events non-NULL) records grad_events[i] (a cudaEvent_t, entries
+ * may be NULL) on `stream` right after the launch that completes weight-gradient group i:
+ * 0 = dW_o, 1 = dW_qg and dW_kg, 2 = dW_q, dW_k and dW_v, 3 = dW_xg (recorded even when an ablation
+ * switch removes the group).  A data-parallel caller all-reduces each group as soon as its event
+ * fires, overlapping the reduction with the rest of the backward. */
+cadet_status cadet_attn_backward_ev(const cadet_attn_config* cfg_h, const cadet_batch* b_h,
+                                    const cadet_attn_weights* w_h, const void* X, const void* saved, const void* dY,
+                                    void* dX, const void* dresid, const cadet_attn_grads* g_h, void* ws,
+                                    size_t ws_bytes, cadet_stream_t stream, void* const* grad_events);
 
 /* ------------------------------------------------------------------ A7 / A8: towers + routed loss (Eqs. 8-9)
  * Hs: bf16 [T, d] transformer output; rows: int32 [n] packed row index of each scored token

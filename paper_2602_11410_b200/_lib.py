@@ -84,6 +84,8 @@ SIGNATURES = {
     "cadet_attn_core_backward": (I32, [PCFG, PB, P, P, P, P, P, P, P, P, P, P, SZ, P]),
     "cadet_attn_forward": (I32, [PCFG, PB, C.POINTER(AttnWeights), P, P, P, P, P, SZ, P]),
     "cadet_attn_backward": (I32, [PCFG, PB, C.POINTER(AttnWeights), P, P, P, P, P, C.POINTER(AttnGrads), P, SZ, P]),
+    "cadet_attn_backward_ev": (I32, [PCFG, PB, C.POINTER(AttnWeights), P, P, P, P, P, C.POINTER(AttnGrads), P, SZ, P,
+                                     C.POINTER(C.c_void_p)]),
     "cadet_heads_forward": (I32, [C.POINTER(HeadConfig), C.POINTER(HeadWeights), P, P, I32, P, P, P, SZ, P]),
     "cadet_heads_loss_backward": (I32, [C.POINTER(HeadConfig), C.POINTER(HeadWeights), P, P, I32, I32, P, P, P, P,
                                         P, P, C.POINTER(HeadGrads), P, SZ, P]),

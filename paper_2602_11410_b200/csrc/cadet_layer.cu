@@ -343,9 +343,10 @@ cadet_status cadet_attn_forward(const cadet_attn_config* cfg, const cadet_batch*
   return cuda_err(e, "attention layer forward");
 }
 
-cadet_status cadet_attn_backward(const cadet_attn_config* cfg, const cadet_batch* b, const cadet_attn_weights* w,
+cadet_status cadet_attn_backward_ev(const cadet_attn_config* cfg, const cadet_batch* b, const cadet_attn_weights* w,
                                  const void* X, const void* saved, const void* dY, void* dX, const void* dresid,
-                                 const cadet_attn_grads* gr, void* ws, size_t ws_bytes, cadet_stream_t stream) {
+                                 const cadet_attn_grads* gr, void* ws, size_t ws_bytes, cadet_stream_t stream,
+                                    void* const* grad_events) {
   cadet_status s = check_cfg(cfg);
   if (s) return s;
   if ((s = check_batch(b, cfg))) return s;
@@ -372,6 +373,9 @@ cadet_status cadet_attn_backward(const cadet_attn_config* cfg, const cadet_batch
   float* gws[7] = {gr->dW_xg, gr->dW_q, gr->dW_k, gr->dW_v, gr->dW_qg, gr->dW_kg, gr->dW_o};
   for (int i = 0; i < 7 && e == cudaSuccess; ++i)
     if (gws[i]) e = cudaMemsetAsync(gws[i], 0, wbytes, st);
+  auto mark = [&](int i) {  // grad group i complete on `st` (SURVEY 8(e) overlap)
+    if (e == cudaSuccess && grad_events && grad_events[i]) e = cudaEventRecord((cudaEvent_t)grad_events[i], st);
+  };
   const void* Xt = cfg->use_rep_gate ? L.Xt : X;
   // A9: dO = dY W_o^T ; dW_o = O^T dY
   const void* dO = dY;
@@ -382,6 +386,7 @@ cadet_status cadet_attn_backward(const cadet_attn_config* cfg, const cadet_batch
     e = gemm_launch2(&g, 1, bn, &gw, 1, bnw, st);
     dO = W.dO;
   }
+  mark(0);
   // A10: attention core backward
   if (e == cudaSuccess) {
     AttnParams p = attn_params(cfg, b, v);
@@ -428,6 +433,7 @@ cadet_status cadet_attn_backward(const cadet_attn_config* cfg, const cadet_batch
         e = rope_gate_bwd_launch(W.dKr, 0, nullptr, nullptr, nullptr, W.dK, 1, T, d, hd, cs, st);
     }
   }
+  mark(1);
   // A12: dXt = dQ W_q^T + dK W_k^T + dV W_v^T (one K = 3d accumulation), weight grads, rep-gate bwd
   if (e == cudaSuccess) {
     GemmProblem g;
@@ -462,6 +468,7 @@ cadet_status cadet_attn_backward(const cadet_attn_config* cfg, const cadet_batch
                            wgrad(Xt, W.dV, gr->dW_v, T, d, d, bnw)};
       e = gemm_launch2(&g, 1, bn, gw, 3, bnw, st);
     }
+    mark(2);
     if (e == cudaSuccess && cfg->use_rep_gate) {  // dX = rx + ux W_xg^T ; dW_xg = X^T ux
       GemmProblem g2 = prob(T, d, d, act(W.ux, T, d), w_bwd(w->W_xg, d, d), EPI_STORE);
       g2.epi.out = dX;
@@ -471,8 +478,15 @@ cadet_status cadet_attn_backward(const cadet_attn_config* cfg, const cadet_batch
       e = gemm_launch2(&g2, 1, bn, &gw, 1, bnw, st);
     }
   }
+  mark(3);
   if (e == cudaSuccess) e = zero_pad_rows_launch(dX, d * 2, T, b->cu_seqlens, n, st);
   return cuda_err(e, "attention layer backward");
+}
+
+cadet_status cadet_attn_backward(const cadet_attn_config* cfg, const cadet_batch* b, const cadet_attn_weights* w,
+                                 const void* X, const void* saved, const void* dY, void* dX, const void* dresid,
+                                 const cadet_attn_grads* gr, void* ws, size_t ws_bytes, cadet_stream_t stream) {
+  return cadet_attn_backward_ev(cfg, b, w, X, saved, dY, dX, dresid, gr, ws, ws_bytes, stream, nullptr);
 }
 
 // =====================================================================================

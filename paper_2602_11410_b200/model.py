@@ -242,6 +242,8 @@ class CadetStack:
         self._ws = None
         self._hws = None
         self._bufs_for = None
+        self._side = None          # DP: stream on which per-group gradient all-reduces are issued
+        self._grad_events = None   # DP: [layer][4] events recorded by cadet_attn_backward_ev
 
     # -------------------------------------------------------------- buffers sized per batch
     def _ensure(self, n_chunks: int, n_imp: int, n_hist: int):
@@ -302,26 +304,44 @@ class CadetStack:
                                     _vp(self.logits), _vp(self.pre), _vp(self._hws), self._hws.numel(), st))
         if not backward:
             return self.logits
-        # gradient buckets: [towers] then one per layer (in backward order), each all-reduced as soon
-        # as its backward is enqueued (overlapped with the backward of earlier layers)
+        # DP: the towers' gradients are all-reduced once their backward is enqueued; each
+        # layer's weight gradients in four groups (W_o | W_qg, W_kg | W_q, W_k, W_v | W_xg), each as soon
+        # as cadet_attn_backward_ev's event for that group fires, overlapping the rest of the backward
         nl, dd = cfg.n_layers, d * d
-        buckets = GradBuckets([self.grads[nl * 7 * dd:]] +
-                              [self.grads[l * 7 * dd:(l + 1) * 7 * dd] for l in reversed(range(nl))], group)
+        buckets = GradBuckets([self.grads[nl * 7 * dd:]], group)
+        if group is not None and self._grad_events is None:
+            self._side = torch.cuda.Stream(self.dev)
+            self._grad_events = [[torch.cuda.Event() for _ in range(4)] for _ in range(nl)]
+            for evs in self._grad_events:
+                for e in evs:
+                    e.record()  # materialises the cudaEvent_t handle
         hg = L.HeadGrads(self.gW1.data_ptr(), self.gb1.data_ptr(), self.gw2.data_ptr(), self.gb2.data_ptr())
         chk(lib.cadet_heads_loss_backward(C.byref(hc), C.byref(hw), _vp(self.Hs[-1]), _vp(inp.rows), n_imp, T,
                                           _vp(self.logits), _vp(self.pre), _vp(inp.bucket), _vp(inp.label),
                                           _vp(self.loss), _vp(self.dHs[-1]), C.byref(hg), _vp(self._hws),
                                           self._hws.numel(), st))
         buckets.launch(0)
+        handles = []
         # A9-A12: layers backward; dX_l = dX_{l+1} (residual) + Attn_l^T(dX_{l+1})
         for l in reversed(range(cfg.n_layers)):
             w = L.AttnWeights(*[x.data_ptr() for x in self.W[l]])
             g = L.AttnGrads(*[x.data_ptr() for x in self.gW[l]])
-            chk(lib.cadet_attn_backward(C.byref(self.acfg), C.byref(b), C.byref(w), _vp(self.Hs[l]),
-                                        _vp(self.saved[l]), _vp(self.dHs[l + 1]), _vp(self.dHs[l]),
-                                        _vp(self.dHs[l + 1]), C.byref(g), ws, wsn, st))
-            buckets.launch(nl - l)
+            evs = self._grad_events[l] if group is not None else None
+            arr = (C.c_void_p * 4)(*[e.cuda_event for e in evs]) if evs else None
+            chk(lib.cadet_attn_backward_ev(C.byref(self.acfg), C.byref(b), C.byref(w), _vp(self.Hs[l]),
+                                           _vp(self.saved[l]), _vp(self.dHs[l + 1]), _vp(self.dHs[l]),
+                                           _vp(self.dHs[l + 1]), C.byref(g), ws, wsn, st, arr))
+            if evs:
+                base = l * 7 * dd
+                groups = (self.grads[base + 6 * dd:base + 7 * dd], self.grads[base + 4 * dd:base + 6 * dd],
+                          self.grads[base + dd:base + 4 * dd], self.grads[base:base + dd])
+                for i, sl in enumerate(groups):
+                    self._side.wait_event(evs[i])
+                    with torch.cuda.stream(self._side):
+                        handles.append(torch.distributed.all_reduce(sl, group=group, async_op=True))
         buckets.wait()
+        for h in handles:
+            h.wait()
         if group is not None:
             torch.distributed.all_reduce(self.loss, group=group)
         return self.loss

@@ -1,0 +1,65 @@
+"""Data-parallel step on 2 GPUs over NCCL: the gradients CadetStack.step reduces with
+per-group all-reduces overlapped with the backward (events from cadet_attn_backward_ev) must equal
+the sum of the ranks' local gradients from a non-DP step on the same shards, and the loss the sum
+of the local losses.  Skips with fewer than 2 GPUs (the host logic is covered by test_dp_gloo.py)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+
+def _worker(rank, world, port, q):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(rank)
+    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", rank))
+    import bench
+    from paper_2602_11410_b200.model import CadetStack, StackConfig
+    wl = dict(bench.WORKLOADS["c3"], budget=16384, n_layers=2)  # small 2-layer shards
+    users, hinp = bench.build_inputs(wl, 0, pin=False, rank=rank, world=world)
+    inp = hinp.to("cuda")
+    st = CadetStack(StackConfig(d_model=wl["d_model"], n_heads=wl["n_heads"], n_layers=wl["n_layers"],
+                                budget=wl["budget"], L_chunk=wl["L_chunk"]), seed=0, device="cuda")
+    st.step(inp)                      # local (no collective)
+    local = st.grads.clone()
+    local_loss = st.loss.clone()
+    st.step(inp, dist.group.WORLD)    # DP: overlapped per-group all-reduces
+    torch.cuda.synchronize()
+    parts = [torch.empty_like(local) for _ in range(world)]
+    dist.all_gather(parts, local)
+    losses = [torch.empty_like(local_loss) for _ in range(world)]
+    dist.all_gather(losses, local_loss)
+    if rank == 0:
+        ref = torch.stack(parts).sum(0)
+        q.put((st.grads.cpu().numpy(), ref.cpu().numpy(), float(st.loss.item()), float(sum(l.item() for l in losses))))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_dp_overlapped_allreduce_equals_sum_of_local_gradients():
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    import torch.multiprocessing as mp
+    from paper_2602_11410_b200 import build
+    build.build()
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got, ref, loss, ref_loss = q.get(timeout=600)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    # fp32 sums of two addends in a different association: equal up to one rounding
+    scale = max(1.0, float(np.abs(ref).max()))
+    assert np.abs(got - ref).max() <= 1e-6 * scale, np.abs(got - ref).max()
+    assert loss == pytest.approx(ref_loss, rel=1e-6)
