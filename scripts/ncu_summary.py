@@ -11,6 +11,10 @@ import sys
 METRICS = [
     ("gpu__time_duration.sum", "duration"),
     ("TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed", "tensor pipe %"),
+    ("sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed", "TMEM active % (tcgen05)"),
+    ("sm__pipe_shared_cycles_active.avg.pct_of_peak_sustained_active", "smem pipe %"),
+    ("sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active", "XU (MUFU) %"),
+    ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue %"),
     ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "dram %"),
     ("dram__bytes_read.sum", "dram read"),
     ("dram__bytes_write.sum", "dram write"),
