@@ -177,3 +177,29 @@ def test_c2_serving_forward_all_sequences():
     z, _, _ = O.heads_forward(Yg, rows.astype(np.int64), hw.W1.astype(np.float64), hw.b1.astype(np.float64),
                               hw.w2.astype(np.float64), hw.b2.astype(np.float64))
     assert_close(logits.cpu().numpy(), z, what="C2 logits")
+
+
+@pytest.mark.parametrize("d,H", [(352, 4), (1024, 8)])
+def test_next1_serving_request_core_forward(d, H):
+    """NEXT-1 shape: ONE request of 4,096 context tokens (causal,
+    Delta = 0) + 512 candidates (context + self), attention core forward, every row of every head
+    against the oracle (dense mask of the whole 4,608-token sequence)."""
+    import sys
+    import os
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "scripts"))
+    from serve_latency import request
+    from paper_2602_11410_b200 import build, ops
+    build.build()
+    cu, t, s, nc, T = request()
+    cfg = ops.config(d, H, delta_delay_ms=0, delta_cand_ms=0, out_f32=1)
+    b = to_dev_batch(cu, t, s, nc, T)
+    rng = np.random.default_rng(7)
+    Qr, Kr, V = [G.bf16_round(rng.standard_normal((T, d)).astype(np.float32) * 0.5) for _ in range(3)]
+    Og, lseg = ops.attn_core_forward(cfg, b, bf16_tensor(Qr), bf16_tensor(Kr), bf16_tensor(V))
+    torch.cuda.synchronize()
+    meta = meta_of(cu, t, s, nc)
+    A = O.seq_mask(meta, 0, oracle_cfg(cfg))
+    assert int(A.sum()) == (4096 * 4097) // 2 + 512 * 4097  # exact allowed pairs (SURVEY: L(L+1)/2 + N(L+1))
+    o, l, _ = O.attention_core_forward(Qr.astype(np.float64), Kr.astype(np.float64), V.astype(np.float64), A, H)
+    assert_close(to_np(Og), o, what="NEXT-1 O")
+    assert_close(to_np(lseg), l, what="NEXT-1 LSE")
