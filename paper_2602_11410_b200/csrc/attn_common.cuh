@@ -71,6 +71,12 @@ struct AttnParams {
   int32_t dq_bf16;
   void* dK;          // bwd out
   void* dV;          // bwd out
+  // forward split-KV (small grids, e.g. one serving request): each (q-tile, head) split into
+  // fwd_splits CTAs over its visit list, writing unnormalised fp32 partials merged afterwards
+  int32_t fwd_splits;
+  float* Opart;      // [splits][T][d]
+  float* Mpart;      // [splits][H][T] running max (log2 units) of the split
+  float* Lpart;      // [splits][H][T] row sum of the split (0 = empty split)
 };
 
 }  // namespace cadet

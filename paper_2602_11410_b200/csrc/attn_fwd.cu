@@ -57,14 +57,19 @@ __global__ void __launch_bounds__(192, 2)
   using G = HeadGeom<HD>;
   using C = FwdCfg<HD>;
   const int nq_total = p.plan.counters[0];
-  const int b = blockIdx.x / p.H;
-  const int h = blockIdx.x % p.H;
+  const int S = p.fwd_splits;
+  const int b = blockIdx.x / (p.H * S);
+  const int h = (blockIdx.x % (p.H * S)) % p.H;
+  const int sp = (blockIdx.x % (p.H * S)) / p.H;  // split index: visit-list slice [j0, j0 + n_kv)
   if (b >= nq_total) return;
   const QTileInfo qi = p.plan.qinfo[p.plan.fwd_order[b]];
   const int sa = p.cu[qi.seq], se = p.cu[qi.seq + 1];
   const int q0 = sa + qi.qt * 128;
   const int rows_valid = min(128, se - q0);
-  const int n_kv = qi.nf + (qi.qt + 1 - qi.kt2);
+  const int n_all = qi.nf + (qi.qt + 1 - qi.kt2);
+  const int chunk = (n_all + S - 1) / S;
+  const int j0 = min(n_all, sp * chunk);
+  const int n_kv = min(n_all, j0 + chunk) - j0;
 
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -96,7 +101,7 @@ __global__ void __launch_bounds__(192, 2)
       for (int blk = 0; blk < G::NB; ++blk)
         tma_load_3d(smem + C::Q_OFF + blk * G::BLK, &mQ, &bars->q_full, blk * G::CB, h, q0);
       for (int j = 0; j < n_kv; ++j) {
-        const int krow = sa + visit_tile(qi, j) * 128;
+        const int krow = sa + visit_tile(qi, j0 + j) * 128;
         if (j > 0) mbar_wait(&bars->k_empty, (j - 1) & 1);
         mbar_expect_tx(&bars->k_full, G::TILE_BYTES);
 #pragma unroll
@@ -163,7 +168,7 @@ __global__ void __launch_bounds__(192, 2)
 #define lane (threadIdx.x == 64 ? 0u : 1u)
 #endif
     for (int j = 0; j < n_kv; ++j) {
-      const int k0 = sa + visit_tile(qi, j) * 128;
+      const int k0 = sa + visit_tile(qi, j0 + j) * 128;
       // s_full(j) also implies PV_{j-1} completed (commit tracks all prior tcgen05 ops)
       mbar_wait(&bars->s_full, j & 1);
       FT_MARK(4)
@@ -262,9 +267,28 @@ __global__ void __launch_bounds__(192, 2)
       mbar_wait(&bars->pv_done, (n_kv - 1) & 1);
       tc_fence_after();
     }
+    if (S > 1) {  // split-KV partial: unnormalised O, the split's max (log2 units) and row sum
+      if (valid) {
+        p.Mpart[((size_t)sp * p.H + h) * p.T + r] = m_used;
+        p.Lpart[((size_t)sp * p.H + h) * p.T + r] = l;
+      }
+#pragma unroll 1
+      for (int c = 0; c < G::HDP / 32 && n_kv > 0; ++c) {
+        uint32_t u[32];
+        tmem_ld32(tmem_addr(tmem, quarter, C::O_COL + c * 32), u);
+        tmem_ld_wait();
+        if (valid) {
+          float* o = p.Opart + ((size_t)sp * p.T + r) * p.d + (size_t)h * p.hd + c * 32;
+          const int ncol = min(32, p.hd - c * 32);
+          for (int q = 0; q < ncol; q += 4)
+            *reinterpret_cast<float4*>(o + q) = make_float4(__uint_as_float(u[q]), __uint_as_float(u[q + 1]),
+                                                            __uint_as_float(u[q + 2]), __uint_as_float(u[q + 3]));
+        }
+      }
+    }
     const float inv_l = (l > 0.f) ? 1.f / l : 0.f;
 #pragma unroll
-    for (int c = 0; c < G::HDP / 32; ++c) {
+    for (int c = 0; c < G::HDP / 32 && S == 1; ++c) {
       uint32_t u[32];
       tmem_ld32(tmem_addr(tmem, quarter, C::O_COL + c * 32), u);
       tmem_ld_wait();
@@ -290,12 +314,48 @@ __global__ void __launch_bounds__(192, 2)
         }
       }
     }
-    if (valid) p.lse[(size_t)h * p.T + r] = (l > 0.f) ? (m_used + __log2f(l)) * 0.6931471805599453f : 0.f;
+    if (valid && S == 1) p.lse[(size_t)h * p.T + r] = (l > 0.f) ? (m_used + __log2f(l)) * 0.6931471805599453f : 0.f;
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   if (warp == 1) tmem_dealloc<C::TMEM_COLS>(tmem);
+}
+
+// Split-KV merge: per row and head, rescale the splits' partials to the common max and normalise.
+// Rows with no visible key in any split (pad rows) get O = 0, LSE = 0 (R17).
+__global__ void __launch_bounds__(256) attn_fwd_merge_kernel(const AttnParams p) {
+  const int row = blockIdx.x;
+  const int S = p.fwd_splits;
+  if (row >= p.cu[p.n]) return;  // pad rows: zeroed by the caller, no partials
+  for (int col = threadIdx.x * 4; col < p.d; col += blockDim.x * 4) {
+    const int h = col / p.hd;
+    float mstar = -INFINITY;
+    for (int s = 0; s < S; ++s)
+      if (p.Lpart[((size_t)s * p.H + h) * p.T + row] > 0.f) mstar = fmaxf(mstar, p.Mpart[((size_t)s * p.H + h) * p.T + row]);
+    float lsum = 0.f, a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+    for (int s = 0; s < S; ++s) {
+      const float ls = p.Lpart[((size_t)s * p.H + h) * p.T + row];
+      if (ls > 0.f) {
+        const float w = exp2f(p.Mpart[((size_t)s * p.H + h) * p.T + row] - mstar);
+        const float4 o = *reinterpret_cast<const float4*>(p.Opart + ((size_t)s * p.T + row) * p.d + col);
+        lsum += w * ls;
+        a0 += w * o.x, a1 += w * o.y, a2 += w * o.z, a3 += w * o.w;
+      }
+    }
+    const float inv = lsum > 0.f ? 1.f / lsum : 0.f;
+    if (p.out_f32) {
+      *reinterpret_cast<float4*>(reinterpret_cast<float*>(p.O) + (size_t)row * p.d + col) =
+          make_float4(a0 * inv, a1 * inv, a2 * inv, a3 * inv);
+    } else {
+      uint2 v;
+      v.x = pack_bf16(a0 * inv, a1 * inv);
+      v.y = pack_bf16(a2 * inv, a3 * inv);
+      *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(p.O) + (size_t)row * p.d + col) = v;
+    }
+    if (col % p.hd == 0)
+      p.lse[(size_t)h * p.T + row] = lsum > 0.f ? (mstar + __log2f(lsum)) * 0.6931471805599453f : 0.f;
+  }
 }
 
 // ---------------------------------------------------------------- host
@@ -321,10 +381,11 @@ static cudaError_t fwd_hd(const CUtensorMap& mQ, const CUtensorMap& mK, const CU
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  const int grid = p.plan.nq_cap * p.H;
+  const int grid = p.plan.nq_cap * p.H * p.fwd_splits;
   if (grid == 0) return cudaSuccess;
-  ProfScope ps(PROF_ATTN_FWD, st, 1);
+  ProfScope ps(PROF_ATTN_FWD, st, p.fwd_splits > 1 ? 2 : 1);
   attn_fwd_kernel<HD><<<grid, 192, C::SMEM, st>>>(mQ, mK, mV, p);
+  if (p.fwd_splits > 1) attn_fwd_merge_kernel<<<p.T, 256, 0, st>>>(p);
   return cudaGetLastError();
 }
 

@@ -29,6 +29,7 @@ cadet_status ws_err(size_t have, size_t need) {
 AttnParams attn_params(const cadet_attn_config* c, const cadet_batch* b, const PlanView& v) {
   AttnParams p;
   memset(&p, 0, sizeof(p));
+  p.fwd_splits = 1;
   p.T = b->total_tokens;
   p.H = c->n_heads;
   p.hd = c->head_dim;
@@ -40,6 +41,43 @@ AttnParams attn_params(const cadet_attn_config* c, const cadet_batch* b, const P
   p.cu = b->cu_seqlens;
   p.plan = v;
   return p;
+}
+
+// Forward split-KV: when one wave of two CTAs per SM would not be filled by
+// the (q-tile, head) grid (a single serving request), each q-tile's visit list is split over 4
+// CTAs; the fp32 partials live at the END of the caller's workspace when it is large enough
+// (cadet_attn_workspace_bytes includes them; otherwise the kernel runs unsplit).
+int fwd_splits_for(const cadet_attn_config* c, int n, int T) {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  const long long nq = (long long)(T + 127) / 128 + n;
+  if (T <= 0) return 1;
+  const long long S = (2LL * sms) / (nq * c->n_heads);  // fill one wave of two CTAs per SM
+  return (int)(S < 1 ? 1 : (S > 4 ? 4 : S));
+}
+size_t fwd_split_bytes(const cadet_attn_config* c, int n, int T) {
+  const int S = fwd_splits_for(c, n, T);
+  if (S <= 1) return 0;
+  return a256((size_t)S * T * c->d_model * 4) + 2 * a256((size_t)S * c->n_heads * T * 4) + 256;
+}
+void set_fwd_split(AttnParams& p, const cadet_attn_config* c, int n, int T, void* ws, size_t ws_bytes,
+                   size_t base_need) {
+  const int S = fwd_splits_for(c, n, T);
+  const size_t sb = fwd_split_bytes(c, n, T);
+  p.fwd_splits = 1;
+  if (S <= 1 || ws_bytes < base_need + sb) return;
+  uint8_t* e = reinterpret_cast<uint8_t*>(ws) + ((ws_bytes - sb + 255) & ~size_t(255));
+  p.Opart = reinterpret_cast<float*>(e);
+  e += a256((size_t)S * T * c->d_model * 4);
+  p.Mpart = reinterpret_cast<float*>(e);
+  e += a256((size_t)S * c->n_heads * T * 4);
+  p.Lpart = reinterpret_cast<float*>(e);
+  p.fwd_splits = S;
 }
 }  // namespace
 
@@ -63,6 +101,7 @@ cadet_status cadet_attn_core_forward(const cadet_attn_config* cfg, const cadet_b
   AttnParams p = attn_params(cfg, b, v);
   p.O = O;
   p.lse = lse;
+  set_fwd_split(p, cfg, b->n_seqs, b->total_tokens, ws, ws_bytes, need);
   const int T = b->total_tokens, d = cfg->d_model;
   // pad rows: O = 0, LSE = 0 (R17)
   cudaError_t e = zero_pad_rows_launch(O, d * (cfg->out_f32 ? 4 : 2), T, b->cu_seqlens, b->n_seqs, st);
@@ -140,10 +179,14 @@ LayerBufs carve_saved(void* saved, const cadet_attn_config* c, int T) {
 size_t saved_bytes(const cadet_attn_config* c, int T) {
   return 10 * bf_sz(T, c->d_model) + a256((size_t)4 * c->n_heads * T);
 }
-size_t layer_ws_bytes(const cadet_attn_config* c, int n, int T) {
+size_t layer_ws_base_bytes(const cadet_attn_config* c, int n, int T) {
   const int d = c->d_model;
   return plan_bytes(n, T, T) + a256(8 * 64) + a256((size_t)4 * T * (c->head_dim + 32)) +
          a256((size_t)4 * c->n_heads * T) + 8 * bf_sz(T, d) + 4 * f_sz(T, d);
+}
+size_t layer_ws_bytes(const cadet_attn_config* c, int n, int T) {
+  const int d = c->d_model;
+  return layer_ws_base_bytes(c, n, T) + fwd_split_bytes(c, n, T);
 }
 LayerWs carve_ws(void* ws, const cadet_attn_config* c, int n, int T) {
   const int d = c->d_model;
@@ -325,6 +368,7 @@ cadet_status cadet_attn_forward(const cadet_attn_config* cfg, const cadet_batch*
     p.out_f32 = 0;
     p.O = L.O;
     p.lse = L.lse;
+    set_fwd_split(p, cfg, n, T, ws, ws_bytes, layer_ws_base_bytes(cfg, n, T));
     e = zero_pad_rows_launch(L.O, d * 2, T, b->cu_seqlens, n, st);
     if (e == cudaSuccess) e = cudaMemsetAsync(L.lse, 0, sizeof(float) * (size_t)T * cfg->n_heads, st);
     if (e == cudaSuccess) e = attn_fwd_launch(L.Qr, L.Kr, L.V, p, st);

@@ -195,11 +195,17 @@ def test_next1_serving_request_core_forward(d, H):
     b = to_dev_batch(cu, t, s, nc, T)
     rng = np.random.default_rng(7)
     Qr, Kr, V = [G.bf16_round(rng.standard_normal((T, d)).astype(np.float32) * 0.5) for _ in range(3)]
-    Og, lseg = ops.attn_core_forward(cfg, b, bf16_tensor(Qr), bf16_tensor(Kr), bf16_tensor(V))
-    torch.cuda.synchronize()
+    from paper_2602_11410_b200 import _lib as L
+    import ctypes as C2
     meta = meta_of(cu, t, s, nc)
     A = O.seq_mask(meta, 0, oracle_cfg(cfg))
     assert int(A.sum()) == (4096 * 4097) // 2 + 512 * 4097  # exact allowed pairs (SURVEY: L(L+1)/2 + N(L+1))
     o, l, _ = O.attention_core_forward(Qr.astype(np.float64), Kr.astype(np.float64), V.astype(np.float64), A, H)
-    assert_close(to_np(Og), o, what="NEXT-1 O")
-    assert_close(to_np(lseg), l, what="NEXT-1 LSE")
+    # plan-sized workspace: one CTA per (q-tile, head); layer-sized: split-KV partials + merge when
+    # the grid is below one wave (d 352 x 4 heads)
+    for ws in (None, ops.workspace(L.lib().cadet_attn_workspace_bytes(C2.byref(cfg), 1, T))):
+        Og, lseg = ops.attn_core_forward(cfg, b, bf16_tensor(Qr), bf16_tensor(Kr), bf16_tensor(V), ws=ws)
+        torch.cuda.synchronize()
+        tag = "unsplit" if ws is None else "layer ws"
+        assert_close(to_np(Og), o, what=f"NEXT-1 O ({tag})")
+        assert_close(to_np(lseg), l, what=f"NEXT-1 LSE ({tag})")
