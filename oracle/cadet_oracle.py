@@ -4,7 +4,7 @@ TEST INFRASTRUCTURE ONLY.  Only `tests/`, `__graft_entry__.smoke()` and
 `bench.py`'s cpu_baseline / `--impl reference` legs may import this module.
 It shares no code with the CUDA path (paper_2602_11410_b200/) and never
 imports it.  Every function follows PAPER.md (P:n) / SPEC.md (S:n) as cited,
-with the readings R1..R21 listed in DESIGN.md §3.
+with the readings R1..R31 listed in DESIGN.md §3 (R29-R31: the NEXT-2 full loss).
 
 Conventions: row-vector projections y = x.W, W[d_in][d_out] (R1); all math in
 float64 on bf16-valued inputs (R20); heads are per-head slices of width hd of
@@ -456,6 +456,98 @@ def heads_loss_backward(H, rows, W1, b1, w2, b2, bucket, label):
     dH = np.zeros_like(np.asarray(H, dtype=np.float64))
     np.add.at(dH, rows, dHr)
     return heads_loss(z, bucket, label), z, dH, dict(dW1=dW1, db1=db1, dw2=dw2, db2=db2)
+
+
+# ------------------------------------------------------------------ NEXT-2: full loss (Eqs. 10-12)
+AUX_KINDS = ("bce", "se")  # R30: S:492 desk-scale tasks: long-dwell indicator (CE), impression duration (SE)
+
+
+def aux_heads_forward(H, rows, W1a, b1a, w2a, b2a):
+    """y^aux_j = MLP_j(h_t) (Eq. 10): J independent two-layer ReLU MLPs d -> da -> 1 on the
+    impression rows (R30); no routing (not context-conditioned)."""
+    return heads_forward(H, rows, W1a, b1a, w2a, b2a)
+
+
+def aux_losses(za, ya, kinds=AUX_KINDS):
+    """L_j^aux summed over impressions (R31): 'bce' = softplus(z) - y z (logits), 'se' = (z - y)^2."""
+    out = []
+    for j, kd in enumerate(kinds):
+        z, y = za[:, j], ya[:, j]
+        out.append(float(np.sum(softplus(z) - y * z)) if kd == "bce" else float(np.sum((z - y) ** 2)))
+    return out
+
+
+def aux_dz(za, ya, kinds=AUX_KINDS):
+    """dL_j^aux / dz: sigma(z) - y (bce), 2 (z - y) (se)."""
+    dz = np.zeros_like(np.asarray(za, dtype=np.float64))
+    for j, kd in enumerate(kinds):
+        dz[:, j] = (sigmoid(za[:, j]) - ya[:, j]) if kd == "bce" else 2.0 * (za[:, j] - ya[:, j])
+    return dz
+
+
+def pairwise_loss(z_pos, z_neg):
+    """RankNet over the batch (Eq. 12, P:428-435): -1/(N+ N-) sum_i sum_j log sigma(z+_i - z-_j);
+    0 when either set is empty (Eq. 12 undefined: S:459)."""
+    z_pos, z_neg = np.asarray(z_pos, np.float64), np.asarray(z_neg, np.float64)
+    if z_pos.size == 0 or z_neg.size == 0:
+        return 0.0
+    return float(np.sum(softplus(-(z_pos[:, None] - z_neg[None, :]))) / (z_pos.size * z_neg.size))
+
+
+def pairwise_grad(z_pos, z_neg):
+    """Adjoint of Eq. 12: dL/dz+_i = -1/(N+N-) sum_j sigma(z-_j - z+_i), dL/dz-_j = +1/(N+N-) sum_i
+    sigma(z-_j - z+_i)."""
+    z_pos, z_neg = np.asarray(z_pos, np.float64), np.asarray(z_neg, np.float64)
+    if z_pos.size == 0 or z_neg.size == 0:
+        return np.zeros_like(z_pos), np.zeros_like(z_neg)
+    s = sigmoid(z_neg[None, :] - z_pos[:, None])
+    c = 1.0 / (z_pos.size * z_neg.size)
+    return -c * s.sum(axis=1), c * s.sum(axis=0)
+
+
+def heads_backward_dz(H, rows, W1, b1, w2, b2, dz):
+    """Tower backward from given logit gradients dz [n, K] (every tower, no routing)."""
+    z, pre, hid = heads_forward(H, rows, W1, b1, w2, b2)
+    Hr = np.asarray(H, dtype=np.float64)[rows]
+    K = W1.shape[0]
+    g = dict(dW1=np.zeros_like(W1, dtype=np.float64), db1=np.zeros_like(b1, dtype=np.float64),
+             dw2=np.zeros_like(w2, dtype=np.float64), db2=dz.sum(axis=0))
+    dHr = np.zeros_like(Hr)
+    for k in range(K):
+        dhid = dz[:, k:k + 1] * w2[k][None, :] * (pre[k] > 0)
+        g["dW1"][k] = Hr.T @ dhid
+        g["db1"][k] = dhid.sum(axis=0)
+        g["dw2"][k] = hid[k].T @ dz[:, k]
+        dHr += dhid @ np.asarray(W1[k], dtype=np.float64).T
+    dH = np.zeros_like(np.asarray(H, dtype=np.float64))
+    np.add.at(dH, rows, dHr)
+    return dH, g
+
+
+def full_loss_backward(H, rows, ctx, aux, bucket, label, ya, lam=(1.0, (0.1, 0.1), 0.1), kinds=AUX_KINDS):
+    """Total loss (Eq. 11): L = lam_ctx L_ctx + sum_j lam_j L_j^aux + lam_pair L_pair, with
+    L_ctx the routed BCE (Eq. 9) and L_pair RankNet over the routed context logits z_{k_t} of the
+    batch (positives y = 1, negatives y = 0: R29).  ctx / aux = (W1, b1, w2, b2) of the towers and
+    the auxiliary heads.  Returns (loss terms dict, dH, ctx grads, aux grads)."""
+    lam_ctx, lam_aux, lam_pair = lam
+    z, _, _ = heads_forward(H, rows, *ctx)
+    za, _, _ = aux_heads_forward(H, rows, *aux)
+    n = z.shape[0]
+    zr = z[np.arange(n), bucket]
+    pos, neg = label > 0.5, label <= 0.5
+    terms = dict(ctx=heads_loss(z, bucket, label), aux=aux_losses(za, ya, kinds),
+                 pair=pairwise_loss(zr[pos], zr[neg]))
+    terms["total"] = lam_ctx * terms["ctx"] + sum(l * a for l, a in zip(lam_aux, terms["aux"])) + lam_pair * terms["pair"]
+    dz = np.zeros_like(z)
+    dz[np.arange(n), bucket] = lam_ctx * (sigmoid(zr) - label)
+    gp, gn = pairwise_grad(zr[pos], zr[neg])
+    dzr = np.zeros(n)
+    dzr[pos], dzr[neg] = gp, gn
+    dz[np.arange(n), bucket] += lam_pair * dzr
+    dza = aux_dz(za, ya, kinds) * np.asarray(lam_aux, np.float64)[None, :]
+    dH1, gc = heads_backward_dz(H, rows, *ctx, dz)
+    dH2, ga = heads_backward_dz(H, rows, *aux, dza)
+    return terms, dH1 + dH2, gc, ga
 
 
 # ------------------------------------------------------------------ per-element loop (check 1)

@@ -261,3 +261,15 @@ def fixed_lengths_batch(lengths, seed: int = 0, cfg: GenConfig | None = None, n_
         nc = 0 if n_cand is None else int(n_cand[u])
         users.append(UserHistory(t, s.astype(np.int32), y, k, np.arange(0, m, 2, dtype=np.int32), nc))
     return concat_users(users)
+
+
+def aux_labels(seed: int, n: int) -> np.ndarray:
+    """Auxiliary-task targets per impression (NEXT-2): column 0 a long-dwell indicator
+    (Bernoulli 0.2), column 1 an impression duration in minutes (log-normal, median 0.5).
+    float32 [n, 2]."""
+    rng = np.random.default_rng([seed, 17])
+    out = np.empty((n, 2), np.float32)
+    out[:, 0] = (rng.random(n) < 0.2).astype(np.float32)
+    out[:, 1] = np.exp(rng.normal(np.log(0.5), 0.8, size=n)).astype(np.float32)
+    return out
+

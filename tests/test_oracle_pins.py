@@ -427,3 +427,112 @@ def test_heads_backward_finite_differences_and_routing():
     # routing isolation: all impressions in bucket 0 -> head 1 gets exactly zero gradient
     L, z, dH, g = O.heads_loss_backward(Hm, rows, W1, b1, w2, b2, np.zeros(n, int), label)
     assert (g["dW1"][1] == 0).all() and g["db2"][1] == 0 and (g["dw2"][1] == 0).all()
+
+
+# ------------------------------------------------------------------ NEXT-2: full loss (Eqs. 10-12)
+def test_pairwise_unit_values_and_translation_invariance():
+    """S:745 loss unit values: RankNet z+ = z- -> ln 2; z+ = 2, z- = 0 -> 0.126928 (+-1e-6); a common
+    logit shift leaves Eq. 12 unchanged; an empty side gives 0."""
+    assert O.pairwise_loss([0.3], [0.3]) == pytest.approx(math.log(2.0), abs=1e-12)
+    assert O.pairwise_loss([2.0], [0.0]) == pytest.approx(0.126928, abs=1e-6)
+    rng = np.random.default_rng(3)
+    zp, zn = rng.normal(size=7), rng.normal(size=5)
+    assert O.pairwise_loss(zp + 3.7, zn + 3.7) == pytest.approx(O.pairwise_loss(zp, zn), abs=1e-12)
+    assert O.pairwise_loss([], zn) == 0.0 and O.pairwise_loss(zp, []) == 0.0
+
+
+def test_pairwise_brute_force_and_gradient():
+    """Eq. 12 as a pure-Python double loop of -log(1 / (1 + exp(-(a - b)))) / (N+ N-), and the
+    analytic adjoint against central differences."""
+    rng = np.random.default_rng(4)
+    zp, zn = rng.normal(size=4), rng.normal(size=6)
+    bf = 0.0
+    for a in zp:
+        for b in zn:
+            bf -= math.log(1.0 / (1.0 + math.exp(-(a - b))))
+    assert O.pairwise_loss(zp, zn) == pytest.approx(bf / (len(zp) * len(zn)), abs=1e-13)
+    gp, gn = O.pairwise_grad(zp, zn)
+    eps = 1e-6
+    for i in range(len(zp)):
+        e = np.zeros_like(zp)
+        e[i] = eps
+        fd = (O.pairwise_loss(zp + e, zn) - O.pairwise_loss(zp - e, zn)) / (2 * eps)
+        assert gp[i] == pytest.approx(fd, abs=1e-8)
+    for j in range(len(zn)):
+        e = np.zeros_like(zn)
+        e[j] = eps
+        fd = (O.pairwise_loss(zp, zn + e) - O.pairwise_loss(zp, zn - e)) / (2 * eps)
+        assert gn[j] == pytest.approx(fd, abs=1e-8)
+
+
+def test_aux_losses_closed_form_and_gradient():
+    """R31: BCE with logits (softplus(z) - y z) and squared error (z - y)^2, summed; dz by FD."""
+    za = np.array([[0.0, 1.5], [2.0, -0.5], [-1.0, 3.0]])
+    ya = np.array([[1.0, 1.0], [0.0, 0.0], [1.0, 2.5]])
+    l = O.aux_losses(za, ya)
+    # rows: (z 0, y 1) -> ln 2; (z 2, y 0) -> log1p(e^2); (z -1, y 1) -> log1p(e^-1) + 1
+    assert l[0] == pytest.approx(math.log(2) + math.log1p(math.exp(2.0)) + math.log1p(math.exp(-1.0)) + 1.0, abs=1e-12)
+    assert l[1] == pytest.approx(0.25 + 0.25 + 0.25, abs=1e-12)
+    dz = O.aux_dz(za, ya)
+    eps = 1e-6
+    for i in range(3):
+        for j in range(2):
+            e = np.zeros_like(za)
+            e[i, j] = eps
+            fd = (O.aux_losses(za + e, ya)[j] - O.aux_losses(za - e, ya)[j]) / (2 * eps)
+            assert dz[i, j] == pytest.approx(fd, abs=1e-7)
+
+
+def _full_case(seed=5, n_rows=9, T=14, d=8, K=2, dh=6, da=4):
+    rng = np.random.default_rng(seed)
+    H = rng.normal(size=(T, d))
+    rows = np.sort(rng.choice(T, size=n_rows, replace=False))
+    ctx = (rng.normal(size=(K, d, dh)) / 3, rng.normal(size=(K, dh)) / 3, rng.normal(size=(K, dh)), rng.normal(size=K))
+    aux = (rng.normal(size=(2, d, da)) / 3, rng.normal(size=(2, da)) / 3, rng.normal(size=(2, da)), rng.normal(size=2))
+    bucket = rng.integers(0, K, size=n_rows)
+    label = (rng.random(n_rows) < 0.4).astype(np.float64)
+    label[0], label[1] = 1.0, 0.0
+    ya = np.stack([(rng.random(n_rows) < 0.3).astype(np.float64), rng.exponential(size=n_rows)], axis=1)
+    return H, rows, ctx, aux, bucket, label, ya
+
+
+def test_full_loss_gradient_by_finite_differences():
+    """Eq. 11 total: the analytic dH (through the towers, the aux heads and RankNet on the routed
+    logits) and a tower / aux weight gradient against central differences of the total."""
+    H, rows, ctx, aux, bucket, label, ya = _full_case()
+    lam = (1.0, (0.3, 0.2), 0.7)
+    terms, dH, gc, ga = O.full_loss_backward(H, rows, ctx, aux, bucket, label, ya, lam)
+    f = lambda H_, ctx_=ctx, aux_=aux: O.full_loss_backward(H_, rows, ctx_, aux_, bucket, label, ya, lam)[0]["total"]
+    eps = 1e-6
+    for (r, c) in [(rows[0], 1), (rows[3], 5), (rows[-1], 0)]:
+        e = np.zeros_like(H)
+        e[r, c] = eps
+        assert dH[r, c] == pytest.approx((f(H + e) - f(H - e)) / (2 * eps), abs=1e-6)
+    for name, g, params, which in (("dW1", gc, ctx, 0), ("dW1", ga, aux, 1)):
+        W1 = params[0]
+        e = np.zeros_like(W1)
+        e[1, 2, 3] = eps
+        p_plus = (W1 + e,) + tuple(params[1:])
+        p_minus = (W1 - e,) + tuple(params[1:])
+        if which == 0:
+            fd = (f(H, p_plus, aux) - f(H, p_minus, aux)) / (2 * eps)
+        else:
+            fd = (f(H, ctx, p_plus) - f(H, ctx, p_minus)) / (2 * eps)
+        assert g[name][1, 2, 3] == pytest.approx(fd, abs=1e-6)
+
+
+def test_full_loss_reductions():
+    """lam_pair = 0 gives exactly the context + aux gradient (S:472 linearity); aux heads do not touch
+    the towers' gradients and vice versa (isolation); lam = (1, 0, 0) reduces to Eq. 9's routed BCE."""
+    H, rows, ctx, aux, bucket, label, ya = _full_case(seed=6)
+    t0, dH0, gc0, ga0 = O.full_loss_backward(H, rows, ctx, aux, bucket, label, ya, (1.0, (0.3, 0.2), 0.0))
+    t1, dH1, gc1, ga1 = O.full_loss_backward(H, rows, ctx, aux, bucket, label, ya, (1.0, (0.3, 0.2), 0.5))
+    assert np.array_equal(ga0["dW1"], ga1["dW1"])        # RankNet acts on the towers only
+    L, z, dHc, gcc = O.heads_loss_backward(H, rows, *ctx, bucket, label)
+    t2, dH2, gc2, ga2 = O.full_loss_backward(H, rows, ctx, aux, bucket, label, ya, (1.0, (0.0, 0.0), 0.0))
+    assert t2["total"] == pytest.approx(L, abs=1e-12)
+    assert np.allclose(dH2, dHc, atol=1e-14) and np.allclose(gc2["dW1"], gcc["dW1"], atol=1e-14)
+    assert np.all(ga2["dW1"] == 0)
+    # pairwise-only part of the tower gradient is linear in lam_pair
+    t3, dH3, gc3, ga3 = O.full_loss_backward(H, rows, ctx, aux, bucket, label, ya, (1.0, (0.3, 0.2), 1.0))
+    assert np.allclose(gc3["db2"] - gc0["db2"], 2.0 * (gc1["db2"] - gc0["db2"]), atol=1e-13)
