@@ -214,6 +214,51 @@ cadet_status cadet_heads_loss_backward(const cadet_head_config* h_h, const cadet
                                        void* dHs, const cadet_head_grads* g_h, void* ws, size_t ws_bytes,
                                        cadet_stream_t stream);
 
+/* ------------------------------------------------------------------ NEXT-2: full loss (Eqs. 10-12)
+ * Auxiliary heads (Eq. 10) run through cadet_heads_forward with their own weight set (K = J
+ * towers, d_hidden = the aux width, never routed).  One training step:
+ *   cadet_routed_logits -> (data parallel: all-gather z and labels over the ranks) ->
+ *   cadet_pairwise_loss -> cadet_full_loss_grads -> cadet_heads_backward (towers, accumulate 0)
+ *   -> cadet_heads_backward (aux heads, accumulate 1) -> layers backward.
+ * Readings: R29 the RankNet term pairs the routed tower logits z_{k_t} of the whole
+ * (global) batch, positives y = 1 vs negatives y = 0; R30 aux heads are 2-layer ReLU MLPs; R31 aux
+ * losses are BCE with logits or squared error (z - y)^2, summed over impressions like L_ctx. */
+typedef struct {
+  int32_t J;              /* auxiliary tasks, 0..8 */
+  int32_t aux_kind[8];    /* 0 = BCE with logits, 1 = squared error */
+  float lambda_ctx, lambda_pair;
+  float lambda_aux[8];    /* Eq. 11 weights; defaults 1.0, 0.1 each, 0.1 */
+} cadet_loss_config;
+void cadet_default_loss_config(cadet_loss_config* lc_h, int32_t J); /* kinds: task 0 BCE, others SE */
+/* z_out [n] = logits[i, bucket[i]] (fp32), the logit the pairwise term compares (R29). */
+cadet_status cadet_routed_logits(const float* logits, int32_t K, const int32_t* bucket, int32_t n, float* z_out,
+                                 cadet_stream_t stream);
+/* RankNet (Eq. 12) of this rank's n samples (routed logits z, labels in {0, 1}) against the batch
+ * z_all / label_all [n_all] (all ranks' samples, gathered in rank order; pass z / label themselves on
+ * one rank).  loss_share[1] = sum over LOCAL positives i and ALL negatives j of
+ * softplus(z_j - z_i) / (N+ N-), so the ranks' shares sum to Eq. 12; dz_pair [n] = dL_pair / dz of
+ * the local samples (overwritten).  N+, N- are counted on label_all; either empty -> 0.
+ * Deterministic (fixed-order reductions).  ws: cadet_pairwise_workspace_bytes(n, n_all). */
+size_t cadet_pairwise_workspace_bytes(int32_t n, int32_t n_all);
+cadet_status cadet_pairwise_loss(const float* z, const float* label, int32_t n, const float* z_all,
+                                 const float* label_all, int32_t n_all, float* loss_share, float* dz_pair, void* ws,
+                                 size_t ws_bytes, cadet_stream_t stream);
+/* Logit gradients and loss terms of Eq. 11 on this rank: dz_ctx [n, K] = lambda_ctx (sigma(z_kt) - y)
+ * + lambda_pair dz_pair[i] on the routed tower, 0 elsewhere; dz_aux [n, J] = lambda_j dL_j/dz.
+ * losses [J + 3] = (L_ctx, L_aux_0 .. L_aux_{J-1}, L_pair share, weighted total), overwritten.
+ * dz_pair / pair_share may be NULL (no pairwise term). */
+cadet_status cadet_full_loss_grads(const cadet_loss_config* lc_h, const float* logits, int32_t K,
+                                   const int32_t* bucket, const float* label, const float* dz_pair,
+                                   const float* pair_share, const float* aux_out, const float* aux_label, int32_t n,
+                                   float* losses, float* dz_ctx, float* dz_aux, cadet_stream_t stream);
+/* Tower backward from given logit gradients dz fp32 [n, K] (every tower; the towers of
+ * cadet_heads_loss_backward or the aux heads).  dHs bf16 [T, d]: accumulate = 0 -> overwritten
+ * (rows not in `rows` 0), 1 -> dHs[rows] += (other rows untouched).  Gradients overwritten. */
+cadet_status cadet_heads_backward(const cadet_head_config* h_h, const cadet_head_weights* w_h, const void* Hs,
+                                  const int32_t* rows, int32_t n, int32_t T, const void* pre, const float* dz,
+                                  int32_t accumulate, void* dHs, const cadet_head_grads* g_h, void* ws,
+                                  size_t ws_bytes, cadet_stream_t stream);
+
 /* ------------------------------------------------------------------ A0 / A13: chunk and pack
  * Chunk: split each sequence [a, e) of cu_in at e - L, e - 2L, ... (newest chunk full, oldest may be
  * short) and write the refined offsets in buffer order to cu_out (capacity cap entries);

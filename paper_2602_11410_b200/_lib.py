@@ -48,6 +48,11 @@ class AttnGrads(C.Structure):
     _fields_ = [(n, C.c_void_p) for n in ("dW_xg", "dW_q", "dW_k", "dW_v", "dW_qg", "dW_kg", "dW_o")]
 
 
+class LossConfig(C.Structure):
+    _fields_ = [("J", C.c_int32), ("aux_kind", C.c_int32 * 8), ("lambda_ctx", C.c_float), ("lambda_pair", C.c_float),
+                ("lambda_aux", C.c_float * 8)]
+
+
 class HeadConfig(C.Structure):
     _fields_ = [("K", C.c_int32), ("d_model", C.c_int32), ("d_hidden", C.c_int32), ("dtype", C.c_int32)]
 
@@ -89,6 +94,13 @@ SIGNATURES = {
     "cadet_heads_forward": (I32, [C.POINTER(HeadConfig), C.POINTER(HeadWeights), P, P, I32, P, P, P, SZ, P]),
     "cadet_heads_loss_backward": (I32, [C.POINTER(HeadConfig), C.POINTER(HeadWeights), P, P, I32, I32, P, P, P, P,
                                         P, P, C.POINTER(HeadGrads), P, SZ, P]),
+    "cadet_default_loss_config": (None, [C.POINTER(LossConfig), I32]),
+    "cadet_routed_logits": (I32, [P, I32, P, I32, P, P]),
+    "cadet_pairwise_workspace_bytes": (SZ, [I32, I32]),
+    "cadet_pairwise_loss": (I32, [P, P, I32, P, P, I32, P, P, P, SZ, P]),
+    "cadet_full_loss_grads": (I32, [C.POINTER(LossConfig), P, I32, P, P, P, P, P, P, I32, P, P, P, P]),
+    "cadet_heads_backward": (I32, [C.POINTER(HeadConfig), C.POINTER(HeadWeights), P, P, I32, I32, P, P, I32, P,
+                                   C.POINTER(HeadGrads), P, SZ, P]),
     "cadet_chunk": (I32, [P, I32, I32, P, I32, P, P, P]),
     "cadet_pack": (I32, [P, P, P, I32, I32, I32, P, P, P, P, P, P, P, P, SZ, P]),
     "cadet_pack_workspace_bytes": (SZ, [I32]),

@@ -592,6 +592,63 @@ cadet_status cadet_heads_forward(const cadet_head_config* h, const cadet_head_we
   return cuda_err(e, "heads forward");
 }
 
+cadet_status cadet_heads_backward(const cadet_head_config* h, const cadet_head_weights* w, const void* Hs,
+                                  const int32_t* rows, int32_t n, int32_t T, const void* pre, const float* dz,
+                                  int32_t accumulate, void* dHs, const cadet_head_grads* gr, void* ws, size_t ws_bytes,
+                                  cadet_stream_t stream) {
+  cadet_status s = check_head(h, w);
+  if (s) return s;
+  if (!Hs || !rows || !pre || !dz || !dHs || !gr || !gr->dW1 || !gr->db1 || !gr->dw2 || !gr->db2 || !ws || n < 0 ||
+      T < 0) {
+    set_error("heads_backward: null pointer");
+    return CADET_E_ARG;
+  }
+  const size_t need = cadet_heads_workspace_bytes(h, n);
+  if (ws_bytes < need) return ws_err(ws_bytes, need);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const int d = h->d_model, N = h->K * h->d_hidden;
+  uint8_t* p = reinterpret_cast<uint8_t*>(ws);
+  uint32_t* err = reinterpret_cast<uint32_t*>(p);
+  void* Hr = p + 256;
+  void* dhid_lo = p + 256 + a256((size_t)n * d * 2);
+  void* dhid = p + 256 + a256((size_t)n * d * 2) + a256((size_t)n * N * 2);
+  cudaError_t e = cudaMemsetAsync(gr->dW1, 0, (size_t)d * N * 4, st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(gr->db1, 0, (size_t)N * 4, st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(gr->dw2, 0, (size_t)N * 4, st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(gr->db2, 0, (size_t)h->K * 4, st);
+  if (e == cudaSuccess && !accumulate) e = cudaMemsetAsync(dHs, 0, (size_t)T * d * 2, st);
+  if (n == 0) return cuda_err(e, "heads backward");
+  if (e == cudaSuccess)
+    e = head_dhid_full_launch(pre, dz, w->w2, n, h->K, h->d_hidden, dhid, dhid_lo, gr->db1, gr->dw2, gr->db2, st);
+  if (e == cudaSuccess) e = gather_rows_launch(Hs, rows, n, T, d, Hr, err, st);
+  if (e == cudaSuccess) {  // dW1 = H_r^T (dhid_hi + dhid_lo), dHs[rows] (+)= (dhid_hi + dhid_lo) W1^T: one launch
+    const int bnw = pick_bn_wgrad(N);
+    GemmProblem gw = prob(d, N, n, act_t(Hr, n, d), act_t(dhid, n, N), EPI_ATOMIC);
+    gw.nseg = 2;
+    gw.K[1] = n;
+    gw.A[1] = act_t(Hr, n, d);
+    gw.B[1] = act_t(dhid_lo, n, N);
+    gw.split_k = pick_split(d, N, bnw, n);
+    gw.epi.out = gr->dW1;
+    gw.epi.out_f32 = 1;
+    GemmProblem g = prob(n, d, N, act(dhid, n, N), w_bwd(w->W1, d, N), EPI_STORE);
+    g.nseg = 2;
+    g.K[1] = N;
+    g.A[1] = act(dhid_lo, n, N);
+    g.B[1] = w_bwd(w->W1, d, N);
+    g.epi.out = dHs;
+    g.epi.ldo = d;
+    g.epi.row_map = rows;
+    if (accumulate) {  // in place: dHs[rows] = dHs[rows] + (...)
+      g.epi.resid = dHs;
+      g.epi.resid_f32 = 0;
+      g.epi.resid_at_out = 1;
+    }
+    e = gemm_launch2(&g, 1, pick_bn(n, d), &gw, 1, bnw, st);
+  }
+  return cuda_err(e, "heads backward");
+}
+
 cadet_status cadet_heads_loss_backward(const cadet_head_config* h, const cadet_head_weights* w, const void* Hs,
                                        const int32_t* rows, int32_t n, int32_t T, const float* logits,
                                        const void* pre, const int32_t* bucket, const float* label, float* loss_sum,

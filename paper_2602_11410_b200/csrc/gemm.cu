@@ -162,7 +162,7 @@ __device__ __forceinline__ void run_epilogue(const EpiParams& e, int row, int M,
     case EPI_STORE: if constexpr (HAS_MODE(EPI_STORE)) {
       if (e.resid) {
         float r[32];
-        load_any32(e.resid, e.resid_f32, in_off, r);
+        load_any32(e.resid, e.resid_f32, e.resid_at_out ? off : in_off, r);
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] += r[j];
       }

@@ -19,5 +19,8 @@ cudaError_t head_dz_launch(const float* logits, const int32_t* bucket, const flo
                            float* loss_sum, float* db2, uint32_t* err, cudaStream_t st);
 cudaError_t head_dhid_launch(const void* pre, const float* dz, const int32_t* bucket, const float* w2, int n, int K,
                              int dh, void* dhid, void* dhid_lo, float* db1, float* dw2, cudaStream_t st);
+// NEXT-2 (loss.cu): tower backward from a full dz [n, K] (dhid hi + lo, db1, dw2, db2)
+cudaError_t head_dhid_full_launch(const void* pre, const float* dz, const float* w2, int n, int K, int dh, void* dhid,
+                                  void* dhid_lo, float* db1, float* dw2, float* db2, cudaStream_t st);
 cudaError_t add_bf16_launch(const void* a, const void* b, void* out, size_t n, cudaStream_t st);
 }  // namespace cadet
