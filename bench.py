@@ -143,7 +143,7 @@ class ClockSampler:
 SHARDS = 8  # the largest scaling run: every N <= 8 takes its ranks' shards from the same 8-way partition
 
 
-def build_inputs(wl: dict, seed: int, pin: bool, rank: int = 0, world: int = 1):
+def build_inputs(wl: dict, seed: int, pin: bool, rank: int = 0, world: int = 1, J: int = 0):
     """One rank's batch: one global user stream of max(8, world) x budget tokens is
     partitioned by LPT (whole users, balanced on estimated cost, each shard under the budget) and
     rank r takes shard r.  Every N <= 8 therefore runs shards of equal estimated cost, so the weak
@@ -160,7 +160,7 @@ def build_inputs(wl: dict, seed: int, pin: bool, rank: int = 0, world: int = 1):
         except ValueError:
             allu = allu[:-1]
     users = [allu[i] for i in parts[rank]]
-    return users, make_inputs(users, wl["d_model"], wl["L_chunk"], seed + 1000 * rank, pin=pin)
+    return users, make_inputs(users, wl["d_model"], wl["L_chunk"], seed + 1000 * rank, pin=pin, J=J)
 
 
 def step_flops(wl: dict, tokens: int, pairs: int, n_imp: int, dh: int, K: int = 2):
@@ -259,6 +259,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--full-loss", action="store_true",
+                    help="NEXT-2: train on Eq. 11 (towers + auxiliary heads + cross-rank RankNet) instead of Eq. 9")
     ap.add_argument("--graph", action="store_true",
                     help="replay the step as one CUDA graph (measured: no gain over eager launches on C4)")
     args = ap.parse_args()
@@ -309,11 +311,11 @@ def main():
         dist.barrier()  # local rank 0 finished any rebuild before the others load the library
     dev = torch.device("cuda", local)
 
-    users, host_inp = build_inputs(wl, 0, pin=True, rank=rank, world=world)
+    users, host_inp = build_inputs(wl, 0, pin=True, rank=rank, world=world, J=2 if args.full_loss else 0)
     inp = host_inp.to(dev)
     torch.cuda.synchronize()
     scfg = StackConfig(d_model=wl["d_model"], n_heads=wl["n_heads"], n_layers=wl["n_layers"], budget=wl["budget"],
-                       L_chunk=wl["L_chunk"])
+                       L_chunk=wl["L_chunk"], full_loss=args.full_loss)
     stack = CadetStack(scfg, seed=0, device=dev)
     pairs = stack.pairs(inp)
     n_imp = inp.rows.numel()
@@ -476,7 +478,7 @@ def main():
                    "allowed_pairs_per_head": pairs, "impressions": n_imp, "layers": wl["n_layers"],
                    "d_model": wl["d_model"], "heads": wl["n_heads"], "L_chunk": wl["L_chunk"],
                    "l2": "inputs > L2 (X 128 MB + activations > 1 GB per step); no flush needed",
-                   "parallelism": f"dp{world}",
+                   "parallelism": f"dp{world}", "loss": "Eq. 11 full (NEXT-2)" if args.full_loss else "Eq. 9 routed BCE",
                    "partition": "rank r = shard r of an LPT partition of one user stream into 8 budgets"},
         "tflops": tflops_all, "tflops_per_gpu": tflops_all / world,
         "frac_of_peak_measured": tflops_all / world / float(peaks.get("bf16_tflops", 1663.9)),

@@ -16,6 +16,7 @@ runs the NCCL collective.
 from __future__ import annotations
 
 import ctypes as C
+import math
 from dataclasses import dataclass
 
 import numpy as np
@@ -36,10 +37,18 @@ class StackConfig:
     d_hidden: int = 0            # 0 -> d_model // 2
     delta_delay_ms: int = 3_600_000
     mask_flags: int = L.CADET_MASK_TIME
+    full_loss: bool = False      # NEXT-2: Eq. 11 = ctx + aux heads (Eq. 10) + RankNet (Eq. 12)
+    J: int = 2                   # auxiliary tasks (long-dwell BCE, duration SE)
 
     @property
     def dh(self) -> int:
         return self.d_hidden or self.d_model // 2
+
+    @property
+    def da(self) -> int:
+        """Aux head width (R30): d / 4 rounded up so that J * da is a multiple of 32."""
+        q = 32 // math.gcd(32, self.J)
+        return -(-(self.d_model // 4) // q) * q
 
 
 @dataclass
@@ -55,22 +64,26 @@ class StepInputs:
     n_hist: int
     n_chunks: int
     tokens: int              # real tokens T_r
+    aux_label: torch.Tensor | None = None  # [n_imp, J] fp32 (NEXT-2 full loss)
 
     def to(self, device, non_blocking=True) -> "StepInputs":
-        f = lambda t: t.to(device, non_blocking=non_blocking)
+        f = lambda t: t.to(device, non_blocking=non_blocking) if t is not None else None
         return StepInputs(f(self.X_hist), f(self.t_hist), f(self.s_hist), f(self.lens), f(self.rows),
-                          f(self.bucket), f(self.label), self.n_hist, self.n_chunks, self.tokens)
+                          f(self.bucket), f(self.label), self.n_hist, self.n_chunks, self.tokens, f(self.aux_label))
+
+    FIELDS = ("X_hist", "t_hist", "s_hist", "lens", "rows", "bucket", "label", "aux_label")
 
     def copy_(self, src: "StepInputs"):
-        for a in ("X_hist", "t_hist", "s_hist", "lens", "rows", "bucket", "label"):
-            getattr(self, a).copy_(getattr(src, a), non_blocking=True)
+        for a in self.FIELDS:
+            if getattr(self, a) is not None:
+                getattr(self, a).copy_(getattr(src, a), non_blocking=True)
 
     def nbytes(self) -> int:
-        return sum(getattr(self, a).numel() * getattr(self, a).element_size()
-                   for a in ("X_hist", "t_hist", "s_hist", "lens", "rows", "bucket", "label"))
+        return sum(getattr(self, a).numel() * getattr(self, a).element_size() for a in self.FIELDS
+                   if getattr(self, a) is not None)
 
 
-def make_inputs(users, d: int, L_chunk: int, seed: int, pin: bool = False) -> StepInputs:
+def make_inputs(users, d: int, L_chunk: int, seed: int, pin: bool = False, J: int = 0) -> StepInputs:
     """Host-side data loader output for one batch of generator users (synth/ Appendix B)."""
     from synth import generator as G
     lens = np.array([u.length for u in users], dtype=np.int32)
@@ -85,11 +98,13 @@ def make_inputs(users, d: int, L_chunk: int, seed: int, pin: bool = False) -> St
     n_chunks = int(sum(-(-int(m) // L_chunk) for m in lens))
     mk = lambda a, dt: (torch.from_numpy(np.ascontiguousarray(a)).to(dt))
     Xt = torch.from_numpy(X).to(torch.bfloat16)
+    aux = mk(G.aux_labels(seed, len(rows))[:, :J], torch.float32) if J > 0 else None
     inp = StepInputs(Xt, mk(t, torch.int64), mk(s, torch.int32), mk(lens, torch.int32), mk(rows, torch.int32),
-                     mk(bucket, torch.int32), mk(label, torch.float32), len(users), n_chunks, R)
+                     mk(bucket, torch.int32), mk(label, torch.float32), len(users), n_chunks, R, aux)
     if pin:
-        inp = StepInputs(*[x.pin_memory() for x in (inp.X_hist, inp.t_hist, inp.s_hist, inp.lens, inp.rows,
-                                                    inp.bucket, inp.label)], inp.n_hist, inp.n_chunks, inp.tokens)
+        pinned = [x.pin_memory() if x is not None else None for x in (inp.X_hist, inp.t_hist, inp.s_hist, inp.lens,
+                                                                       inp.rows, inp.bucket, inp.label, inp.aux_label)]
+        inp = StepInputs(*pinned[:7], inp.n_hist, inp.n_chunks, inp.tokens, pinned[7])
     return inp
 
 
@@ -214,22 +229,31 @@ class CadetStack:
         self.b1 = torch.from_numpy(hw.b1.reshape(-1).copy()).to(self.dev)
         self.w2 = torch.from_numpy(hw.w2.reshape(-1).copy()).to(self.dev)
         self.b2 = torch.from_numpy(hw.b2.copy()).to(self.dev)
-        # flat fp32 gradient buffer: 7 d^2 per layer + towers (one NCCL all-reduce bucket)
+        # flat fp32 gradient buffer: 7 d^2 per layer, the towers (+ the aux heads, NEXT-2); every slice
+        # starts on a 256-byte boundary (the split-K weight-gradient epilogue adds float4 atomics)
         N = cfg.K * cfg.dh
-        self.n_grad = nl * 7 * d * d + d * N + 2 * N + cfg.K
+        Na = cfg.J * cfg.da if cfg.full_loss else 0
+        pad = lambda x: -(-x // 64) * 64
+        sizes = [d * d] * (7 * nl) + [d * N, N, N, cfg.K] + ([d * Na, Na, Na, cfg.J] if cfg.full_loss else [])
+        self.n_grad = sum(pad(x) for x in sizes)
         self.grads = torch.zeros(self.n_grad, dtype=torch.float32, device=self.dev)
-        off = 0
-        self.gW = []
-        for _ in range(nl):
-            gl = []
-            for _ in range(7):
-                gl.append(self.grads[off:off + d * d])
-                off += d * d
-            self.gW.append(gl)
-        self.gW1 = self.grads[off:off + d * N]; off += d * N
-        self.gb1 = self.grads[off:off + N]; off += N
-        self.gw2 = self.grads[off:off + N]; off += N
-        self.gb2 = self.grads[off:off + cfg.K]
+        views, off = [], 0
+        for x in sizes:
+            views.append(self.grads[off:off + x])
+            off += pad(x)
+        self.gW = [views[7 * l:7 * l + 7] for l in range(nl)]
+        self.gW1, self.gb1, self.gw2, self.gb2 = views[7 * nl:7 * nl + 4]
+        self._tower_off = 7 * nl * pad(d * d)  # towers (and aux heads) follow the layers
+        if cfg.full_loss:  # NEXT-2 auxiliary heads (Eq. 10): J towers of width da, never routed
+            aw = G.head_weights(seed + 1, cfg.J, d, cfg.da)
+            self.aW1 = bf(np.concatenate([aw.W1[k] for k in range(cfg.J)], axis=1))
+            self.ab1 = torch.from_numpy(aw.b1.reshape(-1).copy()).to(self.dev)
+            self.aw2 = torch.from_numpy(aw.w2.reshape(-1).copy()).to(self.dev)
+            self.ab2 = torch.from_numpy(aw.b2.copy()).to(self.dev)
+            self.agW1, self.agb1, self.agw2, self.agb2 = views[7 * nl + 4:7 * nl + 8]
+            self.lcfg = L.LossConfig()
+            L.lib().cadet_default_loss_config(C.byref(self.lcfg), cfg.J)
+            self.losses = torch.zeros(cfg.J + 3, dtype=torch.float32, device=self.dev)
         lib = L.lib()
         self.saved_bytes = lib.cadet_attn_saved_bytes(C.byref(self.acfg), T)
         self.saved = [torch.empty(self.saved_bytes, dtype=torch.uint8, device=self.dev) for _ in range(nl)]
@@ -265,6 +289,18 @@ class CadetStack:
         self.cu = torch.empty(n_chunks + 8, dtype=torch.int32, device=self.dev)
         self.n_out = torch.zeros(1, dtype=torch.int32, device=self.dev)
         self.n_packed = torch.zeros(1, dtype=torch.int32, device=self.dev)
+        if cfg.full_loss:
+            ahc = L.HeadConfig(cfg.J, cfg.d_model, cfg.da, 0)
+            awb = lib.cadet_heads_workspace_bytes(C.byref(ahc), n_imp)
+            self._aws = ops.workspace(awb, self.dev)
+            self.za = torch.empty(n_imp, cfg.J, dtype=torch.float32, device=self.dev)
+            self.apre = torch.empty(n_imp, cfg.J * cfg.da, dtype=torch.bfloat16, device=self.dev)
+            self.zr = torch.empty(n_imp, dtype=torch.float32, device=self.dev)
+            self.dz_pair = torch.empty(n_imp, dtype=torch.float32, device=self.dev)
+            self.dz_ctx = torch.empty(n_imp, cfg.K, dtype=torch.float32, device=self.dev)
+            self.dz_aux = torch.empty(n_imp, cfg.J, dtype=torch.float32, device=self.dev)
+            self.pair_share = torch.zeros(1, dtype=torch.float32, device=self.dev)
+            self._pws = None
         self._bufs_for = key
 
     def batch(self, inp: StepInputs) -> ops.PackedBatch:
@@ -302,13 +338,18 @@ class CadetStack:
         hw = L.HeadWeights(self.W1.data_ptr(), self.b1.data_ptr(), self.w2.data_ptr(), self.b2.data_ptr())
         chk(lib.cadet_heads_forward(C.byref(hc), C.byref(hw), _vp(self.Hs[-1]), _vp(inp.rows), n_imp,
                                     _vp(self.logits), _vp(self.pre), _vp(self._hws), self._hws.numel(), st))
+        if cfg.full_loss:  # Eq. 10: auxiliary heads on the same impression rows
+            ahc = L.HeadConfig(cfg.J, d, cfg.da, 0)
+            ahw = L.HeadWeights(self.aW1.data_ptr(), self.ab1.data_ptr(), self.aw2.data_ptr(), self.ab2.data_ptr())
+            chk(lib.cadet_heads_forward(C.byref(ahc), C.byref(ahw), _vp(self.Hs[-1]), _vp(inp.rows), n_imp,
+                                        _vp(self.za), _vp(self.apre), _vp(self._aws), self._aws.numel(), st))
         if not backward:
             return self.logits
         # DP: the towers' gradients are all-reduced once their backward is enqueued; each
         # layer's weight gradients in four groups (W_o | W_qg, W_kg | W_q, W_k, W_v | W_xg), each as soon
         # as cadet_attn_backward_ev's event for that group fires, overlapping the rest of the backward
         nl, dd = cfg.n_layers, d * d
-        buckets = GradBuckets([self.grads[nl * 7 * dd:]], group)
+        buckets = GradBuckets([self.grads[self._tower_off:]], group)
         if group is not None and self._grad_events is None:
             self._side = torch.cuda.Stream(self.dev)
             self._grad_events = [[torch.cuda.Event() for _ in range(4)] for _ in range(nl)]
@@ -316,10 +357,13 @@ class CadetStack:
                 for e in evs:
                     e.record()  # materialises the cudaEvent_t handle
         hg = L.HeadGrads(self.gW1.data_ptr(), self.gb1.data_ptr(), self.gw2.data_ptr(), self.gb2.data_ptr())
-        chk(lib.cadet_heads_loss_backward(C.byref(hc), C.byref(hw), _vp(self.Hs[-1]), _vp(inp.rows), n_imp, T,
-                                          _vp(self.logits), _vp(self.pre), _vp(inp.bucket), _vp(inp.label),
-                                          _vp(self.loss), _vp(self.dHs[-1]), C.byref(hg), _vp(self._hws),
-                                          self._hws.numel(), st))
+        if not cfg.full_loss:  # Eq. 9: routed BCE, fused
+            chk(lib.cadet_heads_loss_backward(C.byref(hc), C.byref(hw), _vp(self.Hs[-1]), _vp(inp.rows), n_imp, T,
+                                              _vp(self.logits), _vp(self.pre), _vp(inp.bucket), _vp(inp.label),
+                                              _vp(self.loss), _vp(self.dHs[-1]), C.byref(hg), _vp(self._hws),
+                                              self._hws.numel(), st))
+        else:
+            self._full_loss_backward(inp, group, hc, hw, hg, st)
         buckets.launch(0)
         handles = []
         # A9-A12: layers backward; dX_l = dX_{l+1} (residual) + Attn_l^T(dX_{l+1})
@@ -360,6 +404,34 @@ class CadetStack:
             if loss_h is not None:
                 loss_h.copy_(self.loss, non_blocking=True)
         return g
+
+    def _full_loss_backward(self, inp, group, hc, hw, hg, st):
+        """NEXT-2 (Eqs. 10-12): routed logits -> (DP) all-gather with labels -> RankNet share of this
+        rank -> Eq. 11 logit gradients -> tower and aux-head backward (dH accumulated).  The ranks'
+        loss totals sum (all-reduced with the gradients) to the global Eq. 11 loss."""
+        cfg, lib, chk = self.cfg, L.lib(), L.check
+        d, T, n = cfg.d_model, cfg.budget, inp.rows.numel()
+        chk(lib.cadet_routed_logits(_vp(self.logits), cfg.K, _vp(inp.bucket), n, _vp(self.zr), st))
+        z_all, y_all = dp_gather_scores(self.zr, inp.label, group)
+        n_all = int(z_all.numel())
+        pwb = lib.cadet_pairwise_workspace_bytes(n, n_all)
+        if self._pws is None or self._pws.numel() < pwb:
+            self._pws = ops.workspace(pwb, self.dev)
+        chk(lib.cadet_pairwise_loss(_vp(self.zr), _vp(inp.label), n, _vp(z_all), _vp(y_all), n_all,
+                                    _vp(self.pair_share), _vp(self.dz_pair), _vp(self._pws), self._pws.numel(), st))
+        chk(lib.cadet_full_loss_grads(C.byref(self.lcfg), _vp(self.logits), cfg.K, _vp(inp.bucket), _vp(inp.label),
+                                      _vp(self.dz_pair), _vp(self.pair_share), _vp(self.za), _vp(inp.aux_label), n,
+                                      _vp(self.losses), _vp(self.dz_ctx), _vp(self.dz_aux), st))
+        chk(lib.cadet_heads_backward(C.byref(hc), C.byref(hw), _vp(self.Hs[-1]), _vp(inp.rows), n, T, _vp(self.pre),
+                                     _vp(self.dz_ctx), 0, _vp(self.dHs[-1]), C.byref(hg), _vp(self._hws),
+                                     self._hws.numel(), st))
+        ahc = L.HeadConfig(cfg.J, d, cfg.da, 0)
+        ahw = L.HeadWeights(self.aW1.data_ptr(), self.ab1.data_ptr(), self.aw2.data_ptr(), self.ab2.data_ptr())
+        ahg = L.HeadGrads(self.agW1.data_ptr(), self.agb1.data_ptr(), self.agw2.data_ptr(), self.agb2.data_ptr())
+        chk(lib.cadet_heads_backward(C.byref(ahc), C.byref(ahw), _vp(self.Hs[-1]), _vp(inp.rows), n, T,
+                                     _vp(self.apre), _vp(self.dz_aux), 1, _vp(self.dHs[-1]), C.byref(ahg),
+                                     _vp(self._aws), self._aws.numel(), st))
+        self.loss.copy_(self.losses[cfg.J + 2:cfg.J + 3])
 
     def pairs(self, inp: StepInputs) -> int:
         """Allowed (i, j) pairs of the planned mask (head-independent), from the plan's export hook."""

@@ -209,3 +209,39 @@ def test_next1_serving_request_core_forward(d, H):
         tag = "unsplit" if ws is None else "layer ws"
         assert_close(to_np(Og), o, what=f"NEXT-1 O ({tag})")
         assert_close(to_np(lseg), l, what=f"NEXT-1 LSE ({tag})")
+
+
+def test_full_loss_step_reduces_to_the_routed_bce_step():
+    """NEXT-2 wiring through CadetStack: with lambda_aux = lambda_pair = 0 the full-loss step (routed
+    logits, pairwise, Eq. 11 gradients, generic tower backward) gives the layer and tower gradients
+    and the loss of the fused Eq. 9 step; with the default lambdas the aux-head gradients are
+    non-zero and the loss grows by the weighted aux / pairwise terms."""
+    import bench
+    from paper_2602_11410_b200 import build
+    from paper_2602_11410_b200.model import CadetStack, StackConfig
+    build.build()
+    wl = dict(bench.WORKLOADS["c3"], budget=16384, n_layers=2)
+    users, hinp = bench.build_inputs(wl, 0, pin=False, J=2)
+    inp = hinp.to("cuda")
+    mk = lambda full: CadetStack(StackConfig(d_model=wl["d_model"], n_heads=wl["n_heads"], n_layers=wl["n_layers"],
+                                             budget=wl["budget"], L_chunk=wl["L_chunk"], full_loss=full), device="cuda")
+    a = mk(False)
+    a.step(inp)
+    b = mk(True)
+    for j in range(8):
+        b.lcfg.lambda_aux[j] = 0.0
+    b.lcfg.lambda_pair = 0.0
+    b.step(inp)
+    torch.cuda.synchronize()
+    n_a = a.grads.numel()
+    ga, gb = a.grads.cpu().numpy(), b.grads[:n_a].cpu().numpy()
+    assert np.abs(ga - gb).max() <= 1e-5 * max(1.0, np.abs(ga).max())
+    assert float(b.loss.item()) == pytest.approx(float(a.loss.item()), rel=1e-5)
+    assert np.all(b.grads[n_a:].cpu().numpy() == 0)       # aux heads untouched with lambda_aux = 0
+    c = mk(True)
+    c.step(inp)
+    torch.cuda.synchronize()
+    terms = c.losses.cpu().numpy()
+    assert np.isfinite(terms).all() and terms[3] > 0       # RankNet share of a one-rank batch
+    assert float(c.loss.item()) == pytest.approx(terms[0] + 0.1 * (terms[1] + terms[2]) + 0.1 * terms[3], rel=1e-5)
+    assert np.abs(c.grads[n_a:].cpu().numpy()).max() > 0
