@@ -21,9 +21,10 @@ __global__ void routed_logits_kernel(const float* logits, int K, const int32_t* 
   if (i < n) z[i] = logits[(size_t)i * K + min(max(bucket[i], 0), K - 1)];
 }
 
-// One block: positives and negatives of label_all in index order (block scan per 1024-chunk).
+// One block: positives and negatives of label_all in index order (block scan per 1024-chunk):
+// their logits (zp, zn) or, for the local samples, their indices (ip, in_).
 __global__ void __launch_bounds__(1024) compact_kernel(const float* z_all, const float* y_all, int n_all, float* zp,
-                                                       float* zn, int* counts) {
+                                                       float* zn, int* counts, int* ip = nullptr, int* in_ = nullptr) {
   __shared__ int sh[1024];
   int np = 0, nn = 0;
   for (int base = 0; base < n_all; base += 1024) {
@@ -42,10 +43,17 @@ __global__ void __launch_bounds__(1024) compact_kernel(const float* z_all, const
     const int tot = sh[1023];
     const int excl = incl - (pos ? 1 : 0);
     if (v) {
-      if (pos)
-        zp[np + excl] = z_all[i];
-      else
-        zn[nn + (i - base) - excl] = z_all[i];
+      if (ip) {
+        if (pos)
+          ip[np + excl] = i;
+        else
+          in_[nn + (i - base) - excl] = i;
+      } else {
+        if (pos)
+          zp[np + excl] = z_all[i];
+        else
+          zn[nn + (i - base) - excl] = z_all[i];
+      }
     }
     const int cnt = min(1024, n_all - base);
     np += tot;
@@ -60,50 +68,53 @@ __global__ void __launch_bounds__(1024) compact_kernel(const float* z_all, const
 
 constexpr int PAIR_TILE = 2048;
 
-// Partial sums over slice blockIdx.y of the opposite-label list:
+// Partial sums over slice blockIdx.y of the opposite-label list; blockIdx.z = 0: local positives
+// (thread = one of them, sweeping the batch's negatives), 1: local negatives (sweeping positives),
+// so every warp runs one uniform loop:
 //   positive i: g = sum_j sigma(z_j - z_i), l = sum_j softplus(z_j - z_i) over negatives j
 //   negative i: g = sum_j sigma(z_i - z_j) over positives j (no loss: counted once, on positives)
-__global__ void __launch_bounds__(256) pair_kernel(const float* z, const float* y, int n, const float* zp,
-                                                   const float* zn, const int* counts, float* part_g, float* part_l) {
+__global__ void __launch_bounds__(256) pair_kernel(const float* z, int n, const int* ip, const int* in_,
+                                                   const int* counts_loc, const float* zp, const float* zn,
+                                                   const int* counts, float* part_g, float* part_l) {
   __shared__ float tile[PAIR_TILE];
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  const int np = counts[0], nn = counts[1];
-  const bool valid = i < n;
-  const bool pos = valid && y[i] > 0.5f;
+  const int side = blockIdx.z;
+  const int nloc = counts_loc[side];
+  if ((int)(blockIdx.x * blockDim.x) >= nloc) return;  // whole block beyond this side's samples
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool valid = t < nloc;
+  const int i = valid ? (side == 0 ? ip[t] : in_[t]) : 0;
   const float zi = valid ? z[i] : 0.f;
+  const float* list = side == 0 ? zn : zp;
+  const int len = side == 0 ? counts[1] : counts[0];
   const int S = gridDim.y, sidx = blockIdx.y;
-  float g_pos = 0.f, l_pos = 0.f, g_neg = 0.f;
-  // the block serves both kinds of samples: walk the negatives' slice, then the positives' slice
-  for (int side = 0; side < 2; ++side) {
-    const float* list = side == 0 ? zn : zp;
-    const int len = side == 0 ? nn : np;
-    const int per = (len + S - 1) / S;
-    const int j0 = min(len, sidx * per), j1 = min(len, j0 + per);
-    for (int t0 = j0; t0 < j1; t0 += PAIR_TILE) {
-      const int tn = min(PAIR_TILE, j1 - t0);
-      __syncthreads();
-      for (int k = threadIdx.x; k < tn; k += blockDim.x) tile[k] = list[t0 + k];
-      __syncthreads();
-      if (side == 0 && pos) {
-        for (int k = 0; k < tn; ++k) {
-          const float x = tile[k] - zi;                                  // z_j- - z_i+
-          const float e = __expf(-fabsf(x));
-          const float sg = x >= 0.f ? __fdividef(1.f, 1.f + e) : __fdividef(e, 1.f + e);  // sigma(x)
-          g_pos += sg;
-          l_pos += fmaxf(x, 0.f) + __logf(1.f + e);                     // softplus(x)
-        }
-      } else if (side == 1 && valid && !pos) {
-        for (int k = 0; k < tn; ++k) {
-          const float x = zi - tile[k];                                  // z_i- - z_j+
-          const float e = __expf(-fabsf(x));
-          g_neg += x >= 0.f ? __fdividef(1.f, 1.f + e) : __fdividef(e, 1.f + e);
-        }
+  const int per = (len + S - 1) / S;
+  const int j0 = min(len, sidx * per), j1 = min(len, j0 + per);
+  float g = 0.f, l = 0.f;
+  for (int t0 = j0; t0 < j1; t0 += PAIR_TILE) {
+    const int tn = min(PAIR_TILE, j1 - t0);
+    __syncthreads();
+    for (int k = threadIdx.x; k < tn; k += blockDim.x) tile[k] = list[t0 + k];
+    __syncthreads();
+    if (side == 0) {
+      for (int k = 0; k < tn; ++k) {
+        const float x = tile[k] - zi;                        // z_j- - z_i+
+        const float e = __expf(-fabsf(x));
+        const float r = __fdividef(1.f, 1.f + e);
+        g += x >= 0.f ? r : e * r;                           // sigma(x)
+        l += fmaxf(x, 0.f) + __logf(1.f + e);               // softplus(x)
+      }
+    } else {
+      for (int k = 0; k < tn; ++k) {
+        const float x = zi - tile[k];                        // z_i- - z_j+
+        const float e = __expf(-fabsf(x));
+        const float r = __fdividef(1.f, 1.f + e);
+        g += x >= 0.f ? r : e * r;
       }
     }
   }
   if (valid) {
-    part_g[(size_t)sidx * n + i] = pos ? g_pos : g_neg;
-    part_l[(size_t)sidx * n + i] = pos ? l_pos : 0.f;
+    part_g[(size_t)sidx * n + i] = g;
+    part_l[(size_t)sidx * n + i] = side == 0 ? l : 0.f;
   }
 }
 
@@ -340,7 +351,8 @@ cadet_status cadet_routed_logits(const float* logits, int32_t K, const int32_t* 
 size_t cadet_pairwise_workspace_bytes(int32_t n, int32_t n_all) {
   if (n < 0 || n_all < 0) return 0;
   const int S = pair_splits(n);
-  return 256 + 2 * a256((size_t)n_all * 4) + 2 * a256((size_t)S * n * 4) + a256((size_t)n * 4);
+  return 256 + 2 * a256((size_t)n_all * 4) + 2 * a256((size_t)S * n * 4) + a256((size_t)n * 4) +
+         2 * a256((size_t)n * 4) + 256;
 }
 
 cadet_status cadet_pairwise_loss(const float* z, const float* label, int32_t n, const float* z_all,
@@ -365,11 +377,16 @@ cadet_status cadet_pairwise_loss(const float* z, const float* label, int32_t n, 
   float* part_g = zn + a256((size_t)n_all * 4) / 4;
   float* part_l = part_g + a256((size_t)S * n * 4) / 4;
   float* lsample = part_l + a256((size_t)S * n * 4) / 4;
+  int* ip = reinterpret_cast<int*>(lsample + a256((size_t)n * 4) / 4);
+  int* in_ = ip + a256((size_t)n * 4) / 4;
+  int* counts_loc = in_ + a256((size_t)n * 4) / 4;
   cudaError_t e = cudaMemsetAsync(loss_share, 0, 4, st);
   if (n_all > 0 && e == cudaSuccess) {
     compact_kernel<<<1, 1024, 0, st>>>(z_all, label_all, n_all, zp, zn, counts);
     if (n > 0) {
-      pair_kernel<<<dim3(blocks(n, 256), S), 256, 0, st>>>(z, label, n, zp, zn, counts, part_g, part_l);
+      compact_kernel<<<1, 1024, 0, st>>>(z, label, n, nullptr, nullptr, counts_loc, ip, in_);
+      pair_kernel<<<dim3(blocks(n, 256), S, 2), 256, 0, st>>>(z, n, ip, in_, counts_loc, zp, zn, counts, part_g,
+                                                             part_l);
       pair_finalize_kernel<<<blocks(n, 256), 256, 0, st>>>(label, n, counts, part_g, part_l, S, dz_pair, lsample);
       sum_kernel<<<1, 1024, 0, st>>>(lsample, n, loss_share);
     }
