@@ -259,6 +259,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--recompute", action="store_true", help="gradient checkpointing (P:453-455): layers re-run fwd in bwd")
     ap.add_argument("--full-loss", action="store_true",
                     help="NEXT-2: train on Eq. 11 (towers + auxiliary heads + cross-rank RankNet) instead of Eq. 9")
     ap.add_argument("--graph", action="store_true",
@@ -315,7 +316,7 @@ def main():
     inp = host_inp.to(dev)
     torch.cuda.synchronize()
     scfg = StackConfig(d_model=wl["d_model"], n_heads=wl["n_heads"], n_layers=wl["n_layers"], budget=wl["budget"],
-                       L_chunk=wl["L_chunk"], full_loss=args.full_loss)
+                       L_chunk=wl["L_chunk"], full_loss=args.full_loss, recompute=args.recompute)
     stack = CadetStack(scfg, seed=0, device=dev)
     pairs = stack.pairs(inp)
     n_imp = inp.rows.numel()
@@ -479,6 +480,7 @@ def main():
                    "d_model": wl["d_model"], "heads": wl["n_heads"], "L_chunk": wl["L_chunk"],
                    "l2": "inputs > L2 (X 128 MB + activations > 1 GB per step); no flush needed",
                    "parallelism": f"dp{world}", "loss": "Eq. 11 full (NEXT-2)" if args.full_loss else "Eq. 9 routed BCE",
+                   "recompute": bool(args.recompute),
                    "partition": "rank r = shard r of an LPT partition of one user stream into 8 budgets"},
         "tflops": tflops_all, "tflops_per_gpu": tflops_all / world,
         "frac_of_peak_measured": tflops_all / world / float(peaks.get("bf16_tflops", 1663.9)),

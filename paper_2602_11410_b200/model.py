@@ -38,6 +38,7 @@ class StackConfig:
     delta_delay_ms: int = 3_600_000
     mask_flags: int = L.CADET_MASK_TIME
     full_loss: bool = False      # NEXT-2: Eq. 11 = ctx + aux heads (Eq. 10) + RankNet (Eq. 12)
+    recompute: bool = False      # gradient checkpointing: one `saved` buffer, layers re-run fwd in bwd
     J: int = 2                   # auxiliary tasks (long-dwell BCE, duration SE)
 
     @property
@@ -256,7 +257,11 @@ class CadetStack:
             self.losses = torch.zeros(cfg.J + 3, dtype=torch.float32, device=self.dev)
         lib = L.lib()
         self.saved_bytes = lib.cadet_attn_saved_bytes(C.byref(self.acfg), T)
-        self.saved = [torch.empty(self.saved_bytes, dtype=torch.uint8, device=self.dev) for _ in range(nl)]
+        # gradient checkpointing keeps only the layer inputs Hs[l] and ONE saved-activation buffer,
+        # refilled by re-running layer l's forward right before its backward
+        n_saved = 1 if cfg.recompute else nl
+        self.saved = [torch.empty(self.saved_bytes, dtype=torch.uint8, device=self.dev) for _ in range(n_saved)]
+        self._rec_y = torch.empty(T, d, dtype=torch.bfloat16, device=self.dev) if cfg.recompute else None
         self.Hs = [torch.empty(T, d, dtype=torch.bfloat16, device=self.dev) for _ in range(nl + 1)]
         self.dHs = [torch.empty(T, d, dtype=torch.bfloat16, device=self.dev) for _ in range(nl + 1)]
         self.t_p = torch.empty(T, dtype=torch.int64, device=self.dev)
@@ -332,7 +337,7 @@ class CadetStack:
         for l in range(cfg.n_layers):
             w = L.AttnWeights(*[x.data_ptr() for x in self.W[l]])
             chk(lib.cadet_attn_forward(C.byref(self.acfg), C.byref(b), C.byref(w), _vp(self.Hs[l]),
-                                       _vp(self.Hs[l + 1]), _vp(self.Hs[l]), _vp(self.saved[l]), ws, wsn, st))
+                                       _vp(self.Hs[l + 1]), _vp(self.Hs[l]), _vp(self._saved(l)), ws, wsn, st))
         # A7-A8: towers on impression rows + routed BCE
         hc = L.HeadConfig(cfg.K, d, cfg.dh, 0)
         hw = L.HeadWeights(self.W1.data_ptr(), self.b1.data_ptr(), self.w2.data_ptr(), self.b2.data_ptr())
@@ -370,10 +375,13 @@ class CadetStack:
         for l in reversed(range(cfg.n_layers)):
             w = L.AttnWeights(*[x.data_ptr() for x in self.W[l]])
             g = L.AttnGrads(*[x.data_ptr() for x in self.gW[l]])
+            if cfg.recompute:  # refill the single saved buffer with layer l's activations (deterministic fwd)
+                chk(lib.cadet_attn_forward(C.byref(self.acfg), C.byref(b), C.byref(w), _vp(self.Hs[l]),
+                                           _vp(self._rec_y), _vp(self.Hs[l]), _vp(self._saved(l)), ws, wsn, st))
             evs = self._grad_events[l] if group is not None else None
             arr = (C.c_void_p * 4)(*[e.cuda_event for e in evs]) if evs else None
             chk(lib.cadet_attn_backward_ev(C.byref(self.acfg), C.byref(b), C.byref(w), _vp(self.Hs[l]),
-                                           _vp(self.saved[l]), _vp(self.dHs[l + 1]), _vp(self.dHs[l]),
+                                           _vp(self._saved(l)), _vp(self.dHs[l + 1]), _vp(self.dHs[l]),
                                            _vp(self.dHs[l + 1]), C.byref(g), ws, wsn, st, arr))
             if evs:
                 base = l * 7 * dd
@@ -404,6 +412,9 @@ class CadetStack:
             if loss_h is not None:
                 loss_h.copy_(self.loss, non_blocking=True)
         return g
+
+    def _saved(self, l: int) -> torch.Tensor:
+        return self.saved[0 if self.cfg.recompute else l]
 
     def _full_loss_backward(self, inp, group, hc, hw, hg, st):
         """NEXT-2 (Eqs. 10-12): routed logits -> (DP) all-gather with labels -> RankNet share of this

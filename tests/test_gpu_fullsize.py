@@ -245,3 +245,29 @@ def test_full_loss_step_reduces_to_the_routed_bce_step():
     assert np.isfinite(terms).all() and terms[3] > 0       # RankNet share of a one-rank batch
     assert float(c.loss.item()) == pytest.approx(terms[0] + 0.1 * (terms[1] + terms[2]) + 0.1 * terms[3], rel=1e-5)
     assert np.abs(c.grads[n_a:].cpu().numpy()).max() > 0
+
+
+def test_gradient_checkpointing_matches_stored_activations():
+    """Gradient checkpointing: keeping only the layer inputs and re-running each layer's
+    forward before its backward gives the stored-activation gradients (forward kernels are
+    deterministic; only the split-K fp32 atomics of the weight gradients may reorder) and loss,
+    with one saved-activation buffer instead of n_layers."""
+    import bench
+    from paper_2602_11410_b200 import build
+    from paper_2602_11410_b200.model import CadetStack, StackConfig
+    build.build()
+    wl = dict(bench.WORKLOADS["c3"], budget=16384, n_layers=3)
+    users, hinp = bench.build_inputs(wl, 0, pin=False)
+    inp = hinp.to("cuda")
+    mk = lambda rc: CadetStack(StackConfig(d_model=wl["d_model"], n_heads=wl["n_heads"], n_layers=wl["n_layers"],
+                                           budget=wl["budget"], L_chunk=wl["L_chunk"], recompute=rc), device="cuda")
+    a, b = mk(False), mk(True)
+    assert len(b.saved) == 1 and len(a.saved) == 3
+    a.step(inp)
+    b.step(inp)
+    torch.cuda.synchronize()
+    ga, gb = a.grads.cpu().numpy(), b.grads.cpu().numpy()
+    assert np.abs(ga - gb).max() <= 1e-5 * max(1.0, np.abs(ga).max())
+    # the loss is summed with per-warp fp32 atomics (order may differ between runs)
+    assert float(b.loss.item()) == pytest.approx(float(a.loss.item()), rel=1e-6)
+    assert float((a.dHs[0].float() - b.dHs[0].float()).abs().max()) <= 1e-2
