@@ -4,7 +4,8 @@ TEST INFRASTRUCTURE ONLY.  Only `tests/`, `__graft_entry__.smoke()` and
 `bench.py`'s cpu_baseline / `--impl reference` legs may import this module.
 It shares no code with the CUDA path (paper_2602_11410_b200/) and never
 imports it.  Every function follows PAPER.md (P:n) / SPEC.md (S:n) as cited,
-with the readings R1..R31 listed in DESIGN.md §3 (R29-R31: the NEXT-2 full loss).
+with the readings R1..R33 listed in DESIGN.md §3 (R29-R31: the NEXT-2 full loss; R32-R33: the
+NEXT-3 block).
 
 Conventions: row-vector projections y = x.W, W[d_in][d_out] (R1); all math in
 float64 on bf16-valued inputs (R20); heads are per-head slices of width hd of
@@ -548,6 +549,69 @@ def full_loss_backward(H, rows, ctx, aux, bucket, label, ya, lam=(1.0, (0.1, 0.1
     dH1, gc = heads_backward_dz(H, rows, *ctx, dz)
     dH2, ga = heads_backward_dz(H, rows, *aux, dza)
     return terms, dH1 + dH2, gc, ga
+
+
+# ------------------------------------------------------------------ NEXT-3: the full CADET block
+RMS_EPS = 1e-6
+
+
+def rmsnorm(x, gamma, eps=RMS_EPS):
+    """R32: y = x / sqrt(mean(x^2) + eps) * gamma per row (pre-norm, S:644 'two normalization layers')."""
+    x = np.asarray(x, np.float64)
+    r = 1.0 / np.sqrt(np.mean(x * x, axis=-1, keepdims=True) + eps)
+    return x * r * np.asarray(gamma, np.float64)[None, :], r
+
+
+def rmsnorm_backward(x, gamma, dy, eps=RMS_EPS):
+    """Adjoint of rmsnorm: dx = r (g dy) - x r^3 mean(x g dy); dgamma = sum_rows dy x r."""
+    x, dy, g = np.asarray(x, np.float64), np.asarray(dy, np.float64), np.asarray(gamma, np.float64)
+    r = 1.0 / np.sqrt(np.mean(x * x, axis=-1, keepdims=True) + eps)
+    gd = dy * g[None, :]
+    dx = r * gd - x * r ** 3 * np.mean(x * gd, axis=-1, keepdims=True)
+    return dx, np.sum(dy * x * r, axis=0)
+
+
+def gelu(u):
+    """R33: exact GELU u Phi(u) ('smooth nonlinearity')."""
+    u = np.asarray(u, np.float64)
+    return 0.5 * u * (1.0 + np.vectorize(math.erf)(u / math.sqrt(2.0)))
+
+
+def gelu_grad(u):
+    u = np.asarray(u, np.float64)
+    return 0.5 * (1.0 + np.vectorize(math.erf)(u / math.sqrt(2.0))) + u * np.exp(-0.5 * u * u) / math.sqrt(2 * math.pi)
+
+
+def ffn_forward(x, W1, W2):
+    """FFN(x) = GELU(x W1) W2, W1 [d, m d], W2 [m d, d], no biases (R33; multiplier m = 4)."""
+    u = np.asarray(x, np.float64) @ W1
+    return gelu(u) @ W2, u
+
+
+def ffn_backward(x, W1, W2, u, dy):
+    g = gelu(u)
+    dg = dy @ W2.T
+    du = dg * gelu_grad(u)
+    return du @ W1.T, x.T @ du, g.T @ dy
+
+
+def block_forward_seq(X, W, ffn, gammas, t_ms, A, cfg: AttnConfig):
+    """Pre-norm CADET block: H = X + Attn(RMSNorm_1(X)); Y = H + FFN(RMSNorm_2(H))."""
+    Xn, _ = rmsnorm(X, gammas[0])
+    Ya, ca = layer_forward_seq(Xn, W, t_ms, A, cfg)
+    H = np.asarray(X, np.float64) + Ya
+    Hn, _ = rmsnorm(H, gammas[1])
+    Yf, u = ffn_forward(Hn, *ffn)
+    return H + Yf, dict(X=np.asarray(X, np.float64), Xn=Xn, ca=ca, H=H, Hn=Hn, u=u)
+
+
+def block_backward_seq(c, W, ffn, gammas, t_ms, A, dY, cfg: AttnConfig):
+    dHn, dW1f, dW2f = ffn_backward(c["Hn"], *ffn, c["u"], dY)
+    dH_norm, dg2 = rmsnorm_backward(c["H"], gammas[1], dHn)
+    dH = dY + dH_norm
+    dXn, gW, _ = layer_backward_seq(c["ca"], W, t_ms, A, dH, cfg)
+    dX_norm, dg1 = rmsnorm_backward(c["X"], gammas[0], dXn)
+    return dH + dX_norm, dict(gW=gW, dW1f=dW1f, dW2f=dW2f, dg1=dg1, dg2=dg2)
 
 
 # ------------------------------------------------------------------ per-element loop (check 1)

@@ -536,3 +536,94 @@ def test_full_loss_reductions():
     # pairwise-only part of the tower gradient is linear in lam_pair
     t3, dH3, gc3, ga3 = O.full_loss_backward(H, rows, ctx, aux, bucket, label, ya, (1.0, (0.3, 0.2), 1.0))
     assert np.allclose(gc3["db2"] - gc0["db2"], 2.0 * (gc1["db2"] - gc0["db2"]), atol=1e-13)
+
+
+# ------------------------------------------------------------------ NEXT-3: the full block
+def test_rmsnorm_unit_rms_scale_invariance_and_gradient():
+    rng = np.random.default_rng(21)
+    x = rng.normal(size=(4, 16)) * 3
+    y, _ = O.rmsnorm(x, np.ones(16), eps=0.0)
+    assert np.allclose(np.sqrt((y ** 2).mean(-1)), 1.0, atol=1e-14)
+    g = rng.normal(size=16)
+    assert np.allclose(O.rmsnorm(7.5 * x, g, eps=0.0)[0], O.rmsnorm(x, g, eps=0.0)[0], atol=1e-13)
+    dy = rng.normal(size=(4, 16))
+    dx, dg = O.rmsnorm_backward(x, g, dy)
+    f = lambda x_, g_: float(np.sum(O.rmsnorm(x_, g_)[0] * dy))
+    eps = 1e-6
+    for (i, j) in [(0, 0), (2, 7), (3, 15)]:
+        e = np.zeros_like(x)
+        e[i, j] = eps
+        assert dx[i, j] == pytest.approx((f(x + e, g) - f(x - e, g)) / (2 * eps), abs=1e-7)
+    e = np.zeros(16)
+    e[5] = eps
+    assert dg[5] == pytest.approx((f(x, g + e) - f(x, g - e)) / (2 * eps), abs=1e-7)
+
+
+def test_gelu_values_and_ffn_gradient():
+    """Exact GELU u Phi(u): Phi(1) = 0.8413447460685429 (normal CDF), GELU(0) = 0, odd-part identity
+    GELU(u) - GELU(-u) = u; FFN adjoint by finite differences."""
+    assert O.gelu(0.0) == 0.0
+    assert O.gelu(1.0) == pytest.approx(0.8413447460685429, abs=1e-15)
+    assert O.gelu(-1.0) == pytest.approx(-0.15865525393145707, abs=1e-15)
+    u = np.linspace(-4, 4, 17)
+    assert np.allclose(O.gelu(u) - O.gelu(-u), u, atol=1e-14)
+    eps = 1e-6
+    assert np.allclose(O.gelu_grad(u), (O.gelu(u + eps) - O.gelu(u - eps)) / (2 * eps), atol=1e-8)
+    rng = np.random.default_rng(22)
+    x = rng.normal(size=(5, 8))
+    W1, W2 = rng.normal(size=(8, 32)) / 3, rng.normal(size=(32, 8)) / 5
+    y, uu = O.ffn_forward(x, W1, W2)
+    dy = rng.normal(size=y.shape)
+    dx, dW1, dW2 = O.ffn_backward(x, W1, W2, uu, dy)
+    f = lambda x_, a, b: float(np.sum(O.ffn_forward(x_, a, b)[0] * dy))
+    for (M, grad, k) in ((x, dx, 0), (W1, dW1, 1), (W2, dW2, 2)):
+        e = np.zeros_like(M)
+        e[1, 2] = eps
+        args_p = [x, W1, W2]
+        args_m = [x, W1, W2]
+        args_p[k] = M + e
+        args_m[k] = M - e
+        assert grad[1, 2] == pytest.approx((f(*args_p) - f(*args_m)) / (2 * eps), abs=1e-7)
+
+
+def test_block_backward_by_finite_differences_and_zero_ffn_reduction():
+    """Pre-norm block through attention: dX and one weight of each part against central
+    differences; W2 = 0 reduces the block to X + Attn(RMSNorm_1(X))."""
+    b = G.fixed_lengths_batch([7], seed=3, cfg=G.stress_config())
+    d, H = 8, 2
+    cfg = O.AttnConfig(d_model=d, n_heads=H, delta_delay_ms=120_000, rope_phi_min=0.5, rope_base=1e4,
+                       rope_dt_max_ms=86_400_000)
+    meta = O.SeqMeta(cu=np.array([0, 7]), t_ms=b.timestamps, n_cand=np.zeros(1, np.int64))
+    A = O.seq_mask(meta, 0, cfg)
+    rng = np.random.default_rng(23)
+    X = rng.normal(size=(7, d))
+    W = [rng.normal(size=(d, d)) / np.sqrt(d) for _ in range(7)]
+    ffn = (rng.normal(size=(d, 4 * d)) / 3, rng.normal(size=(4 * d, d)) / 6)
+    gam = (1.0 + 0.1 * rng.normal(size=d), 1.0 + 0.1 * rng.normal(size=d))
+    Y, c = O.block_forward_seq(X, W, ffn, gam, b.timestamps, A, cfg)
+    dY = rng.normal(size=Y.shape)
+    dX, g = O.block_backward_seq(c, W, ffn, gam, b.timestamps, A, dY, cfg)
+    f = lambda X_=X, W_=W, ffn_=ffn, gam_=gam: float(np.sum(O.block_forward_seq(X_, W_, ffn_, gam_, b.timestamps, A,
+                                                                                   cfg)[0] * dY))
+    eps = 1e-6
+    e = np.zeros_like(X)
+    e[3, 4] = eps
+    assert dX[3, 4] == pytest.approx((f(X_=X + e) - f(X_=X - e)) / (2 * eps), abs=1e-6)
+    e = np.zeros_like(ffn[0])
+    e[2, 9] = eps
+    assert g["dW1f"][2, 9] == pytest.approx((f(ffn_=(ffn[0] + e, ffn[1])) - f(ffn_=(ffn[0] - e, ffn[1]))) / (2 * eps),
+                                            abs=1e-6)
+    e = np.zeros(d)
+    e[1] = eps
+    assert g["dg1"][1] == pytest.approx((f(gam_=(gam[0] + e, gam[1])) - f(gam_=(gam[0] - e, gam[1]))) / (2 * eps),
+                                        abs=1e-6)
+    ew = np.zeros_like(W[1])
+    ew[0, 3] = eps
+    Wp = [w.copy() for w in W]
+    Wm = [w.copy() for w in W]
+    Wp[1] = W[1] + ew
+    Wm[1] = W[1] - ew
+    assert g["gW"][1][0, 3] == pytest.approx((f(W_=Wp) - f(W_=Wm)) / (2 * eps), abs=1e-6)
+    Y0, _ = O.block_forward_seq(X, W, (ffn[0], np.zeros_like(ffn[1])), gam, b.timestamps, A, cfg)
+    Ya, _ = O.layer_forward_seq(O.rmsnorm(X, gam[0])[0], W, b.timestamps, A, cfg)
+    assert np.allclose(Y0, X + Ya, atol=1e-13)
