@@ -170,6 +170,8 @@ def step_flops(wl: dict, tokens: int, pairs: int, n_imp: int, dh: int, K: int = 
     attn_f = nl * 4.0 * d * pairs
     attn_b = nl * 8.0 * d * pairs
     gemm = nl * (14.0 + 28.0) * tokens * d * d + 6.0 * n_imp * K * d * dh
+    if wl.get("block"):  # NEXT-3 FFN: two [d, m d] GEMMs, 2 T d (m d) each fwd, twice that bwd
+        gemm += nl * 3.0 * 2.0 * (2.0 * tokens * d * wl.get("ffn_mult", 4) * d)
     return {"gemm": gemm, "attn_fwd": attn_f, "attn_bwd": attn_b}
 
 
@@ -200,6 +202,11 @@ def run_oracle_step(seqs, wl: dict, seed: int):
     d, H, nl = wl["d_model"], wl["n_heads"], wl["n_layers"]
     cfg = O.AttnConfig(d_model=d, n_heads=H)
     Ws = [[w.astype(np.float64) for w in G.layer_weights(seed, l, d).as_list()] for l in range(nl)]
+    blk = bool(wl.get("block"))
+    if blk:  # NEXT-3: the pre-norm block (RMSNorm, attention, RMSNorm, FFN)
+        bws = [G.block_weights(seed, l, d) for l in range(nl)]
+        ffs = [(w.W1.astype(np.float64), w.W2.astype(np.float64)) for w in bws]
+        gms = [(w.gamma1.astype(np.float64), w.gamma2.astype(np.float64)) for w in bws]
     hw = G.head_weights(seed, 2, d, d // 2)
     rng = np.random.default_rng(seed)
     loss = 0.0
@@ -209,6 +216,10 @@ def run_oracle_step(seqs, wl: dict, seed: int):
         X = rng.standard_normal((e - a, d))
         caches = []
         for l in range(nl):
+            if blk:
+                X, c = O.block_forward_seq(X, Ws[l], ffs[l], gms[l], t, A, cfg)
+                caches.append((None, c))
+                continue
             Y, c = O.layer_forward_seq(X, Ws[l], t, A, cfg)
             caches.append((X, c))
             X = X + Y
@@ -220,6 +231,9 @@ def run_oracle_step(seqs, wl: dict, seed: int):
         dX = dH
         for l in reversed(range(nl)):
             Xl, c = caches[l]
+            if blk:
+                dX, _ = O.block_backward_seq(c, Ws[l], ffs[l], gms[l], t, A, dX, cfg)
+                continue
             dXa, gW, _ = O.layer_backward_seq(c, Ws[l], t, A, dX, cfg)
             dX = dX + dXa
     return loss
@@ -244,8 +258,8 @@ def time_oracle(users, wl, seed, budget_s=15.0, max_tokens=None):
     t0 = time.perf_counter()
     run_oracle_step(seqs, wl, seed)
     dt = time.perf_counter() - t0
-    desc = (f"first {len(seqs)} whole chunks ({tok} tokens) of the rank-0 batch, {wl['n_layers']} layer(s) "
-            f"fwd+bwd + towers, numpy fp64")
+    desc = (f"first {len(seqs)} whole chunks ({tok} tokens) of the rank-0 batch, {wl['n_layers']} "
+            f"{'pre-norm block(s)' if wl.get('block') else 'layer(s)'} fwd+bwd + towers, numpy fp64")
     return tok / dt, tok, dt, desc
 
 
@@ -262,10 +276,12 @@ def main():
     ap.add_argument("--recompute", action="store_true", help="gradient checkpointing (P:453-455): layers re-run fwd in bwd")
     ap.add_argument("--full-loss", action="store_true",
                     help="NEXT-2: train on Eq. 11 (towers + auxiliary heads + cross-rank RankNet) instead of Eq. 9")
+    ap.add_argument("--block", action="store_true",
+                    help="NEXT-3: every layer is the pre-norm CADET block (RMSNorm, gated attention, RMSNorm, FFN x4)")
     ap.add_argument("--graph", action="store_true",
                     help="replay the step as one CUDA graph (measured: no gain over eager launches on C4)")
     args = ap.parse_args()
-    wl = WORKLOADS[args.workload]
+    wl = dict(WORKLOADS[args.workload], block=args.block)
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -274,6 +290,8 @@ def main():
                            "8 heads x 128, 1 gated layer + K=2 towers, fwd+bwd, T=65536/rank",
                      "c3": "C3 paper-shaped: 8 gated layers, d 352, 4 heads x 88, Lc 2048, K=2 towers, fwd+bwd, "
                            "T=65536/rank"}[args.workload]
+    if args.block:
+        workload_name += "; every layer the pre-norm CADET block (RMSNorm, attention, RMSNorm, FFN x4; NEXT-3)"
 
     if args.impl == "reference":
         # The reference arm is the CPU oracle (no reference implementation exists): rank 0 only.
@@ -316,7 +334,7 @@ def main():
     inp = host_inp.to(dev)
     torch.cuda.synchronize()
     scfg = StackConfig(d_model=wl["d_model"], n_heads=wl["n_heads"], n_layers=wl["n_layers"], budget=wl["budget"],
-                       L_chunk=wl["L_chunk"], full_loss=args.full_loss, recompute=args.recompute)
+                       L_chunk=wl["L_chunk"], full_loss=args.full_loss, recompute=args.recompute, block=args.block)
     stack = CadetStack(scfg, seed=0, device=dev)
     pairs = stack.pairs(inp)
     n_imp = inp.rows.numel()
@@ -481,6 +499,8 @@ def main():
                    "l2": "inputs > L2 (X 128 MB + activations > 1 GB per step); no flush needed",
                    "parallelism": f"dp{world}", "loss": "Eq. 11 full (NEXT-2)" if args.full_loss else "Eq. 9 routed BCE",
                    "recompute": bool(args.recompute),
+                   "layer": "pre-norm CADET block: RMSNorm, gated attention, RMSNorm, FFN x4 (NEXT-3)" if args.block
+                   else "gated attention layer (Eq. 3-7) + residual",
                    "partition": "rank r = shard r of an LPT partition of one user stream into 8 budgets"},
         "tflops": tflops_all, "tflops_per_gpu": tflops_all / world,
         "frac_of_peak_measured": tflops_all / world / float(peaks.get("bf16_tflops", 1663.9)),

@@ -259,6 +259,34 @@ cadet_status cadet_heads_backward(const cadet_head_config* h_h, const cadet_head
                                   int32_t accumulate, void* dHs, const cadet_head_grads* g_h, void* ws,
                                   size_t ws_bytes, cadet_stream_t stream);
 
+/* ------------------------------------------------------------------ NEXT-3: the CADET block
+ * Pre-norm block ("two normalization layers" + "feed-forward network", readings R32/R33):
+ *   Xn = RMSNorm_1(X);  H = X + Attn(Xn)     cadet_rmsnorm_forward, cadet_attn_forward(X := Xn, resid := X)
+ *   Hn = RMSNorm_2(H);  Y = H + FFN(Hn)      cadet_rmsnorm_forward, cadet_ffn_forward(resid := H)
+ * Backward in reverse: cadet_ffn_backward(dresid NULL) -> dHn; cadet_rmsnorm_backward(H, dHn, dresid := dY)
+ * -> dH; cadet_attn_backward(dY := dH) -> dXn; cadet_rmsnorm_backward(X, dXn, dresid := dH) -> dX.
+ *
+ * RMSNorm (R32): Y = X / sqrt(mean_row(X^2) + 1e-6) * gamma.  X, Y bf16 [T, d] row-major, gamma fp32
+ * [d], rstd fp32 [T] (saved for the backward).  d % 8 == 0, d <= 1024; else CADET_E_ARG. */
+cadet_status cadet_rmsnorm_forward(const void* X, const float* gamma, int32_t T, int32_t d, void* Y, float* rstd,
+                                   cadet_stream_t stream);
+/* dX = rstd gamma dY - X rstd^3 mean_row(X gamma dY) (+ dresid, nullable), bf16 [T, d];
+ * dgamma fp32 [d] = sum_rows dY X rstd, OVERWRITTEN (column sums: fp32 atomics, order not fixed). */
+cadet_status cadet_rmsnorm_backward(const void* X, const float* gamma, const float* rstd, const void* dY,
+                                    const void* dresid, int32_t T, int32_t d, void* dX, float* dgamma,
+                                    cadet_stream_t stream);
+/* FFN (R33): U = X W1, G = GELU(U) (exact, erf), Y = G W2 (+ resid, nullable).  X, Y, resid bf16 [T, d];
+ * W1 bf16 [d, m d], W2 bf16 [m d, d] (row-vector convention y = x W, R1); U and G bf16 [T, m d] are
+ * written for the backward.  d % 32 == 0.  Two tcgen05 GEMM launches, GELU in the first's epilogue. */
+cadet_status cadet_ffn_forward(const void* X, const void* W1, const void* W2, const void* resid, int32_t T, int32_t d,
+                               int32_t m, void* Y, void* U, void* G, cadet_stream_t stream);
+/* dU = (dY W2^T) * GELU'(U) (in ws), dX = dU W1^T (+ dresid, nullable) bf16 [T, d]; dW1 fp32 [d, m d]
+ * = X^T dU and dW2 fp32 [m d, d] = G^T dY, OVERWRITTEN.  ws >= cadet_ffn_workspace_bytes(T, d, m). */
+size_t cadet_ffn_workspace_bytes(int32_t T, int32_t d, int32_t m);
+cadet_status cadet_ffn_backward(const void* X, const void* W1, const void* W2, const void* U, const void* G,
+                                const void* dY, const void* dresid, int32_t T, int32_t d, int32_t m, void* dX,
+                                float* dW1, float* dW2, void* ws, size_t ws_bytes, cadet_stream_t stream);
+
 /* ------------------------------------------------------------------ A0 / A13: chunk and pack
  * Chunk: split each sequence [a, e) of cu_in at e - L, e - 2L, ... (newest chunk full, oldest may be
  * short) and write the refined offsets in buffer order to cu_out (capacity cap entries);

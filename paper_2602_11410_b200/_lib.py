@@ -101,6 +101,11 @@ SIGNATURES = {
     "cadet_full_loss_grads": (I32, [C.POINTER(LossConfig), P, I32, P, P, P, P, P, P, I32, P, P, P, P]),
     "cadet_heads_backward": (I32, [C.POINTER(HeadConfig), C.POINTER(HeadWeights), P, P, I32, I32, P, P, I32, P,
                                    C.POINTER(HeadGrads), P, SZ, P]),
+    "cadet_rmsnorm_forward": (I32, [P, P, I32, I32, P, P, P]),
+    "cadet_rmsnorm_backward": (I32, [P, P, P, P, P, I32, I32, P, P, P]),
+    "cadet_ffn_workspace_bytes": (SZ, [I32, I32, I32]),
+    "cadet_ffn_forward": (I32, [P, P, P, P, I32, I32, I32, P, P, P, P]),
+    "cadet_ffn_backward": (I32, [P, P, P, P, P, P, P, I32, I32, I32, P, P, P, P, SZ, P]),
     "cadet_chunk": (I32, [P, I32, I32, P, I32, P, P, P]),
     "cadet_pack": (I32, [P, P, P, I32, I32, I32, P, P, P, P, P, P, P, P, SZ, P]),
     "cadet_pack_workspace_bytes": (SZ, [I32]),

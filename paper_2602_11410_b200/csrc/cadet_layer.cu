@@ -704,6 +704,72 @@ cadet_status cadet_heads_loss_backward(const cadet_head_config* h, const cadet_h
   return cuda_err(e, "heads backward");
 }
 
+// ------------------------------------------------------------------ NEXT-3: FFN of the CADET block (R33)
+static cadet_status check_ffn(int T, int d, int m, const void* p0, const void* p1, const void* p2) {
+  if (T < 0 || d <= 0 || m <= 0 || d % 32 || (T > 0 && !p0) || !p1 || !p2) {
+    set_error("ffn: bad argument (d % 32 == 0, m >= 1, non-null operands)");
+    return CADET_E_ARG;
+  }
+  return CADET_OK;
+}
+
+size_t cadet_ffn_workspace_bytes(int32_t T, int32_t d, int32_t m) { return a256((size_t)T * d * m * 2); }
+
+cadet_status cadet_ffn_forward(const void* X, const void* W1, const void* W2, const void* resid, int32_t T, int32_t d,
+                               int32_t m, void* Y, void* U, void* G, cadet_stream_t stream) {
+  cadet_status s = check_ffn(T, d, m, X, W1, W2);
+  if (s) return s;
+  if (T == 0) return CADET_OK;
+  if (!Y || !U || !G) return check_ffn(T, d, m, nullptr, nullptr, nullptr);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const int N = d * m;
+  // U = X W1 (saved pre-activation), G = GELU(U): one GEMM, the activation in its epilogue
+  GemmProblem g1 = prob(T, N, d, act(X, T, d), w_fwd(W1, d, N), EPI_GELU);
+  g1.epi.out = G;
+  g1.epi.aux = U;
+  cudaError_t e = gemm_launch(&g1, 1, pick_bn(T, N), st);
+  if (e == cudaSuccess) {  // Y = G W2 (+ resid)
+    GemmProblem g2 = prob(T, d, N, act(G, T, N), w_fwd(W2, N, d), EPI_STORE);
+    g2.epi.out = Y;
+    g2.epi.resid = resid;
+    e = gemm_launch(&g2, 1, pick_bn(T, d), st);
+  }
+  return cuda_err(e, "ffn forward");
+}
+
+cadet_status cadet_ffn_backward(const void* X, const void* W1, const void* W2, const void* U, const void* G,
+                                const void* dY, const void* dresid, int32_t T, int32_t d, int32_t m, void* dX,
+                                float* dW1, float* dW2, void* ws, size_t ws_bytes, cadet_stream_t stream) {
+  cadet_status s = check_ffn(T, d, m, X, W1, W2);
+  if (s) return s;
+  if (!dW1 || !dW2 || (T > 0 && (!U || !G || !dY || !dX || !ws))) return check_ffn(T, d, m, nullptr, nullptr, nullptr);
+  const size_t need = cadet_ffn_workspace_bytes(T, d, m);
+  if (ws_bytes < need) return ws_err(ws_bytes, need);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const int N = d * m;
+  cudaError_t e = cudaMemsetAsync(dW1, 0, (size_t)d * N * 4, st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(dW2, 0, (size_t)N * d * 4, st);
+  if (T == 0) return cuda_err(e, "ffn backward");
+  void* dU = ws;
+  if (e == cudaSuccess) {  // dU = (dY W2^T) * GELU'(U)  with  dW2 = G^T dY  in the same launch
+    GemmProblem g = prob(T, N, d, act(dY, T, d), w_bwd(W2, N, d), EPI_GELU_BWD);
+    g.epi.out = dU;
+    g.epi.aux = const_cast<void*>(U);
+    const int bnw = pick_bn_wgrad(d);
+    GemmProblem gw = wgrad(G, dY, dW2, T, N, d, bnw);
+    e = gemm_launch2(&g, 1, pick_bn(T, N), &gw, 1, bnw, st);
+  }
+  if (e == cudaSuccess) {  // dX = dU W1^T (+ dresid)  with  dW1 = X^T dU
+    GemmProblem g = prob(T, d, N, act(dU, T, N), w_bwd(W1, d, N), EPI_STORE);
+    g.epi.out = dX;
+    g.epi.resid = dresid;
+    const int bnw = pick_bn_wgrad(N);
+    GemmProblem gw = wgrad(X, dU, dW1, T, d, N, bnw);
+    e = gemm_launch2(&g, 1, pick_bn(T, d), &gw, 1, bnw, st);
+  }
+  return cuda_err(e, "ffn backward");
+}
+
 }  // extern "C"
 
 namespace cadet {

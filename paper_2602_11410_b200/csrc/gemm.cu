@@ -86,7 +86,13 @@ __device__ __forceinline__ void kb_to_seg(const KProb& q, int kb, int& seg, int&
 // problems, so e.g. a plain store does not carry the gate + RoPE epilogue's registers.
 __host__ __device__ constexpr uint32_t MB(int m) { return 1u << m; }
 constexpr uint32_t MODES_ALL = MB(EPI_STORE) | MB(EPI_GATE) | MB(EPI_GATE_ROPE) | MB(EPI_GATE_BWD) | MB(EPI_ATOMIC) |
-                               MB(EPI_HEAD);
+                               MB(EPI_HEAD) | MB(EPI_GELU) | MB(EPI_GELU_BWD);
+
+// exact GELU u Phi(u) and its derivative (R33)
+__device__ __forceinline__ float gelu_f(float u) { return 0.5f * u * (1.f + erff(u * 0.7071067811865476f)); }
+__device__ __forceinline__ float gelu_grad_f(float u) {
+  return 0.5f * (1.f + erff(u * 0.7071067811865476f)) + u * 0.3989422804014327f * __expf(-0.5f * u * u);
+}
 #define HAS_MODE(m) ((MODES & MB(m)) != 0u)
 __device__ __forceinline__ void load_bf16x32(const void* base, float (&x)[32]) {
   const uint4* p = reinterpret_cast<const uint4*>(base);
@@ -208,6 +214,19 @@ __device__ __forceinline__ void run_epilogue(const EpiParams& e, int row, int M,
 #pragma unroll
       for (int q = 0; q < 8; ++q)
         atomicAdd(reinterpret_cast<float4*>(o) + q, make_float4(v[q * 4], v[q * 4 + 1], v[q * 4 + 2], v[q * 4 + 3]));
+    } break;
+    case EPI_GELU: if constexpr (HAS_MODE(EPI_GELU)) {
+      if (e.aux) store_any32(e.aux, e.aux_f32, in_off, v);
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] = gelu_f(v[j]);
+      store_any32(e.out, e.out_f32, off, v);
+    } break;
+    case EPI_GELU_BWD: if constexpr (HAS_MODE(EPI_GELU_BWD)) {
+      float u[32];
+      load_any32(e.aux, e.aux_f32, in_off, u);
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] *= gelu_grad_f(u[j]);
+      store_any32(e.out, e.out_f32, off, v);
     } break;
     case EPI_HEAD: if constexpr (HAS_MODE(EPI_HEAD)) {
       // a 32-column slice covers at most two towers when dh % 32 != 0 (dh >= 32)
@@ -340,6 +359,7 @@ __device__ __forceinline__ const void* epi_primary(const EpiParams& e) {
     case EPI_STORE:
       return e.resid_f32 ? nullptr : e.resid;
     case EPI_GATE_BWD:
+    case EPI_GELU_BWD:
       return e.aux_f32 ? nullptr : e.aux;
     default:
       return nullptr;
@@ -413,6 +433,22 @@ __device__ __forceinline__ void run_epilogue_warp(const EpiParams& e, int row0, 
       }
       warp_store_rows(stg, e.out, e.out_f32, off0, e.ldo, rows_valid, v);
       warp_store_rows(stg, e.out2, e.out2_f32, off0, e.ldo, rows_valid, r);
+    } break;
+    case EPI_GELU: if constexpr (HAS_MODE(EPI_GELU)) {
+      if (e.aux) warp_store_rows(stg, e.aux, e.aux_f32, off0, e.ldo, rows_valid, v);
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] = gelu_f(v[j]);
+      warp_store_rows(stg, e.out, e.out_f32, off0, e.ldo, rows_valid, v);
+    } break;
+    case EPI_GELU_BWD: if constexpr (HAS_MODE(EPI_GELU_BWD)) {
+      float u[32];
+      if (pre)
+        warp_sts_rows_bf16(stg, *reinterpret_cast<const uint4(*)[4]>(pre), u);
+      else
+        warp_load_rows(stg, e.aux, e.aux_f32, off0, e.ldo, rows_valid, u);
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] *= gelu_grad_f(u[j]);
+      warp_store_rows(stg, e.out, e.out_f32, off0, e.ldo, rows_valid, v);
     } break;
     default:
       break;
@@ -837,24 +873,41 @@ static cudaError_t launch_pair_modes(const GemmKParams& P, uint32_t modes, cudaS
     case MB(EPI_GATE_BWD) | MB(EPI_ATOMIC): return launch_pair<MB(EPI_GATE_BWD) | MB(EPI_ATOMIC)>(P, stream);
     case MB(EPI_ATOMIC): return launch_pair<MB(EPI_ATOMIC)>(P, stream);
     case MB(EPI_HEAD): return launch_pair<MB(EPI_HEAD)>(P, stream);
+    case MB(EPI_GELU): return launch_pair<MB(EPI_GELU)>(P, stream);
+    case MB(EPI_GELU_BWD) | MB(EPI_ATOMIC): return launch_pair<MB(EPI_GELU_BWD) | MB(EPI_ATOMIC)>(P, stream);
     default: return launch_pair<MODES_ALL>(P, stream);
   }
 }
 
-template <int BN>
+template <int BN, uint32_t MODES>
 static cudaError_t launch_bn(const GemmKParams& P, cudaStream_t stream) {
   using C = GemmCfg<BN>;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e =
-        cudaFuncSetAttribute(gemm_kernel<BN, MODES_ALL>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    cudaError_t e = cudaFuncSetAttribute(gemm_kernel<BN, MODES>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     if (e != cudaSuccess) return e;
     attr = true;
   }
   const int grid = P.total_units < num_sms() ? P.total_units : num_sms();
   ProfScope ps(PROF_GEMM, stream, 1);
-  gemm_kernel<BN, MODES_ALL><<<grid, GEMM_THREADS, C::SMEM, stream>>>(P);
+  gemm_kernel<BN, MODES><<<grid, GEMM_THREADS, C::SMEM, stream>>>(P);
   return cudaGetLastError();
+}
+
+template <int BN>
+static cudaError_t launch_bn_modes(const GemmKParams& P, uint32_t modes, cudaStream_t stream) {
+  switch (modes) {
+    case MB(EPI_STORE): return launch_bn<BN, MB(EPI_STORE)>(P, stream);
+    case MB(EPI_GATE): return launch_bn<BN, MB(EPI_GATE)>(P, stream);
+    case MB(EPI_GATE_ROPE): return launch_bn<BN, MB(EPI_GATE_ROPE)>(P, stream);
+    case MB(EPI_STORE) | MB(EPI_ATOMIC): return launch_bn<BN, MB(EPI_STORE) | MB(EPI_ATOMIC)>(P, stream);
+    case MB(EPI_GATE_BWD) | MB(EPI_ATOMIC): return launch_bn<BN, MB(EPI_GATE_BWD) | MB(EPI_ATOMIC)>(P, stream);
+    case MB(EPI_ATOMIC): return launch_bn<BN, MB(EPI_ATOMIC)>(P, stream);
+    case MB(EPI_HEAD): return launch_bn<BN, MB(EPI_HEAD)>(P, stream);
+    case MB(EPI_GELU): return launch_bn<BN, MB(EPI_GELU)>(P, stream);
+    case MB(EPI_GELU_BWD) | MB(EPI_ATOMIC): return launch_bn<BN, MB(EPI_GELU_BWD) | MB(EPI_ATOMIC)>(P, stream);
+    default: return launch_bn<BN, MODES_ALL>(P, stream);
+  }
 }
 
 cudaError_t gemm_launch(const GemmProblem* probs, int nprob, int bn, cudaStream_t stream) {
@@ -897,7 +950,7 @@ cudaError_t gemm_launch(const GemmProblem* probs, int nprob, int bn, cudaStream_
   uint32_t modes = 0;
   for (int p = 0; p < nprob; ++p) modes |= MB(probs[p].epi.mode);
   if (pair) return launch_pair_modes(P, modes, stream);
-  return bn == 256 ? launch_bn<256>(P, stream) : launch_bn<128>(P, stream);
+  return bn == 256 ? launch_bn_modes<256>(P, modes, stream) : launch_bn_modes<128>(P, modes, stream);
 }
 
 }  // namespace cadet

@@ -13,6 +13,8 @@ enum EpiMode : int32_t {
   EPI_GATE_BWD = 3,   // g = sigma(aux); out = acc*src*g*(1-g); out2 = acc*g + resid (A12)
   EPI_ATOMIC = 4,     // out += acc (fp32 red.add; split-K weight gradients)
   EPI_HEAD = 5,       // pre = acc + b1; aux = pre; logits[row, n/dh] += relu(pre).w2 (Eq. 8)
+  EPI_GELU = 6,       // NEXT-3 FFN: aux = acc (pre-activation); out = GELU(acc) (R33)
+  EPI_GELU_BWD = 7,   // NEXT-3 FFN: out = acc * GELU'(aux)
 };
 
 struct EpiParams {

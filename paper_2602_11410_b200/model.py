@@ -40,6 +40,8 @@ class StackConfig:
     full_loss: bool = False      # NEXT-2: Eq. 11 = ctx + aux heads (Eq. 10) + RankNet (Eq. 12)
     recompute: bool = False      # gradient checkpointing: one `saved` buffer, layers re-run fwd in bwd
     J: int = 2                   # auxiliary tasks (long-dwell BCE, duration SE)
+    block: bool = False          # NEXT-3: pre-norm CADET block (RMSNorm, attention, RMSNorm, FFN, R32/R33)
+    ffn_mult: int = 4            # FFN width multiplier m
 
     @property
     def dh(self) -> int:
@@ -230,28 +232,45 @@ class CadetStack:
         self.b1 = torch.from_numpy(hw.b1.reshape(-1).copy()).to(self.dev)
         self.w2 = torch.from_numpy(hw.w2.reshape(-1).copy()).to(self.dev)
         self.b2 = torch.from_numpy(hw.b2.copy()).to(self.dev)
-        # flat fp32 gradient buffer: 7 d^2 per layer, the towers (+ the aux heads, NEXT-2); every slice
-        # starts on a 256-byte boundary (the split-K weight-gradient epilogue adds float4 atomics)
+        # flat fp32 gradient buffer: 7 d^2 per layer (+ the block's FFN and RMSNorm scales, NEXT-3), the
+        # towers (+ the aux heads, NEXT-2); every slice starts on a 256-byte boundary (the split-K
+        # weight-gradient epilogue adds float4 atomics)
         N = cfg.K * cfg.dh
         Na = cfg.J * cfg.da if cfg.full_loss else 0
+        md = cfg.ffn_mult * d
         pad = lambda x: -(-x // 64) * 64
-        sizes = [d * d] * (7 * nl) + [d * N, N, N, cfg.K] + ([d * Na, Na, Na, cfg.J] if cfg.full_loss else [])
+        per_layer = [d * d] * 7 + ([d * md, md * d, d, d] if cfg.block else [])
+        npl = len(per_layer)
+        sizes = per_layer * nl + [d * N, N, N, cfg.K] + ([d * Na, Na, Na, cfg.J] if cfg.full_loss else [])
         self.n_grad = sum(pad(x) for x in sizes)
         self.grads = torch.zeros(self.n_grad, dtype=torch.float32, device=self.dev)
-        views, off = [], 0
+        views, offs, off = [], [], 0
         for x in sizes:
             views.append(self.grads[off:off + x])
+            offs.append(off)
             off += pad(x)
-        self.gW = [views[7 * l:7 * l + 7] for l in range(nl)]
-        self.gW1, self.gb1, self.gw2, self.gb2 = views[7 * nl:7 * nl + 4]
-        self._tower_off = 7 * nl * pad(d * d)  # towers (and aux heads) follow the layers
+        self.gW = [views[npl * l:npl * l + 7] for l in range(nl)]
+        # DP all-reduce groups per layer, in the order their gradients complete in the backward
+        rng_ = lambda a, b: self.grads[offs[a]:offs[b - 1] + pad(sizes[b - 1])]
+        self._groups = [dict(attn=(rng_(npl * l + 6, npl * l + 7), rng_(npl * l + 4, npl * l + 6),
+                                   rng_(npl * l + 1, npl * l + 4), rng_(npl * l, npl * l + 1)),
+                             ffn=rng_(npl * l + 7, npl * l + 10) if cfg.block else None,
+                             g1=rng_(npl * l + 10, npl * l + 11) if cfg.block else None) for l in range(nl)]
+        self.gW1, self.gb1, self.gw2, self.gb2 = views[npl * nl:npl * nl + 4]
+        self._tower_off = offs[npl * nl]  # towers (and aux heads) follow the layers
+        if cfg.block:  # NEXT-3: RMSNorm scales (fp32) and FFN weights (bf16) per layer; grads dW1f, dW2f, dg2, dg1
+            bw = [G.block_weights(seed, l, d, cfg.ffn_mult) for l in range(nl)]
+            f32 = lambda a: torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).to(self.dev)
+            self.gam = [(f32(w.gamma1), f32(w.gamma2)) for w in bw]
+            self.F = [(bf(w.W1), bf(w.W2)) for w in bw]
+            self.gF = [views[npl * l + 7:npl * l + 11] for l in range(nl)]
         if cfg.full_loss:  # NEXT-2 auxiliary heads (Eq. 10): J towers of width da, never routed
             aw = G.head_weights(seed + 1, cfg.J, d, cfg.da)
             self.aW1 = bf(np.concatenate([aw.W1[k] for k in range(cfg.J)], axis=1))
             self.ab1 = torch.from_numpy(aw.b1.reshape(-1).copy()).to(self.dev)
             self.aw2 = torch.from_numpy(aw.w2.reshape(-1).copy()).to(self.dev)
             self.ab2 = torch.from_numpy(aw.b2.copy()).to(self.dev)
-            self.agW1, self.agb1, self.agw2, self.agb2 = views[7 * nl + 4:7 * nl + 8]
+            self.agW1, self.agb1, self.agw2, self.agb2 = views[npl * nl + 4:npl * nl + 8]
             self.lcfg = L.LossConfig()
             L.lib().cadet_default_loss_config(C.byref(self.lcfg), cfg.J)
             self.losses = torch.zeros(cfg.J + 3, dtype=torch.float32, device=self.dev)
@@ -263,6 +282,12 @@ class CadetStack:
         self.saved = [torch.empty(self.saved_bytes, dtype=torch.uint8, device=self.dev) for _ in range(n_saved)]
         self._rec_y = torch.empty(T, d, dtype=torch.bfloat16, device=self.dev) if cfg.recompute else None
         self.Hs = [torch.empty(T, d, dtype=torch.bfloat16, device=self.dev) for _ in range(nl + 1)]
+        if cfg.block:  # per (saved) layer: Xn, H (after attention), Hn, rstd1, rstd2, U, G; backward scratch
+            bt = lambda n: torch.empty(T, n, dtype=torch.bfloat16, device=self.dev)
+            ft = lambda: torch.empty(T, dtype=torch.float32, device=self.dev)
+            self.blk = [dict(Xn=bt(d), H=bt(d), Hn=bt(d), r1=ft(), r2=ft(), U=bt(md), G=bt(md)) for _ in range(n_saved)]
+            self._dA, self._dB = bt(d), bt(d)
+            self._fws = ops.workspace(lib.cadet_ffn_workspace_bytes(T, d, cfg.ffn_mult), self.dev)
         self.dHs = [torch.empty(T, d, dtype=torch.bfloat16, device=self.dev) for _ in range(nl + 1)]
         self.t_p = torch.empty(T, dtype=torch.int64, device=self.dev)
         self.s_p = torch.empty(T, dtype=torch.int32, device=self.dev)
@@ -333,11 +358,9 @@ class CadetStack:
         self.acfg.plan_ready = 0
         chk(lib.cadet_mask_plan(C.byref(self.acfg), C.byref(b), ws, wsn, st))
         self.acfg.plan_ready = 2
-        # A1-A6: residual layers  H[l+1] = H[l] + Attn(H[l])
+        # A1-A6: residual layers  H[l+1] = H[l] + Attn(H[l])  (block mode: the pre-norm CADET block)
         for l in range(cfg.n_layers):
-            w = L.AttnWeights(*[x.data_ptr() for x in self.W[l]])
-            chk(lib.cadet_attn_forward(C.byref(self.acfg), C.byref(b), C.byref(w), _vp(self.Hs[l]),
-                                       _vp(self.Hs[l + 1]), _vp(self.Hs[l]), _vp(self._saved(l)), ws, wsn, st))
+            self._layer_forward(l, b, ws, wsn, st, self.Hs[l + 1])
         # A7-A8: towers on impression rows + routed BCE
         hc = L.HeadConfig(cfg.K, d, cfg.dh, 0)
         hw = L.HeadWeights(self.W1.data_ptr(), self.b1.data_ptr(), self.w2.data_ptr(), self.b2.data_ptr())
@@ -353,11 +376,11 @@ class CadetStack:
         # DP: the towers' gradients are all-reduced once their backward is enqueued; each
         # layer's weight gradients in four groups (W_o | W_qg, W_kg | W_q, W_k, W_v | W_xg), each as soon
         # as cadet_attn_backward_ev's event for that group fires, overlapping the rest of the backward
-        nl, dd = cfg.n_layers, d * d
+        nl = cfg.n_layers
         buckets = GradBuckets([self.grads[self._tower_off:]], group)
         if group is not None and self._grad_events is None:
             self._side = torch.cuda.Stream(self.dev)
-            self._grad_events = [[torch.cuda.Event() for _ in range(4)] for _ in range(nl)]
+            self._grad_events = [[torch.cuda.Event() for _ in range(6)] for _ in range(nl)]
             for evs in self._grad_events:
                 for e in evs:
                     e.record()  # materialises the cudaEvent_t handle
@@ -373,24 +396,15 @@ class CadetStack:
         handles = []
         # A9-A12: layers backward; dX_l = dX_{l+1} (residual) + Attn_l^T(dX_{l+1})
         for l in reversed(range(cfg.n_layers)):
-            w = L.AttnWeights(*[x.data_ptr() for x in self.W[l]])
-            g = L.AttnGrads(*[x.data_ptr() for x in self.gW[l]])
             if cfg.recompute:  # refill the single saved buffer with layer l's activations (deterministic fwd)
-                chk(lib.cadet_attn_forward(C.byref(self.acfg), C.byref(b), C.byref(w), _vp(self.Hs[l]),
-                                           _vp(self._rec_y), _vp(self.Hs[l]), _vp(self._saved(l)), ws, wsn, st))
+                self._layer_forward(l, b, ws, wsn, st, self._rec_y)
             evs = self._grad_events[l] if group is not None else None
-            arr = (C.c_void_p * 4)(*[e.cuda_event for e in evs]) if evs else None
-            chk(lib.cadet_attn_backward_ev(C.byref(self.acfg), C.byref(b), C.byref(w), _vp(self.Hs[l]),
-                                           _vp(self._saved(l)), _vp(self.dHs[l + 1]), _vp(self.dHs[l]),
-                                           _vp(self.dHs[l + 1]), C.byref(g), ws, wsn, st, arr))
-            if evs:
-                base = l * 7 * dd
-                groups = (self.grads[base + 6 * dd:base + 7 * dd], self.grads[base + 4 * dd:base + 6 * dd],
-                          self.grads[base + dd:base + 4 * dd], self.grads[base:base + dd])
-                for i, sl in enumerate(groups):
-                    self._side.wait_event(evs[i])
-                    with torch.cuda.stream(self._side):
-                        handles.append(torch.distributed.all_reduce(sl, group=group, async_op=True))
+
+            def reduce(ev, sl):
+                self._side.wait_event(ev)
+                with torch.cuda.stream(self._side):
+                    handles.append(torch.distributed.all_reduce(sl, group=group, async_op=True))
+            self._layer_backward(l, b, ws, wsn, st, evs, reduce)
         buckets.wait()
         for h in handles:
             h.wait()
@@ -415,6 +429,69 @@ class CadetStack:
 
     def _saved(self, l: int) -> torch.Tensor:
         return self.saved[0 if self.cfg.recompute else l]
+
+    def _layer_forward(self, l, b, ws, wsn, st, Y):
+        """Layer l forward into Y: H + Attn(H) (A1-A6), or with cfg.block the pre-norm CADET block
+        (S:644): Xn = RMSNorm1(X); H = X + Attn(Xn); Hn = RMSNorm2(H); Y = H + FFN(Hn)."""
+        cfg, lib, chk = self.cfg, L.lib(), L.check
+        d, T = cfg.d_model, cfg.budget
+        w = L.AttnWeights(*[x.data_ptr() for x in self.W[l]])
+        X = self.Hs[l]
+        if not cfg.block:
+            chk(lib.cadet_attn_forward(C.byref(self.acfg), C.byref(b), C.byref(w), _vp(X), _vp(Y), _vp(X),
+                                       _vp(self._saved(l)), ws, wsn, st))
+            return
+        k = self.blk[0 if cfg.recompute else l]
+        g1, g2 = self.gam[l]
+        chk(lib.cadet_rmsnorm_forward(_vp(X), _vp(g1), T, d, _vp(k["Xn"]), _vp(k["r1"]), st))
+        chk(lib.cadet_attn_forward(C.byref(self.acfg), C.byref(b), C.byref(w), _vp(k["Xn"]), _vp(k["H"]), _vp(X),
+                                   _vp(self._saved(l)), ws, wsn, st))
+        chk(lib.cadet_rmsnorm_forward(_vp(k["H"]), _vp(g2), T, d, _vp(k["Hn"]), _vp(k["r2"]), st))
+        chk(lib.cadet_ffn_forward(_vp(k["Hn"]), _vp(self.F[l][0]), _vp(self.F[l][1]), _vp(k["H"]), T, d,
+                                  cfg.ffn_mult, _vp(Y), _vp(k["U"]), _vp(k["G"]), st))
+
+    def _layer_backward(self, l, b, ws, wsn, st, evs, reduce):
+        """dHs[l] from dHs[l+1] (the residual adds included) and layer l's weight gradients; with DP
+        (evs not None) each gradient group is handed to `reduce(event, slice)` as soon as it is final."""
+        cfg, lib, chk = self.cfg, L.lib(), L.check
+        d, T = cfg.d_model, cfg.budget
+        w = L.AttnWeights(*[x.data_ptr() for x in self.W[l]])
+        g = L.AttnGrads(*[x.data_ptr() for x in self.gW[l]])
+        arr = (C.c_void_p * 4)(*[e.cuda_event for e in evs[:4]]) if evs else None
+        dY, dX = self.dHs[l + 1], self.dHs[l]
+        grp = self._groups[l]
+        if not cfg.block:
+            chk(lib.cadet_attn_backward_ev(C.byref(self.acfg), C.byref(b), C.byref(w), _vp(self.Hs[l]),
+                                           _vp(self._saved(l)), _vp(dY), _vp(dX), _vp(dY), C.byref(g), ws, wsn, st,
+                                           arr))
+            if evs:
+                for i, sl in enumerate(grp["attn"]):
+                    reduce(evs[i], sl)
+            return
+        k = self.blk[0 if cfg.recompute else l]
+        g1, g2 = self.gam[l]
+        dW1f, dW2f, dg2, dg1 = self.gF[l]
+        dA, dB = self._dA, self._dB
+        # FFN^T: dHn = dU W1^T (dA);  RMSNorm2^T + residual: dH = dY + RMSNorm2^T(dHn) (dB)
+        chk(lib.cadet_ffn_backward(_vp(k["Hn"]), _vp(self.F[l][0]), _vp(self.F[l][1]), _vp(k["U"]), _vp(k["G"]),
+                                   _vp(dY), None, T, d, cfg.ffn_mult, _vp(dA), _vp(dW1f), _vp(dW2f), _vp(self._fws),
+                                   self._fws.numel(), st))
+        chk(lib.cadet_rmsnorm_backward(_vp(k["H"]), _vp(g2), _vp(k["r2"]), _vp(dA), _vp(dY), T, d, _vp(dB), _vp(dg2),
+                                       st))
+        if evs:
+            evs[4].record()
+            reduce(evs[4], grp["ffn"])
+        # Attn^T: dXn (dA);  RMSNorm1^T + residual: dX = dH + RMSNorm1^T(dXn)
+        chk(lib.cadet_attn_backward_ev(C.byref(self.acfg), C.byref(b), C.byref(w), _vp(k["Xn"]), _vp(self._saved(l)),
+                                       _vp(dB), _vp(dA), None, C.byref(g), ws, wsn, st, arr))
+        if evs:
+            for i, sl in enumerate(grp["attn"]):
+                reduce(evs[i], sl)
+        chk(lib.cadet_rmsnorm_backward(_vp(self.Hs[l]), _vp(g1), _vp(k["r1"]), _vp(dA), _vp(dB), T, d, _vp(dX),
+                                       _vp(dg1), st))
+        if evs:
+            evs[5].record()
+            reduce(evs[5], grp["g1"])
 
     def _full_loss_backward(self, inp, group, hc, hw, hg, st):
         """NEXT-2 (Eqs. 10-12): routed logits -> (DP) all-gather with labels -> RankNet share of this

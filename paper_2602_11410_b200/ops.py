@@ -127,6 +127,53 @@ def gemm(A, B, a_mn: bool = False, b_mn: bool = False, out_f32: bool = True, res
     return out
 
 
+def rmsnorm_forward(X, gamma, Y=None, rstd=None):
+    """NEXT-3 (R32): Y = X / sqrt(mean(X^2) + 1e-6) * gamma; returns (Y bf16, rstd fp32 [T])."""
+    _need_cuda(X, gamma)
+    T, d = X.shape
+    Y = torch.empty_like(X) if Y is None else Y
+    rstd = torch.empty(T, dtype=torch.float32, device=X.device) if rstd is None else rstd
+    L.check(L.lib().cadet_rmsnorm_forward(_p(X), _p(gamma), T, d, _p(Y), _p(rstd), _stream()))
+    return Y, rstd
+
+
+def rmsnorm_backward(X, gamma, rstd, dY, dresid=None, dX=None, dgamma=None):
+    """dX (+ dresid) and dgamma (fp32 [d], overwritten)."""
+    _need_cuda(X, gamma, rstd, dY, dresid)
+    T, d = X.shape
+    dX = torch.empty_like(X) if dX is None else dX
+    dgamma = torch.empty(d, dtype=torch.float32, device=X.device) if dgamma is None else dgamma
+    L.check(L.lib().cadet_rmsnorm_backward(_p(X), _p(gamma), _p(rstd), _p(dY), _p(dresid), T, d, _p(dX), _p(dgamma),
+                                           _stream()))
+    return dX, dgamma
+
+
+def ffn_forward(X, W1, W2, resid=None, Y=None, U=None, Gt=None):
+    """NEXT-3 (R33): U = X W1, G = GELU(U), Y = G W2 (+ resid); returns (Y, U, G)."""
+    _need_cuda(X, W1, W2, resid)
+    T, d = X.shape
+    m = W1.shape[1] // d
+    Y = torch.empty_like(X) if Y is None else Y
+    U = torch.empty(T, m * d, dtype=BF16, device=X.device) if U is None else U
+    Gt = torch.empty(T, m * d, dtype=BF16, device=X.device) if Gt is None else Gt
+    L.check(L.lib().cadet_ffn_forward(_p(X), _p(W1), _p(W2), _p(resid), T, d, m, _p(Y), _p(U), _p(Gt), _stream()))
+    return Y, U, Gt
+
+
+def ffn_backward(X, W1, W2, U, Gt, dY, dresid=None, dX=None, dW1=None, dW2=None, ws=None):
+    """Returns (dX, dW1, dW2, ws); ws[: T m d bf16] holds dU after the call."""
+    _need_cuda(X, W1, W2, U, Gt, dY, dresid)
+    T, d = X.shape
+    m = W1.shape[1] // d
+    dX = torch.empty_like(X) if dX is None else dX
+    dW1 = torch.empty(d, m * d, dtype=torch.float32, device=X.device) if dW1 is None else dW1
+    dW2 = torch.empty(m * d, d, dtype=torch.float32, device=X.device) if dW2 is None else dW2
+    ws = workspace(L.lib().cadet_ffn_workspace_bytes(T, d, m)) if ws is None else ws
+    L.check(L.lib().cadet_ffn_backward(_p(X), _p(W1), _p(W2), _p(U), _p(Gt), _p(dY), _p(dresid), T, d, m, _p(dX),
+                                       _p(dW1), _p(dW2), _p(ws), ws.numel(), _stream()))
+    return dX, dW1, dW2, ws
+
+
 def chunk(cu_in: torch.Tensor, L_chunk: int, cap: int, ws=None):
     _need_cuda(cu_in)
     ws = workspace(256, cu_in.device) if ws is None else ws

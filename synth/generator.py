@@ -273,3 +273,23 @@ def aux_labels(seed: int, n: int) -> np.ndarray:
     out[:, 1] = np.exp(rng.normal(np.log(0.5), 0.8, size=n)).astype(np.float32)
     return out
 
+
+
+@dataclass
+class BlockWeights:
+    """NEXT-3 (R32, R33): the pre-norm block's RMSNorm scales and FFN weights."""
+    gamma1: np.ndarray  # [d] fp32 (bf16-valued)
+    gamma2: np.ndarray  # [d]
+    W1: np.ndarray      # [d, m d]
+    W2: np.ndarray      # [m d, d]
+
+
+def block_weights(seed: int, layer: int, d: int, m: int = 4) -> BlockWeights:
+    """gamma = 1 + N(0, 0.1^2); W1 ~ N(0, 1/d), W2 ~ N(0, 1/(m d)) (unit-variance activations)."""
+    base = 5000 * (layer + 1)
+    return BlockWeights(
+        gamma1=1.0 + normal_bf16(seed, base + 1, (d,), 0.1),
+        gamma2=1.0 + normal_bf16(seed, base + 2, (d,), 0.1),
+        W1=normal_bf16(seed, base + 3, (d, m * d), 1.0 / np.sqrt(d)),
+        W2=normal_bf16(seed, base + 4, (m * d, d), 1.0 / np.sqrt(m * d)),
+    )
