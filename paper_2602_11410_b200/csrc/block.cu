@@ -26,32 +26,70 @@ __device__ __forceinline__ uint4 pack8(const float (&x)[8]) {
   return make_uint4(pack_bf16(x[0], x[1]), pack_bf16(x[2], x[3]), pack_bf16(x[4], x[5]), pack_bf16(x[6], x[7]));
 }
 
-__global__ void __launch_bounds__(256) rmsnorm_fwd_kernel(const __nv_bfloat16* X, const float* gamma, int T, int d,
-                                                          __nv_bfloat16* Y, float* rstd) {
-  const int row = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
-  if (row >= T) return;
-  float x[RMS_MAXC][8];
-  float ss = 0.f;
+// Both kernels: 256 threads, gamma staged once per block in shared memory, warps grid-stride over
+// rows; each lane keeps its 8-column chunks of a row as raw bf16x8 (uint4) registers and unpacks on
+// the fly, so many rows' loads are in flight per SM (the kernels are HBM-bound).
+__device__ __forceinline__ void load_row(const __nv_bfloat16* base, int d, int lane, uint4 (&r)[RMS_MAXC]) {
 #pragma unroll
   for (int c = 0; c < RMS_MAXC; ++c) {
     const int col = c * 256 + lane * 8;
-    if (col < d) {
-      unpack8(*reinterpret_cast<const uint4*>(X + (size_t)row * d + col), x[c]);
-#pragma unroll
-      for (int e = 0; e < 8; ++e) ss = fmaf(x[c][e], x[c][e], ss);
-    }
+    r[c] = col < d ? __ldcs(reinterpret_cast<const uint4*>(base + col)) : make_uint4(0, 0, 0, 0);
   }
-  for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
-  const float r = rsqrtf(ss / (float)d + RMS_EPS);
-  if (lane == 0) rstd[row] = r;
+}
+
+__global__ void __launch_bounds__(256, 2) rmsnorm_fwd_kernel(const __nv_bfloat16* X, const float* gamma, int T, int d,
+                                                          __nv_bfloat16* Y, float* rstd) {
+  __shared__ __align__(16) float g_s[256 * RMS_MAXC];
+  for (int i = threadIdx.x; i < d; i += blockDim.x) g_s[i] = gamma[i];
+  __syncthreads();
+  const int lane = threadIdx.x & 31, nw = gridDim.x * 8;
+  // two rows per warp per iteration: 8 x 16 B loads per lane in flight
+  for (int row = blockIdx.x * 8 + (threadIdx.x >> 5); row < T; row += 2 * nw) {
+    uint4 xr[2][RMS_MAXC];
+    float ss[2];
 #pragma unroll
-  for (int c = 0; c < RMS_MAXC; ++c) {
-    const int col = c * 256 + lane * 8;
-    if (col < d) {
-      float y[8];
+    for (int h = 0; h < 2; ++h) {
+      if (row + h * nw < T) load_row(X + (size_t)(row + h * nw) * d, d, lane, xr[h]);
+      else
 #pragma unroll
-      for (int e = 0; e < 8; ++e) y[e] = x[c][e] * r * gamma[col + e];
-      *reinterpret_cast<uint4*>(Y + (size_t)row * d + col) = pack8(y);
+        for (int c = 0; c < RMS_MAXC; ++c) xr[h][c] = make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      ss[h] = 0.f;
+#pragma unroll
+      for (int c = 0; c < RMS_MAXC; ++c) {
+        float x[8];
+        unpack8(xr[h][c], x);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) ss[h] = fmaf(x[e], x[e], ss[h]);
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      ss[0] += __shfl_xor_sync(0xffffffffu, ss[0], o);
+      ss[1] += __shfl_xor_sync(0xffffffffu, ss[1], o);
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int rh = row + h * nw;
+      if (rh >= T) continue;
+      const float r = rsqrtf(ss[h] / (float)d + RMS_EPS);
+      if (lane == 0) rstd[rh] = r;
+#pragma unroll
+      for (int c = 0; c < RMS_MAXC; ++c) {
+        const int col = c * 256 + lane * 8;
+        if (col < d) {
+          float x[8], y[8];
+          unpack8(xr[h][c], x);
+          const float4 g0 = *reinterpret_cast<const float4*>(g_s + col);
+          const float4 g1 = *reinterpret_cast<const float4*>(g_s + col + 4);
+          const float g[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+#pragma unroll
+          for (int e = 0; e < 8; ++e) y[e] = x[e] * r * g[e];
+          *reinterpret_cast<uint4*>(Y + (size_t)rh * d + col) = pack8(y);
+        }
+      }
     }
   }
 }
@@ -59,59 +97,67 @@ __global__ void __launch_bounds__(256) rmsnorm_fwd_kernel(const __nv_bfloat16* X
 __global__ void __launch_bounds__(256) rmsnorm_bwd_kernel(const __nv_bfloat16* X, const float* gamma, const float* rstd,
                                                           const __nv_bfloat16* dY, const __nv_bfloat16* dresid, int T,
                                                           int d, __nv_bfloat16* dX, float* dgamma) {
+  __shared__ __align__(16) float g_s[256 * RMS_MAXC];
+  __shared__ __align__(16) float dg_s[8][256 * RMS_MAXC];  // per-warp dgamma partials (lane-private columns)
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  float dg[RMS_MAXC][8];
-#pragma unroll
-  for (int c = 0; c < RMS_MAXC; ++c)
-#pragma unroll
-    for (int e = 0; e < 8; ++e) dg[c][e] = 0.f;
+  for (int i = threadIdx.x; i < d; i += blockDim.x) g_s[i] = gamma[i];
+  for (int i = lane; i < d; i += 32) dg_s[w][i] = 0.f;
+  __syncthreads();
   for (int row = blockIdx.x * 8 + w; row < T; row += gridDim.x * 8) {
-    float x[RMS_MAXC][8], gy[RMS_MAXC][8];
-    float s = 0.f;
+    uint4 xr[RMS_MAXC], yr[RMS_MAXC], rr[RMS_MAXC];
+    load_row(X + (size_t)row * d, d, lane, xr);
+    load_row(dY + (size_t)row * d, d, lane, yr);
+    if (dresid) load_row(dresid + (size_t)row * d, d, lane, rr);
     const float r = rstd[row];
+    float s = 0.f;
 #pragma unroll
     for (int c = 0; c < RMS_MAXC; ++c) {
       const int col = c * 256 + lane * 8;
       if (col < d) {
-        float dy[8];
-        unpack8(*reinterpret_cast<const uint4*>(X + (size_t)row * d + col), x[c]);
-        unpack8(*reinterpret_cast<const uint4*>(dY + (size_t)row * d + col), dy);
+        float x[8], dy[8];
+        unpack8(xr[c], x);
+        unpack8(yr[c], dy);
+        float4* dg = reinterpret_cast<float4*>(&dg_s[w][col]);
+        float4 a0 = dg[0], a1 = dg[1];
+        const float4 g0 = *reinterpret_cast<const float4*>(g_s + col);
+        const float4 g1 = *reinterpret_cast<const float4*>(g_s + col + 4);
+        const float g[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          gy[c][e] = gamma[col + e] * dy[e];
-          s = fmaf(x[c][e], gy[c][e], s);
-          dg[c][e] = fmaf(dy[e], x[c][e] * r, dg[c][e]);
-        }
+        for (int e = 0; e < 8; ++e) s = fmaf(x[e], g[e] * dy[e], s);
+        a0.x = fmaf(dy[0], x[0] * r, a0.x); a0.y = fmaf(dy[1], x[1] * r, a0.y);
+        a0.z = fmaf(dy[2], x[2] * r, a0.z); a0.w = fmaf(dy[3], x[3] * r, a0.w);
+        a1.x = fmaf(dy[4], x[4] * r, a1.x); a1.y = fmaf(dy[5], x[5] * r, a1.y);
+        a1.z = fmaf(dy[6], x[6] * r, a1.z); a1.w = fmaf(dy[7], x[7] * r, a1.w);
+        dg[0] = a0;
+        dg[1] = a1;
       }
     }
+#pragma unroll
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
     const float k = r * r * r * s / (float)d;
 #pragma unroll
     for (int c = 0; c < RMS_MAXC; ++c) {
       const int col = c * 256 + lane * 8;
       if (col < d) {
-        float dx[8], dr[8];
-        if (dresid)
-          unpack8(*reinterpret_cast<const uint4*>(dresid + (size_t)row * d + col), dr);
+        float x[8], dy[8], dr[8], dx[8];
+        unpack8(xr[c], x);
+        unpack8(yr[c], dy);
+        if (dresid) unpack8(rr[c], dr);
+        const float4 g0 = *reinterpret_cast<const float4*>(g_s + col);
+        const float4 g1 = *reinterpret_cast<const float4*>(g_s + col + 4);
+        const float g[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
 #pragma unroll
-        for (int e = 0; e < 8; ++e) dx[e] = r * gy[c][e] - x[c][e] * k + (dresid ? dr[e] : 0.f);
+        for (int e = 0; e < 8; ++e) dx[e] = r * g[e] * dy[e] - x[e] * k + (dresid ? dr[e] : 0.f);
         *reinterpret_cast<uint4*>(dX + (size_t)row * d + col) = pack8(dx);
       }
     }
   }
-  // dgamma: 8 warps of the block into shared memory (fixed order), one atomic per column
-  __shared__ float sh[8][1024];
-#pragma unroll
-  for (int c = 0; c < RMS_MAXC; ++c) {
-    const int col = c * 256 + lane * 8;
-    if (col < d)
-#pragma unroll
-      for (int e = 0; e < 8; ++e) sh[w][col + e] = dg[c][e];
-  }
   __syncthreads();
+  // dgamma: the 8 warps' partials in a fixed order, one atomic per column per block
   for (int col = threadIdx.x; col < d; col += blockDim.x) {
     float a = 0.f;
-    for (int ww = 0; ww < 8; ++ww) a += sh[ww][col];
+#pragma unroll
+    for (int ww = 0; ww < 8; ++ww) a += dg_s[ww][col];
     atomicAdd(dgamma + col, a);
   }
 }
@@ -142,7 +188,7 @@ cadet_status cadet_rmsnorm_forward(const void* X, const float* gamma, int32_t T,
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   ProfScope ps(PROF_OTHER, st, 1);
   if (T > 0)
-    rmsnorm_fwd_kernel<<<(T + 7) / 8, 256, 0, st>>>(reinterpret_cast<const __nv_bfloat16*>(X), gamma, T, d,
+    rmsnorm_fwd_kernel<<<min((T + 15) / 16, 2 * sm_count()), 256, 0, st>>>(reinterpret_cast<const __nv_bfloat16*>(X), gamma, T, d,
                                                    reinterpret_cast<__nv_bfloat16*>(Y), rstd);
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
@@ -167,7 +213,7 @@ cadet_status cadet_rmsnorm_backward(const void* X, const float* gamma, const flo
   }
   ProfScope ps(PROF_OTHER, st, 1);
   if (T > 0) {
-    const int blocks = min((T + 7) / 8, 8 * sm_count());
+    const int blocks = min((T + 7) / 8, 3 * sm_count());
     rmsnorm_bwd_kernel<<<blocks, 256, 0, st>>>(
         reinterpret_cast<const __nv_bfloat16*>(X), gamma, rstd, reinterpret_cast<const __nv_bfloat16*>(dY),
         reinterpret_cast<const __nv_bfloat16*>(dresid), T, d, reinterpret_cast<__nv_bfloat16*>(dX), dgamma);
