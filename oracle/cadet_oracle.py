@@ -4,8 +4,8 @@ TEST INFRASTRUCTURE ONLY.  Only `tests/`, `__graft_entry__.smoke()` and
 `bench.py`'s cpu_baseline / `--impl reference` legs may import this module.
 It shares no code with the CUDA path (paper_2602_11410_b200/) and never
 imports it.  Every function follows PAPER.md (P:n) / SPEC.md (S:n) as cited,
-with the readings R1..R33 listed in DESIGN.md §3 (R29-R31: the NEXT-2 full loss; R32-R33: the
-NEXT-3 block).
+with the readings R1..R35 listed in DESIGN.md §3 (R29-R31: the NEXT-2 full loss; R32-R33: the
+NEXT-3 block; R35: the NEXT-4 optimizer).
 
 Conventions: row-vector projections y = x.W, W[d_in][d_out] (R1); all math in
 float64 on bf16-valued inputs (R20); heads are per-head slices of width hd of
@@ -612,6 +612,21 @@ def block_backward_seq(c, W, ffn, gammas, t_ms, A, dY, cfg: AttnConfig):
     dXn, gW, _ = layer_backward_seq(c["ca"], W, t_ms, A, dH, cfg)
     dX_norm, dg1 = rmsnorm_backward(c["X"], gammas[0], dXn)
     return dH + dX_norm, dict(gW=gW, dW1f=dW1f, dW2f=dW2f, dg1=dg1, dg2=dg2)
+
+
+# ------------------------------------------------------------------ NEXT-4: the optimizer of the HSDP step
+def adamw_step(theta, m, v, g, step, lr=1e-4, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.0):
+    """R35: AdamW (decoupled weight decay), bias-corrected, eps outside the square root — the update
+    every rank applies to its shard of the fp32 master parameters (HSDP shards parameters, gradients
+    and optimizer state within a node; the update is elementwise, so sharding does not change
+    it).  Returns (theta', m', v'); step counts from 1."""
+    theta, m, v, g = (np.asarray(a, np.float64) for a in (theta, m, v, g))
+    m = beta1 * m + (1.0 - beta1) * g
+    v = beta2 * v + (1.0 - beta2) * g * g
+    m_hat = m / (1.0 - beta1 ** step)
+    v_hat = v / (1.0 - beta2 ** step)
+    theta = theta * (1.0 - lr * weight_decay) - lr * m_hat / (np.sqrt(v_hat) + eps)
+    return theta, m, v
 
 
 # ------------------------------------------------------------------ per-element loop (check 1)

@@ -627,3 +627,37 @@ def test_block_backward_by_finite_differences_and_zero_ffn_reduction():
     Y0, _ = O.block_forward_seq(X, W, (ffn[0], np.zeros_like(ffn[1])), gam, b.timestamps, A, cfg)
     Ya, _ = O.layer_forward_seq(O.rmsnorm(X, gam[0])[0], W, b.timestamps, A, cfg)
     assert np.allclose(Y0, X + Ya, atol=1e-13)
+
+
+# ------------------------------------------------------------------ NEXT-4: AdamW (R35)
+def test_adamw_first_step_constant_gradient_and_decay_closed_forms():
+    """Pins of O.adamw_step against closed forms of Adam's algebra (Kingma & Ba, Alg. 1; decoupled
+    decay, Loshchilov & Hutter): (i) step 1: m_hat = g, v_hat = g^2, so the update is
+    -lr g / (|g| + eps) (= -lr sign(g) for |g| >> eps); (ii) a constant gradient keeps m_hat = g and
+    v_hat = g^2 at every step (the bias corrections are exact), so k steps move theta by
+    -k lr g / (|g| + eps); (iii) with g = 0 only the decay acts: theta_k = theta_0 (1 - lr wd)^k;
+    (iv) a hand-computed two-step example with beta1 = 0.5, beta2 = 0.75."""
+    rng = np.random.default_rng(3)
+    th = rng.normal(size=257)
+    g = rng.normal(size=257) * np.logspace(-6, 2, 257)
+    z = np.zeros(257)
+    lr = 1e-3
+    t1, m1, v1 = O.adamw_step(th, z, z, g, 1, lr=lr)
+    assert np.allclose(t1, th - lr * g / (np.abs(g) + 1e-8), rtol=0, atol=1e-15)
+    assert np.allclose(m1, 0.1 * g) and np.allclose(v1, 0.001 * g * g)
+    t, m, v = th, z, z
+    for k in range(1, 8):
+        t, m, v = O.adamw_step(t, m, v, g, k, lr=lr)
+    assert np.allclose(t, th - 7 * lr * g / (np.abs(g) + 1e-8), rtol=0, atol=1e-12)
+    t, m, v = th, z, z
+    for k in range(1, 6):
+        t, m, v = O.adamw_step(t, m, v, z, k, lr=lr, weight_decay=0.1)
+    assert np.allclose(t, th * (1 - lr * 0.1) ** 5, rtol=1e-14)
+    # (iv) theta 1, g = 2 then -1, lr 0.1, beta1 0.5, beta2 0.75, eps 0:
+    # step 1: m = 1, v = 1, m_hat = 2, v_hat = 4 -> theta = 1 - 0.1 * 2 / 2 = 0.9
+    # step 2: m = 0.5 - 0.5 = 0, v = 0.75 + 0.25 = 1 -> m_hat = 0, theta stays 0.9
+    t, m, v = O.adamw_step(np.array([1.0]), np.zeros(1), np.zeros(1), np.array([2.0]), 1, lr=0.1, beta1=0.5,
+                           beta2=0.75, eps=0.0)
+    assert t[0] == pytest.approx(0.9) and m[0] == pytest.approx(1.0) and v[0] == pytest.approx(1.0)
+    t, m, v = O.adamw_step(t, m, v, np.array([-1.0]), 2, lr=0.1, beta1=0.5, beta2=0.75, eps=0.0)
+    assert t[0] == pytest.approx(0.9) and m[0] == pytest.approx(0.0) and v[0] == pytest.approx(1.0)
