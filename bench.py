@@ -278,6 +278,10 @@ def main():
                     help="NEXT-2: train on Eq. 11 (towers + auxiliary heads + cross-rank RankNet) instead of Eq. 9")
     ap.add_argument("--block", action="store_true",
                     help="NEXT-3: every layer is the pre-norm CADET block (RMSNorm, gated attention, RMSNorm, FFN x4)")
+    ap.add_argument("--optimizer", default="none", choices=["none", "adamw"],
+                    help="NEXT-4: append the AdamW step (R35) to every training step")
+    ap.add_argument("--no-shard", action="store_true",
+                    help="with --optimizer and N > 1: replicated AdamW after all-reduce instead of HSDP sharding")
     ap.add_argument("--graph", action="store_true",
                     help="replay the step as one CUDA graph (measured: no gain over eager launches on C4)")
     args = ap.parse_args()
@@ -334,7 +338,8 @@ def main():
     inp = host_inp.to(dev)
     torch.cuda.synchronize()
     scfg = StackConfig(d_model=wl["d_model"], n_heads=wl["n_heads"], n_layers=wl["n_layers"], budget=wl["budget"],
-                       L_chunk=wl["L_chunk"], full_loss=args.full_loss, recompute=args.recompute, block=args.block)
+                       L_chunk=wl["L_chunk"], full_loss=args.full_loss, recompute=args.recompute, block=args.block,
+                       optimizer=args.optimizer, shard=not args.no_shard)
     stack = CadetStack(scfg, seed=0, device=dev)
     pairs = stack.pairs(inp)
     n_imp = inp.rows.numel()
@@ -360,7 +365,9 @@ def main():
     # --graph: the step as one CUDA graph; the per-class CUDA events are nodes of the graph, so after
     # the timed replays they hold the last timed step.  Eager fallback if capture fails.
     graph, graph_err = None, None
-    if args.graph:
+    if args.graph and args.optimizer != "none":
+        graph_err = "not captured: the optimizer's bias corrections change every step"
+    elif args.graph:
         try:
             ops.prof_enable(15, 64 * (wl["n_layers"] + 2))
             n0 = ops.launch_count()
@@ -499,6 +506,9 @@ def main():
                    "l2": "inputs > L2 (X 128 MB + activations > 1 GB per step); no flush needed",
                    "parallelism": f"dp{world}", "loss": "Eq. 11 full (NEXT-2)" if args.full_loss else "Eq. 9 routed BCE",
                    "recompute": bool(args.recompute),
+                   "optimizer": "none (step ends at the gradients, SURVEY 8(a))" if args.optimizer == "none" else
+                   ("AdamW (R35), HSDP: reduce-scatter grads, shard update, all-gather bf16 params" if
+                    (world > 1 and not args.no_shard) else "AdamW (R35), replicated after the gradient all-reduce"),
                    "layer": "pre-norm CADET block: RMSNorm, gated attention, RMSNorm, FFN x4 (NEXT-3)" if args.block
                    else "gated attention layer (Eq. 3-7) + residual",
                    "partition": "rank r = shard r of an LPT partition of one user stream into 8 budgets"},

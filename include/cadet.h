@@ -287,6 +287,27 @@ cadet_status cadet_ffn_backward(const void* X, const void* W1, const void* W2, c
                                 const void* dY, const void* dresid, int32_t T, int32_t d, int32_t m, void* dX,
                                 float* dW1, float* dW2, void* ws, size_t ws_bytes, cadet_stream_t stream);
 
+/* ------------------------------------------------------------------ NEXT-4: HSDP optimizer step
+ * HSDP shards parameters, gradients and optimizer state within a node: each rank
+ * reduce-scatters the flat fp32 gradient buffer (NCCL, the caller), updates ITS shard with
+ * cadet_adamw_step, and the bf16 compute copies are all-gathered (NCCL, the caller).  Reading R35:
+ * AdamW, bias-corrected, eps outside the square root, decoupled weight decay:
+ *   m = b1 m + (1 - b1) g;  v = b2 v + (1 - b2) g^2;
+ *   p = p (1 - lr wd) - lr (m / (1 - b1^step)) / (sqrt(v / (1 - b2^step)) + eps). */
+typedef struct {
+  float lr, beta1, beta2, eps, weight_decay;
+} cadet_adamw_config;
+void cadet_default_adamw_config(cadet_adamw_config* c_h); /* lr 1e-4, (0.9, 0.999), eps 1e-8, wd 0 */
+/* One AdamW step over n fp32 elements (grad read; param, m, v updated in place; step >= 1 counts
+ * from 1).  param_bf16 (nullable) receives bf16(param) — the compute copy.  fp32 buffers 16-byte
+ * aligned, param_bf16 8-byte aligned; else CADET_E_ARG.  Elementwise: any shard split gives the
+ * same result as the whole buffer. */
+cadet_status cadet_adamw_step(const cadet_adamw_config* c_h, int64_t step, const float* grad, float* param, float* m,
+                              float* v, void* param_bf16, int64_t n, cadet_stream_t stream);
+/* dst[i] = (float)src[i] for n bf16 elements (fp32-consumed parameters after a bf16 all-gather).
+ * Both buffers 16-byte aligned. */
+cadet_status cadet_bf16_to_f32(const void* src, float* dst, int64_t n, cadet_stream_t stream);
+
 /* ------------------------------------------------------------------ A0 / A13: chunk and pack
  * Chunk: split each sequence [a, e) of cu_in at e - L, e - 2L, ... (newest chunk full, oldest may be
  * short) and write the refined offsets in buffer order to cu_out (capacity cap entries);

@@ -53,6 +53,11 @@ class LossConfig(C.Structure):
                 ("lambda_aux", C.c_float * 8)]
 
 
+class AdamWConfig(C.Structure):
+    _fields_ = [("lr", C.c_float), ("beta1", C.c_float), ("beta2", C.c_float), ("eps", C.c_float),
+                ("weight_decay", C.c_float)]
+
+
 class HeadConfig(C.Structure):
     _fields_ = [("K", C.c_int32), ("d_model", C.c_int32), ("d_hidden", C.c_int32), ("dtype", C.c_int32)]
 
@@ -106,6 +111,9 @@ SIGNATURES = {
     "cadet_ffn_workspace_bytes": (SZ, [I32, I32, I32]),
     "cadet_ffn_forward": (I32, [P, P, P, P, I32, I32, I32, P, P, P, P]),
     "cadet_ffn_backward": (I32, [P, P, P, P, P, P, P, I32, I32, I32, P, P, P, P, SZ, P]),
+    "cadet_default_adamw_config": (None, [C.POINTER(AdamWConfig)]),
+    "cadet_adamw_step": (I32, [C.POINTER(AdamWConfig), C.c_int64, P, P, P, P, P, C.c_int64, P]),
+    "cadet_bf16_to_f32": (I32, [P, P, C.c_int64, P]),
     "cadet_chunk": (I32, [P, I32, I32, P, I32, P, P, P]),
     "cadet_pack": (I32, [P, P, P, I32, I32, I32, P, P, P, P, P, P, P, P, SZ, P]),
     "cadet_pack_workspace_bytes": (SZ, [I32]),

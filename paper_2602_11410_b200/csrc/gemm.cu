@@ -91,7 +91,7 @@ constexpr uint32_t MODES_ALL = MB(EPI_STORE) | MB(EPI_GATE) | MB(EPI_GATE_ROPE) 
 // exact GELU u Phi(u) and its derivative (R33)
 __device__ __forceinline__ float gelu_f(float u) { return 0.5f * u * (1.f + erff(u * 0.7071067811865476f)); }
 __device__ __forceinline__ float gelu_grad_f(float u) {
-  return 0.5f * (1.f + erff(u * 0.7071067811865476f)) + u * 0.3989422804014327f * __expf(-0.5f * u * u);
+  return 0.5f * (1.f + erff(u * 0.7071067811865476f)) + u * 0.3989422804014327f * ex2_ftz(-0.7213475204444817f * u * u);
 }
 #define HAS_MODE(m) ((MODES & MB(m)) != 0u)
 __device__ __forceinline__ void load_bf16x32(const void* base, float (&x)[32]) {
@@ -180,7 +180,7 @@ __device__ __forceinline__ void run_epilogue(const EpiParams& e, int row, int M,
       float x[32];
       load_bf16x32(reinterpret_cast<const __nv_bfloat16*>(e.src) + in_off, x);
 #pragma unroll
-      for (int j = 0; j < 32; ++j) v[j] = x[j] * __fdividef(1.0f, 1.0f + __expf(-v[j]));
+      for (int j = 0; j < 32; ++j) v[j] = x[j] * sigmoid_fast(v[j]);
       if (HAS_MODE(EPI_GATE_ROPE) && e.mode == EPI_GATE_ROPE) {
         float cs[32];
         load_f32x32(e.rope_cs + (size_t)row * (e.hd + 32) + (n0c % e.hd), cs);
@@ -202,7 +202,7 @@ __device__ __forceinline__ void run_epilogue(const EpiParams& e, int row, int M,
       float u[32];
 #pragma unroll
       for (int j = 0; j < 32; ++j) {
-        const float g = __fdividef(1.0f, 1.0f + __expf(-z[j]));
+        const float g = sigmoid_fast(z[j]);
         u[j] = v[j] * x[j] * g * (1.0f - g);
         r[j] += v[j] * g;
       }
@@ -400,7 +400,7 @@ __device__ __forceinline__ void run_epilogue_warp(const EpiParams& e, int row0, 
       else
         warp_load_rows(stg, e.src, 0, off0, e.ldo, rows_valid, x);
 #pragma unroll
-      for (int j = 0; j < 32; ++j) v[j] = x[j] * __fdividef(1.0f, 1.0f + __expf(-v[j]));
+      for (int j = 0; j < 32; ++j) v[j] = x[j] * sigmoid_fast(v[j]);
       if (HAS_MODE(EPI_GATE_ROPE) && e.mode == EPI_GATE_ROPE) {  // head-local window [n0c % hd, + 32) of the table
         float cs[32];
         if (pre_cs)
@@ -426,7 +426,7 @@ __device__ __forceinline__ void run_epilogue_warp(const EpiParams& e, int row0, 
       }
 #pragma unroll
       for (int j = 0; j < 32; ++j) {
-        const float g = __fdividef(1.0f, 1.0f + __expf(-z[j]));
+        const float g = sigmoid_fast(z[j]);
         const float vj = v[j];
         v[j] = vj * x[j] * g * (1.0f - g);
         r[j] += vj * g;

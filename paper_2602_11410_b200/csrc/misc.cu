@@ -109,7 +109,7 @@ __global__ void __launch_bounds__(256) rope_gate_bwd_kernel(const void* dr, int 
     for (int e = 0; e < 4; ++e) {
       const float2 z = __bfloat1622float2(z2[e]);
       const float2 x = __bfloat1622float2(x2[e]);
-      const float g0 = __fdividef(1.f, 1.f + __expf(-z.x)), g1 = __fdividef(1.f, 1.f + __expf(-z.y));
+      const float g0 = sigmoid_fast(z.x), g1 = sigmoid_fast(z.y);
       __nv_bfloat162 v = __floats2bfloat162_rn(g[2 * e] * x.x * g0 * (1.f - g0), g[2 * e + 1] * x.y * g1 * (1.f - g1));
       uo[e] = *reinterpret_cast<uint32_t*>(&v);
       r[2 * e] = g[2 * e] * g0;

@@ -371,5 +371,19 @@ CADET_DEV uint32_t pack_bf16(float a, float b) {
   return *reinterpret_cast<uint32_t*>(&v);
 }
 CADET_DEV float sigmoidf_(float x) { return 1.0f / (1.0f + __expf(-x)); }
+// MUFU-only forms for the epilogues: ex2 / rcp with flush-to-zero skip the denormal fix-ups that
+// __expf / __fdividef add (3 extra FMUL/FSETP per element); sigma(z) = 1 / (1 + 2^(-z log2 e))
+// saturates correctly at both ends (2^+inf = inf -> rcp = 0).
+CADET_DEV float ex2_ftz(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+CADET_DEV float rcp_ftz(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+CADET_DEV float sigmoid_fast(float z) { return rcp_ftz(1.0f + ex2_ftz(-1.4426950408889634f * z)); }
 
 }  // namespace cadet

@@ -10,6 +10,9 @@ A step (in order):
              all-reduced (SUM) asynchronously as soon as each layer's backward is enqueued, loss and
              impression count all-reduced, logits + labels all-gathered (dp_gather_scores); whole
              users are assigned to ranks by LPT on estimated cost (partition_lpt)
+  NEXT-2..4  optional: the full Eq. 11 loss (full_loss), the pre-norm block (block), gradient
+             checkpointing (recompute), and the AdamW step with HSDP sharding within the node
+             (optimizer="adamw": reduce-scatter, shard update, bf16 all-gather)
 Every computation is a libcadet kernel; PyTorch only allocates memory, provides the stream and
 runs the NCCL collective.
 """
@@ -42,6 +45,11 @@ class StackConfig:
     J: int = 2                   # auxiliary tasks (long-dwell BCE, duration SE)
     block: bool = False          # NEXT-3: pre-norm CADET block (RMSNorm, attention, RMSNorm, FFN, R32/R33)
     ffn_mult: int = 4            # FFN width multiplier m
+    optimizer: str = "none"      # NEXT-4: "adamw" appends the optimizer step (R35) to every training step
+    shard: bool = True           # NEXT-4 with a process group: HSDP within the node (reduce-scatter grads, AdamW on
+                                 # this rank's shard of master params + moments, all-gather bf16 params)
+    lr: float = 1e-4
+    weight_decay: float = 0.0
 
     @property
     def dh(self) -> int:
@@ -216,6 +224,15 @@ def _vp(t):
     return C.c_void_p(t.data_ptr()) if t is not None else None
 
 
+def shard_range(n: int, world: int, rank: int):
+    """NEXT-4: [lo, hi) of rank's equal shard of a flat buffer of n elements (n % (64 world) == 0, so
+    every shard is 256-byte aligned; reduce_scatter_tensor / all_gather_into_tensor split the same way)."""
+    if n % (64 * world):
+        raise ValueError(f"flat buffer of {n} elements does not split into {world} aligned shards")
+    s = n // world
+    return rank * s, (rank + 1) * s
+
+
 class CadetStack:
     """Weights, activations and workspaces for L layers + towers on one GPU."""
 
@@ -225,30 +242,49 @@ class CadetStack:
         self.dev = torch.device(device)
         d, T, nl = cfg.d_model, cfg.budget, cfg.n_layers
         self.acfg = ops.config(d, cfg.n_heads, delta_delay_ms=cfg.delta_delay_ms, mask_flags=cfg.mask_flags)
-        bf = lambda a: torch.from_numpy(a).to(torch.bfloat16).to(self.dev)
-        self.W = [[bf(w) for w in G.layer_weights(seed, l, d, peaky).as_list()] for l in range(nl)]
-        hw = G.head_weights(seed, cfg.K, d, cfg.dh)
-        self.W1 = bf(np.concatenate([hw.W1[k] for k in range(cfg.K)], axis=1))
-        self.b1 = torch.from_numpy(hw.b1.reshape(-1).copy()).to(self.dev)
-        self.w2 = torch.from_numpy(hw.w2.reshape(-1).copy()).to(self.dev)
-        self.b2 = torch.from_numpy(hw.b2.copy()).to(self.dev)
-        # flat fp32 gradient buffer: 7 d^2 per layer (+ the block's FFN and RMSNorm scales, NEXT-3), the
-        # towers (+ the aux heads, NEXT-2); every slice starts on a 256-byte boundary (the split-K
-        # weight-gradient epilogue adds float4 atomics)
+        # ONE flat layout for gradients and parameters: 7 d^2 per layer (+ the block's FFN and RMSNorm
+        # scales, NEXT-3), the towers (+ the aux heads, NEXT-2); every slice starts on a 256-byte
+        # boundary (the split-K weight-gradient epilogue adds float4 atomics) and the total is padded to
+        # a multiple of 8 x 64 elements so it splits into equal, aligned shards for 1/2/4/8 ranks (NEXT-4)
         N = cfg.K * cfg.dh
         Na = cfg.J * cfg.da if cfg.full_loss else 0
         md = cfg.ffn_mult * d
         pad = lambda x: -(-x // 64) * 64
         per_layer = [d * d] * 7 + ([d * md, md * d, d, d] if cfg.block else [])
+        kind_layer = ["m"] * 7 + (["m", "m", "v", "v"] if cfg.block else [])
         npl = len(per_layer)
         sizes = per_layer * nl + [d * N, N, N, cfg.K] + ([d * Na, Na, Na, cfg.J] if cfg.full_loss else [])
-        self.n_grad = sum(pad(x) for x in sizes)
+        kinds = kind_layer * nl + ["m", "v", "v", "v"] + (["m", "v", "v", "v"] if cfg.full_loss else [])
+        self.n_grad = -(-sum(pad(x) for x in sizes) // 512) * 512
         self.grads = torch.zeros(self.n_grad, dtype=torch.float32, device=self.dev)
-        views, offs, off = [], [], 0
-        for x in sizes:
+        # parameters: bf16 compute copies (matrices are consumed as bf16) and fp32 compute copies (vectors:
+        # biases, w2, RMSNorm scales are consumed as fp32), both in the flat layout
+        self.wbf = torch.zeros(self.n_grad, dtype=torch.bfloat16, device=self.dev)
+        self.wf32 = torch.zeros(self.n_grad, dtype=torch.float32, device=self.dev)
+        views, pviews, offs, off = [], [], [], 0
+        for x, k in zip(sizes, kinds):
             views.append(self.grads[off:off + x])
+            pviews.append(self.wbf[off:off + x] if k == "m" else self.wf32[off:off + x])
             offs.append(off)
             off += pad(x)
+        self._slices = list(zip(offs, sizes, kinds))
+
+        def put(i, a, shape=None):  # initial value of parameter slice i
+            t = torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32).reshape(-1)).to(self.dev)
+            pviews[i].copy_(t)
+            self.wbf[offs[i]:offs[i] + sizes[i]].copy_(t)  # bf16 copy of every slice (the all-gathered copy)
+            return pviews[i].view(*shape) if shape else pviews[i]
+        self.W = [[put(npl * l + i, w, (d, d)) for i, w in enumerate(G.layer_weights(seed, l, d, peaky).as_list())]
+                  for l in range(nl)]
+        if cfg.block:  # NEXT-3: FFN weights (bf16) and RMSNorm scales (fp32) per layer
+            bw = [G.block_weights(seed, l, d, cfg.ffn_mult) for l in range(nl)]
+            self.F = [(put(npl * l + 7, w.W1, (d, md)), put(npl * l + 8, w.W2, (md, d))) for l, w in enumerate(bw)]
+            self.gam = [(put(npl * l + 10, w.gamma1), put(npl * l + 9, w.gamma2)) for l, w in enumerate(bw)]
+            self.gF = [views[npl * l + 7:npl * l + 11] for l in range(nl)]  # dW1f, dW2f, dgamma2, dgamma1
+        t0 = npl * nl
+        hw = G.head_weights(seed, cfg.K, d, cfg.dh)
+        self.W1 = put(t0, np.concatenate([hw.W1[k] for k in range(cfg.K)], axis=1), (d, N))
+        self.b1, self.w2, self.b2 = put(t0 + 1, hw.b1), put(t0 + 2, hw.w2), put(t0 + 3, hw.b2)
         self.gW = [views[npl * l:npl * l + 7] for l in range(nl)]
         # DP all-reduce groups per layer, in the order their gradients complete in the backward
         rng_ = lambda a, b: self.grads[offs[a]:offs[b - 1] + pad(sizes[b - 1])]
@@ -256,24 +292,17 @@ class CadetStack:
                                    rng_(npl * l + 1, npl * l + 4), rng_(npl * l, npl * l + 1)),
                              ffn=rng_(npl * l + 7, npl * l + 10) if cfg.block else None,
                              g1=rng_(npl * l + 10, npl * l + 11) if cfg.block else None) for l in range(nl)]
-        self.gW1, self.gb1, self.gw2, self.gb2 = views[npl * nl:npl * nl + 4]
-        self._tower_off = offs[npl * nl]  # towers (and aux heads) follow the layers
-        if cfg.block:  # NEXT-3: RMSNorm scales (fp32) and FFN weights (bf16) per layer; grads dW1f, dW2f, dg2, dg1
-            bw = [G.block_weights(seed, l, d, cfg.ffn_mult) for l in range(nl)]
-            f32 = lambda a: torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).to(self.dev)
-            self.gam = [(f32(w.gamma1), f32(w.gamma2)) for w in bw]
-            self.F = [(bf(w.W1), bf(w.W2)) for w in bw]
-            self.gF = [views[npl * l + 7:npl * l + 11] for l in range(nl)]
+        self.gW1, self.gb1, self.gw2, self.gb2 = views[t0:t0 + 4]
+        self._tower_off = offs[t0]  # towers (and aux heads) follow the layers
         if cfg.full_loss:  # NEXT-2 auxiliary heads (Eq. 10): J towers of width da, never routed
             aw = G.head_weights(seed + 1, cfg.J, d, cfg.da)
-            self.aW1 = bf(np.concatenate([aw.W1[k] for k in range(cfg.J)], axis=1))
-            self.ab1 = torch.from_numpy(aw.b1.reshape(-1).copy()).to(self.dev)
-            self.aw2 = torch.from_numpy(aw.w2.reshape(-1).copy()).to(self.dev)
-            self.ab2 = torch.from_numpy(aw.b2.copy()).to(self.dev)
-            self.agW1, self.agb1, self.agw2, self.agb2 = views[npl * nl + 4:npl * nl + 8]
+            self.aW1 = put(t0 + 4, np.concatenate([aw.W1[k] for k in range(cfg.J)], axis=1), (d, Na))
+            self.ab1, self.aw2, self.ab2 = put(t0 + 5, aw.b1), put(t0 + 6, aw.w2), put(t0 + 7, aw.b2)
+            self.agW1, self.agb1, self.agw2, self.agb2 = views[t0 + 4:t0 + 8]
             self.lcfg = L.LossConfig()
             L.lib().cadet_default_loss_config(C.byref(self.lcfg), cfg.J)
             self.losses = torch.zeros(cfg.J + 3, dtype=torch.float32, device=self.dev)
+        self._opt = None           # NEXT-4 optimizer state, built at the first optimizer step
         lib = L.lib()
         self.saved_bytes = lib.cadet_attn_saved_bytes(C.byref(self.acfg), T)
         # gradient checkpointing keeps only the layer inputs Hs[l] and ONE saved-activation buffer,
@@ -377,8 +406,11 @@ class CadetStack:
         # layer's weight gradients in four groups (W_o | W_qg, W_kg | W_q, W_k, W_v | W_xg), each as soon
         # as cadet_attn_backward_ev's event for that group fires, overlapping the rest of the backward
         nl = cfg.n_layers
-        buckets = GradBuckets([self.grads[self._tower_off:]], group)
-        if group is not None and self._grad_events is None:
+        # HSDP (NEXT-4) replaces the overlapped gradient all-reduces by one reduce-scatter after the backward
+        hsdp = group is not None and cfg.optimizer == "adamw" and cfg.shard
+        dp = None if hsdp else group
+        buckets = GradBuckets([self.grads[self._tower_off:]], dp)
+        if dp is not None and self._grad_events is None:
             self._side = torch.cuda.Stream(self.dev)
             self._grad_events = [[torch.cuda.Event() for _ in range(6)] for _ in range(nl)]
             for evs in self._grad_events:
@@ -398,7 +430,7 @@ class CadetStack:
         for l in reversed(range(cfg.n_layers)):
             if cfg.recompute:  # refill the single saved buffer with layer l's activations (deterministic fwd)
                 self._layer_forward(l, b, ws, wsn, st, self._rec_y)
-            evs = self._grad_events[l] if group is not None else None
+            evs = self._grad_events[l] if dp is not None else None
 
             def reduce(ev, sl):
                 self._side.wait_event(ev)
@@ -408,9 +440,45 @@ class CadetStack:
         buckets.wait()
         for h in handles:
             h.wait()
+        if cfg.optimizer == "adamw":
+            self.optimizer_step(group if hsdp else None)
         if group is not None:
             torch.distributed.all_reduce(self.loss, group=group)
         return self.loss
+
+    # -------------------------------------------------------------- NEXT-4: optimizer step (HSDP)
+    def optimizer_step(self, group=None):
+        """AdamW (R35) on the flat fp32 master parameters.  With `group` (HSDP within the node): the
+        gradients are reduce-scattered (SUM, R15) so each rank holds the reduced gradient of its shard,
+        AdamW updates that shard of the fp32 master and moments and writes its bf16 copy, and the bf16
+        parameters are all-gathered; the fp32-consumed vectors are widened from that bf16 copy.
+        Without `group` the (already reduced) full buffer is updated on every rank."""
+        cfg = self.cfg
+        world = torch.distributed.get_world_size(group) if group is not None else 1
+        rank = torch.distributed.get_rank(group) if group is not None else 0
+        n = self.n_grad
+        lo, hi = shard_range(n, world, rank)
+        if self._opt is None or self._opt["world"] != world:
+            full = ops.bf16_to_f32(self.wbf)               # matrices: the bf16 values are exact in fp32
+            for off, sz, kind in self._slices:
+                if kind == "v":
+                    full[off:off + sz].copy_(self.wf32[off:off + sz])
+            self._opt = dict(world=world, step=0, master=full[lo:hi].clone(),
+                             m=torch.zeros(hi - lo, dtype=torch.float32, device=self.dev),
+                             v=torch.zeros(hi - lo, dtype=torch.float32, device=self.dev),
+                             g=torch.empty(hi - lo, dtype=torch.float32, device=self.dev) if world > 1 else None,
+                             cfg=ops.adamw_config(lr=cfg.lr, weight_decay=cfg.weight_decay))
+        o = self._opt
+        o["step"] += 1
+        if world > 1:
+            torch.distributed.reduce_scatter_tensor(o["g"], self.grads, group=group)
+            g = o["g"]
+        else:
+            g = self.grads
+        ops.adamw_step(o["cfg"], o["step"], g, o["master"], o["m"], o["v"], self.wbf[lo:hi])
+        if world > 1:
+            torch.distributed.all_gather_into_tensor(self.wbf, self.wbf[lo:hi], group=group)
+        ops.bf16_to_f32(self.wbf, self.wf32)
 
     def capture(self, inp: StepInputs, group=None, host_inp: StepInputs | None = None, loss_h=None):
         """CUDA graph of one whole step: every libcadet launch (and, with host_inp / loss_h, the H2D

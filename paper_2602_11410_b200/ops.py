@@ -174,6 +174,31 @@ def ffn_backward(X, W1, W2, U, Gt, dY, dresid=None, dX=None, dW1=None, dW2=None,
     return dX, dW1, dW2, ws
 
 
+def adamw_config(**kw) -> L.AdamWConfig:
+    c = L.AdamWConfig()
+    L.lib().cadet_default_adamw_config(C.byref(c))
+    for k, v in kw.items():
+        setattr(c, k, v)
+    return c
+
+
+def adamw_step(cfg, step: int, grad, param, m, v, param_bf16=None):
+    """NEXT-4 (R35): fused AdamW over fp32 (grad, param, m, v) in place; param_bf16 gets bf16(param)."""
+    _need_cuda(grad, param, m, v, param_bf16)
+    n = param.numel()
+    assert grad.numel() == n and m.numel() == n and v.numel() == n
+    assert param_bf16 is None or param_bf16.numel() == n
+    L.check(L.lib().cadet_adamw_step(C.byref(cfg), int(step), _p(grad), _p(param), _p(m), _p(v), _p(param_bf16), n,
+                                     _stream()))
+
+
+def bf16_to_f32(src, dst=None):
+    _need_cuda(src, dst)
+    dst = torch.empty(src.shape, dtype=torch.float32, device=src.device) if dst is None else dst
+    L.check(L.lib().cadet_bf16_to_f32(_p(src), _p(dst), src.numel(), _stream()))
+    return dst
+
+
 def chunk(cu_in: torch.Tensor, L_chunk: int, cap: int, ws=None):
     _need_cuda(cu_in)
     ws = workspace(256, cu_in.device) if ws is None else ws

@@ -114,3 +114,52 @@ def test_partition_lpt_balances_under_budget():
         assert max(loads) - min(loads) <= max(user_cost(m, 2048, 352) for m in lens) + 1e-6
     with pytest.raises(ValueError):
         partition_lpt([10, 20, 30], 2, 25, 2048, 64)
+
+
+def _hsdp_worker(rank, world, port, q):
+    """NEXT-4 host logic on gloo: shard_range + reduce_scatter_tensor + the oracle's AdamW on the
+    shard + all_gather_into_tensor (in place) reproduce the unsharded AdamW of the summed gradient."""
+    import os
+    import torch.distributed as dist
+    from oracle import cadet_oracle as O
+    from paper_2602_11410_b200.model import shard_range
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    n = 64 * world * 5
+    rng = np.random.default_rng(7)
+    theta = rng.normal(size=n)
+    grads = [rng.normal(size=n) for _ in range(world)]            # every rank's local gradient
+    lo, hi = shard_range(n, world, rank)
+    g_local = torch.tensor(grads[rank])
+    g_shard = torch.empty(hi - lo, dtype=torch.float64)
+    dist.reduce_scatter_tensor(g_shard, g_local)
+    t, m, v = O.adamw_step(theta[lo:hi], np.zeros(hi - lo), np.zeros(hi - lo), g_shard.numpy(), 1, lr=1e-2)
+    full = torch.zeros(n, dtype=torch.float64)
+    full[lo:hi] = torch.tensor(t)
+    dist.all_gather_into_tensor(full, full[lo:hi].clone())
+    ref, _, _ = O.adamw_step(theta, np.zeros(n), np.zeros(n), np.sum(grads, axis=0), 1, lr=1e-2)
+    q.put((rank, float(np.abs(full.numpy() - ref).max())))
+    dist.destroy_process_group()
+
+
+def test_hsdp_shard_update_equals_unsharded_update():
+    import socket
+    import torch.multiprocessing as mp
+    from paper_2602_11410_b200.model import shard_range
+    assert shard_range(512, 4, 2) == (256, 384)
+    with pytest.raises(ValueError):
+        shard_range(100, 2, 0)
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_hsdp_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert all(err <= 1e-12 for _, err in res)
