@@ -143,6 +143,14 @@ void cadet_tile_shape(int32_t* bm_h, int32_t* bn_h); /* 128, 128: the tile of ca
 size_t cadet_plan_workspace_bytes(int32_t n_seqs, int32_t total_tokens);
 size_t cadet_attn_workspace_bytes(const cadet_attn_config* cfg_h, int32_t n_seqs, int32_t total_tokens);
 size_t cadet_attn_saved_bytes(const cadet_attn_config* cfg_h, int32_t total_tokens);
+/* Optional extra layer workspace enabling the two-pass attention backward (A10): with
+ * ws_bytes >= cadet_attn_workspace_bytes + cadet_attn_bwd_ds_bytes(max_seqlen = the batch's
+ * max_seqlen), cadet_attn_backward stores every visited dS^T tile (bf16, [128 x 128] per tile
+ * pair and head) from the dK/dV kernel and forms dQ = dS K from them, instead of a dQ kernel that
+ * recomputes S and dP (5 instead of 7 MMAs per tile pair).  Same results up to MMA accumulation
+ * order; 0 if the bound overflows. */
+size_t cadet_attn_bwd_ds_bytes(const cadet_attn_config* cfg_h, int32_t n_seqs, int32_t total_tokens,
+                               int32_t max_seqlen);
 size_t cadet_heads_workspace_bytes(const cadet_head_config* h_h, int32_t n_rows);
 
 /* ------------------------------------------------------------------ A1: mask plan

@@ -87,6 +87,7 @@ SIGNATURES = {
     "cadet_plan_workspace_bytes": (SZ, [I32, I32]),
     "cadet_attn_workspace_bytes": (SZ, [PCFG, I32, I32]),
     "cadet_attn_saved_bytes": (SZ, [PCFG, I32]),
+    "cadet_attn_bwd_ds_bytes": (SZ, [C.POINTER(AttnConfig), I32, I32, I32]),
     "cadet_heads_workspace_bytes": (SZ, [C.POINTER(HeadConfig), I32]),
     "cadet_mask_plan": (I32, [PCFG, PB, P, SZ, P]),
     "cadet_mask_export": (I32, [PCFG, PB, P, P, P, I64, P, P]),

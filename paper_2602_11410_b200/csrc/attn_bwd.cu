@@ -13,6 +13,7 @@
 // The extra S/dP recompute (7 MMAs per tile pair instead of 5) buys the removal of 1.1 GB of dQ
 // atomics per C4 step and of the drain -> dP dependency.
 #include <algorithm>
+#include <cstring>
 
 #include "attn_common.cuh"
 #include "prof.cuh"
@@ -436,6 +437,8 @@ __global__ void __launch_bounds__(320, 1)
   if (warp == 0) {
     if (elect_one()) {
       int gq = 0;  // global q-tile counter: stage gq & 1, use gq >> 1
+      // Q_i / dO_i are re-read by every k-tile that sees q-tile i: keep them in L2 (evict_last)
+      const uint64_t pol_qd = l2_policy_evict_last();
       for (int w = blockIdx.x, wi = 0; w < n_work; w += gridDim.x, ++wi) {
         const DkvWork t = dkv_work(p, w);
         if (wi > 0) mbar_wait(&bars->kv_empty, (wi - 1) & 1);
@@ -452,14 +455,14 @@ __global__ void __launch_bounds__(320, 1)
           mbar_expect_tx(&bars->q_full[st], G::TILE_BYTES);
 #pragma unroll
           for (int blk = 0; blk < G::NB; ++blk)
-            tma_load_3d(smem + C::Q_OFF + st * G::TILE_BYTES + blk * G::BLK, &mQ, &bars->q_full[st], blk * G::CB, t.h,
-                        q0);
+            tma_load_3d_hint(smem + C::Q_OFF + st * G::TILE_BYTES + blk * G::BLK, &mQ, &bars->q_full[st], blk * G::CB,
+                             t.h, q0, pol_qd);
           if (use > 0) mbar_wait(&bars->do_empty[st], (use - 1) & 1);
           mbar_expect_tx(&bars->do_full[st], G::TILE_BYTES);
 #pragma unroll
           for (int blk = 0; blk < G::NB; ++blk)
-            tma_load_3d(smem + C::DO_OFF + st * G::TILE_BYTES + blk * G::BLK, &mdO, &bars->do_full[st], blk * G::CB,
-                        t.h, q0);
+            tma_load_3d_hint(smem + C::DO_OFF + st * G::TILE_BYTES + blk * G::BLK, &mdO, &bars->do_full[st],
+                             blk * G::CB, t.h, q0, pol_qd);
         }
       }
     }
@@ -569,6 +572,8 @@ __global__ void __launch_bounds__(320, 1)
       const bool has_next = w + gridDim.x < n_work;
       const int key = t.k0 + tr;
       const bool key_valid = tr < t.keys_valid;
+      // two-pass backward: dS^T tiles of this k-tile go to slots tri_off[seq] + qt (qt + 1) / 2 + kt
+      const int ds_base = p.dS ? p.plan.tri_off[t.seq] + t.kt : 0;
       // query row key+1 carries the PAIR_PREV bit: then it sees this key (the transposed pair cell)
       const bool ppn = key_valid && key + 1 < t.se && p.plan.row_pp[key + 1] != 0;
       for (int it = 0; it < t.n_it; ++it) {
@@ -593,6 +598,7 @@ __global__ void __launch_bounds__(320, 1)
         tc_fence_after();
         PTM(tracer, 6)
         const uint32_t vs = smem_u32(vb);
+        uint32_t wkeep[16];
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
           uint32_t us[32], ud[32];
@@ -610,6 +616,13 @@ __global__ void __launch_bounds__(320, 1)
             if (ppn && dd + 1 >= 0 && dd + 1 < 32) extra |= 1u << (dd + 1);
             dkv_chunk<true>(us, ud, vs + c * 128, key, extra, sl2, wp, wd);
           }
+          if (p.dS) {  // dS^T chunk 0 -> the warp's stage now, chunk 1 kept: both stored after the arrive
+            if (c == 0)
+              warp_stage_rows_bf16(smem_u32(smem + C::STG_OFF + (warp - 2) * 2048), wd);
+            else
+#pragma unroll
+              for (int j = 0; j < 16; ++j) wkeep[j] = wd[j];
+          }
           // P^T / dS^T chunk c -> columns [16c, 16c + 16) of this half: only this thread's own,
           // already-loaded S^T / dP^T chunk 0 is overwritten
           tmem_st16(tmem_addr(tmem, quarter, C::S_COL + grp * 64 + c * 16), wp);
@@ -618,6 +631,19 @@ __global__ void __launch_bounds__(320, 1)
         tmem_st_wait();
         tc_fence_before();
         mbar_arrive(&bars->pds_ready[grp]);
+        if (p.dS) {  // two-pass backward: this warp's 32 keys x 64 q columns of dS^T, off the MMA's path
+          const int qt = entry & 0xFFFF;
+          const int slot = ds_base + qt * (qt + 1) / 2;
+          if (slot < p.ds_slots) {  // (a batch violating max_seqlen latches E_TOO_LONG; stay in bounds)
+            const uint32_t stg = smem_u32(smem + C::STG_OFF + (warp - 2) * 2048);
+            __nv_bfloat16* dst =
+                reinterpret_cast<__nv_bfloat16*>(p.dS) + (((size_t)slot * 128 + quarter * 32) * p.H + t.h) * 128 + grp * 64;
+            warp_flush_rows_bf16(stg, dst, (size_t)p.H * 128, 32, 32);
+            warp_store_rows_bf16(stg, wkeep, dst + 32, (size_t)p.H * 128, 32, 32);
+          } else {
+            __syncwarp();
+          }
+        }
       }
       // dK, dV (thread = key row; each warpgroup writes half of the hd columns)
       PTM(tracer, 7)
@@ -666,6 +692,144 @@ __global__ void __launch_bounds__(320, 1)
   tc_fence_after();
   if (warp == 1) tmem_dealloc<512>(tmem);
   if (threadIdx.x == 0) { TR(1, 3, gtime()); }
+}
+
+// ============================================================================ dQ from stored dS
+// Two-pass backward (p.dS set): attn_bwd_dkv_kernel has stored every visited dS^T tile, so
+// dQ_i = sum_j dS_ij K_j needs no recompute of S and dP (7 -> 5 MMAs per tile pair; the dS
+// round trip is 32 KB of HBM per tile pair each way).  Persistent CTA over the (q-tile, head)
+// list: warp 0 streams (dS^T_j, K_j) through STAGES TMA stages, warp 1 issues one SS MMA chain per
+// tile (A = dS^T as an MN-major operand, B = K_j MN-major) into a double-buffered TMEM
+// accumulator, warps 2..5 drain dQ (x 1/sqrt(hd)) while the next item accumulates.
+template <int HD>
+struct Dq2Cfg {
+  using G = HeadGeom<HD>;
+  static constexpr int THREADS = 192;
+  static constexpr int STAGES = 3;
+  static constexpr int DS_BYTES = 2 * 16384;  // [128 keys][128 q] bf16: 2 blocks of 64 columns
+  static constexpr int STAGE_BYTES = DS_BYTES + G::TILE_BYTES;
+  static constexpr int STG_OFF = STAGES * STAGE_BYTES;
+  static constexpr int BAR_OFF = STG_OFF + 4 * 4096;
+  static constexpr int SMEM = BAR_OFF + 256 + 1024;
+};
+struct Dq2Bars {
+  uint64_t full[4], empty[4], acc_full[2], acc_free[2];
+  uint32_t tmem_base;
+};
+
+template <int HD>
+__global__ void __launch_bounds__(192, 1)
+    attn_bwd_dq2_kernel(const __grid_constant__ CUtensorMap mK, const __grid_constant__ CUtensorMap mDS,
+                        const AttnParams p) {
+  using G = HeadGeom<HD>;
+  using C = Dq2Cfg<HD>;
+  const int n_work = p.plan.counters[0] * p.H;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  Dq2Bars* bars = reinterpret_cast<Dq2Bars*>(smem + C::BAR_OFF);
+  const uint32_t warp = warp_id();
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < C::STAGES; ++s) {
+      mbar_init(&bars->full[s], 1);
+      mbar_init(&bars->empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&bars->acc_full[b], 1);
+      mbar_init(&bars->acc_free[b], 128);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc<256>(&bars->tmem_base);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = bars->tmem_base;
+
+  if (warp == 0) {
+    if (elect_one()) {
+      const uint64_t pol_ds = l2_policy_evict_first(), pol_k = l2_policy_evict_last();
+      int g = 0;
+      for (int w = blockIdx.x; w < n_work; w += gridDim.x) {
+        const DqWork t = dq_work(p, w);
+        const int base = p.plan.tri_off[t.qi.seq] + t.qi.qt * (t.qi.qt + 1) / 2;
+        for (int j = 0; j < t.n_kv; ++j, ++g) {
+          const int st = g % C::STAGES, use = g / C::STAGES;
+          const int kt = visit_tile_b(t.qi, j);
+          if (use > 0) mbar_wait(&bars->empty[st], (use - 1) & 1);
+          mbar_expect_tx(&bars->full[st], C::STAGE_BYTES);
+          uint8_t* sbuf = smem + st * C::STAGE_BYTES;
+#pragma unroll
+          for (int blk = 0; blk < 2; ++blk)
+            tma_load_3d_hint(sbuf + blk * 16384, &mDS, &bars->full[st], blk * 64, t.h, (base + kt) * 128, pol_ds);
+#pragma unroll
+          for (int blk = 0; blk < G::NB; ++blk)
+            tma_load_3d_hint(sbuf + C::DS_BYTES + blk * G::BLK, &mK, &bars->full[st], blk * G::CB, t.h,
+                             t.sa + kt * 128, pol_k);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (elect_one()) {
+      const uint32_t id = idesc_bf16(128, G::HDP, 1, 1);
+      int g = 0;
+      for (int w = blockIdx.x, wi = 0; w < n_work; w += gridDim.x, ++wi) {
+        const int n_kv = dq_work(p, w).n_kv;
+        const int buf = wi & 1, ause = wi >> 1;
+        if (ause > 0) mbar_wait(&bars->acc_free[buf], (ause - 1) & 1);
+        tc_fence_after();
+        for (int j = 0; j < n_kv; ++j, ++g) {
+          const int st = g % C::STAGES, use = g / C::STAGES;
+          mbar_wait(&bars->full[st], use & 1);
+          tc_fence_after();
+          const uint32_t sD = smem_u32(smem + st * C::STAGE_BYTES), sK = sD + C::DS_BYTES;
+#pragma unroll
+          for (int kk = 0; kk < 128 / 16; ++kk)
+            mma_bf16_ss(tmem + buf * 128, p_mnmajor_desc(sD, kk), mnmajor_desc<HD>(sK, kk), id,
+                        (j > 0 || kk > 0) ? 1u : 0u);
+          mma_commit(&bars->empty[st]);
+        }
+        mma_commit(&bars->acc_full[buf]);
+      }
+    }
+  } else {
+    const uint32_t quarter = warp & 3;
+    const uint32_t stg = smem_u32(smem + C::STG_OFF + (warp - 2) * 4096);
+    for (int w = blockIdx.x, wi = 0; w < n_work; w += gridDim.x, ++wi) {
+      const DqWork t = dq_work(p, w);
+      const int buf = wi & 1;
+      mbar_wait(&bars->acc_full[buf], (wi >> 1) & 1);
+      tc_fence_after();
+#pragma unroll 1
+      for (int c = 0; c < G::HDP / 32; ++c) {
+        uint32_t u[32];
+        tmem_ld32(tmem_addr(tmem, quarter, buf * 128 + c * 32), u);
+        tmem_ld_wait();
+        if (t.n_kv == 0) {  // no MMA ran: the accumulator holds stale data
+#pragma unroll
+          for (int j = 0; j < 32; ++j) u[j] = 0u;
+        }
+        const float f = p.scale;
+        const size_t off = (size_t)(t.q0 + quarter * 32) * p.d + (size_t)t.h * p.hd + c * 32;
+        if (p.dq_bf16) {
+          uint32_t wv[16];
+#pragma unroll
+          for (int jj = 0; jj < 16; ++jj)
+            wv[jj] = pack_bf16(f * __uint_as_float(u[2 * jj]), f * __uint_as_float(u[2 * jj + 1]));
+          warp_store_rows_bf16(stg, wv, reinterpret_cast<__nv_bfloat16*>(p.dQ) + off, p.d,
+                               t.rows_valid - (int)quarter * 32, min(32, p.hd - c * 32));
+        } else {
+          warp_store_rows_f32(stg, u, f, reinterpret_cast<float*>(p.dQ) + off, p.d, t.rows_valid - (int)quarter * 32,
+                              min(32, p.hd - c * 32));
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&bars->acc_free[buf]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 1) tmem_dealloc<256>(tmem);
 }
 
 // D_i = rowsum(dO_i * O_i) per head (FlashAttention preprocess), bf16 inputs, fp32 out [H, T].
@@ -724,7 +888,7 @@ static int num_sms_attn() {
 
 template <int HD>
 static cudaError_t bwd_hd(const CUtensorMap& mQ, const CUtensorMap& mK, const CUtensorMap& mV, const CUtensorMap& mdO,
-                          const AttnParams& p, cudaStream_t st) {
+                          const CUtensorMap& mDS, const AttnParams& p, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(attn_bwd_dq_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -732,6 +896,9 @@ static cudaError_t bwd_hd(const CUtensorMap& mQ, const CUtensorMap& mK, const CU
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(attn_bwd_dkv_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                DkvCfg<HD>::SMEM);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(attn_bwd_dq2_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               Dq2Cfg<HD>::SMEM);
     if (e != cudaSuccess) return e;
     attr = true;
   }
@@ -740,8 +907,13 @@ static cudaError_t bwd_hd(const CUtensorMap& mQ, const CUtensorMap& mK, const CU
   if (grid == 0) return cudaSuccess;
   {
     ProfScope ps(PROF_ATTN_BWD, st, 2);
-    attn_bwd_dq_kernel<HD><<<grid, DqCfg<HD>::THREADS, DqCfg<HD>::SMEM, st>>>(mQ, mK, mV, mdO, p);
-    attn_bwd_dkv_kernel<HD><<<grid, DkvCfg<HD>::THREADS, DkvCfg<HD>::SMEM, st>>>(mQ, mK, mV, mdO, p);
+    if (p.dS) {  // two-pass: dK, dV and the dS^T tiles, then dQ from the tiles
+      attn_bwd_dkv_kernel<HD><<<grid, DkvCfg<HD>::THREADS, DkvCfg<HD>::SMEM, st>>>(mQ, mK, mV, mdO, p);
+      attn_bwd_dq2_kernel<HD><<<grid, Dq2Cfg<HD>::THREADS, Dq2Cfg<HD>::SMEM, st>>>(mK, mDS, p);
+    } else {
+      attn_bwd_dq_kernel<HD><<<grid, DqCfg<HD>::THREADS, DqCfg<HD>::SMEM, st>>>(mQ, mK, mV, mdO, p);
+      attn_bwd_dkv_kernel<HD><<<grid, DkvCfg<HD>::THREADS, DkvCfg<HD>::SMEM, st>>>(mQ, mK, mV, mdO, p);
+    }
   }
   return cudaGetLastError();
 }
@@ -758,15 +930,17 @@ cudaError_t attn_bwd_pre_launch(const void* O, const void* dO, float* D, float* 
 
 cudaError_t attn_bwd_launch(const void* Qr, const void* Kr, const void* V, const void* dO, const AttnParams& p,
                             cudaStream_t st) {
-  CUtensorMap mQ, mK, mV, mdO;
+  CUtensorMap mQ, mK, mV, mdO, mDS;
+  memset(&mDS, 0, sizeof(mDS));
   if (!make_head_map(&mQ, Qr, p.T, p.H, p.hd) || !make_head_map(&mK, Kr, p.T, p.H, p.hd) ||
-      !make_head_map(&mV, V, p.T, p.H, p.hd) || !make_head_map(&mdO, dO, p.T, p.H, p.hd))
+      !make_head_map(&mV, V, p.T, p.H, p.hd) || !make_head_map(&mdO, dO, p.T, p.H, p.hd) ||
+      (p.dS && !make_head_map(&mDS, p.dS, p.ds_slots * 128, p.H, 128)))
     return cudaErrorInvalidValue;
   switch ((p.hd + 31) / 32 * 32) {
-    case 32: return bwd_hd<32>(mQ, mK, mV, mdO, p, st);
-    case 64: return bwd_hd<64>(mQ, mK, mV, mdO, p, st);
-    case 96: return bwd_hd<96>(mQ, mK, mV, mdO, p, st);
-    case 128: return bwd_hd<128>(mQ, mK, mV, mdO, p, st);
+    case 32: return bwd_hd<32>(mQ, mK, mV, mdO, mDS, p, st);
+    case 64: return bwd_hd<64>(mQ, mK, mV, mdO, mDS, p, st);
+    case 96: return bwd_hd<96>(mQ, mK, mV, mdO, mDS, p, st);
+    case 128: return bwd_hd<128>(mQ, mK, mV, mdO, mDS, p, st);
     default: return cudaErrorInvalidValue;
   }
 }

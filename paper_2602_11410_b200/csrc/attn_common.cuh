@@ -77,6 +77,12 @@ struct AttnParams {
   float* Opart;      // [splits][T][d]
   float* Mpart;      // [splits][H][T] running max (log2 units) of the split
   float* Lpart;      // [splits][H][T] row sum of the split (0 = empty split)
+  // two-pass backward (layer path, when the workspace holds the dS region): attn_bwd_dkv_kernel
+  // stores every visited dS^T tile (bf16, unscaled) at slot tri_off[seq] + qt (qt + 1) / 2 + kt,
+  // rows slot * 128 + key, head h at columns [128 h, 128 h + 128); attn_bwd_dq2_kernel then forms
+  // dQ = dS K from those tiles instead of recomputing S and dP
+  void* dS;          // nullptr: single-pass dQ kernel (recompute)
+  int32_t ds_slots;
 };
 
 }  // namespace cadet

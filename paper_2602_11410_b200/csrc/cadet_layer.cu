@@ -185,8 +185,18 @@ size_t layer_ws_base_bytes(const cadet_attn_config* c, int n, int T) {
          a256((size_t)4 * c->n_heads * T) + 8 * bf_sz(T, d) + 4 * f_sz(T, d);
 }
 size_t layer_ws_bytes(const cadet_attn_config* c, int n, int T) {
-  const int d = c->d_model;
   return layer_ws_base_bytes(c, n, T) + fwd_split_bytes(c, n, T);
+}
+// Two-pass attention backward: dS^T tile slots (sum over sequences of nq_s (nq_s + 1) / 2, bounded
+// with nq_s <= max_seqlen / 128 + 3 exactly like the plan's visit lists) x H x [128 x 128] bf16.
+int32_t ds_slots_of(int n, int T, int max_seqlen) {
+  const long long nq = (T + 127) / 128 + n, hm = (max_seqlen + 127) / 128 + 3;
+  const long long s = nq * (hm + 1) / 2 + hm;
+  return s > (1LL << 24) ? 0 : (int32_t)s;
+}
+size_t ds_bytes_of(const cadet_attn_config* c, int n, int T, int max_seqlen) {
+  const int32_t s = ds_slots_of(n, T, max_seqlen);
+  return s ? a256((size_t)s * c->n_heads * 128 * 128 * 2) : 0;
 }
 LayerWs carve_ws(void* ws, const cadet_attn_config* c, int n, int T) {
   const int d = c->d_model;
@@ -288,6 +298,10 @@ extern "C" {
 size_t cadet_attn_workspace_bytes(const cadet_attn_config* c, int32_t n, int32_t T) {
   if (check_cfg(c)) return 0;
   return layer_ws_bytes(c, n, T);
+}
+size_t cadet_attn_bwd_ds_bytes(const cadet_attn_config* c, int32_t n, int32_t T, int32_t max_seqlen) {
+  if (check_cfg(c) || n < 0 || T < 0 || max_seqlen < 1) return 0;
+  return ds_bytes_of(c, n, T, max_seqlen);
 }
 size_t cadet_attn_saved_bytes(const cadet_attn_config* c, int32_t T) {
   if (check_cfg(c)) return 0;
@@ -441,6 +455,13 @@ cadet_status cadet_attn_backward_ev(const cadet_attn_config* cfg, const cadet_ba
     p.dq_bf16 = 1;  // dQ_r rounded to bf16 like dK_r before R(-alpha) and the gate backward
     p.dK = W.dKr;
     p.dV = W.dV;
+    // two-pass backward when the caller's workspace holds the dS region (after the layer's own
+    // buffers, before the forward split partials at the end; cadet_attn_bwd_ds_bytes)
+    const size_t dsb = ds_bytes_of(cfg, n, T, b->max_seqlen);
+    if (dsb && ws_bytes >= layer_ws_bytes(cfg, n, T) + dsb) {
+      p.dS = reinterpret_cast<uint8_t*>(ws) + layer_ws_base_bytes(cfg, n, T);
+      p.ds_slots = ds_slots_of(n, T, b->max_seqlen);
+    }
     e = attn_bwd_pre_launch(L.O, dO, W.D, W.dQacc, T, H, hd, st);
     if (e == cudaSuccess) e = zero_pad_rows_launch(W.dQacc, d * 2, T, b->cu_seqlens, n, st);
     if (e == cudaSuccess) e = zero_pad_rows_launch(W.dKr, d * 2, T, b->cu_seqlens, n, st);

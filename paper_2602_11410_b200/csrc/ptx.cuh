@@ -112,6 +112,27 @@ CADET_DEV void tma_load_3d(void* dst, const CUtensorMap* m, uint64_t* bar, int c
       : "memory");
 }
 
+// L2 eviction-priority policies for TMA loads: streamed-once data (evict_first) must not push out
+// tiles that other CTAs re-read (evict_last).
+CADET_DEV uint64_t l2_policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+CADET_DEV uint64_t l2_policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+CADET_DEV void tma_load_3d_hint(void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1, int c2,
+                                uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%3, "
+      "%4, %5}], [%2], %6;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "l"(policy)
+      : "memory");
+}
+
 // ------------------------------------------------------------------ tcgen05 / TMEM
 template <uint32_t NCOLS>
 CADET_DEV void tmem_alloc(uint32_t* dst_smem) {  // whole warp
@@ -313,6 +334,26 @@ CADET_DEV void warp_store_rows_bf16(uint32_t stage, const uint32_t (&w)[16], __n
 #pragma unroll
   for (int j = 0; j < 4; ++j)
     sts_u4(stage + lane * 64 + ((j ^ ((lane >> 1) & 3)) << 4), w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
+  __syncwarp();
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int row = i * 8 + (lane >> 2), j = lane & 3;
+    const uint4 v = lds_u4(stage + row * 64 + ((j ^ ((row >> 1) & 3)) << 4));
+    if (row < rows_valid && j * 8 < ncol) *reinterpret_cast<uint4*>(g0 + (size_t)row * ld + j * 8) = v;
+  }
+  __syncwarp();
+}
+// The same store in two phases, so the global half can be deferred (e.g. past a barrier arrive):
+// warp_stage_rows_bf16 writes the lane's row into the swizzled stage; warp_flush_rows_bf16 issues
+// the coalesced global stores from it.
+CADET_DEV void warp_stage_rows_bf16(uint32_t stage, const uint32_t (&w)[16]) {
+  const uint32_t lane = threadIdx.x & 31;
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+    sts_u4(stage + lane * 64 + ((j ^ ((lane >> 1) & 3)) << 4), w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
+}
+CADET_DEV void warp_flush_rows_bf16(uint32_t stage, __nv_bfloat16* g0, size_t ld, int rows_valid, int ncol) {
+  const uint32_t lane = threadIdx.x & 31;
   __syncwarp();
 #pragma unroll
   for (int i = 0; i < 4; ++i) {

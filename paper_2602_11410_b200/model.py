@@ -335,7 +335,9 @@ class CadetStack:
             return
         lib = L.lib()
         cfg = self.cfg
-        wsb = lib.cadet_attn_workspace_bytes(C.byref(self.acfg), n_chunks, cfg.budget)
+        # + the dS region of the two-pass attention backward (cadet_attn_bwd_ds_bytes)
+        wsb = lib.cadet_attn_workspace_bytes(C.byref(self.acfg), n_chunks, cfg.budget) + \
+            lib.cadet_attn_bwd_ds_bytes(C.byref(self.acfg), n_chunks, cfg.budget, cfg.L_chunk)
         if self._ws is None or self._ws.numel() < wsb:
             self._ws = ops.workspace(wsb, self.dev)
         hc = L.HeadConfig(cfg.K, cfg.d_model, cfg.dh, 0)

@@ -83,14 +83,15 @@ def layer_case(lengths, d, H, nc=None, seed=0, peaky=False, T_extra=5, stress=Tr
     return cu, t, s, ncv, T, X, W
 
 
-def run_layer_forward(ops, cfg, b, X, W, T):
+def run_layer_forward(ops, cfg, b, X, W, T, two_pass=False):
     from paper_2602_11410_b200 import _lib as L
     d = cfg.d_model
     Xd = bf16_tensor(X)
     Wd = [bf16_tensor(w) for w in W.as_list()]
     w = L.AttnWeights(*[x.data_ptr() for x in Wd])
     saved = torch.zeros(L.lib().cadet_attn_saved_bytes(C.byref(cfg), T), dtype=torch.uint8, device="cuda")
-    ws = ops.workspace(L.lib().cadet_attn_workspace_bytes(C.byref(cfg), b.n_seqs, T))
+    extra = L.lib().cadet_attn_bwd_ds_bytes(C.byref(cfg), b.n_seqs, T, b.max_seqlen) if two_pass else 0
+    ws = ops.workspace(L.lib().cadet_attn_workspace_bytes(C.byref(cfg), b.n_seqs, T) + extra)
     Y = torch.empty(T, d, dtype=torch.bfloat16, device="cuda")
     L.check(L.lib().cadet_attn_forward(C.byref(cfg), C.byref(b.struct()), C.byref(w), C.c_void_p(Xd.data_ptr()),
                                        C.c_void_p(Y.data_ptr()), None, C.c_void_p(saved.data_ptr()),
@@ -164,14 +165,17 @@ def test_layer_forward_stages_and_end_to_end(ops, case):
     assert (Yg[n:] == 0).all()
 
 
+@pytest.mark.parametrize("two_pass", [False, True])
 @pytest.mark.parametrize("case", range(len(LAYER_CASES)))
-def test_layer_backward_end_to_end(ops, case):
+def test_layer_backward_end_to_end(ops, case, two_pass):
+    """two_pass: the workspace holds the dS region, so dQ comes from the dS^T tiles the dK/dV kernel
+    stored (attn_bwd_dq2_kernel) instead of the recomputing dQ kernel."""
     from paper_2602_11410_b200 import _lib as L
     lengths, d, H, nc, peaky = LAYER_CASES[case]
     cu, t, s, ncv, T, X, W = layer_case(lengths, d, H, nc, seed=20 + case, peaky=peaky)
     cfg = ops.config(d, H, delta_delay_ms=120_000, rope_phi_min=0.5, rope_base=1e4, rope_delta_t_max_ms=86_400_000)
     b = to_dev_batch(cu, t, s, ncv, T)
-    Y, saved, ws, Xd, Wd, w = run_layer_forward(ops, cfg, b, X, W, T)
+    Y, saved, ws, Xd, Wd, w = run_layer_forward(ops, cfg, b, X, W, T, two_pass=two_pass)
     dY = G.normal_bf16(99, case, (T, d))
     dY[cu[-1]:] = 0
     dYd = bf16_tensor(dY)
