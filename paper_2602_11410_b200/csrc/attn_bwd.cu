@@ -16,6 +16,7 @@
 #include <cstring>
 
 #include "attn_common.cuh"
+#include "launch.cuh"
 #include "prof.cuh"
 
 namespace cadet {
@@ -106,7 +107,7 @@ __global__ void __launch_bounds__(320, 1)
                        const AttnParams p) {
   using G = HeadGeom<HD>;
   using C = DqCfg<HD>;
-  const int n_work = p.plan.counters[0] * p.H;
+  pdl_trigger();
   if (threadIdx.x == 0) { TR(0, 0, gtime()); TR(0, 4, smid()); }
 
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -135,6 +136,8 @@ __global__ void __launch_bounds__(320, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = bars->tmem_base;
+  pdl_wait();  // everything below reads the previous kernels' outputs
+  const int n_work = p.plan.counters[0] * p.H;
 
   if (warp == 0) {
     if (elect_one()) {
@@ -404,7 +407,7 @@ __global__ void __launch_bounds__(320, 1)
                         const AttnParams p) {
   using G = HeadGeom<HD>;
   using C = DkvCfg<HD>;
-  const int n_work = p.plan.counters[0] * p.H;
+  pdl_trigger();
   if (threadIdx.x == 0) { TR(1, 0, gtime()); TR(1, 4, smid()); }
 
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -432,6 +435,8 @@ __global__ void __launch_bounds__(320, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = bars->tmem_base;
+  pdl_wait();  // everything below reads the previous kernels' outputs
+  const int n_work = p.plan.counters[0] * p.H;
   const int32_t* list = p.plan.bwd_list;
 
   if (warp == 0) {
@@ -723,7 +728,7 @@ __global__ void __launch_bounds__(192, 1)
                         const AttnParams p) {
   using G = HeadGeom<HD>;
   using C = Dq2Cfg<HD>;
-  const int n_work = p.plan.counters[0] * p.H;
+  pdl_trigger();
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   Dq2Bars* bars = reinterpret_cast<Dq2Bars*>(smem + C::BAR_OFF);
@@ -744,6 +749,8 @@ __global__ void __launch_bounds__(192, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = bars->tmem_base;
+  pdl_wait();  // everything below reads the previous kernels' outputs
+  const int n_work = p.plan.counters[0] * p.H;
 
   if (warp == 0) {
     if (elect_one()) {
@@ -837,6 +844,8 @@ __global__ void __launch_bounds__(192, 1)
 // segmented shuffles when hd / 8 lanes is a power of two dividing the pass, else shared atomics.
 __global__ void __launch_bounds__(256) attn_bwd_pre_kernel(const __nv_bfloat16* O, const __nv_bfloat16* dO, float* D,
                                                             int T, int H, int hd) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ float acc[8][128];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int row = blockIdx.x * 8 + w;
@@ -908,11 +917,15 @@ static cudaError_t bwd_hd(const CUtensorMap& mQ, const CUtensorMap& mK, const CU
   {
     ProfScope ps(PROF_ATTN_BWD, st, 2);
     if (p.dS) {  // two-pass: dK, dV and the dS^T tiles, then dQ from the tiles
-      attn_bwd_dkv_kernel<HD><<<grid, DkvCfg<HD>::THREADS, DkvCfg<HD>::SMEM, st>>>(mQ, mK, mV, mdO, p);
-      attn_bwd_dq2_kernel<HD><<<grid, Dq2Cfg<HD>::THREADS, Dq2Cfg<HD>::SMEM, st>>>(mK, mDS, p);
+      cudaError_t e = launch_pdl(attn_bwd_dkv_kernel<HD>, grid, DkvCfg<HD>::THREADS, DkvCfg<HD>::SMEM, st, mQ, mK, mV,
+                                 mdO, p);
+      if (e == cudaSuccess) e = launch_pdl(attn_bwd_dq2_kernel<HD>, grid, Dq2Cfg<HD>::THREADS, Dq2Cfg<HD>::SMEM, st, mK, mDS, p);
+      if (e != cudaSuccess) return e;
     } else {
-      attn_bwd_dq_kernel<HD><<<grid, DqCfg<HD>::THREADS, DqCfg<HD>::SMEM, st>>>(mQ, mK, mV, mdO, p);
-      attn_bwd_dkv_kernel<HD><<<grid, DkvCfg<HD>::THREADS, DkvCfg<HD>::SMEM, st>>>(mQ, mK, mV, mdO, p);
+      cudaError_t e = launch_pdl(attn_bwd_dq_kernel<HD>, grid, DqCfg<HD>::THREADS, DqCfg<HD>::SMEM, st, mQ, mK, mV, mdO, p);
+      if (e == cudaSuccess)
+        e = launch_pdl(attn_bwd_dkv_kernel<HD>, grid, DkvCfg<HD>::THREADS, DkvCfg<HD>::SMEM, st, mQ, mK, mV, mdO, p);
+      if (e != cudaSuccess) return e;
     }
   }
   return cudaGetLastError();
@@ -922,7 +935,7 @@ cudaError_t attn_bwd_pre_launch(const void* O, const void* dO, float* D, float* 
                                 cudaStream_t st) {
   ProfScope ps(PROF_OTHER, st, 1);
   if (T > 0)
-    attn_bwd_pre_kernel<<<(T + 7) / 8, 256, 0, st>>>(reinterpret_cast<const __nv_bfloat16*>(O),
+    launch_pdl(attn_bwd_pre_kernel, dim3((T + 7) / 8), dim3(256), 0, st, reinterpret_cast<const __nv_bfloat16*>(O),
                                                       reinterpret_cast<const __nv_bfloat16*>(dO), D, T, H, hd);
   (void)dQacc;  // dQ is written exactly once per row by attn_bwd_dq_kernel (pad rows zeroed by the caller)
   return cudaGetLastError();

@@ -14,6 +14,7 @@
 // ~96 KB of shared memory and 256 TMEM columns per CTA, so two CTAs share an SM and one CTA's
 // softmax overlaps the other's MMAs (the role FA4's two softmax warpgroups play).
 #include "attn_common.cuh"
+#include "launch.cuh"
 #include "prof.cuh"
 
 namespace cadet {
@@ -56,6 +57,8 @@ __global__ void __launch_bounds__(192, 2)
                     const __grid_constant__ CUtensorMap mV, const AttnParams p) {
   using G = HeadGeom<HD>;
   using C = FwdCfg<HD>;
+  pdl_trigger();
+  pdl_wait();  // not persistent: the whole kernel reads the previous kernels' outputs
   const int nq_total = p.plan.counters[0];
   const int S = p.fwd_splits;
   const int b = blockIdx.x / (p.H * S);
@@ -325,6 +328,8 @@ __global__ void __launch_bounds__(192, 2)
 // Split-KV merge: per row and head, rescale the splits' partials to the common max and normalise.
 // Rows with no visible key in any split (pad rows) get O = 0, LSE = 0 (R17).
 __global__ void __launch_bounds__(256) attn_fwd_merge_kernel(const AttnParams p) {
+  pdl_trigger();
+  pdl_wait();
   const int row = blockIdx.x;
   const int S = p.fwd_splits;
   if (row >= p.cu[p.n]) return;  // pad rows: zeroed by the caller, no partials
@@ -384,8 +389,9 @@ static cudaError_t fwd_hd(const CUtensorMap& mQ, const CUtensorMap& mK, const CU
   const int grid = p.plan.nq_cap * p.H * p.fwd_splits;
   if (grid == 0) return cudaSuccess;
   ProfScope ps(PROF_ATTN_FWD, st, p.fwd_splits > 1 ? 2 : 1);
-  attn_fwd_kernel<HD><<<grid, 192, C::SMEM, st>>>(mQ, mK, mV, p);
-  if (p.fwd_splits > 1) attn_fwd_merge_kernel<<<p.T, 256, 0, st>>>(p);
+  cudaError_t e = launch_pdl(attn_fwd_kernel<HD>, grid, 192, C::SMEM, st, mQ, mK, mV, p);
+  if (e != cudaSuccess) return e;
+  if (p.fwd_splits > 1) launch_pdl(attn_fwd_merge_kernel, dim3(p.T), dim3(256), 0, st, p);
   return cudaGetLastError();
 }
 

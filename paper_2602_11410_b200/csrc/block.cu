@@ -4,6 +4,7 @@
 //                       registers over grid-strided rows, one block reduction + atomic per column
 // HBM-bound: 2 d B read + 2 d B written per row forward, 6 d B read + 2 d B written backward.
 #include "../../include/cadet.h"
+#include "launch.cuh"
 #include "prof.cuh"
 #include "ptx.cuh"
 
@@ -39,6 +40,8 @@ __device__ __forceinline__ void load_row(const __nv_bfloat16* base, int d, int l
 
 __global__ void __launch_bounds__(256, 2) rmsnorm_fwd_kernel(const __nv_bfloat16* X, const float* gamma, int T, int d,
                                                           __nv_bfloat16* Y, float* rstd) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ __align__(16) float g_s[256 * RMS_MAXC];
   for (int i = threadIdx.x; i < d; i += blockDim.x) g_s[i] = gamma[i];
   __syncthreads();
@@ -97,6 +100,8 @@ __global__ void __launch_bounds__(256, 2) rmsnorm_fwd_kernel(const __nv_bfloat16
 __global__ void __launch_bounds__(256) rmsnorm_bwd_kernel(const __nv_bfloat16* X, const float* gamma, const float* rstd,
                                                           const __nv_bfloat16* dY, const __nv_bfloat16* dresid, int T,
                                                           int d, __nv_bfloat16* dX, float* dgamma) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ __align__(16) float g_s[256 * RMS_MAXC];
   __shared__ __align__(16) float dg_s[8][256 * RMS_MAXC];  // per-warp dgamma partials (lane-private columns)
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -188,7 +193,7 @@ cadet_status cadet_rmsnorm_forward(const void* X, const float* gamma, int32_t T,
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   ProfScope ps(PROF_OTHER, st, 1);
   if (T > 0)
-    rmsnorm_fwd_kernel<<<min((T + 15) / 16, 2 * sm_count()), 256, 0, st>>>(reinterpret_cast<const __nv_bfloat16*>(X), gamma, T, d,
+    launch_pdl(rmsnorm_fwd_kernel, dim3(min((T + 15) / 16, 2 * sm_count())), dim3(256), 0, st, reinterpret_cast<const __nv_bfloat16*>(X), gamma, T, d,
                                                    reinterpret_cast<__nv_bfloat16*>(Y), rstd);
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
@@ -214,8 +219,7 @@ cadet_status cadet_rmsnorm_backward(const void* X, const float* gamma, const flo
   ProfScope ps(PROF_OTHER, st, 1);
   if (T > 0) {
     const int blocks = min((T + 7) / 8, 3 * sm_count());
-    rmsnorm_bwd_kernel<<<blocks, 256, 0, st>>>(
-        reinterpret_cast<const __nv_bfloat16*>(X), gamma, rstd, reinterpret_cast<const __nv_bfloat16*>(dY),
+    launch_pdl(rmsnorm_bwd_kernel, dim3(blocks), dim3(256), 0, st, reinterpret_cast<const __nv_bfloat16*>(X), gamma, rstd, reinterpret_cast<const __nv_bfloat16*>(dY),
         reinterpret_cast<const __nv_bfloat16*>(dresid), T, d, reinterpret_cast<__nv_bfloat16*>(dX), dgamma);
   }
   const cudaError_t e = cudaGetLastError();

@@ -9,6 +9,7 @@
 //
 // C[M,N] = sum_seg A_seg[M,K_seg] . B_seg[K_seg,N], tiles 128 x BN x 64, split-K optional.
 #include "gemm.cuh"
+#include "launch.cuh"
 #include "prof.cuh"
 #include "ptx.cuh"
 #include "tma_host.cuh"
@@ -252,87 +253,6 @@ __device__ __forceinline__ void run_epilogue(const EpiParams& e, int row, int M,
   }
 }
 
-// Warp-cooperative variants: the 32 lanes hold rows row0 .. row0 + 31 of the same 32 columns
-// (tcgen05.ld 32x32b layout).  Global traffic goes through a per-warp 4 KB swizzled transpose
-// (ptx.cuh) so each load / store instruction covers whole row segments instead of 32 lines.
-// bf16 32 x 32 slice in two phases, so the global loads of a later slice can be issued early:
-// (1) coalesced loads (8 rows x 64 B per instruction) into registers, (2) transpose to this lane's row.
-__device__ __forceinline__ void warp_ldg_rows_bf16(const void* base, size_t off0, size_t ld, int rows_valid,
-                                                   uint4 (&g)[4]) {
-  const uint32_t lane = threadIdx.x & 31;
-  const __nv_bfloat16* b = reinterpret_cast<const __nv_bfloat16*>(base) + off0;
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int row = i * 8 + (lane >> 2), j = lane & 3;
-    g[i] = row < rows_valid ? *reinterpret_cast<const uint4*>(b + (size_t)row * ld + j * 8) : make_uint4(0, 0, 0, 0);
-  }
-}
-__device__ __forceinline__ void warp_sts_rows_bf16(uint32_t stg, const uint4 (&g)[4], float (&x)[32]) {
-  const uint32_t lane = threadIdx.x & 31;
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int row = i * 8 + (lane >> 2), j = lane & 3;
-    sts_u4(stg + row * 64 + ((j ^ ((row >> 1) & 3)) << 4), g[i].x, g[i].y, g[i].z, g[i].w);
-  }
-  __syncwarp();
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const uint4 u = lds_u4(stg + lane * 64 + ((j ^ ((lane >> 1) & 3)) << 4));
-    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const float2 f = __bfloat1622float2(h[e]);
-      x[j * 8 + e * 2] = f.x;
-      x[j * 8 + e * 2 + 1] = f.y;
-    }
-  }
-  __syncwarp();
-}
-
-// fp32 32 x 32 slice in the same two phases (4 rows x 128 B per load instruction).
-__device__ __forceinline__ void warp_ldg_rows_f32(const void* base, size_t off0, size_t ld, int rows_valid,
-                                                  uint4 (&g)[8]) {
-  const uint32_t lane = threadIdx.x & 31;
-  const float* b = reinterpret_cast<const float*>(base) + off0;
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const int row = i * 4 + (lane >> 3), j = lane & 7;
-    g[i] = row < rows_valid ? *reinterpret_cast<const uint4*>(b + (size_t)row * ld + j * 4) : make_uint4(0, 0, 0, 0);
-  }
-}
-__device__ __forceinline__ void warp_sts_rows_f32(uint32_t stg, const uint4 (&g)[8], float (&x)[32]) {
-  const uint32_t lane = threadIdx.x & 31;
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const int row = i * 4 + (lane >> 3), j = lane & 7;
-    sts_u4(stg + row * 128 + ((j ^ (row & 7)) << 4), g[i].x, g[i].y, g[i].z, g[i].w);
-  }
-  __syncwarp();
-#pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    const uint4 u = lds_u4(stg + lane * 128 + ((j ^ (lane & 7)) << 4));
-    x[j * 4] = __uint_as_float(u.x);
-    x[j * 4 + 1] = __uint_as_float(u.y);
-    x[j * 4 + 2] = __uint_as_float(u.z);
-    x[j * 4 + 3] = __uint_as_float(u.w);
-  }
-  __syncwarp();
-}
-
-__device__ __forceinline__ void warp_load_rows(uint32_t stg, const void* base, int is_f32, size_t off0, size_t ld,
-                                               int rows_valid, float (&x)[32]) {
-  const uint32_t lane = threadIdx.x & 31;
-  if (!is_f32) {
-    uint4 g[4];
-    warp_ldg_rows_bf16(base, off0, ld, rows_valid, g);
-    warp_sts_rows_bf16(stg, g, x);
-    return;
-  } else {
-    uint4 g[8];
-    warp_ldg_rows_f32(base, off0, ld, rows_valid, g);
-    warp_sts_rows_f32(stg, g, x);
-  }
-}
 __device__ __forceinline__ void warp_store_rows(uint32_t stg, void* base, int is_f32, size_t off0, size_t ld,
                                                 int rows_valid, const float (&v)[32]) {
   if (!is_f32) {
@@ -458,6 +378,7 @@ __device__ __forceinline__ void run_epilogue_warp(const EpiParams& e, int row0, 
 // ---------------------------------------------------------------- kernel
 template <int BN, uint32_t MODES>
 __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_kernel(const __grid_constant__ GemmKParams P) {
+  pdl_trigger();
   using C = GemmCfg<BN>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -491,6 +412,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_kernel(const __grid_cons
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_wait();  // operands / epilogue inputs are the previous kernels' outputs
 
   // registers: warpgroup 0 (TMA, MMA, allocator, idle) gives 104 per thread to the epilogue warpgroups
   if (warp == 0) {
@@ -643,6 +565,7 @@ struct PairCfg {
 template <uint32_t MODES>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
     gemm_pair_kernel(const __grid_constant__ GemmKParams P) {
+  pdl_trigger();
   using C = PairCfg;
   constexpr int BN = 256;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -680,6 +603,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
   cluster_sync_all();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_wait();  // operands / epilogue inputs are the previous kernels' outputs
   const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
 
   if (warp == 0) {
@@ -859,7 +783,11 @@ static cudaError_t launch_pair(const GemmKParams& P, cudaStream_t stream) {
   int pairs = num_sms() / 2;
   if (P.total_units < pairs) pairs = P.total_units;
   ProfScope ps(PROF_GEMM, stream, 1);
-  gemm_pair_kernel<MODES><<<2 * pairs, GEMM_THREADS, PairCfg::SMEM, stream>>>(P);
+  {
+    const cudaError_t e = launch_pdl(gemm_pair_kernel<MODES>, dim3(2 * pairs), dim3(GEMM_THREADS), PairCfg::SMEM,
+                                     stream, P);
+    if (e != cudaSuccess) return e;
+  }
   return cudaGetLastError();
 }
 
@@ -890,7 +818,10 @@ static cudaError_t launch_bn(const GemmKParams& P, cudaStream_t stream) {
   }
   const int grid = P.total_units < num_sms() ? P.total_units : num_sms();
   ProfScope ps(PROF_GEMM, stream, 1);
-  gemm_kernel<BN, MODES><<<grid, GEMM_THREADS, C::SMEM, stream>>>(P);
+  {
+    const cudaError_t e = launch_pdl(gemm_kernel<BN, MODES>, dim3(grid), dim3(GEMM_THREADS), C::SMEM, stream, P);
+    if (e != cudaSuccess) return e;
+  }
   return cudaGetLastError();
 }
 

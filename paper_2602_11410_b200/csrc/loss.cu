@@ -11,12 +11,15 @@
 
 #include "../../include/cadet.h"
 #include "misc.cuh"
+#include "launch.cuh"
 #include "prof.cuh"
 #include "ptx.cuh"
 
 namespace cadet {
 
 __global__ void routed_logits_kernel(const float* logits, int K, const int32_t* bucket, int n, float* z) {
+  pdl_trigger();
+  pdl_wait();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) z[i] = logits[(size_t)i * K + min(max(bucket[i], 0), K - 1)];
 }
@@ -25,6 +28,8 @@ __global__ void routed_logits_kernel(const float* logits, int K, const int32_t* 
 // their logits (zp, zn) or, for the local samples, their indices (ip, in_).
 __global__ void __launch_bounds__(1024) compact_kernel(const float* z_all, const float* y_all, int n_all, float* zp,
                                                        float* zn, int* counts, int* ip = nullptr, int* in_ = nullptr) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ int sh[1024];
   int np = 0, nn = 0;
   for (int base = 0; base < n_all; base += 1024) {
@@ -76,6 +81,8 @@ constexpr int PAIR_TILE = 2048;
 __global__ void __launch_bounds__(256) pair_kernel(const float* z, int n, const int* ip, const int* in_,
                                                    const int* counts_loc, const float* zp, const float* zn,
                                                    const int* counts, float* part_g, float* part_l) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ float tile[PAIR_TILE];
   const int side = blockIdx.z;
   const int nloc = counts_loc[side];
@@ -120,6 +127,8 @@ __global__ void __launch_bounds__(256) pair_kernel(const float* z, int n, const 
 
 __global__ void pair_finalize_kernel(const float* y, int n, const int* counts, const float* part_g,
                                      const float* part_l, int S, float* dz, float* lsample) {
+  pdl_trigger();
+  pdl_wait();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const int np = counts[0], nn = counts[1];
@@ -135,6 +144,8 @@ __global__ void pair_finalize_kernel(const float* y, int n, const int* counts, c
 
 // Fixed-order single-block sum (deterministic).
 __global__ void __launch_bounds__(1024) sum_kernel(const float* v, int n, float* out) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ float sh[1024];
   float a = 0.f;
   for (int i = threadIdx.x; i < n; i += 1024) a += v[i];
@@ -158,6 +169,8 @@ __global__ void __launch_bounds__(256) full_loss_kernel(LossArgs a, const float*
                                                         const float* label, const float* dz_pair, const float* aux_out,
                                                         const float* aux_label, float* losses, float* dz_ctx,
                                                         float* dz_aux) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ float red[9][8];
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   float lt[9];
@@ -199,6 +212,8 @@ __global__ void __launch_bounds__(256) full_loss_kernel(LossArgs a, const float*
 }
 
 __global__ void loss_total_kernel(LossArgs a, const float* pair_share, float* losses) {
+  pdl_trigger();
+  pdl_wait();
   const float lp = pair_share ? *pair_share : 0.f;
   losses[a.J + 1] = lp;
   float t = a.lambda_ctx * losses[0] + a.lambda_pair * lp;
@@ -211,6 +226,8 @@ __global__ void loss_total_kernel(LossArgs a, const float* pair_share, float* lo
 __global__ void __launch_bounds__(256) head_dhid_full_kernel(const __nv_bfloat16* pre, const float* dz, const float* w2,
                                                              int n, int K, int dh, __nv_bfloat16* dhid,
                                                              __nv_bfloat16* dhid_lo, float* db1, float* dw2) {
+  pdl_trigger();
+  pdl_wait();
   const int N = K * dh;
   const int c0 = (blockIdx.x * 32 + threadIdx.x) * 8;
   float s1[8], s2[8];
@@ -266,6 +283,8 @@ __global__ void __launch_bounds__(256) head_dhid_full_kernel(const __nv_bfloat16
 
 // db2[k] = sum_i dz[i, k] (one block per tower, fixed order).
 __global__ void __launch_bounds__(1024) dz_colsum_kernel(const float* dz, int n, int K, float* db2) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ float sh[1024];
   const int k = blockIdx.x;
   float a = 0.f;
@@ -301,10 +320,10 @@ cudaError_t head_dhid_full_launch(const void* pre, const float* dz, const float*
   if (n > 0) {
     dim3 blk(32, 8);
     dim3 grd((K * dh + 255) / 256, (unsigned)min(128, (n + 7) / 8));
-    head_dhid_full_kernel<<<grd, blk, 0, st>>>(reinterpret_cast<const __nv_bfloat16*>(pre), dz, w2, n, K, dh,
+    launch_pdl(head_dhid_full_kernel, dim3(grd), dim3(blk), 0, st, reinterpret_cast<const __nv_bfloat16*>(pre), dz, w2, n, K, dh,
                                                reinterpret_cast<__nv_bfloat16*>(dhid),
                                                reinterpret_cast<__nv_bfloat16*>(dhid_lo), db1, dw2);
-    dz_colsum_kernel<<<K, 1024, 0, st>>>(dz, n, K, db2);
+    launch_pdl(dz_colsum_kernel, dim3(K), dim3(1024), 0, st, dz, n, K, db2);
   }
   return cudaGetLastError();
 }
@@ -339,7 +358,7 @@ cadet_status cadet_routed_logits(const float* logits, int32_t K, const int32_t* 
   }
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   ProfScope ps(PROF_OTHER, st, 1);
-  if (n > 0) routed_logits_kernel<<<blocks(n, 256), 256, 0, st>>>(logits, K, bucket, n, z_out);
+  if (n > 0) launch_pdl(routed_logits_kernel, dim3(blocks(n, 256)), dim3(256), 0, st, logits, K, bucket, n, z_out);
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     set_error(cudaGetErrorString(e));
@@ -382,13 +401,14 @@ cadet_status cadet_pairwise_loss(const float* z, const float* label, int32_t n, 
   int* counts_loc = in_ + a256((size_t)n * 4) / 4;
   cudaError_t e = cudaMemsetAsync(loss_share, 0, 4, st);
   if (n_all > 0 && e == cudaSuccess) {
-    compact_kernel<<<1, 1024, 0, st>>>(z_all, label_all, n_all, zp, zn, counts);
+    launch_pdl(compact_kernel, dim3(1), dim3(1024), 0, st, z_all, label_all, n_all, zp, zn, counts, (int*)nullptr,
+               (int*)nullptr);
     if (n > 0) {
-      compact_kernel<<<1, 1024, 0, st>>>(z, label, n, nullptr, nullptr, counts_loc, ip, in_);
-      pair_kernel<<<dim3(blocks(n, 256), S, 2), 256, 0, st>>>(z, n, ip, in_, counts_loc, zp, zn, counts, part_g,
+      launch_pdl(compact_kernel, dim3(1), dim3(1024), 0, st, z, label, n, nullptr, nullptr, counts_loc, ip, in_);
+      launch_pdl(pair_kernel, dim3(dim3(blocks(n, 256), S, 2)), dim3(256), 0, st, z, n, ip, in_, counts_loc, zp, zn, counts, part_g,
                                                              part_l);
-      pair_finalize_kernel<<<blocks(n, 256), 256, 0, st>>>(label, n, counts, part_g, part_l, S, dz_pair, lsample);
-      sum_kernel<<<1, 1024, 0, st>>>(lsample, n, loss_share);
+      launch_pdl(pair_finalize_kernel, dim3(blocks(n, 256)), dim3(256), 0, st, label, n, counts, part_g, part_l, S, dz_pair, lsample);
+      launch_pdl(sum_kernel, dim3(1), dim3(1024), 0, st, lsample, n, loss_share);
     }
     e = cudaGetLastError();
   }
@@ -423,9 +443,9 @@ cadet_status cadet_full_loss_grads(const cadet_loss_config* lc, const float* log
   ProfScope ps(PROF_OTHER, st, 2);
   cudaError_t e = cudaMemsetAsync(losses, 0, sizeof(float) * (lc->J + 3), st);
   if (e == cudaSuccess && n > 0)
-    full_loss_kernel<<<blocks(n, 256), 256, 0, st>>>(a, logits, bucket, label, dz_pair, aux_out, aux_label, losses,
+    launch_pdl(full_loss_kernel, dim3(blocks(n, 256)), dim3(256), 0, st, a, logits, bucket, label, dz_pair, aux_out, aux_label, losses,
                                                      dz_ctx, dz_aux);
-  if (e == cudaSuccess) loss_total_kernel<<<1, 1, 0, st>>>(a, pair_share, losses);
+  if (e == cudaSuccess) launch_pdl(loss_total_kernel, dim3(1), dim3(1), 0, st, a, pair_share, losses);
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) {
     set_error(cudaGetErrorString(e));

@@ -8,12 +8,15 @@
 //   head_init / head_dz / head_dhid   A7/A8 routed BCE (Eq. 9) and the tower backward
 //   add_kernel              Y = O (+ resid) when the output projection is ablated
 #include "misc.cuh"
+#include "launch.cuh"
 #include "prof.cuh"
 #include "ptx.cuh"
 
 namespace cadet {
 
 __global__ void rope_theta_kernel(double* theta, int half, int hd, double phi_min, double base, double dt_max) {
+  pdl_trigger();
+  pdl_wait();
   const int i = threadIdx.x + blockIdx.x * blockDim.x;
   if (i < half) theta[i] = (phi_min / dt_max) * pow(base, 2.0 * i / (double)hd);
 }
@@ -33,10 +36,13 @@ __device__ __forceinline__ void rope_cs(double dt, double th, float& c, float& s
 // is contiguous (a GEMM epilogue slice may cross one head edge when hd % 32 != 0).
 __global__ void rope_table_kernel(float* cs, int T, int hd, const double* theta, const int64_t* t,
                                   const int32_t* row_seq, const int32_t* cu) {
+  pdl_trigger();
+  pdl_wait();
+  // one thread per (row, entry); T * (hd / 2 + 16) < 2^31 (host-checked), so 32-bit index math
   const int half = hd / 2, w = half + 16;
-  const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= (size_t)T * w) return;
-  const int row = (int)(idx / w), i = (int)(idx % w);
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= T * w) return;
+  const int row = idx / w, i = idx - row * w;
   const int pr = i < half ? i : i - half;
   const int s = row_seq[row];
   const double dt = s >= 0 ? (double)(t[row] - t[cu[s]]) : 0.0;
@@ -48,6 +54,8 @@ __global__ void rope_table_kernel(float* cs, int T, int hd, const double* theta,
 // one thread per (row, pair of columns)
 __global__ void rope_apply_kernel(const __nv_bfloat16* in, __nv_bfloat16* out, int T, int d, int hd,
                                   const float* cs) {
+  pdl_trigger();
+  pdl_wait();
   const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   const size_t pairs = (size_t)T * d / 2;
   if (idx >= pairs) return;
@@ -66,6 +74,8 @@ __global__ void __launch_bounds__(256) rope_gate_bwd_kernel(const void* dr, int 
                                                             const __nv_bfloat16* Z, __nv_bfloat16* out_u,
                                                             void* out_r, int r_bf16, int T, int d, int hd,
                                                             const float* cs) {
+  pdl_trigger();
+  pdl_wait();
   const int per_row = d / 8;
   const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= (size_t)T * per_row) return;
@@ -137,6 +147,8 @@ __global__ void __launch_bounds__(256) rope_gate_bwd_kernel(const void* dr, int 
 
 __global__ void gather_rows_kernel(const uint8_t* H, const int32_t* rows, int n, int T, int row_bytes, uint8_t* out,
                                    uint32_t* err) {
+  pdl_trigger();
+  pdl_wait();
   const int r = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (r >= n) return;
@@ -151,6 +163,8 @@ __global__ void gather_rows_kernel(const uint8_t* H, const int32_t* rows, int n,
 }
 
 __global__ void head_init_kernel(float* logits, const float* b2, int n, int K) {
+  pdl_trigger();
+  pdl_wait();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n * K) logits[i] = b2[i % K];
 }
@@ -158,6 +172,8 @@ __global__ void head_init_kernel(float* logits, const float* b2, int n, int K) {
 // Routed BCE (Eq. 9): loss = sum softplus(z_k) - y z_k; dz = sigma(z_k) - y on the realised tower.
 __global__ void head_dz_kernel(const float* logits, const int32_t* bucket, const float* label, int n, int K,
                                float* dz, float* loss_sum, float* db2, uint32_t* err) {
+  pdl_trigger();
+  pdl_wait();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   float l = 0.f, g = 0.f;
   int k = 0;
@@ -190,6 +206,8 @@ __global__ void head_dz_kernel(const float* logits, const int32_t* bucket, const
 __global__ void __launch_bounds__(256) head_dhid_kernel(const __nv_bfloat16* pre, const float* dz, const int32_t* bucket,
                                                         const float* w2, int n, int K, int dh, __nv_bfloat16* dhid,
                                                         __nv_bfloat16* dhid_lo, float* db1, float* dw2) {
+  pdl_trigger();
+  pdl_wait();
   const int N = K * dh;
   const int c0 = (blockIdx.x * 32 + threadIdx.x) * 8;
   float s1[8], s2[8];
@@ -249,6 +267,8 @@ __global__ void __launch_bounds__(256) head_dhid_kernel(const __nv_bfloat16* pre
 }
 
 __global__ void add_bf16_kernel(const __nv_bfloat16* a, const __nv_bfloat16* b, __nv_bfloat16* out, size_t n2) {
+  pdl_trigger();
+  pdl_wait();
   const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n2) return;
   float2 x = __bfloat1622float2(reinterpret_cast<const __nv_bfloat162*>(a)[i]);
@@ -265,21 +285,22 @@ static inline unsigned blocks(size_t n, unsigned b) { return (unsigned)((n + b -
 
 cudaError_t rope_theta_launch(double* theta, int hd, double phi_min, double base, double dt_max, cudaStream_t st) {
   ProfScope ps(PROF_OTHER, st, 1);
-  rope_theta_kernel<<<1, 128, 0, st>>>(theta, hd / 2, hd, phi_min, base, dt_max);
+  launch_pdl(rope_theta_kernel, dim3(1), dim3(128), 0, st, theta, hd / 2, hd, phi_min, base, dt_max);
   return cudaGetLastError();
 }
 cudaError_t rope_table_launch(float* cs, int T, int hd, const double* theta, const int64_t* t, const int32_t* row_seq,
                               const int32_t* cu, cudaStream_t st) {
   ProfScope ps(PROF_OTHER, st, 1);
   const size_t work = (size_t)T * (hd / 2 + 16);
-  if (work) rope_table_kernel<<<blocks(work, 256), 256, 0, st>>>(cs, T, hd, theta, t, row_seq, cu);
+  if (work >= (size_t)INT32_MAX) return cudaErrorInvalidValue;
+  if (work) launch_pdl(rope_table_kernel, dim3(blocks(work, 256)), dim3(256), 0, st, cs, T, hd, theta, t, row_seq, cu);
   return cudaGetLastError();
 }
 cudaError_t rope_apply_launch(const void* in, void* out, int T, int d, int hd, const float* cs, cudaStream_t st) {
   ProfScope ps(PROF_OTHER, st, 1);
   const size_t pairs = (size_t)T * d / 2;
   if (pairs)
-    rope_apply_kernel<<<blocks(pairs, 256), 256, 0, st>>>(reinterpret_cast<const __nv_bfloat16*>(in),
+    launch_pdl(rope_apply_kernel, dim3(blocks(pairs, 256)), dim3(256), 0, st, reinterpret_cast<const __nv_bfloat16*>(in),
                                                          reinterpret_cast<__nv_bfloat16*>(out), T, d, hd, cs);
   return cudaGetLastError();
 }
@@ -288,8 +309,7 @@ cudaError_t rope_gate_bwd_launch(const void* dr, int dr_f32, const void* Xq, con
   ProfScope ps(PROF_OTHER, st, 1);
   const size_t work = (size_t)T * d / 8;
   if (work)
-    rope_gate_bwd_kernel<<<blocks(work, 256), 256, 0, st>>>(
-        dr, dr_f32, reinterpret_cast<const __nv_bfloat16*>(Xq), reinterpret_cast<const __nv_bfloat16*>(Z),
+    launch_pdl(rope_gate_bwd_kernel, dim3(blocks(work, 256)), dim3(256), 0, st, dr, dr_f32, reinterpret_cast<const __nv_bfloat16*>(Xq), reinterpret_cast<const __nv_bfloat16*>(Z),
         reinterpret_cast<__nv_bfloat16*>(out_u), out_r, r_bf16, T, d, hd, cs);
   return cudaGetLastError();
 }
@@ -297,19 +317,19 @@ cudaError_t gather_rows_launch(const void* H, const int32_t* rows, int n, int T,
                                cudaStream_t st) {
   ProfScope ps(PROF_OTHER, st, 1);
   if (n > 0)
-    gather_rows_kernel<<<blocks(n, 8), 256, 0, st>>>(reinterpret_cast<const uint8_t*>(H), rows, n, T, d * 2,
+    launch_pdl(gather_rows_kernel, dim3(blocks(n, 8)), dim3(256), 0, st, reinterpret_cast<const uint8_t*>(H), rows, n, T, d * 2,
                                                      reinterpret_cast<uint8_t*>(out), err);
   return cudaGetLastError();
 }
 cudaError_t head_init_launch(float* logits, const float* b2, int n, int K, cudaStream_t st) {
   ProfScope ps(PROF_OTHER, st, 1);
-  if (n > 0) head_init_kernel<<<blocks((size_t)n * K, 256), 256, 0, st>>>(logits, b2, n, K);
+  if (n > 0) launch_pdl(head_init_kernel, dim3(blocks((size_t)n * K, 256)), dim3(256), 0, st, logits, b2, n, K);
   return cudaGetLastError();
 }
 cudaError_t head_dz_launch(const float* logits, const int32_t* bucket, const float* label, int n, int K, float* dz,
                            float* loss_sum, float* db2, uint32_t* err, cudaStream_t st) {
   ProfScope ps(PROF_OTHER, st, 1);
-  if (n > 0) head_dz_kernel<<<blocks(n, 256), 256, 0, st>>>(logits, bucket, label, n, K, dz, loss_sum, db2, err);
+  if (n > 0) launch_pdl(head_dz_kernel, dim3(blocks(n, 256)), dim3(256), 0, st, logits, bucket, label, n, K, dz, loss_sum, db2, err);
   return cudaGetLastError();
 }
 cudaError_t head_dhid_launch(const void* pre, const float* dz, const int32_t* bucket, const float* w2, int n, int K,
@@ -318,7 +338,7 @@ cudaError_t head_dhid_launch(const void* pre, const float* dz, const int32_t* bu
   if (n > 0) {
     dim3 blk(32, 8);
     dim3 grd((K * dh + 255) / 256, (unsigned)min(128, (n + 7) / 8));
-    head_dhid_kernel<<<grd, blk, 0, st>>>(reinterpret_cast<const __nv_bfloat16*>(pre), dz, bucket, w2, n, K, dh,
+    launch_pdl(head_dhid_kernel, dim3(grd), dim3(blk), 0, st, reinterpret_cast<const __nv_bfloat16*>(pre), dz, bucket, w2, n, K, dh,
                                           reinterpret_cast<__nv_bfloat16*>(dhid),
                                           reinterpret_cast<__nv_bfloat16*>(dhid_lo), db1, dw2);
   }
@@ -327,7 +347,7 @@ cudaError_t head_dhid_launch(const void* pre, const float* dz, const int32_t* bu
 cudaError_t add_bf16_launch(const void* a, const void* b, void* out, size_t n, cudaStream_t st) {
   ProfScope ps(PROF_OTHER, st, 1);
   if (n)
-    add_bf16_kernel<<<blocks(n / 2, 256), 256, 0, st>>>(reinterpret_cast<const __nv_bfloat16*>(a),
+    launch_pdl(add_bf16_kernel, dim3(blocks(n / 2, 256)), dim3(256), 0, st, reinterpret_cast<const __nv_bfloat16*>(a),
                                                          reinterpret_cast<const __nv_bfloat16*>(b),
                                                          reinterpret_cast<__nv_bfloat16*>(out), n / 2);
   return cudaGetLastError();

@@ -4,6 +4,7 @@
 //   widen_kernel     bf16 -> fp32 (the fp32-consumed parameters, e.g. biases, after the all-gather)
 // Both are HBM-bound elementwise passes: 16-byte vector accesses, grid-stride over 4 x SMs blocks.
 #include "../../include/cadet.h"
+#include "launch.cuh"
 #include "prof.cuh"
 #include "ptx.cuh"
 
@@ -26,6 +27,8 @@ __device__ __forceinline__ float adam_one(float& p, float& m, float& v, float g,
 __global__ void __launch_bounds__(256) adamw_kernel(const float* __restrict__ g, float* __restrict__ p,
                                                     float* __restrict__ m, float* __restrict__ v,
                                                     __nv_bfloat16* __restrict__ pbf, int64_t n, AdamArgs a) {
+  pdl_trigger();
+  pdl_wait();
   const int64_t n4 = n >> 2;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride) {
@@ -54,6 +57,8 @@ __global__ void __launch_bounds__(256) adamw_kernel(const float* __restrict__ g,
 
 __global__ void __launch_bounds__(256) widen_kernel(const __nv_bfloat16* __restrict__ src, float* __restrict__ dst,
                                                     int64_t n) {
+  pdl_trigger();
+  pdl_wait();
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const int64_t n8 = n >> 3;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n8; i += stride) {
@@ -125,7 +130,7 @@ cadet_status cadet_adamw_step(const cadet_adamw_config* c, int64_t step, const f
   a.inv_bc2 = (float)(1.0 / (1.0 - pow((double)c->beta2, (double)step)));
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   ProfScope ps(PROF_OTHER, st, 1);
-  adamw_kernel<<<grid_for(n / 4 + 1), 256, 0, st>>>(grad, param, m, v, reinterpret_cast<__nv_bfloat16*>(param_bf16),
+  launch_pdl(adamw_kernel, dim3(grid_for(n / 4 + 1)), dim3(256), 0, st, grad, param, m, v, reinterpret_cast<__nv_bfloat16*>(param_bf16),
                                                     n, a);
   return launch_err("adamw_step");
 }
@@ -139,7 +144,7 @@ cadet_status cadet_bf16_to_f32(const void* src, float* dst, int64_t n, cadet_str
   if (n == 0) return CADET_OK;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   ProfScope ps(PROF_OTHER, st, 1);
-  widen_kernel<<<grid_for(n / 8 + 1), 256, 0, st>>>(reinterpret_cast<const __nv_bfloat16*>(src), dst, n);
+  launch_pdl(widen_kernel, dim3(grid_for(n / 8 + 1)), dim3(256), 0, st, reinterpret_cast<const __nv_bfloat16*>(src), dst, n);
   return launch_err("bf16_to_f32");
 }
 

@@ -8,6 +8,7 @@
 // on PARTIAL rows only.  This is exactly the structure of the mask of PAPER.md Eq. 6 / Fig. 3 /
 // P:540-546 when timestamps (and session ids) are non-decreasing inside a sequence.
 #include "plan.cuh"
+#include "launch.cuh"
 #include "prof.cuh"
 #include "ptx.cuh"
 
@@ -96,6 +97,8 @@ __device__ __forceinline__ int32_t seq_len_safe(const int32_t* cu, int s, int T)
 
 // ---------------------------------------------------------------- K1
 __global__ void __launch_bounds__(1024) plan_seq_kernel(PlanArgs a, PlanView v) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ long long sh[1024];
   const int tid = threadIdx.x, nt = blockDim.x;
   const int per = (a.n + nt - 1) / nt;
@@ -166,6 +169,8 @@ __device__ __forceinline__ int lower_bound_i32(const int32_t* x, int lo, int hi,
 }
 
 __global__ void __launch_bounds__(256) plan_row_kernel(PlanArgs a, PlanView v) {
+  pdl_trigger();
+  pdl_wait();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   unsigned long long cnt = 0;
   uint32_t err = 0;
@@ -234,6 +239,8 @@ __device__ __forceinline__ int tile_seq(const PlanView& v, int n, int g) {
 }
 
 __global__ void __launch_bounds__(128) plan_tile_kernel(PlanArgs a, PlanView v) {
+  pdl_trigger();
+  pdl_wait();
   const int g = blockIdx.x * blockDim.x + threadIdx.x;
   const int nq_total = v.counters[0];
   if (g >= nq_total) return;
@@ -270,6 +277,8 @@ __global__ void __launch_bounds__(128) plan_tile_kernel(PlanArgs a, PlanView v) 
 // ---------------------------------------------------------------- K4 / K5
 // Exclusive scan of the cost histograms in DESCENDING cost order (LPT: most expensive first).
 __global__ void __launch_bounds__(1024) plan_order_kernel(PlanView v) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ long long sh[1024];
   const int tid = threadIdx.x, nt = blockDim.x;
   for (int which = 0; which < 2; ++which) {
@@ -293,6 +302,8 @@ __global__ void __launch_bounds__(1024) plan_order_kernel(PlanView v) {
 }
 
 __global__ void __launch_bounds__(128) plan_scatter_kernel(PlanArgs a, PlanView v) {
+  pdl_trigger();
+  pdl_wait();
   const int g = blockIdx.x * blockDim.x + threadIdx.x;
   const int nq_total = v.counters[0];
   if (g >= nq_total) return;
@@ -323,19 +334,21 @@ __global__ void __launch_bounds__(128) plan_scatter_kernel(PlanArgs a, PlanView 
 
 cudaError_t plan_launch(const PlanArgs& a, const PlanView& v, cudaStream_t st) {
   ProfScope ps(PROF_OTHER, st, 5);
-  plan_seq_kernel<<<1, 1024, 0, st>>>(a, v);
-  if (a.T > 0) plan_row_kernel<<<(a.T + 255) / 256, 256, 0, st>>>(a, v);
+  launch_pdl(plan_seq_kernel, dim3(1), dim3(1024), 0, st, a, v);
+  if (a.T > 0) launch_pdl(plan_row_kernel, dim3((a.T + 255) / 256), dim3(256), 0, st, a, v);
   const int nb = (v.nq_cap + 127) / 128;
   if (nb > 0) {
-    plan_tile_kernel<<<nb, 128, 0, st>>>(a, v);
-    plan_order_kernel<<<1, 1024, 0, st>>>(v);
-    plan_scatter_kernel<<<nb, 128, 0, st>>>(a, v);
+    launch_pdl(plan_tile_kernel, dim3(nb), dim3(128), 0, st, a, v);
+    launch_pdl(plan_order_kernel, dim3(1), dim3(1024), 0, st, v);
+    launch_pdl(plan_scatter_kernel, dim3(nb), dim3(128), 0, st, a, v);
   }
   return cudaGetLastError();
 }
 
 // ---------------------------------------------------------------- export (test hook)
 __global__ void __launch_bounds__(128) plan_export_kernel(PlanArgs a, PlanView v, int8_t* tc_out, int64_t tc_cap) {
+  pdl_trigger();
+  pdl_wait();
   const int g = blockIdx.x;
   const int nq_total = v.counters[0];
   if (g >= nq_total) return;
@@ -364,6 +377,8 @@ __global__ void __launch_bounds__(128) plan_export_kernel(PlanArgs a, PlanView v
 
 __global__ void copy_kv_end_kernel(const int32_t* src, int32_t* dst, int T, const unsigned long long* pairs,
                                    int64_t* pairs_out) {
+  pdl_trigger();
+  pdl_wait();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < T) dst[i] = src[i];
   if (i == 0 && pairs_out) *pairs_out = (int64_t)*pairs;
@@ -373,15 +388,17 @@ cudaError_t plan_export_launch(const PlanArgs& a, const PlanView& v, int32_t* kv
                                int64_t tc_cap, int64_t* pairs_out, cudaStream_t st) {
   ProfScope ps(PROF_OTHER, st, 2);
   if (kv_end_out || pairs_out)
-    copy_kv_end_kernel<<<(a.T + 255) / 256 + 1, 256, 0, st>>>(v.kv_end, kv_end_out ? kv_end_out : v.kv_end,
+    launch_pdl(copy_kv_end_kernel, dim3((a.T + 255) / 256 + 1), dim3(256), 0, st, v.kv_end, kv_end_out ? kv_end_out : v.kv_end,
                                                               kv_end_out ? a.T : 0, v.pairs, pairs_out);
-  if (tc_out && v.nq_cap > 0) plan_export_kernel<<<v.nq_cap, 128, 0, st>>>(a, v, tc_out, tc_cap);
+  if (tc_out && v.nq_cap > 0) launch_pdl(plan_export_kernel, dim3(v.nq_cap), dim3(128), 0, st, a, v, tc_out, tc_cap);
   return cudaGetLastError();
 }
 
 // ---------------------------------------------------------------- A0 chunk
 __global__ void __launch_bounds__(1024) chunk_kernel(const int32_t* cu_in, int n, int L, int32_t* cu_out, int cap,
                                                       int32_t* n_out, uint32_t* err) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ long long sh[1024];
   const int tid = threadIdx.x, nt = blockDim.x;
   const int per = (n + nt - 1) / nt;
@@ -420,13 +437,15 @@ __global__ void __launch_bounds__(1024) chunk_kernel(const int32_t* cu_in, int n
 cudaError_t chunk_launch(const int32_t* cu_in, int32_t n_in, int32_t L, int32_t* cu_out, int32_t cap, int32_t* n_out,
                          uint32_t* err, cudaStream_t st) {
   ProfScope ps(PROF_OTHER, st, 1);
-  chunk_kernel<<<1, 1024, 0, st>>>(cu_in, n_in, L, cu_out, cap, n_out, err);
+  launch_pdl(chunk_kernel, dim3(1), dim3(1024), 0, st, cu_in, n_in, L, cu_out, cap, n_out, err);
   return cudaGetLastError();
 }
 
 // ---------------------------------------------------------------- A13 pack
 __global__ void __launch_bounds__(1024) pack_offsets_kernel(const int32_t* lens, int B, int budget, int32_t* cu_out,
                                                              int32_t* n_packed, uint32_t* err) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ long long sh[1024];
   const int tid = threadIdx.x, nt = blockDim.x;
   const int per = (B + nt - 1) / nt;
@@ -473,6 +492,8 @@ __global__ void __launch_bounds__(256) pack_rows_kernel(const uint8_t* src, cons
                                                          const int32_t* n_packed, int row_bytes, int budget, const int64_t* tp,
                                                          const int32_t* sp, uint8_t* packed, int64_t* t_out,
                                                          int32_t* s_out) {
+  pdl_trigger();
+  pdl_wait();
   const int warps = blockDim.x / 32;
   const int r = blockIdx.x * warps + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
@@ -511,16 +532,17 @@ cudaError_t pack_launch(const void* src, const int64_t* src_row, const int32_t* 
                         int32_t budget, const int64_t* tp, const int32_t* sp, void* packed, int64_t* t_out,
                         int32_t* s_out, int32_t* cu_out, int32_t* n_packed, uint32_t* err, cudaStream_t st) {
   ProfScope ps(PROF_OTHER, st, 2);
-  pack_offsets_kernel<<<1, 1024, 0, st>>>(lens, B, budget, cu_out, n_packed, err);
+  launch_pdl(pack_offsets_kernel, dim3(1), dim3(1024), 0, st, lens, B, budget, cu_out, n_packed, err);
   const int rows_per_block = 8;
-  pack_rows_kernel<<<(budget + rows_per_block - 1) / rows_per_block, 256, 0, st>>>(
-      reinterpret_cast<const uint8_t*>(src), src_row, cu_out, n_packed, d * 2, budget, tp, sp,
+  launch_pdl(pack_rows_kernel, dim3((budget + rows_per_block - 1) / rows_per_block), dim3(256), 0, st, reinterpret_cast<const uint8_t*>(src), src_row, cu_out, n_packed, d * 2, budget, tp, sp,
       reinterpret_cast<uint8_t*>(packed), t_out, s_out);
   return cudaGetLastError();
 }
 
 // ---------------------------------------------------------------- zero pad rows [cu[n], T)
 __global__ void zero_pad_rows_kernel(uint8_t* buf, int row_bytes, int T, const int32_t* cu, int n) {
+  pdl_trigger();
+  pdl_wait();
   const int nreal = n > 0 ? min(max(cu[n], 0), T) : 0;
   const size_t begin = (size_t)nreal * row_bytes, end = (size_t)T * row_bytes;
   for (size_t i = begin + ((size_t)blockIdx.x * blockDim.x + threadIdx.x) * 16; i < end;
@@ -531,7 +553,7 @@ __global__ void zero_pad_rows_kernel(uint8_t* buf, int row_bytes, int T, const i
 cudaError_t zero_pad_rows_launch(void* buf, int32_t row_bytes, int32_t T, const int32_t* cu, int32_t n,
                                  cudaStream_t st) {
   ProfScope ps(PROF_OTHER, st, 1);
-  zero_pad_rows_kernel<<<148, 256, 0, st>>>(reinterpret_cast<uint8_t*>(buf), row_bytes, T, cu, n);
+  launch_pdl(zero_pad_rows_kernel, dim3(148), dim3(256), 0, st, reinterpret_cast<uint8_t*>(buf), row_bytes, T, cu, n);
   return cudaGetLastError();
 }
 

@@ -427,4 +427,86 @@ CADET_DEV float rcp_ftz(float x) {
 }
 CADET_DEV float sigmoid_fast(float z) { return rcp_ftz(1.0f + ex2_ftz(-1.4426950408889634f * z)); }
 
+// Warp-cooperative variants: the 32 lanes hold rows row0 .. row0 + 31 of the same 32 columns
+// (tcgen05.ld 32x32b layout).  Global traffic goes through a per-warp 4 KB swizzled transpose
+// (ptx.cuh) so each load / store instruction covers whole row segments instead of 32 lines.
+// bf16 32 x 32 slice in two phases, so the global loads of a later slice can be issued early:
+// (1) coalesced loads (8 rows x 64 B per instruction) into registers, (2) transpose to this lane's row.
+CADET_DEV void warp_ldg_rows_bf16(const void* base, size_t off0, size_t ld, int rows_valid,
+                                                   uint4 (&g)[4]) {
+  const uint32_t lane = threadIdx.x & 31;
+  const __nv_bfloat16* b = reinterpret_cast<const __nv_bfloat16*>(base) + off0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int row = i * 8 + (lane >> 2), j = lane & 3;
+    g[i] = row < rows_valid ? *reinterpret_cast<const uint4*>(b + (size_t)row * ld + j * 8) : make_uint4(0, 0, 0, 0);
+  }
+}
+CADET_DEV void warp_sts_rows_bf16(uint32_t stg, const uint4 (&g)[4], float (&x)[32]) {
+  const uint32_t lane = threadIdx.x & 31;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int row = i * 8 + (lane >> 2), j = lane & 3;
+    sts_u4(stg + row * 64 + ((j ^ ((row >> 1) & 3)) << 4), g[i].x, g[i].y, g[i].z, g[i].w);
+  }
+  __syncwarp();
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const uint4 u = lds_u4(stg + lane * 64 + ((j ^ ((lane >> 1) & 3)) << 4));
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float2 f = __bfloat1622float2(h[e]);
+      x[j * 8 + e * 2] = f.x;
+      x[j * 8 + e * 2 + 1] = f.y;
+    }
+  }
+  __syncwarp();
+}
+
+// fp32 32 x 32 slice in the same two phases (4 rows x 128 B per load instruction).
+CADET_DEV void warp_ldg_rows_f32(const void* base, size_t off0, size_t ld, int rows_valid,
+                                                  uint4 (&g)[8]) {
+  const uint32_t lane = threadIdx.x & 31;
+  const float* b = reinterpret_cast<const float*>(base) + off0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int row = i * 4 + (lane >> 3), j = lane & 7;
+    g[i] = row < rows_valid ? *reinterpret_cast<const uint4*>(b + (size_t)row * ld + j * 4) : make_uint4(0, 0, 0, 0);
+  }
+}
+CADET_DEV void warp_sts_rows_f32(uint32_t stg, const uint4 (&g)[8], float (&x)[32]) {
+  const uint32_t lane = threadIdx.x & 31;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int row = i * 4 + (lane >> 3), j = lane & 7;
+    sts_u4(stg + row * 128 + ((j ^ (row & 7)) << 4), g[i].x, g[i].y, g[i].z, g[i].w);
+  }
+  __syncwarp();
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const uint4 u = lds_u4(stg + lane * 128 + ((j ^ (lane & 7)) << 4));
+    x[j * 4] = __uint_as_float(u.x);
+    x[j * 4 + 1] = __uint_as_float(u.y);
+    x[j * 4 + 2] = __uint_as_float(u.z);
+    x[j * 4 + 3] = __uint_as_float(u.w);
+  }
+  __syncwarp();
+}
+
+CADET_DEV void warp_load_rows(uint32_t stg, const void* base, int is_f32, size_t off0, size_t ld,
+                                               int rows_valid, float (&x)[32]) {
+  const uint32_t lane = threadIdx.x & 31;
+  if (!is_f32) {
+    uint4 g[4];
+    warp_ldg_rows_bf16(base, off0, ld, rows_valid, g);
+    warp_sts_rows_bf16(stg, g, x);
+    return;
+  } else {
+    uint4 g[8];
+    warp_ldg_rows_f32(base, off0, ld, rows_valid, g);
+    warp_sts_rows_f32(stg, g, x);
+  }
+}
+
 }  // namespace cadet
