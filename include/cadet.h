@@ -329,6 +329,8 @@ cadet_status cadet_chunk(const int32_t* cu_in, int32_t n_in, int32_t L_chunk, in
  * prefix sum of lens).  t_src (nullable) int64 and s_src (nullable) int32 are per src row and are
  * packed alongside into t_out / s_out ([budget]).
  * Outputs: packed [budget, d], cu_out [B+1] (entries past n_packed repeat the total), n_packed[0].
+ * src = packed = NULL packs only the offsets and t / s (one thread per row), and t_out = s_out =
+ * NULL only the rows, so the row move can run on another stream than the metadata the plan needs.
  * ws (>= cadet_pack_workspace_bytes) holds the error word read by cadet_poll. */
 cadet_status cadet_pack(const void* src, const int64_t* src_row, const int32_t* lens, int32_t B, int32_t d,
                         int32_t budget, const int64_t* t_src, const int32_t* s_src, void* packed, int64_t* t_out,

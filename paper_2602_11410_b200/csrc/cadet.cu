@@ -187,7 +187,7 @@ cadet_status cadet_pack(const void* src, const int64_t* src_row, const int32_t* 
                         int32_t budget, const int64_t* t_src, const int32_t* s_src, void* packed, int64_t* t_out,
                         int32_t* s_out, int32_t* cu_out, int32_t* n_packed, void* ws, size_t ws_bytes,
                         cadet_stream_t stream) {
-  if (!src || !lens || !packed || !cu_out || !n_packed || B < 0 || d <= 0 || budget <= 0 || !ws)
+  if (!lens || (!src != !packed) || !cu_out || !n_packed || B < 0 || d <= 0 || budget <= 0 || !ws)
     return fail(CADET_E_ARG, "cadet_pack args");
   if (d % 8) return fail(CADET_E_ARG, "d must be a multiple of 8");
   if (ws_bytes < 256) return fail(CADET_E_WORKSPACE, "pack workspace");

@@ -429,8 +429,11 @@ cadet_status cadet_attn_backward_ev(const cadet_attn_config* cfg, const cadet_ba
   cudaError_t e = cfg->plan_ready >= 2 ? cudaSuccess : rope_prepare(cfg, b, W, v, st);
   const float* cs = cfg->use_rope ? W.rope_cs : nullptr;
   float* gws[7] = {gr->dW_xg, gr->dW_q, gr->dW_k, gr->dW_v, gr->dW_qg, gr->dW_kg, gr->dW_o};
-  for (int i = 0; i < 7 && e == cudaSuccess; ++i)
-    if (gws[i]) e = cudaMemsetAsync(gws[i], 0, wbytes, st);
+  if (e == cudaSuccess) {  // the 7 weight gradients are split-K accumulated: zero them in one launch
+    ZeroSpan zs[7];
+    for (int i = 0; i < 7; ++i) zs[i] = ZeroSpan{gws[i], wbytes};
+    e = zero_many_launch(zs, 7, st);
+  }
   auto mark = [&](int i) {  // grad group i complete on `st` (SURVEY 8(e) overlap)
     if (e == cudaSuccess && grad_events && grad_events[i]) e = cudaEventRecord((cudaEvent_t)grad_events[i], st);
   };
@@ -633,11 +636,9 @@ cadet_status cadet_heads_backward(const cadet_head_config* h, const cadet_head_w
   void* Hr = p + 256;
   void* dhid_lo = p + 256 + a256((size_t)n * d * 2);
   void* dhid = p + 256 + a256((size_t)n * d * 2) + a256((size_t)n * N * 2);
-  cudaError_t e = cudaMemsetAsync(gr->dW1, 0, (size_t)d * N * 4, st);
-  if (e == cudaSuccess) e = cudaMemsetAsync(gr->db1, 0, (size_t)N * 4, st);
-  if (e == cudaSuccess) e = cudaMemsetAsync(gr->dw2, 0, (size_t)N * 4, st);
-  if (e == cudaSuccess) e = cudaMemsetAsync(gr->db2, 0, (size_t)h->K * 4, st);
-  if (e == cudaSuccess && !accumulate) e = cudaMemsetAsync(dHs, 0, (size_t)T * d * 2, st);
+  const ZeroSpan zs[5] = {{gr->dW1, (size_t)d * N * 4}, {gr->db1, (size_t)N * 4}, {gr->dw2, (size_t)N * 4},
+                          {gr->db2, (size_t)h->K * 4}, {accumulate ? nullptr : dHs, (size_t)T * d * 2}};
+  cudaError_t e = zero_many_launch(zs, 5, st);
   if (n == 0) return cuda_err(e, "heads backward");
   if (e == cudaSuccess)
     e = head_dhid_full_launch(pre, dz, w->w2, n, h->K, h->d_hidden, dhid, dhid_lo, gr->db1, gr->dw2, gr->db2, st);
@@ -692,12 +693,9 @@ cadet_status cadet_heads_loss_backward(const cadet_head_config* h, const cadet_h
   void* dhid_lo = p + 256 + a256((size_t)n * d * 2);  // the forward's `pre` slot (pre is caller-owned here)
   void* dhid = p + 256 + a256((size_t)n * d * 2) + a256((size_t)n * N * 2);
   float* dz = reinterpret_cast<float*>(p + 256 + a256((size_t)n * d * 2) + 2 * a256((size_t)n * N * 2));
-  cudaError_t e = cudaMemsetAsync(loss_sum, 0, 4, st);
-  if (e == cudaSuccess) e = cudaMemsetAsync(gr->dW1, 0, (size_t)d * N * 4, st);
-  if (e == cudaSuccess) e = cudaMemsetAsync(gr->db1, 0, (size_t)N * 4, st);
-  if (e == cudaSuccess) e = cudaMemsetAsync(gr->dw2, 0, (size_t)N * 4, st);
-  if (e == cudaSuccess) e = cudaMemsetAsync(gr->db2, 0, (size_t)h->K * 4, st);
-  if (e == cudaSuccess) e = cudaMemsetAsync(dHs, 0, (size_t)T * d * 2, st);
+  const ZeroSpan zs[6] = {{loss_sum, 4},          {gr->dW1, (size_t)d * N * 4}, {gr->db1, (size_t)N * 4},
+                          {gr->dw2, (size_t)N * 4}, {gr->db2, (size_t)h->K * 4}, {dHs, (size_t)T * d * 2}};
+  cudaError_t e = zero_many_launch(zs, 6, st);
   if (n == 0) return cuda_err(e, "heads backward");
   if (e == cudaSuccess) e = head_dz_launch(logits, bucket, label, n, h->K, dz, loss_sum, gr->db2, err, st);
   if (e == cudaSuccess) e = head_dhid_launch(pre, dz, bucket, w->w2, n, h->K, h->d_hidden, dhid, dhid_lo, gr->db1, gr->dw2, st);
@@ -768,8 +766,8 @@ cadet_status cadet_ffn_backward(const void* X, const void* W1, const void* W2, c
   if (ws_bytes < need) return ws_err(ws_bytes, need);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const int N = d * m;
-  cudaError_t e = cudaMemsetAsync(dW1, 0, (size_t)d * N * 4, st);
-  if (e == cudaSuccess) e = cudaMemsetAsync(dW2, 0, (size_t)N * d * 4, st);
+  const ZeroSpan zs[2] = {{dW1, (size_t)d * N * 4}, {dW2, (size_t)N * d * 4}};
+  cudaError_t e = zero_many_launch(zs, 2, st);
   if (T == 0) return cuda_err(e, "ffn backward");
   void* dU = ws;
   if (e == cudaSuccess) {  // dU = (dY W2^T) * GELU'(U)  with  dW2 = G^T dY  in the same launch

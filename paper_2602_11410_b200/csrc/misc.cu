@@ -353,4 +353,48 @@ cudaError_t add_bf16_launch(const void* a, const void* b, void* out, size_t n, c
   return cudaGetLastError();
 }
 
+
+struct ZeroSpans {
+  void* p[8];
+  unsigned long long n[8];
+  int count;
+};
+__global__ void __launch_bounds__(256) zero_many_kernel(ZeroSpans z) {
+  pdl_trigger();
+  pdl_wait();
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  const size_t tid = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (int s = 0; s < z.count; ++s) {
+    uint4* q = reinterpret_cast<uint4*>(z.p[s]);
+    const size_t n16 = (reinterpret_cast<uintptr_t>(z.p[s]) & 15) ? 0 : z.n[s] / 16;  // unaligned: bytewise
+    for (size_t i = tid; i < n16; i += stride) q[i] = make_uint4(0u, 0u, 0u, 0u);
+    for (size_t i = n16 * 16 + tid; i < z.n[s]; i += stride) reinterpret_cast<uint8_t*>(z.p[s])[i] = 0;
+  }
+}
+cudaError_t zero_many_launch(const ZeroSpan* spans, int n, cudaStream_t st) {
+  ZeroSpans z;
+  z.count = 0;
+  size_t total = 0;
+  for (int i = 0; i < n && z.count < 8; ++i) {
+    if (!spans[i].ptr || !spans[i].bytes) continue;
+    z.p[z.count] = spans[i].ptr;
+    z.n[z.count] = spans[i].bytes;
+    total += spans[i].bytes;
+    ++z.count;
+  }
+  if (z.count == 0) return cudaSuccess;
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  const size_t b = (total / 16 + 255) / 256;
+  const int grid = (int)(b < 1 ? 1 : (b > (size_t)4 * sms ? (size_t)4 * sms : b));
+  ProfScope ps(PROF_OTHER, st, 1);
+  launch_pdl(zero_many_kernel, dim3(grid), dim3(256), 0, st, z);
+  return cudaGetLastError();
+}
+
 }  // namespace cadet

@@ -23,4 +23,11 @@ cudaError_t head_dhid_launch(const void* pre, const float* dz, const int32_t* bu
 cudaError_t head_dhid_full_launch(const void* pre, const float* dz, const float* w2, int n, int K, int dh, void* dhid,
                                   void* dhid_lo, float* db1, float* dw2, float* db2, cudaStream_t st);
 cudaError_t add_bf16_launch(const void* a, const void* b, void* out, size_t n, cudaStream_t st);
+// Zero up to 8 buffers in ONE launch (instead of one memset node each): spans of `bytes` at `ptr`
+// (null entries skipped; 16-byte stores when ptr is 16-byte aligned, bytewise otherwise).
+struct ZeroSpan {
+  void* ptr;
+  size_t bytes;
+};
+cudaError_t zero_many_launch(const ZeroSpan* spans, int n, cudaStream_t st);
 }  // namespace cadet

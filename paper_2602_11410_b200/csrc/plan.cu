@@ -528,11 +528,44 @@ __global__ void __launch_bounds__(256) pack_rows_kernel(const uint8_t* src, cons
   }
 }
 
+// Metadata-only pack (src == packed == null): the per-row timestamps / session ids, one thread per
+// row, so the row data can be moved by a second call on another stream.
+__global__ void __launch_bounds__(256) pack_meta_kernel(const int64_t* src_row, const int32_t* cu,
+                                                         const int32_t* n_packed, int budget, const int64_t* tp,
+                                                         const int32_t* sp, int64_t* t_out, int32_t* s_out) {
+  pdl_trigger();
+  pdl_wait();
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= budget) return;
+  const int k = *n_packed;
+  if (r < cu[k]) {
+    int lo = 0, hi = k - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (cu[mid] <= r)
+        lo = mid;
+      else
+        hi = mid - 1;
+    }
+    const size_t sr = src_row ? (size_t)src_row[lo] + (r - cu[lo]) : (size_t)r;
+    if (t_out) t_out[r] = tp ? tp[sr] : 0;
+    if (s_out) s_out[r] = sp ? sp[sr] : 0;
+  } else {
+    if (t_out) t_out[r] = 0;
+    if (s_out) s_out[r] = 0;
+  }
+}
+
 cudaError_t pack_launch(const void* src, const int64_t* src_row, const int32_t* lens, int32_t B, int32_t d,
                         int32_t budget, const int64_t* tp, const int32_t* sp, void* packed, int64_t* t_out,
                         int32_t* s_out, int32_t* cu_out, int32_t* n_packed, uint32_t* err, cudaStream_t st) {
   ProfScope ps(PROF_OTHER, st, 2);
   launch_pdl(pack_offsets_kernel, dim3(1), dim3(1024), 0, st, lens, B, budget, cu_out, n_packed, err);
+  if (!packed) {
+    launch_pdl(pack_meta_kernel, dim3((budget + 255) / 256), dim3(256), 0, st, src_row, cu_out, n_packed, budget, tp,
+               sp, t_out, s_out);
+    return cudaGetLastError();
+  }
   const int rows_per_block = 8;
   launch_pdl(pack_rows_kernel, dim3((budget + rows_per_block - 1) / rows_per_block), dim3(256), 0, st, reinterpret_cast<const uint8_t*>(src), src_row, cu_out, n_packed, d * 2, budget, tp, sp,
       reinterpret_cast<uint8_t*>(packed), t_out, s_out);

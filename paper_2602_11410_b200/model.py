@@ -326,6 +326,8 @@ class CadetStack:
         self._hws = None
         self._bufs_for = None
         self._side = None          # DP: stream on which per-group gradient all-reduces are issued
+        self._pack_stream = None   # side stream of the A13 row move
+        self._pack_done = None
         self._grad_events = None   # DP: [layer][4] events recorded by cadet_attn_backward_ev
 
     # -------------------------------------------------------------- buffers sized per batch
@@ -350,6 +352,8 @@ class CadetStack:
         self.cu = torch.empty(n_chunks + 8, dtype=torch.int32, device=self.dev)
         self.n_out = torch.zeros(1, dtype=torch.int32, device=self.dev)
         self.n_packed = torch.zeros(1, dtype=torch.int32, device=self.dev)
+        self.cu_hist2 = torch.empty(n_hist + 1, dtype=torch.int32, device=self.dev)  # the row-move pack's copy
+        self.n_packed2 = torch.zeros(1, dtype=torch.int32, device=self.dev)
         if cfg.full_loss:
             ahc = L.HeadConfig(cfg.J, cfg.d_model, cfg.da, 0)
             awb = lib.cadet_heads_workspace_bytes(C.byref(ahc), n_imp)
@@ -376,10 +380,23 @@ class CadetStack:
         self._ensure(inp.n_chunks, n_imp, inp.n_hist)
         st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
         chk = L.check
-        # A13 pack (contiguous histories, src_row = NULL) and A0 chunk
-        chk(lib.cadet_pack(_vp(inp.X_hist), None, _vp(inp.lens), inp.n_hist, d, T, _vp(inp.t_hist),
-                           _vp(inp.s_hist), _vp(self.Hs[0]), _vp(self.t_p), _vp(self.s_p), _vp(self.cu_hist),
-                           _vp(self.n_packed), _vp(self.small_ws), 256, st))
+        # A13 pack (contiguous histories, src_row = NULL) and A0 chunk.  The row move (HBM-bound) runs
+        # on a side stream while this stream packs the timestamps / sessions, chunks, plans and builds
+        # the RoPE table (latency-bound); the first layer waits for the rows.
+        cur = torch.cuda.current_stream()
+        if self._pack_stream is None:
+            self._pack_stream = torch.cuda.Stream(self.dev)
+            self._pack_done = torch.cuda.Event()
+        self._pack_stream.wait_stream(cur)
+        with torch.cuda.stream(self._pack_stream):
+            chk(lib.cadet_pack(_vp(inp.X_hist), None, _vp(inp.lens), inp.n_hist, d, T, None, None, _vp(self.Hs[0]),
+                               None, None, _vp(self.cu_hist2), _vp(self.n_packed2),
+                               C.c_void_p(self.small_ws.data_ptr() + 512), 256,
+                               C.c_void_p(self._pack_stream.cuda_stream)))
+            self._pack_done.record()
+        chk(lib.cadet_pack(None, None, _vp(inp.lens), inp.n_hist, d, T, _vp(inp.t_hist), _vp(inp.s_hist), None,
+                           _vp(self.t_p), _vp(self.s_p), _vp(self.cu_hist), _vp(self.n_packed), _vp(self.small_ws),
+                           256, st))
         chk(lib.cadet_chunk(_vp(self.cu_hist), inp.n_hist, cfg.L_chunk, _vp(self.cu), inp.n_chunks + 8,
                             _vp(self.n_out), C.c_void_p(self.small_ws.data_ptr() + 256), st))
         b = self.batch(inp).struct()
@@ -389,6 +406,7 @@ class CadetStack:
         self.acfg.plan_ready = 0
         chk(lib.cadet_mask_plan(C.byref(self.acfg), C.byref(b), ws, wsn, st))
         self.acfg.plan_ready = 2
+        cur.wait_event(self._pack_done)  # packed rows H[0]
         # A1-A6: residual layers  H[l+1] = H[l] + Attn(H[l])  (block mode: the pre-norm CADET block)
         for l in range(cfg.n_layers):
             self._layer_forward(l, b, ws, wsn, st, self.Hs[l + 1])
@@ -604,3 +622,4 @@ class CadetStack:
         ops.poll(self._hws)
         ops.poll(self.small_ws)            # pack error word
         ops.poll(self.small_ws[256:])      # chunk error word
+        ops.poll(self.small_ws[512:])      # row-move pack error word
