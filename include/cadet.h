@@ -119,6 +119,8 @@ typedef struct {
   int32_t d_model;
   int32_t d_hidden; /* dh >= 32, multiple of 8, K*dh multiple of 32 (default d/2) */
   int32_t dtype;    /* CADET_BF16 */
+  int32_t rows_in_ws; /* backward calls: 1 = ws still holds H[rows] gathered by cadet_heads_forward (same Hs, rows,
+                         n, ws), so the gather is skipped; the rows are still bounds-checked by the scatter */
 } cadet_head_config;
 typedef struct {
   const void* W1;   /* bf16 [d, K*dh] */

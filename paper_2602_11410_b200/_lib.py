@@ -59,7 +59,8 @@ class AdamWConfig(C.Structure):
 
 
 class HeadConfig(C.Structure):
-    _fields_ = [("K", C.c_int32), ("d_model", C.c_int32), ("d_hidden", C.c_int32), ("dtype", C.c_int32)]
+    _fields_ = [("K", C.c_int32), ("d_model", C.c_int32), ("d_hidden", C.c_int32), ("dtype", C.c_int32),
+                ("rows_in_ws", C.c_int32)]
 
 
 class HeadWeights(C.Structure):

@@ -642,7 +642,7 @@ cadet_status cadet_heads_backward(const cadet_head_config* h, const cadet_head_w
   if (n == 0) return cuda_err(e, "heads backward");
   if (e == cudaSuccess)
     e = head_dhid_full_launch(pre, dz, w->w2, n, h->K, h->d_hidden, dhid, dhid_lo, gr->db1, gr->dw2, gr->db2, st);
-  if (e == cudaSuccess) e = gather_rows_launch(Hs, rows, n, T, d, Hr, err, st);
+  if (e == cudaSuccess && !h->rows_in_ws) e = gather_rows_launch(Hs, rows, n, T, d, Hr, err, st);
   if (e == cudaSuccess) {  // dW1 = H_r^T (dhid_hi + dhid_lo), dHs[rows] (+)= (dhid_hi + dhid_lo) W1^T: one launch
     const int bnw = pick_bn_wgrad(N);
     GemmProblem gw = prob(d, N, n, act_t(Hr, n, d), act_t(dhid, n, N), EPI_ATOMIC);
@@ -661,6 +661,7 @@ cadet_status cadet_heads_backward(const cadet_head_config* h, const cadet_head_w
     g.epi.out = dHs;
     g.epi.ldo = d;
     g.epi.row_map = rows;
+    g.epi.row_map_max = T;  // invalid rows (latched by the gather) never scatter out of bounds
     if (accumulate) {  // in place: dHs[rows] = dHs[rows] + (...)
       g.epi.resid = dHs;
       g.epi.resid_f32 = 0;
@@ -699,7 +700,7 @@ cadet_status cadet_heads_loss_backward(const cadet_head_config* h, const cadet_h
   if (n == 0) return cuda_err(e, "heads backward");
   if (e == cudaSuccess) e = head_dz_launch(logits, bucket, label, n, h->K, dz, loss_sum, gr->db2, err, st);
   if (e == cudaSuccess) e = head_dhid_launch(pre, dz, bucket, w->w2, n, h->K, h->d_hidden, dhid, dhid_lo, gr->db1, gr->dw2, st);
-  if (e == cudaSuccess) e = gather_rows_launch(Hs, rows, n, T, d, Hr, err, st);
+  if (e == cudaSuccess && !h->rows_in_ws) e = gather_rows_launch(Hs, rows, n, T, d, Hr, err, st);
   if (e == cudaSuccess) {  // dW1 = H_r^T (dhid_hi + dhid_lo) and dHs[rows] = (dhid_hi + dhid_lo) W1^T: one launch
     const int bnw = pick_bn_wgrad(N);
     GemmProblem gw = prob(d, N, n, act_t(Hr, n, d), act_t(dhid, n, N), EPI_ATOMIC);
@@ -718,6 +719,7 @@ cadet_status cadet_heads_loss_backward(const cadet_head_config* h, const cadet_h
     g.epi.out = dHs;
     g.epi.ldo = d;
     g.epi.row_map = rows;
+    g.epi.row_map_max = T;  // invalid rows (latched by the gather) never scatter out of bounds
     e = gemm_launch2(&g, 1, pick_bn(n, d), &gw, 1, bnw, st);
   }
   return cuda_err(e, "heads backward");

@@ -161,7 +161,7 @@ __device__ __forceinline__ void run_epilogue(const EpiParams& e, int row, int M,
   int orow = row;
   if (e.row_map) {
     orow = e.row_map[row];
-    if (orow < 0) return;
+    if (orow < 0 || (e.row_map_max > 0 && orow >= e.row_map_max)) return;
   }
   const size_t off = (size_t)orow * e.ldo + n0c;
   const size_t in_off = (size_t)row * e.ldo + n0c;

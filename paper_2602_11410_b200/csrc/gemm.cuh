@@ -33,6 +33,7 @@ struct EpiParams {
   int32_t out2_f32;
   const int32_t* row_map;  // optional output-row remap (scatter); < 0 = drop row
   int32_t resid_at_out;    // row_map stores: resid read at the output row (in-place accumulate)
+  int32_t row_map_max;     // row_map stores: rows >= this are dropped (0 = no bound)
   // RoPE (EPI_GATE_ROPE): (cos, sin) table [M][hd + 32] floats, interleaved per frequency
   const float* rope_cs;
   // heads (EPI_HEAD)

@@ -411,7 +411,7 @@ class CadetStack:
         for l in range(cfg.n_layers):
             self._layer_forward(l, b, ws, wsn, st, self.Hs[l + 1])
         # A7-A8: towers on impression rows + routed BCE
-        hc = L.HeadConfig(cfg.K, d, cfg.dh, 0)
+        hc = L.HeadConfig(cfg.K, d, cfg.dh, 0, 1)  # rows_in_ws: backward reuses the gathered rows
         hw = L.HeadWeights(self.W1.data_ptr(), self.b1.data_ptr(), self.w2.data_ptr(), self.b2.data_ptr())
         chk(lib.cadet_heads_forward(C.byref(hc), C.byref(hw), _vp(self.Hs[-1]), _vp(inp.rows), n_imp,
                                     _vp(self.logits), _vp(self.pre), _vp(self._hws), self._hws.numel(), st))
@@ -601,7 +601,7 @@ class CadetStack:
         chk(lib.cadet_heads_backward(C.byref(hc), C.byref(hw), _vp(self.Hs[-1]), _vp(inp.rows), n, T, _vp(self.pre),
                                      _vp(self.dz_ctx), 0, _vp(self.dHs[-1]), C.byref(hg), _vp(self._hws),
                                      self._hws.numel(), st))
-        ahc = L.HeadConfig(cfg.J, d, cfg.da, 0)
+        ahc = L.HeadConfig(cfg.J, d, cfg.da, 0, 1)
         ahw = L.HeadWeights(self.aW1.data_ptr(), self.ab1.data_ptr(), self.aw2.data_ptr(), self.ab2.data_ptr())
         ahg = L.HeadGrads(self.agW1.data_ptr(), self.agb1.data_ptr(), self.agw2.data_ptr(), self.agb2.data_ptr())
         chk(lib.cadet_heads_backward(C.byref(ahc), C.byref(ahw), _vp(self.Hs[-1]), _vp(inp.rows), n, T,
