@@ -354,20 +354,20 @@ cadet_status cadet_attn_forward(const cadet_attn_config* cfg, const cadet_batch*
   // A4: interaction gates + timestamp RoPE  (Eq. 5)
   if (e == cudaSuccess) {
     if (cfg->use_int_gate) {
+      // Zq = Q W_qg, Zk = K W_kg stored plainly (saved for the backward); sigma, the product with Q, K
+      // and the rotation run in one HBM pass after (a fused gate+RoPE epilogue made these GEMMs
+      // epilogue-bound at 0.66 of their mainloop rate)
       GemmProblem g[2];
       const void* Ws[2] = {w->W_qg, w->W_kg};
       const void* src[2] = {L.Q, L.K};
-      void* outs[2] = {L.Qr, L.Kr};
-      void* aux[2] = {L.Zq, L.Zk};
+      void* zs[2] = {L.Zq, L.Zk};
       for (int i = 0; i < 2; ++i) {
-        g[i] = prob(T, d, d, act(src[i], T, d), w_fwd(Ws[i], d, d), cfg->use_rope ? EPI_GATE_ROPE : EPI_GATE);
-        g[i].epi.out = outs[i];
-        g[i].epi.src = src[i];
-        g[i].epi.aux = aux[i];
-        g[i].epi.hd = hd;
-        g[i].epi.rope_cs = W.rope_cs;
+        g[i] = prob(T, d, d, act(src[i], T, d), w_fwd(Ws[i], d, d), EPI_STORE);
+        g[i].epi.out = zs[i];
       }
       e = gemm_launch(g, 2, bn, st);
+      if (e == cudaSuccess)
+        e = gate_rope_fwd_launch(L.Q, L.K, L.Zq, L.Zk, cfg->use_rope ? W.rope_cs : nullptr, L.Qr, L.Kr, T, d, hd, st);
     } else if (cfg->use_rope) {
       e = rope_apply_launch(L.Q, L.Qr, T, d, hd, W.rope_cs, st);
       if (e == cudaSuccess) e = rope_apply_launch(L.K, L.Kr, T, d, hd, W.rope_cs, st);

@@ -66,6 +66,46 @@ __global__ void rope_apply_kernel(const __nv_bfloat16* in, __nv_bfloat16* out, i
   reinterpret_cast<__nv_bfloat162*>(out)[idx] = __floats2bfloat162_rn(v.x * r.x - v.y * r.y, v.x * r.y + v.y * r.x);
 }
 
+// A4 after the gate GEMMs (Z_q = Q W_qg, Z_k = K W_kg stored bf16): Qr = RoPE_t(Q * sigma(Z_q)) and
+// Kr = RoPE_t(K * sigma(Z_k)) in one HBM pass (Eq. 5 + P:274); one thread per (row, 8 columns), Q
+// and K together so the row's table window is read once; cs null = no RoPE.
+__global__ void __launch_bounds__(256) gate_rope_fwd_kernel(const __nv_bfloat16* Q, const __nv_bfloat16* K,
+                                                            const __nv_bfloat16* Gq, const __nv_bfloat16* Gk,
+                                                            const float* cs, __nv_bfloat16* Qr, __nv_bfloat16* Kr,
+                                                            int T, int d, int hd) {
+  pdl_trigger();
+  pdl_wait();
+  const int per_row = d / 8;
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= T * per_row) return;
+  const int row = idx / per_row, c0 = (idx - row * per_row) * 8;
+  const size_t off = (size_t)row * d + c0;
+  float cv[4] = {1.f, 1.f, 1.f, 1.f}, sv[4] = {0.f, 0.f, 0.f, 0.f};
+  if (cs) {  // the 8-column group never crosses a head edge (hd % 8 == 0)
+    const float4* q = reinterpret_cast<const float4*>(cs + (size_t)row * (hd + 32) + (c0 % hd));
+    const float4 a = q[0], b = q[1];
+    cv[0] = a.x, sv[0] = a.y, cv[1] = a.z, sv[1] = a.w, cv[2] = b.x, sv[2] = b.y, cv[3] = b.z, sv[3] = b.w;
+  }
+  const __nv_bfloat16* src[2] = {Q, K};
+  const __nv_bfloat16* gate[2] = {Gq, Gk};
+  __nv_bfloat16* dst[2] = {Qr, Kr};
+#pragma unroll
+  for (int w = 0; w < 2; ++w) {
+    const uint4 xu = *reinterpret_cast<const uint4*>(src[w] + off);
+    const uint4 gu = *reinterpret_cast<const uint4*>(gate[w] + off);
+    const __nv_bfloat162* x2 = reinterpret_cast<const __nv_bfloat162*>(&xu);
+    const __nv_bfloat162* g2 = reinterpret_cast<const __nv_bfloat162*>(&gu);
+    uint32_t o[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float2 x = __bfloat1622float2(x2[e]), z = __bfloat1622float2(g2[e]);
+      const float a = x.x * sigmoid_fast(z.x), b = x.y * sigmoid_fast(z.y);
+      o[e] = pack_bf16(a * cv[e] - b * sv[e], a * sv[e] + b * cv[e]);
+    }
+    *reinterpret_cast<uint4*>(dst[w] + off) = make_uint4(o[0], o[1], o[2], o[3]);
+  }
+}
+
 // dr: fp32 (dQr accumulator) or bf16 (dKr).  gate (Z) bf16 may be null (no interaction gate):
 // then out_u is unused and out_r (bf16 if r_bf16) receives dQt directly.
 // One thread = 8 consecutive columns (4 pairs) of one row: 16-byte accesses, (cos, sin) from the
@@ -311,6 +351,18 @@ cudaError_t rope_gate_bwd_launch(const void* dr, int dr_f32, const void* Xq, con
   if (work)
     launch_pdl(rope_gate_bwd_kernel, dim3(blocks(work, 256)), dim3(256), 0, st, dr, dr_f32, reinterpret_cast<const __nv_bfloat16*>(Xq), reinterpret_cast<const __nv_bfloat16*>(Z),
         reinterpret_cast<__nv_bfloat16*>(out_u), out_r, r_bf16, T, d, hd, cs);
+  return cudaGetLastError();
+}
+cudaError_t gate_rope_fwd_launch(const void* Q, const void* K, const void* Gq, const void* Gk, const float* cs,
+                                 void* Qr, void* Kr, int T, int d, int hd, cudaStream_t st) {
+  ProfScope ps(PROF_OTHER, st, 1);
+  const size_t work = (size_t)T * d / 8;
+  if (work >= (size_t)INT32_MAX) return cudaErrorInvalidValue;
+  if (work)
+    launch_pdl(gate_rope_fwd_kernel, dim3(blocks(work, 256)), dim3(256), 0, st,
+               reinterpret_cast<const __nv_bfloat16*>(Q), reinterpret_cast<const __nv_bfloat16*>(K),
+               reinterpret_cast<const __nv_bfloat16*>(Gq), reinterpret_cast<const __nv_bfloat16*>(Gk), cs,
+               reinterpret_cast<__nv_bfloat16*>(Qr), reinterpret_cast<__nv_bfloat16*>(Kr), T, d, hd);
   return cudaGetLastError();
 }
 cudaError_t gather_rows_launch(const void* H, const int32_t* rows, int n, int T, int d, void* out, uint32_t* err,

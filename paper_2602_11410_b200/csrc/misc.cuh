@@ -10,6 +10,9 @@ cudaError_t rope_theta_launch(double* theta, int hd, double phi_min, double base
 cudaError_t rope_table_launch(float* cs, int T, int hd, const double* theta, const int64_t* t, const int32_t* row_seq,
                               const int32_t* cu, cudaStream_t st);
 cudaError_t rope_apply_launch(const void* in, void* out, int T, int d, int hd, const float* cs, cudaStream_t st);
+// A4 elementwise half: Qr = RoPE(Q * sigma(Z_q)), Kr = RoPE(K * sigma(Z_k)) (Z stored by the gate GEMMs)
+cudaError_t gate_rope_fwd_launch(const void* Q, const void* K, const void* Gq, const void* Gk, const float* cs,
+                                 void* Qr, void* Kr, int T, int d, int hd, cudaStream_t st);
 cudaError_t rope_gate_bwd_launch(const void* dr, int dr_f32, const void* Xq, const void* Z, void* out_u, void* out_r,
                                  int r_bf16, int T, int d, int hd, const float* cs, cudaStream_t st);
 cudaError_t gather_rows_launch(const void* H, const int32_t* rows, int n, int T, int d, void* out, uint32_t* err,

@@ -76,11 +76,12 @@ def test_c4_sampled_sequences_forward_backward(c4):
         for nm, Wi in (("Q", Wl[1]), ("K", Wl[2]), ("V", Wl[3])):
             assert_close_stored(sv[nm][a:e], sv["Xt"][a:e] @ Wi, what=f"{nm} {tag}")
         for nm, src, Wg, zn in (("Qr", "Q", Wl[4], "Zq"), ("Kr", "K", Wl[5], "Zk")):
+            # Qr / Kr are formed elementwise from the stored (bf16) Q and Zq
             Z = sv[src][a:e] @ Wg
             assert_close_stored(sv[zn][a:e], Z, what=f"{zn} {tag}")
             # the stored Qr / Kr are rotated by times rebased to the sequence start (R21:
             # scores depend only on differences); the oracle stage gets the same rebased times
-            assert_close_stored(sv[nm][a:e], O.rope_heads(sv[src][a:e] * O.sigmoid(Z), t[a:e] - t[a], ocfg),
+            assert_close_stored(sv[nm][a:e], O.rope_heads(sv[src][a:e] * O.sigmoid(sv[zn][a:e]), t[a:e] - t[a], ocfg),
                                 what=f"{nm} {tag}")
         o, l, _ = O.attention_core_forward(sv["Qr"][a:e], sv["Kr"][a:e], sv["V"][a:e], A, H)
         assert_close_stored(sv["O"][a:e], o, what=f"O {tag}")

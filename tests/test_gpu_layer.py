@@ -139,9 +139,10 @@ def test_layer_forward_stages_and_end_to_end(ops, case):
         assert_close_stored(sv[nm][:n], (sv["Xt"] @ Wi)[:n], what=nm)
     # A4: gates + RoPE fed by the GPU's Q, K
     for nm, src, Wg, zn in (("Qr", "Q", Wl[4], "Zq"), ("Kr", "K", Wl[5], "Zk")):
+        # Qr / Kr are formed elementwise from the stored (bf16) Q and Zq
         Z = sv[src] @ Wg
         assert_close_stored(sv[zn][:n], Z[:n], what=zn)
-        ref = O.rope_heads(sv[src] * O.sigmoid(Z), t, ocfg)
+        ref = O.rope_heads(sv[src] * O.sigmoid(sv[zn]), t, ocfg)
         assert_close_stored(sv[nm][:n], ref[:n], what=nm)
     # A5: core fed by the GPU's Qr, Kr, V
     Oref = np.zeros((T, d))
