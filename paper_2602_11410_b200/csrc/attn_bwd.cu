@@ -643,8 +643,11 @@ __global__ void __launch_bounds__(320, 1)
             const uint32_t stg = smem_u32(smem + C::STG_OFF + (warp - 2) * 2048);
             __nv_bfloat16* dst =
                 reinterpret_cast<__nv_bfloat16*>(p.dS) + (((size_t)slot * 128 + quarter * 32) * p.H + t.h) * 128 + grp * 64;
-            warp_flush_rows_bf16(stg, dst, (size_t)p.H * 128, 32, 32);
-            warp_store_rows_bf16(stg, wkeep, dst + 32, (size_t)p.H * 128, 32, 32);
+            // streaming (evict-first) stores: the dS^T tiles are read once, by the next kernel, from
+            // HBM anyway; keep L2 for the Q / dO tiles the other k-tiles re-read
+            warp_flush_rows_bf16<true>(stg, dst, (size_t)p.H * 128, 32, 32);
+            warp_stage_rows_bf16(stg, wkeep);
+            warp_flush_rows_bf16<true>(stg, dst + 32, (size_t)p.H * 128, 32, 32);
           } else {
             __syncwarp();
           }

@@ -352,6 +352,8 @@ CADET_DEV void warp_stage_rows_bf16(uint32_t stage, const uint32_t (&w)[16]) {
   for (int j = 0; j < 4; ++j)
     sts_u4(stage + lane * 64 + ((j ^ ((lane >> 1) & 3)) << 4), w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
 }
+// STREAM: evict-first stores (st.global.cs) for data no later kernel re-reads soon from L2.
+template <bool STREAM = false>
 CADET_DEV void warp_flush_rows_bf16(uint32_t stage, __nv_bfloat16* g0, size_t ld, int rows_valid, int ncol) {
   const uint32_t lane = threadIdx.x & 31;
   __syncwarp();
@@ -359,7 +361,13 @@ CADET_DEV void warp_flush_rows_bf16(uint32_t stage, __nv_bfloat16* g0, size_t ld
   for (int i = 0; i < 4; ++i) {
     const int row = i * 8 + (lane >> 2), j = lane & 3;
     const uint4 v = lds_u4(stage + row * 64 + ((j ^ ((row >> 1) & 3)) << 4));
-    if (row < rows_valid && j * 8 < ncol) *reinterpret_cast<uint4*>(g0 + (size_t)row * ld + j * 8) = v;
+    if (row < rows_valid && j * 8 < ncol) {
+      uint4* dst = reinterpret_cast<uint4*>(g0 + (size_t)row * ld + j * 8);
+      if (STREAM)
+        __stcs(dst, v);
+      else
+        *dst = v;
+    }
   }
   __syncwarp();
 }
