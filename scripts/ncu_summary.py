@@ -39,7 +39,8 @@ def main():
     for a in sys.argv[2:]:
         if a.endswith(".csv"):
             data = launch_list(a)
-            starts = [i for i, d in enumerate(data) if "pack_offsets_kernel" in d["Kernel Name"]]
+            # a step starts at the pack_offsets launch right before its row-move pack (pack_rows)
+            starts = [i - 1 for i, d in enumerate(data) if "pack_rows_kernel" in d["Kernel Name"]]
             step = data[starts[-1]:] if starts else data
             tot = sum(float(d["Metric Value"]) for d in step)
             agg = collections.OrderedDict()

@@ -13,7 +13,7 @@ def klass(name: str) -> str:
         return "gemm"
     if "attn_fwd_kernel" in name:
         return "attn_fwd"
-    if "attn_bwd_dq_kernel" in name or "attn_bwd_dkv_kernel" in name:
+    if "attn_bwd_dq_kernel" in name or "attn_bwd_dkv_kernel" in name or "attn_bwd_dq2_kernel" in name:
         return "attn_bwd"
     return "other"
 
@@ -25,8 +25,9 @@ per = collections.OrderedDict()
 for d in data:
     per.setdefault(d["ID"], {"name": d["Kernel Name"]})[d["Metric Name"]] = float(d["Metric Value"])
 launches = list(per.values())
-# the last step starts at the last pack_offsets launch (first kernel of CadetStack.step)
-start = max(i for i, l in enumerate(launches) if "pack_offsets" in l["name"])
+# the last step starts at the pack_offsets launch right before the last pack_rows launch (the
+# row-move pack, issued first by CadetStack.step on its side stream)
+start = max(i for i, l in enumerate(launches) if "pack_rows" in l["name"]) - 1
 step = launches[start:]
 agg = collections.defaultdict(lambda: {"dram_bytes_per_step": 0.0, "launches": 0, "time_us": 0.0})
 for l in step:
