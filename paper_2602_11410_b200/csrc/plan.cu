@@ -33,10 +33,11 @@ size_t plan_bytes(int32_t n, int32_t T, int32_t max_seqlen) {
   b += align256((size_t)(n + 1) * 8);
   b += align256(nq * sizeof(QTileInfo));
   b += align256(nq * 4) * 2;
-  b += align256(hm * 2 * 4);
+  b += align256(hm * 3 * 4);
   b += align256((size_t)(n + 1) * 4);
   b += align256(nq * 4) * 2;
   b += align256(list_cap_of(nq, hm) * 4);
+  b += align256((size_t)(n + 1) * 4);       // seq_rank
   return b;
 }
 
@@ -62,11 +63,12 @@ PlanView plan_carve(void* ws, int32_t n, int32_t T, int32_t max_seqlen) {
   v.qinfo = reinterpret_cast<QTileInfo*>(take((size_t)v.nq_cap * sizeof(QTileInfo)));
   v.fwd_order = reinterpret_cast<int32_t*>(take((size_t)v.nq_cap * 4));
   v.bwd_order = reinterpret_cast<int32_t*>(take((size_t)v.nq_cap * 4));
-  v.hist = reinterpret_cast<int32_t*>(take((size_t)v.hmax * 2 * 4));
+  v.hist = reinterpret_cast<int32_t*>(take((size_t)v.hmax * 3 * 4));
   v.tri_off = reinterpret_cast<int32_t*>(take((size_t)(n + 1) * 4));
   v.bwd_off = reinterpret_cast<int32_t*>(take((size_t)v.nq_cap * 4));
   v.bwd_cnt = reinterpret_cast<int32_t*>(take((size_t)v.nq_cap * 4));
   v.bwd_list = reinterpret_cast<int32_t*>(take(list_cap_of(v.nq_cap, v.hmax) * 4));
+  v.seq_rank = reinterpret_cast<int32_t*>(take((size_t)(n + 1) * 4));
   return v;
 }
 
@@ -141,7 +143,7 @@ __global__ void __launch_bounds__(1024) plan_seq_kernel(PlanArgs a, PlanView v) 
     v.counters[1] = a.n;
     *v.pairs = 0ull;
   }
-  for (int i = tid; i < 2 * v.hmax; i += nt) v.hist[i] = 0;
+  for (int i = tid; i < 3 * v.hmax; i += nt) v.hist[i] = 0;
   if (err) atomicOr(v.err, err);
 }
 
@@ -269,9 +271,10 @@ __global__ void __launch_bounds__(128) plan_tile_kernel(PlanArgs a, PlanView v) 
   info.pad0 = info.pad1 = 0;
   v.qinfo[g] = info;
   const int cost_f = min(nf + (qt + 1 - kt2), v.hmax - 1);
-  const int cost_b = min(nq_s - qt, v.hmax - 1);
+  const int lb = min(nq_s, v.hmax - 1);
   atomicAdd(&v.hist[cost_f], 1);
-  atomicAdd(&v.hist[v.hmax + cost_b], 1);
+  atomicAdd(&v.hist[v.hmax + lb], 1);                        // tiles per sequence-length bucket
+  if (qt == 0) v.seq_rank[s] = atomicAdd(&v.hist[2 * v.hmax + lb], 1);  // the sequence's rank in it
 }
 
 // ---------------------------------------------------------------- K4 / K5
@@ -311,9 +314,17 @@ __global__ void __launch_bounds__(128) plan_scatter_kernel(PlanArgs a, PlanView 
   const int len = min(seq_len_safe(a.cu, info.seq, a.T), a.max_seqlen);
   const int nq_s = (len + TILE - 1) / TILE;
   const int cost_f = min(info.nf + (info.qt + 1 - info.kt2), v.hmax - 1);
-  const int cost_b = min(nq_s - info.qt, v.hmax - 1);
-  v.fwd_order[atomicAdd(&v.hist[cost_f], 1)] = g;
-  v.bwd_order[atomicAdd(&v.hist[v.hmax + cost_b], 1)] = g;
+  const int lb = min(nq_s, v.hmax - 1);
+  (void)cost_f;
+  // sequence-major orders: bucket start (longest sequences first) + rank * tiles + tile, q-tiles
+  // in descending order (the last q-tile sees the most keys), k-tiles ascending (k-tile 0 is seen
+  // by every q-tile): the CTAs running together work on one sequence, whose K / V (forward) or
+  // Q / dO (backward) tiles then come from L2
+  const int seq0 = v.hist[v.hmax + lb] + v.seq_rank[info.seq] * lb;
+  if (seq0 + lb <= v.nq_cap) {
+    v.fwd_order[seq0 + (lb - 1 - info.qt)] = g;
+    v.bwd_order[seq0 + info.qt] = g;
+  }
   // visit list of g as a k-tile (transpose of the forward visit rule): q-tiles qt >= kt of the
   // sequence with kt < nf(qt) or kt2(qt) <= kt <= qt; slots [base, base + nq_s - kt) of the
   // sequence's triangle

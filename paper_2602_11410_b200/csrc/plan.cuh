@@ -27,13 +27,16 @@ struct PlanView {   // device pointers into the workspace
   int32_t* tile_off;  // [n+1] prefix sum of nq_s
   int64_t* tc_off;    // [n+1] prefix sum of nq_s^2 (export)
   QTileInfo* qinfo;   // [nq_cap]
-  int32_t* fwd_order; // [nq_cap] q-tiles by descending forward cost
-  int32_t* bwd_order; // [nq_cap] k-tiles by descending backward cost
-  int32_t* hist;      // [2 * hmax] histograms / cursors
+  int32_t* fwd_order; // [nq_cap] q-tiles, sequence-major (see bwd_order), each sequence's q-tiles descending
+  int32_t* bwd_order; // [nq_cap] k-tiles, sequence-major: sequences by descending length, each sequence's
+                      // k-tiles in ascending order (heaviest first), so the CTAs running together share
+                      // one sequence's Q / dO tiles in L2
+  int32_t* hist;      // [3 * hmax] histograms / cursors (fwd cost, bwd sequence length, rank counters)
   int32_t* tri_off;   // [n+1] prefix sum of nq_s (nq_s + 1) / 2 (visit-list slots per sequence)
   int32_t* bwd_off;   // [nq_cap] start of k-tile g's visit list in bwd_list
   int32_t* bwd_cnt;   // [nq_cap] its length
   int32_t* bwd_list;  // [list_cap] q-tiles visiting k-tile g: qt | FULL << 30 (all cells visible)
+  int32_t* seq_rank;  // [n] rank of a sequence among those with the same tile count (bwd order)
   int32_t nq_cap, hmax, list_cap;
 };
 
