@@ -429,10 +429,13 @@ cadet_status cadet_attn_backward_ev(const cadet_attn_config* cfg, const cadet_ba
   cudaError_t e = cfg->plan_ready >= 2 ? cudaSuccess : rope_prepare(cfg, b, W, v, st);
   const float* cs = cfg->use_rope ? W.rope_cs : nullptr;
   float* gws[7] = {gr->dW_xg, gr->dW_q, gr->dW_k, gr->dW_v, gr->dW_qg, gr->dW_kg, gr->dW_o};
-  if (e == cudaSuccess) {  // the 7 weight gradients are split-K accumulated: zero them in one launch
-    ZeroSpan zs[7];
+  // A10's preprocess D = rowsum(dO * O) per head comes out of the A9 GEMM's epilogue when it exists
+  const bool d_in_a9 = cfg->use_out_proj && hd % 32 == 0;
+  if (e == cudaSuccess) {  // the 7 weight gradients (split-K accumulated) and D (atomics): one launch
+    ZeroSpan zs[8];
     for (int i = 0; i < 7; ++i) zs[i] = ZeroSpan{gws[i], wbytes};
-    e = zero_many_launch(zs, 7, st);
+    zs[7] = ZeroSpan{d_in_a9 ? W.D : nullptr, sizeof(float) * (size_t)H * T};
+    e = zero_many_launch(zs, 8, st);
   }
   auto mark = [&](int i) {  // grad group i complete on `st` (SURVEY 8(e) overlap)
     if (e == cudaSuccess && grad_events && grad_events[i]) e = cudaEventRecord((cudaEvent_t)grad_events[i], st);
@@ -443,6 +446,12 @@ cadet_status cadet_attn_backward_ev(const cadet_attn_config* cfg, const cadet_ba
   if (e == cudaSuccess && cfg->use_out_proj) {
     GemmProblem g = prob(T, d, d, act(dY, T, d), w_bwd(w->W_o, d, d), EPI_STORE);
     g.epi.out = W.dO;
+    if (d_in_a9) {
+      g.epi.dot_src = L.O;
+      g.epi.dot_out = W.D;
+      g.epi.dot_T = T;
+      g.epi.hd = hd;
+    }
     GemmProblem gw = wgrad(L.O, dY, gr->dW_o, T, d, d, bnw);
     e = gemm_launch2(&g, 1, bn, &gw, 1, bnw, st);
     dO = W.dO;
@@ -465,7 +474,7 @@ cadet_status cadet_attn_backward_ev(const cadet_attn_config* cfg, const cadet_ba
       p.dS = reinterpret_cast<uint8_t*>(ws) + layer_ws_base_bytes(cfg, n, T);
       p.ds_slots = ds_slots_of(n, T, b->max_seqlen);
     }
-    e = attn_bwd_pre_launch(L.O, dO, W.D, W.dQacc, T, H, hd, st);
+    if (!d_in_a9) e = attn_bwd_pre_launch(L.O, dO, W.D, W.dQacc, T, H, hd, st);
     if (e == cudaSuccess) e = zero_pad_rows_launch(W.dQacc, d * 2, T, b->cu_seqlens, n, st);
     if (e == cudaSuccess) e = zero_pad_rows_launch(W.dKr, d * 2, T, b->cu_seqlens, n, st);
     if (e == cudaSuccess) e = zero_pad_rows_launch(W.dV, d * 2, T, b->cu_seqlens, n, st);

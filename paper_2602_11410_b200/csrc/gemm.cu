@@ -277,7 +277,7 @@ __device__ __forceinline__ const void* epi_primary(const EpiParams& e) {
     case EPI_GATE_ROPE:
       return e.src;
     case EPI_STORE:
-      return e.resid_f32 ? nullptr : e.resid;
+      return e.resid ? (e.resid_f32 ? nullptr : e.resid) : e.dot_src;
     case EPI_GATE_BWD:
     case EPI_GELU_BWD:
       return e.aux_f32 ? nullptr : e.aux;
@@ -308,6 +308,17 @@ __device__ __forceinline__ void run_epilogue_warp(const EpiParams& e, int row0, 
           warp_load_rows(stg, e.resid, e.resid_f32, off0, e.ldo, rows_valid, r);
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] += r[j];
+      }
+      if (e.dot_out) {  // per-(row, head) partial of rowsum(acc * dot_src)
+        float x[32];
+        if (pre && !e.resid)
+          warp_sts_rows_bf16(stg, *reinterpret_cast<const uint4(*)[4]>(pre), x);
+        else
+          warp_load_rows(stg, e.dot_src, 0, off0, e.ldo, rows_valid, x);
+        float s = 0.f;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) s = fmaf(v[j], x[j], s);
+        if (lane < rows_valid) atomicAdd(e.dot_out + (size_t)(n0c / e.hd) * e.dot_T + row0 + lane, s);
       }
       warp_store_rows(stg, e.out, e.out_f32, off0, e.ldo, rows_valid, v);
     } break;
