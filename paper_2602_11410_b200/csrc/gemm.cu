@@ -86,7 +86,7 @@ __device__ __forceinline__ void kb_to_seg(const KProb& q, int kb, int& seg, int&
 // Epilogue mode sets (compile time): each GEMM launch instantiates only the epilogues of its
 // problems, so e.g. a plain store does not carry the gate + RoPE epilogue's registers.
 __host__ __device__ constexpr uint32_t MB(int m) { return 1u << m; }
-constexpr uint32_t MODES_ALL = MB(EPI_STORE) | MB(EPI_GATE) | MB(EPI_GATE_ROPE) | MB(EPI_GATE_BWD) | MB(EPI_ATOMIC) |
+constexpr uint32_t MODES_ALL = MB(EPI_STORE) | MB(EPI_GATE) | MB(EPI_GATE_BWD) | MB(EPI_ATOMIC) |
                                MB(EPI_HEAD) | MB(EPI_GELU) | MB(EPI_GELU_BWD);
 
 // exact GELU u Phi(u) and its derivative (R33)
@@ -145,16 +145,6 @@ __device__ __forceinline__ void store_any32(void* base, int is_f32, size_t off, 
   }
 }
 
-// Rotate adjacent pairs (v[2j], v[2j+1]) by alpha_j: cs = (cos, sin) interleaved.
-__device__ __forceinline__ void rope_rotate32(float (&v)[32], const float (&cs)[32]) {
-#pragma unroll
-  for (int j = 0; j < 32; j += 2) {
-    const float x0 = v[j], x1 = v[j + 1], c = cs[j], s = cs[j + 1];
-    v[j] = x0 * c - x1 * s;
-    v[j + 1] = x0 * s + x1 * c;
-  }
-}
-
 template <uint32_t MODES>
 __device__ __forceinline__ void run_epilogue(const EpiParams& e, int row, int M, int n0c, float (&v)[32]) {
   if (row >= M) return;
@@ -175,18 +165,12 @@ __device__ __forceinline__ void run_epilogue(const EpiParams& e, int row, int M,
       }
       store_any32(e.out, e.out_f32, off, v);
     } break;
-    case EPI_GATE:
-    case EPI_GATE_ROPE: if constexpr (HAS_MODE(EPI_GATE) || HAS_MODE(EPI_GATE_ROPE)) {
+    case EPI_GATE: if constexpr (HAS_MODE(EPI_GATE)) {
       if (e.aux) store_any32(e.aux, e.aux_f32, in_off, v);
       float x[32];
       load_bf16x32(reinterpret_cast<const __nv_bfloat16*>(e.src) + in_off, x);
 #pragma unroll
       for (int j = 0; j < 32; ++j) v[j] = x[j] * sigmoid_fast(v[j]);
-      if (HAS_MODE(EPI_GATE_ROPE) && e.mode == EPI_GATE_ROPE) {
-        float cs[32];
-        load_f32x32(e.rope_cs + (size_t)row * (e.hd + 32) + (n0c % e.hd), cs);
-        rope_rotate32(v, cs);
-      }
       store_any32(e.out, e.out_f32, off, v);
     } break;
     case EPI_GATE_BWD: if constexpr (HAS_MODE(EPI_GATE_BWD)) {
@@ -274,7 +258,6 @@ __device__ __forceinline__ const void* epi_primary(const EpiParams& e) {
   if (e.row_map) return nullptr;
   switch (e.mode) {
     case EPI_GATE:
-    case EPI_GATE_ROPE:
       return e.src;
     case EPI_STORE:
       return e.resid ? (e.resid_f32 ? nullptr : e.resid) : e.dot_src;
@@ -288,8 +271,7 @@ __device__ __forceinline__ const void* epi_primary(const EpiParams& e) {
 
 template <uint32_t MODES>
 __device__ __forceinline__ void run_epilogue_warp(const EpiParams& e, int row0, int M, int n0c, float (&v)[32],
-                                                  uint32_t stg, const uint4* pre = nullptr,
-                                                  const uint4* pre_cs = nullptr) {
+                                                  uint32_t stg, const uint4* pre = nullptr) {
   const int lane = threadIdx.x & 31;
   if (e.row_map || e.mode == EPI_ATOMIC || e.mode == EPI_HEAD) {
     run_epilogue<MODES>(e, row0 + lane, M, n0c, v);
@@ -322,8 +304,7 @@ __device__ __forceinline__ void run_epilogue_warp(const EpiParams& e, int row0, 
       }
       warp_store_rows(stg, e.out, e.out_f32, off0, e.ldo, rows_valid, v);
     } break;
-    case EPI_GATE:
-    case EPI_GATE_ROPE: if constexpr (HAS_MODE(EPI_GATE) || HAS_MODE(EPI_GATE_ROPE)) {
+    case EPI_GATE: if constexpr (HAS_MODE(EPI_GATE)) {
       if (e.aux) warp_store_rows(stg, e.aux, e.aux_f32, off0, e.ldo, rows_valid, v);
       float x[32];
       if (pre)
@@ -332,14 +313,6 @@ __device__ __forceinline__ void run_epilogue_warp(const EpiParams& e, int row0, 
         warp_load_rows(stg, e.src, 0, off0, e.ldo, rows_valid, x);
 #pragma unroll
       for (int j = 0; j < 32; ++j) v[j] = x[j] * sigmoid_fast(v[j]);
-      if (HAS_MODE(EPI_GATE_ROPE) && e.mode == EPI_GATE_ROPE) {  // head-local window [n0c % hd, + 32) of the table
-        float cs[32];
-        if (pre_cs)
-          warp_sts_rows_f32(stg, *reinterpret_cast<const uint4(*)[8]>(pre_cs), cs);
-        else
-          warp_load_rows(stg, e.rope_cs, 1, (size_t)row0 * (e.hd + 32) + (n0c % e.hd), e.hd + 32, rows_valid, cs);
-        rope_rotate32(v, cs);
-      }
       warp_store_rows(stg, e.out, e.out_f32, off0, e.ldo, rows_valid, v);
     } break;
     case EPI_GATE_BWD: if constexpr (HAS_MODE(EPI_GATE_BWD)) {
@@ -513,29 +486,17 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_kernel(const __grid_cons
       const int n0 = U.n0 * BN;
       // the primary epilogue input of slice c + 2 is requested before slice c is processed
       const void* pb = epi_primary(q.epi);
-      // gate + RoPE launches also request the slice's RoPE table window a slice ahead
-      constexpr bool RPM = MODES == MB(EPI_GATE_ROPE);
-      const bool rp = RPM && q.epi.mode == EPI_GATE_ROPE && !q.epi.row_map;
-      uint4 g[4], gc[RPM ? 8 : 1];
+      uint4 g[4];
       auto issue = [&](int c) {
         const int n0c = n0 + c * 32;
-        if (c < BN / 32 && n0c < q.N && row0 < q.M) {
-          if (pb) warp_ldg_rows_bf16(pb, (size_t)row0 * q.epi.ldo + n0c, q.epi.ldo, q.M - row0, g);
-          if constexpr (RPM) {
-            if (rp)
-              warp_ldg_rows_f32(q.epi.rope_cs, (size_t)row0 * (q.epi.hd + 32) + (n0c % q.epi.hd), q.epi.hd + 32,
-                                q.M - row0, gc);
-          }
-        }
+        if (c < BN / 32 && n0c < q.N && row0 < q.M && pb)
+          warp_ldg_rows_bf16(pb, (size_t)row0 * q.epi.ldo + n0c, q.epi.ldo, q.M - row0, g);
       };
       issue(half);
       for (int c = half; c < BN / 32; c += 2) {
         const int n0c = n0 + c * 32;
         if (n0c >= q.N) break;
         uint4 cur[4] = {g[0], g[1], g[2], g[3]};
-        uint4 curc[RPM ? 8 : 1];
-#pragma unroll
-        for (int i = 0; i < (RPM ? 8 : 1); ++i) curc[i] = gc[i];
         issue(c + 2);
         uint32_t r[32];
         tmem_ld32(tmem_addr(tmem_base, quarter, buf * BN + c * 32), r);
@@ -543,7 +504,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_kernel(const __grid_cons
         float v[32];
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-        run_epilogue_warp<MODES>(q.epi, row0, q.M, n0c, v, stg, pb ? cur : nullptr, rp ? curc : nullptr);
+        run_epilogue_warp<MODES>(q.epi, row0, q.M, n0c, v, stg, pb ? cur : nullptr);
       }
       tc_fence_before();
       __syncwarp();
@@ -707,29 +668,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
       const int n0 = U.n0 * BN;
       // the primary epilogue input of slice c + 2 is requested before slice c is processed
       const void* pb = epi_primary(q.epi);
-      // gate + RoPE launches also request the slice's RoPE table window a slice ahead
-      constexpr bool RPM = MODES == MB(EPI_GATE_ROPE);
-      const bool rp = RPM && q.epi.mode == EPI_GATE_ROPE && !q.epi.row_map;
-      uint4 g[4], gc[RPM ? 8 : 1];
+      uint4 g[4];
       auto issue = [&](int c) {
         const int n0c = n0 + c * 32;
-        if (c < BN / 32 && n0c < q.N && row0 < q.M) {
-          if (pb) warp_ldg_rows_bf16(pb, (size_t)row0 * q.epi.ldo + n0c, q.epi.ldo, q.M - row0, g);
-          if constexpr (RPM) {
-            if (rp)
-              warp_ldg_rows_f32(q.epi.rope_cs, (size_t)row0 * (q.epi.hd + 32) + (n0c % q.epi.hd), q.epi.hd + 32,
-                                q.M - row0, gc);
-          }
-        }
+        if (c < BN / 32 && n0c < q.N && row0 < q.M && pb)
+          warp_ldg_rows_bf16(pb, (size_t)row0 * q.epi.ldo + n0c, q.epi.ldo, q.M - row0, g);
       };
       issue(half);
       for (int c = half; c < BN / 32; c += 2) {
         const int n0c = n0 + c * 32;
         if (n0c >= q.N) break;
         uint4 cur[4] = {g[0], g[1], g[2], g[3]};
-        uint4 curc[RPM ? 8 : 1];
-#pragma unroll
-        for (int i = 0; i < (RPM ? 8 : 1); ++i) curc[i] = gc[i];
         issue(c + 2);
         uint32_t r[32];
         tmem_ld32(tmem_addr(tmem_base, quarter, buf * BN + c * 32), r);
@@ -737,7 +686,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
         float v[32];
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-        run_epilogue_warp<MODES>(q.epi, row0, q.M, n0c, v, stg, pb ? cur : nullptr, rp ? curc : nullptr);
+        run_epilogue_warp<MODES>(q.epi, row0, q.M, n0c, v, stg, pb ? cur : nullptr);
       }
       tc_fence_before();
       __syncwarp();
@@ -807,7 +756,6 @@ static cudaError_t launch_pair_modes(const GemmKParams& P, uint32_t modes, cudaS
   switch (modes) {
     case MB(EPI_STORE): return launch_pair<MB(EPI_STORE)>(P, stream);
     case MB(EPI_GATE): return launch_pair<MB(EPI_GATE)>(P, stream);
-    case MB(EPI_GATE_ROPE): return launch_pair<MB(EPI_GATE_ROPE)>(P, stream);
     case MB(EPI_STORE) | MB(EPI_ATOMIC): return launch_pair<MB(EPI_STORE) | MB(EPI_ATOMIC)>(P, stream);
     case MB(EPI_GATE_BWD) | MB(EPI_ATOMIC): return launch_pair<MB(EPI_GATE_BWD) | MB(EPI_ATOMIC)>(P, stream);
     case MB(EPI_ATOMIC): return launch_pair<MB(EPI_ATOMIC)>(P, stream);
@@ -841,7 +789,6 @@ static cudaError_t launch_bn_modes(const GemmKParams& P, uint32_t modes, cudaStr
   switch (modes) {
     case MB(EPI_STORE): return launch_bn<BN, MB(EPI_STORE)>(P, stream);
     case MB(EPI_GATE): return launch_bn<BN, MB(EPI_GATE)>(P, stream);
-    case MB(EPI_GATE_ROPE): return launch_bn<BN, MB(EPI_GATE_ROPE)>(P, stream);
     case MB(EPI_STORE) | MB(EPI_ATOMIC): return launch_bn<BN, MB(EPI_STORE) | MB(EPI_ATOMIC)>(P, stream);
     case MB(EPI_GATE_BWD) | MB(EPI_ATOMIC): return launch_bn<BN, MB(EPI_GATE_BWD) | MB(EPI_ATOMIC)>(P, stream);
     case MB(EPI_ATOMIC): return launch_bn<BN, MB(EPI_ATOMIC)>(P, stream);

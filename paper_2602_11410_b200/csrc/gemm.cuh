@@ -9,7 +9,7 @@ namespace cadet {
 enum EpiMode : int32_t {
   EPI_STORE = 0,      // out = acc (+ resid)                                        (A3, A6, A9, A12 ...)
   EPI_GATE = 1,       // out = src * sigma(acc); aux = acc                          (Eq. 4)
-  EPI_GATE_ROPE = 2,  // out = RoPE_t(src * sigma(acc)); aux = acc                  (Eq. 5 + P:274)
+  // 2: formerly the fused gate + RoPE epilogue (A4 now stores Z and runs gate_rope_fwd_kernel)
   EPI_GATE_BWD = 3,   // g = sigma(aux); out = acc*src*g*(1-g); out2 = acc*g + resid (A12)
   EPI_ATOMIC = 4,     // out += acc (fp32 red.add; split-K weight gradients)
   EPI_HEAD = 5,       // pre = acc + b1; aux = pre; logits[row, n/dh] += relu(pre).w2 (Eq. 8)
@@ -23,7 +23,7 @@ struct EpiParams {
   int32_t ldo;      // leading dim of out / resid / src / aux (elements)
   int32_t resid_f32;
   int32_t aux_f32;
-  int32_t hd;       // RoPE head dim (EPI_GATE_ROPE) or head hidden width dh (EPI_HEAD)
+  int32_t hd;       // head dim (EPI_STORE dot_out) or head hidden width dh (EPI_HEAD)
   int32_t n_towers; // EPI_HEAD: K
   void* out;
   const void* resid;
@@ -39,8 +39,6 @@ struct EpiParams {
   const void* dot_src;
   float* dot_out;
   int32_t dot_T;
-  // RoPE (EPI_GATE_ROPE): (cos, sin) table [M][hd + 32] floats, interleaved per frequency
-  const float* rope_cs;
   // heads (EPI_HEAD)
   const float* b1;
   const float* w2;
