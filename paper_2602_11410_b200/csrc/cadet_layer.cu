@@ -139,8 +139,10 @@ cadet_status cadet_attn_core_backward(const cadet_attn_config* cfg, const cadet_
   const int ob = d * (cfg->out_f32 ? 4 : 2);
   cudaError_t e = attn_bwd_pre_launch(O, dO, D, dQr, T, H, cfg->head_dim, st);
   if (e == cudaSuccess) e = zero_pad_rows_launch(dQr, d * 4, T, b->cu_seqlens, b->n_seqs, st);
-  if (e == cudaSuccess) e = zero_pad_rows_launch(dKr, ob, T, b->cu_seqlens, b->n_seqs, st);
-  if (e == cudaSuccess) e = zero_pad_rows_launch(dV, ob, T, b->cu_seqlens, b->n_seqs, st);
+  if (e == cudaSuccess) {
+    void* pads[2] = {dKr, dV};
+    e = zero_pad_rows_multi_launch(pads, 2, ob, T, b->cu_seqlens, b->n_seqs, st);
+  }
   if (e == cudaSuccess) e = attn_bwd_launch(Qr, Kr, V, dO, p, st);
   return cuda_err(e, "attention backward");
 }
@@ -475,9 +477,10 @@ cadet_status cadet_attn_backward_ev(const cadet_attn_config* cfg, const cadet_ba
       p.ds_slots = ds_slots_of(n, T, b->max_seqlen);
     }
     if (!d_in_a9) e = attn_bwd_pre_launch(L.O, dO, W.D, W.dQacc, T, H, hd, st);
-    if (e == cudaSuccess) e = zero_pad_rows_launch(W.dQacc, d * 2, T, b->cu_seqlens, n, st);
-    if (e == cudaSuccess) e = zero_pad_rows_launch(W.dKr, d * 2, T, b->cu_seqlens, n, st);
-    if (e == cudaSuccess) e = zero_pad_rows_launch(W.dV, d * 2, T, b->cu_seqlens, n, st);
+    if (e == cudaSuccess) {  // pad rows of the attention gradients: one launch for the three
+      void* pads[3] = {W.dQacc, W.dKr, W.dV};
+      e = zero_pad_rows_multi_launch(pads, 3, d * 2, T, b->cu_seqlens, n, st);
+    }
     if (e == cudaSuccess) e = attn_bwd_launch(L.Qr, L.Kr, L.V, dO, p, st);
   }
   // A11: R(-alpha) + interaction-gate backward

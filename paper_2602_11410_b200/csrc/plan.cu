@@ -584,9 +584,14 @@ cudaError_t pack_launch(const void* src, const int64_t* src_row, const int32_t* 
 }
 
 // ---------------------------------------------------------------- zero pad rows [cu[n], T)
-__global__ void zero_pad_rows_kernel(uint8_t* buf, int row_bytes, int T, const int32_t* cu, int n) {
+struct PadBufs {
+  uint8_t* buf[4];
+};
+// blockIdx.y selects the buffer: up to 4 [T, row_bytes] buffers in one launch
+__global__ void zero_pad_rows_kernel(PadBufs b, int row_bytes, int T, const int32_t* cu, int n) {
   pdl_trigger();
   pdl_wait();
+  uint8_t* buf = b.buf[blockIdx.y];
   const int nreal = n > 0 ? min(max(cu[n], 0), T) : 0;
   const size_t begin = (size_t)nreal * row_bytes, end = (size_t)T * row_bytes;
   for (size_t i = begin + ((size_t)blockIdx.x * blockDim.x + threadIdx.x) * 16; i < end;
@@ -596,8 +601,16 @@ __global__ void zero_pad_rows_kernel(uint8_t* buf, int row_bytes, int T, const i
 
 cudaError_t zero_pad_rows_launch(void* buf, int32_t row_bytes, int32_t T, const int32_t* cu, int32_t n,
                                  cudaStream_t st) {
+  void* one[1] = {buf};
+  return zero_pad_rows_multi_launch(one, 1, row_bytes, T, cu, n, st);
+}
+cudaError_t zero_pad_rows_multi_launch(void* const* bufs, int nbuf, int32_t row_bytes, int32_t T, const int32_t* cu,
+                                       int32_t n, cudaStream_t st) {
+  if (nbuf < 1 || nbuf > 4) return cudaErrorInvalidValue;
+  PadBufs b;
+  for (int i = 0; i < 4; ++i) b.buf[i] = reinterpret_cast<uint8_t*>(bufs[i < nbuf ? i : 0]);
   ProfScope ps(PROF_OTHER, st, 1);
-  launch_pdl(zero_pad_rows_kernel, dim3(148), dim3(256), 0, st, reinterpret_cast<uint8_t*>(buf), row_bytes, T, cu, n);
+  launch_pdl(zero_pad_rows_kernel, dim3(148, nbuf), dim3(256), 0, st, b, row_bytes, T, cu, n);
   return cudaGetLastError();
 }
 

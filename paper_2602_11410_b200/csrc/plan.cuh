@@ -63,5 +63,8 @@ cudaError_t pack_launch(const void* src, const int64_t* src_row, const int32_t* 
                         int32_t* s_out, int32_t* cu_out, int32_t* n_packed, uint32_t* err, cudaStream_t st);
 cudaError_t zero_pad_rows_launch(void* buf, int32_t row_bytes, int32_t T, const int32_t* cu, int32_t n,
                                  cudaStream_t st);
+// the same for up to 4 buffers of equal row size in one launch
+cudaError_t zero_pad_rows_multi_launch(void* const* bufs, int nbuf, int32_t row_bytes, int32_t T, const int32_t* cu,
+                                       int32_t n, cudaStream_t st);
 
 }  // namespace cadet
