@@ -592,7 +592,14 @@ static cadet_status check_head(const cadet_head_config* h, const cadet_head_weig
 size_t cadet_heads_workspace_bytes(const cadet_head_config* h, int32_t n) {
   if (!h || n < 0) return 0;
   const int N = h->K * h->d_hidden;
-  return 256 + a256((size_t)n * h->d_model * 2) + a256((size_t)n * N * 2) * 2 + a256((size_t)n * 4);
+  return 256 + a256((size_t)n * h->d_model * 2) + a256((size_t)n * N * 2) * 2 + a256((size_t)n * 4) +
+         a256((size_t)h->d_model * N * 2);
+}
+// fp16 copy of W1 in the heads workspace (after the error word, H_r, pre / spare, dhid and dz)
+static void* heads_w1h(void* ws, const cadet_head_config* h, int n) {
+  const int N = h->K * h->d_hidden;
+  return reinterpret_cast<uint8_t*>(ws) + 256 + a256((size_t)n * h->d_model * 2) + a256((size_t)n * N * 2) * 2 +
+         a256((size_t)n * 4);
 }
 
 cadet_status cadet_heads_forward(const cadet_head_config* h, const cadet_head_weights* w, const void* Hs,
@@ -613,10 +620,14 @@ cadet_status cadet_heads_forward(const cadet_head_config* h, const cadet_head_we
   uint32_t* err = reinterpret_cast<uint32_t*>(p);
   void* Hr = p + 256;
   void* pre = pre_out ? pre_out : (void*)(p + 256 + a256((size_t)n * d * 2));
-  cudaError_t e = gather_rows_launch(Hs, rows, n, 1 << 30, d, Hr, err, st);
+  // the towers' GEMMs run on fp16 operands (R27): H_r gathered as fp16, W1 converted once per call
+  void* W1h = heads_w1h(ws, h, n);
+  cudaError_t e = gather_rows_launch(Hs, rows, n, 1 << 30, d, Hr, err, st, 1);
+  if (e == cudaSuccess) e = bf16_to_f16_launch(w->W1, W1h, (size_t)d * N, st);
   if (e == cudaSuccess) e = head_init_launch(logits, w->b2, n, h->K, st);
   if (e == cudaSuccess) {
-    GemmProblem g = prob(n, N, d, act(Hr, n, d), w_fwd(w->W1, d, N), EPI_HEAD);
+    GemmProblem g = prob(n, N, d, act(Hr, n, d), w_fwd(W1h, d, N), EPI_HEAD);
+    g.f16 = 1;
     g.epi.aux = pre;
     g.epi.b1 = w->b1;
     g.epi.w2 = w->w2;
@@ -646,30 +657,27 @@ cadet_status cadet_heads_backward(const cadet_head_config* h, const cadet_head_w
   uint8_t* p = reinterpret_cast<uint8_t*>(ws);
   uint32_t* err = reinterpret_cast<uint32_t*>(p);
   void* Hr = p + 256;
-  void* dhid_lo = p + 256 + a256((size_t)n * d * 2);
   void* dhid = p + 256 + a256((size_t)n * d * 2) + a256((size_t)n * N * 2);
   const ZeroSpan zs[5] = {{gr->dW1, (size_t)d * N * 4}, {gr->db1, (size_t)N * 4}, {gr->dw2, (size_t)N * 4},
                           {gr->db2, (size_t)h->K * 4}, {accumulate ? nullptr : dHs, (size_t)T * d * 2}};
   cudaError_t e = zero_many_launch(zs, 5, st);
   if (n == 0) return cuda_err(e, "heads backward");
   if (e == cudaSuccess)
-    e = head_dhid_full_launch(pre, dz, w->w2, n, h->K, h->d_hidden, dhid, dhid_lo, gr->db1, gr->dw2, gr->db2, st);
-  if (e == cudaSuccess && !h->rows_in_ws) e = gather_rows_launch(Hs, rows, n, T, d, Hr, err, st);
-  if (e == cudaSuccess) {  // dW1 = H_r^T (dhid_hi + dhid_lo), dHs[rows] (+)= (dhid_hi + dhid_lo) W1^T: one launch
+    e = head_dhid_full_launch(pre, dz, w->w2, n, h->K, h->d_hidden, dhid, nullptr, gr->db1, gr->dw2, gr->db2, st);
+  void* W1h = heads_w1h(ws, h, n);
+  if (e == cudaSuccess && !h->rows_in_ws) {  // else ws holds the forward's fp16 H_r and W1 copies
+    e = gather_rows_launch(Hs, rows, n, T, d, Hr, err, st, 1);
+    if (e == cudaSuccess) e = bf16_to_f16_launch(w->W1, W1h, (size_t)d * N, st);
+  }
+  if (e == cudaSuccess) {  // dW1 = H_r^T dhid and dHs[rows] (+)= dhid W1^T (fp16 operands, R27): one launch
     const int bnw = pick_bn_wgrad(N);
     GemmProblem gw = prob(d, N, n, act_t(Hr, n, d), act_t(dhid, n, N), EPI_ATOMIC);
-    gw.nseg = 2;
-    gw.K[1] = n;
-    gw.A[1] = act_t(Hr, n, d);
-    gw.B[1] = act_t(dhid_lo, n, N);
+    gw.f16 = 1;
     gw.split_k = pick_split(d, N, bnw, n);
     gw.epi.out = gr->dW1;
     gw.epi.out_f32 = 1;
-    GemmProblem g = prob(n, d, N, act(dhid, n, N), w_bwd(w->W1, d, N), EPI_STORE);
-    g.nseg = 2;
-    g.K[1] = N;
-    g.A[1] = act(dhid_lo, n, N);
-    g.B[1] = w_bwd(w->W1, d, N);
+    GemmProblem g = prob(n, d, N, act(dhid, n, N), w_bwd(W1h, d, N), EPI_STORE);
+    g.f16 = 1;
     g.epi.out = dHs;
     g.epi.ldo = d;
     g.epi.row_map = rows;
@@ -703,7 +711,6 @@ cadet_status cadet_heads_loss_backward(const cadet_head_config* h, const cadet_h
   uint8_t* p = reinterpret_cast<uint8_t*>(ws);
   uint32_t* err = reinterpret_cast<uint32_t*>(p);
   void* Hr = p + 256;
-  void* dhid_lo = p + 256 + a256((size_t)n * d * 2);  // the forward's `pre` slot (pre is caller-owned here)
   void* dhid = p + 256 + a256((size_t)n * d * 2) + a256((size_t)n * N * 2);
   float* dz = reinterpret_cast<float*>(p + 256 + a256((size_t)n * d * 2) + 2 * a256((size_t)n * N * 2));
   const ZeroSpan zs[6] = {{loss_sum, 4},          {gr->dW1, (size_t)d * N * 4}, {gr->db1, (size_t)N * 4},
@@ -711,23 +718,21 @@ cadet_status cadet_heads_loss_backward(const cadet_head_config* h, const cadet_h
   cudaError_t e = zero_many_launch(zs, 6, st);
   if (n == 0) return cuda_err(e, "heads backward");
   if (e == cudaSuccess) e = head_dz_launch(logits, bucket, label, n, h->K, dz, loss_sum, gr->db2, err, st);
-  if (e == cudaSuccess) e = head_dhid_launch(pre, dz, bucket, w->w2, n, h->K, h->d_hidden, dhid, dhid_lo, gr->db1, gr->dw2, st);
-  if (e == cudaSuccess && !h->rows_in_ws) e = gather_rows_launch(Hs, rows, n, T, d, Hr, err, st);
-  if (e == cudaSuccess) {  // dW1 = H_r^T (dhid_hi + dhid_lo) and dHs[rows] = (dhid_hi + dhid_lo) W1^T: one launch
+  if (e == cudaSuccess) e = head_dhid_launch(pre, dz, bucket, w->w2, n, h->K, h->d_hidden, dhid, nullptr, gr->db1, gr->dw2, st);
+  void* W1h = heads_w1h(ws, h, n);
+  if (e == cudaSuccess && !h->rows_in_ws) {  // else ws holds the forward's fp16 H_r and W1 copies
+    e = gather_rows_launch(Hs, rows, n, T, d, Hr, err, st, 1);
+    if (e == cudaSuccess) e = bf16_to_f16_launch(w->W1, W1h, (size_t)d * N, st);
+  }
+  if (e == cudaSuccess) {  // dW1 = H_r^T dhid and dHs[rows] (+)= dhid W1^T (fp16 operands, R27): one launch
     const int bnw = pick_bn_wgrad(N);
     GemmProblem gw = prob(d, N, n, act_t(Hr, n, d), act_t(dhid, n, N), EPI_ATOMIC);
-    gw.nseg = 2;
-    gw.K[1] = n;
-    gw.A[1] = act_t(Hr, n, d);
-    gw.B[1] = act_t(dhid_lo, n, N);
+    gw.f16 = 1;
     gw.split_k = pick_split(d, N, bnw, n);
     gw.epi.out = gr->dW1;
     gw.epi.out_f32 = 1;
-    GemmProblem g = prob(n, d, N, act(dhid, n, N), w_bwd(w->W1, d, N), EPI_STORE);
-    g.nseg = 2;
-    g.K[1] = N;
-    g.A[1] = act(dhid_lo, n, N);
-    g.B[1] = w_bwd(w->W1, d, N);
+    GemmProblem g = prob(n, d, N, act(dhid, n, N), w_bwd(W1h, d, N), EPI_STORE);
+    g.f16 = 1;
     g.epi.out = dHs;
     g.epi.ldo = d;
     g.epi.row_map = rows;

@@ -25,6 +25,7 @@ struct KProb {
   int32_t M, N, nseg, kb_total, split_k, m_tiles, n_tiles, unit_begin;
   int32_t kb[GEMM_MAX_SEG];
   int32_t a_mn[GEMM_MAX_SEG], b_mn[GEMM_MAX_SEG];
+  int32_t f16;
   EpiParams epi;
 };
 
@@ -451,7 +452,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_kernel(const __grid_cons
           int seg, kk;
           kb_to_seg(q, kb, seg, kk);
           const uint32_t a_mn = q.a_mn[seg], b_mn = q.b_mn[seg];
-          const uint32_t idesc = idesc_bf16(BM, BN, a_mn, b_mn);
+          const uint32_t idesc = idesc_bf16(BM, BN, a_mn, b_mn) & (q.f16 ? ~((7u << 7) | (7u << 10)) : ~0u);  // F16: format 0
           const uint32_t sA = smem_u32(smem + stage * C::STAGE_BYTES);
           const uint32_t sB = sA + C::A_BYTES;
 #pragma unroll
@@ -632,7 +633,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
           int seg, kk;
           kb_to_seg(q, kb, seg, kk);
           const uint32_t a_mn = q.a_mn[seg], b_mn = q.b_mn[seg];
-          const uint32_t idesc = idesc_bf16(256, BN, a_mn, b_mn);
+          const uint32_t idesc = idesc_bf16(256, BN, a_mn, b_mn) & (q.f16 ? ~((7u << 7) | (7u << 10)) : ~0u);  // F16: format 0
           const uint32_t sA = smem_u32(smem + stage * C::STAGE_BYTES);
           const uint32_t sB = sA + C::A_BYTES;
 #pragma unroll
@@ -829,6 +830,7 @@ cudaError_t gemm_launch(const GemmProblem* probs, int nprob, int bn, cudaStream_
       q.kb_total += q.kb[s];
     }
     q.split_k = g.split_k < 1 ? 1 : (g.split_k > q.kb_total ? q.kb_total : g.split_k);
+    q.f16 = g.f16;
     q.m_tiles = (g.M + P.bm - 1) / P.bm;
     q.n_tiles = (g.N + bn - 1) / bn;
     q.unit_begin = total;

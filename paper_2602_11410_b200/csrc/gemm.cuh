@@ -60,6 +60,7 @@ struct GemmProblem {
   int32_t K[GEMM_MAX_SEG];
   OperandDesc A[GEMM_MAX_SEG], B[GEMM_MAX_SEG];
   int32_t split_k;   // > 1 only with EPI_ATOMIC
+  int32_t f16;       // operands are fp16 instead of bf16 (both A and B)
   EpiParams epi;
 };
 

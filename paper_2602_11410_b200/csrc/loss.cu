@@ -11,6 +11,7 @@
 
 #include "../../include/cadet.h"
 #include "misc.cuh"
+#include <cuda_fp16.h>
 #include "launch.cuh"
 #include "prof.cuh"
 #include "ptx.cuh"
@@ -251,14 +252,19 @@ __global__ void __launch_bounds__(256) head_dhid_full_kernel(const __nv_bfloat16
         s1[2 * e + 1] += g1;
         s2[2 * e] += z * fmaxf(pr.x, 0.f);
         s2[2 * e + 1] += z * fmaxf(pr.y, 0.f);
-        const __nv_bfloat162 h = __floats2bfloat162_rn(g0, g1);
-        const float2 hf = __bfloat1622float2(h);
-        const __nv_bfloat162 l = __floats2bfloat162_rn(g0 - hf.x, g1 - hf.y);
-        hi[e] = *reinterpret_cast<const uint32_t*>(&h);
-        lo[e] = *reinterpret_cast<const uint32_t*>(&l);
+        if (dhid_lo) {  // bf16 hi + lo (R27)
+          const __nv_bfloat162 h = __floats2bfloat162_rn(g0, g1);
+          const float2 hf = __bfloat1622float2(h);
+          const __nv_bfloat162 l = __floats2bfloat162_rn(g0 - hf.x, g1 - hf.y);
+          hi[e] = *reinterpret_cast<const uint32_t*>(&h);
+          lo[e] = *reinterpret_cast<const uint32_t*>(&l);
+        } else {        // one fp16 operand (R27)
+          const __half2 h = __floats2half2_rn(g0, g1);
+          hi[e] = *reinterpret_cast<const uint32_t*>(&h);
+        }
       }
       *reinterpret_cast<uint4*>(dhid + (size_t)i * N + c0) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
-      *reinterpret_cast<uint4*>(dhid_lo + (size_t)i * N + c0) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+      if (dhid_lo) *reinterpret_cast<uint4*>(dhid_lo + (size_t)i * N + c0) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
     }
   }
   __shared__ float sh1[8][257], sh2[8][257];

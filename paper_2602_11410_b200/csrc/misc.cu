@@ -8,6 +8,7 @@
 //   head_init / head_dz / head_dhid   A7/A8 routed BCE (Eq. 9) and the tower backward
 //   add_kernel              Y = O (+ resid) when the output projection is ablated
 #include "misc.cuh"
+#include <cuda_fp16.h>
 #include "launch.cuh"
 #include "prof.cuh"
 #include "ptx.cuh"
@@ -185,8 +186,29 @@ __global__ void __launch_bounds__(256) rope_gate_bwd_kernel(const void* dr, int 
   }
 }
 
+// bf16 16-byte chunk -> fp16 (the towers' GEMMs run on fp16 operands, R27)
+__device__ __forceinline__ uint4 bf16x8_to_f16x8(const uint4 u) {
+  const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&u);
+  uint4 o;
+  uint32_t* w = reinterpret_cast<uint32_t*>(&o);
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const float2 f = __bfloat1622float2(b[e]);
+    const __half2 h = __floats2half2_rn(f.x, f.y);
+    w[e] = *reinterpret_cast<const uint32_t*>(&h);
+  }
+  return o;
+}
+
+__global__ void bf16_to_f16_kernel(const uint4* src, uint4* dst, size_t n8) {
+  pdl_trigger();
+  pdl_wait();
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n8; i += (size_t)gridDim.x * blockDim.x)
+    dst[i] = bf16x8_to_f16x8(src[i]);
+}
+
 __global__ void gather_rows_kernel(const uint8_t* H, const int32_t* rows, int n, int T, int row_bytes, uint8_t* out,
-                                   uint32_t* err) {
+                                   uint32_t* err, int to_f16) {
   pdl_trigger();
   pdl_wait();
   const int r = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
@@ -199,7 +221,10 @@ __global__ void gather_rows_kernel(const uint8_t* H, const int32_t* rows, int n,
   }
   const uint4* s = reinterpret_cast<const uint4*>(H + (size_t)src * row_bytes);
   uint4* o = reinterpret_cast<uint4*>(out + (size_t)r * row_bytes);
-  for (int c = lane; c < row_bytes / 16; c += 32) o[c] = s[c];
+  if (to_f16)
+    for (int c = lane; c < row_bytes / 16; c += 32) o[c] = bf16x8_to_f16x8(s[c]);
+  else
+    for (int c = lane; c < row_bytes / 16; c += 32) o[c] = s[c];
 }
 
 __global__ void head_init_kernel(float* logits, const float* b2, int n, int K) {
@@ -273,16 +298,20 @@ __global__ void __launch_bounds__(256) head_dhid_kernel(const __nv_bfloat16* pre
           s1[2 * e + 1] += g1;
           s2[2 * e] += z * fmaxf(pr.x, 0.f);
           s2[2 * e + 1] += z * fmaxf(pr.y, 0.f);
-          // bf16 hi + lo split: the GEMM operand keeps ~16 bits (R27)
-          const __nv_bfloat162 h = __floats2bfloat162_rn(g0, g1);
-          const float2 hf = __bfloat1622float2(h);
-          const __nv_bfloat162 l = __floats2bfloat162_rn(g0 - hf.x, g1 - hf.y);
-          hi[e] = *reinterpret_cast<const uint32_t*>(&h);
-          lo[e] = *reinterpret_cast<const uint32_t*>(&l);
+          if (dhid_lo) {  // bf16 hi + lo split: the GEMM operand keeps ~16 bits (R27)
+            const __nv_bfloat162 h = __floats2bfloat162_rn(g0, g1);
+            const float2 hf = __bfloat1622float2(h);
+            const __nv_bfloat162 l = __floats2bfloat162_rn(g0 - hf.x, g1 - hf.y);
+            hi[e] = *reinterpret_cast<const uint32_t*>(&h);
+            lo[e] = *reinterpret_cast<const uint32_t*>(&l);
+          } else {        // one fp16 operand (11-bit mantissa; R27)
+            const __half2 h = __floats2half2_rn(g0, g1);
+            hi[e] = *reinterpret_cast<const uint32_t*>(&h);
+          }
         }
       }
       *reinterpret_cast<uint4*>(dhid + (size_t)i * N + c0) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
-      *reinterpret_cast<uint4*>(dhid_lo + (size_t)i * N + c0) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+      if (dhid_lo) *reinterpret_cast<uint4*>(dhid_lo + (size_t)i * N + c0) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
     }
   }
   __shared__ float sh1[8][257], sh2[8][257];
@@ -366,11 +395,21 @@ cudaError_t gate_rope_fwd_launch(const void* Q, const void* K, const void* Gq, c
   return cudaGetLastError();
 }
 cudaError_t gather_rows_launch(const void* H, const int32_t* rows, int n, int T, int d, void* out, uint32_t* err,
-                               cudaStream_t st) {
+                               cudaStream_t st, int to_f16) {
   ProfScope ps(PROF_OTHER, st, 1);
   if (n > 0)
-    launch_pdl(gather_rows_kernel, dim3(blocks(n, 8)), dim3(256), 0, st, reinterpret_cast<const uint8_t*>(H), rows, n, T, d * 2,
-                                                     reinterpret_cast<uint8_t*>(out), err);
+    launch_pdl(gather_rows_kernel, dim3(blocks(n, 8)), dim3(256), 0, st, reinterpret_cast<const uint8_t*>(H), rows, n,
+               T, d * 2, reinterpret_cast<uint8_t*>(out), err, to_f16);
+  return cudaGetLastError();
+}
+cudaError_t bf16_to_f16_launch(const void* src, void* dst, size_t n, cudaStream_t st) {
+  ProfScope ps(PROF_OTHER, st, 1);
+  if (n % 8) return cudaErrorInvalidValue;
+  if (n) {
+    const size_t b = (n / 8 + 255) / 256;
+    launch_pdl(bf16_to_f16_kernel, dim3((unsigned)(b > 1184 ? 1184 : b)), dim3(256), 0, st,
+               reinterpret_cast<const uint4*>(src), reinterpret_cast<uint4*>(dst), n / 8);
+  }
   return cudaGetLastError();
 }
 cudaError_t head_init_launch(float* logits, const float* b2, int n, int K, cudaStream_t st) {

@@ -15,8 +15,10 @@ cudaError_t gate_rope_fwd_launch(const void* Q, const void* K, const void* Gq, c
                                  void* Qr, void* Kr, int T, int d, int hd, cudaStream_t st);
 cudaError_t rope_gate_bwd_launch(const void* dr, int dr_f32, const void* Xq, const void* Z, void* out_u, void* out_r,
                                  int r_bf16, int T, int d, int hd, const float* cs, cudaStream_t st);
+// to_f16: the gathered rows are written as fp16 (the towers' GEMM operand)
 cudaError_t gather_rows_launch(const void* H, const int32_t* rows, int n, int T, int d, void* out, uint32_t* err,
-                               cudaStream_t st);
+                               cudaStream_t st, int to_f16 = 0);
+cudaError_t bf16_to_f16_launch(const void* src, void* dst, size_t n, cudaStream_t st);
 cudaError_t head_init_launch(float* logits, const float* b2, int n, int K, cudaStream_t st);
 cudaError_t head_dz_launch(const float* logits, const int32_t* bucket, const float* label, int n, int K, float* dz,
                            float* loss_sum, float* db2, uint32_t* err, cudaStream_t st);
