@@ -432,7 +432,7 @@ cadet_status cadet_attn_backward_ev(const cadet_attn_config* cfg, const cadet_ba
   const float* cs = cfg->use_rope ? W.rope_cs : nullptr;
   float* gws[7] = {gr->dW_xg, gr->dW_q, gr->dW_k, gr->dW_v, gr->dW_qg, gr->dW_kg, gr->dW_o};
   // A10's preprocess D = rowsum(dO * O) per head comes out of the A9 GEMM's epilogue when it exists
-  const bool d_in_a9 = cfg->use_out_proj && hd % 32 == 0;
+  const bool d_in_a9 = cfg->use_out_proj && hd >= 32;
   if (e == cudaSuccess) {  // the 7 weight gradients (split-K accumulated) and D (atomics): one launch
     ZeroSpan zs[8];
     for (int i = 0; i < 7; ++i) zs[i] = ZeroSpan{gws[i], wbytes};

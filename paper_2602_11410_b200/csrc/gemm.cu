@@ -298,10 +298,20 @@ __device__ __forceinline__ void run_epilogue_warp(const EpiParams& e, int row0, 
           warp_sts_rows_bf16(stg, *reinterpret_cast<const uint4(*)[4]>(pre), x);
         else
           warp_load_rows(stg, e.dot_src, 0, off0, e.ldo, rows_valid, x);
-        float s = 0.f;
+        // a 32-column slice covers at most two heads (hd >= 32): split the sum at the head edge
+        const int h0 = n0c / e.hd, split = (h0 + 1) * e.hd - n0c;
+        float s0 = 0.f, s1 = 0.f;
 #pragma unroll
-        for (int j = 0; j < 32; ++j) s = fmaf(v[j], x[j], s);
-        if (lane < rows_valid) atomicAdd(e.dot_out + (size_t)(n0c / e.hd) * e.dot_T + row0 + lane, s);
+        for (int j = 0; j < 32; ++j) {
+          if (j < split)
+            s0 = fmaf(v[j], x[j], s0);
+          else
+            s1 = fmaf(v[j], x[j], s1);
+        }
+        if (lane < rows_valid) {
+          atomicAdd(e.dot_out + (size_t)h0 * e.dot_T + row0 + lane, s0);
+          if (split < 32) atomicAdd(e.dot_out + (size_t)(h0 + 1) * e.dot_T + row0 + lane, s1);
+        }
       }
       warp_store_rows(stg, e.out, e.out_f32, off0, e.ldo, rows_valid, v);
     } break;

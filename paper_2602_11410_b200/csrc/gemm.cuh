@@ -35,7 +35,7 @@ struct EpiParams {
   int32_t resid_at_out;    // row_map stores: resid read at the output row (in-place accumulate)
   int32_t row_map_max;     // row_map stores: rows >= this are dropped (0 = no bound)
   // EPI_STORE extra (A9 -> A10 preprocess): dot_out[(n / hd) * dot_T + row] += sum over the slice's
-  // columns of acc * dot_src (bf16, same layout as out); needs hd % 32 == 0, dot_out zeroed
+  // columns of acc * dot_src (bf16, same layout as out), per head (hd >= 32); dot_out zeroed
   const void* dot_src;
   float* dot_out;
   int32_t dot_T;
