@@ -175,6 +175,47 @@ def test_pack_bit_exact(ops):
     assert (to_np(packed)[:14] == G.bf16_round(X[:14])).all() and (to_np(packed)[14:] == 0).all()
 
 
+def test_pack_split_modes_match_the_full_pack(ops):
+    """cadet_pack with src = packed = NULL (offsets + timestamps / sessions only, one thread per row)
+    and with t / s NULL (offsets + rows only) together reproduce the full call bit for bit — the
+    split CadetStack uses to move the rows on a side stream."""
+    import ctypes as C
+    from paper_2602_11410_b200 import _lib as L
+    rng = np.random.default_rng(9)
+    lens = [513, 1, 77, 300, 129, 1000]
+    R, d, budget = sum(lens), 64, 1500
+    X = bf16_tensor(rng.standard_normal((R, d)).astype(np.float32))
+    tp = torch.tensor(rng.integers(0, 10**12, size=R), dtype=torch.int64, device="cuda")
+    sp = torch.tensor(rng.integers(0, 50, size=R), dtype=torch.int32, device="cuda")
+    ln = torch.tensor(lens, dtype=torch.int32, device="cuda")
+    full = ops.pack(X, ln, budget, t_src=tp, s_src=sp)
+    st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    vp = lambda t: C.c_void_p(t.data_ptr()) if t is not None else None
+    ws = ops.workspace(L.lib().cadet_pack_workspace_bytes(len(lens)))
+    t_out = torch.full((budget,), -1, dtype=torch.int64, device="cuda")
+    s_out = torch.full((budget,), -1, dtype=torch.int32, device="cuda")
+    cu1 = torch.empty(len(lens) + 1, dtype=torch.int32, device="cuda")
+    n1 = torch.zeros(1, dtype=torch.int32, device="cuda")
+    L.check(L.lib().cadet_pack(None, None, vp(ln), len(lens), d, budget, vp(tp), vp(sp), None, vp(t_out), vp(s_out),
+                               vp(cu1), vp(n1), vp(ws), ws.numel(), st))
+    rows = torch.full((budget, d), 7.0, dtype=torch.bfloat16, device="cuda")
+    cu2 = torch.empty(len(lens) + 1, dtype=torch.int32, device="cuda")
+    n2 = torch.zeros(1, dtype=torch.int32, device="cuda")
+    L.check(L.lib().cadet_pack(vp(X), None, vp(ln), len(lens), d, budget, None, None, vp(rows), None, None, vp(cu2),
+                               vp(n2), vp(ws), ws.numel(), st))
+    ops.poll(ws)
+    packed, t_full, s_full, cu, n_packed, _ = full
+    assert torch.equal(n1, n_packed) and torch.equal(n2, n_packed)
+    k = int(n_packed.item())
+    assert torch.equal(cu1[: k + 1], cu[: k + 1]) and torch.equal(cu2[: k + 1], cu[: k + 1])
+    assert torch.equal(t_out, t_full) and torch.equal(s_out, s_full)
+    assert torch.equal(rows, packed)
+    # one of src / packed alone is an argument error
+    with pytest.raises(L.CadetError):
+        L.check(L.lib().cadet_pack(vp(X), None, vp(ln), len(lens), d, budget, vp(tp), vp(sp), None, vp(t_out),
+                                   vp(s_out), vp(cu1), vp(n1), vp(ws), ws.numel(), st))
+
+
 # ------------------------------------------------------------------ attention core forward
 def core_case(lengths, d, H, nc=None, scale=1.0, seed=0, flags=1, dl=120_000, T_extra=7):
     cu, t, s, ncv, T = make_case(lengths, n_cand=nc, seed=seed)
