@@ -488,9 +488,14 @@ cadet_status cadet_attn_backward_ev(const cadet_attn_config* cfg, const cadet_ba
   const void* dK = W.dK;
   if (e == cudaSuccess) {
     if (cfg->use_int_gate) {
-      e = rope_gate_bwd_launch(W.dQacc, 0, L.Q, L.Zq, W.uq, W.rq, 1, T, d, hd, cs, st);
-      if (e == cudaSuccess)
-        e = rope_gate_bwd_launch(W.dKr, 0, L.K, L.Zk, W.uk, W.rk, 1, T, d, hd, cs, st);
+      {  // Q and K sides in one launch
+        const void* drs[2] = {W.dQacc, W.dKr};
+        const void* xs[2] = {L.Q, L.K};
+        const void* zs[2] = {L.Zq, L.Zk};
+        void* us[2] = {W.uq, W.uk};
+        void* rs[2] = {W.rq, W.rk};
+        e = rope_gate_bwd_launch2(drs, xs, zs, us, rs, 2, 0, 1, T, d, hd, cs, st);
+      }
       if (e == cudaSuccess) {  // dQ = rq + uq W_qg^T ; dK = rk + uk W_kg^T
         GemmProblem g[2];
         const void* us[2] = {W.uq, W.uk};

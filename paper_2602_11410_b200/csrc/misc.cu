@@ -111,12 +111,27 @@ __global__ void __launch_bounds__(256) gate_rope_fwd_kernel(const __nv_bfloat16*
 // then out_u is unused and out_r (bf16 if r_bf16) receives dQt directly.
 // One thread = 8 consecutive columns (4 pairs) of one row: 16-byte accesses, (cos, sin) from the
 // rope table (cs, row stride hd + 32; null without RoPE).
-__global__ void __launch_bounds__(256) rope_gate_bwd_kernel(const void* dr, int dr_f32, const __nv_bfloat16* Xq,
-                                                            const __nv_bfloat16* Z, __nv_bfloat16* out_u,
-                                                            void* out_r, int r_bf16, int T, int d, int hd,
-                                                            const float* cs) {
+struct RgSide {
+  const void* dr;
+  const __nv_bfloat16* Xq;
+  const __nv_bfloat16* Z;
+  __nv_bfloat16* out_u;
+  void* out_r;
+};
+struct RgSides {
+  RgSide s[2];
+};
+// blockIdx.y = side (Q, K): both sides of A11 in one launch
+__global__ void __launch_bounds__(256) rope_gate_bwd_kernel(RgSides sides, int dr_f32, int r_bf16, int T, int d,
+                                                            int hd, const float* cs) {
   pdl_trigger();
   pdl_wait();
+  const RgSide& sd = sides.s[blockIdx.y];
+  const void* dr = sd.dr;
+  const __nv_bfloat16* Xq = sd.Xq;
+  const __nv_bfloat16* Z = sd.Z;
+  __nv_bfloat16* out_u = sd.out_u;
+  void* out_r = sd.out_r;
   const int per_row = d / 8;
   const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= (size_t)T * per_row) return;
@@ -373,14 +388,26 @@ cudaError_t rope_apply_launch(const void* in, void* out, int T, int d, int hd, c
                                                          reinterpret_cast<__nv_bfloat16*>(out), T, d, hd, cs);
   return cudaGetLastError();
 }
-cudaError_t rope_gate_bwd_launch(const void* dr, int dr_f32, const void* Xq, const void* Z, void* out_u, void* out_r,
-                                 int r_bf16, int T, int d, int hd, const float* cs, cudaStream_t st) {
+cudaError_t rope_gate_bwd_launch2(const void* const* dr, const void* const* Xq, const void* const* Z,
+                                  void* const* out_u, void* const* out_r, int nsides, int dr_f32, int r_bf16, int T,
+                                  int d, int hd, const float* cs, cudaStream_t st) {
+  if (nsides < 1 || nsides > 2) return cudaErrorInvalidValue;
+  RgSides sides;
+  for (int i = 0; i < 2; ++i) {
+    const int k = i < nsides ? i : 0;
+    sides.s[i] = RgSide{dr[k], reinterpret_cast<const __nv_bfloat16*>(Xq[k]), reinterpret_cast<const __nv_bfloat16*>(Z[k]),
+                        reinterpret_cast<__nv_bfloat16*>(out_u[k]), out_r[k]};
+  }
   ProfScope ps(PROF_OTHER, st, 1);
   const size_t work = (size_t)T * d / 8;
   if (work)
-    launch_pdl(rope_gate_bwd_kernel, dim3(blocks(work, 256)), dim3(256), 0, st, dr, dr_f32, reinterpret_cast<const __nv_bfloat16*>(Xq), reinterpret_cast<const __nv_bfloat16*>(Z),
-        reinterpret_cast<__nv_bfloat16*>(out_u), out_r, r_bf16, T, d, hd, cs);
+    launch_pdl(rope_gate_bwd_kernel, dim3(blocks(work, 256), nsides), dim3(256), 0, st, sides, dr_f32, r_bf16, T, d,
+               hd, cs);
   return cudaGetLastError();
+}
+cudaError_t rope_gate_bwd_launch(const void* dr, int dr_f32, const void* Xq, const void* Z, void* out_u, void* out_r,
+                                 int r_bf16, int T, int d, int hd, const float* cs, cudaStream_t st) {
+  return rope_gate_bwd_launch2(&dr, &Xq, &Z, &out_u, &out_r, 1, dr_f32, r_bf16, T, d, hd, cs, st);
 }
 cudaError_t gate_rope_fwd_launch(const void* Q, const void* K, const void* Gq, const void* Gk, const float* cs,
                                  void* Qr, void* Kr, int T, int d, int hd, cudaStream_t st) {

@@ -13,6 +13,10 @@ cudaError_t rope_apply_launch(const void* in, void* out, int T, int d, int hd, c
 // A4 elementwise half: Qr = RoPE(Q * sigma(Z_q)), Kr = RoPE(K * sigma(Z_k)) (Z stored by the gate GEMMs)
 cudaError_t gate_rope_fwd_launch(const void* Q, const void* K, const void* Gq, const void* Gk, const float* cs,
                                  void* Qr, void* Kr, int T, int d, int hd, cudaStream_t st);
+// both sides (Q and K) in one launch: arrays of nsides (<= 2) pointers
+cudaError_t rope_gate_bwd_launch2(const void* const* dr, const void* const* Xq, const void* const* Z,
+                                  void* const* out_u, void* const* out_r, int nsides, int dr_f32, int r_bf16, int T,
+                                  int d, int hd, const float* cs, cudaStream_t st);
 cudaError_t rope_gate_bwd_launch(const void* dr, int dr_f32, const void* Xq, const void* Z, void* out_u, void* out_r,
                                  int r_bf16, int T, int d, int hd, const float* cs, cudaStream_t st);
 // to_f16: the gathered rows are written as fp16 (the towers' GEMM operand)
