@@ -295,7 +295,16 @@ __global__ void __launch_bounds__(192, 2)
       uint32_t u[32];
       tmem_ld32(tmem_addr(tmem, quarter, C::O_COL + c * 32), u);
       tmem_ld_wait();
-      if (valid) {
+      if (!p.out_f32) {  // bf16 O through a per-warp transpose in the (now idle) Q tile: coalesced rows
+        uint32_t w[16];
+#pragma unroll
+        for (int q = 0; q < 16; ++q)
+          w[q] = pack_bf16(__uint_as_float(u[2 * q]) * inv_l, __uint_as_float(u[2 * q + 1]) * inv_l);
+        warp_store_rows_bf16(smem_u32(smem + C::Q_OFF) + (warp - 2) * 2048, w,
+                             reinterpret_cast<__nv_bfloat16*>(p.O) + (size_t)(q0 + quarter * 32) * p.d +
+                                 (size_t)h * p.hd + c * 32,
+                             p.d, rows_valid - (int)quarter * 32, min(32, p.hd - c * 32));
+      } else if (valid) {
         const size_t off = (size_t)r * p.d + (size_t)h * p.hd + c * 32;
         const int ncol = min(32, p.hd - c * 32);
         if (p.out_f32) {
@@ -304,16 +313,6 @@ __global__ void __launch_bounds__(192, 2)
             *reinterpret_cast<float4*>(o + q) =
                 make_float4(__uint_as_float(u[q]) * inv_l, __uint_as_float(u[q + 1]) * inv_l,
                             __uint_as_float(u[q + 2]) * inv_l, __uint_as_float(u[q + 3]) * inv_l);
-        } else {
-          __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(p.O) + off;
-          for (int q = 0; q < ncol; q += 8) {
-            uint4 v;
-            v.x = pack_bf16(__uint_as_float(u[q]) * inv_l, __uint_as_float(u[q + 1]) * inv_l);
-            v.y = pack_bf16(__uint_as_float(u[q + 2]) * inv_l, __uint_as_float(u[q + 3]) * inv_l);
-            v.z = pack_bf16(__uint_as_float(u[q + 4]) * inv_l, __uint_as_float(u[q + 5]) * inv_l);
-            v.w = pack_bf16(__uint_as_float(u[q + 6]) * inv_l, __uint_as_float(u[q + 7]) * inv_l);
-            *reinterpret_cast<uint4*>(o + q) = v;
-          }
         }
       }
     }
