@@ -262,3 +262,24 @@ def test_heads_forward_backward(ops, n_rows, T, d, K, dh):
     assert_close(gr[1].cpu().numpy(), g["db1"].reshape(-1), what="db1")
     assert_close(gr[2].cpu().numpy(), g["dw2"].reshape(-1), what="dw2")
     assert_close(gr[3].cpu().numpy(), g["db2"], what="db2")
+    # rows_in_ws = 1: the backward reuses the forward's fp16 gathered rows and W1 copy in ws
+    # (re-run the forward first: the first backward reused the slots); same results up to the
+    # fp32 atomic order of the logits (tower partial dots) and of the split-K dW1
+    L.check(L.lib().cadet_heads_forward(C.byref(hc), C.byref(hwst), C.c_void_p(Hd.data_ptr()),
+                                        C.c_void_p(tens["rows"].data_ptr()), n_rows, C.c_void_p(logits.data_ptr()),
+                                        C.c_void_p(pre.data_ptr()), C.c_void_p(ws.data_ptr()), ws.numel(), st))
+    hc1 = L.HeadConfig(K, d, dh, 0, 1)
+    dH1 = torch.empty_like(dH)
+    gr1 = [torch.empty_like(x) for x in gr]
+    hg1 = L.HeadGrads(*[x.data_ptr() for x in gr1])
+    L.check(L.lib().cadet_heads_loss_backward(C.byref(hc1), C.byref(hwst), C.c_void_p(Hd.data_ptr()),
+                                              C.c_void_p(tens["rows"].data_ptr()), n_rows, T,
+                                              C.c_void_p(logits.data_ptr()), C.c_void_p(pre.data_ptr()),
+                                              C.c_void_p(tens["bucket"].data_ptr()),
+                                              C.c_void_p(tens["label"].data_ptr()), C.c_void_p(loss.data_ptr()),
+                                              C.c_void_p(dH1.data_ptr()), C.byref(hg1), C.c_void_p(ws.data_ptr()),
+                                              ws.numel(), st))
+    torch.cuda.synchronize()
+    assert float((dH1.float() - dH.float()).abs().max()) <= 1e-2 * max(1e-3, float(dH.float().abs().max()))
+    for a_, b_ in zip(gr1, gr):
+        assert float((a_ - b_).abs().max()) <= 1e-5 * max(1.0, float(b_.abs().max()))
