@@ -35,21 +35,27 @@ __device__ __forceinline__ void rope_cs(double dt, double th, float& c, float& s
 // dt_row = t_row - t_(sequence start); row stride hd + 32 floats, the first 32 entries
 // repeated at [hd, hd + 32) so that any 32-float window starting at an even head-local column
 // is contiguous (a GEMM epilogue slice may cross one head edge when hd % 32 != 0).
-__global__ void rope_table_kernel(float* cs, int T, int hd, const double* theta, const int64_t* t,
-                                  const int32_t* row_seq, const int32_t* cu) {
+__global__ void __launch_bounds__(256) rope_table_kernel(float* cs, int T, int hd, const double* theta,
+                                                         const int64_t* t, const int32_t* row_seq,
+                                                         const int32_t* cu) {
   pdl_trigger();
   pdl_wait();
-  // one thread per (row, entry); T * (hd / 2 + 16) < 2^31 (host-checked), so 32-bit index math
+  // one warp per row: the row's rebased time is loaded once, theta_i from shared memory, each lane
+  // evaluates entries lane, lane + 32, ... of the row's hd / 2 + 16 (cos, sin) pairs
+  __shared__ double th[64];
   const int half = hd / 2, w = half + 16;
-  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= T * w) return;
-  const int row = idx / w, i = idx - row * w;
-  const int pr = i < half ? i : i - half;
+  for (int i = threadIdx.x; i < half; i += blockDim.x) th[i] = theta[i];
+  __syncthreads();
+  const int row = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (row >= T) return;
   const int s = row_seq[row];
   const double dt = s >= 0 ? (double)(t[row] - t[cu[s]]) : 0.0;
-  float c, sn;
-  rope_cs(dt, theta[pr], c, sn);
-  reinterpret_cast<float2*>(cs + (size_t)row * (hd + 32))[i] = make_float2(c, sn);
+  float2* out = reinterpret_cast<float2*>(cs + (size_t)row * (hd + 32));
+  for (int i = lane; i < w; i += 32) {
+    float c, sn;
+    rope_cs(dt, th[i < half ? i : i - half], c, sn);
+    out[i] = make_float2(c, sn);
+  }
 }
 
 // one thread per (row, pair of columns)
@@ -377,7 +383,8 @@ cudaError_t rope_table_launch(float* cs, int T, int hd, const double* theta, con
   ProfScope ps(PROF_OTHER, st, 1);
   const size_t work = (size_t)T * (hd / 2 + 16);
   if (work >= (size_t)INT32_MAX) return cudaErrorInvalidValue;
-  if (work) launch_pdl(rope_table_kernel, dim3(blocks(work, 256)), dim3(256), 0, st, cs, T, hd, theta, t, row_seq, cu);
+  if (hd / 2 > 64) return cudaErrorInvalidValue;
+  if (work) launch_pdl(rope_table_kernel, dim3((T + 7) / 8), dim3(256), 0, st, cs, T, hd, theta, t, row_seq, cu);
   return cudaGetLastError();
 }
 cudaError_t rope_apply_launch(const void* in, void* out, int T, int d, int hd, const float* cs, cudaStream_t st) {
