@@ -240,10 +240,11 @@ __device__ __forceinline__ int tile_seq(const PlanView& v, int n, int g) {
   return lo;
 }
 
+// one warp per tile: the 128 rows' visible-prefix ends are reduced across the lanes
 __global__ void __launch_bounds__(128) plan_tile_kernel(PlanArgs a, PlanView v) {
   pdl_trigger();
   pdl_wait();
-  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  const int g = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   const int nq_total = v.counters[0];
   if (g >= nq_total) return;
   const int s = tile_seq(v, a.n, g);
@@ -253,11 +254,17 @@ __global__ void __launch_bounds__(128) plan_tile_kernel(PlanArgs a, PlanView v) 
   const int nq_s = (len + TILE - 1) / TILE;
   const int r0 = sa + qt * TILE, r1 = min(sa + len, r0 + TILE);
   int emax = 0, emin = 1 << 30;
-  for (int r = r0; r < r1; ++r) {
+  for (int r = r0 + lane; r < r1; r += 32) {
     const int e = v.kv_end[r] - sa;
     emax = max(emax, e);
     emin = min(emin, e);
   }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    emax = max(emax, __shfl_xor_sync(0xffffffffu, emax, o));
+    emin = min(emin, __shfl_xor_sync(0xffffffffu, emin, o));
+  }
+  if (lane != 0) return;
   const int nf = min((emax + TILE - 1) / TILE, qt + 1);
   const int kt_pp = (qt > 0 && v.row_pp[r0]) ? qt - 1 : qt;
   const int kt2 = max(nf, kt_pp);
@@ -349,7 +356,7 @@ cudaError_t plan_launch(const PlanArgs& a, const PlanView& v, cudaStream_t st) {
   if (a.T > 0) launch_pdl(plan_row_kernel, dim3((a.T + 255) / 256), dim3(256), 0, st, a, v);
   const int nb = (v.nq_cap + 127) / 128;
   if (nb > 0) {
-    launch_pdl(plan_tile_kernel, dim3(nb), dim3(128), 0, st, a, v);
+    launch_pdl(plan_tile_kernel, dim3((v.nq_cap + 3) / 4), dim3(128), 0, st, a, v);
     launch_pdl(plan_order_kernel, dim3(1), dim3(1024), 0, st, v);
     launch_pdl(plan_scatter_kernel, dim3(nb), dim3(128), 0, st, a, v);
   }
