@@ -159,7 +159,6 @@ struct LayerBufs {  // carved from `saved`
   float* lse;
 };
 struct LayerWs {    // carved from `ws` after the plan
-  double* theta;
   float* rope_cs;   // [T][hd + 32] (cos, sin) table
   float* D;
   void *dO, *dKr, *dV, *uq, *uk, *dQ, *dK, *ux;
@@ -183,7 +182,7 @@ size_t saved_bytes(const cadet_attn_config* c, int T) {
 }
 size_t layer_ws_base_bytes(const cadet_attn_config* c, int n, int T) {
   const int d = c->d_model;
-  return plan_bytes(n, T, T) + a256(8 * 64) + a256((size_t)4 * T * (c->head_dim + 32)) +
+  return plan_bytes(n, T, T) + a256((size_t)4 * T * (c->head_dim + 32)) +
          a256((size_t)4 * c->n_heads * T) + 8 * bf_sz(T, d) + 4 * f_sz(T, d);
 }
 size_t layer_ws_bytes(const cadet_attn_config* c, int n, int T) {
@@ -204,8 +203,6 @@ LayerWs carve_ws(void* ws, const cadet_attn_config* c, int n, int T) {
   const int d = c->d_model;
   uint8_t* p = reinterpret_cast<uint8_t*>(ws) + plan_bytes(n, T, T);
   LayerWs W;
-  W.theta = reinterpret_cast<double*>(p);
-  p += a256(8 * 64);
   W.rope_cs = reinterpret_cast<float*>(p);
   p += a256((size_t)4 * T * (c->head_dim + 32));
   W.D = reinterpret_cast<float*>(p);
@@ -223,13 +220,14 @@ LayerWs carve_ws(void* ws, const cadet_attn_config* c, int n, int T) {
   return W;
 }
 
-// theta_i and the per-step (cos, sin) table (rope_table_kernel) into the layer workspace.
+// The per-step (cos, sin) table (rope_table_kernel) into the layer workspace.
 cudaError_t rope_prepare(const cadet_attn_config* cfg, const cadet_batch* b, const LayerWs& W, const PlanView& v,
                          cudaStream_t st) {
   const int hd = cfg->head_dim;
-  cudaError_t e = rope_theta_launch(W.theta, hd, cfg->rope_phi_min, cfg->rope_base, (double)cfg->rope_delta_t_max_ms, st);
-  if (e == cudaSuccess && cfg->use_rope)
-    e = rope_table_launch(W.rope_cs, b->total_tokens, hd, W.theta, b->timestamps_ms, v.row_seq, b->cu_seqlens, st);
+  cudaError_t e = cudaSuccess;
+  if (cfg->use_rope)
+    e = rope_table_launch(W.rope_cs, b->total_tokens, hd, cfg->rope_phi_min, cfg->rope_base,
+                          (double)cfg->rope_delta_t_max_ms, b->timestamps_ms, v.row_seq, b->cu_seqlens, st);
   return e;
 }
 

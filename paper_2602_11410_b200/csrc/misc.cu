@@ -1,7 +1,7 @@
 // Elementwise / reduction kernels of the hot path that are HBM-bound (no tensor cores):
-//   rope_theta_kernel       theta_i = (phi_min / dt_max) * base^(2i/hd)
-//   rope_table_kernel       (cos, sin)(dt_row theta_i) per (row, frequency), shared by every head
-//                           and by Q and K (forward epilogue and backward)
+//   rope_table_kernel       (cos, sin)(dt_row theta_i) per (row, frequency), theta_i = (phi_min /
+//                           dt_max) base^(2i/hd); shared by every head and by Q and K
+//   gate_rope_fwd_kernel    A4: Qr = RoPE(Q * sigma(Zq)), Kr = RoPE(K * sigma(Zk))
 //   rope_apply_kernel       RoPE without interaction gate (ablation path)
 //   rope_gate_bwd_kernel    A11: dQt = R(-alpha) dQr; g = sigma(Zq); u = dQt*Q*g*(1-g); r = dQt*g
 //   gather_rows_kernel      H_r = H[rows] (A7 operand)
@@ -15,12 +15,6 @@
 
 namespace cadet {
 
-__global__ void rope_theta_kernel(double* theta, int half, int hd, double phi_min, double base, double dt_max) {
-  pdl_trigger();
-  pdl_wait();
-  const int i = threadIdx.x + blockIdx.x * blockDim.x;
-  if (i < half) theta[i] = (phi_min / dt_max) * pow(base, 2.0 * i / (double)hd);
-}
 
 // alpha = dt * theta in fp64, reduced mod 2 pi in fp64 (|k| <= ~1e3: the 2 pi rounding error
 // k * 2.4e-16 is negligible), then MUFU sincos on r in [-pi, pi] (abs err ~5e-7).
@@ -35,8 +29,9 @@ __device__ __forceinline__ void rope_cs(double dt, double th, float& c, float& s
 // dt_row = t_row - t_(sequence start); row stride hd + 32 floats, the first 32 entries
 // repeated at [hd, hd + 32) so that any 32-float window starting at an even head-local column
 // is contiguous (a GEMM epilogue slice may cross one head edge when hd % 32 != 0).
-__global__ void __launch_bounds__(256) rope_table_kernel(float* cs, int T, int hd, const double* theta,
-                                                         const int64_t* t, const int32_t* row_seq,
+// theta_i = (phi_min / Delta t_max) base^(2i / hd), evaluated per block into shared memory
+__global__ void __launch_bounds__(256) rope_table_kernel(float* cs, int T, int hd, double phi_min, double base,
+                                                         double dt_max, const int64_t* t, const int32_t* row_seq,
                                                          const int32_t* cu) {
   pdl_trigger();
   pdl_wait();
@@ -44,7 +39,7 @@ __global__ void __launch_bounds__(256) rope_table_kernel(float* cs, int T, int h
   // evaluates entries lane, lane + 32, ... of the row's hd / 2 + 16 (cos, sin) pairs
   __shared__ double th[64];
   const int half = hd / 2, w = half + 16;
-  for (int i = threadIdx.x; i < half; i += blockDim.x) th[i] = theta[i];
+  for (int i = threadIdx.x; i < half; i += blockDim.x) th[i] = (phi_min / dt_max) * pow(base, 2.0 * i / (double)hd);
   __syncthreads();
   const int row = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (row >= T) return;
@@ -373,18 +368,15 @@ __global__ void add_bf16_kernel(const __nv_bfloat16* a, const __nv_bfloat16* b, 
 // ---------------------------------------------------------------- launchers
 static inline unsigned blocks(size_t n, unsigned b) { return (unsigned)((n + b - 1) / b); }
 
-cudaError_t rope_theta_launch(double* theta, int hd, double phi_min, double base, double dt_max, cudaStream_t st) {
-  ProfScope ps(PROF_OTHER, st, 1);
-  launch_pdl(rope_theta_kernel, dim3(1), dim3(128), 0, st, theta, hd / 2, hd, phi_min, base, dt_max);
-  return cudaGetLastError();
-}
-cudaError_t rope_table_launch(float* cs, int T, int hd, const double* theta, const int64_t* t, const int32_t* row_seq,
-                              const int32_t* cu, cudaStream_t st) {
+cudaError_t rope_table_launch(float* cs, int T, int hd, double phi_min, double base, double dt_max, const int64_t* t,
+                              const int32_t* row_seq, const int32_t* cu, cudaStream_t st) {
   ProfScope ps(PROF_OTHER, st, 1);
   const size_t work = (size_t)T * (hd / 2 + 16);
   if (work >= (size_t)INT32_MAX) return cudaErrorInvalidValue;
   if (hd / 2 > 64) return cudaErrorInvalidValue;
-  if (work) launch_pdl(rope_table_kernel, dim3((T + 7) / 8), dim3(256), 0, st, cs, T, hd, theta, t, row_seq, cu);
+  if (work)
+    launch_pdl(rope_table_kernel, dim3((T + 7) / 8), dim3(256), 0, st, cs, T, hd, phi_min, base, dt_max, t, row_seq,
+               cu);
   return cudaGetLastError();
 }
 cudaError_t rope_apply_launch(const void* in, void* out, int T, int d, int hd, const float* cs, cudaStream_t st) {

@@ -5,10 +5,9 @@
 #include <stdint.h>
 
 namespace cadet {
-cudaError_t rope_theta_launch(double* theta, int hd, double phi_min, double base, double dt_max, cudaStream_t st);
 // (cos, sin) table [T][hd + 32] floats (see rope_table_kernel); cs = null means no RoPE
-cudaError_t rope_table_launch(float* cs, int T, int hd, const double* theta, const int64_t* t, const int32_t* row_seq,
-                              const int32_t* cu, cudaStream_t st);
+cudaError_t rope_table_launch(float* cs, int T, int hd, double phi_min, double base, double dt_max, const int64_t* t,
+                              const int32_t* row_seq, const int32_t* cu, cudaStream_t st);
 cudaError_t rope_apply_launch(const void* in, void* out, int T, int d, int hd, const float* cs, cudaStream_t st);
 // A4 elementwise half: Qr = RoPE(Q * sigma(Z_q)), Kr = RoPE(K * sigma(Z_k)) (Z stored by the gate GEMMs)
 cudaError_t gate_rope_fwd_launch(const void* Q, const void* K, const void* Gq, const void* Gk, const float* cs,
