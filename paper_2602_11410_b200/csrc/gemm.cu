@@ -274,7 +274,7 @@ template <uint32_t MODES>
 __device__ __forceinline__ void run_epilogue_warp(const EpiParams& e, int row0, int M, int n0c, float (&v)[32],
                                                   uint32_t stg, const uint4* pre = nullptr) {
   const int lane = threadIdx.x & 31;
-  if (e.row_map || e.mode == EPI_ATOMIC || e.mode == EPI_HEAD) {
+  if (e.row_map || e.mode == EPI_ATOMIC) {
     run_epilogue<MODES>(e, row0 + lane, M, n0c, v);
     return;
   }
@@ -348,6 +348,35 @@ __device__ __forceinline__ void run_epilogue_warp(const EpiParams& e, int row0, 
       }
       warp_store_rows(stg, e.out, e.out_f32, off0, e.ldo, rows_valid, v);
       warp_store_rows(stg, e.out2, e.out2_f32, off0, e.ldo, rows_valid, r);
+    } break;
+    case EPI_HEAD: if constexpr (HAS_MODE(EPI_HEAD)) {
+      // pre = acc + b1 (saved through the warp transpose), logits[row, k] += relu(pre) . w2; a
+      // 32-column slice covers at most two towers when dh % 32 != 0 (dh >= 32)
+      const int k0 = n0c / e.hd;
+      const int split = (k0 + 1) * e.hd - n0c;
+      const float4* b4 = reinterpret_cast<const float4*>(e.b1 + n0c);
+      const float4* w4 = reinterpret_cast<const float4*>(e.w2 + n0c);
+      float part0 = 0.f, part1 = 0.f;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const float4 bb = b4[q], ww = w4[q];
+        const float bv[4] = {bb.x, bb.y, bb.z, bb.w}, wv[4] = {ww.x, ww.y, ww.z, ww.w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int j = 4 * q + k;
+          v[j] += bv[k];
+          const float c = fmaxf(v[j], 0.f) * wv[k];
+          if (j < split)
+            part0 += c;
+          else
+            part1 += c;
+        }
+      }
+      if (e.aux) warp_store_rows(stg, e.aux, e.aux_f32, off0, e.ldo, rows_valid, v);
+      if (lane < rows_valid) {
+        atomicAdd(e.logits + (size_t)(row0 + lane) * e.n_towers + k0, part0);
+        if (split < 32) atomicAdd(e.logits + (size_t)(row0 + lane) * e.n_towers + k0 + 1, part1);
+      }
     } break;
     case EPI_GELU: if constexpr (HAS_MODE(EPI_GELU)) {
       if (e.aux) warp_store_rows(stg, e.aux, e.aux_f32, off0, e.ldo, rows_valid, v);
