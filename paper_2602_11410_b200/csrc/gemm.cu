@@ -274,7 +274,7 @@ template <uint32_t MODES>
 __device__ __forceinline__ void run_epilogue_warp(const EpiParams& e, int row0, int M, int n0c, float (&v)[32],
                                                   uint32_t stg, const uint4* pre = nullptr) {
   const int lane = threadIdx.x & 31;
-  if (e.row_map || e.mode == EPI_ATOMIC) {
+  if (e.row_map) {
     run_epilogue<MODES>(e, row0 + lane, M, n0c, v);
     return;
   }
@@ -348,6 +348,25 @@ __device__ __forceinline__ void run_epilogue_warp(const EpiParams& e, int row0, 
       }
       warp_store_rows(stg, e.out, e.out_f32, off0, e.ldo, rows_valid, v);
       warp_store_rows(stg, e.out2, e.out2_f32, off0, e.ldo, rows_valid, r);
+    } break;
+    case EPI_ATOMIC: if constexpr (HAS_MODE(EPI_ATOMIC)) {
+      // split-K partials: transpose through the stage, then fp32 vector reductions that cover 4 rows
+      // x 128 B per instruction (instead of 32 rows x 16 B)
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        sts_u4(stg + lane * 128 + ((j ^ (lane & 7)) << 4), __float_as_uint(v[4 * j]), __float_as_uint(v[4 * j + 1]),
+               __float_as_uint(v[4 * j + 2]), __float_as_uint(v[4 * j + 3]));
+      __syncwarp();
+      float* base = reinterpret_cast<float*>(e.out) + off0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int row = i * 4 + (lane >> 3), j = lane & 7;
+        const uint4 u = lds_u4(stg + row * 128 + ((j ^ (row & 7)) << 4));
+        if (row < rows_valid)
+          atomicAdd(reinterpret_cast<float4*>(base + (size_t)row * e.ldo + j * 4),
+                    make_float4(__uint_as_float(u.x), __uint_as_float(u.y), __uint_as_float(u.z), __uint_as_float(u.w)));
+      }
+      __syncwarp();
     } break;
     case EPI_HEAD: if constexpr (HAS_MODE(EPI_HEAD)) {
       // pre = acc + b1 (saved through the warp transpose), logits[row, k] += relu(pre) . w2; a
