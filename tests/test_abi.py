@@ -55,3 +55,35 @@ def test_host_validation_errors_without_gpu():
     c.dtype = 1
     assert L.cadet_mask_plan(C.byref(c), C.byref(b), None, 0, None) == 9
     assert L.cadet_gemm(0, 32, 32, None, 0, None, 0, None, 1, None, None) == 1
+
+
+def test_next_rows_host_validation_and_size_queries_without_gpu():
+    """NEXT-3 / NEXT-4 / two-pass backward entry points: argument errors are host-detected and
+    returned synchronously (no CUDA call), and the size queries follow their documented formulas."""
+    import ctypes as C
+    from paper_2602_11410_b200 import _lib
+    L = _lib.lib()
+    E_ARG = 1
+    # RMSNorm: d % 8 == 0 and d <= 1024
+    g = C.c_void_p(256)  # never dereferenced: the call fails before any device work
+    assert L.cadet_rmsnorm_forward(g, g, 4, 1025, g, g, None) == E_ARG
+    assert L.cadet_rmsnorm_forward(g, g, 4, 12, g, g, None) == E_ARG
+    assert L.cadet_rmsnorm_backward(g, None, g, g, None, 4, 64, g, g, None) == E_ARG   # gamma null
+    # FFN: d % 32 == 0, weights non-null
+    assert L.cadet_ffn_forward(g, g, g, None, 4, 48, 4, g, g, g, None) == E_ARG
+    assert L.cadet_ffn_forward(g, None, g, None, 4, 64, 4, g, g, g, None) == E_ARG
+    assert L.cadet_ffn_workspace_bytes(1000, 256, 4) == -(-1000 * 256 * 4 * 2 // 256) * 256
+    # AdamW: step >= 1 and 16-byte-aligned fp32 buffers
+    cfg = _lib.AdamWConfig()
+    L.cadet_default_adamw_config(C.byref(cfg))
+    assert abs(cfg.lr - 1e-4) < 1e-9 and abs(cfg.beta2 - 0.999) < 1e-7 and cfg.weight_decay == 0.0
+    assert L.cadet_adamw_step(C.byref(cfg), 0, g, g, g, g, None, 16, None) == E_ARG
+    assert L.cadet_adamw_step(C.byref(cfg), 1, C.c_void_p(260), g, g, g, None, 16, None) == E_ARG
+    assert L.cadet_bf16_to_f32(C.c_void_p(264), g, 8, None) == E_ARG
+    # two-pass backward region: dS^T slots bounded like the plan's visit lists, times H x 32 KB
+    c = _lib.default_config(1024, 8)
+    n, T, L_max = 136, 65536, 2048
+    nq, hm = (T + 127) // 128 + n, (L_max + 127) // 128 + 3
+    slots = nq * (hm + 1) // 2 + hm
+    assert L.cadet_attn_bwd_ds_bytes(C.byref(c), n, T, L_max) == -(-slots * 8 * 128 * 128 * 2 // 256) * 256
+    assert L.cadet_attn_bwd_ds_bytes(C.byref(c), n, T, 1 << 30) == 0   # bound overflows: no region
