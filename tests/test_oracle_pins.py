@@ -72,6 +72,68 @@ def test_candidate_pattern_example():
     assert (A[:3, :3] == np.tril(np.ones((3, 3), bool))).all()
 
 
+def _fixture(name):
+    """Golden mask fixture: 'key v v ...' header lines, then 0/1 rows (hand-worked, cited inside)."""
+    meta, rows = {}, []
+    for line in _read_bits(name):
+        parts = line.split()
+        if parts[0][0].isalpha():
+            meta[parts[0]] = [int(v) for v in parts[1:]]
+        else:
+            rows.append(line)
+    return meta, np.array([[c == "1" for c in r] for r in rows])
+
+
+def test_session_mask_hand_worked():
+    """R10 reading of P:288-290 (same-session information hidden): SESSION-only rule, by hand."""
+    meta, want = _fixture("session_mask.txt")
+    m = len(meta["sessions"])
+    cfg = O.AttnConfig(d_model=2, n_heads=1, mask_flags=O.MASK_SESSION)
+    A = O.mask_dense(np.zeros(m, np.int64), 0, cfg, session_ids=np.array(meta["sessions"]))
+    assert (A == want).all()
+
+
+def test_session_and_time_rules_combine_by_and():
+    """Both flags = AND of Eq. 6 and the session rule (R10), by hand."""
+    meta, want = _fixture("session_time_and.txt")
+    cfg = O.AttnConfig(d_model=2, n_heads=1, mask_flags=O.MASK_TIME | O.MASK_SESSION,
+                       delta_delay_ms=meta["delta"][0])
+    A = O.mask_dense(np.array(meta["times"]), 0, cfg, session_ids=np.array(meta["sessions"]))
+    assert (A == want).all()
+    # each rule alone is a superset of the combination
+    At = O.mask_dense(np.array(meta["times"]), 0, dataclasses.replace(cfg, mask_flags=O.MASK_TIME))
+    As = O.mask_dense(np.array(meta["times"]), 0, dataclasses.replace(cfg, mask_flags=O.MASK_SESSION),
+                      session_ids=np.array(meta["sessions"]))
+    assert (A == (At & As)).all() and not (A == At).all() and not (A == As).all()
+
+
+def test_pair_prev_exception_hand_worked():
+    """S:310 (action token sees its own impression; reading R12), by hand; without the flag the
+    paper-literal rule hides exactly the flagged i-1 cells."""
+    meta, want = _fixture("pair_prev_mask.txt")
+    t, fl = np.array(meta["times"]), np.array(meta["flags"], np.uint8)
+    cfg = O.AttnConfig(d_model=2, n_heads=1, mask_flags=O.MASK_TIME | O.MASK_PAIR_PREV,
+                       delta_delay_ms=meta["delta"][0])
+    A = O.mask_dense(t, 0, cfg, pair_flags=fl)
+    assert (A == want).all()
+    Alit = O.mask_dense(t, 0, dataclasses.replace(cfg, mask_flags=O.MASK_TIME))
+    diff = {(i, j) for i in range(len(t)) for j in range(len(t)) if A[i, j] != Alit[i, j]}
+    assert diff == {(1, 0), (3, 2), (5, 4)}
+    # canonical kv_end (R24) is taken from the mask WITHOUT the exception: the prefix ends
+    assert list(O.kv_end_local(Alit)) == [0, 0, 2, 2, 2, 2]
+
+
+def test_static_prefix_always_visible_hand_worked():
+    """S:319 / R13: the static prefix M (Eq. 1) is visible to every context query."""
+    meta, want = _fixture("static_prefix_mask.txt")
+    cfg = O.AttnConfig(d_model=2, n_heads=1, mask_flags=O.MASK_TIME, delta_delay_ms=meta["delta"][0])
+    A = O.mask_dense(np.array(meta["times"]), 0, cfg, n_static=meta["n_static"][0])
+    assert (A == want).all()
+    # n_static = 0 leaves only the diagonal (all timestamps equal, Delta > 0)
+    A0 = O.mask_dense(np.array(meta["times"]), 0, cfg, n_static=0)
+    assert (A0 == np.eye(len(meta["times"]), dtype=bool)).all()
+
+
 @pytest.mark.parametrize("L,N", [(0, 1), (1, 0), (3, 2), (7, 5), (16, 9), (40, 0), (33, 17)])
 def test_pair_count_closed_form(L, N):
     """allowed pairs of the inference pattern = L(L+1)/2 + N(L+1) (brute count)."""
