@@ -44,7 +44,7 @@ typedef struct CUstream_st* cadet_stream_t; /* == cudaStream_t; NULL = legacy de
 
 typedef enum {
   CADET_OK = 0,
-  CADET_E_ARG = 1,         /* null pointer / bad shape: d % H, odd head_dim, head_dim > 128, d % 32 ("dimension error") */
+  CADET_E_ARG = 1,         /* null pointer / bad shape: d % H, head_dim not in {32,64,88,96,128}, H > 128, d % 32 ("dimension error") */
   CADET_E_OFFSETS = 2,     /* cu_seqlens[0] != 0, empty or decreasing sequence, cu[n] > T          (device) */
   CADET_E_ORDER = 3,       /* timestamps or session ids decrease inside a sequence ("ordering error") (device) */
   CADET_E_TOO_LONG = 4,    /* a sequence longer than max_seqlen or the budget: chunk first          (device) */
@@ -70,11 +70,16 @@ enum {
 
 typedef struct {
   int32_t d_model;   /* d, multiple of 32 */
-  int32_t n_heads;   /* H; head_dim = d / H must be in {32, 64, 88, 96, 128} (even, <= 128) */
+  int32_t n_heads;   /* H <= 128; head_dim = d / H must be one of {32, 64, 88, 96, 128} (else CADET_E_ARG) */
   int32_t head_dim;  /* must equal d_model / n_heads */
   int32_t dtype;     /* CADET_BF16 (bf16 operands, fp32 accumulation); CADET_FP32 -> CADET_E_UNSUPPORTED in v1 */
   int32_t mask_flags;
-  int32_t out_f32;   /* core calls: 1 = write O / dQr / dKr / dV as fp32 (parity protocol, SURVEY 8(c) iii) */
+  int32_t out_f32;   /* core calls: 1 = write O / dQr / dKr / dV as fp32 (parity protocol, SURVEY 8(c) iii).
+                        layer calls: 1 = ALSO write every stage's fp32 value before its bf16 rounding into the
+                        tap region of ws (cadet_attn_workspace_bytes grows by CADET_N_TAPS * T * d * 4 B;
+                        pointers from cadet_attn_stage_views); the bf16 results are unchanged.  The attention
+                        taps (O, dQr, dKr, dV) come from a second run of the same deterministic kernels with
+                        fp32 stores.  Parity / debugging only (about 2x the layer's time). */
   int32_t use_rope, use_rep_gate, use_int_gate, use_out_proj; /* ablation switches (Table 1) */
   int32_t deterministic; /* reserved, must be 0 (attention fwd/bwd are atomic-free and deterministic; split-K
                             weight gradients accumulate with fp32 atomics) */
@@ -206,6 +211,33 @@ cadet_status cadet_attn_backward_ev(const cadet_attn_config* cfg_h, const cadet_
                                     const cadet_attn_weights* w_h, const void* X, const void* saved, const void* dY,
                                     void* dX, const void* dresid, const cadet_attn_grads* g_h, void* ws,
                                     size_t ws_bytes, cadet_stream_t stream, void* const* grad_events);
+
+/* ------------------------------------------------------------------ parity views of the layer (SURVEY 8(c) iii)
+ * Stage-by-stage parity needs (a) each stage's value before its bf16 storage rounding and (b) the bf16
+ * tensors the next stage consumed.  cadet_attn_stage_views fills views_h[CADET_N_VIEWS] (host array of
+ * device pointers into ws, the layer workspace of cadet_attn_forward / cadet_attn_backward with the
+ * same cfg, n_seqs and T):
+ *   [CADET_TAP_*]  fp32 [T, d] taps, written by the layer calls only when cfg.out_f32 = 1 (else NULL);
+ *                  ablated stages are not written;
+ *   [CADET_WS_*]   bf16 [T, d] backward intermediates (valid after cadet_attn_backward) and D fp32 [H, T].
+ * The forward's bf16 stage outputs are in `saved` (Zx, X~, Q, K, Zq, Zk, Qr, Kr, V, O, LSE; see above). */
+enum {
+  /* forward (A2-A6): Z_x = X W_xg, X~, Q, K, V, Z_q, Z_k, Q_r, K_r, O, Y */
+  CADET_TAP_ZX = 0, CADET_TAP_XT, CADET_TAP_Q, CADET_TAP_K, CADET_TAP_V, CADET_TAP_ZQ, CADET_TAP_ZK, CADET_TAP_QR,
+  CADET_TAP_KR, CADET_TAP_O, CADET_TAP_Y,
+  /* backward (A9-A12): dO = dY W_o^T, dQ_r, dK_r, dV (attention), u_q, r_q, u_k, r_k (A11 elementwise:
+     u = R(-a) dQ_r * Q * g (1 - g), r = R(-a) dQ_r * g), dQ = r_q + u_q W_qg^T, dK, u_x, r_x (A12 gate
+     backward of dX~), dX */
+  CADET_TAP_DO, CADET_TAP_DQR, CADET_TAP_DKR, CADET_TAP_DV, CADET_TAP_UQ, CADET_TAP_RQ, CADET_TAP_UK, CADET_TAP_RK,
+  CADET_TAP_DQ, CADET_TAP_DK, CADET_TAP_UX, CADET_TAP_RX, CADET_TAP_DX,
+  CADET_N_TAPS,
+  /* bf16 backward intermediates in ws, then D = rowsum(dO * O) per head (fp32 [H, T]) */
+  CADET_WS_DO = 32, CADET_WS_DQR, CADET_WS_DKR, CADET_WS_DV, CADET_WS_UQ, CADET_WS_RQ, CADET_WS_UK, CADET_WS_RK,
+  CADET_WS_DQ, CADET_WS_DK, CADET_WS_UX, CADET_WS_RX, CADET_WS_D,
+  CADET_N_VIEWS
+};
+cadet_status cadet_attn_stage_views(const cadet_attn_config* cfg_h, int32_t n_seqs, int32_t total_tokens, void* ws,
+                                    size_t ws_bytes, void** views_h);
 
 /* ------------------------------------------------------------------ A7 / A8: towers + routed loss (Eqs. 8-9)
  * Hs: bf16 [T, d] transformer output; rows: int32 [n] packed row index of each scored token

@@ -13,6 +13,15 @@ CADET_MASK_TIME = 1
 CADET_MASK_SESSION = 2
 CADET_MASK_PAIR_PREV = 4
 
+# cadet_attn_stage_views indices (include/cadet.h)
+TAP_NAMES = ["Zx", "Xt", "Q", "K", "V", "Zq", "Zk", "Qr", "Kr", "O", "Y", "dO", "dQr", "dKr", "dV", "uq", "rq", "uk",
+             "rk", "dQ", "dK", "ux", "rx", "dX"]
+CADET_N_TAPS = 24
+WS_NAMES = ["dO", "dQr", "dKr", "dV", "uq", "rq", "uk", "rk", "dQ", "dK", "ux", "rx"]
+CADET_WS_DO = 32
+CADET_WS_D = 44
+CADET_N_VIEWS = 45
+
 STATUS = {0: "CADET_OK", 1: "CADET_E_ARG", 2: "CADET_E_OFFSETS", 3: "CADET_E_ORDER", 4: "CADET_E_TOO_LONG",
           5: "CADET_E_CAND", 6: "CADET_E_BUCKET", 7: "CADET_E_NONFINITE", 8: "CADET_E_WORKSPACE",
           9: "CADET_E_UNSUPPORTED", 10: "CADET_E_CUDA"}
@@ -90,6 +99,7 @@ SIGNATURES = {
     "cadet_attn_saved_bytes": (SZ, [PCFG, I32]),
     "cadet_attn_bwd_ds_bytes": (SZ, [C.POINTER(AttnConfig), I32, I32, I32]),
     "cadet_heads_workspace_bytes": (SZ, [C.POINTER(HeadConfig), I32]),
+    "cadet_attn_stage_views": (I32, [PCFG, I32, I32, P, SZ, C.POINTER(C.c_void_p)]),
     "cadet_mask_plan": (I32, [PCFG, PB, P, SZ, P]),
     "cadet_mask_export": (I32, [PCFG, PB, P, P, P, I64, P, P]),
     "cadet_attn_core_forward": (I32, [PCFG, PB, P, P, P, P, P, P, SZ, P]),

@@ -107,7 +107,6 @@ __global__ void __launch_bounds__(320, 1)
                        const AttnParams p) {
   using G = HeadGeom<HD>;
   using C = DqCfg<HD>;
-  pdl_trigger();
   if (threadIdx.x == 0) { TR(0, 0, gtime()); TR(0, 4, smid()); }
 
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -136,6 +135,7 @@ __global__ void __launch_bounds__(320, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = bars->tmem_base;
+  pdl_trigger();  // after the TMEM allocation: a dependent CTA never takes this CTA's columns first
   pdl_wait();  // everything below reads the previous kernels' outputs
   const int n_work = p.plan.counters[0] * p.H;
 
@@ -407,7 +407,6 @@ __global__ void __launch_bounds__(320, 1)
                         const AttnParams p) {
   using G = HeadGeom<HD>;
   using C = DkvCfg<HD>;
-  pdl_trigger();
   if (threadIdx.x == 0) { TR(1, 0, gtime()); TR(1, 4, smid()); }
 
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -435,6 +434,7 @@ __global__ void __launch_bounds__(320, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = bars->tmem_base;
+  pdl_trigger();  // after the TMEM allocation: a dependent CTA never takes this CTA's columns first
   pdl_wait();  // everything below reads the previous kernels' outputs
   const int n_work = p.plan.counters[0] * p.H;
   const int32_t* list = p.plan.bwd_list;
@@ -731,7 +731,6 @@ __global__ void __launch_bounds__(192, 1)
                         const AttnParams p) {
   using G = HeadGeom<HD>;
   using C = Dq2Cfg<HD>;
-  pdl_trigger();
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   Dq2Bars* bars = reinterpret_cast<Dq2Bars*>(smem + C::BAR_OFF);
@@ -752,6 +751,7 @@ __global__ void __launch_bounds__(192, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = bars->tmem_base;
+  pdl_trigger();  // after the TMEM allocation: a dependent CTA never takes this CTA's columns first
   pdl_wait();  // everything below reads the previous kernels' outputs
   const int n_work = p.plan.counters[0] * p.H;
 

@@ -57,7 +57,6 @@ __global__ void __launch_bounds__(192, 2)
                     const __grid_constant__ CUtensorMap mV, const AttnParams p) {
   using G = HeadGeom<HD>;
   using C = FwdCfg<HD>;
-  pdl_trigger();
   pdl_wait();  // not persistent: the whole kernel reads the previous kernels' outputs
   const int nq_total = p.plan.counters[0];
   const int S = p.fwd_splits;
@@ -95,6 +94,7 @@ __global__ void __launch_bounds__(192, 2)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = bars->tmem_base;
+  pdl_trigger();  // after the TMEM allocation: a dependent CTA never takes this CTA's columns first
 
   if (warp == 0) {
     // ============================ producer

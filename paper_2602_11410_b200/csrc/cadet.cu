@@ -42,7 +42,11 @@ cadet_status check_cfg(const cadet_attn_config* c) {
     return fail(CADET_E_ARG, "d_model %d not divisible by n_heads %d", c->d_model, c->n_heads);
   const int hd = c->d_model / c->n_heads;
   if (c->head_dim != hd) return fail(CADET_E_ARG, "head_dim %d != d_model / n_heads = %d", c->head_dim, hd);
-  if (hd % 8 || hd > 128 || hd < 8) return fail(CADET_E_ARG, "head_dim %d must be a multiple of 8 in [8, 128]", hd);
+  // the kernels are built and parity-tested for these head dims (88 runs padded to 96 by TMA zero-fill)
+  if (hd != 32 && hd != 64 && hd != 88 && hd != 96 && hd != 128)
+    return fail(CADET_E_ARG, "head_dim %d must be one of 32, 64, 88, 96, 128", hd);
+  // per-row head sums (attn_bwd_pre_kernel) and the per-head plan arrays hold at most 128 heads
+  if (c->n_heads > 128) return fail(CADET_E_ARG, "n_heads %d > 128", c->n_heads);
   if (c->d_model % 32) return fail(CADET_E_ARG, "d_model %d must be a multiple of 32", c->d_model);
   if (c->dtype != CADET_BF16) return fail(CADET_E_UNSUPPORTED, "dtype %d not supported (bf16 only in v1)", c->dtype);
   if (c->deterministic) return fail(CADET_E_UNSUPPORTED, "deterministic mode not implemented in v1");

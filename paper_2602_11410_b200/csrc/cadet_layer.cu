@@ -158,11 +158,17 @@ struct LayerBufs {  // carved from `saved`
   void *Zx, *Xt, *Q, *K, *Zq, *Zk, *Qr, *Kr, *V, *O;
   float* lse;
 };
+// Parity taps (cfg.out_f32 = 1 on the layer calls): fp32 [T, d] copies of every stage's value before
+// its bf16 rounding, in the order of the CADET_TAP_* views of include/cadet.h.
+enum { TAP_ZX, TAP_XT, TAP_Q, TAP_K, TAP_V, TAP_ZQ, TAP_ZK, TAP_QR, TAP_KR, TAP_O, TAP_Y, TAP_DO, TAP_DQR, TAP_DKR,
+       TAP_DV, TAP_UQ, TAP_RQ, TAP_UK, TAP_RK, TAP_DQ, TAP_DK, TAP_UX, TAP_RX, TAP_DX, N_TAPS };
+static_assert(N_TAPS == CADET_N_TAPS, "tap list out of sync with cadet.h");
 struct LayerWs {    // carved from `ws` after the plan
   float* rope_cs;   // [T][hd + 32] (cos, sin) table
   float* D;
   void *dO, *dKr, *dV, *uq, *uk, *dQ, *dK, *ux;
   float *dQacc, *rq, *rk, *rx;
+  float* tap[N_TAPS];  // all null unless cfg.out_f32
 };
 
 size_t bf_sz(int T, int d) { return a256((size_t)T * d * 2); }
@@ -183,7 +189,7 @@ size_t saved_bytes(const cadet_attn_config* c, int T) {
 size_t layer_ws_base_bytes(const cadet_attn_config* c, int n, int T) {
   const int d = c->d_model;
   return plan_bytes(n, T, T) + a256((size_t)4 * T * (c->head_dim + 32)) +
-         a256((size_t)4 * c->n_heads * T) + 8 * bf_sz(T, d) + 4 * f_sz(T, d);
+         a256((size_t)4 * c->n_heads * T) + 8 * bf_sz(T, d) + 4 * f_sz(T, d) + (c->out_f32 ? N_TAPS * f_sz(T, d) : 0);
 }
 size_t layer_ws_bytes(const cadet_attn_config* c, int n, int T) {
   return layer_ws_base_bytes(c, n, T) + fwd_split_bytes(c, n, T);
@@ -216,6 +222,10 @@ LayerWs carve_ws(void* ws, const cadet_attn_config* c, int n, int T) {
   for (int i = 0; i < 4; ++i) {
     *fp[i] = reinterpret_cast<float*>(p);
     p += f_sz(T, d);
+  }
+  for (int i = 0; i < N_TAPS; ++i) {
+    W.tap[i] = c->out_f32 ? reinterpret_cast<float*>(p) : nullptr;
+    if (c->out_f32) p += f_sz(T, d);
   }
   return W;
 }
@@ -308,6 +318,25 @@ size_t cadet_attn_saved_bytes(const cadet_attn_config* c, int32_t T) {
   return saved_bytes(c, T);
 }
 
+cadet_status cadet_attn_stage_views(const cadet_attn_config* cfg, int32_t n, int32_t T, void* ws, size_t ws_bytes,
+                                    void** views_h) {
+  cadet_status s = check_cfg(cfg);
+  if (s) return s;
+  if (!ws || !views_h || n < 0 || T < 0) {
+    set_error("cadet_attn_stage_views: null pointer or negative size");
+    return CADET_E_ARG;
+  }
+  const size_t need = layer_ws_bytes(cfg, n, T);
+  if (ws_bytes < need) return ws_err(ws_bytes, need);
+  LayerWs W = carve_ws(ws, cfg, n, T);
+  for (int i = 0; i < CADET_N_VIEWS; ++i) views_h[i] = nullptr;
+  for (int i = 0; i < N_TAPS; ++i) views_h[i] = W.tap[i];
+  void* bf[12] = {W.dO, W.dQacc, W.dKr, W.dV, W.uq, W.rq, W.uk, W.rk, W.dQ, W.dK, W.ux, W.rx};
+  for (int i = 0; i < 12; ++i) views_h[CADET_WS_DO + i] = bf[i];
+  views_h[CADET_WS_D] = W.D;
+  return CADET_OK;
+}
+
 cadet_status cadet_attn_forward(const cadet_attn_config* cfg, const cadet_batch* b, const cadet_attn_weights* w,
                                 const void* X, void* Y, const void* resid, void* saved, void* ws, size_t ws_bytes,
                                 cadet_stream_t stream) {
@@ -337,6 +366,8 @@ cadet_status cadet_attn_forward(const cadet_attn_config* cfg, const cadet_batch*
     g.epi.out = L.Xt;
     g.epi.src = X;
     g.epi.aux = L.Zx;
+    g.epi.tap = W.tap[TAP_XT];
+    g.epi.tap2 = W.tap[TAP_ZX];
     e = gemm_launch(&g, 1, bn, st);
     Xt = L.Xt;
   }
@@ -348,6 +379,7 @@ cadet_status cadet_attn_forward(const cadet_attn_config* cfg, const cadet_batch*
     for (int i = 0; i < 3; ++i) {
       g[i] = prob(T, d, d, act(Xt, T, d), w_fwd(Ws[i], d, d), EPI_STORE);
       g[i].epi.out = outs[i];
+      g[i].epi.tap = W.tap[TAP_Q + i];
     }
     e = gemm_launch(g, 3, bn, st);
   }
@@ -364,10 +396,12 @@ cadet_status cadet_attn_forward(const cadet_attn_config* cfg, const cadet_batch*
       for (int i = 0; i < 2; ++i) {
         g[i] = prob(T, d, d, act(src[i], T, d), w_fwd(Ws[i], d, d), EPI_STORE);
         g[i].epi.out = zs[i];
+        g[i].epi.tap = W.tap[TAP_ZQ + i];
       }
       e = gemm_launch(g, 2, bn, st);
       if (e == cudaSuccess)
-        e = gate_rope_fwd_launch(L.Q, L.K, L.Zq, L.Zk, cfg->use_rope ? W.rope_cs : nullptr, L.Qr, L.Kr, T, d, hd, st);
+        e = gate_rope_fwd_launch(L.Q, L.K, L.Zq, L.Zk, cfg->use_rope ? W.rope_cs : nullptr, L.Qr, L.Kr, T, d, hd, st,
+                                 W.tap[TAP_QR], W.tap[TAP_KR]);
     } else if (cfg->use_rope) {
       e = rope_apply_launch(L.Q, L.Qr, T, d, hd, W.rope_cs, st);
       if (e == cudaSuccess) e = rope_apply_launch(L.K, L.Kr, T, d, hd, W.rope_cs, st);
@@ -386,6 +420,12 @@ cadet_status cadet_attn_forward(const cadet_attn_config* cfg, const cadet_batch*
     e = zero_pad_rows_launch(L.O, d * 2, T, b->cu_seqlens, n, st);
     if (e == cudaSuccess) e = cudaMemsetAsync(L.lse, 0, sizeof(float) * (size_t)T * cfg->n_heads, st);
     if (e == cudaSuccess) e = attn_fwd_launch(L.Qr, L.Kr, L.V, p, st);
+    if (e == cudaSuccess && W.tap[TAP_O]) {  // parity tap: the same (deterministic) kernel, fp32 O
+      p.out_f32 = 1;
+      p.O = W.tap[TAP_O];
+      e = zero_pad_rows_launch(W.tap[TAP_O], d * 4, T, b->cu_seqlens, n, st);
+      if (e == cudaSuccess) e = attn_fwd_launch(L.Qr, L.Kr, L.V, p, st);
+    }
   }
   // A6: Y = O W_o (+ resid)
   if (e == cudaSuccess) {
@@ -393,6 +433,7 @@ cadet_status cadet_attn_forward(const cadet_attn_config* cfg, const cadet_batch*
       GemmProblem g = prob(T, d, d, act(L.O, T, d), w_fwd(w->W_o, d, d), EPI_STORE);
       g.epi.out = Y;
       g.epi.resid = resid;
+      g.epi.tap = W.tap[TAP_Y];
       e = gemm_launch(&g, 1, bn, st);
     } else {
       e = add_bf16_launch(L.O, resid, Y, (size_t)T * d, st);
@@ -446,6 +487,7 @@ cadet_status cadet_attn_backward_ev(const cadet_attn_config* cfg, const cadet_ba
   if (e == cudaSuccess && cfg->use_out_proj) {
     GemmProblem g = prob(T, d, d, act(dY, T, d), w_bwd(w->W_o, d, d), EPI_STORE);
     g.epi.out = W.dO;
+    g.epi.tap = W.tap[TAP_DO];
     if (d_in_a9) {
       g.epi.dot_src = L.O;
       g.epi.dot_out = W.D;
@@ -480,6 +522,16 @@ cadet_status cadet_attn_backward_ev(const cadet_attn_config* cfg, const cadet_ba
       e = zero_pad_rows_multi_launch(pads, 3, d * 2, T, b->cu_seqlens, n, st);
     }
     if (e == cudaSuccess) e = attn_bwd_launch(L.Qr, L.Kr, L.V, dO, p, st);
+    if (e == cudaSuccess && W.tap[TAP_DQR]) {  // parity taps: the same (deterministic) kernels, fp32 outputs
+      p.out_f32 = 1;
+      p.dq_bf16 = 0;
+      p.dQ = W.tap[TAP_DQR];
+      p.dK = W.tap[TAP_DKR];
+      p.dV = W.tap[TAP_DV];
+      void* pads[3] = {W.tap[TAP_DQR], W.tap[TAP_DKR], W.tap[TAP_DV]};
+      e = zero_pad_rows_multi_launch(pads, 3, d * 4, T, b->cu_seqlens, n, st);
+      if (e == cudaSuccess) e = attn_bwd_launch(L.Qr, L.Kr, L.V, dO, p, st);
+    }
   }
   // A11: R(-alpha) + interaction-gate backward
   const void* dQ = W.dQ;
@@ -492,7 +544,9 @@ cadet_status cadet_attn_backward_ev(const cadet_attn_config* cfg, const cadet_ba
         const void* zs[2] = {L.Zq, L.Zk};
         void* us[2] = {W.uq, W.uk};
         void* rs[2] = {W.rq, W.rk};
-        e = rope_gate_bwd_launch2(drs, xs, zs, us, rs, 2, 0, 1, T, d, hd, cs, st);
+        float* tu[2] = {W.tap[TAP_UQ], W.tap[TAP_UK]};
+        float* tr[2] = {W.tap[TAP_RQ], W.tap[TAP_RK]};
+        e = rope_gate_bwd_launch2(drs, xs, zs, us, rs, 2, 0, 1, T, d, hd, cs, st, tu, tr);
       }
       if (e == cudaSuccess) {  // dQ = rq + uq W_qg^T ; dK = rk + uk W_kg^T
         GemmProblem g[2];
@@ -505,6 +559,7 @@ cadet_status cadet_attn_backward_ev(const cadet_attn_config* cfg, const cadet_ba
           g[i].epi.out = outs[i];
           g[i].epi.resid = rs[i];
           g[i].epi.resid_f32 = 0;
+          g[i].epi.tap = W.tap[TAP_DQ + i];
         }
         // dW_qg = Q^T uq ; dW_kg = K^T uk share the u operands: same launch
         GemmProblem gw[2] = {wgrad(L.Q, W.uq, gr->dW_qg, T, d, d, bnw), wgrad(L.K, W.uk, gr->dW_kg, T, d, d, bnw)};
@@ -541,10 +596,13 @@ cadet_status cadet_attn_backward_ev(const cadet_attn_config* cfg, const cadet_ba
       g.epi.src = X;
       g.epi.aux = L.Zx;
       g.epi.resid = dresid;
+      g.epi.tap = W.tap[TAP_UX];
+      g.epi.tap2 = W.tap[TAP_RX];
     } else {
       g.epi.mode = EPI_STORE;
       g.epi.out = dX;
       g.epi.resid = dresid;
+      g.epi.tap = W.tap[TAP_DX];
     }
     {  // with the weight gradients of W_q, W_k, W_v (same dQ, dK, dV operands) in one launch
       GemmProblem gw[3] = {wgrad(Xt, dQ, gr->dW_q, T, d, d, bnw), wgrad(Xt, dK, gr->dW_k, T, d, d, bnw),
@@ -557,6 +615,7 @@ cadet_status cadet_attn_backward_ev(const cadet_attn_config* cfg, const cadet_ba
       g2.epi.out = dX;
       g2.epi.resid = W.rx;
       g2.epi.resid_f32 = 0;
+      g2.epi.tap = W.tap[TAP_DX];
       GemmProblem gw = wgrad(X, W.ux, gr->dW_xg, T, d, d, bnw);
       e = gemm_launch2(&g2, 1, bn, &gw, 1, bnw, st);
     }

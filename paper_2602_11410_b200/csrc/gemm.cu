@@ -313,10 +313,16 @@ __device__ __forceinline__ void run_epilogue_warp(const EpiParams& e, int row0, 
           if (split < 32) atomicAdd(e.dot_out + (size_t)(h0 + 1) * e.dot_T + row0 + lane, s1);
         }
       }
+      if constexpr (HAS_MODE(EPI_TAPS)) {
+        if (e.tap) warp_store_rows(stg, e.tap, 1, off0, e.ldo, rows_valid, v);
+      }
       warp_store_rows(stg, e.out, e.out_f32, off0, e.ldo, rows_valid, v);
     } break;
     case EPI_GATE: if constexpr (HAS_MODE(EPI_GATE)) {
       if (e.aux) warp_store_rows(stg, e.aux, e.aux_f32, off0, e.ldo, rows_valid, v);
+      if constexpr (HAS_MODE(EPI_TAPS)) {
+        if (e.tap2) warp_store_rows(stg, e.tap2, 1, off0, e.ldo, rows_valid, v);
+      }
       float x[32];
       if (pre)
         warp_sts_rows_bf16(stg, *reinterpret_cast<const uint4(*)[4]>(pre), x);
@@ -324,6 +330,9 @@ __device__ __forceinline__ void run_epilogue_warp(const EpiParams& e, int row0, 
         warp_load_rows(stg, e.src, 0, off0, e.ldo, rows_valid, x);
 #pragma unroll
       for (int j = 0; j < 32; ++j) v[j] = x[j] * sigmoid_fast(v[j]);
+      if constexpr (HAS_MODE(EPI_TAPS)) {
+        if (e.tap) warp_store_rows(stg, e.tap, 1, off0, e.ldo, rows_valid, v);
+      }
       warp_store_rows(stg, e.out, e.out_f32, off0, e.ldo, rows_valid, v);
     } break;
     case EPI_GATE_BWD: if constexpr (HAS_MODE(EPI_GATE_BWD)) {
@@ -345,6 +354,10 @@ __device__ __forceinline__ void run_epilogue_warp(const EpiParams& e, int row0, 
         const float vj = v[j];
         v[j] = vj * x[j] * g * (1.0f - g);
         r[j] += vj * g;
+      }
+      if constexpr (HAS_MODE(EPI_TAPS)) {
+        if (e.tap) warp_store_rows(stg, e.tap, 1, off0, e.ldo, rows_valid, v);
+        if (e.tap2) warp_store_rows(stg, e.tap2, 1, off0, e.ldo, rows_valid, r);
       }
       warp_store_rows(stg, e.out, e.out_f32, off0, e.ldo, rows_valid, v);
       warp_store_rows(stg, e.out2, e.out2_f32, off0, e.ldo, rows_valid, r);
@@ -421,7 +434,6 @@ __device__ __forceinline__ void run_epilogue_warp(const EpiParams& e, int row0, 
 // ---------------------------------------------------------------- kernel
 template <int BN, uint32_t MODES>
 __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_kernel(const __grid_constant__ GemmKParams P) {
-  pdl_trigger();
   using C = GemmCfg<BN>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -455,6 +467,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_kernel(const __grid_cons
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_trigger();  // after the TMEM allocation: a dependent CTA never takes this CTA's columns first
   pdl_wait();  // operands / epilogue inputs are the previous kernels' outputs
 
   // registers: warpgroup 0 (TMA, MMA, allocator, idle) gives 104 per thread to the epilogue warpgroups
@@ -596,7 +609,6 @@ struct PairCfg {
 template <uint32_t MODES>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
     gemm_pair_kernel(const __grid_constant__ GemmKParams P) {
-  pdl_trigger();
   using C = PairCfg;
   constexpr int BN = 256;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -634,6 +646,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
   cluster_sync_all();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_trigger();  // after the TMEM allocation: a dependent CTA never takes this CTA's columns first
   pdl_wait();  // operands / epilogue inputs are the previous kernels' outputs
   const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
 
@@ -812,6 +825,7 @@ static cudaError_t launch_pair(const GemmKParams& P, cudaStream_t stream) {
 
 // the mode sets the layer launches get their own instantiation; anything else runs the all-modes one
 static cudaError_t launch_pair_modes(const GemmKParams& P, uint32_t modes, cudaStream_t stream) {
+  if (modes & MB(EPI_TAPS)) return launch_pair<MODES_ALL | MB(EPI_TAPS)>(P, stream);  // parity taps
   switch (modes) {
     case MB(EPI_STORE): return launch_pair<MB(EPI_STORE)>(P, stream);
     case MB(EPI_GATE): return launch_pair<MB(EPI_GATE)>(P, stream);
@@ -845,6 +859,7 @@ static cudaError_t launch_bn(const GemmKParams& P, cudaStream_t stream) {
 
 template <int BN>
 static cudaError_t launch_bn_modes(const GemmKParams& P, uint32_t modes, cudaStream_t stream) {
+  if (modes & MB(EPI_TAPS)) return launch_bn<BN, MODES_ALL | MB(EPI_TAPS)>(P, stream);  // parity taps
   switch (modes) {
     case MB(EPI_STORE): return launch_bn<BN, MB(EPI_STORE)>(P, stream);
     case MB(EPI_GATE): return launch_bn<BN, MB(EPI_GATE)>(P, stream);
@@ -897,7 +912,10 @@ cudaError_t gemm_launch(const GemmProblem* probs, int nprob, int bn, cudaStream_
   }
   P.total_units = total;
   uint32_t modes = 0;
-  for (int p = 0; p < nprob; ++p) modes |= MB(probs[p].epi.mode);
+  for (int p = 0; p < nprob; ++p) {
+    modes |= MB(probs[p].epi.mode);
+    if (probs[p].epi.tap || probs[p].epi.tap2) modes |= MB(EPI_TAPS);
+  }
   if (pair) return launch_pair_modes(P, modes, stream);
   return bn == 256 ? launch_bn_modes<256>(P, modes, stream) : launch_bn_modes<128>(P, modes, stream);
 }

@@ -16,6 +16,8 @@ enum EpiMode : int32_t {
   EPI_GELU = 6,       // NEXT-3 FFN: aux = acc (pre-activation); out = GELU(acc) (R33)
   EPI_GELU_BWD = 7,   // NEXT-3 FFN: out = acc * GELU'(aux)
 };
+// Not a mode: the bit of the compile-time mode set that enables the parity taps (tap / tap2 below).
+constexpr int EPI_TAPS = 8;
 
 struct EpiParams {
   int32_t mode;
@@ -39,6 +41,11 @@ struct EpiParams {
   const void* dot_src;
   float* dot_out;
   int32_t dot_T;
+  // parity taps (SURVEY 8(c) protocol iii, cadet_attn_stage_views): fp32 copies, [rows][ldo], of the
+  // value stored to out (tap) and of aux (EPI_GATE: Z) / out2 (EPI_GATE_BWD: r) (tap2) BEFORE their
+  // bf16 rounding; null = off.  Only the warp-cooperative epilogue (no row_map) writes them.
+  float* tap;
+  float* tap2;
   // heads (EPI_HEAD)
   const float* b1;
   const float* w2;

@@ -74,7 +74,7 @@ __global__ void rope_apply_kernel(const __nv_bfloat16* in, __nv_bfloat16* out, i
 __global__ void __launch_bounds__(256) gate_rope_fwd_kernel(const __nv_bfloat16* Q, const __nv_bfloat16* K,
                                                             const __nv_bfloat16* Gq, const __nv_bfloat16* Gk,
                                                             const float* cs, __nv_bfloat16* Qr, __nv_bfloat16* Kr,
-                                                            int T, int d, int hd) {
+                                                            int T, int d, int hd, float* tapQ, float* tapK) {
   pdl_trigger();
   pdl_wait();
   const int per_row = d / 8;
@@ -91,6 +91,7 @@ __global__ void __launch_bounds__(256) gate_rope_fwd_kernel(const __nv_bfloat16*
   const __nv_bfloat16* src[2] = {Q, K};
   const __nv_bfloat16* gate[2] = {Gq, Gk};
   __nv_bfloat16* dst[2] = {Qr, Kr};
+  float* tap[2] = {tapQ, tapK};
 #pragma unroll
   for (int w = 0; w < 2; ++w) {
     const uint4 xu = *reinterpret_cast<const uint4*>(src[w] + off);
@@ -98,13 +99,21 @@ __global__ void __launch_bounds__(256) gate_rope_fwd_kernel(const __nv_bfloat16*
     const __nv_bfloat162* x2 = reinterpret_cast<const __nv_bfloat162*>(&xu);
     const __nv_bfloat162* g2 = reinterpret_cast<const __nv_bfloat162*>(&gu);
     uint32_t o[4];
+    float f[8];
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       const float2 x = __bfloat1622float2(x2[e]), z = __bfloat1622float2(g2[e]);
       const float a = x.x * sigmoid_fast(z.x), b = x.y * sigmoid_fast(z.y);
-      o[e] = pack_bf16(a * cv[e] - b * sv[e], a * sv[e] + b * cv[e]);
+      f[2 * e] = a * cv[e] - b * sv[e];
+      f[2 * e + 1] = a * sv[e] + b * cv[e];
+      o[e] = pack_bf16(f[2 * e], f[2 * e + 1]);
     }
     *reinterpret_cast<uint4*>(dst[w] + off) = make_uint4(o[0], o[1], o[2], o[3]);
+    if (tap[w]) {  // parity tap: the fp32 value before its bf16 rounding
+      float4* t4 = reinterpret_cast<float4*>(tap[w] + off);
+      t4[0] = make_float4(f[0], f[1], f[2], f[3]);
+      t4[1] = make_float4(f[4], f[5], f[6], f[7]);
+    }
   }
 }
 
@@ -118,6 +127,8 @@ struct RgSide {
   const __nv_bfloat16* Z;
   __nv_bfloat16* out_u;
   void* out_r;
+  float* tap_u;  // parity taps (nullable): fp32 u and r before their bf16 rounding
+  float* tap_r;
 };
 struct RgSides {
   RgSide s[2];
@@ -177,8 +188,10 @@ __global__ void __launch_bounds__(256) rope_gate_bwd_kernel(RgSides sides, int d
       const float2 z = __bfloat1622float2(z2[e]);
       const float2 x = __bfloat1622float2(x2[e]);
       const float g0 = sigmoid_fast(z.x), g1 = sigmoid_fast(z.y);
-      __nv_bfloat162 v = __floats2bfloat162_rn(g[2 * e] * x.x * g0 * (1.f - g0), g[2 * e + 1] * x.y * g1 * (1.f - g1));
+      const float u0 = g[2 * e] * x.x * g0 * (1.f - g0), u1 = g[2 * e + 1] * x.y * g1 * (1.f - g1);
+      __nv_bfloat162 v = __floats2bfloat162_rn(u0, u1);
       uo[e] = *reinterpret_cast<uint32_t*>(&v);
+      if (sd.tap_u) *reinterpret_cast<float2*>(sd.tap_u + off + 2 * e) = make_float2(u0, u1);
       r[2 * e] = g[2 * e] * g0;
       r[2 * e + 1] = g[2 * e + 1] * g1;
     }
@@ -186,6 +199,11 @@ __global__ void __launch_bounds__(256) rope_gate_bwd_kernel(RgSides sides, int d
   } else {
 #pragma unroll
     for (int e = 0; e < 8; ++e) r[e] = g[e];
+  }
+  if (sd.tap_r) {
+    float4* t4 = reinterpret_cast<float4*>(sd.tap_r + off);
+    t4[0] = make_float4(r[0], r[1], r[2], r[3]);
+    t4[1] = make_float4(r[4], r[5], r[6], r[7]);
   }
   if (r_bf16) {
     uint32_t ro[4];
@@ -389,13 +407,15 @@ cudaError_t rope_apply_launch(const void* in, void* out, int T, int d, int hd, c
 }
 cudaError_t rope_gate_bwd_launch2(const void* const* dr, const void* const* Xq, const void* const* Z,
                                   void* const* out_u, void* const* out_r, int nsides, int dr_f32, int r_bf16, int T,
-                                  int d, int hd, const float* cs, cudaStream_t st) {
+                                  int d, int hd, const float* cs, cudaStream_t st, float* const* tap_u,
+                                  float* const* tap_r) {
   if (nsides < 1 || nsides > 2) return cudaErrorInvalidValue;
   RgSides sides;
   for (int i = 0; i < 2; ++i) {
     const int k = i < nsides ? i : 0;
     sides.s[i] = RgSide{dr[k], reinterpret_cast<const __nv_bfloat16*>(Xq[k]), reinterpret_cast<const __nv_bfloat16*>(Z[k]),
-                        reinterpret_cast<__nv_bfloat16*>(out_u[k]), out_r[k]};
+                        reinterpret_cast<__nv_bfloat16*>(out_u[k]), out_r[k], tap_u ? tap_u[k] : nullptr,
+                        tap_r ? tap_r[k] : nullptr};
   }
   ProfScope ps(PROF_OTHER, st, 1);
   const size_t work = (size_t)T * d / 8;
@@ -409,7 +429,8 @@ cudaError_t rope_gate_bwd_launch(const void* dr, int dr_f32, const void* Xq, con
   return rope_gate_bwd_launch2(&dr, &Xq, &Z, &out_u, &out_r, 1, dr_f32, r_bf16, T, d, hd, cs, st);
 }
 cudaError_t gate_rope_fwd_launch(const void* Q, const void* K, const void* Gq, const void* Gk, const float* cs,
-                                 void* Qr, void* Kr, int T, int d, int hd, cudaStream_t st) {
+                                 void* Qr, void* Kr, int T, int d, int hd, cudaStream_t st, float* tapQ,
+                                 float* tapK) {
   ProfScope ps(PROF_OTHER, st, 1);
   const size_t work = (size_t)T * d / 8;
   if (work >= (size_t)INT32_MAX) return cudaErrorInvalidValue;
@@ -417,7 +438,7 @@ cudaError_t gate_rope_fwd_launch(const void* Q, const void* K, const void* Gq, c
     launch_pdl(gate_rope_fwd_kernel, dim3(blocks(work, 256)), dim3(256), 0, st,
                reinterpret_cast<const __nv_bfloat16*>(Q), reinterpret_cast<const __nv_bfloat16*>(K),
                reinterpret_cast<const __nv_bfloat16*>(Gq), reinterpret_cast<const __nv_bfloat16*>(Gk), cs,
-               reinterpret_cast<__nv_bfloat16*>(Qr), reinterpret_cast<__nv_bfloat16*>(Kr), T, d, hd);
+               reinterpret_cast<__nv_bfloat16*>(Qr), reinterpret_cast<__nv_bfloat16*>(Kr), T, d, hd, tapQ, tapK);
   return cudaGetLastError();
 }
 cudaError_t gather_rows_launch(const void* H, const int32_t* rows, int n, int T, int d, void* out, uint32_t* err,

@@ -11,11 +11,13 @@ cudaError_t rope_table_launch(float* cs, int T, int hd, double phi_min, double b
 cudaError_t rope_apply_launch(const void* in, void* out, int T, int d, int hd, const float* cs, cudaStream_t st);
 // A4 elementwise half: Qr = RoPE(Q * sigma(Z_q)), Kr = RoPE(K * sigma(Z_k)) (Z stored by the gate GEMMs)
 cudaError_t gate_rope_fwd_launch(const void* Q, const void* K, const void* Gq, const void* Gk, const float* cs,
-                                 void* Qr, void* Kr, int T, int d, int hd, cudaStream_t st);
+                                 void* Qr, void* Kr, int T, int d, int hd, cudaStream_t st, float* tapQ = nullptr,
+                                 float* tapK = nullptr);
 // both sides (Q and K) in one launch: arrays of nsides (<= 2) pointers
 cudaError_t rope_gate_bwd_launch2(const void* const* dr, const void* const* Xq, const void* const* Z,
                                   void* const* out_u, void* const* out_r, int nsides, int dr_f32, int r_bf16, int T,
-                                  int d, int hd, const float* cs, cudaStream_t st);
+                                  int d, int hd, const float* cs, cudaStream_t st, float* const* tap_u = nullptr,
+                                  float* const* tap_r = nullptr);
 cudaError_t rope_gate_bwd_launch(const void* dr, int dr_f32, const void* Xq, const void* Z, void* out_u, void* out_r,
                                  int r_bf16, int T, int d, int hd, const float* cs, cudaStream_t st);
 // to_f16: the gathered rows are written as fp16 (the towers' GEMM operand)

@@ -20,6 +20,8 @@ def err_stats(got, ref):
 
 def assert_close(got, ref, max_abs=MAX_ABS, mean_abs=MEAN_ABS, what=""):
     mx, mn, rms = err_stats(got, ref)
+    if what:
+        print(f"[parity] {what}: max {mx:.3e} mean {mn:.3e} (rms ref {rms:.3e})")
     assert mx <= max_abs and mn <= mean_abs, f"{what}: max {mx:.3e} mean {mn:.3e} (rms ref {rms:.3e})"
     return mx, mn
 

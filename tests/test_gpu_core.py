@@ -96,6 +96,39 @@ def test_mask_plan_bit_exact(ops, case):
     assert int(pairs.item()) == pairs_ref
 
 
+# (lengths, n_cand, flags, delta, n_static): static prefixes across a tile edge, pair flags on every
+# odd row and on rows 128 k (the flagged i-1 cell in the previous tile), all three rules at once
+PLAN_CASES_STATIC = [
+    ([300, 129, 700], None, 1, 60_000, [130, 0, 5]),
+    ([513, 257, 1], [0, 40, 0], 1 | 4, 600_000, [2, 129, 1]),
+    ([400, 300, 129], [0, 50, 0], 1 | 2 | 4, 120_000, [0, 200, 128]),
+    ([256, 256], None, 2, 0, [255, 1]),
+]
+
+
+@pytest.mark.parametrize("case", range(len(PLAN_CASES_STATIC)))
+def test_mask_plan_static_prefix_and_tile_edge_pairs_bit_exact(ops, case):
+    """n_static (R13) and PAIR_PREV (R12) with flagged rows at 128-row tile edges."""
+    lengths, nc, flags, dl, nst = PLAN_CASES_STATIC[case]
+    cu, t, s, ncv, T = make_case(lengths, n_cand=nc)
+    pf = np.zeros(T, np.uint8)
+    for a, e in zip(cu[:-1], cu[1:]):
+        loc = np.arange(e - a)
+        pf[a:e] = ((loc % 2 == 1) | ((loc % 128 == 0) & (loc > 0))).astype(np.uint8)
+    nstv = np.asarray(nst, np.int32)
+    cfg = ops.config(32, 1, mask_flags=flags, delta_delay_ms=dl)
+    b = to_dev_batch(cu, t, s, ncv, T, n_static=nstv, flags=pf)
+    ws = ops.plan_workspace(b)
+    ops.mask_plan(cfg, b, ws)
+    cap = int(sum(((l + 127) // 128) ** 2 for l in lengths))
+    kv_end, tc, pairs = ops.mask_export(cfg, b, ws, cap)
+    ops.poll(ws)
+    kv_ref, tc_ref, pairs_ref = O.mask_artifacts(meta_of(cu, t, s, ncv, n_static=nstv, flags=pf), oracle_cfg(cfg), T)
+    assert (kv_end.cpu().numpy() == kv_ref).all()
+    assert (tc.cpu().numpy() == tc_ref).all()
+    assert int(pairs.item()) == pairs_ref
+
+
 def test_mask_plan_fig3_and_tile_vector(ops):
     # Fig. 3 (P:305-385) with one token per time unit and delay width 2
     cfg = ops.config(32, 1, delta_delay_ms=2)

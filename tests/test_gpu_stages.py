@@ -1,0 +1,265 @@
+"""GPU parity of the full gated layer STAGE BY STAGE (SURVEY 8(c) protocol iii), forward A2-A6 and
+backward A9-A12, against the fp64 oracle.
+
+With cfg.out_f32 = 1 the layer calls also write each stage's fp32 value before its bf16 storage
+rounding (cadet_attn_stage_views taps), so every stage is gated on its accumulator at the north-star
+tolerance (max-abs 1e-2, mean-abs 1e-3 after the R19 normalisation) with NO storage allowance.  Each
+stage's oracle is fed the bf16 tensors that GPU stage consumed (saved activations, the backward's
+bf16 intermediates in ws), so an error is attributed to the stage that made it.  The cases cover
+every mask rule: TIME (Eq. 6), SESSION (R10), the PAIR_PREV exception (R12)
+with flagged rows at 128-row tile edges, the static prefix (R13), candidates, length-1
+sequences and pad rows, head dims 32 / 64 / 88 / 128 and the flat and peaky regimes.
+"""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+from oracle import cadet_oracle as O
+from synth import generator as G
+from tests.helpers import assert_close, bf16_tensor, err_stats, to_dev_batch, to_np
+from tests.test_gpu_core import meta_of, oracle_cfg
+from tests.test_gpu_layer import layer_case, saved_views
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+T_, S_, P_ = 1, 2, 4  # CADET_MASK_TIME / SESSION / PAIR_PREV
+
+
+@pytest.fixture(scope="module")
+def ops():
+    from paper_2602_11410_b200 import build, ops as _ops
+    build.build()
+    return _ops
+
+
+def pair_flags_for(cu, T):
+    """Action tokens (odd local rows, Eq. 1's (I_t, A_t) pairs) plus every local row 128 k, so the
+    flagged i-1 cell sits in the previous 128-row tile."""
+    f = np.zeros(T, np.uint8)
+    for a, e in zip(cu[:-1], cu[1:]):
+        loc = np.arange(e - a)
+        f[a:e] = ((loc % 2 == 1) | ((loc % 128 == 0) & (loc > 0))).astype(np.uint8)
+    return f
+
+
+# lengths, d, H, n_cand, peaky, mask flags, n_static (or None), pair flags
+STAGE_CASES = [
+    ([64, 1, 33, 17], 32, 1, None, False, T_, None, False),
+    ([200, 77, 300], 128, 2, [0, 7, 30], False, T_, None, False),
+    ([300, 129, 700], 256, 2, None, True, T_, None, False),
+    ([513, 257, 1, 300], 352, 4, None, False, T_ | S_, None, False),
+    ([260, 5, 700], 512, 8, None, False, T_ | P_, [130, 0, 3], True),
+    ([400, 300, 129], 128, 1, [0, 50, 0], False, T_ | S_ | P_, [2, 129, 0], True),
+    ([300, 256, 1], 256, 4, [0, 0, 0], False, S_, [0, 140, 1], False),
+]
+
+
+def peaky_ok(name, got, ref, peaky):
+    if not peaky:
+        return assert_close(got, ref, what=name)
+    # R23: in the peaky regime P and dS are bf16 MMA operands: 1e-1 / 5e-3 for the attention core
+    mx, mn, rms = err_stats(got, ref)
+    assert mx <= 1e-1 and mn <= 5e-3, (name, mx, mn)
+    return mx, mn
+
+
+def run_case(ops, case, with_resid):
+    from paper_2602_11410_b200 import _lib as L
+    lengths, d, H, nc, peaky, flags, nst, use_pf = STAGE_CASES[case]
+    cu, t, s, ncv, T, X, W = layer_case(lengths, d, H, nc, seed=40 + case, peaky=peaky)
+    pf = pair_flags_for(cu, T) if use_pf else None
+    nstv = None if nst is None else np.asarray(nst, np.int32)
+    cfg = ops.config(d, H, mask_flags=flags, delta_delay_ms=120_000, rope_phi_min=0.5, rope_base=1e4,
+                     rope_delta_t_max_ms=86_400_000, out_f32=1)
+    b = to_dev_batch(cu, t, s, ncv, T, n_static=nstv, flags=pf)
+    lib = L.lib()
+    Xd = bf16_tensor(X)
+    Wd = [bf16_tensor(w) for w in W.as_list()]
+    w = L.AttnWeights(*[x.data_ptr() for x in Wd])
+    saved = torch.zeros(lib.cadet_attn_saved_bytes(C.byref(cfg), T), dtype=torch.uint8, device="cuda")
+    extra = lib.cadet_attn_bwd_ds_bytes(C.byref(cfg), b.n_seqs, T, b.max_seqlen)   # two-pass backward
+    ws = ops.workspace(lib.cadet_attn_workspace_bytes(C.byref(cfg), b.n_seqs, T) + extra)
+    ws.zero_()
+    Y = torch.empty(T, d, dtype=torch.bfloat16, device="cuda")
+    R = G.normal_bf16(7, case, (T, d)) if with_resid else None
+    if R is not None:
+        R[cu[-1]:] = 0
+    Rd = bf16_tensor(R) if R is not None else None
+    st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    L.check(lib.cadet_attn_forward(C.byref(cfg), C.byref(b.struct()), C.byref(w), C.c_void_p(Xd.data_ptr()),
+                                   C.c_void_p(Y.data_ptr()), C.c_void_p(Rd.data_ptr()) if Rd is not None else None,
+                                   C.c_void_p(saved.data_ptr()), C.c_void_p(ws.data_ptr()), ws.numel(), st))
+    dY = G.normal_bf16(99, 50 + case, (T, d))
+    dY[cu[-1]:] = 0
+    dYd = bf16_tensor(dY)
+    dX = torch.empty(T, d, dtype=torch.bfloat16, device="cuda")
+    gs = [torch.empty(d, d, dtype=torch.float32, device="cuda") for _ in range(7)]
+    g = L.AttnGrads(*[x.data_ptr() for x in gs])
+    dR = dYd if with_resid else None    # the residual path's gradient is added into dX
+    L.check(lib.cadet_attn_backward(C.byref(cfg), C.byref(b.struct()), C.byref(w), C.c_void_p(Xd.data_ptr()),
+                                    C.c_void_p(saved.data_ptr()), C.c_void_p(dYd.data_ptr()),
+                                    C.c_void_p(dX.data_ptr()), C.c_void_p(dR.data_ptr()) if dR is not None else None,
+                                    C.byref(g), C.c_void_p(ws.data_ptr()), ws.numel(), st))
+    torch.cuda.synchronize()
+    ops.poll(ws)
+    views = (C.c_void_p * L.CADET_N_VIEWS)()
+    L.check(lib.cadet_attn_stage_views(C.byref(cfg), b.n_seqs, T, C.c_void_p(ws.data_ptr()), ws.numel(), views))
+    base = ws.data_ptr()
+
+    def at(ptr, nbytes):
+        off = ptr - base
+        assert 0 <= off and off + nbytes <= ws.numel()
+        return ws[off: off + nbytes]
+
+    taps = {n: at(views[i], T * d * 4).view(torch.float32).view(T, d).cpu().numpy().astype(np.float64)
+            for i, n in enumerate(L.TAP_NAMES)}
+    wsb = {n: to_np(at(views[L.CADET_WS_DO + i], T * d * 2).view(torch.bfloat16).view(T, d))
+           for i, n in enumerate(L.WS_NAMES)}
+    Dg = at(views[L.CADET_WS_D], H * T * 4).view(torch.float32).view(H, T).cpu().numpy().astype(np.float64)
+    return dict(cu=cu, t=t, s=s, ncv=ncv, T=T, X=X.astype(np.float64), W=[x.astype(np.float64) for x in W.as_list()],
+                cfg=cfg, meta=meta_of(cu, t, s, ncv, n_static=nstv, flags=pf), sv=saved_views(saved, T, d, H),
+                taps=taps, wsb=wsb, D=Dg, Y=to_np(Y), dX=to_np(dX), gW=[x.cpu().numpy().astype(np.float64) for x in gs],
+                dY=dY.astype(np.float64), R=None if R is None else R.astype(np.float64), peaky=peaky, H=H, d=d,
+                lengths=lengths)
+
+
+@pytest.mark.parametrize("case", range(len(STAGE_CASES)))
+def test_layer_stages_forward_and_backward(ops, case):
+    r = run_case(ops, case, with_resid=(case % 2 == 1))
+    cu, T, d, H, peaky = r["cu"], r["T"], r["d"], r["H"], r["peaky"]
+    n = int(cu[-1])
+    sv, tp, wb = r["sv"], r["taps"], r["wsb"]
+    Wxg, Wq, Wk, Wv, Wqg, Wkg, Wo = r["W"]
+    X = r["X"]
+    ocfg = oracle_cfg(r["cfg"])
+    t = r["t"]
+    rs = lambda a: a[:n]
+    # ---- forward: A2 (Eq. 4) fed the bf16 X
+    Zx = X @ Wxg
+    assert_close(rs(tp["Zx"]), rs(Zx), what="A2 Zx")
+    assert_close(rs(tp["Xt"]), rs(X * O.sigmoid(Zx)), what="A2 Xt")
+    # A3 (Eq. 3; R2) fed the GPU's bf16 Xt
+    for nm, Wi in (("Q", Wq), ("K", Wk), ("V", Wv)):
+        assert_close(rs(tp[nm]), rs(sv["Xt"] @ Wi), what="A3 " + nm)
+    # A4 (Eq. 5; RoPE P:274): Z from the bf16 Q/K, the rotation of Q * sigma(bf16 Z)
+    for nm, src, Wg, zn in (("Qr", "Q", Wqg, "Zq"), ("Kr", "K", Wkg, "Zk")):
+        assert_close(rs(tp[zn]), rs(sv[src] @ Wg), what="A4 " + zn)
+        assert_close(rs(tp[nm]), rs(O.rope_heads(sv[src] * O.sigmoid(sv[zn]), t, ocfg)), what="A4 " + nm)
+    # A5 (Eq. 7) fed the bf16 Qr, Kr, V
+    Oref, lref = np.zeros((T, d)), np.zeros((H, T))
+    for k in range(len(r["lengths"])):
+        a, e = cu[k], cu[k + 1]
+        A = O.seq_mask(r["meta"], k, ocfg)
+        o, l, _ = O.attention_core_forward(sv["Qr"][a:e], sv["Kr"][a:e], sv["V"][a:e], A, H)
+        Oref[a:e], lref[:, a:e] = o, l
+    peaky_ok("A5 O", tp["O"], Oref, peaky)
+    assert_close(sv["lse"], lref, what="A5 LSE")
+    # A6 fed the bf16 O (+ the bf16 residual)
+    Yref = sv["O"] @ Wo + (0 if r["R"] is None else r["R"])
+    assert_close(rs(tp["Y"]), rs(Yref), what="A6 Y")
+    assert (r["Y"][n:] == 0).all()
+    # ---- backward: A9 dO = dY W_o^T, D = rowsum(dO * O) per head (dO's fp32 value, bf16 O), dW_o = O^T dY
+    dY = r["dY"]
+    dOref = dY @ Wo.T
+    assert_close(rs(tp["dO"]), rs(dOref), what="A9 dO")
+    hd = d // H
+    Dref = np.stack([(dOref[:, h * hd:(h + 1) * hd] * sv["O"][:, h * hd:(h + 1) * hd]).sum(1) for h in range(H)])
+    assert_close(r["D"][:, :n], Dref[:, :n], what="A9/A10 D")
+    assert_close(r["gW"][6], sv["O"].T @ dY, what="A9 dW_o")
+    # A10 (adjoint of Eq. 7) fed the bf16 Qr, Kr, V and the bf16 dO it consumed
+    ref = [np.zeros((T, d)) for _ in range(3)]
+    for k in range(len(r["lengths"])):
+        a, e = cu[k], cu[k + 1]
+        A = O.seq_mask(r["meta"], k, ocfg)
+        out = O.attention_core_backward(sv["Qr"][a:e], sv["Kr"][a:e], sv["V"][a:e], A, wb["dO"][a:e], H)
+        for j in range(3):
+            ref[j][a:e] = out[j]
+    for nm, rf in zip(("dQr", "dKr", "dV"), ref):
+        peaky_ok("A10 " + nm, tp[nm], rf, peaky)
+    # A11 (adjoint of Eq. 5 and of the rotation) fed the bf16 dQr / dKr, Q / K and Z
+    for side, src, zn, Wg, gi in (("q", "Q", "Zq", Wqg, 4), ("k", "K", "Zk", Wkg, 5)):
+        dr = wb["dQr"] if side == "q" else wb["dKr"]
+        dT = O.rope_heads(dr, t, ocfg, -1.0)
+        gg = O.sigmoid(sv[zn])
+        assert_close(rs(tp["u" + side]), rs(dT * sv[src] * gg * (1 - gg)), what="A11 u_" + side)
+        assert_close(rs(tp["r" + side]), rs(dT * gg), what="A11 r_" + side)
+        dname = "dQ" if side == "q" else "dK"
+        assert_close(rs(tp[dname]), rs(wb["r" + side] + wb["u" + side] @ Wg.T), what="A11 " + dname)
+        assert_close(r["gW"][gi], sv[src].T @ wb["u" + side], what="A11 dW_" + side + "g")
+    # A12 (adjoint of Eqs. 3-4) fed the bf16 dQ, dK, dV, X, Zx
+    dXt = wb["dQ"] @ Wq.T + wb["dK"] @ Wk.T + wb["dV"] @ Wv.T
+    gx = O.sigmoid(sv["Zx"])
+    assert_close(rs(tp["ux"]), rs(dXt * X * gx * (1 - gx)), what="A12 u_x")
+    rx = dXt * gx + (0 if r["R"] is None else dY)
+    assert_close(rs(tp["rx"]), rs(rx), what="A12 r_x")
+    assert_close(rs(tp["dX"]), rs(wb["rx"] + wb["ux"] @ Wxg.T), what="A12 dX")
+    for gi, src in ((1, wb["dQ"]), (2, wb["dK"]), (3, wb["dV"])):
+        assert_close(r["gW"][gi], sv["Xt"].T @ src, what=f"A12 dW {gi}")
+    assert_close(r["gW"][0], X.T @ wb["ux"], what="A12 dW_xg")
+    assert (r["dX"][n:] == 0).all()
+
+
+def test_taps_do_not_change_the_bf16_results(ops):
+    """out_f32 = 1 only adds fp32 copies: Y, dX and the weight gradients match the plain run (up to
+    the split-K atomic order of the weight gradients)."""
+    from paper_2602_11410_b200 import _lib as L
+    import dataclasses
+    r1 = run_case(ops, 1, with_resid=False)
+    lengths, d, H, nc, peaky, flags, nst, use_pf = STAGE_CASES[1]
+    cu, t, s, ncv, T, X, W = layer_case(lengths, d, H, nc, seed=41, peaky=peaky)
+    cfg = ops.config(d, H, mask_flags=flags, delta_delay_ms=120_000, rope_phi_min=0.5, rope_base=1e4,
+                     rope_delta_t_max_ms=86_400_000, out_f32=0)
+    b = to_dev_batch(cu, t, s, ncv, T)
+    from tests.test_gpu_layer import run_layer_forward
+    Y, saved, ws, Xd, Wd, w = run_layer_forward(ops, cfg, b, X, W, T, two_pass=True)
+    assert (to_np(Y) == r1["Y"]).all()
+
+
+# ------------------------------------------------------------------ attention core (single-pass dQ kernel)
+CORE_MASK_CASES = [
+    # lengths, d, H, n_cand, flags, n_static, pair flags
+    ([300, 129, 700], 128, 2, None, T_ | S_, None, False),
+    ([513, 257, 1, 300], 352, 4, [0, 30, 0, 0], T_ | P_, [130, 0, 1, 0], True),
+    ([400, 300, 129], 256, 2, [0, 50, 0], T_ | S_ | P_, [2, 129, 0], True),
+    ([256, 256, 5], 64, 1, None, S_, [255, 1, 0], False),
+]
+
+
+@pytest.mark.parametrize("case", range(len(CORE_MASK_CASES)))
+def test_attn_core_mask_rules_forward_backward(ops, case):
+    """SESSION (R10), PAIR_PREV with tile-edge flags and the static prefix through the
+    core ABI (attention forward + the single-pass recomputing dQ kernel + dK/dV), fp32 outputs."""
+    from tests.test_gpu_core import core_case
+    lengths, d, H, nc, flags, nst, use_pf = CORE_MASK_CASES[case]
+    cu, t, s, ncv, T, Qr, Kr, V = core_case(lengths, d, H, nc, 0.55, seed=60 + case)
+    pf = pair_flags_for(cu, T) if use_pf else None
+    nstv = None if nst is None else np.asarray(nst, np.int32)
+    rng = np.random.default_rng(61 + case)
+    dO = G.bf16_round(rng.standard_normal((T, d)).astype(np.float32))
+    cfg = ops.config(d, H, mask_flags=flags, delta_delay_ms=120_000, out_f32=0)
+    b = to_dev_batch(cu, t, s, ncv, T, n_static=nstv, flags=pf)
+    q, k, v, g = bf16_tensor(Qr), bf16_tensor(Kr), bf16_tensor(V), bf16_tensor(dO)
+    Og, lse = ops.attn_core_forward(cfg, b, q, k, v)
+    cfg.out_f32 = 1
+    Of, _ = ops.attn_core_forward(cfg, b, q, k, v)
+    dQ, dK, dV = ops.attn_core_backward(cfg, b, q, k, v, Og, lse, g)
+    torch.cuda.synchronize()
+    ocfg = oracle_cfg(cfg)
+    meta = meta_of(cu, t, s, ncv, n_static=nstv, flags=pf)
+    Oref, lref = np.zeros((T, d)), np.zeros((H, T))
+    ref = [np.zeros((T, d)) for _ in range(3)]
+    for i in range(len(lengths)):
+        a, e = cu[i], cu[i + 1]
+        A = O.seq_mask(meta, i, ocfg)
+        args = (Qr[a:e].astype(np.float64), Kr[a:e].astype(np.float64), V[a:e].astype(np.float64))
+        o, l, _ = O.attention_core_forward(*args, A, H)
+        Oref[a:e], lref[:, a:e] = o, l
+        for j, x in enumerate(O.attention_core_backward(*args, A, dO[a:e].astype(np.float64), H)):
+            ref[j][a:e] = x
+    assert_close(to_np(Of), Oref, what="O")
+    assert_close(to_np(lse), lref, what="LSE")
+    for nm, got, rf in zip(("dQ", "dK", "dV"), (dQ, dK, dV), ref):
+        assert_close(to_np(got), rf, what=nm)
+        assert (to_np(got)[cu[-1]:] == 0).all()
