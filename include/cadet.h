@@ -52,7 +52,7 @@ typedef enum {
   CADET_E_BUCKET = 6,      /* bucket outside [0, K) ("routing error")                                (device) */
   CADET_E_NONFINITE = 7,   /* NaN/Inf in a loss (fail-fast numerics)                                  (device) */
   CADET_E_WORKSPACE = 8,   /* workspace / capacity too small                                                         */
-  CADET_E_UNSUPPORTED = 9, /* valid but not implemented in this build (e.g. dtype FP32)                               */
+  CADET_E_UNSUPPORTED = 9, /* valid but not implemented in this build                                                  */
   CADET_E_CUDA = 10        /* a CUDA runtime error; see cadet_last_error()                                          */
 } cadet_status;
 
@@ -72,7 +72,11 @@ typedef struct {
   int32_t d_model;   /* d, multiple of 32 */
   int32_t n_heads;   /* H <= 128; head_dim = d / H must be one of {32, 64, 88, 96, 128} (else CADET_E_ARG) */
   int32_t head_dim;  /* must equal d_model / n_heads */
-  int32_t dtype;     /* CADET_BF16 (bf16 operands, fp32 accumulation); CADET_FP32 -> CADET_E_UNSUPPORTED in v1 */
+  int32_t dtype;     /* CADET_BF16: bf16 tensors and weights, fp32 accumulation (the product path).
+                        CADET_FP32: the parity mode (SURVEY 8(c) ii, north star "1e-4 for an fp32 mode"): every
+                        tensor / weight argument of the layer and core calls is fp32 (saved and workspace sizes
+                        follow), GEMMs are 3xTF32 on the tensor cores, gates / RoPE / attention run in fp32
+                        arithmetic; out_f32 and the two-pass dS workspace do not apply. */
   int32_t mask_flags;
   int32_t out_f32;   /* core calls: 1 = write O / dQr / dKr / dV as fp32 (parity protocol, SURVEY 8(c) iii).
                         layer calls: 1 = ALSO write every stage's fp32 value before its bf16 rounding into the
@@ -123,7 +127,7 @@ typedef struct {
   int32_t K;        /* towers (K = 2 at P:624) */
   int32_t d_model;
   int32_t d_hidden; /* dh >= 32, multiple of 8, K*dh multiple of 32 (default d/2) */
-  int32_t dtype;    /* CADET_BF16 */
+  int32_t dtype;    /* CADET_BF16 (W1, Hs, dHs, pre bf16) or CADET_FP32 (all fp32, 3xTF32 GEMMs: parity mode) */
   int32_t rows_in_ws; /* backward calls: 1 = ws still holds H[rows] gathered by cadet_heads_forward (same Hs, rows,
                          n, ws), so the gather is skipped; the rows are still bounds-checked by the scatter */
 } cadet_head_config;
@@ -378,6 +382,16 @@ size_t cadet_pack_workspace_bytes(int32_t B);
  * [M, N]; resid (nullable) same dtype as C.  N % 32 == 0, K % 8 == 0, M % 8 == 0 when MN-major. */
 cadet_status cadet_gemm(int32_t M, int32_t N, int32_t K, const void* A, int32_t a_mn, const void* B, int32_t b_mn,
                         void* C, int32_t c_f32, const void* resid, cadet_stream_t stream);
+
+/* 3xTF32 GEMM of the CADET_FP32 mode (building block / test hook): C[M, N] = op(A) op(B) (+ resid), all fp32,
+ * op(A) [M, K] = A stored [M][K] (a_t = 0) or [K][M] (a_t = 1); op(B) [K, N] = B stored [K][N] (b_t = 0, the
+ * x . W case) or [N][K] (b_t = 1, the g . W^T case).  Each operand is split once into hi = tf32(x) and
+ * lo = x - hi, and C = A_hi B_hi + A_hi B_lo + A_lo B_hi accumulates in fp32 on the tensor cores
+ * (kind::tf32).  N % 32 == 0; ws >= cadet_gemm_fp32_workspace_bytes(M, N, K) (the split operands). */
+size_t cadet_gemm_fp32_workspace_bytes(int32_t M, int32_t N, int32_t K);
+cadet_status cadet_gemm_fp32(int32_t M, int32_t N, int32_t K, const float* A, int32_t a_t, const float* B,
+                             int32_t b_t, float* C, const float* resid, void* ws, size_t ws_bytes,
+                             cadet_stream_t stream);
 
 /* ------------------------------------------------------------------ instrumentation (bench / tests)
  * cadet_launch_count: number of libcadet kernels launched by this process so far.

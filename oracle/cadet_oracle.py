@@ -436,8 +436,12 @@ def heads_loss(z, bucket, label):
     return float(np.sum(softplus(zk) - label * zk))
 
 
-def heads_loss_backward(H, rows, W1, b1, w2, b2, bucket, label):
-    """Routed BCE adjoint: dz_{k_t} = sigma(z_{k_t}) - y_t, 0 for other heads."""
+def heads_loss_backward(H, rows, W1, b1, w2, b2, bucket, label, relu_active=None):
+    """Routed BCE adjoint: dz_{k_t} = sigma(z_{k_t}) - y_t, 0 for other heads.
+
+    relu_active (optional, [K][n, dh] bool): the ReLU derivative's 0/1 decision taken from the
+    implementation under test, for pre-activations at the kink (|pre| ~ rounding) where the two
+    sides may round to opposite signs; default pre > 0."""
     z, pre, hid = heads_forward(H, rows, W1, b1, w2, b2)
     n, K = z.shape
     dz = np.zeros_like(z)
@@ -449,7 +453,8 @@ def heads_loss_backward(H, rows, W1, b1, w2, b2, bucket, label):
     db2 = dz.sum(axis=0)
     dHr = np.zeros_like(Hr)
     for k in range(K):
-        dhid = dz[:, k:k + 1] * w2[k][None, :] * (pre[k] > 0)
+        act = (pre[k] > 0) if relu_active is None else np.asarray(relu_active[k], dtype=bool)
+        dhid = dz[:, k:k + 1] * w2[k][None, :] * act
         dW1[k] = Hr.T @ dhid
         db1[k] = dhid.sum(axis=0)
         dw2[k] = hid[k].T @ dz[:, k]
@@ -515,7 +520,8 @@ def heads_backward_dz(H, rows, W1, b1, w2, b2, dz):
              dw2=np.zeros_like(w2, dtype=np.float64), db2=dz.sum(axis=0))
     dHr = np.zeros_like(Hr)
     for k in range(K):
-        dhid = dz[:, k:k + 1] * w2[k][None, :] * (pre[k] > 0)
+        act = (pre[k] > 0) if relu_active is None else np.asarray(relu_active[k], dtype=bool)
+        dhid = dz[:, k:k + 1] * w2[k][None, :] * act
         g["dW1"][k] = Hr.T @ dhid
         g["db1"][k] = dhid.sum(axis=0)
         g["dw2"][k] = hid[k].T @ dz[:, k]

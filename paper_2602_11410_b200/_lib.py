@@ -130,6 +130,8 @@ SIGNATURES = {
     "cadet_pack": (I32, [P, P, P, I32, I32, I32, P, P, P, P, P, P, P, P, SZ, P]),
     "cadet_pack_workspace_bytes": (SZ, [I32]),
     "cadet_gemm": (I32, [I32, I32, I32, P, I32, P, I32, P, I32, P, P]),
+    "cadet_gemm_fp32_workspace_bytes": (SZ, [I32, I32, I32]),
+    "cadet_gemm_fp32": (I32, [I32, I32, I32, P, I32, P, I32, P, P, P, SZ, P]),
     "cadet_poll": (I32, [P, P]),
     "cadet_launch_count": (I64, []),
     "cadet_prof_enable": (I32, [I32, I32]),

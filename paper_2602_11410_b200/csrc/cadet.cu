@@ -10,6 +10,7 @@
 #include <string>
 
 #include "../../include/cadet.h"
+#include "fp32.cuh"
 #include "gemm.cuh"
 #include "layer.cuh"
 #include "plan.cuh"
@@ -48,7 +49,7 @@ cadet_status check_cfg(const cadet_attn_config* c) {
   // per-row head sums (attn_bwd_pre_kernel) and the per-head plan arrays hold at most 128 heads
   if (c->n_heads > 128) return fail(CADET_E_ARG, "n_heads %d > 128", c->n_heads);
   if (c->d_model % 32) return fail(CADET_E_ARG, "d_model %d must be a multiple of 32", c->d_model);
-  if (c->dtype != CADET_BF16) return fail(CADET_E_UNSUPPORTED, "dtype %d not supported (bf16 only in v1)", c->dtype);
+  if (c->dtype != CADET_BF16 && c->dtype != CADET_FP32) return fail(CADET_E_ARG, "dtype %d unknown", c->dtype);
   if (c->deterministic) return fail(CADET_E_UNSUPPORTED, "deterministic mode not implemented in v1");
   if (c->delta_delay_ms < 0 || c->delta_cand_ms < 0) return fail(CADET_E_ARG, "negative delta");
   if (c->use_rope && (c->rope_delta_t_max_ms <= 0 || c->rope_phi_min <= 0 || c->rope_base <= 1.0))
@@ -221,6 +222,22 @@ cadet_status cadet_gemm(int32_t M, int32_t N, int32_t K, const void* A, int32_t 
   g.epi.resid_f32 = c_f32;
   const int bn = (N % 256 == 0 && M >= 256) ? 256 : 128;  // 256 -> CTA-pair (cta_group::2) kernel
   return cuda_check(gemm_launch(&g, 1, bn, reinterpret_cast<cudaStream_t>(stream)), "gemm");
+}
+
+size_t cadet_gemm_fp32_workspace_bytes(int32_t M, int32_t N, int32_t K) {
+  if (M <= 0 || N <= 0 || K <= 0) return 0;
+  return gemm3x_scratch_bytes(M, N, K);
+}
+
+cadet_status cadet_gemm_fp32(int32_t M, int32_t N, int32_t K, const float* A, int32_t a_t, const float* B,
+                             int32_t b_t, float* C, const float* resid, void* ws, size_t ws_bytes,
+                             cadet_stream_t stream) {
+  if (!A || !B || !C || M <= 0 || N <= 0 || K <= 0 || (!ws && ws_bytes)) return fail(CADET_E_ARG, "cadet_gemm_fp32 args");
+  if (N % 32) return fail(CADET_E_ARG, "cadet_gemm_fp32: N %% 32 != 0");
+  const size_t need = gemm3x_scratch_bytes(M, N, K);
+  if (ws_bytes < need) return fail(CADET_E_WORKSPACE, "workspace %zu < required %zu", ws_bytes, need);
+  return cuda_check(gemm3x(M, N, K, A, a_t, B, b_t, C, resid, ws, reinterpret_cast<cudaStream_t>(stream)),
+                    "gemm fp32");
 }
 
 }  // extern "C"

@@ -4,6 +4,7 @@
 #include <string.h>
 
 #include "../../include/cadet.h"
+#include "fp32.cuh"
 #include "gemm.cuh"
 #include "layer.cuh"
 #include "misc.cuh"
@@ -98,6 +99,9 @@ cadet_status cadet_attn_core_forward(const cadet_attn_config* cfg, const cadet_b
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   if (!cfg->plan_ready && (s = cadet_mask_plan(cfg, b, ws, ws_bytes, stream))) return s;
   PlanView v = plan_carve(ws, b->n_seqs, b->total_tokens, b->total_tokens);
+  if (cfg->dtype == CADET_FP32)  // fp32 Qr, Kr, V in; fp32 O out
+    return cuda_err(attn_fwd_f32(cfg, b, v, (const float*)Qr, (const float*)Kr, (const float*)V, (float*)O, lse, st),
+                    "attention forward (fp32)");
   AttnParams p = attn_params(cfg, b, v);
   p.O = O;
   p.lse = lse;
@@ -130,6 +134,10 @@ cadet_status cadet_attn_core_backward(const cadet_attn_config* cfg, const cadet_
   if (!cfg->plan_ready && (s = cadet_mask_plan(cfg, b, ws, ws_bytes, stream))) return s;
   PlanView v = plan_carve(ws, b->n_seqs, T, T);
   float* D = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ws) + pb);
+  if (cfg->dtype == CADET_FP32)  // every tensor fp32
+    return cuda_err(attn_bwd_f32(cfg, b, v, (const float*)Qr, (const float*)Kr, (const float*)V, (const float*)O, lse,
+                                 (const float*)dO, D, dQr, (float*)dKr, (float*)dV, st),
+                    "attention backward (fp32)");
   AttnParams p = attn_params(cfg, b, v);
   p.lse = const_cast<float*>(lse);
   p.D = D;
@@ -184,6 +192,7 @@ LayerBufs carve_saved(void* saved, const cadet_attn_config* c, int T) {
   return L;
 }
 size_t saved_bytes(const cadet_attn_config* c, int T) {
+  if (c->dtype == CADET_FP32) return f32_saved_bytes(c, T);
   return 10 * bf_sz(T, c->d_model) + a256((size_t)4 * c->n_heads * T);
 }
 size_t layer_ws_base_bytes(const cadet_attn_config* c, int n, int T) {
@@ -192,6 +201,7 @@ size_t layer_ws_base_bytes(const cadet_attn_config* c, int n, int T) {
          a256((size_t)4 * c->n_heads * T) + 8 * bf_sz(T, d) + 4 * f_sz(T, d) + (c->out_f32 ? N_TAPS * f_sz(T, d) : 0);
 }
 size_t layer_ws_bytes(const cadet_attn_config* c, int n, int T) {
+  if (c->dtype == CADET_FP32) return f32_layer_ws_bytes(c, n, T);
   return layer_ws_base_bytes(c, n, T) + fwd_split_bytes(c, n, T);
 }
 // Two-pass attention backward: dS^T tile slots (sum over sequences of nq_s (nq_s + 1) / 2, bounded
@@ -310,7 +320,7 @@ size_t cadet_attn_workspace_bytes(const cadet_attn_config* c, int32_t n, int32_t
   return layer_ws_bytes(c, n, T);
 }
 size_t cadet_attn_bwd_ds_bytes(const cadet_attn_config* c, int32_t n, int32_t T, int32_t max_seqlen) {
-  if (check_cfg(c) || n < 0 || T < 0 || max_seqlen < 1) return 0;
+  if (check_cfg(c) || n < 0 || T < 0 || max_seqlen < 1 || c->dtype == CADET_FP32) return 0;
   return ds_bytes_of(c, n, T, max_seqlen);
 }
 size_t cadet_attn_saved_bytes(const cadet_attn_config* c, int32_t T) {
@@ -325,6 +335,10 @@ cadet_status cadet_attn_stage_views(const cadet_attn_config* cfg, int32_t n, int
   if (!ws || !views_h || n < 0 || T < 0) {
     set_error("cadet_attn_stage_views: null pointer or negative size");
     return CADET_E_ARG;
+  }
+  if (cfg->dtype == CADET_FP32) {
+    set_error("cadet_attn_stage_views: bf16 layer only (the fp32 mode stores every stage in fp32)");
+    return CADET_E_UNSUPPORTED;
   }
   const size_t need = layer_ws_bytes(cfg, n, T);
   if (ws_bytes < need) return ws_err(ws_bytes, need);
@@ -354,6 +368,9 @@ cadet_status cadet_attn_forward(const cadet_attn_config* cfg, const cadet_batch*
   if (T == 0) return CADET_OK;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   if (!cfg->plan_ready && (s = cadet_mask_plan(cfg, b, ws, ws_bytes, stream))) return s;
+  if (cfg->dtype == CADET_FP32)  // X, Y, resid, weights fp32 (3xTF32 GEMMs)
+    return cuda_err(layer_forward_f32(cfg, b, w, (const float*)X, (float*)Y, (const float*)resid, saved, ws, st),
+                    "attention layer forward (fp32)");
   PlanView v = plan_carve(ws, n, T, T);
   LayerBufs L = carve_saved(saved, cfg, T);
   LayerWs W = carve_ws(ws, cfg, n, T);
@@ -461,6 +478,10 @@ cadet_status cadet_attn_backward_ev(const cadet_attn_config* cfg, const cadet_ba
   if (T == 0) return CADET_OK;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   if (!cfg->plan_ready && (s = cadet_mask_plan(cfg, b, ws, ws_bytes, stream))) return s;
+  if (cfg->dtype == CADET_FP32)  // X, dY, dX, dresid, weights fp32 (3xTF32 GEMMs)
+    return cuda_err(layer_backward_f32(cfg, b, w, (const float*)X, saved, (const float*)dY, (float*)dX,
+                                       (const float*)dresid, gr, ws, st, grad_events),
+                    "attention layer backward (fp32)");
   PlanView v = plan_carve(ws, n, T, T);
   LayerBufs L = carve_saved(const_cast<void*>(saved), cfg, T);
   LayerWs W = carve_ws(ws, cfg, n, T);
@@ -644,15 +665,16 @@ static cadet_status check_head(const cadet_head_config* h, const cadet_head_weig
     set_error("heads: K >= 1, d_model % 8 == 0, d_hidden % 8 == 0 and >= 32, K*d_hidden % 32 == 0 required");
     return CADET_E_ARG;
   }
-  if (h->dtype != CADET_BF16) {
-    set_error("heads: bf16 only");
-    return CADET_E_UNSUPPORTED;
+  if (h->dtype != CADET_BF16 && h->dtype != CADET_FP32) {
+    set_error("heads: dtype must be CADET_BF16 or CADET_FP32");
+    return CADET_E_ARG;
   }
   return CADET_OK;
 }
 
 size_t cadet_heads_workspace_bytes(const cadet_head_config* h, int32_t n) {
   if (!h || n < 0) return 0;
+  if (h->dtype == CADET_FP32) return f32_heads_ws_bytes(h, n);
   const int N = h->K * h->d_hidden;
   return 256 + a256((size_t)n * h->d_model * 2) + a256((size_t)n * N * 2) * 2 + a256((size_t)n * 4) +
          a256((size_t)h->d_model * N * 2);
@@ -677,6 +699,9 @@ cadet_status cadet_heads_forward(const cadet_head_config* h, const cadet_head_we
   if (ws_bytes < need) return ws_err(ws_bytes, need);
   if (n == 0) return CADET_OK;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (h->dtype == CADET_FP32)
+    return cuda_err(heads_forward_f32(h, w, (const float*)Hs, rows, n, logits, (float*)pre_out, ws, st),
+                    "heads forward (fp32)");
   const int d = h->d_model, N = h->K * h->d_hidden;
   uint8_t* p = reinterpret_cast<uint8_t*>(ws);
   uint32_t* err = reinterpret_cast<uint32_t*>(p);
@@ -715,6 +740,10 @@ cadet_status cadet_heads_backward(const cadet_head_config* h, const cadet_head_w
   const size_t need = cadet_heads_workspace_bytes(h, n);
   if (ws_bytes < need) return ws_err(ws_bytes, need);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (h->dtype == CADET_FP32)
+    return cuda_err(heads_backward_f32(h, w, (const float*)Hs, rows, n, T, (const float*)pre, dz, nullptr, nullptr,
+                                       nullptr, nullptr, accumulate, (float*)dHs, gr, ws, st),
+                    "heads backward (fp32)");
   const int d = h->d_model, N = h->K * h->d_hidden;
   uint8_t* p = reinterpret_cast<uint8_t*>(ws);
   uint32_t* err = reinterpret_cast<uint32_t*>(p);
@@ -769,6 +798,10 @@ cadet_status cadet_heads_loss_backward(const cadet_head_config* h, const cadet_h
   const size_t need = cadet_heads_workspace_bytes(h, n);
   if (ws_bytes < need) return ws_err(ws_bytes, need);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (h->dtype == CADET_FP32)
+    return cuda_err(heads_backward_f32(h, w, (const float*)Hs, rows, n, T, (const float*)pre, nullptr, logits, bucket,
+                                       label, loss_sum, 0, (float*)dHs, gr, ws, st),
+                    "heads backward (fp32)");
   const int d = h->d_model, N = h->K * h->d_hidden;
   uint8_t* p = reinterpret_cast<uint8_t*>(ws);
   uint32_t* err = reinterpret_cast<uint32_t*>(p);
@@ -877,7 +910,8 @@ namespace cadet {
 // per-step RoPE table, so the layer calls of the step skip it.
 cudaError_t layer_plan_extras(const cadet_attn_config* cfg, const cadet_batch* b, void* ws, size_t ws_bytes,
                               cudaStream_t st) {
-  if (!cfg->use_rope || ws_bytes < layer_ws_bytes(cfg, b->n_seqs, b->total_tokens) || b->total_tokens == 0)
+  if (!cfg->use_rope || cfg->dtype == CADET_FP32 || ws_bytes < layer_ws_bytes(cfg, b->n_seqs, b->total_tokens) ||
+      b->total_tokens == 0)
     return cudaSuccess;
   PlanView v = plan_carve(ws, b->n_seqs, b->total_tokens, b->total_tokens);
   LayerWs W = carve_ws(ws, cfg, b->n_seqs, b->total_tokens);

@@ -25,7 +25,7 @@ struct KProb {
   int32_t M, N, nseg, kb_total, split_k, m_tiles, n_tiles, unit_begin;
   int32_t kb[GEMM_MAX_SEG];
   int32_t a_mn[GEMM_MAX_SEG], b_mn[GEMM_MAX_SEG];
-  int32_t f16;
+  int32_t f16, tf32;
   EpiParams epi;
 };
 
@@ -485,7 +485,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_kernel(const __grid_cons
           if (use > 0) mbar_wait(&empty[stage], (use - 1) & 1);
           int seg, kk;
           kb_to_seg(q, kb, seg, kk);
-          const int k0 = kk * BK;
+          const int k0 = kk * (q.tf32 ? BK / 2 : BK);  // a 128-byte K row: 64 bf16 / 32 fp32
           uint8_t* sA = smem + stage * C::STAGE_BYTES;
           uint8_t* sB = sA + C::A_BYTES;
           mbar_expect_tx(&full[stage], C::STAGE_BYTES);
@@ -523,16 +523,24 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_kernel(const __grid_cons
           int seg, kk;
           kb_to_seg(q, kb, seg, kk);
           const uint32_t a_mn = q.a_mn[seg], b_mn = q.b_mn[seg];
-          const uint32_t idesc = idesc_bf16(BM, BN, a_mn, b_mn) & (q.f16 ? ~((7u << 7) | (7u << 10)) : ~0u);  // F16: format 0
           const uint32_t sA = smem_u32(smem + stage * C::STAGE_BYTES);
           const uint32_t sB = sA + C::A_BYTES;
+          if (q.tf32) {  // K-major fp32 tiles: 4 x (K = 8) per 128-byte row, same 32-byte descriptor steps
+            const uint32_t idesc = idesc_tf32(BM, BN);
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k) {
-            const uint64_t ad = a_mn ? smem_desc(sA + k * 2048, 8192, 1024, SWZ_128B)
-                                     : smem_desc(sA + k * 32, 16, 1024, SWZ_128B);
-            const uint64_t bd = b_mn ? smem_desc(sB + k * 2048, 8192, 1024, SWZ_128B)
-                                     : smem_desc(sB + k * 32, 16, 1024, SWZ_128B);
-            mma_bf16_ss(d_tmem, ad, bd, idesc, (kb > U.kb_lo || k > 0) ? 1u : 0u);
+            for (int k = 0; k < BK / 16; ++k)
+              mma_tf32_ss(d_tmem, smem_desc(sA + k * 32, 16, 1024, SWZ_128B), smem_desc(sB + k * 32, 16, 1024, SWZ_128B),
+                          idesc, (kb > U.kb_lo || k > 0) ? 1u : 0u);
+          } else {
+            const uint32_t idesc = idesc_bf16(BM, BN, a_mn, b_mn) & (q.f16 ? ~((7u << 7) | (7u << 10)) : ~0u);  // F16: format 0
+#pragma unroll
+            for (int k = 0; k < BK / 16; ++k) {
+              const uint64_t ad = a_mn ? smem_desc(sA + k * 2048, 8192, 1024, SWZ_128B)
+                                       : smem_desc(sA + k * 32, 16, 1024, SWZ_128B);
+              const uint64_t bd = b_mn ? smem_desc(sB + k * 2048, 8192, 1024, SWZ_128B)
+                                       : smem_desc(sB + k * 32, 16, 1024, SWZ_128B);
+              mma_bf16_ss(d_tmem, ad, bd, idesc, (kb > U.kb_lo || k > 0) ? 1u : 0u);
+            }
           }
           mma_commit(&empty[stage]);
         }
@@ -789,9 +797,17 @@ static int num_sms() {
   return n;
 }
 
-static bool make_operand_map(CUtensorMap* m, const OperandDesc& o, int box_rows_kmajor) {
+static bool make_operand_map(CUtensorMap* m, const OperandDesc& o, int box_rows_kmajor, int tf32) {
+  const uint64_t ld = o.ld > 0 ? (uint64_t)o.ld : (uint64_t)o.cols;
+  if (tf32) {  // fp32 K-major: 32-element (128-byte) K boxes, TMA zero-fills the K tail
+    if (o.mn_major || (ld * 4) % 16) return false;
+    uint64_t dims[2] = {(uint64_t)o.cols, (uint64_t)o.rows};
+    uint64_t strides[1] = {ld * 4};
+    uint32_t box[2] = {32, (uint32_t)box_rows_kmajor};
+    return encode_map(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, o.ptr, 2, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B);
+  }
   uint64_t dims[2] = {(uint64_t)o.cols, (uint64_t)o.rows};
-  uint64_t strides[1] = {(uint64_t)o.cols * 2};
+  uint64_t strides[1] = {ld * 2};
   uint32_t box[2];
   if (!o.mn_major) {
     box[0] = 64;
@@ -880,7 +896,7 @@ cudaError_t gemm_launch(const GemmProblem* probs, int nprob, int bn, cudaStream_
   P.nprob = nprob;
   // CTA pairs (cta_group::2, 256 x 256 tiles) whenever the N tile is 256 and every M spans a pair tile
   bool pair = bn == 256;
-  for (int p = 0; p < nprob; ++p) pair = pair && probs[p].M >= 256;
+  for (int p = 0; p < nprob; ++p) pair = pair && probs[p].M >= 256 && !probs[p].tf32;
   P.bm = pair ? 256 : BM;
   int total = 0;
   for (int p = 0; p < nprob; ++p) {
@@ -894,16 +910,18 @@ cudaError_t gemm_launch(const GemmProblem* probs, int nprob, int bn, cudaStream_
     for (int s = 0; s < g.nseg; ++s) {
       const OperandDesc& A = g.A[s];
       const OperandDesc& B = g.B[s];
-      if (A.cols % 8 || B.cols % 8 || g.K[s] <= 0) return cudaErrorInvalidValue;
-      if (!make_operand_map(&P.mA[p][s], A, BM)) return cudaErrorInvalidValue;
-      if (!make_operand_map(&P.mB[p][s], B, pair ? 128 : bn)) return cudaErrorInvalidValue;
+      if ((!g.tf32 && (A.cols % 8 || B.cols % 8)) || g.K[s] <= 0) return cudaErrorInvalidValue;
+      if (!make_operand_map(&P.mA[p][s], A, BM, g.tf32)) return cudaErrorInvalidValue;
+      if (!make_operand_map(&P.mB[p][s], B, pair ? 128 : bn, g.tf32)) return cudaErrorInvalidValue;
       q.a_mn[s] = A.mn_major;
       q.b_mn[s] = B.mn_major;
-      q.kb[s] = (g.K[s] + BK - 1) / BK;
+      const int bke = g.tf32 ? BK / 2 : BK;
+      q.kb[s] = (g.K[s] + bke - 1) / bke;
       q.kb_total += q.kb[s];
     }
     q.split_k = g.split_k < 1 ? 1 : (g.split_k > q.kb_total ? q.kb_total : g.split_k);
     q.f16 = g.f16;
+    q.tf32 = g.tf32;
     q.m_tiles = (g.M + P.bm - 1) / P.bm;
     q.n_tiles = (g.N + bn - 1) / bn;
     q.unit_begin = total;

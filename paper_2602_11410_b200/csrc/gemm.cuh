@@ -53,9 +53,10 @@ struct EpiParams {
 };
 
 struct OperandDesc {
-  const void* ptr;  // bf16, row-major storage [rows][cols]
+  const void* ptr;  // bf16 (fp32 for tf32 problems), row-major storage [rows][cols] (row stride ld if > 0)
   int32_t rows, cols;
   int32_t mn_major; // 0: storage is [MN][K] (K-major); 1: storage is [K][MN] (MN-major)
+  int32_t ld;       // row stride in elements (0 = cols)
 };
 
 constexpr int GEMM_MAX_PROB = 4;
@@ -68,6 +69,7 @@ struct GemmProblem {
   OperandDesc A[GEMM_MAX_SEG], B[GEMM_MAX_SEG];
   int32_t split_k;   // > 1 only with EPI_ATOMIC
   int32_t f16;       // operands are fp16 instead of bf16 (both A and B)
+  int32_t tf32;      // operands are fp32 (both K-major), multiplied as TF32 (kind::tf32; CADET_FP32 mode)
   EpiParams epi;
 };
 

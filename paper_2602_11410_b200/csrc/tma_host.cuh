@@ -23,9 +23,16 @@ inline PFN_encodeTiled get_encode_fn() {
   return fn;
 }
 
+// dims[0] innermost; strides_bytes has rank-1 entries (dims 1..rank-1).
+inline bool encode_map(CUtensorMap* m, CUtensorMapDataType dt, const void* ptr, int rank, const uint64_t* dims,
+                       const uint64_t* strides_bytes, const uint32_t* box, CUtensorMapSwizzle swz);
 // bf16 tensor, dims[0] innermost; strides_bytes has rank-1 entries (dims 1..rank-1).
 inline bool encode_bf16_map(CUtensorMap* m, const void* ptr, int rank, const uint64_t* dims,
                             const uint64_t* strides_bytes, const uint32_t* box, CUtensorMapSwizzle swz) {
+  return encode_map(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, ptr, rank, dims, strides_bytes, box, swz);
+}
+inline bool encode_map(CUtensorMap* m, CUtensorMapDataType dt, const void* ptr, int rank, const uint64_t* dims,
+                       const uint64_t* strides_bytes, const uint32_t* box, CUtensorMapSwizzle swz) {
   PFN_encodeTiled fn = get_encode_fn();
   if (!fn) return false;
   cuuint64_t d[5], s[4];
@@ -36,7 +43,7 @@ inline bool encode_bf16_map(CUtensorMap* m, const void* ptr, int rank, const uin
     e[i] = 1;
   }
   for (int i = 0; i < rank - 1; ++i) s[i] = strides_bytes[i];
-  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(ptr), d, s, b, e,
+  CUresult r = fn(m, dt, rank, const_cast<void*>(ptr), d, s, b, e,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;

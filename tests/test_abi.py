@@ -51,9 +51,19 @@ def test_host_validation_errors_without_gpu():
     c = _lib.default_config(100, 3)   # d % H != 0
     b = _lib.BatchStruct()
     assert L.cadet_mask_plan(C.byref(c), C.byref(b), None, 0, None) == 1
-    c = _lib.default_config(64, 1)    # head_dim 64 ok, dtype fp32 unsupported
+    c = _lib.default_config(64, 1)    # head_dim 64 ok, unknown dtype
+    c.dtype = 7
+    assert L.cadet_mask_plan(C.byref(c), C.byref(b), None, 0, None) == 1
+    c = _lib.default_config(2048, 256)  # head_dim 8 is not a supported head size; H > 128
+    assert L.cadet_mask_plan(C.byref(c), C.byref(b), None, 0, None) == 1
+    c = _lib.default_config(8192, 256)  # head_dim 32 ok, but H > 128
+    assert L.cadet_mask_plan(C.byref(c), C.byref(b), None, 0, None) == 1
+    c = _lib.default_config(64, 1)    # the fp32 parity mode: sizes follow the fp32 layout
     c.dtype = 1
-    assert L.cadet_mask_plan(C.byref(c), C.byref(b), None, 0, None) == 9
+    c16 = _lib.default_config(64, 1)
+    assert L.cadet_attn_saved_bytes(C.byref(c), 1000) > L.cadet_attn_saved_bytes(C.byref(c16), 1000)
+    assert L.cadet_attn_bwd_ds_bytes(C.byref(c), 1, 1000, 1000) == 0
+    assert L.cadet_gemm_fp32_workspace_bytes(100, 64, 30) == 2 * 12800 + 2 * 8192  # K padded to 32
     assert L.cadet_gemm(0, 32, 32, None, 0, None, 0, None, 1, None, None) == 1
 
 
