@@ -50,6 +50,8 @@ class StackConfig:
                                  # this rank's shard of master params + moments, all-gather bf16 params)
     lr: float = 1e-4
     weight_decay: float = 0.0
+    taps: bool = False           # parity taps (cfg.out_f32 = 1 on the layer calls): fp32 stage values in the
+                                 # workspace, read with cadet_attn_stage_views (tests only; ~2x the layer time)
 
     @property
     def dh(self) -> int:
@@ -241,7 +243,8 @@ class CadetStack:
         self.cfg = cfg
         self.dev = torch.device(device)
         d, T, nl = cfg.d_model, cfg.budget, cfg.n_layers
-        self.acfg = ops.config(d, cfg.n_heads, delta_delay_ms=cfg.delta_delay_ms, mask_flags=cfg.mask_flags)
+        self.acfg = ops.config(d, cfg.n_heads, delta_delay_ms=cfg.delta_delay_ms, mask_flags=cfg.mask_flags,
+                               out_f32=1 if cfg.taps else 0)
         # ONE flat layout for gradients and parameters: 7 d^2 per layer (+ the block's FFN and RMSNorm
         # scales, NEXT-3), the towers (+ the aux heads, NEXT-2); every slice starts on a 256-byte
         # boundary (the split-K weight-gradient epilogue adds float4 atomics) and the total is padded to

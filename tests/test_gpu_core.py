@@ -296,3 +296,78 @@ def test_attn_core_forward(ops, case):
     assert_close(to_np(Og), Oref, what="O")
     assert_close(to_np(lseg), lref, what="LSE")
     assert (to_np(Og)[cu[-1]:] == 0).all()
+
+
+# ------------------------------------------------------------------ device-latched input errors (cadet.h)
+@pytest.mark.parametrize("kind", ["offsets_start", "offsets_decreasing", "offsets_past_T", "too_long", "cand"])
+def test_mask_plan_device_latches(ops, kind):
+    """Each device-detected input error of cadet_mask_plan latches its bit and cadet_poll returns it
+    (then clears it): OFFSETS, TOO_LONG, CAND."""
+    from paper_2602_11410_b200 import _lib
+    T = 300
+    cu = np.array([0, 100, 250], np.int32)
+    nc = np.zeros(2, np.int32)
+    maxlen = 256
+    want = {"offsets_start": 2, "offsets_decreasing": 2, "offsets_past_T": 2, "too_long": 4, "cand": 5}[kind]
+    if kind == "offsets_start":
+        cu = np.array([1, 100, 250], np.int32)
+    elif kind == "offsets_decreasing":
+        cu = np.array([0, 100, 90], np.int32)
+    elif kind == "offsets_past_T":
+        cu = np.array([0, 100, 301], np.int32)
+    elif kind == "too_long":
+        maxlen = 120
+    elif kind == "cand":
+        nc = np.array([0, 151], np.int32)
+    t = np.arange(T, dtype=np.int64) * 1000
+    cfg = ops.config(32, 1)
+    b = to_dev_batch(cu, t, np.zeros(T, np.int32), nc, T, max_seqlen=maxlen)
+    ws = ops.plan_workspace(b)
+    ops.mask_plan(cfg, b, ws)
+    with pytest.raises(_lib.CadetError) as e:
+        ops.poll(ws)
+    assert e.value.status == want
+    ops.poll(ws)  # the word was cleared
+
+
+@pytest.mark.parametrize("dtype", [0, 1])
+@pytest.mark.parametrize("kind", ["bucket", "nonfinite"])
+def test_heads_device_latches(ops, kind, dtype):
+    """Routed BCE (Eq. 9): a bucket outside [0, K) latches BUCKET ("routing error"); a non-finite
+    loss latches NONFINITE (fail-fast numerics).  bf16 and fp32 towers."""
+    import ctypes as C
+    from paper_2602_11410_b200 import _lib as L
+    n, T, d, K, dh = 40, 64, 64, 2, 32
+    rng = np.random.default_rng(1)
+    el = torch.float32 if dtype else torch.bfloat16
+    Hs = torch.tensor(rng.standard_normal((T, d)), dtype=torch.float32, device="cuda").to(el)
+    W1 = torch.tensor(rng.standard_normal((d, K * dh)) * 0.1, dtype=torch.float32, device="cuda").to(el)
+    b1, w2 = (torch.zeros(K * dh, device="cuda") for _ in range(2))
+    b2 = torch.zeros(K, device="cuda")
+    rows = torch.arange(n, dtype=torch.int32, device="cuda")
+    bucket = torch.zeros(n, dtype=torch.int32, device="cuda")
+    label = torch.zeros(n, device="cuda")
+    logits = torch.zeros(n, K, device="cuda")
+    if kind == "bucket":
+        bucket[7] = K
+    else:
+        logits[3, 0] = float("nan")
+    hc = L.HeadConfig(K, d, dh, dtype)
+    hw = L.HeadWeights(W1.data_ptr(), b1.data_ptr(), w2.data_ptr(), b2.data_ptr())
+    ws = ops.workspace(L.lib().cadet_heads_workspace_bytes(C.byref(hc), n))
+    ws.zero_()
+    pre = torch.zeros(n, K * dh, dtype=el, device="cuda")
+    loss = torch.zeros(1, device="cuda")
+    dH = torch.empty(T, d, dtype=el, device="cuda")
+    gr = [torch.empty(d, K * dh, device="cuda"), torch.empty(K * dh, device="cuda"), torch.empty(K * dh, device="cuda"),
+          torch.empty(K, device="cuda")]
+    hg = L.HeadGrads(*[x.data_ptr() for x in gr])
+    L.check(L.lib().cadet_heads_loss_backward(C.byref(hc), C.byref(hw), C.c_void_p(Hs.data_ptr()),
+                                              C.c_void_p(rows.data_ptr()), n, T, C.c_void_p(logits.data_ptr()),
+                                              C.c_void_p(pre.data_ptr()), C.c_void_p(bucket.data_ptr()),
+                                              C.c_void_p(label.data_ptr()), C.c_void_p(loss.data_ptr()),
+                                              C.c_void_p(dH.data_ptr()), C.byref(hg), C.c_void_p(ws.data_ptr()),
+                                              ws.numel(), C.c_void_p(torch.cuda.current_stream().cuda_stream)))
+    with pytest.raises(L.CadetError) as e:
+        ops.poll(ws)
+    assert e.value.status == (6 if kind == "bucket" else 7)

@@ -127,78 +127,13 @@ def run_case(ops, case, with_resid):
 
 @pytest.mark.parametrize("case", range(len(STAGE_CASES)))
 def test_layer_stages_forward_and_backward(ops, case):
+    from tests.stage_check import check_layer_stages
     r = run_case(ops, case, with_resid=(case % 2 == 1))
-    cu, T, d, H, peaky = r["cu"], r["T"], r["d"], r["H"], r["peaky"]
-    n = int(cu[-1])
-    sv, tp, wb = r["sv"], r["taps"], r["wsb"]
-    Wxg, Wq, Wk, Wv, Wqg, Wkg, Wo = r["W"]
-    X = r["X"]
-    ocfg = oracle_cfg(r["cfg"])
-    t = r["t"]
-    rs = lambda a: a[:n]
-    # ---- forward: A2 (Eq. 4) fed the bf16 X
-    Zx = X @ Wxg
-    assert_close(rs(tp["Zx"]), rs(Zx), what="A2 Zx")
-    assert_close(rs(tp["Xt"]), rs(X * O.sigmoid(Zx)), what="A2 Xt")
-    # A3 (Eq. 3; R2) fed the GPU's bf16 Xt
-    for nm, Wi in (("Q", Wq), ("K", Wk), ("V", Wv)):
-        assert_close(rs(tp[nm]), rs(sv["Xt"] @ Wi), what="A3 " + nm)
-    # A4 (Eq. 5; RoPE P:274): Z from the bf16 Q/K, the rotation of Q * sigma(bf16 Z)
-    for nm, src, Wg, zn in (("Qr", "Q", Wqg, "Zq"), ("Kr", "K", Wkg, "Zk")):
-        assert_close(rs(tp[zn]), rs(sv[src] @ Wg), what="A4 " + zn)
-        assert_close(rs(tp[nm]), rs(O.rope_heads(sv[src] * O.sigmoid(sv[zn]), t, ocfg)), what="A4 " + nm)
-    # A5 (Eq. 7) fed the bf16 Qr, Kr, V
-    Oref, lref = np.zeros((T, d)), np.zeros((H, T))
-    for k in range(len(r["lengths"])):
-        a, e = cu[k], cu[k + 1]
-        A = O.seq_mask(r["meta"], k, ocfg)
-        o, l, _ = O.attention_core_forward(sv["Qr"][a:e], sv["Kr"][a:e], sv["V"][a:e], A, H)
-        Oref[a:e], lref[:, a:e] = o, l
-    peaky_ok("A5 O", tp["O"], Oref, peaky)
-    assert_close(sv["lse"], lref, what="A5 LSE")
-    # A6 fed the bf16 O (+ the bf16 residual)
-    Yref = sv["O"] @ Wo + (0 if r["R"] is None else r["R"])
-    assert_close(rs(tp["Y"]), rs(Yref), what="A6 Y")
-    assert (r["Y"][n:] == 0).all()
-    # ---- backward: A9 dO = dY W_o^T, D = rowsum(dO * O) per head (dO's fp32 value, bf16 O), dW_o = O^T dY
-    dY = r["dY"]
-    dOref = dY @ Wo.T
-    assert_close(rs(tp["dO"]), rs(dOref), what="A9 dO")
-    hd = d // H
-    Dref = np.stack([(dOref[:, h * hd:(h + 1) * hd] * sv["O"][:, h * hd:(h + 1) * hd]).sum(1) for h in range(H)])
-    assert_close(r["D"][:, :n], Dref[:, :n], what="A9/A10 D")
-    assert_close(r["gW"][6], sv["O"].T @ dY, what="A9 dW_o")
-    # A10 (adjoint of Eq. 7) fed the bf16 Qr, Kr, V and the bf16 dO it consumed
-    ref = [np.zeros((T, d)) for _ in range(3)]
-    for k in range(len(r["lengths"])):
-        a, e = cu[k], cu[k + 1]
-        A = O.seq_mask(r["meta"], k, ocfg)
-        out = O.attention_core_backward(sv["Qr"][a:e], sv["Kr"][a:e], sv["V"][a:e], A, wb["dO"][a:e], H)
-        for j in range(3):
-            ref[j][a:e] = out[j]
-    for nm, rf in zip(("dQr", "dKr", "dV"), ref):
-        peaky_ok("A10 " + nm, tp[nm], rf, peaky)
-    # A11 (adjoint of Eq. 5 and of the rotation) fed the bf16 dQr / dKr, Q / K and Z
-    for side, src, zn, Wg, gi in (("q", "Q", "Zq", Wqg, 4), ("k", "K", "Zk", Wkg, 5)):
-        dr = wb["dQr"] if side == "q" else wb["dKr"]
-        dT = O.rope_heads(dr, t, ocfg, -1.0)
-        gg = O.sigmoid(sv[zn])
-        assert_close(rs(tp["u" + side]), rs(dT * sv[src] * gg * (1 - gg)), what="A11 u_" + side)
-        assert_close(rs(tp["r" + side]), rs(dT * gg), what="A11 r_" + side)
-        dname = "dQ" if side == "q" else "dK"
-        assert_close(rs(tp[dname]), rs(wb["r" + side] + wb["u" + side] @ Wg.T), what="A11 " + dname)
-        assert_close(r["gW"][gi], sv[src].T @ wb["u" + side], what="A11 dW_" + side + "g")
-    # A12 (adjoint of Eqs. 3-4) fed the bf16 dQ, dK, dV, X, Zx
-    dXt = wb["dQ"] @ Wq.T + wb["dK"] @ Wk.T + wb["dV"] @ Wv.T
-    gx = O.sigmoid(sv["Zx"])
-    assert_close(rs(tp["ux"]), rs(dXt * X * gx * (1 - gx)), what="A12 u_x")
-    rx = dXt * gx + (0 if r["R"] is None else dY)
-    assert_close(rs(tp["rx"]), rs(rx), what="A12 r_x")
-    assert_close(rs(tp["dX"]), rs(wb["rx"] + wb["ux"] @ Wxg.T), what="A12 dX")
-    for gi, src in ((1, wb["dQ"]), (2, wb["dK"]), (3, wb["dV"])):
-        assert_close(r["gW"][gi], sv["Xt"].T @ src, what=f"A12 dW {gi}")
-    assert_close(r["gW"][0], X.T @ wb["ux"], what="A12 dW_xg")
-    assert (r["dX"][n:] == 0).all()
+    n = int(r["cu"][-1])
+    check_layer_stages(r["X"], r["W"], r["sv"], r["taps"], r["wsb"], r["D"], r["dY"], r["meta"], oracle_cfg(r["cfg"]),
+                       range(len(r["lengths"])), resid=r["R"], dresid=None if r["R"] is None else r["dY"],
+                       peaky=r["peaky"], weight_grads=r["gW"], tag=f"case {case}")
+    assert (r["Y"][n:] == 0).all() and (r["dX"][n:] == 0).all()
 
 
 def test_taps_do_not_change_the_bf16_results(ops):
