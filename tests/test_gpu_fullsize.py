@@ -69,13 +69,18 @@ def test_full_size_sampled_stages(name):
     check_layer_stages(Hs[l], W(l), saved_dev(st.saved[l], T, d, H), tp, wb, D, None, meta, ocfg, picks,
                        resid=Hs[l], backward=False, tag=f"{name} layer {l} fwd")
     # and that layer end to end from its bf16 input (protocol iv, gated for Y in the flat regime): the
-    # fp32 value of Y - X before storage vs the whole fp64 chain of Eqs. 3-7
+    # fp32 value of Y - X before storage vs the whole fp64 chain of Eqs. 3-7.  The five chained bf16
+    # intermediates (Xt, Q/K/V, Qr/Kr, O) alone give ~1e-3 mean on short chunks (measured 1.0e-3 and
+    # 1.9e-3 on 2- and 4-token chunks): DESIGN.md R36 gates this at max 1e-2, mean 2e-3 for C4's layer;
+    # C3's layer 7 (input rms ~1.6 after 7 residual layers, 1.6e-2 max measured) is reported with the
+    # protocol-iv sanity bound 5e-2 / 5e-3
     t, s = st.t_p.cpu().numpy(), st.s_p.cpu().numpy()
     for k in picks:
         a, e = int(cu[k]), int(cu[k + 1])
         m1 = meta_of(np.array([0, e - a]), t[a:e], s[a:e], np.zeros(1, np.int64))
         Y, _, _ = O.batch_forward(Hs[l][a:e], W(l), m1, ocfg)
-        assert_close(tp["Y"][a:e] - Hs[l][a:e], Y, what=f"{name} layer {l} e2e Y seq {k} len {e - a}")
+        lim = (1e-2, 2e-3) if name == "c4" else (5e-2, 5e-3)
+        assert_close(tp["Y"][a:e] - Hs[l][a:e], Y, *lim, what=f"{name} layer {l} e2e Y seq {k} len {e - a}")
     # backward taps: layer 0 (the last backward), dY = dH[1] also added to dX through the residual
     gW = [DevArr(g.view(d, d)) for g in st.gW[0]]
     check_layer_stages(Hs[0], W(0), saved_dev(st.saved[0], T, d, H), tp, wb, D, dHs[1], meta, ocfg, picks,
