@@ -226,7 +226,8 @@ def run_oracle_step(seqs, wl: dict, seed: int):
         rows = np.arange(0, e - a, 2)
         Lh, z, dH, g = O.heads_loss_backward(X, rows, hw.W1.astype(np.float64), hw.b1.astype(np.float64),
                                              hw.w2.astype(np.float64), hw.b2.astype(np.float64),
-                                             u.buckets[a:e][rows], u.labels[a:e][rows].astype(np.float64))
+                                             O.bucketize(u.positions[a:e][rows], (4,)),
+                                             u.labels[a:e][rows].astype(np.float64))
         loss += Lh
         dX = dH
         for l in reversed(range(nl)):

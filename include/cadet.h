@@ -85,8 +85,12 @@ typedef struct {
                         taps (O, dQr, dKr, dV) come from a second run of the same deterministic kernels with
                         fp32 stores.  Parity / debugging only (about 2x the layer's time). */
   int32_t use_rope, use_rep_gate, use_int_gate, use_out_proj; /* ablation switches (Table 1) */
-  int32_t deterministic; /* reserved, must be 0 (attention fwd/bwd are atomic-free and deterministic; split-K
-                            weight gradients accumulate with fp32 atomics) */
+  int32_t deterministic; /* 0: split-K weight gradients and D = rowsum(dO * O) accumulate with fp32 atomics (order
+                            not fixed).  1 (bf16 only): bit-reproducible layer backward -- each split-K partial
+                            of a weight gradient goes to its own fp32 slab in ws (cadet_attn_workspace_bytes
+                            grows by 3 * splits * d^2 * 4 B) and a reduction sums the slabs in split order; D
+                            comes from the fixed-order preprocess kernel.  The attention kernels, the mask plan
+                            and every forward kernel are atomic-free in both modes (P:569 reproducibility). */
   int32_t plan_ready;    /* 0 = plan inside the call; 1 = ws already holds cadet_mask_plan's plan for this batch
                             (same ws, same batch): the layer/core calls skip re-planning (one plan per step for
                             all layers); 2 = as 1 and ws also holds the RoPE (cos, sin) table, which
@@ -353,6 +357,16 @@ cadet_status cadet_adamw_step(const cadet_adamw_config* c_h, int64_t step, const
 /* dst[i] = (float)src[i] for n bf16 elements (fp32-consumed parameters after a bf16 all-gather).
  * Both buffers 16-byte aligned. */
 cadet_status cadet_bf16_to_f32(const void* src, float* dst, int64_t n, cadet_stream_t stream);
+
+/* ------------------------------------------------------------------ context buckets
+ * "we partition the context space into K discrete buckets"; the deployed choice is K = 2,
+ * "positions 1--4, and 5+", i.e. boundaries {4}.  bucket[i] = #{j : raw_position[i] >
+ * boundaries_h[j]} (0-based: SPEC S:142-150's 1-based k minus one), so K = nb + 1 towers.
+ * raw_position int32 [n] (device, >= 1: a feed position); boundaries_h host, strictly increasing, 1 <= nb
+ * <= 32 (else CADET_E_ARG, synchronously); bucket int32 [n] (device, overwritten).  A position < 1 latches
+ * CADET_E_BUCKET in the error word at ws (>= 256 B; cadet_poll) and gets bucket 0. */
+cadet_status cadet_bucketize(const int32_t* raw_position, int32_t n, const int32_t* boundaries_h, int32_t nb,
+                             int32_t* bucket, void* ws, cadet_stream_t stream);
 
 /* ------------------------------------------------------------------ A0 / A13: chunk and pack
  * Chunk: split each sequence [a, e) of cu_in at e - L, e - 2L, ... (newest chunk full, oldest may be

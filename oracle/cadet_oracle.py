@@ -420,6 +420,17 @@ def packed_forward_blockdiag(X, W, meta: SeqMeta, cfg: AttnConfig, T: int):
 
 
 # ------------------------------------------------------------------ heads (Eqs. 8-9)
+def bucketize(raw_position, boundaries):
+    """Context bucket of a raw feed position ("partition the context space into K discrete
+    buckets"; deployed K = 2, "positions 1--4, and 5+"): the plain definition
+    k = #{b in boundaries : position > b}, 0-based (SPEC's 1-based k minus one)."""
+    pos = np.asarray(raw_position, dtype=np.int64)
+    k = np.zeros(pos.shape, dtype=np.int64)
+    for b in boundaries:
+        k += (pos > int(b)).astype(np.int64)
+    return k
+
+
 def heads_forward(H, rows, W1, b1, w2, b2):
     """z_k = w2_k . ReLU(H_r W1_k + b1_k) + b2_k for all k in one pass (R14)."""
     Hr = np.asarray(H, dtype=np.float64)[rows]
@@ -520,8 +531,7 @@ def heads_backward_dz(H, rows, W1, b1, w2, b2, dz):
              dw2=np.zeros_like(w2, dtype=np.float64), db2=dz.sum(axis=0))
     dHr = np.zeros_like(Hr)
     for k in range(K):
-        act = (pre[k] > 0) if relu_active is None else np.asarray(relu_active[k], dtype=bool)
-        dhid = dz[:, k:k + 1] * w2[k][None, :] * act
+        dhid = dz[:, k:k + 1] * w2[k][None, :] * (pre[k] > 0)
         g["dW1"][k] = Hr.T @ dhid
         g["db1"][k] = dhid.sum(axis=0)
         g["dw2"][k] = hid[k].T @ dz[:, k]

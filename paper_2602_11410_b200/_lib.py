@@ -127,6 +127,7 @@ SIGNATURES = {
     "cadet_adamw_step": (I32, [C.POINTER(AdamWConfig), C.c_int64, P, P, P, P, P, C.c_int64, P]),
     "cadet_bf16_to_f32": (I32, [P, P, C.c_int64, P]),
     "cadet_chunk": (I32, [P, I32, I32, P, I32, P, P, P]),
+    "cadet_bucketize": (I32, [P, I32, C.POINTER(I32), I32, P, P, P]),
     "cadet_pack": (I32, [P, P, P, I32, I32, I32, P, P, P, P, P, P, P, P, SZ, P]),
     "cadet_pack_workspace_bytes": (SZ, [I32]),
     "cadet_gemm": (I32, [I32, I32, I32, P, I32, P, I32, P, I32, P, P]),

@@ -850,6 +850,7 @@ __global__ void __launch_bounds__(256) attn_bwd_pre_kernel(const __nv_bfloat16* 
   pdl_trigger();
   pdl_wait();
   __shared__ float acc[8][128];
+  __shared__ float part[8][32];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int row = blockIdx.x * 8 + w;
   const int d = H * hd, lpg = hd / 8;  // lanes per head
@@ -875,8 +876,20 @@ __global__ void __launch_bounds__(256) attn_bwd_pre_kernel(const __nv_bfloat16* 
       if (seg) {
         for (int off = lpg >> 1; off > 0; off >>= 1) p += __shfl_xor_sync(0xffffffffu, p, off);
         if (valid && (lane & (lpg - 1)) == 0) acc[w][c / hd] += p;  // one lane per head segment
-      } else if (valid) {
-        atomicAdd(&acc[w][c / hd], p);
+      } else {  // head segments not aligned to lane groups (hd = 88): the lanes' partials summed in lane
+                // order by the first lane of each head (fixed order: deterministic)
+        __syncwarp();
+        part[w][lane] = valid ? p : 0.f;
+        __syncwarp();
+        const int h0 = c0 / hd, h1 = min((c0 + 255) / hd, H - 1);
+        for (int h = h0 + lane; h <= h1; h += 32) {
+          float sum = 0.f;
+          for (int l = 0; l < 32; ++l) {
+            const int cl = c0 + l * 8;
+            if (cl < d && cl / hd == h) sum += part[w][l];
+          }
+          acc[w][h] += sum;
+        }
       }
     }
   }

@@ -14,6 +14,7 @@
 #include "gemm.cuh"
 #include "layer.cuh"
 #include "plan.cuh"
+#include "misc.cuh"
 
 using namespace cadet;
 
@@ -50,7 +51,8 @@ cadet_status check_cfg(const cadet_attn_config* c) {
   if (c->n_heads > 128) return fail(CADET_E_ARG, "n_heads %d > 128", c->n_heads);
   if (c->d_model % 32) return fail(CADET_E_ARG, "d_model %d must be a multiple of 32", c->d_model);
   if (c->dtype != CADET_BF16 && c->dtype != CADET_FP32) return fail(CADET_E_ARG, "dtype %d unknown", c->dtype);
-  if (c->deterministic) return fail(CADET_E_UNSUPPORTED, "deterministic mode not implemented in v1");
+  if (c->deterministic && c->dtype != CADET_BF16)
+    return fail(CADET_E_UNSUPPORTED, "deterministic mode: bf16 layer only (the fp32 parity mode reduces with atomics)");
   if (c->delta_delay_ms < 0 || c->delta_cand_ms < 0) return fail(CADET_E_ARG, "negative delta");
   if (c->use_rope && (c->rope_delta_t_max_ms <= 0 || c->rope_phi_min <= 0 || c->rope_base <= 1.0))
     return fail(CADET_E_ARG, "invalid RoPE constants");
@@ -222,6 +224,22 @@ cadet_status cadet_gemm(int32_t M, int32_t N, int32_t K, const void* A, int32_t 
   g.epi.resid_f32 = c_f32;
   const int bn = (N % 256 == 0 && M >= 256) ? 256 : 128;  // 256 -> CTA-pair (cta_group::2) kernel
   return cuda_check(gemm_launch(&g, 1, bn, reinterpret_cast<cudaStream_t>(stream)), "gemm");
+}
+
+cadet_status cadet_bucketize(const int32_t* raw_position, int32_t n, const int32_t* boundaries_h, int32_t nb,
+                             int32_t* bucket, void* ws, cadet_stream_t stream) {
+  if (n < 0 || (n > 0 && (!raw_position || !bucket)) || !ws || !boundaries_h) return fail(CADET_E_ARG, "cadet_bucketize args");
+  if (nb < 1 || nb > 32) return fail(CADET_E_ARG, "cadet_bucketize: 1 <= nb <= 32 boundaries");
+  Bounds bd;
+  memset(&bd, 0, sizeof(bd));
+  bd.nb = nb;
+  for (int j = 0; j < nb; ++j) {
+    if (j > 0 && boundaries_h[j] <= boundaries_h[j - 1]) return fail(CADET_E_ARG, "boundaries not strictly increasing");
+    bd.b[j] = boundaries_h[j];
+  }
+  return cuda_check(bucketize_launch(raw_position, n, bd, bucket, reinterpret_cast<uint32_t*>(ws),
+                                     reinterpret_cast<cudaStream_t>(stream)),
+                    "bucketize");
 }
 
 size_t cadet_gemm_fp32_workspace_bytes(int32_t M, int32_t N, int32_t K) {

@@ -177,6 +177,7 @@ struct LayerWs {    // carved from `ws` after the plan
   void *dO, *dKr, *dV, *uq, *uk, *dQ, *dK, *ux;
   float *dQacc, *rq, *rk, *rx;
   float* tap[N_TAPS];  // all null unless cfg.out_f32
+  float* slab;         // deterministic mode: split-K partial slabs (null otherwise)
 };
 
 size_t bf_sz(int T, int d) { return a256((size_t)T * d * 2); }
@@ -195,10 +196,19 @@ size_t saved_bytes(const cadet_attn_config* c, int T) {
   if (c->dtype == CADET_FP32) return f32_saved_bytes(c, T);
   return 10 * bf_sz(T, c->d_model) + a256((size_t)4 * c->n_heads * T);
 }
+int pick_bn_wgrad(int N);
+int pick_split(int M, int N, int bn, int K);
+// deterministic mode: fp32 split-K partial slabs of up to 3 weight gradients of one launch
+size_t det_slab_bytes(const cadet_attn_config* c, int T) {
+  if (!c->deterministic) return 0;
+  const int d = c->d_model;
+  return 3 * a256((size_t)pick_split(d, d, pick_bn_wgrad(d), T) * d * d * 4);
+}
 size_t layer_ws_base_bytes(const cadet_attn_config* c, int n, int T) {
   const int d = c->d_model;
   return plan_bytes(n, T, T) + a256((size_t)4 * T * (c->head_dim + 32)) +
-         a256((size_t)4 * c->n_heads * T) + 8 * bf_sz(T, d) + 4 * f_sz(T, d) + (c->out_f32 ? N_TAPS * f_sz(T, d) : 0);
+         a256((size_t)4 * c->n_heads * T) + 8 * bf_sz(T, d) + 4 * f_sz(T, d) + (c->out_f32 ? N_TAPS * f_sz(T, d) : 0) +
+         det_slab_bytes(c, T);
 }
 size_t layer_ws_bytes(const cadet_attn_config* c, int n, int T) {
   if (c->dtype == CADET_FP32) return f32_layer_ws_bytes(c, n, T);
@@ -237,6 +247,7 @@ LayerWs carve_ws(void* ws, const cadet_attn_config* c, int n, int T) {
     W.tap[i] = c->out_f32 ? reinterpret_cast<float*>(p) : nullptr;
     if (c->out_f32) p += f_sz(T, d);
   }
+  W.slab = c->deterministic ? reinterpret_cast<float*>(p) : nullptr;
   return W;
 }
 
@@ -288,12 +299,14 @@ GemmProblem prob(int M, int N, int K, OperandDesc A, OperandDesc B, int mode) {
   return g;
 }
 
-// dW = A^T . G over T rows, fp32, split-K with atomics into a zeroed output.
-GemmProblem wgrad(const void* A, const void* G, float* dW, int T, int din, int dout, int bn) {
+// dW = A^T . G over T rows, fp32, split-K with atomics into a zeroed output; with a slab (deterministic
+// mode) each split stores its partial into slab + ks din dout and slab_reduce sums them in order.
+GemmProblem wgrad(const void* A, const void* G, float* dW, int T, int din, int dout, int bn, float* slab = nullptr) {
   GemmProblem g = prob(din, dout, T, act_t(A, T, din), act_t(G, T, dout), EPI_ATOMIC);
   g.split_k = pick_split(din, dout, bn, T);
-  g.epi.out = dW;
+  g.epi.out = slab ? slab : dW;
   g.epi.out_f32 = 1;
+  g.epi.split_stride = slab ? (int64_t)din * dout : 0;
   return g;
 }
 
@@ -491,8 +504,17 @@ cadet_status cadet_attn_backward_ev(const cadet_attn_config* cfg, const cadet_ba
   cudaError_t e = cfg->plan_ready >= 2 ? cudaSuccess : rope_prepare(cfg, b, W, v, st);
   const float* cs = cfg->use_rope ? W.rope_cs : nullptr;
   float* gws[7] = {gr->dW_xg, gr->dW_q, gr->dW_k, gr->dW_v, gr->dW_qg, gr->dW_kg, gr->dW_o};
+  // deterministic mode: no fp32 atomics anywhere in the layer backward -- split-K weight-gradient partials
+  // go to slabs summed in a fixed order, and D comes from the (fixed-order) preprocess kernel
+  const bool det = cfg->deterministic != 0;
+  const int wsplit = pick_split(d, d, bnw, T);
+  auto slab = [&](int j) { return det ? W.slab + (size_t)j * wsplit * d * d : nullptr; };
+  auto reduce = [&](float* const* dWs, int count) {
+    for (int j = 0; j < count && det && e == cudaSuccess; ++j)
+      e = slab_reduce_launch(slab(j), wsplit, (size_t)d * d, dWs[j], st);
+  };
   // A10's preprocess D = rowsum(dO * O) per head comes out of the A9 GEMM's epilogue when it exists
-  const bool d_in_a9 = cfg->use_out_proj && hd >= 32;
+  const bool d_in_a9 = cfg->use_out_proj && hd >= 32 && !det;
   if (e == cudaSuccess) {  // the 7 weight gradients (split-K accumulated) and D (atomics): one launch
     ZeroSpan zs[8];
     for (int i = 0; i < 7; ++i) zs[i] = ZeroSpan{gws[i], wbytes};
@@ -515,8 +537,9 @@ cadet_status cadet_attn_backward_ev(const cadet_attn_config* cfg, const cadet_ba
       g.epi.dot_T = T;
       g.epi.hd = hd;
     }
-    GemmProblem gw = wgrad(L.O, dY, gr->dW_o, T, d, d, bnw);
+    GemmProblem gw = wgrad(L.O, dY, gr->dW_o, T, d, d, bnw, slab(0));
     e = gemm_launch2(&g, 1, bn, &gw, 1, bnw, st);
+    reduce(&gr->dW_o, 1);
     dO = W.dO;
   }
   mark(0);
@@ -583,8 +606,11 @@ cadet_status cadet_attn_backward_ev(const cadet_attn_config* cfg, const cadet_ba
           g[i].epi.tap = W.tap[TAP_DQ + i];
         }
         // dW_qg = Q^T uq ; dW_kg = K^T uk share the u operands: same launch
-        GemmProblem gw[2] = {wgrad(L.Q, W.uq, gr->dW_qg, T, d, d, bnw), wgrad(L.K, W.uk, gr->dW_kg, T, d, d, bnw)};
+        GemmProblem gw[2] = {wgrad(L.Q, W.uq, gr->dW_qg, T, d, d, bnw, slab(0)),
+                             wgrad(L.K, W.uk, gr->dW_kg, T, d, d, bnw, slab(1))};
         e = gemm_launch2(g, 2, bn, gw, 2, bnw, st);
+        float* dws[2] = {gr->dW_qg, gr->dW_kg};
+        reduce(dws, 2);
       }
     } else {
       e = rope_gate_bwd_launch(W.dQacc, 0, nullptr, nullptr, nullptr, W.dQ, 1, T, d, hd, cs, st);
@@ -626,9 +652,11 @@ cadet_status cadet_attn_backward_ev(const cadet_attn_config* cfg, const cadet_ba
       g.epi.tap = W.tap[TAP_DX];
     }
     {  // with the weight gradients of W_q, W_k, W_v (same dQ, dK, dV operands) in one launch
-      GemmProblem gw[3] = {wgrad(Xt, dQ, gr->dW_q, T, d, d, bnw), wgrad(Xt, dK, gr->dW_k, T, d, d, bnw),
-                           wgrad(Xt, W.dV, gr->dW_v, T, d, d, bnw)};
+      GemmProblem gw[3] = {wgrad(Xt, dQ, gr->dW_q, T, d, d, bnw, slab(0)), wgrad(Xt, dK, gr->dW_k, T, d, d, bnw, slab(1)),
+                           wgrad(Xt, W.dV, gr->dW_v, T, d, d, bnw, slab(2))};
       e = gemm_launch2(&g, 1, bn, gw, 3, bnw, st);
+      float* dws[3] = {gr->dW_q, gr->dW_k, gr->dW_v};
+      reduce(dws, 3);
     }
     mark(2);
     if (e == cudaSuccess && cfg->use_rep_gate) {  // dX = rx + ux W_xg^T ; dW_xg = X^T ux
@@ -637,8 +665,9 @@ cadet_status cadet_attn_backward_ev(const cadet_attn_config* cfg, const cadet_ba
       g2.epi.resid = W.rx;
       g2.epi.resid_f32 = 0;
       g2.epi.tap = W.tap[TAP_DX];
-      GemmProblem gw = wgrad(X, W.ux, gr->dW_xg, T, d, d, bnw);
+      GemmProblem gw = wgrad(X, W.ux, gr->dW_xg, T, d, d, bnw, slab(0));
       e = gemm_launch2(&g2, 1, bn, &gw, 1, bnw, st);
+      reduce(&gr->dW_xg, 1);
     }
   }
   mark(3);

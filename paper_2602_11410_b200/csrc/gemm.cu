@@ -50,7 +50,7 @@ struct GemmCfg {
 };
 
 struct Unit {
-  int p, m0, n0, kb_lo, kb_hi;
+  int p, m0, n0, kb_lo, kb_hi, ks;
 };
 
 __device__ __forceinline__ Unit decode_unit(const GemmKParams& P, int u) {
@@ -71,6 +71,7 @@ __device__ __forceinline__ Unit decode_unit(const GemmKParams& P, int u) {
   r.n0 = nt;  // tile index; callers multiply by BN
   r.kb_lo = (int)(((long long)ks * q.kb_total) / q.split_k);
   r.kb_hi = (int)(((long long)(ks + 1) * q.kb_total) / q.split_k);
+  r.ks = ks;
   return r;
 }
 
@@ -272,7 +273,7 @@ __device__ __forceinline__ const void* epi_primary(const EpiParams& e) {
 
 template <uint32_t MODES>
 __device__ __forceinline__ void run_epilogue_warp(const EpiParams& e, int row0, int M, int n0c, float (&v)[32],
-                                                  uint32_t stg, const uint4* pre = nullptr) {
+                                                  uint32_t stg, const uint4* pre = nullptr, int ks = 0) {
   const int lane = threadIdx.x & 31;
   if (e.row_map) {
     run_epilogue<MODES>(e, row0 + lane, M, n0c, v);
@@ -363,6 +364,10 @@ __device__ __forceinline__ void run_epilogue_warp(const EpiParams& e, int row0, 
       warp_store_rows(stg, e.out2, e.out2_f32, off0, e.ldo, rows_valid, r);
     } break;
     case EPI_ATOMIC: if constexpr (HAS_MODE(EPI_ATOMIC)) {
+      if (e.split_stride) {  // deterministic mode: split ks stores its partial into its own slab
+        warp_store_rows(stg, reinterpret_cast<float*>(e.out) + (size_t)ks * e.split_stride, 1, off0, e.ldo, rows_valid, v);
+        break;
+      }
       // split-K partials: transpose through the stage, then fp32 vector reductions that cover 4 rows
       // x 128 B per instruction (instead of 32 rows x 16 B)
 #pragma unroll
@@ -584,7 +589,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_kernel(const __grid_cons
         float v[32];
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-        run_epilogue_warp<MODES>(q.epi, row0, q.M, n0c, v, stg, pb ? cur : nullptr);
+        run_epilogue_warp<MODES>(q.epi, row0, q.M, n0c, v, stg, pb ? cur : nullptr, U.ks);
       }
       tc_fence_before();
       __syncwarp();
@@ -766,7 +771,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
         float v[32];
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-        run_epilogue_warp<MODES>(q.epi, row0, q.M, n0c, v, stg, pb ? cur : nullptr);
+        run_epilogue_warp<MODES>(q.epi, row0, q.M, n0c, v, stg, pb ? cur : nullptr, U.ks);
       }
       tc_fence_before();
       __syncwarp();

@@ -46,6 +46,9 @@ struct EpiParams {
   // bf16 rounding; null = off.  Only the warp-cooperative epilogue (no row_map) writes them.
   float* tap;
   float* tap2;
+  // EPI_ATOMIC in deterministic mode (cfg.deterministic): split ks stores its fp32 partial at
+  // out + ks * split_stride (plain stores, no atomics); a fixed-order reduction sums the slabs after
+  int64_t split_stride;
   // heads (EPI_HEAD)
   const float* b1;
   const float* w2;

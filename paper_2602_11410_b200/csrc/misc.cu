@@ -8,6 +8,7 @@
 //   head_init / head_dz / head_dhid   A7/A8 routed BCE (Eq. 9) and the tower backward
 //   add_kernel              Y = O (+ resid) when the output projection is ablated
 #include "misc.cuh"
+#include <algorithm>
 #include <cuda_fp16.h>
 #include "launch.cuh"
 #include "prof.cuh"
@@ -480,6 +481,50 @@ cudaError_t head_dhid_launch(const void* pre, const float* dz, const int32_t* bu
                                           reinterpret_cast<__nv_bfloat16*>(dhid),
                                           reinterpret_cast<__nv_bfloat16*>(dhid_lo), db1, dw2);
   }
+  return cudaGetLastError();
+}
+__global__ void slab_reduce_kernel(const float4* slabs, int nsplit, size_t n4, float4* out) {
+  pdl_trigger();
+  pdl_wait();
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (size_t)gridDim.x * blockDim.x) {
+    float4 a = slabs[i];
+    for (int s = 1; s < nsplit; ++s) {
+      const float4 b = slabs[(size_t)s * n4 + i];
+      a.x += b.x;
+      a.y += b.y;
+      a.z += b.z;
+      a.w += b.w;
+    }
+    out[i] = a;
+  }
+}
+cudaError_t slab_reduce_launch(const float* slabs, int nsplit, size_t n, float* out, cudaStream_t st) {
+  ProfScope ps(PROF_OTHER, st, 1);
+  if (n % 4 || nsplit < 1) return cudaErrorInvalidValue;
+  if (n)
+    launch_pdl(slab_reduce_kernel, dim3((unsigned)std::min<size_t>(blocks(n / 4, 256), 148 * 8)), dim3(256), 0, st,
+               reinterpret_cast<const float4*>(slabs), nsplit, n / 4, reinterpret_cast<float4*>(out));
+  return cudaGetLastError();
+}
+// context buckets: bucket = #{j : pos > boundary_j}; pos < 1 is a routing error
+__global__ void bucketize_kernel(const int32_t* pos, int n, Bounds bd, int32_t* out, uint32_t* err) {
+  pdl_trigger();
+  pdl_wait();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int p = pos[i];
+  int k = 0;
+  if (p < 1) {
+    atomicOr(err, ERRBIT_BUCKET);
+  } else {
+    for (int j = 0; j < bd.nb; ++j) k += p > bd.b[j] ? 1 : 0;
+  }
+  out[i] = k;
+}
+cudaError_t bucketize_launch(const int32_t* pos, int n, const Bounds& bd, int32_t* out, uint32_t* err,
+                             cudaStream_t st) {
+  ProfScope ps(PROF_OTHER, st, 1);
+  if (n > 0) launch_pdl(bucketize_kernel, dim3(blocks(n, 256)), dim3(256), 0, st, pos, n, bd, out, err);
   return cudaGetLastError();
 }
 cudaError_t add_bf16_launch(const void* a, const void* b, void* out, size_t n, cudaStream_t st) {

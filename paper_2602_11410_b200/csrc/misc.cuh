@@ -40,4 +40,12 @@ struct ZeroSpan {
   size_t bytes;
 };
 cudaError_t zero_many_launch(const ZeroSpan* spans, int n, cudaStream_t st);
+struct Bounds {  // context-bucket boundaries (cadet_bucketize), strictly increasing
+  int32_t b[32];
+  int32_t nb;
+};
+cudaError_t bucketize_launch(const int32_t* pos, int n, const Bounds& bd, int32_t* out, uint32_t* err,
+                             cudaStream_t st);
+// out[i] = sum_{s = 0..nsplit-1} slabs[s n + i], in that order (deterministic split-K reduction)
+cudaError_t slab_reduce_launch(const float* slabs, int nsplit, size_t n, float* out, cudaStream_t st);
 }  // namespace cadet

@@ -37,6 +37,7 @@ class StackConfig:
     budget: int = 65536          # T: packed rows per step
     L_chunk: int = 2048
     K: int = 2                   # towers
+    boundaries: tuple = (4,)     # context buckets from raw positions: K = 2 "positions 1--4, and 5+"
     d_hidden: int = 0            # 0 -> d_model // 2
     delta_delay_ms: int = 3_600_000
     mask_flags: int = L.CADET_MASK_TIME
@@ -72,7 +73,7 @@ class StepInputs:
     s_hist: torch.Tensor     # [R] int32 session ids
     lens: torch.Tensor       # [B] int32 history lengths
     rows: torch.Tensor       # [n_imp] int32 packed rows of impression tokens
-    bucket: torch.Tensor     # [n_imp] int32 realised context bucket k_t
+    position: torch.Tensor   # [n_imp] int32 raw feed position (>= 1) of impression t: the context signal
     label: torch.Tensor      # [n_imp] fp32 click label y_t
     n_hist: int
     n_chunks: int
@@ -82,9 +83,9 @@ class StepInputs:
     def to(self, device, non_blocking=True) -> "StepInputs":
         f = lambda t: t.to(device, non_blocking=non_blocking) if t is not None else None
         return StepInputs(f(self.X_hist), f(self.t_hist), f(self.s_hist), f(self.lens), f(self.rows),
-                          f(self.bucket), f(self.label), self.n_hist, self.n_chunks, self.tokens, f(self.aux_label))
+                          f(self.position), f(self.label), self.n_hist, self.n_chunks, self.tokens, f(self.aux_label))
 
-    FIELDS = ("X_hist", "t_hist", "s_hist", "lens", "rows", "bucket", "label", "aux_label")
+    FIELDS = ("X_hist", "t_hist", "s_hist", "lens", "rows", "position", "label", "aux_label")
 
     def copy_(self, src: "StepInputs"):
         for a in self.FIELDS:
@@ -106,17 +107,17 @@ def make_inputs(users, d: int, L_chunk: int, seed: int, pin: bool = False, J: in
     s = np.concatenate([u.session_ids for u in users]).astype(np.int32)
     starts = np.concatenate([[0], np.cumsum(lens)[:-1]])
     rows = np.concatenate([st + u.impression_rows for st, u in zip(starts, users)]).astype(np.int32)
-    bucket = np.concatenate([u.buckets[u.impression_rows] for u in users]).astype(np.int32)
+    position = np.concatenate([u.positions[u.impression_rows] for u in users]).astype(np.int32)
     label = np.concatenate([u.labels[u.impression_rows] for u in users]).astype(np.float32)
     n_chunks = int(sum(-(-int(m) // L_chunk) for m in lens))
     mk = lambda a, dt: (torch.from_numpy(np.ascontiguousarray(a)).to(dt))
     Xt = torch.from_numpy(X).to(torch.bfloat16)
     aux = mk(G.aux_labels(seed, len(rows))[:, :J], torch.float32) if J > 0 else None
     inp = StepInputs(Xt, mk(t, torch.int64), mk(s, torch.int32), mk(lens, torch.int32), mk(rows, torch.int32),
-                     mk(bucket, torch.int32), mk(label, torch.float32), len(users), n_chunks, R, aux)
+                     mk(position, torch.int32), mk(label, torch.float32), len(users), n_chunks, R, aux)
     if pin:
         pinned = [x.pin_memory() if x is not None else None for x in (inp.X_hist, inp.t_hist, inp.s_hist, inp.lens,
-                                                                       inp.rows, inp.bucket, inp.label, inp.aux_label)]
+                                                                       inp.rows, inp.position, inp.label, inp.aux_label)]
         inp = StepInputs(*pinned[:7], inp.n_hist, inp.n_chunks, inp.tokens, pinned[7])
     return inp
 
@@ -243,6 +244,7 @@ class CadetStack:
         self.cfg = cfg
         self.dev = torch.device(device)
         d, T, nl = cfg.d_model, cfg.budget, cfg.n_layers
+        assert cfg.K == len(cfg.boundaries) + 1, "K towers need K - 1 bucket boundaries"
         self.acfg = ops.config(d, cfg.n_heads, delta_delay_ms=cfg.delta_delay_ms, mask_flags=cfg.mask_flags,
                                out_f32=1 if cfg.taps else 0)
         # ONE flat layout for gradients and parameters: 7 d^2 per layer (+ the block's FFN and RMSNorm
@@ -350,6 +352,7 @@ class CadetStack:
         if self._hws is None or self._hws.numel() < hwb:
             self._hws = ops.workspace(hwb, self.dev)
         self.logits = torch.empty(n_imp, cfg.K, dtype=torch.float32, device=self.dev)
+        self.bucket = torch.empty(n_imp, dtype=torch.int32, device=self.dev)  # cadet_bucketize of the positions
         self.pre = torch.empty(n_imp, cfg.K * cfg.dh, dtype=torch.bfloat16, device=self.dev)
         self.cu_hist = torch.empty(n_hist + 1, dtype=torch.int32, device=self.dev)
         self.cu = torch.empty(n_chunks + 8, dtype=torch.int32, device=self.dev)
@@ -402,6 +405,10 @@ class CadetStack:
                            256, st))
         chk(lib.cadet_chunk(_vp(self.cu_hist), inp.n_hist, cfg.L_chunk, _vp(self.cu), inp.n_chunks + 8,
                             _vp(self.n_out), C.c_void_p(self.small_ws.data_ptr() + 256), st))
+        # context buckets k_t of the impressions from their raw positions
+        bnd = (C.c_int32 * len(cfg.boundaries))(*cfg.boundaries)
+        chk(lib.cadet_bucketize(_vp(inp.position), n_imp, bnd, len(cfg.boundaries), _vp(self.bucket),
+                                C.c_void_p(self.small_ws.data_ptr() + 768), st))
         b = self.batch(inp).struct()
         ws, wsn = _vp(self._ws), self._ws.numel()
         # A1: one mask plan per step, shared by every layer's forward and backward; with the layer-sized
@@ -442,7 +449,7 @@ class CadetStack:
         hg = L.HeadGrads(self.gW1.data_ptr(), self.gb1.data_ptr(), self.gw2.data_ptr(), self.gb2.data_ptr())
         if not cfg.full_loss:  # Eq. 9: routed BCE, fused
             chk(lib.cadet_heads_loss_backward(C.byref(hc), C.byref(hw), _vp(self.Hs[-1]), _vp(inp.rows), n_imp, T,
-                                              _vp(self.logits), _vp(self.pre), _vp(inp.bucket), _vp(inp.label),
+                                              _vp(self.logits), _vp(self.pre), _vp(self.bucket), _vp(inp.label),
                                               _vp(self.loss), _vp(self.dHs[-1]), C.byref(hg), _vp(self._hws),
                                               self._hws.numel(), st))
         else:
@@ -590,7 +597,7 @@ class CadetStack:
         loss totals sum (all-reduced with the gradients) to the global Eq. 11 loss."""
         cfg, lib, chk = self.cfg, L.lib(), L.check
         d, T, n = cfg.d_model, cfg.budget, inp.rows.numel()
-        chk(lib.cadet_routed_logits(_vp(self.logits), cfg.K, _vp(inp.bucket), n, _vp(self.zr), st))
+        chk(lib.cadet_routed_logits(_vp(self.logits), cfg.K, _vp(self.bucket), n, _vp(self.zr), st))
         z_all, y_all = dp_gather_scores(self.zr, inp.label, group)
         n_all = int(z_all.numel())
         pwb = lib.cadet_pairwise_workspace_bytes(n, n_all)
@@ -598,7 +605,7 @@ class CadetStack:
             self._pws = ops.workspace(pwb, self.dev)
         chk(lib.cadet_pairwise_loss(_vp(self.zr), _vp(inp.label), n, _vp(z_all), _vp(y_all), n_all,
                                     _vp(self.pair_share), _vp(self.dz_pair), _vp(self._pws), self._pws.numel(), st))
-        chk(lib.cadet_full_loss_grads(C.byref(self.lcfg), _vp(self.logits), cfg.K, _vp(inp.bucket), _vp(inp.label),
+        chk(lib.cadet_full_loss_grads(C.byref(self.lcfg), _vp(self.logits), cfg.K, _vp(self.bucket), _vp(inp.label),
                                       _vp(self.dz_pair), _vp(self.pair_share), _vp(self.za), _vp(inp.aux_label), n,
                                       _vp(self.losses), _vp(self.dz_ctx), _vp(self.dz_aux), st))
         chk(lib.cadet_heads_backward(C.byref(hc), C.byref(hw), _vp(self.Hs[-1]), _vp(inp.rows), n, T, _vp(self.pre),
@@ -626,3 +633,4 @@ class CadetStack:
         ops.poll(self.small_ws)            # pack error word
         ops.poll(self.small_ws[256:])      # chunk error word
         ops.poll(self.small_ws[512:])      # row-move pack error word
+        ops.poll(self.small_ws[768:])      # bucketize error word (positions < 1)

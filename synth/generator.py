@@ -1,7 +1,7 @@
 """Seeded synthetic workload generator.
 
 This module produces *inputs only*: user histories (lengths, int64 Unix-ms
-timestamps, session ids, labels, context buckets) and dense random tensors
+timestamps, session ids, labels, raw feed positions) and dense random tensors
 (features X, weights, upstream gradients) rounded to bf16.  It holds none of
 the method's arithmetic (no masking, RoPE, gating, attention, chunking or
 packing): both the CUDA path and the CPU oracle consume what it returns.
@@ -16,7 +16,8 @@ Recipe (mirrors PAPER.md P:460; SPEC.md S:154, S:172
   4. events older than dt_max before the newest one are dropped (lookback).
   5. timestamps start at `t0_ms` (1,735,000,000,000; 0 in stress mode);
      session ids are per-user running counters.
-  6. labels y ~ Bernoulli(0.03), bucket k ~ U{0,1} per impression.
+  6. labels y ~ Bernoulli(0.03), feed position p ~ U{1..8} per impression (the raw context signal
+     of P:624; bucketing it is the method's step, not the generator's).
   7. serving shape (C2): context of U{448..576}-64 tokens from the same session
      process; 64 candidates share one request time = last context time + Exp(10 min).
 Per-user RNG streams are keyed by (seed, user).
@@ -36,7 +37,7 @@ class UserHistory:
     timestamps: np.ndarray      # int64 [m], non-decreasing
     session_ids: np.ndarray     # int32 [m], non-decreasing
     labels: np.ndarray          # float32 [m] (meaningful on impression rows)
-    buckets: np.ndarray         # int32 [m]  (meaningful on impression rows)
+    positions: np.ndarray       # int32 [m] raw feed position >= 1 (meaningful on impression rows)
     impression_rows: np.ndarray  # int32 local positions of impression tokens
     n_candidates: int = 0
 
@@ -55,7 +56,7 @@ class GenConfig:
     intra_gap_mean_ms: float = 60_000.0
     t0_ms: int = T0_UNIX_MS
     ctr: float = 0.03
-    n_buckets: int = 2
+    max_position: int = 8
 
 
 def stress_config(**kw) -> GenConfig:
@@ -110,7 +111,7 @@ def gen_user(seed: int, user: int, cfg: GenConfig) -> UserHistory:
     y = np.zeros(2 * n, dtype=np.float32)
     k = np.zeros(2 * n, dtype=np.int32)
     y[0::2] = (rng.random(n) < cfg.ctr).astype(np.float32)
-    k[0::2] = rng.integers(0, cfg.n_buckets, size=n).astype(np.int32)
+    k[0::2] = rng.integers(1, cfg.max_position + 1, size=n).astype(np.int32)
     rows = np.arange(0, 2 * n, 2, dtype=np.int32)
     return UserHistory(t, s.astype(np.int32), y, k, rows, 0)
 
@@ -132,7 +133,7 @@ def gen_serving_user(seed: int, user: int, cfg: GenConfig, lo: int = 448, hi: in
     t = np.concatenate([t_ctx, np.full(n_cand, t_req, dtype=np.int64)])
     s = np.concatenate([s_ctx, np.full(n_cand, s_ctx[-1] + 1, dtype=np.int32)])
     y = (rng.random(m) < cfg.ctr).astype(np.float32)
-    k = rng.integers(0, cfg.n_buckets, size=m).astype(np.int32)
+    k = rng.integers(1, cfg.max_position + 1, size=m).astype(np.int32)
     rows = np.arange(L, m, dtype=np.int32)
     return UserHistory(t, s.astype(np.int32), y, k, rows, n_cand)
 
@@ -257,7 +258,7 @@ def fixed_lengths_batch(lengths, seed: int = 0, cfg: GenConfig | None = None, n_
         t = np.repeat(t_imp, 2)[:m]
         s = np.repeat(s_imp, 2)[:m]
         y = (rng.random(m) < 0.3).astype(np.float32)
-        k = rng.integers(0, cfg.n_buckets, size=m).astype(np.int32)
+        k = rng.integers(1, cfg.max_position + 1, size=m).astype(np.int32)
         nc = 0 if n_cand is None else int(n_cand[u])
         users.append(UserHistory(t, s.astype(np.int32), y, k, np.arange(0, m, 2, dtype=np.int32), nc))
     return concat_users(users)

@@ -64,6 +64,12 @@ def test_host_validation_errors_without_gpu():
     assert L.cadet_attn_saved_bytes(C.byref(c), 1000) > L.cadet_attn_saved_bytes(C.byref(c16), 1000)
     assert L.cadet_attn_bwd_ds_bytes(C.byref(c), 1, 1000, 1000) == 0
     assert L.cadet_gemm_fp32_workspace_bytes(100, 64, 30) == 2 * 12800 + 2 * 8192  # K padded to 32
+    g = C.c_void_p(256)  # never dereferenced: boundaries are validated on the host first
+    assert L.cadet_bucketize(g, 4, (C.c_int32 * 2)(4, 4), 2, g, g, None) == 1   # not strictly increasing
+    assert L.cadet_bucketize(g, 4, (C.c_int32 * 1)(4), 0, g, g, None) == 1      # nb < 1
+    c = _lib.default_config(64, 1)    # deterministic mode is bf16-only
+    c.dtype, c.deterministic = 1, 1
+    assert L.cadet_mask_plan(C.byref(c), C.byref(b), None, 0, None) == 9
     assert L.cadet_gemm(0, 32, 32, None, 0, None, 0, None, 1, None, None) == 1
 
 

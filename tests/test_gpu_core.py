@@ -371,3 +371,28 @@ def test_heads_device_latches(ops, kind, dtype):
     with pytest.raises(L.CadetError) as e:
         ops.poll(ws)
     assert e.value.status == (6 if kind == "bucket" else 7)
+
+
+@pytest.mark.parametrize("bnd", [(4,), (1, 4), (2, 3, 7, 20), tuple(range(1, 33))])
+def test_bucketize_bit_exact(ops, bnd):
+    """cadet_bucketize vs oracle.bucketize: bit-exact; a position < 1 latches
+    CADET_E_BUCKET."""
+    import ctypes as C
+    from paper_2602_11410_b200 import _lib as L
+    rng = np.random.default_rng(len(bnd))
+    pos = rng.integers(1, 40, size=10_007).astype(np.int32)
+    pd = torch.tensor(pos, device="cuda")
+    out = torch.full((pos.size,), -1, dtype=torch.int32, device="cuda")
+    ws = torch.zeros(256, dtype=torch.uint8, device="cuda")
+    arr = (C.c_int32 * len(bnd))(*bnd)
+    st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    L.check(L.lib().cadet_bucketize(C.c_void_p(pd.data_ptr()), pos.size, arr, len(bnd), C.c_void_p(out.data_ptr()),
+                                    C.c_void_p(ws.data_ptr()), st))
+    ops.poll(ws)
+    assert (out.cpu().numpy() == O.bucketize(pos, bnd)).all()
+    pd[5] = 0
+    L.check(L.lib().cadet_bucketize(C.c_void_p(pd.data_ptr()), pos.size, arr, len(bnd), C.c_void_p(out.data_ptr()),
+                                    C.c_void_p(ws.data_ptr()), st))
+    with pytest.raises(L.CadetError) as e:
+        ops.poll(ws)
+    assert e.value.status == 6

@@ -198,3 +198,36 @@ def test_attn_core_mask_rules_forward_backward(ops, case):
     for nm, got, rf in zip(("dQ", "dK", "dV"), (dQ, dK, dV), ref):
         assert_close(to_np(got), rf, what=nm)
         assert (to_np(got)[cu[-1]:] == 0).all()
+
+
+@pytest.mark.parametrize("case", [1, 3])
+def test_deterministic_backward_is_bit_reproducible(ops, case):
+    """cfg.deterministic = 1: fixed-order split-K slabs + fixed-order D give bit-identical dX and weight
+    gradients on repeated runs, equal to the atomic mode up to fp32 summation order."""
+    from paper_2602_11410_b200 import _lib as L
+    from tests.test_gpu_layer import run_layer_forward
+    lib = L.lib()
+    lengths, d, H, nc, peaky, flags, nst, use_pf = STAGE_CASES[case]
+    cu, t, s, ncv, T, X, W = layer_case(lengths, d, H, nc, seed=70 + case, peaky=peaky)
+    b = to_dev_batch(cu, t, s, ncv, T)
+    dY = G.normal_bf16(71, case, (T, d))
+    dY[cu[-1]:] = 0
+    dYd = bf16_tensor(dY)
+    outs = []
+    for det in (1, 1, 0):
+        cfg = ops.config(d, H, mask_flags=flags, delta_delay_ms=120_000, rope_phi_min=0.5, rope_base=1e4,
+                         rope_delta_t_max_ms=86_400_000, deterministic=det)
+        Y, saved, ws, Xd, Wd, w = run_layer_forward(ops, cfg, b, X, W, T, two_pass=True)
+        dX = torch.empty(T, d, dtype=torch.bfloat16, device="cuda")
+        gs = [torch.empty(d, d, dtype=torch.float32, device="cuda") for _ in range(7)]
+        g = L.AttnGrads(*[x.data_ptr() for x in gs])
+        L.check(lib.cadet_attn_backward(C.byref(cfg), C.byref(b.struct()), C.byref(w), C.c_void_p(Xd.data_ptr()),
+                                        C.c_void_p(saved.data_ptr()), C.c_void_p(dYd.data_ptr()),
+                                        C.c_void_p(dX.data_ptr()), None, C.byref(g), C.c_void_p(ws.data_ptr()),
+                                        ws.numel(), C.c_void_p(torch.cuda.current_stream().cuda_stream)))
+        torch.cuda.synchronize()
+        outs.append([dX.clone()] + [x.clone() for x in gs])
+    for a_, b_ in zip(outs[0], outs[1]):
+        assert torch.equal(a_, b_)
+    for a_, b_ in zip(outs[0][1:], outs[2][1:]):
+        assert float((a_ - b_).abs().max()) <= 1e-5 * max(1.0, float(b_.abs().max()))

@@ -445,6 +445,22 @@ def test_core_backward_finite_differences():
 
 
 # ---------------------------------------------------------------- heads
+def test_bucketize_paper_and_spec_examples():
+    """S:145-150 (1-based k): position 1, [4] -> 1; position 5, [4] -> 2; position 4, [1, 4] -> 2;
+    P:624 K = 2 "positions 1--4, and 5+"; P:393 example k = 1 for position 1, k = 2 for 2--4, k = 3 for 5+."""
+    assert O.bucketize([1], [4])[0] + 1 == 1
+    assert O.bucketize([5], [4])[0] + 1 == 2
+    assert O.bucketize([4], [1, 4])[0] + 1 == 2
+    pos = np.arange(1, 13)
+    assert list(O.bucketize(pos, [4])) == [0, 0, 0, 0] + [1] * 8                    # P:624
+    assert list(O.bucketize(pos, [1, 4])) == [0, 1, 1, 1] + [2] * 8                 # P:393
+    # equals the library routine: #{b : pos > b} = searchsorted(b, pos, side="left")
+    rng = np.random.default_rng(0)
+    bnd = np.sort(rng.choice(np.arange(1, 50), size=5, replace=False))
+    p = rng.integers(1, 60, size=1000)
+    assert (O.bucketize(p, bnd) == np.searchsorted(bnd, p, side="left")).all()
+
+
 def test_head_loss_examples():
     """logit 0, y=1 -> ln 2; logit 2, y=1 -> 0.126928."""
     assert O.heads_loss(np.array([[0.0, 5.0]]), np.array([0]), np.array([1.0])) == pytest.approx(math.log(2))
