@@ -75,7 +75,8 @@ def _core_tol(name, got, ref, peaky):
 
 
 def check_layer_stages(X, W, sv, tp, wb, D, dY, meta, ocfg, seqs, resid=None, dresid=None, peaky=False,
-                       forward=True, backward=True, weight_grads=None, wg_sample=None, tag=""):
+                       forward=True, backward=True, weight_grads=None, wg_sample=None, d_from_stored=False,
+                       tag=""):
     """X: the layer input (bf16 values) [T, d]; W: the 7 weights (fp64); sv: saved views; tp: taps;
     wb / D: backward intermediates; dY: the upstream gradient; meta / ocfg: the batch for the oracle;
     seqs: sequence indices to check row-wise; resid / dresid: the residual added to Y / to dX (or
@@ -119,7 +120,9 @@ def check_layer_stages(X, W, sv, tp, wb, D, dY, meta, ocfg, seqs, resid=None, dr
             # A9: dO = dY W_o^T; D = rowsum(dO * O) per head (dO's fp32 value, the bf16 O)
             dO = g @ Wo.T
             assert_close(tp["dO"][sl], dO, what=f"A9 dO {tg}")
-            Dr = np.stack([(dO[:, h * hd:(h + 1) * hd] * sv["O"][sl][:, h * hd:(h + 1) * hd]).sum(1) for h in range(H)])
+            # (d_from_stored: D comes from the preprocess kernel fed the stored bf16 dO -- deterministic mode)
+            dOD = wb["dO"][sl] if d_from_stored else dO
+            Dr = np.stack([(dOD[:, h * hd:(h + 1) * hd] * sv["O"][sl][:, h * hd:(h + 1) * hd]).sum(1) for h in range(H)])
             assert_close(D[:, sl], Dr, what=f"A9 D {tg}")
             # A10 (adjoint of Eq. 7) fed the bf16 Qr, Kr, V and the bf16 dO it consumed
             ref = O.attention_core_backward(sv["Qr"][sl], sv["Kr"][sl], sv["V"][sl], A, wb["dO"][sl], H)

@@ -65,14 +65,14 @@ def peaky_ok(name, got, ref, peaky):
     return mx, mn
 
 
-def run_case(ops, case, with_resid):
+def run_case(ops, case, with_resid, det=0):
     from paper_2602_11410_b200 import _lib as L
     lengths, d, H, nc, peaky, flags, nst, use_pf = STAGE_CASES[case]
     cu, t, s, ncv, T, X, W = layer_case(lengths, d, H, nc, seed=40 + case, peaky=peaky)
     pf = pair_flags_for(cu, T) if use_pf else None
     nstv = None if nst is None else np.asarray(nst, np.int32)
     cfg = ops.config(d, H, mask_flags=flags, delta_delay_ms=120_000, rope_phi_min=0.5, rope_base=1e4,
-                     rope_delta_t_max_ms=86_400_000, out_f32=1)
+                     rope_delta_t_max_ms=86_400_000, out_f32=1, deterministic=det)
     b = to_dev_batch(cu, t, s, ncv, T, n_static=nstv, flags=pf)
     lib = L.lib()
     Xd = bf16_tensor(X)
@@ -200,34 +200,19 @@ def test_attn_core_mask_rules_forward_backward(ops, case):
         assert (to_np(got)[cu[-1]:] == 0).all()
 
 
-@pytest.mark.parametrize("case", [1, 3])
-def test_deterministic_backward_is_bit_reproducible(ops, case):
-    """cfg.deterministic = 1: fixed-order split-K slabs + fixed-order D give bit-identical dX and weight
-    gradients on repeated runs, equal to the atomic mode up to fp32 summation order."""
-    from paper_2602_11410_b200 import _lib as L
-    from tests.test_gpu_layer import run_layer_forward
-    lib = L.lib()
-    lengths, d, H, nc, peaky, flags, nst, use_pf = STAGE_CASES[case]
-    cu, t, s, ncv, T, X, W = layer_case(lengths, d, H, nc, seed=70 + case, peaky=peaky)
-    b = to_dev_batch(cu, t, s, ncv, T)
-    dY = G.normal_bf16(71, case, (T, d))
-    dY[cu[-1]:] = 0
-    dYd = bf16_tensor(dY)
-    outs = []
-    for det in (1, 1, 0):
-        cfg = ops.config(d, H, mask_flags=flags, delta_delay_ms=120_000, rope_phi_min=0.5, rope_base=1e4,
-                         rope_delta_t_max_ms=86_400_000, deterministic=det)
-        Y, saved, ws, Xd, Wd, w = run_layer_forward(ops, cfg, b, X, W, T, two_pass=True)
-        dX = torch.empty(T, d, dtype=torch.bfloat16, device="cuda")
-        gs = [torch.empty(d, d, dtype=torch.float32, device="cuda") for _ in range(7)]
-        g = L.AttnGrads(*[x.data_ptr() for x in gs])
-        L.check(lib.cadet_attn_backward(C.byref(cfg), C.byref(b.struct()), C.byref(w), C.c_void_p(Xd.data_ptr()),
-                                        C.c_void_p(saved.data_ptr()), C.c_void_p(dYd.data_ptr()),
-                                        C.c_void_p(dX.data_ptr()), None, C.byref(g), C.c_void_p(ws.data_ptr()),
-                                        ws.numel(), C.c_void_p(torch.cuda.current_stream().cuda_stream)))
-        torch.cuda.synchronize()
-        outs.append([dX.clone()] + [x.clone() for x in gs])
-    for a_, b_ in zip(outs[0], outs[1]):
-        assert torch.equal(a_, b_)
-    for a_, b_ in zip(outs[0][1:], outs[2][1:]):
-        assert float((a_ - b_).abs().max()) <= 1e-5 * max(1.0, float(b_.abs().max()))
+@pytest.mark.parametrize("case", [1, 3, 4])
+def test_deterministic_backward_stages_and_bit_reproducibility(ops, case):
+    """cfg.deterministic = 1: fixed-order split-K slabs + the fixed-order D preprocess.  Every stage
+    passes the same gates as the atomic mode, and two runs give bit-identical dX, taps and weight
+    gradients."""
+    from tests.stage_check import check_layer_stages
+    r1 = run_case(ops, case, with_resid=True, det=1)
+    r2 = run_case(ops, case, with_resid=True, det=1)
+    check_layer_stages(r1["X"], r1["W"], r1["sv"], r1["taps"], r1["wsb"], r1["D"], r1["dY"], r1["meta"],
+                       oracle_cfg(r1["cfg"]), range(len(r1["lengths"])), resid=r1["R"], dresid=r1["dY"],
+                       peaky=r1["peaky"], weight_grads=r1["gW"], d_from_stored=True, tag=f"deterministic case {case}")
+    assert (r1["dX"] == r2["dX"]).all() and (r1["D"] == r2["D"]).all()
+    for a_, b_ in zip(r1["gW"], r2["gW"]):
+        assert (a_ == b_).all()
+    for k in ("dQr", "dKr", "dV", "dQ", "dK", "dX"):
+        assert (r1["taps"][k] == r2["taps"][k]).all(), k
