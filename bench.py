@@ -240,6 +240,16 @@ def run_oracle_step(seqs, wl: dict, seed: int):
     return loss
 
 
+def blas_info():
+    """The BLAS the oracle's numpy runs on (threadpoolctl), e.g. openblas / mkl and its thread count."""
+    try:
+        from threadpoolctl import threadpool_info
+        return [{k: i.get(k) for k in ("internal_api", "version", "num_threads", "threading_layer")}
+                for i in threadpool_info() if i.get("user_api") == "blas"]
+    except Exception as ex:  # noqa: BLE001
+        return f"unavailable: {type(ex).__name__}"
+
+
 def cpu_cores():
     try:
         return len(os.sched_getaffinity(0))
@@ -283,6 +293,9 @@ def main():
                     help="NEXT-4: append the AdamW step (R35) to every training step")
     ap.add_argument("--no-shard", action="store_true",
                     help="with --optimizer and N > 1: replicated AdamW after all-reduce instead of HSDP sharding")
+    ap.add_argument("--seeds", type=int, default=1,
+                    help="also time the step on batches of seeds 0..S-1 (SURVEY 8(d): mean +- sd over seeds); "
+                         "the headline value stays seed 0")
     ap.add_argument("--graph", action="store_true",
                     help="replay the step as one CUDA graph (measured: no gain over eager launches on C4)")
     args = ap.parse_args()
@@ -316,7 +329,7 @@ def main():
                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                "config": {"workload": workload_name, "sample": desc},
                "cpu_baseline": {"value": val, "unit": "tokens/s", "cores": cpu_cores(), "kind": "oracle",
-                                "sample": desc},
+                                "sample": desc, "blas": blas_info()},
                "e2e": {"value": val, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(out))
         return
@@ -426,6 +439,7 @@ def main():
     if not args.no_e2e:
         steps = args.steps
         loss_h = torch.zeros(steps + 2, dtype=torch.float32).pin_memory()
+        logits_h = torch.zeros(2, n_imp, scfg.K, dtype=torch.float32).pin_memory()  # the step's result: tower logits
         bufs = [inp, host_inp.to(dev)]
         main = torch.cuda.current_stream()
         copy_st = torch.cuda.Stream(dev)
@@ -450,6 +464,7 @@ def main():
                 stack.step(bufs[bi], step_group)
                 free[bi].record(main)
                 loss_h[i:i + 1].copy_(stack.loss, non_blocking=True)
+                logits_h[i & 1].copy_(stack.logits, non_blocking=True)
         run(2)
         torch.cuda.synchronize()
         barrier()
@@ -463,10 +478,43 @@ def main():
         if group is not None:
             dist.all_reduce(ems, op=dist.ReduceOp.MAX)
         e2e = {"value": tokens_all / (float(ems.item()) / 1000.0), "unit": "tokens/s",
-               "h2d_bytes_per_step": int(host_inp.nbytes()), "d2h_bytes_per_step": 4,
+               "h2d_bytes_per_step": int(host_inp.nbytes()), "d2h_bytes_per_step": 4 + 4 * n_imp * scfg.K,
+               "d2h": "loss + the K tower logits of every impression (the north star's output)",
                "ms_per_step": float(ems.item()),
                "pipeline": "inputs of step i+1 copied (pinned host -> HBM, copy stream) while step i computes"}
     stack.poll()
+
+    # ---------------- other batches (seeds 1..S-1), each timed like seed 0 (resident inputs)
+    seeds = None
+    if args.seeds > 1:
+        per = [(0, ms_max, inp.tokens, total_flops)]
+        for sd in range(1, args.seeds):
+            _, h_s = build_inputs(wl, sd, pin=False, rank=rank, world=world, J=2 if args.full_loss else 0)
+            inp_s = h_s.to(dev)
+            fl_s = sum(step_flops(wl, inp_s.tokens, stack.pairs(inp_s), inp_s.rows.numel(), scfg.dh).values())
+            for _ in range(args.warmup):
+                stack.step(inp_s, step_group)
+            torch.cuda.synchronize()
+            barrier()
+            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a0.record()
+            for _ in range(args.steps):
+                stack.step(inp_s, step_group)
+            a1.record()
+            torch.cuda.synchronize()
+            barrier()
+            tt = torch.tensor([a0.elapsed_time(a1) / args.steps], dtype=torch.float64, device=dev)
+            if group is not None:
+                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            per.append((sd, float(tt.item()), inp_s.tokens, fl_s))
+            stack.poll()
+        msv = np.array([p_[1] for p_ in per])
+        tokv = np.array([p_[2] for p_ in per]) * world / (msv / 1000.0)
+        tfv = np.array([p_[3] for p_ in per]) / (msv / 1000.0) / 1e12
+        seeds = {"n": len(per), "ms_per_step": {"mean": float(msv.mean()), "sd": float(msv.std(ddof=1))},
+                 "tokens_per_s": {"mean": float(tokv.mean()), "sd": float(tokv.std(ddof=1))},
+                 "tflops_per_gpu": {"mean": float(tfv.mean()), "sd": float(tfv.std(ddof=1))},
+                 "per_seed": [{"seed": p_[0], "ms": p_[1], "tokens": p_[2]} for p_ in per]}
 
     if rank != 0:
         if group is not None:
@@ -478,7 +526,14 @@ def main():
     per_step_ms = {k: v[0] / prof_steps for k, v in prof.items()}
     dom = max(("gemm", "attn_fwd", "attn_bwd"), key=lambda k: per_step_ms[k])
     achieved = flops[dom] / (per_step_ms[dom] / 1000.0) / 1e12 if per_step_ms[dom] > 0 else 0.0
-    peak = float(peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops")))
+    # Peak: the measured BURST bf16 rate for a timed region shorter than a second at full clocks with no
+    # power capping (the driver's burst figure is the matmul timed alone); the SUSTAINED rate when the
+    # region is long or the clocks show capping / throttling (MEASURED_PEAKS.json holds both)
+    region_s = ms * args.steps / 1000.0
+    capped = bool(clk.get("reasons")) or (clk.get("sm_mhz") or 0) < 0.95 * (clk.get("sm_max_mhz") or 1)
+    burst = region_s < 1.0 and not capped
+    peak_key = "bf16_tflops" if burst else "bf16_tflops_sustained"
+    peak = float(peaks.get(peak_key, peaks.get("bf16_tflops")))
     traffic, traffic_src = None, None
     tpath = os.path.join(ROOT, "profiles", TRAFFIC_PROFILE)
     if os.path.exists(tpath) and args.workload == "c4":
@@ -488,14 +543,33 @@ def main():
     roofline = {"bound": "tensor", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                 "frac": achieved / peak, "traffic": traffic, "traffic_unit": "DRAM bytes per launch",
                 "traffic_source": traffic_src,
-                "peak_source": f"{peak_src} bf16_tflops_sustained (kernel timed inside a long step)",
+                "peak_source": f"{peak_src} {peak_key}",
+                "peak_rule": (f"timed region {region_s:.3f} s, clocks median {clk.get('sm_mhz')} of {clk.get('sm_max_mhz')} "
+                              f"MHz, reasons {clk.get('reasons')}: burst if < 1 s and uncapped, else sustained"),
                 "share_of_step": per_step_ms[dom] / ms, "per_class_ms_per_step": per_step_ms,
                 "launches_per_step": {k: v[1] / prof_steps for k, v in prof.items()}}
+    # the attention core alone (SURVEY 8(d) view 2): A5 + A10 algorithmic FLOPs on allowed pairs
+    # (4 d P fwd + 8 d P bwd per layer), against the same peak; the FlashAttention convention
+    # (bwd = 2.5 x fwd) printed for comparability; DRAM bytes vs the 8 d / 20 d B per token per layer
+    attn_ms = per_step_ms["attn_fwd"] + per_step_ms["attn_bwd"]
+    attn_fl = flops["attn_fwd"] + flops["attn_bwd"]
+    attn_tf = attn_fl / (attn_ms / 1000.0) / 1e12 if attn_ms > 0 else 0.0
+    attn_view = {"flops_per_step": attn_fl, "ms_per_step": attn_ms, "achieved": attn_tf, "peak": peak,
+                 "unit": "TFLOP/s", "frac": attn_tf / peak,
+                 "fwd": {"ms": per_step_ms["attn_fwd"], "tflops": flops["attn_fwd"] / max(per_step_ms["attn_fwd"], 1e-9) / 1e9},
+                 "bwd": {"ms": per_step_ms["attn_bwd"], "tflops": flops["attn_bwd"] / max(per_step_ms["attn_bwd"], 1e-9) / 1e9},
+                 "flash_attention_convention_tflops": 3.5 * flops["attn_fwd"] / (attn_ms / 1000.0) / 1e12 if attn_ms > 0 else 0.0,
+                 "algorithmic_bytes_per_step": {"fwd": 8.0 * wl["d_model"] * inp.tokens * wl["n_layers"],
+                                                "bwd": 20.0 * wl["d_model"] * inp.tokens * wl["n_layers"]}}
+    if os.path.exists(tpath) and args.workload == "c4":
+        tj = json.load(open(tpath))
+        attn_view["dram_bytes_per_step"] = {k: tj[k]["dram_bytes_per_step"] for k in ("attn_fwd", "attn_bwd") if k in tj}
+        attn_view["dram_source"] = f"profiles/{TRAFFIC_PROFILE}"
     cpu = None
     if not args.no_cpu and world == 1:
         v, tokc, dt, desc = time_oracle(users, wl, 0)
         cpu = {"value": v, "unit": "tokens/s", "cores": cpu_cores(), "kind": "oracle", "sample": desc,
-               "seconds": dt}
+               "seconds": dt, "blas": blas_info()}
     out = {
         "metric": metric, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
@@ -514,10 +588,11 @@ def main():
                    else "gated attention layer (Eq. 3-7) + residual",
                    "partition": "rank r = shard r of an LPT partition of one user stream into 8 budgets"},
         "tflops": tflops_all, "tflops_per_gpu": tflops_all / world,
-        "frac_of_peak_measured": tflops_all / world / float(peaks.get("bf16_tflops", 1663.9)),
+        "frac_of_peak_measured": tflops_all / world / peak, "peak_measured": {"key": peak_key, "tflops": peak},
         "frac_of_peak_spec": tflops_all / world / 2250.0,
         "flops_per_step_per_rank": flops,
-        "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
+        "roofline": roofline, "attention_core": attn_view, "seeds": seeds,
+        "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
         "cuda_graph": graph is not None, "cuda_graph_error": graph_err,
     }
     print(json.dumps(out))

@@ -135,6 +135,7 @@ struct RgSides {
   RgSide s[2];
 };
 // blockIdx.y = side (Q, K): both sides of A11 in one launch
+template <bool TAPS>
 __global__ void __launch_bounds__(256) rope_gate_bwd_kernel(RgSides sides, int dr_f32, int r_bf16, int T, int d,
                                                             int hd, const float* cs) {
   pdl_trigger();
@@ -192,7 +193,9 @@ __global__ void __launch_bounds__(256) rope_gate_bwd_kernel(RgSides sides, int d
       const float u0 = g[2 * e] * x.x * g0 * (1.f - g0), u1 = g[2 * e + 1] * x.y * g1 * (1.f - g1);
       __nv_bfloat162 v = __floats2bfloat162_rn(u0, u1);
       uo[e] = *reinterpret_cast<uint32_t*>(&v);
-      if (sd.tap_u) *reinterpret_cast<float2*>(sd.tap_u + off + 2 * e) = make_float2(u0, u1);
+      if constexpr (TAPS) {
+        if (sd.tap_u) *reinterpret_cast<float2*>(sd.tap_u + off + 2 * e) = make_float2(u0, u1);
+      }
       r[2 * e] = g[2 * e] * g0;
       r[2 * e + 1] = g[2 * e + 1] * g1;
     }
@@ -201,10 +204,12 @@ __global__ void __launch_bounds__(256) rope_gate_bwd_kernel(RgSides sides, int d
 #pragma unroll
     for (int e = 0; e < 8; ++e) r[e] = g[e];
   }
-  if (sd.tap_r) {
-    float4* t4 = reinterpret_cast<float4*>(sd.tap_r + off);
-    t4[0] = make_float4(r[0], r[1], r[2], r[3]);
-    t4[1] = make_float4(r[4], r[5], r[6], r[7]);
+  if constexpr (TAPS) {
+    if (sd.tap_r) {
+      float4* t4 = reinterpret_cast<float4*>(sd.tap_r + off);
+      t4[0] = make_float4(r[0], r[1], r[2], r[3]);
+      t4[1] = make_float4(r[4], r[5], r[6], r[7]);
+    }
   }
   if (r_bf16) {
     uint32_t ro[4];
@@ -421,7 +426,8 @@ cudaError_t rope_gate_bwd_launch2(const void* const* dr, const void* const* Xq, 
   ProfScope ps(PROF_OTHER, st, 1);
   const size_t work = (size_t)T * d / 8;
   if (work)
-    launch_pdl(rope_gate_bwd_kernel, dim3(blocks(work, 256), nsides), dim3(256), 0, st, sides, dr_f32, r_bf16, T, d,
+    launch_pdl((tap_u || tap_r) ? rope_gate_bwd_kernel<true> : rope_gate_bwd_kernel<false>, dim3(blocks(work, 256), nsides),
+               dim3(256), 0, st, sides, dr_f32, r_bf16, T, d,
                hd, cs);
   return cudaGetLastError();
 }
