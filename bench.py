@@ -530,7 +530,10 @@ def main():
     # power capping (the driver's burst figure is the matmul timed alone); the SUSTAINED rate when the
     # region is long or the clocks show capping / throttling (MEASURED_PEAKS.json holds both)
     region_s = ms * args.steps / 1000.0
-    capped = bool(clk.get("reasons")) or (clk.get("sm_mhz") or 0) < 0.95 * (clk.get("sm_max_mhz") or 1)
+    # (a sw_power_cap flag with the median SM clock at max does not lower the rate; a median clock below
+    # 95 % of max or a thermal / hardware slowdown does)
+    hard = {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"} & set(clk.get("reasons") or [])
+    capped = bool(hard) or (clk.get("sm_mhz") or 0) < 0.95 * (clk.get("sm_max_mhz") or 1)
     burst = region_s < 1.0 and not capped
     peak_key = "bf16_tflops" if burst else "bf16_tflops_sustained"
     peak = float(peaks.get(peak_key, peaks.get("bf16_tflops")))
@@ -545,7 +548,8 @@ def main():
                 "traffic_source": traffic_src,
                 "peak_source": f"{peak_src} {peak_key}",
                 "peak_rule": (f"timed region {region_s:.3f} s, clocks median {clk.get('sm_mhz')} of {clk.get('sm_max_mhz')} "
-                              f"MHz, reasons {clk.get('reasons')}: burst if < 1 s and uncapped, else sustained"),
+                              f"MHz, reasons {clk.get('reasons')}: burst if < 1 s, median clock >= 95 % of max and no thermal / "
+                              f"hw slowdown, else sustained"),
                 "share_of_step": per_step_ms[dom] / ms, "per_class_ms_per_step": per_step_ms,
                 "launches_per_step": {k: v[1] / prof_steps for k, v in prof.items()}}
     # the attention core alone (SURVEY 8(d) view 2): A5 + A10 algorithmic FLOPs on allowed pairs

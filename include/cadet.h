@@ -91,11 +91,10 @@ typedef struct {
                             grows by 3 * splits * d^2 * 4 B) and a reduction sums the slabs in split order; D
                             comes from the fixed-order preprocess kernel.  The attention kernels, the mask plan
                             and every forward kernel are atomic-free in both modes (P:569 reproducibility). */
-  int32_t plan_ready;    /* 0 = plan inside the call; 1 = ws already holds cadet_mask_plan's plan for this batch
-                            (same ws, same batch): the layer/core calls skip re-planning (one plan per step for
-                            all layers); 2 = as 1 and ws also holds the RoPE (cos, sin) table, which
-                            cadet_mask_plan builds when given >= cadet_attn_workspace_bytes with use_rope
-                            (one table per step instead of one per layer call) */
+  int32_t plan_ready;    /* 0 = plan inside the call; 1 (or 2, kept for compatibility) = ws already holds
+                            cadet_mask_plan's plan for this batch (same ws, same batch): the layer/core calls skip
+                            re-planning (one plan per step for all layers).  RoPE angles are evaluated on the fly
+                            from the int64 timestamps by the kernels that rotate: no (cos, sin) table in HBM. */
   int64_t delta_delay_ms;       /* Delta for context queries, Eq. 6; default 3,600,000 */
   int64_t delta_cand_ms;        /* Delta for candidate queries; default 0 (R11) */
   int64_t rope_delta_t_max_ms;  /* Delta t_max; default 31,536,000,000 = 1 year (R6) */

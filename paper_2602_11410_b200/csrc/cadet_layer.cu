@@ -172,7 +172,6 @@ enum { TAP_ZX, TAP_XT, TAP_Q, TAP_K, TAP_V, TAP_ZQ, TAP_ZK, TAP_QR, TAP_KR, TAP_
        TAP_DV, TAP_UQ, TAP_RQ, TAP_UK, TAP_RK, TAP_DQ, TAP_DK, TAP_UX, TAP_RX, TAP_DX, N_TAPS };
 static_assert(N_TAPS == CADET_N_TAPS, "tap list out of sync with cadet.h");
 struct LayerWs {    // carved from `ws` after the plan
-  float* rope_cs;   // [T][hd + 32] (cos, sin) table
   float* D;
   void *dO, *dKr, *dV, *uq, *uk, *dQ, *dK, *ux;
   float *dQacc, *rq, *rk, *rx;
@@ -206,8 +205,7 @@ size_t det_slab_bytes(const cadet_attn_config* c, int T) {
 }
 size_t layer_ws_base_bytes(const cadet_attn_config* c, int n, int T) {
   const int d = c->d_model;
-  return plan_bytes(n, T, T) + a256((size_t)4 * T * (c->head_dim + 32)) +
-         a256((size_t)4 * c->n_heads * T) + 8 * bf_sz(T, d) + 4 * f_sz(T, d) + (c->out_f32 ? N_TAPS * f_sz(T, d) : 0) +
+  return plan_bytes(n, T, T) + a256((size_t)4 * c->n_heads * T) + 8 * bf_sz(T, d) + 4 * f_sz(T, d) + (c->out_f32 ? N_TAPS * f_sz(T, d) : 0) +
          det_slab_bytes(c, T);
 }
 size_t layer_ws_bytes(const cadet_attn_config* c, int n, int T) {
@@ -229,8 +227,6 @@ LayerWs carve_ws(void* ws, const cadet_attn_config* c, int n, int T) {
   const int d = c->d_model;
   uint8_t* p = reinterpret_cast<uint8_t*>(ws) + plan_bytes(n, T, T);
   LayerWs W;
-  W.rope_cs = reinterpret_cast<float*>(p);
-  p += a256((size_t)4 * T * (c->head_dim + 32));
   W.D = reinterpret_cast<float*>(p);
   p += a256((size_t)4 * c->n_heads * T);
   void** bf[8] = {&W.dO, &W.dKr, &W.dV, &W.uq, &W.uk, &W.dQ, &W.dK, &W.ux};
@@ -251,15 +247,16 @@ LayerWs carve_ws(void* ws, const cadet_attn_config* c, int n, int T) {
   return W;
 }
 
-// The per-step (cos, sin) table (rope_table_kernel) into the layer workspace.
-cudaError_t rope_prepare(const cadet_attn_config* cfg, const cadet_batch* b, const LayerWs& W, const PlanView& v,
-                         cudaStream_t st) {
-  const int hd = cfg->head_dim;
-  cudaError_t e = cudaSuccess;
-  if (cfg->use_rope)
-    e = rope_table_launch(W.rope_cs, b->total_tokens, hd, cfg->rope_phi_min, cfg->rope_base,
-                          (double)cfg->rope_delta_t_max_ms, b->timestamps_ms, v.row_seq, b->cu_seqlens, st);
-  return e;
+// Timestamp RoPE of the layer, evaluated on the fly by the kernels that rotate
+RopeOTF rope_of(const cadet_attn_config* cfg, const cadet_batch* b, const PlanView& v) {
+  RopeOTF r;
+  r.t = b->timestamps_ms;
+  r.row_seq = v.row_seq;
+  r.cu = b->cu_seqlens;
+  r.th0 = cfg->rope_phi_min / (double)cfg->rope_delta_t_max_ms;
+  r.base = cfg->rope_base;
+  r.on = cfg->use_rope;
+  return r;
 }
 
 int pick_bn(int M, int N) {
@@ -387,7 +384,8 @@ cadet_status cadet_attn_forward(const cadet_attn_config* cfg, const cadet_batch*
   PlanView v = plan_carve(ws, n, T, T);
   LayerBufs L = carve_saved(saved, cfg, T);
   LayerWs W = carve_ws(ws, cfg, n, T);
-  cudaError_t e = cfg->plan_ready >= 2 ? cudaSuccess : rope_prepare(cfg, b, W, v, st);
+  cudaError_t e = cudaSuccess;
+  const RopeOTF rp = rope_of(cfg, b, v);
   const int bn = pick_bn(T, d);
   // A2: representation gate  Xt = X * sigma(X W_xg)   (Eq. 4)
   const void* Xt = X;
@@ -430,11 +428,11 @@ cadet_status cadet_attn_forward(const cadet_attn_config* cfg, const cadet_batch*
       }
       e = gemm_launch(g, 2, bn, st);
       if (e == cudaSuccess)
-        e = gate_rope_fwd_launch(L.Q, L.K, L.Zq, L.Zk, cfg->use_rope ? W.rope_cs : nullptr, L.Qr, L.Kr, T, d, hd, st,
+        e = gate_rope_fwd_launch(L.Q, L.K, L.Zq, L.Zk, rp, L.Qr, L.Kr, T, d, hd, st,
                                  W.tap[TAP_QR], W.tap[TAP_KR]);
     } else if (cfg->use_rope) {
-      e = rope_apply_launch(L.Q, L.Qr, T, d, hd, W.rope_cs, st);
-      if (e == cudaSuccess) e = rope_apply_launch(L.K, L.Kr, T, d, hd, W.rope_cs, st);
+      e = rope_apply_launch(L.Q, L.Qr, T, d, hd, rp, st);
+      if (e == cudaSuccess) e = rope_apply_launch(L.K, L.Kr, T, d, hd, rp, st);
     } else {
       e = cudaMemcpyAsync(L.Qr, L.Q, (size_t)T * d * 2, cudaMemcpyDeviceToDevice, st);
       if (e == cudaSuccess) e = cudaMemcpyAsync(L.Kr, L.K, (size_t)T * d * 2, cudaMemcpyDeviceToDevice, st);
@@ -501,8 +499,8 @@ cadet_status cadet_attn_backward_ev(const cadet_attn_config* cfg, const cadet_ba
   const int bn = pick_bn(T, d);
   const int bnw = pick_bn_wgrad(d);
   const size_t wbytes = (size_t)d * d * 4;
-  cudaError_t e = cfg->plan_ready >= 2 ? cudaSuccess : rope_prepare(cfg, b, W, v, st);
-  const float* cs = cfg->use_rope ? W.rope_cs : nullptr;
+  cudaError_t e = cudaSuccess;
+  const RopeOTF cs = rope_of(cfg, b, v);
   float* gws[7] = {gr->dW_xg, gr->dW_q, gr->dW_k, gr->dW_v, gr->dW_qg, gr->dW_kg, gr->dW_o};
   // deterministic mode: no fp32 atomics anywhere in the layer backward -- split-K weight-gradient partials
   // go to slabs summed in a fixed order, and D comes from the (fixed-order) preprocess kernel
@@ -935,15 +933,9 @@ cadet_status cadet_ffn_backward(const void* X, const void* W1, const void* W2, c
 }  // extern "C"
 
 namespace cadet {
-// cadet_mask_plan's extension (plan_ready = 2): with a layer-sized workspace also build the
-// per-step RoPE table, so the layer calls of the step skip it.
-cudaError_t layer_plan_extras(const cadet_attn_config* cfg, const cadet_batch* b, void* ws, size_t ws_bytes,
-                              cudaStream_t st) {
-  if (!cfg->use_rope || cfg->dtype == CADET_FP32 || ws_bytes < layer_ws_bytes(cfg, b->n_seqs, b->total_tokens) ||
-      b->total_tokens == 0)
-    return cudaSuccess;
-  PlanView v = plan_carve(ws, b->n_seqs, b->total_tokens, b->total_tokens);
-  LayerWs W = carve_ws(ws, cfg, b->n_seqs, b->total_tokens);
-  return rope_prepare(cfg, b, W, v, st);
+// cadet_mask_plan's extension (plan_ready = 2): formerly the per-step RoPE table; RoPE angles are now
+// evaluated on the fly, so there is nothing to prepare.
+cudaError_t layer_plan_extras(const cadet_attn_config*, const cadet_batch*, void*, size_t, cudaStream_t) {
+  return cudaSuccess;
 }
 }  // namespace cadet

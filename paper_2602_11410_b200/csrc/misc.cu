@@ -1,6 +1,6 @@
 // Elementwise / reduction kernels of the hot path that are HBM-bound (no tensor cores):
-//   rope_table_kernel       (cos, sin)(dt_row theta_i) per (row, frequency), theta_i = (phi_min /
-//                           dt_max) base^(2i/hd); shared by every head and by Q and K
+//   (RoPE angles alpha_i = dt_row theta_i, theta_i = (phi_min / dt_max) base^(2i/hd), are
+//    evaluated on the fly by the kernels that rotate: no (cos, sin) table exists in HBM)
 //   gate_rope_fwd_kernel    A4: Qr = RoPE(Q * sigma(Zq)), Kr = RoPE(K * sigma(Zk))
 //   rope_apply_kernel       RoPE without interaction gate (ablation path)
 //   rope_gate_bwd_kernel    A11: dQt = R(-alpha) dQr; g = sigma(Zq); u = dQt*Q*g*(1-g); r = dQt*g
@@ -26,38 +26,27 @@ __device__ __forceinline__ void rope_cs(double dt, double th, float& c, float& s
   __sincosf(r, &s, &c);
 }
 
-// cs[row][2i] = cos(alpha_i), cs[row][2i + 1] = sin(alpha_i), alpha_i = dt_row theta_i with
-// dt_row = t_row - t_(sequence start); row stride hd + 32 floats, the first 32 entries
-// repeated at [hd, hd + 32) so that any 32-float window starting at an even head-local column
-// is contiguous (a GEMM epilogue slice may cross one head edge when hd % 32 != 0).
-// theta_i = (phi_min / Delta t_max) base^(2i / hd), evaluated per block into shared memory
-__global__ void __launch_bounds__(256) rope_table_kernel(float* cs, int T, int hd, double phi_min, double base,
-                                                         double dt_max, const int64_t* t, const int32_t* row_seq,
-                                                         const int32_t* cu) {
-  pdl_trigger();
-  pdl_wait();
-  // one warp per row: the row's rebased time is loaded once, theta_i from shared memory, each lane
-  // evaluates entries lane, lane + 32, ... of the row's hd / 2 + 16 (cos, sin) pairs
-  __shared__ double th[64];
-  const int half = hd / 2, w = half + 16;
-  for (int i = threadIdx.x; i < half; i += blockDim.x) th[i] = (phi_min / dt_max) * pow(base, 2.0 * i / (double)hd);
+// theta_i of the block's head dim into shared memory (identical formula on every path)
+__device__ __forceinline__ void rope_theta_smem(double* th, const RopeOTF& rp, int hd) {
+  if (rp.on)
+    for (int i = threadIdx.x; i < hd / 2; i += blockDim.x) th[i] = rp.th0 * pow(rp.base, 2.0 * i / (double)hd);
   __syncthreads();
-  const int row = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
-  if (row >= T) return;
-  const int s = row_seq[row];
-  const double dt = s >= 0 ? (double)(t[row] - t[cu[s]]) : 0.0;
-  float2* out = reinterpret_cast<float2*>(cs + (size_t)row * (hd + 32));
-  for (int i = lane; i < w; i += 32) {
-    float c, sn;
-    rope_cs(dt, th[i < half ? i : i - half], c, sn);
-    out[i] = make_float2(c, sn);
-  }
+}
+// (cos, sin) of pairs i0 .. i0 + N - 1 of `row` (rebased time of the row's sequence)
+template <int N>
+__device__ __forceinline__ void rope_row_cs(const RopeOTF& rp, const double* th, int row, int i0, float (&c)[N],
+                                            float (&s)[N]) {
+  const int sq = rp.row_seq[row];
+  const double dt = sq >= 0 ? (double)(rp.t[row] - rp.t[rp.cu[sq]]) : 0.0;
+#pragma unroll
+  for (int e = 0; e < N; ++e) rope_cs(dt, th[i0 + e], c[e], s[e]);
 }
 
 // one thread per (row, pair of columns)
-__global__ void rope_apply_kernel(const __nv_bfloat16* in, __nv_bfloat16* out, int T, int d, int hd,
-                                  const float* cs) {
+__global__ void rope_apply_kernel(const __nv_bfloat16* in, __nv_bfloat16* out, int T, int d, int hd, RopeOTF rp) {
   pdl_trigger();
+  __shared__ double th[64];
+  rope_theta_smem(th, rp, hd);
   pdl_wait();
   const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   const size_t pairs = (size_t)T * d / 2;
@@ -65,18 +54,22 @@ __global__ void rope_apply_kernel(const __nv_bfloat16* in, __nv_bfloat16* out, i
   const int row = (int)(idx / (d / 2));
   const int c = (int)(idx % (d / 2)) * 2;
   const float2 v = __bfloat1622float2(reinterpret_cast<const __nv_bfloat162*>(in)[idx]);
-  const float2 r = *reinterpret_cast<const float2*>(cs + (size_t)row * (hd + 32) + (c % hd));
-  reinterpret_cast<__nv_bfloat162*>(out)[idx] = __floats2bfloat162_rn(v.x * r.x - v.y * r.y, v.x * r.y + v.y * r.x);
+  float cv[1] = {1.f}, sv[1] = {0.f};
+  if (rp.on) rope_row_cs<1>(rp, th, row, (c % hd) / 2, cv, sv);
+  reinterpret_cast<__nv_bfloat162*>(out)[idx] =
+      __floats2bfloat162_rn(v.x * cv[0] - v.y * sv[0], v.x * sv[0] + v.y * cv[0]);
 }
 
 // A4 after the gate GEMMs (Z_q = Q W_qg, Z_k = K W_kg stored bf16): Qr = RoPE_t(Q * sigma(Z_q)) and
 // Kr = RoPE_t(K * sigma(Z_k)) in one HBM pass (Eq. 5 + P:274); one thread per (row, 8 columns), Q
-// and K together so the row's table window is read once; cs null = no RoPE.
+// and K together so the row's angles are evaluated once; rp.on = 0: no RoPE.
 __global__ void __launch_bounds__(256) gate_rope_fwd_kernel(const __nv_bfloat16* Q, const __nv_bfloat16* K,
                                                             const __nv_bfloat16* Gq, const __nv_bfloat16* Gk,
-                                                            const float* cs, __nv_bfloat16* Qr, __nv_bfloat16* Kr,
+                                                            RopeOTF rp, __nv_bfloat16* Qr, __nv_bfloat16* Kr,
                                                             int T, int d, int hd, float* tapQ, float* tapK) {
   pdl_trigger();
+  __shared__ double th[64];
+  rope_theta_smem(th, rp, hd);
   pdl_wait();
   const int per_row = d / 8;
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;
@@ -84,11 +77,7 @@ __global__ void __launch_bounds__(256) gate_rope_fwd_kernel(const __nv_bfloat16*
   const int row = idx / per_row, c0 = (idx - row * per_row) * 8;
   const size_t off = (size_t)row * d + c0;
   float cv[4] = {1.f, 1.f, 1.f, 1.f}, sv[4] = {0.f, 0.f, 0.f, 0.f};
-  if (cs) {  // the 8-column group never crosses a head edge (hd % 8 == 0)
-    const float4* q = reinterpret_cast<const float4*>(cs + (size_t)row * (hd + 32) + (c0 % hd));
-    const float4 a = q[0], b = q[1];
-    cv[0] = a.x, sv[0] = a.y, cv[1] = a.z, sv[1] = a.w, cv[2] = b.x, sv[2] = b.y, cv[3] = b.z, sv[3] = b.w;
-  }
+  if (rp.on) rope_row_cs<4>(rp, th, row, (c0 % hd) / 2, cv, sv);  // the 8-column group never crosses a head edge
   const __nv_bfloat16* src[2] = {Q, K};
   const __nv_bfloat16* gate[2] = {Gq, Gk};
   __nv_bfloat16* dst[2] = {Qr, Kr};
@@ -121,7 +110,7 @@ __global__ void __launch_bounds__(256) gate_rope_fwd_kernel(const __nv_bfloat16*
 // dr: fp32 (dQr accumulator) or bf16 (dKr).  gate (Z) bf16 may be null (no interaction gate):
 // then out_u is unused and out_r (bf16 if r_bf16) receives dQt directly.
 // One thread = 8 consecutive columns (4 pairs) of one row: 16-byte accesses, (cos, sin) from the
-// rope table (cs, row stride hd + 32; null without RoPE).
+// row's RoPE angles evaluated on the fly (rp.on = 0: no RoPE).
 struct RgSide {
   const void* dr;
   const __nv_bfloat16* Xq;
@@ -137,8 +126,10 @@ struct RgSides {
 // blockIdx.y = side (Q, K): both sides of A11 in one launch
 template <bool TAPS>
 __global__ void __launch_bounds__(256) rope_gate_bwd_kernel(RgSides sides, int dr_f32, int r_bf16, int T, int d,
-                                                            int hd, const float* cs) {
+                                                            int hd, RopeOTF rp) {
   pdl_trigger();
+  __shared__ double th[64];
+  rope_theta_smem(th, rp, hd);
   pdl_wait();
   const RgSide& sd = sides.s[blockIdx.y];
   const void* dr = sd.dr;
@@ -167,10 +158,9 @@ __global__ void __launch_bounds__(256) rope_gate_bwd_kernel(RgSides sides, int d
       g[2 * e + 1] = f.y;
     }
   }
-  if (cs) {  // R(-alpha): the 8-column group never crosses a head edge (hd % 8 == 0)
-    const float4* q = reinterpret_cast<const float4*>(cs + (size_t)row * (hd + 32) + (c0 % hd));
-    const float4 a = q[0], b = q[1];
-    const float cv[4] = {a.x, a.z, b.x, b.z}, sv[4] = {a.y, a.w, b.y, b.w};
+  if (rp.on) {  // R(-alpha): the 8-column group never crosses a head edge (hd % 8 == 0)
+    float cv[4], sv[4];
+    rope_row_cs<4>(rp, th, row, (c0 % hd) / 2, cv, sv);
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       const float x0 = g[2 * e], x1 = g[2 * e + 1];
@@ -392,28 +382,17 @@ __global__ void add_bf16_kernel(const __nv_bfloat16* a, const __nv_bfloat16* b, 
 // ---------------------------------------------------------------- launchers
 static inline unsigned blocks(size_t n, unsigned b) { return (unsigned)((n + b - 1) / b); }
 
-cudaError_t rope_table_launch(float* cs, int T, int hd, double phi_min, double base, double dt_max, const int64_t* t,
-                              const int32_t* row_seq, const int32_t* cu, cudaStream_t st) {
-  ProfScope ps(PROF_OTHER, st, 1);
-  const size_t work = (size_t)T * (hd / 2 + 16);
-  if (work >= (size_t)INT32_MAX) return cudaErrorInvalidValue;
-  if (hd / 2 > 64) return cudaErrorInvalidValue;
-  if (work)
-    launch_pdl(rope_table_kernel, dim3((T + 7) / 8), dim3(256), 0, st, cs, T, hd, phi_min, base, dt_max, t, row_seq,
-               cu);
-  return cudaGetLastError();
-}
-cudaError_t rope_apply_launch(const void* in, void* out, int T, int d, int hd, const float* cs, cudaStream_t st) {
+cudaError_t rope_apply_launch(const void* in, void* out, int T, int d, int hd, const RopeOTF& rp, cudaStream_t st) {
   ProfScope ps(PROF_OTHER, st, 1);
   const size_t pairs = (size_t)T * d / 2;
   if (pairs)
     launch_pdl(rope_apply_kernel, dim3(blocks(pairs, 256)), dim3(256), 0, st, reinterpret_cast<const __nv_bfloat16*>(in),
-                                                         reinterpret_cast<__nv_bfloat16*>(out), T, d, hd, cs);
+                                                         reinterpret_cast<__nv_bfloat16*>(out), T, d, hd, rp);
   return cudaGetLastError();
 }
 cudaError_t rope_gate_bwd_launch2(const void* const* dr, const void* const* Xq, const void* const* Z,
                                   void* const* out_u, void* const* out_r, int nsides, int dr_f32, int r_bf16, int T,
-                                  int d, int hd, const float* cs, cudaStream_t st, float* const* tap_u,
+                                  int d, int hd, const RopeOTF& rp, cudaStream_t st, float* const* tap_u,
                                   float* const* tap_r) {
   if (nsides < 1 || nsides > 2) return cudaErrorInvalidValue;
   RgSides sides;
@@ -427,15 +406,14 @@ cudaError_t rope_gate_bwd_launch2(const void* const* dr, const void* const* Xq, 
   const size_t work = (size_t)T * d / 8;
   if (work)
     launch_pdl((tap_u || tap_r) ? rope_gate_bwd_kernel<true> : rope_gate_bwd_kernel<false>, dim3(blocks(work, 256), nsides),
-               dim3(256), 0, st, sides, dr_f32, r_bf16, T, d,
-               hd, cs);
+               dim3(256), 0, st, sides, dr_f32, r_bf16, T, d, hd, rp);
   return cudaGetLastError();
 }
 cudaError_t rope_gate_bwd_launch(const void* dr, int dr_f32, const void* Xq, const void* Z, void* out_u, void* out_r,
-                                 int r_bf16, int T, int d, int hd, const float* cs, cudaStream_t st) {
-  return rope_gate_bwd_launch2(&dr, &Xq, &Z, &out_u, &out_r, 1, dr_f32, r_bf16, T, d, hd, cs, st);
+                                 int r_bf16, int T, int d, int hd, const RopeOTF& rp, cudaStream_t st) {
+  return rope_gate_bwd_launch2(&dr, &Xq, &Z, &out_u, &out_r, 1, dr_f32, r_bf16, T, d, hd, rp, st);
 }
-cudaError_t gate_rope_fwd_launch(const void* Q, const void* K, const void* Gq, const void* Gk, const float* cs,
+cudaError_t gate_rope_fwd_launch(const void* Q, const void* K, const void* Gq, const void* Gk, const RopeOTF& rp,
                                  void* Qr, void* Kr, int T, int d, int hd, cudaStream_t st, float* tapQ,
                                  float* tapK) {
   ProfScope ps(PROF_OTHER, st, 1);
@@ -444,7 +422,7 @@ cudaError_t gate_rope_fwd_launch(const void* Q, const void* K, const void* Gq, c
   if (work)
     launch_pdl(gate_rope_fwd_kernel, dim3(blocks(work, 256)), dim3(256), 0, st,
                reinterpret_cast<const __nv_bfloat16*>(Q), reinterpret_cast<const __nv_bfloat16*>(K),
-               reinterpret_cast<const __nv_bfloat16*>(Gq), reinterpret_cast<const __nv_bfloat16*>(Gk), cs,
+               reinterpret_cast<const __nv_bfloat16*>(Gq), reinterpret_cast<const __nv_bfloat16*>(Gk), rp,
                reinterpret_cast<__nv_bfloat16*>(Qr), reinterpret_cast<__nv_bfloat16*>(Kr), T, d, hd, tapQ, tapK);
   return cudaGetLastError();
 }

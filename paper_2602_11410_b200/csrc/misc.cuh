@@ -5,21 +5,29 @@
 #include <stdint.h>
 
 namespace cadet {
-// (cos, sin) table [T][hd + 32] floats (see rope_table_kernel); cs = null means no RoPE
-cudaError_t rope_table_launch(float* cs, int T, int hd, double phi_min, double base, double dt_max, const int64_t* t,
-                              const int32_t* row_seq, const int32_t* cu, cudaStream_t st);
-cudaError_t rope_apply_launch(const void* in, void* out, int T, int d, int hd, const float* cs, cudaStream_t st);
+// Timestamp RoPE evaluated on the fly (no (cos, sin) table in HBM): alpha_i = (t_row -
+// t_(sequence start)) theta_i, theta_i = (phi_min / dt_max) base^(2i / hd), fp64 product
+// and mod-2 pi reduction, MUFU sincos.  on = 0: no RoPE (ablation).
+struct RopeOTF {
+  const int64_t* t;
+  const int32_t* row_seq;  // the plan's row -> sequence map (-1 for pad rows)
+  const int32_t* cu;
+  double th0;              // phi_min / dt_max
+  double base;
+  int32_t on;
+};
+cudaError_t rope_apply_launch(const void* in, void* out, int T, int d, int hd, const RopeOTF& rp, cudaStream_t st);
 // A4 elementwise half: Qr = RoPE(Q * sigma(Z_q)), Kr = RoPE(K * sigma(Z_k)) (Z stored by the gate GEMMs)
-cudaError_t gate_rope_fwd_launch(const void* Q, const void* K, const void* Gq, const void* Gk, const float* cs,
+cudaError_t gate_rope_fwd_launch(const void* Q, const void* K, const void* Gq, const void* Gk, const RopeOTF& rp,
                                  void* Qr, void* Kr, int T, int d, int hd, cudaStream_t st, float* tapQ = nullptr,
                                  float* tapK = nullptr);
 // both sides (Q and K) in one launch: arrays of nsides (<= 2) pointers
 cudaError_t rope_gate_bwd_launch2(const void* const* dr, const void* const* Xq, const void* const* Z,
                                   void* const* out_u, void* const* out_r, int nsides, int dr_f32, int r_bf16, int T,
-                                  int d, int hd, const float* cs, cudaStream_t st, float* const* tap_u = nullptr,
+                                  int d, int hd, const RopeOTF& rp, cudaStream_t st, float* const* tap_u = nullptr,
                                   float* const* tap_r = nullptr);
 cudaError_t rope_gate_bwd_launch(const void* dr, int dr_f32, const void* Xq, const void* Z, void* out_u, void* out_r,
-                                 int r_bf16, int T, int d, int hd, const float* cs, cudaStream_t st);
+                                 int r_bf16, int T, int d, int hd, const RopeOTF& rp, cudaStream_t st);
 // to_f16: the gathered rows are written as fp16 (the towers' GEMM operand)
 cudaError_t gather_rows_launch(const void* H, const int32_t* rows, int n, int T, int d, void* out, uint32_t* err,
                                cudaStream_t st, int to_f16 = 0);
