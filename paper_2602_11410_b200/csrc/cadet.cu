@@ -80,6 +80,10 @@ PlanArgs plan_args(const cadet_attn_config* c, const cadet_batch* b) {
   a.ncand = b->n_candidates;
   a.nstatic = b->n_static;
   a.flags = b->token_flags;
+  a.rope_phi_min = c->rope_phi_min;
+  a.rope_dt_max = (double)c->rope_delta_t_max_ms;
+  a.rope_base = c->rope_base;
+  a.head_dim = c->head_dim;
   return a;
 }
 void set_error(const char* msg) { g_err = msg; }

@@ -253,8 +253,7 @@ RopeOTF rope_of(const cadet_attn_config* cfg, const cadet_batch* b, const PlanVi
   r.t = b->timestamps_ms;
   r.row_seq = v.row_seq;
   r.cu = b->cu_seqlens;
-  r.th0 = cfg->rope_phi_min / (double)cfg->rope_delta_t_max_ms;
-  r.base = cfg->rope_base;
+  r.theta = v.theta;
   r.on = cfg->use_rope;
   return r;
 }

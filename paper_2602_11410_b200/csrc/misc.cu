@@ -10,6 +10,7 @@
 #include "misc.cuh"
 #include <algorithm>
 #include <cuda_fp16.h>
+#include <string.h>
 #include "launch.cuh"
 #include "prof.cuh"
 #include "ptx.cuh"
@@ -26,27 +27,33 @@ __device__ __forceinline__ void rope_cs(double dt, double th, float& c, float& s
   __sincosf(r, &s, &c);
 }
 
-// theta_i of the block's head dim into shared memory (identical formula on every path)
-__device__ __forceinline__ void rope_theta_smem(double* th, const RopeOTF& rp, int hd) {
-  if (rp.on)
-    for (int i = threadIdx.x; i < hd / 2; i += blockDim.x) th[i] = rp.th0 * pow(rp.base, 2.0 * i / (double)hd);
-  __syncthreads();
+// alpha = dt theta in compensated fp32: dt = dth + dtl (exact), theta = thh + thl; p + lo = dt theta to
+// ~2^-40 relative; reduction by 2 pi = 6.2831855f - 1.7484556e-7f (two FMAs), then MUFU sincos
+__device__ __forceinline__ void rope_cs_f(float dth, float dtl, float thh, float thl, float& c, float& s) {
+  const float p = dth * thh;
+  const float lo = fmaf(dth, thl, fmaf(dtl, thh, fmaf(dth, thh, -p)));
+  const float k = rintf(p * 0.15915494f);
+  float r = fmaf(-k, 6.28318548202514648f, p);
+  r = fmaf(-k, -1.7484556e-7f, r) + lo;
+  __sincosf(r, &s, &c);
 }
-// (cos, sin) of pairs i0 .. i0 + N - 1 of `row` (rebased time of the row's sequence)
+// (cos, sin) of pairs i0 .. i0 + N - 1 of `row` (time rebased to the row's sequence start)
 template <int N>
-__device__ __forceinline__ void rope_row_cs(const RopeOTF& rp, const double* th, int row, int i0, float (&c)[N],
-                                            float (&s)[N]) {
+__device__ __forceinline__ void rope_row_cs(const RopeOTF& rp, int row, int i0, float (&c)[N], float (&s)[N]) {
   const int sq = rp.row_seq[row];
-  const double dt = sq >= 0 ? (double)(rp.t[row] - rp.t[rp.cu[sq]]) : 0.0;
+  const long long dt = sq >= 0 ? (long long)(rp.t[row] - rp.t[rp.cu[sq]]) : 0;
+  const float dth = (float)dt;
+  const float dtl = (float)(dt - (long long)dth);
 #pragma unroll
-  for (int e = 0; e < N; ++e) rope_cs(dt, th[i0 + e], c[e], s[e]);
+  for (int e = 0; e < N; ++e) {
+    const float2 th = rp.theta[i0 + e];
+    rope_cs_f(dth, dtl, th.x, th.y, c[e], s[e]);
+  }
 }
 
 // one thread per (row, pair of columns)
 __global__ void rope_apply_kernel(const __nv_bfloat16* in, __nv_bfloat16* out, int T, int d, int hd, RopeOTF rp) {
   pdl_trigger();
-  __shared__ double th[64];
-  rope_theta_smem(th, rp, hd);
   pdl_wait();
   const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   const size_t pairs = (size_t)T * d / 2;
@@ -55,7 +62,7 @@ __global__ void rope_apply_kernel(const __nv_bfloat16* in, __nv_bfloat16* out, i
   const int c = (int)(idx % (d / 2)) * 2;
   const float2 v = __bfloat1622float2(reinterpret_cast<const __nv_bfloat162*>(in)[idx]);
   float cv[1] = {1.f}, sv[1] = {0.f};
-  if (rp.on) rope_row_cs<1>(rp, th, row, (c % hd) / 2, cv, sv);
+  if (rp.on) rope_row_cs<1>(rp, row, (c % hd) / 2, cv, sv);
   reinterpret_cast<__nv_bfloat162*>(out)[idx] =
       __floats2bfloat162_rn(v.x * cv[0] - v.y * sv[0], v.x * sv[0] + v.y * cv[0]);
 }
@@ -68,8 +75,6 @@ __global__ void __launch_bounds__(256) gate_rope_fwd_kernel(const __nv_bfloat16*
                                                             RopeOTF rp, __nv_bfloat16* Qr, __nv_bfloat16* Kr,
                                                             int T, int d, int hd, float* tapQ, float* tapK) {
   pdl_trigger();
-  __shared__ double th[64];
-  rope_theta_smem(th, rp, hd);
   pdl_wait();
   const int per_row = d / 8;
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;
@@ -77,7 +82,7 @@ __global__ void __launch_bounds__(256) gate_rope_fwd_kernel(const __nv_bfloat16*
   const int row = idx / per_row, c0 = (idx - row * per_row) * 8;
   const size_t off = (size_t)row * d + c0;
   float cv[4] = {1.f, 1.f, 1.f, 1.f}, sv[4] = {0.f, 0.f, 0.f, 0.f};
-  if (rp.on) rope_row_cs<4>(rp, th, row, (c0 % hd) / 2, cv, sv);  // the 8-column group never crosses a head edge
+  if (rp.on) rope_row_cs<4>(rp, row, (c0 % hd) / 2, cv, sv);  // the 8-column group never crosses a head edge
   const __nv_bfloat16* src[2] = {Q, K};
   const __nv_bfloat16* gate[2] = {Gq, Gk};
   __nv_bfloat16* dst[2] = {Qr, Kr};
@@ -128,8 +133,6 @@ template <bool TAPS>
 __global__ void __launch_bounds__(256) rope_gate_bwd_kernel(RgSides sides, int dr_f32, int r_bf16, int T, int d,
                                                             int hd, RopeOTF rp) {
   pdl_trigger();
-  __shared__ double th[64];
-  rope_theta_smem(th, rp, hd);
   pdl_wait();
   const RgSide& sd = sides.s[blockIdx.y];
   const void* dr = sd.dr;
@@ -160,7 +163,7 @@ __global__ void __launch_bounds__(256) rope_gate_bwd_kernel(RgSides sides, int d
   }
   if (rp.on) {  // R(-alpha): the 8-column group never crosses a head edge (hd % 8 == 0)
     float cv[4], sv[4];
-    rope_row_cs<4>(rp, th, row, (c0 % hd) / 2, cv, sv);
+    rope_row_cs<4>(rp, row, (c0 % hd) / 2, cv, sv);
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       const float x0 = g[2 * e], x1 = g[2 * e + 1];
@@ -405,7 +408,8 @@ cudaError_t rope_gate_bwd_launch2(const void* const* dr, const void* const* Xq, 
   ProfScope ps(PROF_OTHER, st, 1);
   const size_t work = (size_t)T * d / 8;
   if (work)
-    launch_pdl((tap_u || tap_r) ? rope_gate_bwd_kernel<true> : rope_gate_bwd_kernel<false>, dim3(blocks(work, 256), nsides),
+    launch_pdl(((tap_u && (tap_u[0] || tap_u[nsides - 1])) || (tap_r && (tap_r[0] || tap_r[nsides - 1])))
+                   ? rope_gate_bwd_kernel<true> : rope_gate_bwd_kernel<false>, dim3(blocks(work, 256), nsides),
                dim3(256), 0, st, sides, dr_f32, r_bf16, T, d, hd, rp);
   return cudaGetLastError();
 }

@@ -6,14 +6,16 @@
 
 namespace cadet {
 // Timestamp RoPE evaluated on the fly (no (cos, sin) table in HBM): alpha_i = (t_row -
-// t_(sequence start)) theta_i, theta_i = (phi_min / dt_max) base^(2i / hd), fp64 product
-// and mod-2 pi reduction, MUFU sincos.  on = 0: no RoPE (ablation).
+// t_(sequence start)) theta_i, theta_i = (phi_min / dt_max) base^(2i / hd).  theta_i is
+// evaluated once per plan in fp64 and kept as a float pair (hi + lo, PlanView::theta); the product with
+// the int64 rebased time (also split hi + lo) and the mod-2 pi reduction run in compensated fp32 (an FMA
+// two-product and a two-constant 2 pi), ~3e-7 rad absolute for |alpha| <= 1e4 rad, then MUFU sincos.
+// on = 0: no RoPE (ablation).
 struct RopeOTF {
   const int64_t* t;
   const int32_t* row_seq;  // the plan's row -> sequence map (-1 for pad rows)
   const int32_t* cu;
-  double th0;              // phi_min / dt_max
-  double base;
+  const float2* theta;     // [hd / 2] (hi, lo)
   int32_t on;
 };
 cudaError_t rope_apply_launch(const void* in, void* out, int T, int d, int hd, const RopeOTF& rp, cudaStream_t st);

@@ -38,6 +38,7 @@ size_t plan_bytes(int32_t n, int32_t T, int32_t max_seqlen) {
   b += align256(nq * 4) * 2;
   b += align256(list_cap_of(nq, hm) * 4);
   b += align256((size_t)(n + 1) * 4);       // seq_rank
+  b += align256(64 * sizeof(float2));       // RoPE theta (hi, lo)
   return b;
 }
 
@@ -69,6 +70,7 @@ PlanView plan_carve(void* ws, int32_t n, int32_t T, int32_t max_seqlen) {
   v.bwd_cnt = reinterpret_cast<int32_t*>(take((size_t)v.nq_cap * 4));
   v.bwd_list = reinterpret_cast<int32_t*>(take(list_cap_of(v.nq_cap, v.hmax) * 4));
   v.seq_rank = reinterpret_cast<int32_t*>(take((size_t)(n + 1) * 4));
+  v.theta = reinterpret_cast<float2*>(take(64 * sizeof(float2)));
   return v;
 }
 
@@ -106,6 +108,15 @@ __global__ void __launch_bounds__(1024) plan_seq_kernel(PlanArgs a, PlanView v) 
   const int per = (a.n + nt - 1) / nt;
   const int s0 = min(tid * per, a.n), s1 = min(s0 + per, a.n);
   uint32_t err = 0;
+  if (tid < 64) {  // RoPE theta_i in fp64, stored as a float hi + lo pair (exact to ~2^-48 relative)
+    float2 th = make_float2(0.f, 0.f);
+    if (tid < a.head_dim / 2 && a.rope_dt_max > 0.0) {
+      const double x = (a.rope_phi_min / a.rope_dt_max) * pow(a.rope_base, 2.0 * tid / (double)a.head_dim);
+      th.x = (float)x;
+      th.y = (float)(x - (double)th.x);
+    }
+    v.theta[tid] = th;
+  }
   if (tid == 0) {
     if (a.n > 0 && a.cu[0] != 0) err |= ERRBIT_OFFSETS;
     if (a.n > 0 && a.cu[a.n] > a.T) err |= ERRBIT_OFFSETS;

@@ -37,6 +37,7 @@ struct PlanView {   // device pointers into the workspace
   int32_t* bwd_cnt;   // [nq_cap] its length
   int32_t* bwd_list;  // [list_cap] q-tiles visiting k-tile g: qt | FULL << 30 (all cells visible)
   int32_t* seq_rank;  // [n] rank of a sequence among those with the same tile count (bwd order)
+  float2* theta;      // [64] RoPE theta_i as (hi, lo) floats, i < head_dim / 2
   int32_t nq_cap, hmax, list_cap;
 };
 
@@ -49,6 +50,10 @@ struct PlanArgs {
   const int32_t* ncand;
   const int32_t* nstatic;
   const uint8_t* flags;
+  // timestamp RoPE frequencies theta_i = (phi_min / dt_max) base^(2i / hd), written by the
+  // plan as float hi + lo pairs for the kernels that rotate (angles evaluated on the fly)
+  double rope_phi_min, rope_dt_max, rope_base;
+  int32_t head_dim;
 };
 
 size_t plan_bytes(int32_t n, int32_t T, int32_t max_seqlen);
