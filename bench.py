@@ -143,7 +143,7 @@ class ClockSampler:
 SHARDS = 8  # the largest scaling run: every N <= 8 takes its ranks' shards from the same 8-way partition
 
 
-def build_inputs(wl: dict, seed: int, pin: bool, rank: int = 0, world: int = 1, J: int = 0):
+def build_inputs(wl: dict, seed: int, pin: bool, rank: int = 0, world: int = 1, J: int = 0, vocab=None):
     """One rank's batch: one global user stream of max(8, world) x budget tokens is
     partitioned by LPT (whole users, balanced on estimated cost, each shard under the budget) and
     rank r takes shard r.  Every N <= 8 therefore runs shards of equal estimated cost, so the weak
@@ -160,7 +160,7 @@ def build_inputs(wl: dict, seed: int, pin: bool, rank: int = 0, world: int = 1, 
         except ValueError:
             allu = allu[:-1]
     users = [allu[i] for i in parts[rank]]
-    return users, make_inputs(users, wl["d_model"], wl["L_chunk"], seed + 1000 * rank, pin=pin, J=J)
+    return users, make_inputs(users, wl["d_model"], wl["L_chunk"], seed + 1000 * rank, pin=pin, J=J, vocab=vocab)
 
 
 def step_flops(wl: dict, tokens: int, pairs: int, n_imp: int, dh: int, K: int = 2):
@@ -289,6 +289,9 @@ def main():
                     help="NEXT-2: train on Eq. 11 (towers + auxiliary heads + cross-rank RankNet) instead of Eq. 9")
     ap.add_argument("--block", action="store_true",
                     help="NEXT-3: every layer is the pre-norm CADET block (RMSNorm, gated attention, RMSNorm, FFN x4)")
+    ap.add_argument("--embed", action="store_true",
+                    help="NEXT-3: the step starts from token field ids (summed id + type embeddings, Eq. 1) and ends "
+                         "with the embedding gradients (implied by --block: the paper's whole training step)")
     ap.add_argument("--optimizer", default="none", choices=["none", "adamw"],
                     help="NEXT-4: append the AdamW step (R35) to every training step")
     ap.add_argument("--no-shard", action="store_true",
@@ -299,6 +302,7 @@ def main():
     ap.add_argument("--graph", action="store_true",
                     help="replay the step as one CUDA graph (measured: no gain over eager launches on C4)")
     args = ap.parse_args()
+    args.embed = args.embed or args.block
     wl = dict(WORKLOADS[args.workload], block=args.block)
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -310,6 +314,8 @@ def main():
                            "T=65536/rank"}[args.workload]
     if args.block:
         workload_name += "; every layer the pre-norm CADET block (RMSNorm, attention, RMSNorm, FFN x4; NEXT-3)"
+    if args.embed:
+        workload_name += "; inputs are token field ids: summed id + type embeddings (Eq. 1; vocab 2/16384/8/4)"
 
     if args.impl == "reference":
         # The reference arm is the CPU oracle (no reference implementation exists): rank 0 only.
@@ -348,12 +354,14 @@ def main():
         dist.barrier()  # local rank 0 finished any rebuild before the others load the library
     dev = torch.device("cuda", local)
 
-    users, host_inp = build_inputs(wl, 0, pin=True, rank=rank, world=world, J=2 if args.full_loss else 0)
+    from paper_2602_11410_b200.model import StackConfig as _SC
+    vocab = _SC().vocab if args.embed else None
+    users, host_inp = build_inputs(wl, 0, pin=True, rank=rank, world=world, J=2 if args.full_loss else 0, vocab=vocab)
     inp = host_inp.to(dev)
     torch.cuda.synchronize()
     scfg = StackConfig(d_model=wl["d_model"], n_heads=wl["n_heads"], n_layers=wl["n_layers"], budget=wl["budget"],
                        L_chunk=wl["L_chunk"], full_loss=args.full_loss, recompute=args.recompute, block=args.block,
-                       optimizer=args.optimizer, shard=not args.no_shard)
+                       optimizer=args.optimizer, shard=not args.no_shard, embed=args.embed)
     stack = CadetStack(scfg, seed=0, device=dev)
     pairs = stack.pairs(inp)
     n_imp = inp.rows.numel()
@@ -489,7 +497,8 @@ def main():
     if args.seeds > 1:
         per = [(0, ms_max, inp.tokens, total_flops)]
         for sd in range(1, args.seeds):
-            _, h_s = build_inputs(wl, sd, pin=False, rank=rank, world=world, J=2 if args.full_loss else 0)
+            _, h_s = build_inputs(wl, sd, pin=False, rank=rank, world=world, J=2 if args.full_loss else 0,
+                                  vocab=vocab)
             inp_s = h_s.to(dev)
             fl_s = sum(step_flops(wl, inp_s.tokens, stack.pairs(inp_s), inp_s.rows.numel(), scfg.dh).values())
             for _ in range(args.warmup):

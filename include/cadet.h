@@ -336,6 +336,30 @@ cadet_status cadet_ffn_backward(const void* X, const void* W1, const void* W2, c
                                 const void* dY, const void* dresid, int32_t T, int32_t d, int32_t m, void* dX,
                                 float* dW1, float* dW2, void* ws, size_t ws_bytes, cadet_stream_t stream);
 
+/* ------------------------------------------------------------------ NEXT-3: input embeddings (Eq. 1)
+ * x = [M; I_1, (C_1, A_1); ...; I_L] (Eq. 1): each token's input row is the sum of its id embeddings and its
+ * token-type embedding (reading R37): F tables E_f bf16 [vocab[f], d], token t uses row
+ * ids[t * F + f] of table f (an id < 0 = the field is absent for this token kind, e.g. no ad id on an
+ * action token).  X[t] = sum_f E_f[ids[t, f]] (fp32 sum, bf16 out) for t < *n_valid (device scalar; NULL
+ * = all T rows), rows [*n_valid, T) are 0 (pad rows).  An id >= vocab[f] latches CADET_E_BUCKET and is
+ * skipped.  Backward: dE_f[v] = sum_{t : ids[t, f] = v} dX[t], fp32 [vocab[f], d], OVERWRITTEN,
+ * deterministic (no order-dependent float atomics: tables with vocab <= 16 reduce per-CTA register
+ * partials in a fixed order, larger ones add 64-bit fixed-point values, 2^-24 resolution).
+ * d % 8 == 0, 1 <= n_tables <= 8; ws >= cadet_embed_workspace_bytes (the first 256 B: error word). */
+#define CADET_EMBED_MAX_TABLES 8
+typedef struct {
+  int32_t n_tables;
+  int32_t d_model;
+  int32_t vocab[CADET_EMBED_MAX_TABLES];
+} cadet_embed_config;
+size_t cadet_embed_workspace_bytes(const cadet_embed_config* c_h);
+cadet_status cadet_embed_forward(const cadet_embed_config* c_h, const void* const* tables_h, const int32_t* ids,
+                                 int32_t T, const int32_t* n_valid, void* X, void* ws, size_t ws_bytes,
+                                 cadet_stream_t stream);
+cadet_status cadet_embed_backward(const cadet_embed_config* c_h, const int32_t* ids, int32_t T,
+                                  const int32_t* n_valid, const void* dX, float* const* dtables_h, void* ws,
+                                  size_t ws_bytes, cadet_stream_t stream);
+
 /* ------------------------------------------------------------------ NEXT-4: HSDP optimizer step
  * HSDP shards parameters, gradients and optimizer state within a node: each rank
  * reduce-scatters the flat fp32 gradient buffer (NCCL, the caller), updates ITS shard with

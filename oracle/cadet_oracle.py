@@ -475,6 +475,32 @@ def heads_loss_backward(H, rows, W1, b1, w2, b2, bucket, label, relu_active=None
     return heads_loss(z, bucket, label), z, dH, dict(dW1=dW1, db1=db1, dw2=dw2, db2=db2)
 
 
+# ------------------------------------------------------------------ NEXT-3: input embeddings (Eq. 1)
+def embed_forward(ids, tables):
+    """x_t = sum_f E_f[id_{t,f}] over the fields present for the token (id >= 0): the input sequence
+    x = [M; I_1, (C_1, A_1); ...] of Eq. 1 (P:193) as summed id + token-type embeddings (S:602, S:648;
+    reading R37)."""
+    ids = np.asarray(ids, dtype=np.int64)
+    X = np.zeros((ids.shape[0], tables[0].shape[1]))
+    for f, E in enumerate(tables):
+        m = ids[:, f] >= 0
+        X[m] += np.asarray(E, dtype=np.float64)[ids[m, f]]
+    return X
+
+
+def embed_backward(ids, dX, vocab):
+    """Adjoint of embed_forward: dE_f[v] = sum of dX over the tokens whose field f has id v."""
+    ids = np.asarray(ids, dtype=np.int64)
+    dX = np.asarray(dX, dtype=np.float64)
+    out = []
+    for f, V in enumerate(vocab):
+        g = np.zeros((V, dX.shape[1]))
+        m = ids[:, f] >= 0
+        np.add.at(g, ids[m, f], dX[m])
+        out.append(g)
+    return out
+
+
 # ------------------------------------------------------------------ NEXT-2: full loss (Eqs. 10-12, P:412-435)
 AUX_KINDS = ("bce", "se")  # R30: S:492 desk-scale tasks: long-dwell indicator (CE), impression duration (SE)
 

@@ -62,6 +62,10 @@ class LossConfig(C.Structure):
                 ("lambda_aux", C.c_float * 8)]
 
 
+class EmbedConfig(C.Structure):
+    _fields_ = [("n_tables", C.c_int32), ("d_model", C.c_int32), ("vocab", C.c_int32 * 8)]
+
+
 class AdamWConfig(C.Structure):
     _fields_ = [("lr", C.c_float), ("beta1", C.c_float), ("beta2", C.c_float), ("eps", C.c_float),
                 ("weight_decay", C.c_float)]
@@ -123,6 +127,9 @@ SIGNATURES = {
     "cadet_ffn_workspace_bytes": (SZ, [I32, I32, I32]),
     "cadet_ffn_forward": (I32, [P, P, P, P, I32, I32, I32, P, P, P, P]),
     "cadet_ffn_backward": (I32, [P, P, P, P, P, P, P, I32, I32, I32, P, P, P, P, SZ, P]),
+    "cadet_embed_workspace_bytes": (SZ, [C.POINTER(EmbedConfig)]),
+    "cadet_embed_forward": (I32, [C.POINTER(EmbedConfig), C.POINTER(C.c_void_p), P, I32, P, P, P, SZ, P]),
+    "cadet_embed_backward": (I32, [C.POINTER(EmbedConfig), P, I32, P, P, C.POINTER(C.c_void_p), P, SZ, P]),
     "cadet_default_adamw_config": (None, [C.POINTER(AdamWConfig)]),
     "cadet_adamw_step": (I32, [C.POINTER(AdamWConfig), C.c_int64, P, P, P, P, P, C.c_int64, P]),
     "cadet_bf16_to_f32": (I32, [P, P, C.c_int64, P]),

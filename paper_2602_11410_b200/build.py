@@ -6,7 +6,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libcadet.so")
-SOURCES = ["cadet.cu", "cadet_layer.cu", "plan.cu", "gemm.cu", "attn_fwd.cu", "attn_bwd.cu", "misc.cu", "prof.cu", "loss.cu", "block.cu", "optim.cu", "fp32.cu"]
+SOURCES = ["cadet.cu", "cadet_layer.cu", "plan.cu", "gemm.cu", "attn_fwd.cu", "attn_bwd.cu", "misc.cu", "prof.cu", "loss.cu", "block.cu", "optim.cu", "fp32.cu", "embed.cu"]
 OPTIONAL = []
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-std=c++17", "-lineinfo",
          "-Xcompiler", "-fPIC", "-diag-suppress", "550,177"]

@@ -178,7 +178,7 @@ cadet_status cadet_poll(void* ws, cadet_stream_t stream) {
   if (word & ERRBIT_ORDER) return fail(CADET_E_ORDER, "timestamps/session ids decrease inside a sequence (device)");
   if (word & ERRBIT_TOO_LONG) return fail(CADET_E_TOO_LONG, "sequence longer than max_seqlen / budget (device)");
   if (word & ERRBIT_CAND) return fail(CADET_E_CAND, "n_candidates out of range (device)");
-  if (word & ERRBIT_BUCKET) return fail(CADET_E_BUCKET, "bucket outside [0, K) (device)");
+  if (word & ERRBIT_BUCKET) return fail(CADET_E_BUCKET, "bucket / position / embedding id out of range (device)");
   if (word & ERRBIT_NONFINITE) return fail(CADET_E_NONFINITE, "non-finite loss (device)");
   if (word & ERRBIT_CAPACITY) return fail(CADET_E_WORKSPACE, "output capacity too small (device)");
   return CADET_OK;
@@ -244,6 +244,38 @@ cadet_status cadet_bucketize(const int32_t* raw_position, int32_t n, const int32
   return cuda_check(bucketize_launch(raw_position, n, bd, bucket, reinterpret_cast<uint32_t*>(ws),
                                      reinterpret_cast<cudaStream_t>(stream)),
                     "bucketize");
+}
+
+static cadet_status check_embed(const cadet_embed_config* c) {
+  if (!c || c->n_tables < 1 || c->n_tables > CADET_EMBED_MAX_TABLES || c->d_model <= 0 || c->d_model % 8)
+    return fail(CADET_E_ARG, "embed: 1 <= n_tables <= 8, d_model % 8 == 0");
+  for (int f = 0; f < c->n_tables; ++f)
+    if (c->vocab[f] < 1) return fail(CADET_E_ARG, "embed: vocab[%d] < 1", f);
+  return CADET_OK;
+}
+size_t cadet_embed_workspace_bytes(const cadet_embed_config* c) { return check_embed(c) ? 0 : embed_ws_bytes(c); }
+cadet_status cadet_embed_forward(const cadet_embed_config* c, const void* const* tables, const int32_t* ids, int32_t T,
+                                 const int32_t* n_valid, void* X, void* ws, size_t ws_bytes, cadet_stream_t stream) {
+  cadet_status s = check_embed(c);
+  if (s) return s;
+  if (T < 0 || !tables || (T > 0 && (!ids || !X)) || !ws) return fail(CADET_E_ARG, "embed_forward: null pointer");
+  for (int f = 0; f < c->n_tables; ++f)
+    if (!tables[f]) return fail(CADET_E_ARG, "embed_forward: null table %d", f);
+  if (ws_bytes < embed_ws_bytes(c)) return fail(CADET_E_WORKSPACE, "embed workspace too small");
+  return cuda_check(embed_forward_launch(c, tables, ids, T, n_valid, X, ws, reinterpret_cast<cudaStream_t>(stream)),
+                    "embed forward");
+}
+cadet_status cadet_embed_backward(const cadet_embed_config* c, const int32_t* ids, int32_t T, const int32_t* n_valid,
+                                  const void* dX, float* const* dtables, void* ws, size_t ws_bytes,
+                                  cadet_stream_t stream) {
+  cadet_status s = check_embed(c);
+  if (s) return s;
+  if (T < 0 || !dtables || (T > 0 && (!ids || !dX)) || !ws) return fail(CADET_E_ARG, "embed_backward: null pointer");
+  for (int f = 0; f < c->n_tables; ++f)
+    if (!dtables[f]) return fail(CADET_E_ARG, "embed_backward: null gradient %d", f);
+  if (ws_bytes < embed_ws_bytes(c)) return fail(CADET_E_WORKSPACE, "embed workspace too small");
+  return cuda_check(embed_backward_launch(c, ids, T, n_valid, dX, dtables, ws, reinterpret_cast<cudaStream_t>(stream)),
+                    "embed backward");
 }
 
 size_t cadet_gemm_fp32_workspace_bytes(int32_t M, int32_t N, int32_t K) {

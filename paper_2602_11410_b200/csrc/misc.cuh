@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 #include <stddef.h>
 #include <stdint.h>
+#include "../../include/cadet.h"
 
 namespace cadet {
 // Timestamp RoPE evaluated on the fly (no (cos, sin) table in HBM): alpha_i = (t_row -
@@ -50,6 +51,12 @@ struct ZeroSpan {
   size_t bytes;
 };
 cudaError_t zero_many_launch(const ZeroSpan* spans, int n, cudaStream_t st);
+// NEXT-3 embeddings (embed.cu)
+size_t embed_ws_bytes(const cadet_embed_config* c);
+cudaError_t embed_forward_launch(const cadet_embed_config* c, const void* const* tables, const int32_t* ids, int T,
+                                 const int32_t* n_valid, void* X, void* ws, cudaStream_t st);
+cudaError_t embed_backward_launch(const cadet_embed_config* c, const int32_t* ids, int T, const int32_t* n_valid,
+                                  const void* dX, float* const* dtables, void* ws, cudaStream_t st);
 struct Bounds {  // context-bucket boundaries (cadet_bucketize), strictly increasing
   int32_t b[32];
   int32_t nb;

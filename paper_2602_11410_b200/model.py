@@ -51,6 +51,8 @@ class StackConfig:
                                  # this rank's shard of master params + moments, all-gather bf16 params)
     lr: float = 1e-4
     weight_decay: float = 0.0
+    embed: bool = False          # NEXT-3 input embeddings (Eq. 1): H[0] = sum of id + type embedding rows
+    vocab: tuple = (2, 16384, 8, 4)  # token type, ad id, request feature, action id (synth.generator.EMBED_VOCAB)
     taps: bool = False           # parity taps (cfg.out_f32 = 1 on the layer calls): fp32 stage values in the
                                  # workspace, read with cadet_attn_stage_views (tests only; ~2x the layer time)
 
@@ -79,13 +81,15 @@ class StepInputs:
     n_chunks: int
     tokens: int              # real tokens T_r
     aux_label: torch.Tensor | None = None  # [n_imp, J] fp32 (NEXT-2 full loss)
+    ids: torch.Tensor | None = None        # [R, F] int32 embedded field ids (NEXT-3 embeddings; X_hist is None)
 
     def to(self, device, non_blocking=True) -> "StepInputs":
         f = lambda t: t.to(device, non_blocking=non_blocking) if t is not None else None
         return StepInputs(f(self.X_hist), f(self.t_hist), f(self.s_hist), f(self.lens), f(self.rows),
-                          f(self.position), f(self.label), self.n_hist, self.n_chunks, self.tokens, f(self.aux_label))
+                          f(self.position), f(self.label), self.n_hist, self.n_chunks, self.tokens, f(self.aux_label),
+                          f(self.ids))
 
-    FIELDS = ("X_hist", "t_hist", "s_hist", "lens", "rows", "position", "label", "aux_label")
+    FIELDS = ("X_hist", "t_hist", "s_hist", "lens", "rows", "position", "label", "aux_label", "ids")
 
     def copy_(self, src: "StepInputs"):
         for a in self.FIELDS:
@@ -97,12 +101,13 @@ class StepInputs:
                    if getattr(self, a) is not None)
 
 
-def make_inputs(users, d: int, L_chunk: int, seed: int, pin: bool = False, J: int = 0) -> StepInputs:
-    """Host-side data loader output for one batch of generator users (synth/ Appendix B)."""
+def make_inputs(users, d: int, L_chunk: int, seed: int, pin: bool = False, J: int = 0, vocab=None) -> StepInputs:
+    """Host-side data loader output for one batch of generator users (synth/ Appendix B).  With `vocab`
+    (NEXT-3 embeddings) the tokens carry their field ids instead of dense feature rows."""
     from synth import generator as G
     lens = np.array([u.length for u in users], dtype=np.int32)
     R = int(lens.sum())
-    X = G.normal_bf16(seed, 11, (R, d))
+    X = G.normal_bf16(seed, 11, (R, d)) if vocab is None else None
     t = np.concatenate([u.timestamps for u in users]).astype(np.int64)
     s = np.concatenate([u.session_ids for u in users]).astype(np.int32)
     starts = np.concatenate([[0], np.cumsum(lens)[:-1]])
@@ -111,14 +116,16 @@ def make_inputs(users, d: int, L_chunk: int, seed: int, pin: bool = False, J: in
     label = np.concatenate([u.labels[u.impression_rows] for u in users]).astype(np.float32)
     n_chunks = int(sum(-(-int(m) // L_chunk) for m in lens))
     mk = lambda a, dt: (torch.from_numpy(np.ascontiguousarray(a)).to(dt))
-    Xt = torch.from_numpy(X).to(torch.bfloat16)
+    Xt = torch.from_numpy(X).to(torch.bfloat16) if X is not None else None
     aux = mk(G.aux_labels(seed, len(rows))[:, :J], torch.float32) if J > 0 else None
+    ids = mk(G.token_ids(seed, users, vocab), torch.int32) if vocab is not None else None
     inp = StepInputs(Xt, mk(t, torch.int64), mk(s, torch.int32), mk(lens, torch.int32), mk(rows, torch.int32),
-                     mk(position, torch.int32), mk(label, torch.float32), len(users), n_chunks, R, aux)
+                     mk(position, torch.int32), mk(label, torch.float32), len(users), n_chunks, R, aux, ids)
     if pin:
         pinned = [x.pin_memory() if x is not None else None for x in (inp.X_hist, inp.t_hist, inp.s_hist, inp.lens,
-                                                                       inp.rows, inp.position, inp.label, inp.aux_label)]
-        inp = StepInputs(*pinned[:7], inp.n_hist, inp.n_chunks, inp.tokens, pinned[7])
+                                                                       inp.rows, inp.position, inp.label, inp.aux_label,
+                                                                       inp.ids)]
+        inp = StepInputs(*pinned[:7], inp.n_hist, inp.n_chunks, inp.tokens, pinned[7], pinned[8])
     return inp
 
 
@@ -260,6 +267,10 @@ class CadetStack:
         npl = len(per_layer)
         sizes = per_layer * nl + [d * N, N, N, cfg.K] + ([d * Na, Na, Na, cfg.J] if cfg.full_loss else [])
         kinds = kind_layer * nl + ["m", "v", "v", "v"] + (["m", "v", "v", "v"] if cfg.full_loss else [])
+        n_before_embed = len(sizes)
+        if cfg.embed:  # NEXT-3 embedding tables (bf16 compute copies, fp32 gradients) after everything else
+            sizes += [V * d for V in cfg.vocab]
+            kinds += ["m"] * len(cfg.vocab)
         self.n_grad = -(-sum(pad(x) for x in sizes) // 512) * 512
         self.grads = torch.zeros(self.n_grad, dtype=torch.float32, device=self.dev)
         # parameters: bf16 compute copies (matrices are consumed as bf16) and fp32 compute copies (vectors:
@@ -299,6 +310,13 @@ class CadetStack:
                              g1=rng_(npl * l + 10, npl * l + 11) if cfg.block else None) for l in range(nl)]
         self.gW1, self.gb1, self.gw2, self.gb2 = views[t0:t0 + 4]
         self._tower_off = offs[t0]  # towers (and aux heads) follow the layers
+        self._embed_off = offs[n_before_embed] if cfg.embed else self.n_grad  # then the embedding tables
+        if cfg.embed:
+            et = G.embed_tables(seed, d, cfg.vocab)
+            self.E = [put(n_before_embed + f, et[f], (V, d)) for f, V in enumerate(cfg.vocab)]
+            self.dE = [views[n_before_embed + f].view(V, d) for f, V in enumerate(cfg.vocab)]
+            self.ecfg = L.EmbedConfig(len(cfg.vocab), d, (C.c_int32 * 8)(*cfg.vocab))
+            self._ews = ops.workspace(L.lib().cadet_embed_workspace_bytes(C.byref(self.ecfg)), self.dev)
         if cfg.full_loss:  # NEXT-2 auxiliary heads (Eq. 10): J towers of width da, never routed
             aw = G.head_weights(seed + 1, cfg.J, d, cfg.da)
             self.aW1 = put(t0 + 4, np.concatenate([aw.W1[k] for k in range(cfg.J)], axis=1), (d, Na))
@@ -394,17 +412,24 @@ class CadetStack:
             self._pack_stream = torch.cuda.Stream(self.dev)
             self._pack_done = torch.cuda.Event()
         self._pack_stream.wait_stream(cur)
-        with torch.cuda.stream(self._pack_stream):
-            chk(lib.cadet_pack(_vp(inp.X_hist), None, _vp(inp.lens), inp.n_hist, d, T, None, None, _vp(self.Hs[0]),
-                               None, None, _vp(self.cu_hist2), _vp(self.n_packed2),
-                               C.c_void_p(self.small_ws.data_ptr() + 512), 256,
-                               C.c_void_p(self._pack_stream.cuda_stream)))
-            self._pack_done.record()
+        if not cfg.embed:
+            with torch.cuda.stream(self._pack_stream):
+                chk(lib.cadet_pack(_vp(inp.X_hist), None, _vp(inp.lens), inp.n_hist, d, T, None, None,
+                                   _vp(self.Hs[0]), None, None, _vp(self.cu_hist2), _vp(self.n_packed2),
+                                   C.c_void_p(self.small_ws.data_ptr() + 512), 256,
+                                   C.c_void_p(self._pack_stream.cuda_stream)))
+        self._pack_done.record(self._pack_stream)
         chk(lib.cadet_pack(None, None, _vp(inp.lens), inp.n_hist, d, T, _vp(inp.t_hist), _vp(inp.s_hist), None,
                            _vp(self.t_p), _vp(self.s_p), _vp(self.cu_hist), _vp(self.n_packed), _vp(self.small_ws),
                            256, st))
         chk(lib.cadet_chunk(_vp(self.cu_hist), inp.n_hist, cfg.L_chunk, _vp(self.cu), inp.n_chunks + 8,
                             _vp(self.n_out), C.c_void_p(self.small_ws.data_ptr() + 256), st))
+        if cfg.embed:  # NEXT-3: H[0] = summed embeddings of the packed tokens (contiguous histories: the packed
+            # rows are the first cu_hist[n_hist] history rows; the rest of the budget is padding)
+            tabs = (C.c_void_p * len(cfg.vocab))(*[e.data_ptr() for e in self.E])
+            chk(lib.cadet_embed_forward(C.byref(self.ecfg), tabs, _vp(inp.ids), T,
+                                        C.c_void_p(self.cu_hist.data_ptr() + 4 * inp.n_hist), _vp(self.Hs[0]),
+                                        _vp(self._ews), self._ews.numel(), st))
         # context buckets k_t of the impressions from their raw positions
         bnd = (C.c_int32 * len(cfg.boundaries))(*cfg.boundaries)
         chk(lib.cadet_bucketize(_vp(inp.position), n_imp, bnd, len(cfg.boundaries), _vp(self.bucket),
@@ -439,7 +464,8 @@ class CadetStack:
         # HSDP (NEXT-4) replaces the overlapped gradient all-reduces by one reduce-scatter after the backward
         hsdp = group is not None and cfg.optimizer == "adamw" and cfg.shard
         dp = None if hsdp else group
-        buckets = GradBuckets([self.grads[self._tower_off:]], dp)
+        buckets = GradBuckets([self.grads[self._tower_off:self._embed_off]] +
+                              ([self.grads[self._embed_off:]] if cfg.embed else []), dp)
         if dp is not None and self._grad_events is None:
             self._side = torch.cuda.Stream(self.dev)
             self._grad_events = [[torch.cuda.Event() for _ in range(6)] for _ in range(nl)]
@@ -467,6 +493,12 @@ class CadetStack:
                 with torch.cuda.stream(self._side):
                     handles.append(torch.distributed.all_reduce(sl, group=group, async_op=True))
             self._layer_backward(l, b, ws, wsn, st, evs, reduce)
+        if cfg.embed:  # NEXT-3: the embedding tables' gradients from dH[0] (deterministic scatter-add)
+            dts = (C.c_void_p * len(cfg.vocab))(*[g.data_ptr() for g in self.dE])
+            chk(lib.cadet_embed_backward(C.byref(self.ecfg), _vp(inp.ids), T,
+                                         C.c_void_p(self.cu_hist.data_ptr() + 4 * inp.n_hist), _vp(self.dHs[0]), dts,
+                                         _vp(self._ews), self._ews.numel(), st))
+            buckets.launch(1)
         buckets.wait()
         for h in handles:
             h.wait()
@@ -634,3 +666,5 @@ class CadetStack:
         ops.poll(self.small_ws[256:])      # chunk error word
         ops.poll(self.small_ws[512:])      # row-move pack error word
         ops.poll(self.small_ws[768:])      # bucketize error word (positions < 1)
+        if self.cfg.embed:
+            ops.poll(self._ews)              # embedding ids out of range

@@ -264,6 +264,37 @@ def fixed_lengths_batch(lengths, seed: int = 0, cfg: GenConfig | None = None, n_
     return concat_users(users)
 
 
+EMBED_VOCAB = (2, 16384, 8, 4)   # token type (impression / action), ad id, request feature, action id
+
+
+def token_ids(seed: int, users, vocab=EMBED_VOCAB) -> np.ndarray:
+    """Per-token integer ids of the embedded input fields (Eq. 1), int32 [R, 4] for the
+    users' tokens back to back, -1 = field absent for the token kind (R37):
+      column 0  token type: 0 = impression I_t (even local rows), 1 = action token (C_t, A_t)
+      column 1  ad id of the impression, Zipf(1.2) over vocab[1] (impressions only)
+      column 2  request feature (e.g. device type) ~ U{0 .. vocab[2]-1} (impressions only)
+      column 3  action id ~ U{0 .. vocab[3]-1} (action tokens only)
+    Raw categorical inputs only: looking the rows up and summing them is the method's step."""
+    out = []
+    for u, usr in enumerate(users):
+        rng = np.random.default_rng([seed, 7919, u])
+        m = usr.length
+        ids = np.full((m, 4), -1, dtype=np.int32)
+        imp = (np.arange(m) % 2) == 0
+        ids[:, 0] = np.where(imp, 0, 1)
+        n_i, n_a = int(imp.sum()), int((~imp).sum())
+        ids[imp, 1] = (rng.zipf(1.2, size=n_i) - 1) % vocab[1]
+        ids[imp, 2] = rng.integers(0, vocab[2], size=n_i)
+        ids[~imp, 3] = rng.integers(0, vocab[3], size=n_a)
+        out.append(ids)
+    return np.concatenate(out) if out else np.zeros((0, 4), np.int32)
+
+
+def embed_tables(seed: int, d: int, vocab=EMBED_VOCAB) -> list:
+    """Embedding tables E_f ~ N(0, 1/len(vocab)) rounded to bf16 (the summed row has unit variance)."""
+    return [normal_bf16(seed, 8000 + f, (V, d), scale=1.0 / np.sqrt(len(vocab))) for f, V in enumerate(vocab)]
+
+
 def aux_labels(seed: int, n: int) -> np.ndarray:
     """Auxiliary-task targets per impression (NEXT-2): column 0 a long-dwell indicator
     (Bernoulli 0.2), column 1 an impression duration in minutes (log-normal, median 0.5).

@@ -250,3 +250,75 @@ def test_block_stack_checkpointing_matches(block_stacks):
     assert np.abs(ga - gb).max() <= 1e-5 * max(1.0, np.abs(ga).max())
     assert float(b.loss.item()) == pytest.approx(float(a.loss.item()), rel=1e-6)
     assert np.abs(ga).max() > 0 and all(float(g_.abs().max()) > 0 for g_ in a.gF[0])
+
+
+# ------------------------------------------------------------------ NEXT-3 input embeddings (Eq. 1)
+@pytest.mark.parametrize("d,T,n_valid", [(64, 300, 290), (1024, 5000, 5000), (352, 4097, 3000)])
+def test_embeddings_forward_backward(ops, d, T, n_valid):
+    """cadet_embed_forward: bit-exact bf16 rounding of the fp64 sum (<= 4 bf16 rows sum exactly in fp32);
+    rows >= n_valid are 0.  cadet_embed_backward vs oracle.embed_backward at 1e-5 (fp32 in-order sums /
+    2^-24 fixed point) and bit-identical on a second run (deterministic)."""
+    import ctypes as C
+    from paper_2602_11410_b200 import _lib as L
+    vocab = G.EMBED_VOCAB
+    users = G.fixed_lengths_batch([T // 3, T // 3, T - 2 * (T // 3)], seed=5).users
+    ids = G.token_ids(5, users, vocab)
+    tables = G.embed_tables(5, d, vocab)
+    cfg = L.EmbedConfig(len(vocab), d, (C.c_int32 * 8)(*vocab))
+    lib = L.lib()
+    ws = torch.zeros(lib.cadet_embed_workspace_bytes(C.byref(cfg)), dtype=torch.uint8, device="cuda")
+    tabs = [bf16_tensor(t) for t in tables]
+    idd = torch.tensor(ids, device="cuda")
+    nv = torch.tensor([n_valid], dtype=torch.int32, device="cuda")
+    X = torch.empty(T, d, dtype=torch.bfloat16, device="cuda")
+    st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    L.check(lib.cadet_embed_forward(C.byref(cfg), (C.c_void_p * 4)(*[t.data_ptr() for t in tabs]),
+                                    C.c_void_p(idd.data_ptr()), T, C.c_void_p(nv.data_ptr()), C.c_void_p(X.data_ptr()),
+                                    C.c_void_p(ws.data_ptr()), ws.numel(), st))
+    ref = O.embed_forward(ids, [t.astype(np.float64) for t in tables])
+    ref[n_valid:] = 0
+    got = to_np(X)
+    assert (got == G.bf16_round(ref.astype(np.float32)).astype(np.float64)).all()
+    dX = G.normal_bf16(6, 0, (T, d))
+    dXd = bf16_tensor(dX)
+    outs = []
+    for _ in range(2):
+        dE = [torch.full((V, d), float("nan"), device="cuda") for V in vocab]
+        L.check(lib.cadet_embed_backward(C.byref(cfg), C.c_void_p(idd.data_ptr()), T, C.c_void_p(nv.data_ptr()),
+                                         C.c_void_p(dXd.data_ptr()), (C.c_void_p * 4)(*[g.data_ptr() for g in dE]),
+                                         C.c_void_p(ws.data_ptr()), ws.numel(), st))
+        torch.cuda.synchronize()
+        outs.append([g.cpu().numpy().astype(np.float64) for g in dE])
+    ops.poll(ws)
+    dXm = dX.astype(np.float64)
+    dXm[n_valid:] = 0
+    refs = O.embed_backward(ids, dXm, vocab)
+    for f, (g, r) in enumerate(zip(outs[0], refs)):
+        assert_close(g, r, 1e-5, 1e-6, what=f"dE table {f} (vocab {vocab[f]})")
+        assert (outs[0][f] == outs[1][f]).all()
+
+
+def test_block_stack_with_embeddings_steps():
+    """CadetStack(block=True, embed=True): H[0] is the embedding of the packed tokens and the embedding
+    gradients equal the oracle adjoint of the GPU's own dH[0]."""
+    import bench
+    from paper_2602_11410_b200.model import CadetStack, StackConfig
+    wl = dict(d_model=256, n_heads=2, n_layers=2, budget=8192, L_chunk=1024, max_tokens=2048)
+    users, hinp = bench.build_inputs(wl, 3, pin=False, vocab=StackConfig().vocab)
+    inp = hinp.to("cuda")
+    st = CadetStack(StackConfig(d_model=256, n_heads=2, n_layers=2, budget=8192, L_chunk=1024, block=True,
+                                embed=True), seed=3, device="cuda")
+    loss = st.step(inp)
+    torch.cuda.synchronize()
+    st.poll()
+    assert np.isfinite(loss.item())
+    n = int(st.cu_hist[inp.n_hist].item())
+    ids = inp.ids.cpu().numpy()[:8192]
+    E = [to_np(e) for e in st.E]
+    H0 = O.embed_forward(ids[:n], E)
+    assert (to_np(st.Hs[0])[:n] == G.bf16_round(H0.astype(np.float32)).astype(np.float64)).all()
+    assert (to_np(st.Hs[0])[n:] == 0).all()
+    dH0 = to_np(st.dHs[0])
+    refs = O.embed_backward(ids[:n], dH0[:n], st.cfg.vocab)
+    for f, r in enumerate(refs):
+        assert_close(st.dE[f].cpu().numpy(), r, 1e-5, 1e-6, what=f"stack dE {f}")

@@ -708,6 +708,32 @@ def test_block_backward_by_finite_differences_and_zero_ffn_reduction():
 
 
 # ------------------------------------------------------------------ NEXT-4: AdamW (R35)
+def test_embeddings_onehot_matmul_loop_and_adjoint():
+    """NEXT-3 embeddings (Eq. 1): the gather-sum equals the one-hot matmul sum_f onehot_f E_f (a
+    library routine) and a per-token loop; the backward equals onehot_f^T dX and satisfies the adjoint
+    identity <embed(E), dX> = sum_f <E_f, dE_f>."""
+    rng = np.random.default_rng(3)
+    vocab, d, T = (2, 50, 5, 3), 16, 200
+    ids = np.stack([rng.integers(-1, V, size=T) for V in vocab], axis=1)
+    tables = [rng.standard_normal((V, d)) for V in vocab]
+    X = O.embed_forward(ids, tables)
+    onehot = [np.eye(V)[np.where(ids[:, f] >= 0, ids[:, f], 0)] * (ids[:, f] >= 0)[:, None] for f, V in enumerate(vocab)]
+    assert np.allclose(X, sum(oh @ E for oh, E in zip(onehot, tables)), atol=1e-12)
+    loop = np.zeros((T, d))
+    for t in range(T):
+        for f in range(len(vocab)):
+            if ids[t, f] >= 0:
+                loop[t] += tables[f][ids[t, f]]
+    assert np.array_equal(X, loop)
+    dX = rng.standard_normal((T, d))
+    dE = O.embed_backward(ids, dX, vocab)
+    for oh, g in zip(onehot, dE):
+        assert np.allclose(g, oh.T @ dX, atol=1e-12)
+    lhs = float((X * dX).sum())
+    rhs = sum(float((E * g).sum()) for E, g in zip(tables, dE))
+    assert abs(lhs - rhs) <= 1e-9 * max(1.0, abs(lhs))
+
+
 def test_adamw_first_step_constant_gradient_and_decay_closed_forms():
     """Pins of O.adamw_step against closed forms of Adam's algebra (Kingma & Ba, Alg. 1; decoupled
     decay, Loshchilov & Hutter): (i) step 1: m_hat = g, v_hat = g^2, so the update is
