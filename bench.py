@@ -250,6 +250,28 @@ def blas_info():
         return f"unavailable: {type(ex).__name__}"
 
 
+def bind_numa_local(dev_index: int):
+    """Pin this rank's host threads to the CPUs of its GPU's NUMA node (sysfs local_cpulist), so the
+    pinned input buffers are first-touched on the GPU's local memory and the e2e host->device copies do
+    not cross the socket interconnect.  Returns the CPU list or None (no sysfs entry: unchanged)."""
+    try:
+        import torch
+        pp = torch.cuda.get_device_properties(dev_index)
+        pci = f"{getattr(pp, 'pci_domain_id', 0):04x}:{pp.pci_bus_id:02x}:{getattr(pp, 'pci_device_id', 0):02x}.0"
+        txt = open(f"/sys/bus/pci/devices/{pci}/local_cpulist").read().strip()
+        cpus = set()
+        for part in txt.split(","):
+            a, _, b = part.partition("-")
+            cpus.update(range(int(a), int(b or a) + 1))
+        cpus &= set(os.sched_getaffinity(0)) or cpus
+        if cpus:
+            os.sched_setaffinity(0, cpus)
+            return sorted(cpus)
+    except Exception:  # noqa: BLE001
+        pass
+    return None
+
+
 def cpu_cores():
     try:
         return len(os.sched_getaffinity(0))
@@ -347,6 +369,7 @@ def main():
     if local == 0:
         build.build(verbose=False)  # no-op when the shipped libcadet.so is current
     torch.cuda.set_device(local)
+    numa_cpus = bind_numa_local(local) if world > 1 else None  # N > 1: each rank's host memory on its GPU's node
     group = None
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -489,7 +512,8 @@ def main():
                "h2d_bytes_per_step": int(host_inp.nbytes()), "d2h_bytes_per_step": 4 + 4 * n_imp * scfg.K,
                "d2h": "loss + the K tower logits of every impression (the north star's output)",
                "ms_per_step": float(ems.item()),
-               "pipeline": "inputs of step i+1 copied (pinned host -> HBM, copy stream) while step i computes"}
+               "pipeline": "inputs of step i+1 copied (pinned host -> HBM, copy stream) while step i computes",
+               "host_numa_cpus": None if numa_cpus is None else f"{len(numa_cpus)} cpus local to the GPU"}
     stack.poll()
 
     # ---------------- other batches (seeds 1..S-1), each timed like seed 0 (resident inputs)

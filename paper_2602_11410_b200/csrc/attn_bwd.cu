@@ -561,7 +561,7 @@ __global__ void __launch_bounds__(320, 1)
       const int entry = list[u.off + it];
       const int q = u.sa + (entry & 0xFFFF) * 128 + grp * 64 + gt;
       const bool v = q < u.se;
-      nl = v ? p.lse[(size_t)u.h * p.T + q] * LOG2E : INFINITY;
+      nl = v ? p.lse[(size_t)u.h * p.T + q] : INFINITY;  // x log2e when staged (keeps the load asynchronous)
       nd = v ? p.D[(size_t)u.h * p.T + q] : 0.f;
       ne = v ? p.plan.kv_end[q] : -1;
       nent = entry;
@@ -585,7 +585,7 @@ __global__ void __launch_bounds__(320, 1)
         const int g = gq + it;
         float* vb = vgrp + (g & 1) * 256;
         if (gt < 64) {
-          vb[gt] = nl;
+          vb[gt] = nl * LOG2E;
           vb[64 + gt] = nd;
           reinterpret_cast<int*>(vb)[128 + gt] = ne;
           if (gt == 0) reinterpret_cast<int*>(vb)[192] = nent;
