@@ -362,6 +362,8 @@ def main():
         print(json.dumps(out))
         return
 
+    # NCCL writes its version / debug lines to stdout by default; keep stdout for the one JSON line
+    os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
     import torch
     import torch.distributed as dist
     from paper_2602_11410_b200 import build, ops
