@@ -362,8 +362,11 @@ def main():
         print(json.dumps(out))
         return
 
-    # NCCL writes its version / debug lines to stdout by default; keep stdout for the one JSON line
-    os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+    # keep stdout for the one JSON line: anything else written to fd 1 (NCCL's version / debug lines, other
+    # native prints) goes to stderr; the JSON line is printed through a duplicate of the original stdout
+    sys.stdout.flush()
+    json_out = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
     import torch
     import torch.distributed as dist
     from paper_2602_11410_b200 import build, ops
@@ -634,7 +637,8 @@ def main():
         "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
         "cuda_graph": graph is not None, "cuda_graph_error": graph_err,
     }
-    print(json.dumps(out))
+    json_out.write(json.dumps(out) + "\n")
+    json_out.flush()
     if group is not None:
         dist.destroy_process_group()
 
