@@ -249,10 +249,9 @@ LayerWs carve_ws(void* ws, const cadet_attn_config* c, int n, int T) {
 
 // Timestamp RoPE of the layer, evaluated on the fly by the kernels that rotate
 RopeOTF rope_of(const cadet_attn_config* cfg, const cadet_batch* b, const PlanView& v) {
+  (void)b;
   RopeOTF r;
-  r.t = b->timestamps_ms;
-  r.row_seq = v.row_seq;
-  r.cu = b->cu_seqlens;
+  r.dt = v.rope_dt;
   r.theta = v.theta;
   r.on = cfg->use_rope;
   return r;

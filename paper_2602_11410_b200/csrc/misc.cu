@@ -40,10 +40,8 @@ __device__ __forceinline__ void rope_cs_f(float dth, float dtl, float thh, float
 // (cos, sin) of pairs i0 .. i0 + N - 1 of `row` (time rebased to the row's sequence start)
 template <int N>
 __device__ __forceinline__ void rope_row_cs(const RopeOTF& rp, int row, int i0, float (&c)[N], float (&s)[N]) {
-  const int sq = rp.row_seq[row];
-  const long long dt = sq >= 0 ? (long long)(rp.t[row] - rp.t[rp.cu[sq]]) : 0;
-  const float dth = (float)dt;
-  const float dtl = (float)(dt - (long long)dth);
+  const float2 d = rp.dt[row];  // one load: the plan rebased and split the row's time
+  const float dth = d.x, dtl = d.y;
 #pragma unroll
   for (int e = 0; e < N; ++e) {
     const float2 th = rp.theta[i0 + e];

@@ -13,9 +13,7 @@ namespace cadet {
 // two-product and a two-constant 2 pi), ~3e-7 rad absolute for |alpha| <= 1e4 rad, then MUFU sincos.
 // on = 0: no RoPE (ablation).
 struct RopeOTF {
-  const int64_t* t;
-  const int32_t* row_seq;  // the plan's row -> sequence map (-1 for pad rows)
-  const int32_t* cu;
+  const float2* dt;        // [T] the plan's rebased row times (hi, lo): t_row - t_(sequence start)
   const float2* theta;     // [hd / 2] (hi, lo)
   int32_t on;
 };

@@ -39,6 +39,7 @@ size_t plan_bytes(int32_t n, int32_t T, int32_t max_seqlen) {
   b += align256(list_cap_of(nq, hm) * 4);
   b += align256((size_t)(n + 1) * 4);       // seq_rank
   b += align256(64 * sizeof(float2));       // RoPE theta (hi, lo)
+  b += align256((size_t)T * sizeof(float2));  // per-row rebased time (hi, lo)
   return b;
 }
 
@@ -71,6 +72,7 @@ PlanView plan_carve(void* ws, int32_t n, int32_t T, int32_t max_seqlen) {
   v.bwd_list = reinterpret_cast<int32_t*>(take(list_cap_of(v.nq_cap, v.hmax) * 4));
   v.seq_rank = reinterpret_cast<int32_t*>(take((size_t)(n + 1) * 4));
   v.theta = reinterpret_cast<float2*>(take(64 * sizeof(float2)));
+  v.rope_dt = reinterpret_cast<float2*>(take((size_t)T * sizeof(float2)));
   return v;
 }
 
@@ -193,6 +195,7 @@ __global__ void __launch_bounds__(256) plan_row_kernel(PlanArgs a, PlanView v) {
       v.kv_end[i] = i;
       v.row_seq[i] = -1;
       v.row_pp[i] = 0;
+      v.rope_dt[i] = make_float2(0.f, 0.f);
     } else {
       // sequence of row i: largest s with cu[s] <= i
       int lo = 0, hi = a.n - 1;
@@ -212,6 +215,11 @@ __global__ void __launch_bounds__(256) plan_row_kernel(PlanArgs a, PlanView v) {
       const int L = m - nc;
       const int li = i - sa;
       const int64_t ti = a.t[i];
+      {  // the row's time rebased to its sequence start, split exactly into two floats (RoPE; R21)
+        const long long dt = (long long)(ti - a.t[sa]);
+        const float hi = (float)dt;
+        v.rope_dt[i] = make_float2(hi, (float)(dt - (long long)hi));
+      }
       if (li > 0 && a.t[i - 1] > ti) err |= ERRBIT_ORDER;
       if (a.sess && li > 0 && a.sess[i - 1] > a.sess[i]) err |= ERRBIT_ORDER;
       int e;

@@ -38,6 +38,7 @@ struct PlanView {   // device pointers into the workspace
   int32_t* bwd_list;  // [list_cap] q-tiles visiting k-tile g: qt | FULL << 30 (all cells visible)
   int32_t* seq_rank;  // [n] rank of a sequence among those with the same tile count (bwd order)
   float2* theta;      // [64] RoPE theta_i as (hi, lo) floats, i < head_dim / 2
+  float2* rope_dt;    // [T] t_row - t_(sequence start) as exact (hi, lo) floats (0 for pad rows)
   int32_t nq_cap, hmax, list_cap;
 };
 
