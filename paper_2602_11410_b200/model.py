@@ -668,3 +668,86 @@ class CadetStack:
         ops.poll(self.small_ws[768:])      # bucketize error word (positions < 1)
         if self.cfg.embed:
             ops.poll(self._ews)              # embedding ids out of range
+
+
+# ------------------------------------------------------------------ NEXT-1: serving
+class ServingGraph:
+    """Latency path for the paper's serving shape: a request = ONE packed sequence
+    of n_ctx context tokens followed by n_cand candidates (context causal with Delta = 0, candidates
+    see the context and themselves), scored by L gated layers + the K towers on the
+    candidate rows (all towers in one pass).  The whole forward -- mask plan, every layer and
+    the towers -- is captured ONCE as a CUDA graph over static buffers; a request copies its features
+    and timestamps into those buffers and replays the graph (no per-kernel host launches).  The
+    paper's kernel "integrates with torch.compile"; a CUDA graph is the B200-native
+    equivalent here (no tracing compiler)."""
+
+    def __init__(self, d_model: int, n_heads: int, n_ctx: int, n_cand: int, n_layers: int = 1, K: int = 2,
+                 seed: int = 0, device="cuda"):
+        from synth import generator as G
+        self.dev = torch.device(device)
+        self.d, self.H, self.L, self.K = d_model, n_heads, n_layers, K
+        self.T = T = n_ctx + n_cand
+        self.n_cand = n_cand
+        lib = L.lib()
+        self.acfg = ops.config(d_model, n_heads, delta_delay_ms=0, delta_cand_ms=0)
+        mk = lambda a, dt: torch.tensor(np.asarray(a), dtype=dt, device=self.dev)
+        self.cu = mk([0, T], torch.int32)
+        self.ncand = mk([n_cand], torch.int32)
+        self.t = torch.zeros(T, dtype=torch.int64, device=self.dev)
+        self.X = torch.zeros(T, d_model, dtype=torch.bfloat16, device=self.dev)
+        self.rows = mk(np.arange(n_ctx, T), torch.int32)
+        self.W = [[mk(w, torch.float32).to(torch.bfloat16) for w in G.layer_weights(seed, l, d_model).as_list()]
+                  for l in range(n_layers)]
+        dh = d_model // 2
+        hw = G.head_weights(seed, K, d_model, dh)
+        self.W1 = mk(np.concatenate([hw.W1[k] for k in range(K)], axis=1), torch.float32).to(torch.bfloat16)
+        self.b1, self.w2, self.b2 = (mk(x.reshape(-1), torch.float32) for x in (hw.b1, hw.w2, hw.b2))
+        self.hc = L.HeadConfig(K, d_model, dh, 0)
+        self.Hs = [self.X] + [torch.zeros(T, d_model, dtype=torch.bfloat16, device=self.dev) for _ in range(n_layers)]
+        self.saved = torch.empty(lib.cadet_attn_saved_bytes(C.byref(self.acfg), T), dtype=torch.uint8,
+                                 device=self.dev)
+        self.ws = ops.workspace(lib.cadet_attn_workspace_bytes(C.byref(self.acfg), 1, T), self.dev)
+        self.hws = ops.workspace(lib.cadet_heads_workspace_bytes(C.byref(self.hc), n_cand), self.dev)
+        self.logits = torch.empty(n_cand, K, dtype=torch.float32, device=self.dev)
+        self.pre = torch.empty(n_cand, K * dh, dtype=torch.bfloat16, device=self.dev)
+        self.graph = None
+
+    def _batch(self):
+        return ops.PackedBatch(cu_seqlens=self.cu, timestamps_ms=self.t, total_tokens=self.T, max_seqlen=self.T,
+                               n_candidates=self.ncand).struct()
+
+    def forward(self):
+        """The eager forward on the static buffers (what the graph replays): plan, layers, towers."""
+        lib, chk = L.lib(), L.check
+        st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+        b = self._batch()
+        self.acfg.plan_ready = 0
+        chk(lib.cadet_mask_plan(C.byref(self.acfg), C.byref(b), _vp(self.ws), self.ws.numel(), st))
+        self.acfg.plan_ready = 1
+        for l in range(self.L):
+            w = L.AttnWeights(*[x.data_ptr() for x in self.W[l]])
+            chk(lib.cadet_attn_forward(C.byref(self.acfg), C.byref(b), C.byref(w), _vp(self.Hs[l]),
+                                       _vp(self.Hs[l + 1]), _vp(self.Hs[l]), _vp(self.saved), _vp(self.ws),
+                                       self.ws.numel(), st))
+        hw = L.HeadWeights(self.W1.data_ptr(), self.b1.data_ptr(), self.w2.data_ptr(), self.b2.data_ptr())
+        chk(lib.cadet_heads_forward(C.byref(self.hc), C.byref(hw), _vp(self.Hs[-1]), _vp(self.rows), self.n_cand,
+                                    _vp(self.logits), _vp(self.pre), _vp(self.hws), self.hws.numel(), st))
+        return self.logits
+
+    def capture(self):
+        self.forward()  # sizes, one-time attributes, TMA descriptors warm
+        torch.cuda.synchronize()
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            self.forward()
+        return self.graph
+
+    def score(self, X: torch.Tensor, t_ms: torch.Tensor) -> torch.Tensor:
+        """One request: features [T, d] bf16 and timestamps [T] int64 (context then candidates) ->
+        candidate logits [n_cand, K] (the graph's static output buffer)."""
+        self.X.copy_(X, non_blocking=True)
+        self.t.copy_(t_ms, non_blocking=True)
+        if self.graph is None:
+            return self.forward()
+        self.graph.replay()
+        return self.logits

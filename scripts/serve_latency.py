@@ -91,9 +91,34 @@ def main():
         pairs = (4096 * 4097) // 2 + 512 * 4097  # L(L+1)/2 + N(L+1) (SURVEY: exact allowed pairs)
         flops = 4.0 * hd * H * pairs
         ops.poll(ws)
+        # the whole request (plan + layer + towers on the 512 candidates): eager launches vs the CUDA graph
+        # (model.ServingGraph), device time per request and host wall time per request (synchronised)
+        from paper_2602_11410_b200.model import ServingGraph
+        import time
+        sg = ServingGraph(d, H, 4096, 512, n_layers=1)
+        Xr = (torch.randn(T, d, generator=g)).to(torch.bfloat16).to(dev)
+        tr = torch.tensor(t, device=dev)
+        eager_us = time_calls(lambda: sg.score(Xr, tr), iters=100)
+        sg.capture()
+        graph_us = time_calls(lambda: sg.score(Xr, tr), iters=200)
+
+        def wall(n=200):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            for _ in range(n):
+                sg.score(Xr, tr)
+                torch.cuda.synchronize()
+            return (time.perf_counter() - t0) * 1e6 / n
+        graph_wall = wall()
+        sg.graph = None
+        eager_wall = wall(100)
+        ops.poll(sg.ws)
         out["results"].append({"d_model": d, "heads": H, "head_dim": hd, "attn_core_us": core_us,
                                "attn_core_tflops_on_allowed_pairs": flops / (core_us * 1e-6) / 1e12,
-                               "layer_fwd_us": layer_us, "allowed_pairs_per_head": pairs})
+                               "layer_fwd_us": layer_us, "allowed_pairs_per_head": pairs,
+                               "request_eager_device_us": eager_us, "request_graph_device_us": graph_us,
+                               "request_eager_wall_us": eager_wall, "request_graph_wall_us": graph_wall,
+                               "request": "plan + 1 gated layer + K=2 towers on 512 candidates"})
     print(json.dumps(out))
 
 

@@ -285,3 +285,46 @@ def test_gradient_checkpointing_matches_stored_activations():
     # the loss is summed with per-warp fp32 atomics (order may differ between runs)
     assert float(b.loss.item()) == pytest.approx(float(a.loss.item()), rel=1e-6)
     assert float((a.dHs[0].float() - b.dHs[0].float()).abs().max()) <= 1e-2
+
+
+def test_next1_serving_graph_replays_the_eager_forward():
+    """NEXT-1 latency path: the request forward (plan, gated layer, towers on the 512
+    candidate rows) captured once as a CUDA graph; replaying it on a NEW request's features / times
+    reproduces the eager forward of that request, whose candidate logits match the fp64 oracle."""
+    from paper_2602_11410_b200 import build
+    from paper_2602_11410_b200.model import ServingGraph
+    build.build()
+    n_ctx, n_cand, d, H = 4096, 512, 352, 4
+    sg = ServingGraph(d, H, n_ctx, n_cand, n_layers=1, seed=3)
+    T = n_ctx + n_cand
+
+    def req(seed):
+        rng = np.random.default_rng(seed)
+        t_ctx = np.cumsum(rng.integers(1, 600_000, size=n_ctx)).astype(np.int64) + 1_700_000_000_000
+        t = np.concatenate([t_ctx, np.full(n_cand, t_ctx[-1] + 1, np.int64)])
+        X = G.normal_bf16(seed, 2, (T, d))
+        return X, t
+
+    X0, t0 = req(1)
+    sg.score(bf16_tensor(X0), torch.tensor(t0, device="cuda"))
+    sg.capture()
+    X1, t1 = req(2)
+    z_graph = sg.score(bf16_tensor(X1), torch.tensor(t1, device="cuda")).clone()
+    sg.graph = None
+    z_eager = sg.score(bf16_tensor(X1), torch.tensor(t1, device="cuda")).clone()
+    torch.cuda.synchronize()
+    ops_poll = __import__("paper_2602_11410_b200.ops", fromlist=["poll"]).poll
+    ops_poll(sg.ws)
+    assert float((z_graph - z_eager).abs().max()) <= 1e-5 * max(1.0, float(z_eager.abs().max()))
+    # oracle: layer (residual) + towers on the candidate rows of the request
+    ocfg = O.AttnConfig(d_model=d, n_heads=H, delta_delay_ms=0, delta_cand_ms=0)
+    Wl = [w.astype(np.float64) for w in G.layer_weights(3, 0, d).as_list()]
+    meta = meta_of(np.array([0, T]), t1, np.zeros(T, np.int64), np.array([n_cand]))
+    Y, _, _ = O.batch_forward(X1.astype(np.float64), Wl, meta, ocfg)
+    Hn = X1.astype(np.float64) + Y
+    hw = G.head_weights(3, 2, d, d // 2)
+    z, _, _ = O.heads_forward(Hn, np.arange(n_ctx, T), hw.W1.astype(np.float64), hw.b1.astype(np.float64),
+                              hw.w2.astype(np.float64), hw.b2.astype(np.float64))
+    mx, mn, rms = err_stats(z_eager.cpu().numpy(), z)
+    print(f"[parity] NEXT-1 serving graph logits vs oracle (bf16 pipeline, reported): max {mx:.3e} mean {mn:.3e}")
+    assert mx <= 5e-2 and mn <= 5e-3
