@@ -77,8 +77,10 @@ CADET_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t a = smem_u32(bar);
   if (mbar_try_wait(a, parity)) return;
   const uint64_t t0 = global_ns();
-  while (!mbar_try_wait(a, parity)) {
-    if (global_ns() - t0 > 20000000000ull) {
+  // the deadline is checked every 64th unsuccessful try_wait only: a waiting warp issues as few
+  // instructions as possible (it shares the scheduler with the warps doing the work)
+  for (uint32_t n = 1; !mbar_try_wait(a, parity); ++n) {
+    if ((n & 63u) == 0 && global_ns() - t0 > 20000000000ull) {
       printf("cadet: mbarrier timeout block %d thread %d\n", blockIdx.x, threadIdx.x);
       __trap();
     }
