@@ -8,7 +8,7 @@ import pytest
 
 from oracle import cadet_oracle as O
 from synth import generator as G
-from tests.helpers import assert_close, assert_close_stored, bf16_tensor, err_stats, make_case, to_dev_batch, to_np
+from tests.helpers import assert_close, bf16_tensor, err_stats, make_case, to_dev_batch, to_np
 from tests.test_gpu_core import core_case, meta_of, oracle_cfg
 
 pytestmark = pytest.mark.gpu
@@ -119,48 +119,23 @@ LAYER_CASES = [
 
 
 @pytest.mark.parametrize("case", range(len(LAYER_CASES)))
-def test_layer_forward_stages_and_end_to_end(ops, case):
+def test_layer_forward_end_to_end(ops, case):
+    """Protocol (iv): the bf16 layer output Y from X through the whole fp64 chain of Eqs. 3-7 (gated
+    at 1e-2 / 1e-3 in the flat regime, reported in the peaky one).  The per-stage gates (protocol iii,
+    on the fp32 accumulators) are in test_gpu_stages.py."""
     lengths, d, H, nc, peaky = LAYER_CASES[case]
     cu, t, s, ncv, T, X, W = layer_case(lengths, d, H, nc, seed=case, peaky=peaky)
     cfg = ops.config(d, H, delta_delay_ms=120_000, rope_phi_min=0.5, rope_base=1e4, rope_delta_t_max_ms=86_400_000)
     b = to_dev_batch(cu, t, s, ncv, T)
     Y, saved, ws, *_ = run_layer_forward(ops, cfg, b, X, W, T)
-    sv = saved_views(saved, T, d, H)
     ocfg = oracle_cfg(cfg)
     meta = meta_of(cu, t, s, ncv)
     Wl = [w.astype(np.float64) for w in W.as_list()]
     n = cu[-1]
-    Xf = X.astype(np.float64)
-    # A2: stage fed by the same bf16 X
-    assert_close_stored(sv["Zx"][:n], (Xf @ Wl[0])[:n], what="Zx")
-    assert_close_stored(sv["Xt"][:n], (Xf * O.sigmoid(Xf @ Wl[0]))[:n], what="Xt")
-    # A3: fed by the GPU's Xt
-    for nm, Wi in (("Q", Wl[1]), ("K", Wl[2]), ("V", Wl[3])):
-        assert_close_stored(sv[nm][:n], (sv["Xt"] @ Wi)[:n], what=nm)
-    # A4: gates + RoPE fed by the GPU's Q, K
-    for nm, src, Wg, zn in (("Qr", "Q", Wl[4], "Zq"), ("Kr", "K", Wl[5], "Zk")):
-        # Qr / Kr are formed elementwise from the stored (bf16) Q and Zq
-        Z = sv[src] @ Wg
-        assert_close_stored(sv[zn][:n], Z[:n], what=zn)
-        ref = O.rope_heads(sv[src] * O.sigmoid(sv[zn]), t, ocfg)
-        assert_close_stored(sv[nm][:n], ref[:n], what=nm)
-    # A5: core fed by the GPU's Qr, Kr, V
-    Oref = np.zeros((T, d))
-    lref = np.zeros((H, T))
-    for k in range(len(lengths)):
-        a, e = cu[k], cu[k + 1]
-        A = O.seq_mask(meta, k, ocfg)
-        o, l, _ = O.attention_core_forward(sv["Qr"][a:e], sv["Kr"][a:e], sv["V"][a:e], A, H)
-        Oref[a:e], lref[:, a:e] = o, l
-    assert_close_stored(sv["O"], Oref, what="O")
-    assert_close(sv["lse"], lref, what="LSE")
-    # A6
     Yg = to_np(Y)
-    assert_close_stored(Yg, sv["O"] @ Wl[6], what="Y stage")
-    # end to end (bf16 intermediates) vs the full fp64 chain
-    Yref, _, _ = O.batch_forward(Xf, Wl, meta, ocfg)
+    Yref, _, _ = O.batch_forward(X.astype(np.float64), Wl, meta, ocfg)
     mx, mn, rms = err_stats(Yg, Yref)
-    print(f"e2e Y: max {mx:.3e} mean {mn:.3e} rms {rms:.3f}")
+    print(f"[parity] e2e Y (bf16 pipeline): max {mx:.3e} mean {mn:.3e} rms {rms:.3f}")
     if not peaky:
         assert mx <= 1e-2 and mn <= 1e-3
     assert (Yg[n:] == 0).all()
