@@ -224,3 +224,45 @@ def test_layer_and_towers_fp32_end_to_end(ops, case):
     for nm, gg, rr in zip(G.NAMES, gs, gWr):
         assert_close(npf(gg), rr, MAX32, MEAN32, what="fp32 e2e d" + nm)
     assert (npf(Y)[n_real:] == 0).all() and (npf(dX)[n_real:] == 0).all()
+
+
+@pytest.mark.parametrize("ablate", ["use_rep_gate", "use_int_gate", "use_rope", "use_out_proj"])
+def test_layer_fp32_ablations(ops, ablate):
+    """Table 1's ablation switches in the fp32 mode: each stage can be turned off and the layer forward /
+    backward still matches the oracle (with the same switch) end to end within 1e-4."""
+    from paper_2602_11410_b200 import _lib as L
+    lib = L.lib()
+    lengths, d, H = [300, 129, 77], 128, 2
+    cu, t, s, ncv, T, X, W = layer_case(lengths, d, H, None, seed=7)
+    cfg = ops.config(d, H, delta_delay_ms=120_000, rope_phi_min=0.5, rope_base=1e4, rope_delta_t_max_ms=86_400_000)
+    cfg.dtype = 1
+    setattr(cfg, ablate, 0)
+    b = to_dev_batch(cu, t, s, ncv, T)
+    Xd, Wd = f32(X), [f32(x) for x in W.as_list()]
+    w = L.AttnWeights(*[x.data_ptr() for x in Wd])
+    saved = torch.zeros(lib.cadet_attn_saved_bytes(C.byref(cfg), T), dtype=torch.uint8, device="cuda")
+    ws = ops.workspace(lib.cadet_attn_workspace_bytes(C.byref(cfg), b.n_seqs, T))
+    Y = torch.empty(T, d, dtype=torch.float32, device="cuda")
+    L.check(lib.cadet_attn_forward(C.byref(cfg), C.byref(b.struct()), C.byref(w), C.c_void_p(Xd.data_ptr()),
+                                   C.c_void_p(Y.data_ptr()), None, C.c_void_p(saved.data_ptr()),
+                                   C.c_void_p(ws.data_ptr()), ws.numel(), st()))
+    dY = np.random.default_rng(8).standard_normal((T, d)).astype(np.float32)
+    dY[cu[-1]:] = 0
+    dX = torch.empty(T, d, dtype=torch.float32, device="cuda")
+    gs = [torch.empty(d, d, dtype=torch.float32, device="cuda") for _ in range(7)]
+    g = L.AttnGrads(*[x.data_ptr() for x in gs])
+    dYd = f32(dY)
+    L.check(lib.cadet_attn_backward(C.byref(cfg), C.byref(b.struct()), C.byref(w), C.c_void_p(Xd.data_ptr()),
+                                    C.c_void_p(saved.data_ptr()), C.c_void_p(dYd.data_ptr()), C.c_void_p(dX.data_ptr()),
+                                    None, C.byref(g), C.c_void_p(ws.data_ptr()), ws.numel(), st()))
+    torch.cuda.synchronize()
+    ops.poll(ws)
+    ocfg = oracle_cfg(cfg)
+    meta = meta_of(cu, t, s, ncv)
+    Wl = [x.astype(np.float64) for x in W.as_list()]
+    Yr, caches, _ = O.batch_forward(X.astype(np.float64), Wl, meta, ocfg)
+    dXr, gWr, _ = O.batch_backward(caches, Wl, meta, dY.astype(np.float64), ocfg)
+    assert_close(npf(Y), Yr, MAX32, MEAN32, what=f"fp32 {ablate}=0 Y")
+    assert_close(npf(dX), dXr, MAX32, MEAN32, what=f"fp32 {ablate}=0 dX")
+    for nm, gg, rr in zip(G.NAMES, gs, gWr):
+        assert_close(npf(gg), rr, MAX32, MEAN32, what=f"fp32 {ablate}=0 d{nm}")
