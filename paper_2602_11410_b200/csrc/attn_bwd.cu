@@ -23,7 +23,7 @@ namespace cadet {
 
 #ifdef CADET_PHASE_TIMING
 // Phase timers (profiling builds only): per CTA, summed clock64 deltas, [blockIdx][8].
-__device__ unsigned long long g_phase[8192][8];
+__device__ unsigned long long g_phase[8192][16];
 // CTA timeline: [blockIdx][kernel 0=dq 1=dkv] {entry, first MMA result, all MMAs done, exit, smid, n}
 __device__ unsigned long long g_trace[8192][2][6];
 CADET_DEV unsigned long long gtime() {
@@ -331,32 +331,50 @@ __global__ void __launch_bounds__(320, 1)
 template <bool MASKED>
 CADET_DEV void dkv_chunk(const uint32_t (&us)[32], const uint32_t (&ud)[32], uint32_t vaddr, int key, uint32_t extra,
                          float sl2, uint32_t (&wp)[16], uint32_t (&wd)[16]) {
+  // per-column vectors of the q-tile stage: LSE (natural log) at vaddr, D at +512, visible-prefix end at +1024;
+  // packed f32x2 arithmetic (sm_100 FFMA2 / FADD2 / FMUL2) for everything but the exponentials
+  const float2 sl2v = make_float2(sl2, sl2), nlog2e = make_float2(-1.4426950408889634f, -1.4426950408889634f);
 #pragma unroll
   for (int i = 0; i < 32; i += 4) {
     const float4 l4 = lds_f4(vaddr + i * 4);
-    const float4 d4 = lds_f4(vaddr + 256 + i * 4);
-    const float lv[4] = {l4.x, l4.y, l4.z, l4.w}, dv[4] = {d4.x, d4.y, d4.z, d4.w};
-    int ev[4] = {0, 0, 0, 0};
-    if (MASKED) {
-      const int4 e4 = lds_i4(vaddr + 512 + i * 4);
-      ev[0] = e4.x, ev[1] = e4.y, ev[2] = e4.z, ev[3] = e4.w;
+    const float4 d4 = lds_f4(vaddr + 512 + i * 4);
+    const float2 nl01 = __fmul2_rn(make_float2(l4.x, l4.y), nlog2e), nl23 = __fmul2_rn(make_float2(l4.z, l4.w), nlog2e);
+    float2 x01 = __ffma2_rn(make_float2(__uint_as_float(us[i]), __uint_as_float(us[i + 1])), sl2v, nl01);
+    float2 x23 = __ffma2_rn(make_float2(__uint_as_float(us[i + 2]), __uint_as_float(us[i + 3])), sl2v, nl23);
+    if (MASKED) {  // extra = the chunk's visibility mask
+      if (!((extra >> i) & 1u)) x01.x = -INFINITY;
+      if (!((extra >> (i + 1)) & 1u)) x01.y = -INFINITY;
+      if (!((extra >> (i + 2)) & 1u)) x23.x = -INFINITY;
+      if (!((extra >> (i + 3)) & 1u)) x23.y = -INFINITY;
     }
-    float pv[4], sv[4];
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      float x = fmaf(__uint_as_float(us[i + e]), sl2, -lv[e]);
-      if (MASKED) {
-        const bool vis = (key < ev[e]) | (((extra >> (i + e)) & 1u) != 0u);
-        x = vis ? x : -INFINITY;
-      }
-      pv[e] = fast_exp2(x);
-      sv[e] = pv[e] * (__uint_as_float(ud[i + e]) - dv[e]);
-    }
-    wp[i >> 1] = pack_bf16(pv[0], pv[1]);
-    wp[(i >> 1) + 1] = pack_bf16(pv[2], pv[3]);
-    wd[i >> 1] = pack_bf16(sv[0], sv[1]);
-    wd[(i >> 1) + 1] = pack_bf16(sv[2], sv[3]);
+    const float2 p01 = make_float2(fast_exp2(x01.x), fast_exp2(x01.y));
+    const float2 p23 = make_float2(fast_exp2(x23.x), fast_exp2(x23.y));
+    const float2 dd01 = __fadd2_rn(make_float2(__uint_as_float(ud[i]), __uint_as_float(ud[i + 1])), make_float2(-d4.x, -d4.y));
+    const float2 dd23 =
+        __fadd2_rn(make_float2(__uint_as_float(ud[i + 2]), __uint_as_float(ud[i + 3])), make_float2(-d4.z, -d4.w));
+    const float2 s01 = __fmul2_rn(p01, dd01), s23 = __fmul2_rn(p23, dd23);
+    wp[i >> 1] = pack_bf16(p01.x, p01.y);
+    wp[(i >> 1) + 1] = pack_bf16(p23.x, p23.y);
+    wd[i >> 1] = pack_bf16(s01.x, s01.y);
+    wd[(i >> 1) + 1] = pack_bf16(s23.x, s23.y);
   }
+}
+
+// PARTIAL tile: column i of the chunk is visible iff it is a valid column (colmask) and key < e_i or bit i
+// of extra (diagonal / transposed pair)
+CADET_DEV void dkv_chunk_masked(const uint32_t (&us)[32], const uint32_t (&ud)[32], uint32_t vaddr, int key,
+                                uint32_t extra, uint32_t colmask, float sl2, uint32_t (&wp)[16], uint32_t (&wd)[16]) {
+  uint32_t vis = 0;
+#pragma unroll
+  for (int i = 0; i < 32; i += 4) {
+    const int4 e4 = lds_i4(vaddr + 1024 + i * 4);
+    vis |= (key < e4.x ? 1u : 0u) << i;
+    vis |= (key < e4.y ? 1u : 0u) << (i + 1);
+    vis |= (key < e4.z ? 1u : 0u) << (i + 2);
+    vis |= (key < e4.w ? 1u : 0u) << (i + 3);
+  }
+  vis = (vis | extra) & colmask;
+  dkv_chunk<true>(us, ud, vaddr, key, vis, sl2, wp, wd);
 }
 
 template <int HD>
@@ -366,18 +384,22 @@ struct DkvCfg {
   static constexpr int V_OFF = K_OFF + G::TILE_BYTES;
   static constexpr int Q_OFF = V_OFF + G::TILE_BYTES;          // two stages
   static constexpr int DO_OFF = Q_OFF + 2 * G::TILE_BYTES;     // two stages
-  static constexpr int VEC_OFF = DO_OFF + 2 * G::TILE_BYTES;   // [2 groups][2 bufs][256] x 4 B
-  static constexpr int STG_OFF = VEC_OFF + 2 * 2 * 256 * 4;    // [8 compute warps][2 KB] store transpose
+  // VSTAGES stages of one q-tile's column vectors, written by the vector-loader warp: LSE [128] f32 at +0,
+  // D [128] f32 at +512, kv_end [128] i32 at +1024, the visit-list entry at +1536
+  static constexpr int VSTAGES = 4;
+  static constexpr int VEC_OFF = DO_OFF + 2 * G::TILE_BYTES;
+  static constexpr int VEC_BYTES = 2048;
+  static constexpr int STG_OFF = VEC_OFF + VSTAGES * VEC_BYTES;  // [8 compute warps][2 KB] store transpose
   static constexpr int BAR_OFF = STG_OFF + 8 * 2048;
   static constexpr int SMEM = BAR_OFF + 256 + 1024;
   // S^T/P^T half-buffers at [0,64) and [64,128); dP^T/dS^T at [128,192) and [192,256)
   static constexpr int S_COL = 0, DP_COL = 128, DV_COL = 256, DK_COL = 384;
-  static constexpr int THREADS = 320;  // producer, MMA, 2 compute warpgroups (one per half-buffer)
+  static constexpr int THREADS = 352;  // producer, MMA, 2 compute warpgroups (one per half-buffer), vector loader
 };
 
 struct DkvBars {
   uint64_t kv_full, kv_empty, q_full[2], q_empty[2], do_full[2], do_empty[2], sdp_full[2], pds_ready[2], mma_done,
-      acc_free;
+      acc_free, vec_full[4], vec_empty[4];
   uint32_t tmem_base;
 };
 
@@ -401,7 +423,7 @@ CADET_DEV DkvWork dkv_work(const AttnParams& p, int w) {
 }
 
 template <int HD>
-__global__ void __launch_bounds__(320, 1)
+__global__ void __launch_bounds__(352, 1)
     attn_bwd_dkv_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constant__ CUtensorMap mK,
                         const __grid_constant__ CUtensorMap mV, const __grid_constant__ CUtensorMap mdO,
                         const AttnParams p) {
@@ -412,7 +434,6 @@ __global__ void __launch_bounds__(320, 1)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   DkvBars* bars = reinterpret_cast<DkvBars*>(smem + C::BAR_OFF);
-  float* vec = reinterpret_cast<float*>(smem + C::VEC_OFF);
   const uint32_t warp = warp_id(), lane = lane_id();
   if (threadIdx.x == 0) {
     mbar_init(&bars->kv_full, 1);
@@ -427,6 +448,10 @@ __global__ void __launch_bounds__(320, 1)
     }
     mbar_init(&bars->mma_done, 1);
     mbar_init(&bars->acc_free, 256);
+    for (int i = 0; i < 4; ++i) {
+      mbar_init(&bars->vec_full[i], 32);
+      mbar_init(&bars->vec_empty[i], 8);
+    }
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc<512>(&bars->tmem_base);
@@ -543,6 +568,38 @@ __global__ void __launch_bounds__(320, 1)
         gq += n_it;
       }
     }
+  } else if (warp == 10) {
+    // ============================ vector loader: per visited q-tile, LSE, D and kv_end of its 128 columns
+    // (coalesced, +inf / 0 / -1 past the sequence end) and the visit-list entry, VSTAGES q-tiles ahead
+    int g = 0;
+    for (int w = blockIdx.x; w < n_work; w += gridDim.x) {
+      const DkvWork t = dkv_work(p, w);
+      for (int it = 0; it < t.n_it; ++it, ++g) {
+        const int vs = g % C::VSTAGES, use = g / C::VSTAGES;
+        const int entry = list[t.off + it];
+        const int q0 = t.sa + (entry & 0xFFFF) * 128;
+        float lv[4], dv[4];
+        int ev[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int q = q0 + j * 32 + lane;
+          const bool v = q < t.se;
+          lv[j] = v ? p.lse[(size_t)t.h * p.T + q] : INFINITY;
+          dv[j] = v ? p.D[(size_t)t.h * p.T + q] : 0.f;
+          ev[j] = v ? p.plan.kv_end[q] : -1;
+        }
+        if (use > 0) mbar_wait(&bars->vec_empty[vs], (use - 1) & 1);
+        float* vb = reinterpret_cast<float*>(smem + C::VEC_OFF + vs * C::VEC_BYTES);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          vb[j * 32 + lane] = lv[j];
+          vb[128 + j * 32 + lane] = dv[j];
+          reinterpret_cast<int*>(vb)[256 + j * 32 + lane] = ev[j];
+        }
+        if (lane == 0) reinterpret_cast<int*>(vb)[384] = entry;
+        mbar_arrive(&bars->vec_full[vs]);
+      }
+    }
   } else {
     // warpgroup grp (warps 2..5 -> 0, 6..9 -> 1) owns TMEM half-buffer grp = q columns [64 grp, +64)
     const uint32_t quarter = warp & 3;
@@ -550,27 +607,10 @@ __global__ void __launch_bounds__(320, 1)
     const int tr = quarter * 32 + lane;
     const int gt = (threadIdx.x - 64) & 127;  // 0..127 inside the warpgroup
     const float sl2 = p.scale_log2;
-    const float LOG2E = 1.4426950408889634f;
-    float* vgrp = vec + grp * 2 * 256;
     const bool tracer = gt == 0;
-    float nl = 0.f, nd = 0.f;
-    int ne = -1, nent = 0;
-    // the group's first 64 threads load the 64 columns' vectors of iteration it of item u
-    auto fetch = [&](const DkvWork& u, int it) {
-      if (gt >= 64) return;
-      const int entry = list[u.off + it];
-      const int q = u.sa + (entry & 0xFFFF) * 128 + grp * 64 + gt;
-      const bool v = q < u.se;
-      nl = v ? p.lse[(size_t)u.h * p.T + q] : INFINITY;  // x log2e when staged (keeps the load asynchronous)
-      nd = v ? p.D[(size_t)u.h * p.T + q] : 0.f;
-      ne = v ? p.plan.kv_end[q] : -1;
-      nent = entry;
-    };
-    // items are decoded one ahead and the first iteration's vectors fetched during the previous
-    // item, so no dependent global-load chain sits at an item boundary
+    // items are decoded one ahead, so no dependent global-load chain sits at an item boundary
     DkvWork t = dkv_work(p, blockIdx.x < n_work ? blockIdx.x : 0);
     DkvWork tn = dkv_work(p, blockIdx.x + gridDim.x < n_work ? blockIdx.x + gridDim.x : 0);
-    if (blockIdx.x < n_work && t.n_it > 0) fetch(t, 0);
     int gq = 0;
     PT_DECL
     for (int w = blockIdx.x, wi = 0; w < n_work; w += gridDim.x, ++wi) {
@@ -582,27 +622,16 @@ __global__ void __launch_bounds__(320, 1)
       // query row key+1 carries the PAIR_PREV bit: then it sees this key (the transposed pair cell)
       const bool ppn = key_valid && key + 1 < t.se && p.plan.row_pp[key + 1] != 0;
       for (int it = 0; it < t.n_it; ++it) {
-        const int g = gq + it;
-        float* vb = vgrp + (g & 1) * 256;
-        if (gt < 64) {
-          vb[gt] = nl * LOG2E;
-          vb[64 + gt] = nd;
-          reinterpret_cast<int*>(vb)[128 + gt] = ne;
-          if (gt == 0) reinterpret_cast<int*>(vb)[192] = nent;
-        }
-        if (it + 1 < t.n_it)
-          fetch(t, it + 1);
-        else if (has_next && tn.n_it > 0)
-          fetch(tn, 0);
-        named_bar_sync(1 + grp, 128);
-        const int entry = reinterpret_cast<const int*>(vb)[192];
-        const bool full = (entry >> 30) & 1;
-        const int qbase = t.sa + (entry & 0xFFFF) * 128 + grp * 64;
+        const int g = gq + it, vs = g % C::VSTAGES;
+        const uint32_t vst = smem_u32(smem + C::VEC_OFF + vs * C::VEC_BYTES);
         PTM(tracer, 7)
+        mbar_wait(&bars->vec_full[vs], (g / C::VSTAGES) & 1);  // this q-tile's column vectors
         mbar_wait(&bars->sdp_full[grp], g & 1);
         tc_fence_after();
         PTM(tracer, 6)
-        const uint32_t vs = smem_u32(vb);
+        const int entry = *reinterpret_cast<const int*>(smem + C::VEC_OFF + vs * C::VEC_BYTES + 1536);
+        const bool full = (entry >> 30) & 1;
+        const int qbase = t.sa + (entry & 0xFFFF) * 128 + grp * 64;
         uint32_t wkeep[16];
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
@@ -610,16 +639,23 @@ __global__ void __launch_bounds__(320, 1)
           tmem_ld32(tmem_addr(tmem, quarter, C::S_COL + grp * 64 + c * 32), us);
           tmem_ld32(tmem_addr(tmem, quarter, C::DP_COL + grp * 64 + c * 32), ud);
           tmem_ld_wait();
+          PTM(tracer, 8)
           uint32_t wp[16], wd[16];
+          const uint32_t va = vst + (grp * 64 + c * 32) * 4;
           if (full) {
-            dkv_chunk<false>(us, ud, vs + c * 128, key, 0u, sl2, wp, wd);
+            dkv_chunk<false>(us, ud, va, key, 0u, sl2, wp, wd);
           } else {
-            // diagonal (key == q) and transposed pair (q == key + 1 with PAIR_PREV) columns of the chunk
-            const int dd = key - (qbase + c * 32);
+            // diagonal (key == q) and transposed pair (q == key + 1 with PAIR_PREV) columns of the chunk;
+            // columns past the sequence end (pad / next sequence rows of the stage) are never visible
+            const int q0c = qbase + c * 32;
+            const int dd = key - q0c;
             uint32_t extra = 0;
             if (key_valid && dd >= 0 && dd < 32) extra |= 1u << dd;
             if (ppn && dd + 1 >= 0 && dd + 1 < 32) extra |= 1u << (dd + 1);
-            dkv_chunk<true>(us, ud, vs + c * 128, key, extra, sl2, wp, wd);
+            const int nv = t.se - q0c;  // valid columns of the chunk
+            const uint32_t colmask = nv >= 32 ? 0xFFFFFFFFu : (nv <= 0 ? 0u : ((1u << nv) - 1u));
+            const uint32_t vis_key = key_valid ? 0xFFFFFFFFu : 0u;
+            dkv_chunk_masked(us, ud, va, key, extra, colmask & vis_key, sl2, wp, wd);
           }
           if (p.dS) {  // dS^T chunk 0 -> the warp's stage now, chunk 1 kept: both stored after the arrive
             if (c == 0)
@@ -628,6 +664,7 @@ __global__ void __launch_bounds__(320, 1)
 #pragma unroll
               for (int j = 0; j < 16; ++j) wkeep[j] = wd[j];
           }
+          PTM(tracer, 9)
           // P^T / dS^T chunk c -> columns [16c, 16c + 16) of this half: only this thread's own,
           // already-loaded S^T / dP^T chunk 0 is overwritten
           tmem_st16(tmem_addr(tmem, quarter, C::S_COL + grp * 64 + c * 16), wp);
@@ -636,6 +673,9 @@ __global__ void __launch_bounds__(320, 1)
         tmem_st_wait();
         tc_fence_before();
         mbar_arrive(&bars->pds_ready[grp]);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bars->vec_empty[vs]);  // the warp's vector reads are done
+        PTM(tracer, 10)
         if (p.dS) {  // two-pass backward: this warp's 32 keys x 64 q columns of dS^T, off the MMA's path
           const int qt = entry & 0xFFFF;
           const int slot = ds_base + qt * (qt + 1) / 2;
@@ -689,7 +729,6 @@ __global__ void __launch_bounds__(320, 1)
       mbar_arrive(&bars->acc_free);
       PTM(tracer, 5)
       gq += t.n_it;
-      if (has_next && t.n_it == 0 && tn.n_it > 0) fetch(tn, 0);
       t = tn;
       const int w2 = w + 2 * gridDim.x;
       if (w2 < n_work) tn = dkv_work(p, w2);
@@ -978,7 +1017,7 @@ cudaError_t attn_bwd_launch(const void* Qr, const void* Kr, const void* V, const
 
 #ifdef CADET_PHASE_TIMING
 extern "C" int cadet_debug_phase_read(unsigned long long* out, int n) {
-  if (n > 8192 * 8) n = 8192 * 8;
+  if (n > 8192 * 16) n = 8192 * 16;
   cudaMemcpyFromSymbol(out, cadet::g_phase, sizeof(unsigned long long) * n);
   return n;
 }
@@ -988,7 +1027,7 @@ extern "C" int cadet_debug_trace_read(unsigned long long* out, int n) {
   return n;
 }
 extern "C" int cadet_debug_phase_reset() {
-  static unsigned long long z[8192 * 8];
+  static unsigned long long z[8192 * 16];
   cudaMemcpyToSymbol(cadet::g_phase, z, sizeof(z));
   return 0;
 }

@@ -13,6 +13,9 @@
 //                conditional rescaling (threshold 2^8), tcgen05.st P, O rescale, final O / l, LSE.
 // ~96 KB of shared memory and 256 TMEM columns per CTA, so two CTAs share an SM and one CTA's
 // softmax overlaps the other's MMAs (the role FA4's two softmax warpgroups play).
+#include <algorithm>
+#include <cstdlib>
+
 #include "attn_common.cuh"
 #include "launch.cuh"
 #include "prof.cuh"
@@ -20,15 +23,28 @@
 namespace cadet {
 
 #ifdef CADET_PHASE_TIMING
-__device__ unsigned long long g_phase_fwd[8192][8];
+__device__ unsigned long long g_phase_fwd[8192][16];
 #define FT_MARK(slot)                                                              \
   if (lane == 0 && blockIdx.x < 8192) {                                             \
     unsigned long long _n = clock64();                                              \
     atomicAdd(&g_phase_fwd[blockIdx.x][slot], _n - _ft);                            \
     _ft = _n;                                                                       \
   }
+#define PP_DECL unsigned long long _pp = clock64(), _pacc[16] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+#define PP_MARK(slot)                    \
+  {                                      \
+    unsigned long long _n = clock64();   \
+    _pacc[slot] += _n - _pp;             \
+    _pp = _n;                            \
+  }
+#define PP_FLUSH(lo, hi)                                                                  \
+  if (blockIdx.x < 8192)                                                                  \
+    for (int _i = lo; _i < hi; ++_i) atomicAdd(&g_phase_fwd[blockIdx.x][_i], _pacc[_i]);
 #else
 #define FT_MARK(slot)
+#define PP_DECL
+#define PP_MARK(slot)
+#define PP_FLUSH(lo, hi)
 #endif
 
 template <int HD>
@@ -362,6 +378,448 @@ __global__ void __launch_bounds__(256) attn_fwd_merge_kernel(const AttnParams p)
   }
 }
 
+// ============================================================================ paired forward
+// A5 as one persistent CTA per SM over (q-tile pair, head) items (plan pair_list; dynamic work
+// counter, so the jagged items balance like the hardware's own CTA scheduling would).  An item is two
+// q-tiles of one sequence (qt, qt - 1) that share one K / V stream: the union of their visit lists,
+// each K / V tile loaded once for both.  Two softmax warpgroups, one per q-tile ("slot"), each with
+// its own S and O accumulators in TMEM (S0 S1 O0 O1 = 512 columns), so that the tensor core computes
+// one slot's S = Q K^T or O += P V while the other slot's softmax runs:
+//   warp 0     : producer (work counter, item ring, Q per slot, K / V ring of STAGES)
+//   warp 1     : TMEM owner + MMA issuer; per union tile u: PV of each slot's previous tile, then
+//                S of the slots that see u (PV_s(prev) precedes S_s(u): P aliases S)
+//   warps 4..7 : softmax of slot 0;  warps 8..11 : slot 1 (thread = query row): full S row in
+//                registers, mask, conditional rescale (threshold 2^8), exp2 (a fraction on the FMA
+//                pipe, exp2_poly3), P as packed bf16 over the row's S columns; item end: O / l, LSE.
+template <int HD>
+struct PairCfg {
+  using G = HeadGeom<HD>;
+  static constexpr int STAGES = HD <= 64 ? 3 : 2;
+  static constexpr int Q_OFF = 0;                                   // 2 slots
+  static constexpr int K_OFF = Q_OFF + 2 * G::TILE_BYTES;           // STAGES
+  static constexpr int V_OFF = K_OFF + STAGES * G::TILE_BYTES;      // STAGES
+  static constexpr int STG_OFF = V_OFF + STAGES * G::TILE_BYTES;    // [8 softmax warps][2 KB] O store transpose
+  static constexpr int BAR_OFF = STG_OFF + 8 * 2048;
+  // at least 116 KB: one CTA per SM (the 512 TMEM columns are the whole SM's)
+  static constexpr int SMEM = (BAR_OFF + 1024 + 1024) > 118784 ? (BAR_OFF + 1024 + 1024) : 118784;
+  static constexpr int THREADS = 384;
+  static constexpr int RING = 4;  // item ring entries
+};
+
+struct PairItem {  // one decoded work item (the producer writes it into the ring)
+  int w, h, sa, se, nslot, pad[3];
+  QTileInfo qi[2];
+};
+struct PairBars {
+  uint64_t q_full[2], q_empty[2], s_full[2], p_full[2], o_full[2], o_free[2];
+  uint64_t k_full[3], k_empty[3], v_full[3], v_empty[3];
+  uint64_t item_full[4], item_empty[4];
+  uint32_t tmem_base;
+  PairItem item[4];
+};
+static_assert(sizeof(PairBars) <= 1024, "pair kernel barrier block");
+CADET_DEV void pair_item(const AttnParams& p, int w, PairItem& t) {
+  t.w = w;
+  if (w < 0) return;
+  t.h = w % p.H;
+  const int g = p.plan.pair_list[w / p.H];
+  t.qi[0] = p.plan.qinfo[g];
+  t.nslot = t.qi[0].qt >= 1 ? 2 : 1;
+  t.qi[1] = t.nslot == 2 ? p.plan.qinfo[g - 1] : t.qi[0];
+  t.sa = p.cu[t.qi[0].seq];
+  t.se = p.cu[t.qi[0].seq + 1];
+}
+CADET_DEV bool tile_sees(const QTileInfo& qi, int kt) { return kt < qi.nf || (kt >= qi.kt2 && kt <= qi.qt); }
+// next visited k-tile of the slot (or of the union) at or after kt; > qt when none is left
+CADET_DEV int next_seen(const QTileInfo& qi, int kt) { return kt < qi.nf ? kt : max(kt, qi.kt2); }
+
+// 2^x for two cells at once on the FMA / ALU pipes (FA4-style MUFU offload): n = rint(x) (1.5 * 2^23
+// trick), 2^f on [-1/2, 1/2] by a degree-3 relative-minimax polynomial (max rel err 7.5e-5, far below
+// the bf16 rounding of P), n added to the exponent field.  x < -126 (incl. -inf: masked cells) gives
+// exactly 0 like ex2.approx.ftz.  Packed f32x2 FADD / FFMA (sm_100) for the float arithmetic.
+CADET_DEV float2 exp2_poly3x2(float2 x) {
+  const float2 xc = make_float2(fmaxf(x.x, -127.f), fmaxf(x.y, -127.f));
+  const float2 magic = make_float2(12582912.f, 12582912.f);
+  const float2 t = __fadd2_rn(xc, magic);
+  const float2 f = __fadd2_rn(xc, __fadd2_rn(magic, make_float2(-t.x, -t.y)));
+  float2 q = __ffma2_rn(make_float2(0.05516947f, 0.05516947f), f, make_float2(0.24260798f, 0.24260798f));
+  q = __ffma2_rn(q, f, make_float2(0.69326111f, 0.69326111f));
+  q = __ffma2_rn(q, f, make_float2(0.99992828f, 0.99992828f));
+  const float r0 = __int_as_float(__float_as_int(q.x) + (__float_as_int(t.x) << 23));
+  const float r1 = __int_as_float(__float_as_int(q.y) + (__float_as_int(t.y) << 23));
+  return make_float2(x.x < -126.f ? 0.f : r0, x.y < -126.f ? 0.f : r1);
+}
+
+template <int HD, int NPOLY>
+__global__ void __launch_bounds__(384, 1)
+    attn_fwd_pair_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constant__ CUtensorMap mK,
+                         const __grid_constant__ CUtensorMap mV, const AttnParams p) {
+  using G = HeadGeom<HD>;
+  using C = PairCfg<HD>;
+  constexpr int ST = C::STAGES;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  PairBars* bars = reinterpret_cast<PairBars*>(smem + C::BAR_OFF);
+  const uint32_t warp = warp_id(), lane = lane_id();
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&bars->q_full[s], 1);
+      mbar_init(&bars->q_empty[s], 1);
+      mbar_init(&bars->s_full[s], 1);
+      mbar_init(&bars->p_full[s], 128);
+      mbar_init(&bars->o_full[s], 1);
+      mbar_init(&bars->o_free[s], 128);
+    }
+    for (int i = 0; i < ST; ++i) {
+      mbar_init(&bars->k_full[i], 1);
+      mbar_init(&bars->k_empty[i], 1);
+      mbar_init(&bars->v_full[i], 1);
+      mbar_init(&bars->v_empty[i], 1);
+    }
+    for (int i = 0; i < C::RING; ++i) {
+      mbar_init(&bars->item_full[i], 1);
+      mbar_init(&bars->item_empty[i], 2 + 8);  // producer, MMA thread, lane 0 of each softmax warp
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc<512>(&bars->tmem_base);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = bars->tmem_base;
+  pdl_trigger();  // after the TMEM allocation
+  pdl_wait();     // every role reads the previous kernels' outputs (plan, Q / K / V)
+  const int n_items = p.plan.counters[2] * p.H;
+
+  // registers: warpgroup 0 (producer, MMA, 2 idle warps) gives 112 per thread to the softmax warpgroups
+  if (warp == 0) {
+    // ============================ producer
+    setmaxnreg_dec<56>();
+    if (elect_one()) {
+      int u = 0, nq[2] = {0, 0};
+      for (int it = 0;; ++it) {
+        const int r = it % C::RING;
+        mbar_wait(&bars->item_full[r], (it / C::RING) & 1);
+        const PairItem t = bars->item[r];
+        mbar_arrive(&bars->item_empty[r]);
+        if (t.w < 0) break;
+#pragma unroll
+        for (int s = 0; s < 2; ++s) {
+          if (s >= t.nslot) continue;
+          if (nq[s] > 0) mbar_wait(&bars->q_empty[s], (nq[s] - 1) & 1);
+          ++nq[s];
+          mbar_expect_tx(&bars->q_full[s], G::TILE_BYTES);
+#pragma unroll
+          for (int blk = 0; blk < G::NB; ++blk)
+            tma_load_3d(smem + C::Q_OFF + s * G::TILE_BYTES + blk * G::BLK, &mQ, &bars->q_full[s], blk * G::CB, t.h,
+                        t.sa + t.qi[s].qt * 128);
+        }
+        const int qtA = t.qi[0].qt;
+        for (int kt = 0; kt <= qtA; ++kt) {
+          const bool a = tile_sees(t.qi[0], kt), b = t.nslot == 2 && tile_sees(t.qi[1], kt);
+          if (!a && !b) continue;
+          const int stg = u % ST, use = u / ST;
+          const int krow = t.sa + kt * 128;
+          if (use > 0) mbar_wait(&bars->k_empty[stg], (use - 1) & 1);
+          mbar_expect_tx(&bars->k_full[stg], G::TILE_BYTES);
+#pragma unroll
+          for (int blk = 0; blk < G::NB; ++blk)
+            tma_load_3d(smem + C::K_OFF + stg * G::TILE_BYTES + blk * G::BLK, &mK, &bars->k_full[stg], blk * G::CB,
+                        t.h, krow);
+          if (use > 0) mbar_wait(&bars->v_empty[stg], (use - 1) & 1);
+          mbar_expect_tx(&bars->v_full[stg], G::TILE_BYTES);
+#pragma unroll
+          for (int blk = 0; blk < G::NB; ++blk)
+            tma_load_3d(smem + C::V_OFF + stg * G::TILE_BYTES + blk * G::BLK, &mV, &bars->v_full[stg], blk * G::CB,
+                        t.h, krow);
+          ++u;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ============================ MMA issuer
+    setmaxnreg_dec<56>();
+    if (elect_one()) {
+      const uint32_t idesc_s = idesc_bf16(128, 128, 0, 0);
+      const uint32_t idesc_o = idesc_bf16(128, G::HDP, 0, 1);
+      int u = 0;
+      int nq[2] = {0, 0};     // items per slot (q_full parity, o_free parity)
+      int npv[2] = {0, 0};    // PVs issued per slot (p_full parity)
+      int pend_u[2] = {-1, -1};   // union tile of the slot's S whose PV is not issued yet
+      bool pend_first[2] = {false, false};
+      int vleft[3] = {0, 0, 0};  // PVs still to issue per V stage
+      PP_DECL
+      auto issue_pv = [&](int s) {
+        const int pu = pend_u[s];
+        const int stg = pu % ST;
+        PP_MARK(4)
+        mbar_wait(&bars->p_full[s], npv[s] & 1);
+        PP_MARK(2)
+        if (pend_first[s] && nq[s] > 1) mbar_wait(&bars->o_free[s], (nq[s] - 2) & 1);
+        mbar_wait(&bars->v_full[stg], (pu / ST) & 1);
+        PP_MARK(3)
+        tc_fence_after();
+        const uint32_t sV = smem_u32(smem + C::V_OFF + stg * G::TILE_BYTES);
+#pragma unroll
+        for (int kk = 0; kk < 128 / 16; ++kk)
+          mma_bf16_ts(tmem + 256 + s * 128, tmem + s * 128 + kk * 8, mnmajor_desc<HD>(sV, kk), idesc_o,
+                      (!pend_first[s] || kk > 0) ? 1u : 0u);
+        ++npv[s];
+        pend_u[s] = -1;
+        int left = 0;
+#pragma unroll
+        for (int i = 0; i < ST; ++i)
+          if (i == stg) left = --vleft[i];
+        if (left == 0) mma_commit(&bars->v_empty[stg]);
+      };
+      for (int it = 0;; ++it) {
+        const int r = it % C::RING;
+        PP_MARK(4)
+        mbar_wait(&bars->item_full[r], (it / C::RING) & 1);
+        PP_MARK(0)
+        const PairItem t = bars->item[r];
+        mbar_arrive(&bars->item_empty[r]);
+        if (t.w < 0) break;
+        bool first[2] = {true, true};
+        int last[2];
+#pragma unroll
+        for (int s = 0; s < 2; ++s) {
+          if (s < t.nslot) ++nq[s];
+          last[s] = t.qi[s].qt;  // the diagonal tile is always the slot's last
+        }
+        const int qtA = t.qi[0].qt;
+        for (int kt = 0; kt <= qtA; ++kt) {
+          const bool sees[2] = {tile_sees(t.qi[0], kt), t.nslot == 2 && tile_sees(t.qi[1], kt)};
+          if (!sees[0] && !sees[1]) continue;
+          const int stg = u % ST;
+          PP_MARK(4)
+          mbar_wait(&bars->k_full[stg], (u / ST) & 1);
+          PP_MARK(1)
+#pragma unroll
+          for (int i = 0; i < ST; ++i)
+            if (i == stg) vleft[i] = (int)sees[0] + (int)sees[1];
+#pragma unroll
+          for (int s = 0; s < 2; ++s) {
+            if (pend_u[s] >= 0) issue_pv(s);
+            if (!sees[s]) continue;
+            if (first[s]) {
+              PP_MARK(4)
+              mbar_wait(&bars->q_full[s], (nq[s] - 1) & 1);
+              PP_MARK(1)
+            }
+            tc_fence_after();
+            const uint32_t sQ = smem_u32(smem + C::Q_OFF + s * G::TILE_BYTES);
+            const uint32_t sK = smem_u32(smem + C::K_OFF + stg * G::TILE_BYTES);
+#pragma unroll
+            for (int kk = 0; kk < G::HDP / 16; ++kk)
+              mma_bf16_ss(tmem + s * 128, kmajor_desc<HD>(sQ, kk), kmajor_desc<HD>(sK, kk), idesc_s, kk > 0 ? 1u : 0u);
+            mma_commit(&bars->s_full[s]);
+            if (kt == last[s]) mma_commit(&bars->q_empty[s]);
+            pend_u[s] = u;
+            pend_first[s] = first[s];
+            first[s] = false;
+          }
+          mma_commit(&bars->k_empty[stg]);
+          ++u;
+        }
+        // the item's last PVs, then its O accumulators are complete
+#pragma unroll
+        for (int s = 0; s < 2; ++s) {
+          if (s >= t.nslot) continue;
+          if (pend_u[s] >= 0) issue_pv(s);
+          mma_commit(&bars->o_full[s]);
+        }
+      }
+      PP_FLUSH(0, 5)
+    }
+  } else if (warp == 2) {
+    // ============================ scheduler: claims items (dynamic counter) and decodes them into the
+    // ring up to RING items ahead, so no role waits on the atomic or the plan loads at an item boundary
+    setmaxnreg_dec<56>();
+    if (elect_one()) {
+      for (int it = 0;; ++it) {
+        int w = atomicAdd(&p.plan.counters[4], 1);
+        if (w >= n_items) w = -1;
+        PairItem t;
+        pair_item(p, w, t);
+        const int r = it % C::RING;
+        if (it >= C::RING) mbar_wait(&bars->item_empty[r], ((it / C::RING) - 1) & 1);
+        bars->item[r] = t;
+        mbar_arrive(&bars->item_full[r]);
+        if (w < 0) break;
+      }
+    }
+  } else if (warp < 4) {
+    setmaxnreg_dec<56>();
+  } else {
+    // ============================ softmax warpgroups
+    setmaxnreg_inc<224>();
+    const int s = (warp - 4) >> 2;
+    const uint32_t quarter = warp & 3;
+    const int rt = quarter * 32 + lane;
+    const float sl2 = p.scale_log2;
+    const uint32_t tS = tmem_addr(tmem, quarter, s * 128);
+    const uint32_t tO = tmem_addr(tmem, quarter, 256 + s * 128);
+    const uint32_t stg = smem_u32(smem + C::STG_OFF + (warp - 4) * 2048);
+    int nt = 0, ni = 0;  // tiles / items of this slot so far
+    PP_DECL
+    for (int it = 0;; ++it) {
+      const int r = it % C::RING;
+      mbar_wait(&bars->item_full[r], (it / C::RING) & 1);
+      const PairItem& ti = bars->item[r];
+      const int w = ti.w, h = ti.h, sa = ti.sa, se = ti.se, nslot = ti.nslot;
+      const QTileInfo qi = ti.qi[s];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bars->item_empty[r]);
+      if (w < 0) break;
+      if (s >= nslot) continue;
+      const int q0 = sa + qi.qt * 128;
+      const int rows_valid = min(128, se - q0);
+      const int row = q0 + rt;
+      const bool valid = rt < rows_valid;
+      const int e_r = valid ? p.plan.kv_end[row] : 0;
+      const bool pp = valid ? (p.plan.row_pp[row] != 0) : false;
+      float m_used = -INFINITY, l = 0.f;
+      int j = 0;
+      for (int kt = next_seen(qi, 0); kt <= qi.qt; kt = next_seen(qi, kt + 1), ++j, ++nt) {
+        const int k0 = sa + kt * 128;
+        PP_MARK(7)
+        mbar_wait(&bars->s_full[s], nt & 1);
+        PP_MARK(5)
+        tc_fence_after();
+        uint32_t sv[128];
+        tmem_ld32(tS, *reinterpret_cast<uint32_t(*)[32]>(&sv[0]));
+        tmem_ld32(tS + 32, *reinterpret_cast<uint32_t(*)[32]>(&sv[32]));
+        tmem_ld32(tS + 64, *reinterpret_cast<uint32_t(*)[32]>(&sv[64]));
+        tmem_ld32(tS + 96, *reinterpret_cast<uint32_t(*)[32]>(&sv[96]));
+        tmem_ld_wait();
+        PP_MARK(8)
+        if (!valid || e_r < k0 + 128) {  // PARTIAL row: mask the cells outside its visible set
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const uint32_t m = valid ? row_mask32(e_r, row, pp, k0 + c * 32) : 0u;
+#pragma unroll
+            for (int q = 0; q < 32; ++q)
+              if (!((m >> q) & 1u)) sv[c * 32 + q] = __float_as_uint(-INFINITY);
+          }
+        }
+        float mx0 = -INFINITY, mx1 = -INFINITY, mx2 = -INFINITY, mx3 = -INFINITY;
+#pragma unroll
+        for (int q = 0; q < 128; q += 8) {
+          mx0 = fmaxf(mx0, fmaxf(__uint_as_float(sv[q]), __uint_as_float(sv[q + 1])));
+          mx1 = fmaxf(mx1, fmaxf(__uint_as_float(sv[q + 2]), __uint_as_float(sv[q + 3])));
+          mx2 = fmaxf(mx2, fmaxf(__uint_as_float(sv[q + 4]), __uint_as_float(sv[q + 5])));
+          mx3 = fmaxf(mx3, fmaxf(__uint_as_float(sv[q + 6]), __uint_as_float(sv[q + 7])));
+        }
+        const float mx_s = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3)) * sl2;
+        PP_MARK(9)
+        float factor = 1.f;
+        bool rescale = false;
+        if (mx_s > m_used + 8.f) {  // conditional rescale (also the first finite max)
+          factor = (m_used == -INFINITY) ? 0.f : fast_exp2(m_used - mx_s);
+          m_used = mx_s;
+          rescale = true;
+        }
+        const float base = (m_used == -INFINITY) ? 0.f : m_used;
+        const float2 sl2v = make_float2(sl2, sl2), nbase = make_float2(-base, -base);
+        float2 rs0 = make_float2(0.f, 0.f), rs1 = make_float2(0.f, 0.f);
+        // P packed in place: word q / 2 of sv takes cells q, q + 1 (both already consumed); each 64-cell
+        // half is stored as soon as it is packed, so the first STTM overlaps the second half's math
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+#pragma unroll
+          for (int q = hh * 64; q < hh * 64 + 64; q += 4) {
+            const float2 x01 = __ffma2_rn(make_float2(__uint_as_float(sv[q]), __uint_as_float(sv[q + 1])), sl2v, nbase);
+            const float2 x23 =
+                __ffma2_rn(make_float2(__uint_as_float(sv[q + 2]), __uint_as_float(sv[q + 3])), sl2v, nbase);
+            // NPOLY of every 16 cells on the FMA pipe (MUFU offload), in pairs
+            float2 p01, p23;
+            if ((q & 15) + 2 > 16 - NPOLY) p01 = exp2_poly3x2(x01);
+            else p01 = make_float2(fast_exp2(x01.x), fast_exp2(x01.y));
+            if ((q & 15) + 4 > 16 - NPOLY) p23 = exp2_poly3x2(x23);
+            else p23 = make_float2(fast_exp2(x23.x), fast_exp2(x23.y));
+            rs0 = __fadd2_rn(rs0, p01);
+            rs1 = __fadd2_rn(rs1, p23);
+            sv[q >> 1] = pack_bf16(p01.x, p01.y);  // F2FP: not on the MUFU pipe (scripts/pipe_bench.cu)
+            sv[(q >> 1) + 1] = pack_bf16(p23.x, p23.y);
+          }
+          tmem_st32(tS + hh * 32, *reinterpret_cast<uint32_t(*)[32]>(&sv[hh * 32]));
+        }
+        PP_MARK(10)
+        // O rescale after the S row is dead (registers); s_full(j) was committed after PV(j - 1), so O
+        // holds every earlier tile's product, and PV(j) waits for p_full(j) below
+        if (j > 0 && __any_sync(0xffffffffu, rescale)) {
+          const float f = rescale ? factor : 1.f;
+#pragma unroll
+          for (int c = 0; c < G::HDP / 32; ++c) {
+            uint32_t o[32];
+            tmem_ld32(tO + c * 32, o);
+            tmem_ld_wait();
+#pragma unroll
+            for (int q = 0; q < 32; ++q) o[q] = __float_as_uint(__uint_as_float(o[q]) * f);
+            tmem_st32(tO + c * 32, o);
+          }
+        }
+        tmem_st_wait();
+        tc_fence_before();
+        mbar_arrive(&bars->p_full[s]);
+        PP_MARK(11)
+        l = l * factor + ((rs0.x + rs1.x) + (rs0.y + rs1.y));
+      }
+      // ---- item end: O / l (bf16 rows through the warp's staging transpose, or fp32), LSE
+      PP_MARK(7)
+      mbar_wait(&bars->o_full[s], ni & 1);
+      PP_MARK(12)
+      tc_fence_after();
+      const float inv_l = (l > 0.f) ? 1.f / l : 0.f;
+      {
+        uint32_t o[G::HDP];  // the whole O row in registers, then the accumulator is released at once
+#pragma unroll
+        for (int c = 0; c < G::HDP / 32; ++c) tmem_ld32(tO + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&o[c * 32]));
+        tmem_ld_wait();
+        tc_fence_before();
+        mbar_arrive(&bars->o_free[s]);
+#pragma unroll
+        for (int c = 0; c < G::HDP / 32; ++c) {
+          const int ncol = min(32, p.hd - c * 32);
+          if (!p.out_f32) {
+            uint32_t wv[16];
+#pragma unroll
+            for (int q = 0; q < 16; ++q)
+              wv[q] = pack_bf16(__uint_as_float(o[c * 32 + 2 * q]) * inv_l, __uint_as_float(o[c * 32 + 2 * q + 1]) * inv_l);
+            warp_store_rows_bf16(stg, wv,
+                                 reinterpret_cast<__nv_bfloat16*>(p.O) + (size_t)(q0 + quarter * 32) * p.d +
+                                     (size_t)h * p.hd + c * 32,
+                                 p.d, rows_valid - (int)quarter * 32, ncol);
+          } else if (valid) {
+            float* dst = reinterpret_cast<float*>(p.O) + (size_t)row * p.d + (size_t)h * p.hd + c * 32;
+            for (int q = 0; q < ncol; q += 4)
+              *reinterpret_cast<float4*>(dst + q) =
+                  make_float4(__uint_as_float(o[c * 32 + q]) * inv_l, __uint_as_float(o[c * 32 + q + 1]) * inv_l,
+                              __uint_as_float(o[c * 32 + q + 2]) * inv_l, __uint_as_float(o[c * 32 + q + 3]) * inv_l);
+          }
+        }
+      }
+      if (valid) p.lse[(size_t)h * p.T + row] = (l > 0.f) ? (m_used + __log2f(l)) * 0.6931471805599453f : 0.f;
+      PP_MARK(13)
+      ++ni;
+    }
+    if (threadIdx.x == 128) { PP_FLUSH(5, 16) }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 1) tmem_dealloc<512>(tmem);
+  if (threadIdx.x == 0) {  // the last CTA out resets the work counters for the next launch on this plan
+    __threadfence();
+    if (atomicAdd(&p.plan.counters[5], 1) == (int)gridDim.x - 1) {
+      p.plan.counters[4] = 0;
+      p.plan.counters[5] = 0;
+      __threadfence();
+    }
+  }
+}
+
 // ---------------------------------------------------------------- host
 bool make_head_map(CUtensorMap* m, const void* ptr, int T, int H, int hd);  // attn_host (below)
 
@@ -373,6 +831,16 @@ bool make_head_map(CUtensorMap* m, const void* ptr, int T, int H, int hd) {
   uint32_t box[3] = {(uint32_t)(RB / 2), 1, 128};
   return encode_bf16_map(m, ptr, 3, dims, strides, box,
                          RB == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B);
+}
+
+#ifndef FWD_NPOLY
+#define FWD_NPOLY 5
+#endif
+// The paired persistent kernel is opt-in (CADET_FWD_PAIRED=1): same-box A/B on C4 measured it slower
+// than the one-q-tile-per-CTA kernel (0.321 vs 0.305 ms, round 2).
+static bool pair_disabled() {
+  const char* e = getenv("CADET_FWD_PAIRED");
+  return !(e && e[0] == '1');
 }
 
 template <int HD>
@@ -387,6 +855,30 @@ static cudaError_t fwd_hd(const CUtensorMap& mQ, const CUtensorMap& mK, const CU
   }
   const int grid = p.plan.nq_cap * p.H * p.fwd_splits;
   if (grid == 0) return cudaSuccess;
+  if (p.fwd_splits == 1 && !pair_disabled()) {  // persistent paired kernel, one CTA per SM
+    using PC = PairCfg<HD>;
+    constexpr int NPOLY = FWD_NPOLY;
+    static bool pattr = false;
+    if (!pattr) {
+      cudaError_t e = cudaFuncSetAttribute(attn_fwd_pair_kernel<HD, NPOLY>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           PC::SMEM);
+      if (e != cudaSuccess) return e;
+      pattr = true;
+    }
+    static int sms = 0;
+    if (!sms) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    // pairs <= (nq_cap + n) / 2 + n; the kernel reads the exact count from the plan
+    const int items_cap = ((p.plan.nq_cap + 1) / 2 + p.n) * p.H;
+    ProfScope ps(PROF_ATTN_FWD, st, 1);
+    cudaError_t e = launch_pdl(attn_fwd_pair_kernel<HD, NPOLY>, dim3(std::min(sms, std::max(items_cap, 1))),
+                               dim3(PC::THREADS), PC::SMEM, st, mQ, mK, mV, p);
+    if (e != cudaSuccess) return e;
+    return cudaGetLastError();
+  }
   ProfScope ps(PROF_ATTN_FWD, st, p.fwd_splits > 1 ? 2 : 1);
   cudaError_t e = launch_pdl(attn_fwd_kernel<HD>, grid, 192, C::SMEM, st, mQ, mK, mV, p);
   if (e != cudaSuccess) return e;
@@ -416,7 +908,7 @@ extern "C" int cadet_debug_phase_read_fwd(unsigned long long* out, int n) {
   return n;
 }
 extern "C" int cadet_debug_phase_reset_fwd() {
-  static unsigned long long z[8192 * 8];
+  static unsigned long long z[8192 * 16];
   cudaMemcpyToSymbol(cadet::g_phase_fwd, z, sizeof(z));
   return 0;
 }

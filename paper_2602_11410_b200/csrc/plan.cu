@@ -38,6 +38,7 @@ size_t plan_bytes(int32_t n, int32_t T, int32_t max_seqlen) {
   b += align256(nq * 4) * 2;
   b += align256(list_cap_of(nq, hm) * 4);
   b += align256((size_t)(n + 1) * 4);       // seq_rank
+  b += align256(nq * 4);                    // pair_list
   b += align256(64 * sizeof(float2));       // RoPE theta (hi, lo)
   b += align256((size_t)T * sizeof(float2));  // per-row rebased time (hi, lo)
   return b;
@@ -71,6 +72,7 @@ PlanView plan_carve(void* ws, int32_t n, int32_t T, int32_t max_seqlen) {
   v.bwd_cnt = reinterpret_cast<int32_t*>(take((size_t)v.nq_cap * 4));
   v.bwd_list = reinterpret_cast<int32_t*>(take(list_cap_of(v.nq_cap, v.hmax) * 4));
   v.seq_rank = reinterpret_cast<int32_t*>(take((size_t)(n + 1) * 4));
+  v.pair_list = reinterpret_cast<int32_t*>(take((size_t)v.nq_cap * 4));
   v.theta = reinterpret_cast<float2*>(take(64 * sizeof(float2)));
   v.rope_dt = reinterpret_cast<float2*>(take((size_t)T * sizeof(float2)));
   return v;
@@ -154,6 +156,9 @@ __global__ void __launch_bounds__(1024) plan_seq_kernel(PlanArgs a, PlanView v) 
     v.tc_off[a.n] = tot_tc;
     v.counters[0] = (int32_t)min(tot_nq, (long long)v.nq_cap);
     v.counters[1] = a.n;
+    v.counters[2] = 0;
+    v.counters[4] = 0;  // pair-forward work counter / done counter
+    v.counters[5] = 0;
     *v.pairs = 0ull;
   }
   for (int i = tid; i < 3 * v.hmax; i += nt) v.hist[i] = 0;
@@ -310,17 +315,22 @@ __global__ void __launch_bounds__(1024) plan_order_kernel(PlanView v) {
   pdl_wait();
   __shared__ long long sh[1024];
   const int tid = threadIdx.x, nt = blockDim.x;
-  for (int which = 0; which < 2; ++which) {
+  // which = 2: the per-bucket sequence counts (rank counters, no longer needed after plan_tile) become
+  // the bucket's first forward pair: sequences of b tiles contribute ceil(b / 2) pairs each
+  for (int which = 0; which < 3; ++which) {
     int* h = v.hist + which * v.hmax;
     const int per = (v.hmax + nt - 1) / nt;
+    auto wgt = [&](int b) { return which == 2 ? (b + 1) / 2 : 1; };
     // thread t owns reversed positions [t*per, (t+1)*per): cost c = hmax-1-pos
     long long local = 0;
-    for (int q = tid * per; q < min((tid + 1) * per, v.hmax); ++q) local += h[v.hmax - 1 - q];
+    for (int q = tid * per; q < min((tid + 1) * per, v.hmax); ++q)
+      local += (long long)h[v.hmax - 1 - q] * wgt(v.hmax - 1 - q);
     long long total;
     long long pre = block_exclusive_scan<long long>(local, sh, total);
+    if (which == 2 && tid == 0) v.counters[2] = (int)total;
     int vals[64];
     const int cnt = max(0, min((tid + 1) * per, v.hmax) - tid * per);
-    for (int q = 0; q < cnt && q < 64; ++q) vals[q] = h[v.hmax - 1 - (tid * per + q)];
+    for (int q = 0; q < cnt && q < 64; ++q) vals[q] = h[v.hmax - 1 - (tid * per + q)] * wgt(v.hmax - 1 - (tid * per + q));
     __syncthreads();
     for (int q = 0; q < cnt && q < 64; ++q) {
       h[v.hmax - 1 - (tid * per + q)] = (int)pre;
@@ -350,6 +360,12 @@ __global__ void __launch_bounds__(128) plan_scatter_kernel(PlanArgs a, PlanView 
   if (seq0 + lb <= v.nq_cap) {
     v.fwd_order[seq0 + (lb - 1 - info.qt)] = g;
     v.bwd_order[seq0 + info.qt] = g;
+  }
+  // forward pairs: the sequence's q-tiles from the last down, two at a time (a lone tile 0 at the end)
+  const int rel = lb - 1 - info.qt;
+  if (rel >= 0 && (rel & 1) == 0) {
+    const int pi = v.hist[2 * v.hmax + lb] + v.seq_rank[info.seq] * ((lb + 1) / 2) + rel / 2;
+    if (pi < v.nq_cap) v.pair_list[pi] = g;
   }
   // visit list of g as a k-tile (transpose of the forward visit rule): q-tiles qt >= kt of the
   // sequence with kt < nf(qt) or kt2(qt) <= kt <= qt; slots [base, base + nq_s - kt) of the

@@ -37,6 +37,10 @@ struct PlanView {   // device pointers into the workspace
   int32_t* bwd_cnt;   // [nq_cap] its length
   int32_t* bwd_list;  // [list_cap] q-tiles visiting k-tile g: qt | FULL << 30 (all cells visible)
   int32_t* seq_rank;  // [n] rank of a sequence among those with the same tile count (bwd order)
+  int32_t* pair_list; // [nq_cap] forward work items: q-tile g (descending inside its sequence) paired with
+                      // tile g - 1 of the same sequence when qt(g) >= 1; sequence-major like fwd_order.
+                      // counters[2] = number of pairs; counters[4..5] = the pair kernel's dynamic work
+                      // counter and done counter (zeroed by the plan, reset by the kernel's last CTA)
   float2* theta;      // [64] RoPE theta_i as (hi, lo) floats, i < head_dim / 2
   float2* rope_dt;    // [T] t_row - t_(sequence start) as exact (hi, lo) floats (0 for pad rows)
   int32_t nq_cap, hmax, list_cap;

@@ -14,7 +14,7 @@ lib_dbg = os.path.join(B.HERE, "libcadet_dbg.so")
 objs = []
 for src in B.sources():
     obj = os.path.join(B.HERE, "build", os.path.basename(src) + ".dbg.o")
-    subprocess.check_call(["nvcc", *B.FLAGS, "-DCADET_PHASE_TIMING", "-c", src, "-o", obj])
+    subprocess.check_call(["nvcc", *B.FLAGS, "-DCADET_PHASE_TIMING", *os.environ.get("PHASE_FLAGS", "").split(), "-c", src, "-o", obj])
     objs.append(obj)
 subprocess.check_call(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-shared", *objs, "-o", lib_dbg, "-lcudart"])
 from paper_2602_11410_b200 import _lib  # noqa: E402
@@ -34,21 +34,27 @@ L.cadet_debug_phase_reset()
 L.cadet_debug_phase_reset_fwd()
 st.step(inp)
 torch.cuda.synchronize()
-buf = (C.c_ulonglong * (8192 * 8))()
-L.cadet_debug_phase_read(buf, 8192 * 8)
-a = np.frombuffer(buf, dtype=np.uint64).reshape(8192, 8).astype(np.float64)
+buf = (C.c_ulonglong * (8192 * 16))()
+L.cadet_debug_phase_read(buf, 8192 * 16)
+a = np.frombuffer(buf, dtype=np.uint64).reshape(8192, 16).astype(np.float64)
 used = a[a.sum(1) > 0]
-names = ["mma: kv wait", "mma: q_full wait", "mma: S+dP issue", "mma: pds wait", "cmp: s/dp wait",
-         "cmp: compute", "cmp: bar+store", "mma: tail"]
+names = ["mma: kv wait", "mma: acc_free wait", "mma: pds wait", "mma: issue", "cmp x2: mma_done wait",
+         "cmp x2: dK/dV drain", "cmp x2: vec+sdp wait", "cmp x2: dS store+loop", "cmp x2: ldtm", "cmp x2: math",
+         "cmp x2: sttm+arrive", "-", "-", "-", "-", "-"]
 print("CTAs", len(used))
 for i, n in enumerate(names):
-    print(f"{n:18s} mean per CTA {used[:, i].mean():12.0f} clk   total share {used[:, i].sum() / used[:, [0,1,2,3,7]].sum():.3f}")
+    print(f"{n:22s} mean per CTA {used[:, i].mean():12.0f} clk")
 
-L.cadet_debug_phase_read_fwd(buf, 8192 * 8)
-a = np.frombuffer(buf, dtype=np.uint64).reshape(8192, 8).astype(np.float64)
+buf16 = (C.c_ulonglong * (8192 * 16))()
+L.cadet_debug_phase_read_fwd(buf16, 8192 * 16)
+a = np.frombuffer(buf16, dtype=np.uint64).reshape(8192, 16).astype(np.float64)
 used = a[a.sum(1) > 0]
-names = ["mma: q wait", "mma: k_full wait", "mma: S issue+p_full wait", "mma: v_full wait", "smx: s_full wait",
-         "smx: pass1", "smx: rescale+pass2+arrive", "-"]
+names = ["mma: item wait", "mma: k/q wait", "mma: p_full wait", "mma: o_free/v wait", "mma: issue+other",
+         "smx0: s_full wait", "smx0: (rest)", "smx0: item wait+decode", "smx0: ldtm", "smx0: mask+max",
+         "smx0: exp+sttm", "smx0: rescale+arrive", "smx0: o_full wait", "smx0: drain+store", "-", "-"]
+if os.environ.get("CADET_FWD_PAIRED") != "1":
+    names = ["mma: q wait", "mma: k_full wait", "mma: S issue+p_full wait", "mma: v_full wait", "smx: s_full wait",
+             "smx: pass1", "smx: rescale+pass2+arrive", "-"]
 print("FWD CTAs", len(used))
-for i, n in enumerate(names[:7]):
+for i, n in enumerate(names):
     print(f"{n:26s} mean per CTA {used[:, i].mean():12.0f} clk")

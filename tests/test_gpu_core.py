@@ -274,8 +274,12 @@ CORE_CASES = [
 ]
 
 
+@pytest.mark.parametrize("paired", [False, True], ids=["one_tile_per_cta", "paired_persistent"])
 @pytest.mark.parametrize("case", range(len(CORE_CASES)))
-def test_attn_core_forward(ops, case):
+def test_attn_core_forward(ops, case, paired, monkeypatch):
+    # paired: the opt-in persistent kernel (two q-tiles of a sequence share one K / V stream), read per launch
+    if paired:
+        monkeypatch.setenv("CADET_FWD_PAIRED", "1")
     lengths, d, H, nc, scale = CORE_CASES[case]
     cu, t, s, ncv, T, Qr, Kr, V = core_case(lengths, d, H, nc, scale, seed=case)
     cfg = ops.config(d, H, delta_delay_ms=120_000, out_f32=1)
