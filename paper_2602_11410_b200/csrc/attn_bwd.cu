@@ -50,6 +50,18 @@ CADET_DEV uint32_t smid() {
 #define PT_MARK(slot)
 #define TR(k, slot, v)
 #endif
+#ifdef CADET_PHASE_TIMING
+// per-thread event timelines of CTA 7 (no atomics: each traced thread owns a row, its counter in a register)
+__device__ unsigned long long g_tl[4][4096];
+#define TLX(code, idx)                                                                  \
+  if (blockIdx.x == 7 && _tln < 4096) {                                                 \
+    g_tl[_tlr][_tln++] = (clock64() << 16) | ((unsigned long long)(code) << 10) | ((idx) & 1023); \
+  }
+#define TL_DECL(row) int _tln = 0; const int _tlr = (row);
+#else
+#define TLX(code, idx)
+#define TL_DECL(row)
+#endif
 #define PTM(cond, slot) \
   if (cond) { PT_MARK(slot) }
 
@@ -328,6 +340,9 @@ __global__ void __launch_bounds__(320, 1)
 // per-column vectors (LSE*log2e, D, visible-prefix end) read from shared memory at vaddr,
 // vaddr + 256 and vaddr + 512.  MASKED: column i is visible iff key < e_i or bit i of extra.
 // dS^T is left unscaled (the dK epilogue applies 1/sqrt(hd)).
+#ifndef BWD_NPOLY
+#define BWD_NPOLY 0
+#endif
 template <bool MASKED>
 CADET_DEV void dkv_chunk(const uint32_t (&us)[32], const uint32_t (&ud)[32], uint32_t vaddr, int key, uint32_t extra,
                          float sl2, uint32_t (&wp)[16], uint32_t (&wd)[16]) {
@@ -347,8 +362,10 @@ CADET_DEV void dkv_chunk(const uint32_t (&us)[32], const uint32_t (&ud)[32], uin
       if (!((extra >> (i + 2)) & 1u)) x23.x = -INFINITY;
       if (!((extra >> (i + 3)) & 1u)) x23.y = -INFINITY;
     }
-    const float2 p01 = make_float2(fast_exp2(x01.x), fast_exp2(x01.y));
-    const float2 p23 = make_float2(fast_exp2(x23.x), fast_exp2(x23.y));
+    // BWD_NPOLY of every 16 cells on the FMA pipe (the two compute warpgroups' exponentials otherwise
+    // saturate the MUFU pipe: 2 warps x 64 ex2 x 8 cycles per SM sub-partition and q-tile)
+    const float2 p01 = ((i & 15) + 2 > 16 - BWD_NPOLY) ? exp2_poly3x2(x01) : make_float2(fast_exp2(x01.x), fast_exp2(x01.y));
+    const float2 p23 = ((i & 15) + 4 > 16 - BWD_NPOLY) ? exp2_poly3x2(x23) : make_float2(fast_exp2(x23.x), fast_exp2(x23.y));
     const float2 dd01 = __fadd2_rn(make_float2(__uint_as_float(ud[i]), __uint_as_float(ud[i + 1])), make_float2(-d4.x, -d4.y));
     const float2 dd23 =
         __fadd2_rn(make_float2(__uint_as_float(ud[i + 2]), __uint_as_float(ud[i + 3])), make_float2(-d4.z, -d4.w));
@@ -503,6 +520,7 @@ __global__ void __launch_bounds__(352, 1)
       const uint32_t sK = smem_u32(smem + C::K_OFF), sV = smem_u32(smem + C::V_OFF);
       int gq = 0;  // global q-tile counter; global half index 2 gq + hh
       PT_DECL
+      TL_DECL(0)
       for (int w = blockIdx.x, wi = 0; w < n_work; w += gridDim.x, ++wi) {
         const int n_it = dkv_work(p, w).n_it;
         PT_MARK(3)
@@ -516,8 +534,10 @@ __global__ void __launch_bounds__(352, 1)
           const uint32_t sQ = smem_u32(smem + C::Q_OFF + st * G::TILE_BYTES) + hf * 64 * G::RB;
           const uint32_t sdO = smem_u32(smem + C::DO_OFF + st * G::TILE_BYTES) + hf * 64 * G::RB;
           if (hf == 0) {
+            PT_MARK(3)
             mbar_wait(&bars->q_full[st], use & 1);
             mbar_wait(&bars->do_full[st], use & 1);
+            PT_MARK(11)
             tc_fence_after();
           }
           // over P^T/dS^T of half hh-2: in-order after its dV/dK MMAs, issued after pds_ready(hh-2)
@@ -534,11 +554,14 @@ __global__ void __launch_bounds__(352, 1)
         if (nh > 0) issue_sdp(0);
         for (int hh = 0; hh < nh; ++hh) {
           const int hf = hh & 1, g = gq + (hh >> 1), st = g & 1;
+          TLX(1, hh)
           if (hh + 1 < nh) issue_sdp(hh + 1);
+          TLX(2, hh)
           if (hh + 1 == nh - 1) mma_commit(&bars->kv_empty);  // the item's last reads of K / V are issued
           PT_MARK(3)
           mbar_wait(&bars->pds_ready[hf], g & 1);
           tc_fence_after();
+          TLX(3, hh)
           PT_MARK(2)
           if (hh == 0 && wi > 0) {
             mbar_wait(&bars->acc_free, (wi - 1) & 1);
@@ -559,6 +582,7 @@ __global__ void __launch_bounds__(352, 1)
             mma_commit(&bars->do_empty[st]);
             mma_commit(&bars->q_empty[st]);
           }
+          TLX(4, hh)
         }
         if (nh == 0) {
           mma_commit(&bars->kv_empty);
@@ -613,6 +637,7 @@ __global__ void __launch_bounds__(352, 1)
     DkvWork tn = dkv_work(p, blockIdx.x + gridDim.x < n_work ? blockIdx.x + gridDim.x : 0);
     int gq = 0;
     PT_DECL
+    TL_DECL(1 + grp)
     for (int w = blockIdx.x, wi = 0; w < n_work; w += gridDim.x, ++wi) {
       const bool has_next = w + gridDim.x < n_work;
       const int key = t.k0 + tr;
@@ -628,11 +653,22 @@ __global__ void __launch_bounds__(352, 1)
         mbar_wait(&bars->vec_full[vs], (g / C::VSTAGES) & 1);  // this q-tile's column vectors
         mbar_wait(&bars->sdp_full[grp], g & 1);
         tc_fence_after();
+        if (tracer) { TLX(10 + grp, g) }
         PTM(tracer, 6)
         const int entry = *reinterpret_cast<const int*>(smem + C::VEC_OFF + vs * C::VEC_BYTES + 1536);
         const bool full = (entry >> 30) & 1;
         const int qbase = t.sa + (entry & 0xFFFF) * 128 + grp * 64;
         uint32_t wkeep[16];
+#ifdef CADET_EXP_NOCOMPUTE
+        if (true) {  // diagnostic: hand the buffers straight back (garbage values) to time the MMA pipeline alone
+          tc_fence_before();
+          mbar_arrive(&bars->pds_ready[grp]);
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&bars->vec_empty[vs]);
+          if (tracer) { TLX(12 + grp, g) }
+          continue;
+        }
+#endif
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
           uint32_t us[32], ud[32];
@@ -642,6 +678,15 @@ __global__ void __launch_bounds__(352, 1)
           PTM(tracer, 8)
           uint32_t wp[16], wd[16];
           const uint32_t va = vst + (grp * 64 + c * 32) * 4;
+#ifdef CADET_EXP_NOMATH
+          if (true) {  // diagnostic: no exponentials / vectors (wrong values), to time the kernel's structure
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              wp[j] = pack_bf16(__uint_as_float(us[2 * j]), __uint_as_float(us[2 * j + 1]));
+              wd[j] = pack_bf16(__uint_as_float(ud[2 * j]), __uint_as_float(ud[2 * j + 1]));
+            }
+          } else
+#endif
           if (full) {
             dkv_chunk<false>(us, ud, va, key, 0u, sl2, wp, wd);
           } else {
@@ -673,6 +718,7 @@ __global__ void __launch_bounds__(352, 1)
         tmem_st_wait();
         tc_fence_before();
         mbar_arrive(&bars->pds_ready[grp]);
+        if (tracer) { TLX(12 + grp, g) }
         __syncwarp();
         if (lane == 0) mbar_arrive(&bars->vec_empty[vs]);  // the warp's vector reads are done
         PTM(tracer, 10)
@@ -692,6 +738,7 @@ __global__ void __launch_bounds__(352, 1)
             __syncwarp();
           }
         }
+        if (tracer) { TLX(14 + grp, g) }
       }
       // dK, dV (thread = key row; each warpgroup writes half of the hd columns)
       PTM(tracer, 7)
@@ -1025,6 +1072,16 @@ extern "C" int cadet_debug_trace_read(unsigned long long* out, int n) {
   if (n > 8192 * 12) n = 8192 * 12;
   cudaMemcpyFromSymbol(out, cadet::g_trace, sizeof(unsigned long long) * n);
   return n;
+}
+extern "C" int cadet_debug_tl_read(unsigned long long* out, int n) {
+  if (n > 4 * 4096) n = 4 * 4096;
+  cudaMemcpyFromSymbol(out, cadet::g_tl, sizeof(unsigned long long) * n);
+  return n;
+}
+extern "C" int cadet_debug_tl_reset() {
+  static unsigned long long z[4 * 4096];
+  cudaMemcpyToSymbol(cadet::g_tl, z, sizeof(z));
+  return 0;
 }
 extern "C" int cadet_debug_phase_reset() {
   static unsigned long long z[8192 * 16];

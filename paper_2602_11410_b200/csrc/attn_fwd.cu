@@ -433,23 +433,6 @@ CADET_DEV bool tile_sees(const QTileInfo& qi, int kt) { return kt < qi.nf || (kt
 // next visited k-tile of the slot (or of the union) at or after kt; > qt when none is left
 CADET_DEV int next_seen(const QTileInfo& qi, int kt) { return kt < qi.nf ? kt : max(kt, qi.kt2); }
 
-// 2^x for two cells at once on the FMA / ALU pipes (FA4-style MUFU offload): n = rint(x) (1.5 * 2^23
-// trick), 2^f on [-1/2, 1/2] by a degree-3 relative-minimax polynomial (max rel err 7.5e-5, far below
-// the bf16 rounding of P), n added to the exponent field.  x < -126 (incl. -inf: masked cells) gives
-// exactly 0 like ex2.approx.ftz.  Packed f32x2 FADD / FFMA (sm_100) for the float arithmetic.
-CADET_DEV float2 exp2_poly3x2(float2 x) {
-  const float2 xc = make_float2(fmaxf(x.x, -127.f), fmaxf(x.y, -127.f));
-  const float2 magic = make_float2(12582912.f, 12582912.f);
-  const float2 t = __fadd2_rn(xc, magic);
-  const float2 f = __fadd2_rn(xc, __fadd2_rn(magic, make_float2(-t.x, -t.y)));
-  float2 q = __ffma2_rn(make_float2(0.05516947f, 0.05516947f), f, make_float2(0.24260798f, 0.24260798f));
-  q = __ffma2_rn(q, f, make_float2(0.69326111f, 0.69326111f));
-  q = __ffma2_rn(q, f, make_float2(0.99992828f, 0.99992828f));
-  const float r0 = __int_as_float(__float_as_int(q.x) + (__float_as_int(t.x) << 23));
-  const float r1 = __int_as_float(__float_as_int(q.y) + (__float_as_int(t.y) << 23));
-  return make_float2(x.x < -126.f ? 0.f : r0, x.y < -126.f ? 0.f : r1);
-}
-
 template <int HD, int NPOLY>
 __global__ void __launch_bounds__(384, 1)
     attn_fwd_pair_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constant__ CUtensorMap mK,

@@ -32,6 +32,7 @@ torch.cuda.synchronize()
 L = _lib.lib()
 L.cadet_debug_phase_reset()
 L.cadet_debug_phase_reset_fwd()
+L.cadet_debug_tl_reset()
 st.step(inp)
 torch.cuda.synchronize()
 buf = (C.c_ulonglong * (8192 * 16))()
@@ -40,7 +41,7 @@ a = np.frombuffer(buf, dtype=np.uint64).reshape(8192, 16).astype(np.float64)
 used = a[a.sum(1) > 0]
 names = ["mma: kv wait", "mma: acc_free wait", "mma: pds wait", "mma: issue", "cmp x2: mma_done wait",
          "cmp x2: dK/dV drain", "cmp x2: vec+sdp wait", "cmp x2: dS store+loop", "cmp x2: ldtm", "cmp x2: math",
-         "cmp x2: sttm+arrive", "-", "-", "-", "-", "-"]
+         "cmp x2: sttm+arrive", "mma: q/dO wait", "-", "-", "-", "-"]
 print("CTAs", len(used))
 for i, n in enumerate(names):
     print(f"{n:22s} mean per CTA {used[:, i].mean():12.0f} clk")
@@ -58,3 +59,18 @@ if os.environ.get("CADET_FWD_PAIRED") != "1":
 print("FWD CTAs", len(used))
 for i, n in enumerate(names):
     print(f"{n:26s} mean per CTA {used[:, i].mean():12.0f} clk")
+
+# dK/dV timeline of CTA 7: (code, index, clock); codes 1/2 issue S+dP(hh+1) start/end, 3 pds_ready(hh) seen,
+# 4 dV/dK(hh) issued; 10+g sdp seen by group g, 12+g arrive, 14+g dS stores done
+tl = (C.c_ulonglong * (4 * 4096))()
+L.cadet_debug_tl_read(tl, 4 * 4096)
+t = np.frombuffer(tl, dtype=np.uint64).copy()
+t = t[t > 0]
+clk = (t >> 16).astype(np.int64)
+code = ((t >> 10) & 63).astype(np.int64)
+idx = (t & 1023).astype(np.int64)
+o = np.argsort(clk)
+clk, code, idx = clk[o], code[o], idx[o]
+print("timeline events", len(t))
+for c, k, i in list(zip(clk - clk[0], code, idx))[:200]:
+    print(f"{c:9d}  {k:3d}  {i}")
