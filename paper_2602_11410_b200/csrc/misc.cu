@@ -126,94 +126,107 @@ struct RgSide {
 struct RgSides {
   RgSide s[2];
 };
-// blockIdx.y = side (Q, K): both sides of A11 in one launch
+// Both sides of A11 (Q, K) in one thread: the row's (cos, sin) are evaluated once for the two sides (the
+// MUFU sincos work was half of this kernel's issue slots), and all of the thread's loads (up to six 16-byte
+// chunks) are issued before any arithmetic.  nsides = 1: the single-side entry point.
 template <bool TAPS>
-__global__ void __launch_bounds__(256) rope_gate_bwd_kernel(RgSides sides, int dr_f32, int r_bf16, int T, int d,
-                                                            int hd, RopeOTF rp) {
+__global__ void __launch_bounds__(256) rope_gate_bwd_kernel(RgSides sides, int nsides, int dr_f32, int r_bf16, int T,
+                                                            int d, int hd, RopeOTF rp) {
   pdl_trigger();
   pdl_wait();
-  const RgSide& sd = sides.s[blockIdx.y];
-  const void* dr = sd.dr;
-  const __nv_bfloat16* Xq = sd.Xq;
-  const __nv_bfloat16* Z = sd.Z;
-  __nv_bfloat16* out_u = sd.out_u;
-  void* out_r = sd.out_r;
   const int per_row = d / 8;
   const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= (size_t)T * per_row) return;
   const int row = (int)(idx / per_row);
   const int c0 = (int)(idx % per_row) * 8;
   const size_t off = (size_t)row * d + c0;
-  float g[8];
-  if (dr_f32) {
-    const float4 a = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(dr) + off)[0];
-    const float4 b = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(dr) + off)[1];
-    g[0] = a.x; g[1] = a.y; g[2] = a.z; g[3] = a.w; g[4] = b.x; g[5] = b.y; g[6] = b.z; g[7] = b.w;
-  } else {
-    const uint4 u = *reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(dr) + off);
-    const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+  // loads of both sides first
+  uint4 dru[2][2], zu[2], xu[2];
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const float2 f = __bfloat1622float2(h2[e]);
-      g[2 * e] = f.x;
-      g[2 * e + 1] = f.y;
+  for (int sd = 0; sd < 2; ++sd) {
+    if (sd >= nsides) break;
+    const RgSide& S = sides.s[sd];
+    if (dr_f32) {
+      dru[sd][0] = reinterpret_cast<const uint4*>(reinterpret_cast<const float*>(S.dr) + off)[0];
+      dru[sd][1] = reinterpret_cast<const uint4*>(reinterpret_cast<const float*>(S.dr) + off)[1];
+    } else {
+      dru[sd][0] = *reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(S.dr) + off);
+    }
+    if (S.Z) {
+      zu[sd] = *reinterpret_cast<const uint4*>(S.Z + off);
+      xu[sd] = *reinterpret_cast<const uint4*>(S.Xq + off);
     }
   }
-  if (rp.on) {  // R(-alpha): the 8-column group never crosses a head edge (hd % 8 == 0)
-    float cv[4], sv[4];
-    rope_row_cs<4>(rp, row, (c0 % hd) / 2, cv, sv);
+  float cv[4] = {1.f, 1.f, 1.f, 1.f}, sv[4] = {0.f, 0.f, 0.f, 0.f};
+  if (rp.on) rope_row_cs<4>(rp, row, (c0 % hd) / 2, cv, sv);  // the 8-column group never crosses a head edge
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
+  for (int sd = 0; sd < 2; ++sd) {
+    if (sd >= nsides) break;
+    const RgSide& S = sides.s[sd];
+    float g[8];
+    if (dr_f32) {
+      const float* f = reinterpret_cast<const float*>(&dru[sd][0]);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) g[e] = f[e];
+    } else {
+      const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&dru[sd][0]);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float2 f = __bfloat1622float2(h2[e]);
+        g[2 * e] = f.x;
+        g[2 * e + 1] = f.y;
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {  // R(-alpha)
       const float x0 = g[2 * e], x1 = g[2 * e + 1];
       g[2 * e] = x0 * cv[e] + x1 * sv[e];
       g[2 * e + 1] = x1 * cv[e] - x0 * sv[e];
     }
-  }
-  float r[8];
-  if (Z) {
-    const uint4 zu = *reinterpret_cast<const uint4*>(Z + off);
-    const uint4 xu = *reinterpret_cast<const uint4*>(Xq + off);
-    const __nv_bfloat162* z2 = reinterpret_cast<const __nv_bfloat162*>(&zu);
-    const __nv_bfloat162* x2 = reinterpret_cast<const __nv_bfloat162*>(&xu);
-    uint32_t uo[4];
+    float r[8];
+    if (S.Z) {
+      const __nv_bfloat162* z2 = reinterpret_cast<const __nv_bfloat162*>(&zu[sd]);
+      const __nv_bfloat162* x2 = reinterpret_cast<const __nv_bfloat162*>(&xu[sd]);
+      uint32_t uo[4];
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const float2 z = __bfloat1622float2(z2[e]);
-      const float2 x = __bfloat1622float2(x2[e]);
-      const float g0 = sigmoid_fast(z.x), g1 = sigmoid_fast(z.y);
-      const float u0 = g[2 * e] * x.x * g0 * (1.f - g0), u1 = g[2 * e + 1] * x.y * g1 * (1.f - g1);
-      __nv_bfloat162 v = __floats2bfloat162_rn(u0, u1);
-      uo[e] = *reinterpret_cast<uint32_t*>(&v);
-      if constexpr (TAPS) {
-        if (sd.tap_u) *reinterpret_cast<float2*>(sd.tap_u + off + 2 * e) = make_float2(u0, u1);
+      for (int e = 0; e < 4; ++e) {
+        const float2 z = __bfloat1622float2(z2[e]);
+        const float2 x = __bfloat1622float2(x2[e]);
+        const float g0 = sigmoid_fast(z.x), g1 = sigmoid_fast(z.y);
+        const float u0 = g[2 * e] * x.x * g0 * (1.f - g0), u1 = g[2 * e + 1] * x.y * g1 * (1.f - g1);
+        __nv_bfloat162 v = __floats2bfloat162_rn(u0, u1);
+        uo[e] = *reinterpret_cast<uint32_t*>(&v);
+        if constexpr (TAPS) {
+          if (S.tap_u) *reinterpret_cast<float2*>(S.tap_u + off + 2 * e) = make_float2(u0, u1);
+        }
+        r[2 * e] = g[2 * e] * g0;
+        r[2 * e + 1] = g[2 * e + 1] * g1;
       }
-      r[2 * e] = g[2 * e] * g0;
-      r[2 * e + 1] = g[2 * e + 1] * g1;
-    }
-    *reinterpret_cast<uint4*>(out_u + off) = make_uint4(uo[0], uo[1], uo[2], uo[3]);
-  } else {
+      *reinterpret_cast<uint4*>(S.out_u + off) = make_uint4(uo[0], uo[1], uo[2], uo[3]);
+    } else {
 #pragma unroll
-    for (int e = 0; e < 8; ++e) r[e] = g[e];
-  }
-  if constexpr (TAPS) {
-    if (sd.tap_r) {
-      float4* t4 = reinterpret_cast<float4*>(sd.tap_r + off);
-      t4[0] = make_float4(r[0], r[1], r[2], r[3]);
-      t4[1] = make_float4(r[4], r[5], r[6], r[7]);
+      for (int e = 0; e < 8; ++e) r[e] = g[e];
     }
-  }
-  if (r_bf16) {
-    uint32_t ro[4];
+    if constexpr (TAPS) {
+      if (S.tap_r) {
+        float4* t4 = reinterpret_cast<float4*>(S.tap_r + off);
+        t4[0] = make_float4(r[0], r[1], r[2], r[3]);
+        t4[1] = make_float4(r[4], r[5], r[6], r[7]);
+      }
+    }
+    if (r_bf16) {
+      uint32_t ro[4];
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      __nv_bfloat162 v = __floats2bfloat162_rn(r[2 * e], r[2 * e + 1]);
-      ro[e] = *reinterpret_cast<uint32_t*>(&v);
+      for (int e = 0; e < 4; ++e) {
+        __nv_bfloat162 v = __floats2bfloat162_rn(r[2 * e], r[2 * e + 1]);
+        ro[e] = *reinterpret_cast<uint32_t*>(&v);
+      }
+      *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(S.out_r) + off) = make_uint4(ro[0], ro[1], ro[2], ro[3]);
+    } else {
+      float4* o = reinterpret_cast<float4*>(reinterpret_cast<float*>(S.out_r) + off);
+      o[0] = make_float4(r[0], r[1], r[2], r[3]);
+      o[1] = make_float4(r[4], r[5], r[6], r[7]);
     }
-    *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(out_r) + off) = make_uint4(ro[0], ro[1], ro[2], ro[3]);
-  } else {
-    float4* o = reinterpret_cast<float4*>(reinterpret_cast<float*>(out_r) + off);
-    o[0] = make_float4(r[0], r[1], r[2], r[3]);
-    o[1] = make_float4(r[4], r[5], r[6], r[7]);
   }
 }
 
@@ -407,8 +420,8 @@ cudaError_t rope_gate_bwd_launch2(const void* const* dr, const void* const* Xq, 
   const size_t work = (size_t)T * d / 8;
   if (work)
     launch_pdl(((tap_u && (tap_u[0] || tap_u[nsides - 1])) || (tap_r && (tap_r[0] || tap_r[nsides - 1])))
-                   ? rope_gate_bwd_kernel<true> : rope_gate_bwd_kernel<false>, dim3(blocks(work, 256), nsides),
-               dim3(256), 0, st, sides, dr_f32, r_bf16, T, d, hd, rp);
+                   ? rope_gate_bwd_kernel<true> : rope_gate_bwd_kernel<false>, dim3(blocks(work, 256)),
+               dim3(256), 0, st, sides, nsides, dr_f32, r_bf16, T, d, hd, rp);
   return cudaGetLastError();
 }
 cudaError_t rope_gate_bwd_launch(const void* dr, int dr_f32, const void* Xq, const void* Z, void* out_u, void* out_r,
