@@ -47,6 +47,9 @@ __device__ unsigned long long g_phase_fwd[8192][16];
 #define PP_FLUSH(lo, hi)
 #endif
 
+#ifndef FWD1_NPOLY
+#define FWD1_NPOLY 4
+#endif
 template <int HD>
 struct FwdCfg {
   using G = HeadGeom<HD>;
@@ -248,14 +251,17 @@ __global__ void __launch_bounds__(192, 2)
       // own 32 columns (chunks 2, 3 from registers first, then chunks 0, 1 reloaded)
       const float base = (m_used == -INFINITY) ? 0.f : m_used;
       float rs = 0.f;
+      // packed f32x2 math; FWD1_NPOLY of every 16 cells' exponentials on the FMA pipe (MUFU offload)
+      const float2 sl2v = make_float2(sl2, sl2), nbase = make_float2(-base, -base);
+      float2 rs2 = make_float2(0.f, 0.f);
       auto exp_store = [&](int c, const uint32_t (&u)[32]) {
         uint32_t w[16];
 #pragma unroll
         for (int q = 0; q < 32; q += 2) {
-          const float p0 = fast_exp2(fmaf(__uint_as_float(u[q]), sl2, -base));
-          const float p1 = fast_exp2(fmaf(__uint_as_float(u[q + 1]), sl2, -base));
-          rs += p0 + p1;
-          w[q >> 1] = pack_bf16(p0, p1);
+          const float2 x = __ffma2_rn(make_float2(__uint_as_float(u[q]), __uint_as_float(u[q + 1])), sl2v, nbase);
+          const float2 pp = ((q & 15) + 2 > 16 - FWD1_NPOLY) ? exp2_poly3x2(x) : make_float2(fast_exp2(x.x), fast_exp2(x.y));
+          rs2 = __fadd2_rn(rs2, pp);
+          w[q >> 1] = pack_bf16(pp.x, pp.y);
         }
         tmem_st16(tmem_addr(tmem, quarter, C::S_COL + c * 32), w);
       };
@@ -274,7 +280,7 @@ __global__ void __launch_bounds__(192, 2)
       tmem_st_wait();
       tc_fence_before();
       mbar_arrive(&bars->p_full);
-      l = l * factor + rs;
+      l = l * factor + (rs + rs2.x + rs2.y);
       FT_MARK(6)
     }
 #ifdef CADET_PHASE_TIMING
