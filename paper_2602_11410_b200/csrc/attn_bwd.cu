@@ -343,44 +343,10 @@ __global__ void __launch_bounds__(320, 1)
 #ifndef BWD_NPOLY
 #define BWD_NPOLY 0
 #endif
-template <bool MASKED>
-CADET_DEV void dkv_chunk(const uint32_t (&us)[32], const uint32_t (&ud)[32], uint32_t vaddr, int key, uint32_t extra,
-                         float sl2, uint32_t (&wp)[16], uint32_t (&wd)[16]) {
-  // per-column vectors of the q-tile stage: LSE (natural log) at vaddr, D at +512, visible-prefix end at +1024;
-  // packed f32x2 arithmetic (sm_100 FFMA2 / FADD2 / FMUL2) for everything but the exponentials
-  const float2 sl2v = make_float2(sl2, sl2), nlog2e = make_float2(-1.4426950408889634f, -1.4426950408889634f);
-#pragma unroll
-  for (int i = 0; i < 32; i += 4) {
-    const float4 l4 = lds_f4(vaddr + i * 4);
-    const float4 d4 = lds_f4(vaddr + 512 + i * 4);
-    const float2 nl01 = __fmul2_rn(make_float2(l4.x, l4.y), nlog2e), nl23 = __fmul2_rn(make_float2(l4.z, l4.w), nlog2e);
-    float2 x01 = __ffma2_rn(make_float2(__uint_as_float(us[i]), __uint_as_float(us[i + 1])), sl2v, nl01);
-    float2 x23 = __ffma2_rn(make_float2(__uint_as_float(us[i + 2]), __uint_as_float(us[i + 3])), sl2v, nl23);
-    if (MASKED) {  // extra = the chunk's visibility mask
-      if (!((extra >> i) & 1u)) x01.x = -INFINITY;
-      if (!((extra >> (i + 1)) & 1u)) x01.y = -INFINITY;
-      if (!((extra >> (i + 2)) & 1u)) x23.x = -INFINITY;
-      if (!((extra >> (i + 3)) & 1u)) x23.y = -INFINITY;
-    }
-    // BWD_NPOLY of every 16 cells on the FMA pipe (the two compute warpgroups' exponentials otherwise
-    // saturate the MUFU pipe: 2 warps x 64 ex2 x 8 cycles per SM sub-partition and q-tile)
-    const float2 p01 = ((i & 15) + 2 > 16 - BWD_NPOLY) ? exp2_poly3x2(x01) : make_float2(fast_exp2(x01.x), fast_exp2(x01.y));
-    const float2 p23 = ((i & 15) + 4 > 16 - BWD_NPOLY) ? exp2_poly3x2(x23) : make_float2(fast_exp2(x23.x), fast_exp2(x23.y));
-    const float2 dd01 = __fadd2_rn(make_float2(__uint_as_float(ud[i]), __uint_as_float(ud[i + 1])), make_float2(-d4.x, -d4.y));
-    const float2 dd23 =
-        __fadd2_rn(make_float2(__uint_as_float(ud[i + 2]), __uint_as_float(ud[i + 3])), make_float2(-d4.z, -d4.w));
-    const float2 s01 = __fmul2_rn(p01, dd01), s23 = __fmul2_rn(p23, dd23);
-    wp[i >> 1] = pack_bf16(p01.x, p01.y);
-    wp[(i >> 1) + 1] = pack_bf16(p23.x, p23.y);
-    wd[i >> 1] = pack_bf16(s01.x, s01.y);
-    wd[(i >> 1) + 1] = pack_bf16(s23.x, s23.y);
-  }
-}
-
-// PARTIAL tile: column i of the chunk is visible iff it is a valid column (colmask) and key < e_i or bit i
-// of extra (diagonal / transposed pair)
-CADET_DEV void dkv_chunk_masked(const uint32_t (&us)[32], const uint32_t (&ud)[32], uint32_t vaddr, int key,
-                                uint32_t extra, uint32_t colmask, float sl2, uint32_t (&wp)[16], uint32_t (&wd)[16]) {
+// Visible-prefix bits of a 32-column chunk for key row `key`: column i is visible iff key < e_i (the
+// column's prefix end, staged at vaddr + 1024); the caller ORs in the diagonal / transposed-pair bits and
+// masks columns past the sequence end.
+CADET_DEV uint32_t dkv_prefix_mask(uint32_t vaddr, int key) {
   uint32_t vis = 0;
 #pragma unroll
   for (int i = 0; i < 32; i += 4) {
@@ -390,8 +356,46 @@ CADET_DEV void dkv_chunk_masked(const uint32_t (&us)[32], const uint32_t (&ud)[3
     vis |= (key < e4.z ? 1u : 0u) << (i + 2);
     vis |= (key < e4.w ? 1u : 0u) << (i + 3);
   }
-  vis = (vis | extra) & colmask;
-  dkv_chunk<true>(us, ud, vaddr, key, vis, sl2, wp, wd);
+  return vis;
+}
+// Softmax phase of one 32-column chunk: P = exp2(S^T log2e / sqrt(hd) - LSE log2e) (LSE at vaddr), fp32 into
+// pv[o .. o + 32) and packed bf16 into wp; MASKED: invisible columns (vis bit clear) give exactly 0.
+template <bool MASKED>
+CADET_DEV void dkv_p_chunk(const uint32_t (&us)[32], uint32_t vaddr, uint32_t vis, float sl2, float (&pv)[64], int o,
+                           uint32_t (&wp)[16]) {
+  const float2 sl2v = make_float2(sl2, sl2), nlog2e = make_float2(-1.4426950408889634f, -1.4426950408889634f);
+#pragma unroll
+  for (int i = 0; i < 32; i += 4) {
+    const float4 l4 = lds_f4(vaddr + i * 4);
+    const float2 nl01 = __fmul2_rn(make_float2(l4.x, l4.y), nlog2e), nl23 = __fmul2_rn(make_float2(l4.z, l4.w), nlog2e);
+    float2 x01 = __ffma2_rn(make_float2(__uint_as_float(us[i]), __uint_as_float(us[i + 1])), sl2v, nl01);
+    float2 x23 = __ffma2_rn(make_float2(__uint_as_float(us[i + 2]), __uint_as_float(us[i + 3])), sl2v, nl23);
+    if (MASKED) {
+      if (!((vis >> i) & 1u)) x01.x = -INFINITY;
+      if (!((vis >> (i + 1)) & 1u)) x01.y = -INFINITY;
+      if (!((vis >> (i + 2)) & 1u)) x23.x = -INFINITY;
+      if (!((vis >> (i + 3)) & 1u)) x23.y = -INFINITY;
+    }
+    const float2 p01 = ((i & 15) + 2 > 16 - BWD_NPOLY) ? exp2_poly3x2(x01) : make_float2(fast_exp2(x01.x), fast_exp2(x01.y));
+    const float2 p23 = ((i & 15) + 4 > 16 - BWD_NPOLY) ? exp2_poly3x2(x23) : make_float2(fast_exp2(x23.x), fast_exp2(x23.y));
+    pv[o + i] = p01.x, pv[o + i + 1] = p01.y, pv[o + i + 2] = p23.x, pv[o + i + 3] = p23.y;
+    wp[i >> 1] = pack_bf16(p01.x, p01.y);
+    wp[(i >> 1) + 1] = pack_bf16(p23.x, p23.y);
+  }
+}
+// dS phase of one chunk: dS^T = P^T (dP^T - D) (D at vaddr + 512), packed bf16 into wd
+CADET_DEV void dkv_ds_chunk(const uint32_t (&ud)[32], const float (&pv)[64], int o, uint32_t vaddr, uint32_t (&wd)[16]) {
+#pragma unroll
+  for (int i = 0; i < 32; i += 4) {
+    const float4 d4 = lds_f4(vaddr + 512 + i * 4);
+    const float2 dd01 = __fadd2_rn(make_float2(__uint_as_float(ud[i]), __uint_as_float(ud[i + 1])), make_float2(-d4.x, -d4.y));
+    const float2 dd23 =
+        __fadd2_rn(make_float2(__uint_as_float(ud[i + 2]), __uint_as_float(ud[i + 3])), make_float2(-d4.z, -d4.w));
+    const float2 s01 = __fmul2_rn(make_float2(pv[o + i], pv[o + i + 1]), dd01);
+    const float2 s23 = __fmul2_rn(make_float2(pv[o + i + 2], pv[o + i + 3]), dd23);
+    wd[i >> 1] = pack_bf16(s01.x, s01.y);
+    wd[(i >> 1) + 1] = pack_bf16(s23.x, s23.y);
+  }
 }
 
 template <int HD>
@@ -415,8 +419,8 @@ struct DkvCfg {
 };
 
 struct DkvBars {
-  uint64_t kv_full, kv_empty, q_full[2], q_empty[2], do_full[2], do_empty[2], sdp_full[2], pds_ready[2], mma_done,
-      acc_free, vec_full[4], vec_empty[4];
+  uint64_t kv_full, kv_empty, q_full[2], q_empty[2], do_full[2], do_empty[2], s_full, dp_full, p_ready[2], ds_ready[2],
+      mma_done, acc_free, vec_full[4], vec_empty[4];
   uint32_t tmem_base;
 };
 
@@ -460,9 +464,11 @@ __global__ void __launch_bounds__(352, 1)
       mbar_init(&bars->q_empty[i], 1);
       mbar_init(&bars->do_full[i], 1);
       mbar_init(&bars->do_empty[i], 1);
-      mbar_init(&bars->sdp_full[i], 1);
-      mbar_init(&bars->pds_ready[i], 128);
+      mbar_init(&bars->p_ready[i], 128);
+      mbar_init(&bars->ds_ready[i], 128);
     }
+    mbar_init(&bars->s_full, 1);
+    mbar_init(&bars->dp_full, 1);
     mbar_init(&bars->mma_done, 1);
     mbar_init(&bars->acc_free, 256);
     for (int i = 0; i < 4; ++i) {
@@ -514,79 +520,94 @@ __global__ void __launch_bounds__(352, 1)
       }
     }
   } else if (warp == 1) {
+    // ============================ MMA issuer.  Per q-tile g (full 128-column S^T / dP^T, N = 128 MMAs at
+    // their floor): S^T(g) -> [softmax phase] -> dV(g), then S^T(g + 1) over the consumed P^T(g);
+    // dP^T(g) -> [dS phase] -> dK(g), then dP^T(g + 1) over the consumed dS^T(g).  The tensor core runs
+    // dP^T(g) during the softmax phase and dV(g) + S^T(g + 1) during the dS phase.
     if (elect_one()) {
-      const uint32_t id_s = idesc_bf16(128, 64, 0, 0);
+      const uint32_t id_s = idesc_bf16(128, 128, 0, 0);
       const uint32_t id_kv = idesc_bf16(128, G::HDP, 0, 1);
       const uint32_t sK = smem_u32(smem + C::K_OFF), sV = smem_u32(smem + C::V_OFF);
-      int gq = 0;  // global q-tile counter; global half index 2 gq + hh
+      int gq = 0;  // global q-tile counter
       PT_DECL
       TL_DECL(0)
+      auto issue_s = [&](int g) {  // S^T = K Q_g^T into S_COL
+        const int st = g & 1;
+        const uint32_t sQ = smem_u32(smem + C::Q_OFF + st * G::TILE_BYTES);
+        mbar_wait(&bars->q_full[st], (g >> 1) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < G::HDP / 16; ++kk)
+          mma_bf16_ss(tmem + C::S_COL, kmajor_desc<HD>(sK, kk), kmajor_desc<HD>(sQ, kk), id_s, kk > 0 ? 1u : 0u);
+        mma_commit(&bars->s_full);
+      };
+      auto issue_dp = [&](int g) {  // dP^T = V dO_g^T into DP_COL
+        const int st = g & 1;
+        const uint32_t sdO = smem_u32(smem + C::DO_OFF + st * G::TILE_BYTES);
+        mbar_wait(&bars->do_full[st], (g >> 1) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < G::HDP / 16; ++kk)
+          mma_bf16_ss(tmem + C::DP_COL, kmajor_desc<HD>(sV, kk), kmajor_desc<HD>(sdO, kk), id_s, kk > 0 ? 1u : 0u);
+        mma_commit(&bars->dp_full);
+      };
       for (int w = blockIdx.x, wi = 0; w < n_work; w += gridDim.x, ++wi) {
         const int n_it = dkv_work(p, w).n_it;
         PT_MARK(3)
         mbar_wait(&bars->kv_full, wi & 1);
         tc_fence_after();
         PT_MARK(0)
-        const int nh = 2 * n_it;
-        // half hh: q-tile hh >> 1, columns [64 (hh & 1), +64), TMEM half-buffer hh & 1
-        auto issue_sdp = [&](int hh) {
-          const int hf = hh & 1, g = gq + (hh >> 1), st = g & 1, use = g >> 1;
-          const uint32_t sQ = smem_u32(smem + C::Q_OFF + st * G::TILE_BYTES) + hf * 64 * G::RB;
-          const uint32_t sdO = smem_u32(smem + C::DO_OFF + st * G::TILE_BYTES) + hf * 64 * G::RB;
-          if (hf == 0) {
-            PT_MARK(3)
-            mbar_wait(&bars->q_full[st], use & 1);
-            mbar_wait(&bars->do_full[st], use & 1);
-            PT_MARK(11)
-            tc_fence_after();
-          }
-          // over P^T/dS^T of half hh-2: in-order after its dV/dK MMAs, issued after pds_ready(hh-2)
-#pragma unroll
-          for (int kk = 0; kk < G::HDP / 16; ++kk)
-            mma_bf16_ss(tmem + C::S_COL + hf * 64, kmajor_desc<HD>(sK, kk), kmajor_desc<HD>(sQ, kk), id_s,
-                        kk > 0 ? 1u : 0u);
-#pragma unroll
-          for (int kk = 0; kk < G::HDP / 16; ++kk)
-            mma_bf16_ss(tmem + C::DP_COL + hf * 64, kmajor_desc<HD>(sV, kk), kmajor_desc<HD>(sdO, kk), id_s,
-                        kk > 0 ? 1u : 0u);
-          mma_commit(&bars->sdp_full[hf]);
-        };
-        if (nh > 0) issue_sdp(0);
-        for (int hh = 0; hh < nh; ++hh) {
-          const int hf = hh & 1, g = gq + (hh >> 1), st = g & 1;
-          TLX(1, hh)
-          if (hh + 1 < nh) issue_sdp(hh + 1);
-          TLX(2, hh)
-          if (hh + 1 == nh - 1) mma_commit(&bars->kv_empty);  // the item's last reads of K / V are issued
+        if (n_it == 0) {
+          mma_commit(&bars->kv_empty);
+          if (wi > 0) mbar_wait(&bars->acc_free, (wi - 1) & 1);
+          mma_commit(&bars->mma_done);
+          continue;
+        }
+        issue_s(gq);
+        issue_dp(gq);
+        if (n_it == 1) mma_commit(&bars->kv_empty);  // the item's last reads of K / V are issued
+        for (int it = 0; it < n_it; ++it) {
+          const int g = gq + it, st = g & 1;
+          const uint32_t sQ = smem_u32(smem + C::Q_OFF + st * G::TILE_BYTES);
+          const uint32_t sdO = smem_u32(smem + C::DO_OFF + st * G::TILE_BYTES);
           PT_MARK(3)
-          mbar_wait(&bars->pds_ready[hf], g & 1);
+          mbar_wait(&bars->p_ready[0], g & 1);
+          mbar_wait(&bars->p_ready[1], g & 1);
           tc_fence_after();
-          TLX(3, hh)
+          TLX(3, 2 * it)
           PT_MARK(2)
-          if (hh == 0 && wi > 0) {
+          if (it == 0 && wi > 0) {
             mbar_wait(&bars->acc_free, (wi - 1) & 1);
             tc_fence_after();
           }
           PT_MARK(1)
-          const uint32_t sQ = smem_u32(smem + C::Q_OFF + st * G::TILE_BYTES);
-          const uint32_t sdO = smem_u32(smem + C::DO_OFF + st * G::TILE_BYTES);
 #pragma unroll
-          for (int kk = 0; kk < 64 / 16; ++kk)
-            mma_bf16_ts(tmem + C::DV_COL, tmem + C::S_COL + hf * 64 + kk * 8, mnmajor_desc<HD>(sdO, hf * 4 + kk),
-                        id_kv, (hh > 0 || kk > 0) ? 1u : 0u);
+          for (int hf = 0; hf < 2; ++hf)
 #pragma unroll
-          for (int kk = 0; kk < 64 / 16; ++kk)
-            mma_bf16_ts(tmem + C::DK_COL, tmem + C::DP_COL + hf * 64 + kk * 8, mnmajor_desc<HD>(sQ, hf * 4 + kk),
-                        id_kv, (hh > 0 || kk > 0) ? 1u : 0u);
-          if (hf == 1) {
-            mma_commit(&bars->do_empty[st]);
-            mma_commit(&bars->q_empty[st]);
+            for (int kk = 0; kk < 64 / 16; ++kk)
+              mma_bf16_ts(tmem + C::DV_COL, tmem + C::S_COL + hf * 64 + kk * 8, mnmajor_desc<HD>(sdO, hf * 4 + kk),
+                          id_kv, (it > 0 || hf > 0 || kk > 0) ? 1u : 0u);
+          mma_commit(&bars->do_empty[st]);  // dO(g): dP^T(g) and dV(g) issued
+          if (it + 1 < n_it) issue_s(g + 1);  // over P^T(g): after dV(g) in issue order
+          TLX(4, 2 * it)
+          PT_MARK(3)
+          mbar_wait(&bars->ds_ready[0], g & 1);
+          mbar_wait(&bars->ds_ready[1], g & 1);
+          tc_fence_after();
+          TLX(3, 2 * it + 1)
+          PT_MARK(2)
+#pragma unroll
+          for (int hf = 0; hf < 2; ++hf)
+#pragma unroll
+            for (int kk = 0; kk < 64 / 16; ++kk)
+              mma_bf16_ts(tmem + C::DK_COL, tmem + C::DP_COL + hf * 64 + kk * 8, mnmajor_desc<HD>(sQ, hf * 4 + kk),
+                          id_kv, (it > 0 || hf > 0 || kk > 0) ? 1u : 0u);
+          mma_commit(&bars->q_empty[st]);  // Q(g): S^T(g) and dK(g) issued
+          if (it + 1 < n_it) {
+            issue_dp(g + 1);  // over dS^T(g): after dK(g) in issue order
+            if (it + 1 == n_it - 1) mma_commit(&bars->kv_empty);
           }
-          TLX(4, hh)
-        }
-        if (nh == 0) {
-          mma_commit(&bars->kv_empty);
-          if (wi > 0) mbar_wait(&bars->acc_free, (wi - 1) & 1);
+          TLX(4, 2 * it + 1)
         }
         mma_commit(&bars->mma_done);
         gq += n_it;
@@ -651,73 +672,73 @@ __global__ void __launch_bounds__(352, 1)
         const uint32_t vst = smem_u32(smem + C::VEC_OFF + vs * C::VEC_BYTES);
         PTM(tracer, 7)
         mbar_wait(&bars->vec_full[vs], (g / C::VSTAGES) & 1);  // this q-tile's column vectors
-        mbar_wait(&bars->sdp_full[grp], g & 1);
+        mbar_wait(&bars->s_full, g & 1);
         tc_fence_after();
         if (tracer) { TLX(10 + grp, g) }
         PTM(tracer, 6)
         const int entry = *reinterpret_cast<const int*>(smem + C::VEC_OFF + vs * C::VEC_BYTES + 1536);
         const bool full = (entry >> 30) & 1;
         const int qbase = t.sa + (entry & 0xFFFF) * 128 + grp * 64;
-        uint32_t wkeep[16];
-#ifdef CADET_EXP_NOCOMPUTE
-        if (true) {  // diagnostic: hand the buffers straight back (garbage values) to time the MMA pipeline alone
-          tc_fence_before();
-          mbar_arrive(&bars->pds_ready[grp]);
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&bars->vec_empty[vs]);
-          if (tracer) { TLX(12 + grp, g) }
-          continue;
-        }
-#endif
-#pragma unroll
-        for (int c = 0; c < 2; ++c) {
-          uint32_t us[32], ud[32];
-          tmem_ld32(tmem_addr(tmem, quarter, C::S_COL + grp * 64 + c * 32), us);
-          tmem_ld32(tmem_addr(tmem, quarter, C::DP_COL + grp * 64 + c * 32), ud);
-          tmem_ld_wait();
+        // ---- softmax phase: P^T of this warpgroup's 64 columns (kept in fp32 for the dS phase)
+        float pv[64];
+        {
           PTM(tracer, 8)
-          uint32_t wp[16], wd[16];
-          const uint32_t va = vst + (grp * 64 + c * 32) * 4;
-#ifdef CADET_EXP_NOMATH
-          if (true) {  // diagnostic: no exponentials / vectors (wrong values), to time the kernel's structure
 #pragma unroll
-            for (int j = 0; j < 16; ++j) {
-              wp[j] = pack_bf16(__uint_as_float(us[2 * j]), __uint_as_float(us[2 * j + 1]));
-              wd[j] = pack_bf16(__uint_as_float(ud[2 * j]), __uint_as_float(ud[2 * j + 1]));
+          for (int c = 0; c < 2; ++c) {
+            uint32_t us[32];
+            tmem_ld32(tmem_addr(tmem, quarter, C::S_COL + grp * 64 + c * 32), us);
+            tmem_ld_wait();
+            const uint32_t va = vst + (grp * 64 + c * 32) * 4;
+            uint32_t wp[16];
+            if (full) {
+              dkv_p_chunk<false>(us, va, 0u, sl2, pv, c * 32, wp);
+            } else {
+              // diagonal (key == q) and transposed pair (q == key + 1 with PAIR_PREV) columns of the chunk;
+              // columns past the sequence end (pad / next sequence rows of the stage) are never visible
+              const int q0c = qbase + c * 32;
+              const int dd = key - q0c;
+              uint32_t extra = 0;
+              if (key_valid && dd >= 0 && dd < 32) extra |= 1u << dd;
+              if (ppn && dd + 1 >= 0 && dd + 1 < 32) extra |= 1u << (dd + 1);
+              const int nv = t.se - q0c;  // valid columns of the chunk
+              const uint32_t colmask = nv >= 32 ? 0xFFFFFFFFu : (nv <= 0 ? 0u : ((1u << nv) - 1u));
+              const uint32_t vis = (dkv_prefix_mask(va, key) | extra) & colmask & (key_valid ? 0xFFFFFFFFu : 0u);
+              dkv_p_chunk<true>(us, va, vis, sl2, pv, c * 32, wp);
             }
-          } else
-#endif
-          if (full) {
-            dkv_chunk<false>(us, ud, va, key, 0u, sl2, wp, wd);
-          } else {
-            // diagonal (key == q) and transposed pair (q == key + 1 with PAIR_PREV) columns of the chunk;
-            // columns past the sequence end (pad / next sequence rows of the stage) are never visible
-            const int q0c = qbase + c * 32;
-            const int dd = key - q0c;
-            uint32_t extra = 0;
-            if (key_valid && dd >= 0 && dd < 32) extra |= 1u << dd;
-            if (ppn && dd + 1 >= 0 && dd + 1 < 32) extra |= 1u << (dd + 1);
-            const int nv = t.se - q0c;  // valid columns of the chunk
-            const uint32_t colmask = nv >= 32 ? 0xFFFFFFFFu : (nv <= 0 ? 0u : ((1u << nv) - 1u));
-            const uint32_t vis_key = key_valid ? 0xFFFFFFFFu : 0u;
-            dkv_chunk_masked(us, ud, va, key, extra, colmask & vis_key, sl2, wp, wd);
+            // P^T chunk c -> columns [16c, 16c + 16) of this half (only this thread's consumed S^T)
+            tmem_st16(tmem_addr(tmem, quarter, C::S_COL + grp * 64 + c * 16), wp);
           }
-          if (p.dS) {  // dS^T chunk 0 -> the warp's stage now, chunk 1 kept: both stored after the arrive
-            if (c == 0)
-              warp_stage_rows_bf16(smem_u32(smem + C::STG_OFF + (warp - 2) * 2048), wd);
-            else
-#pragma unroll
-              for (int j = 0; j < 16; ++j) wkeep[j] = wd[j];
-          }
+          tmem_st_wait();
+          tc_fence_before();
+          mbar_arrive(&bars->p_ready[grp]);
           PTM(tracer, 9)
-          // P^T / dS^T chunk c -> columns [16c, 16c + 16) of this half: only this thread's own,
-          // already-loaded S^T / dP^T chunk 0 is overwritten
-          tmem_st16(tmem_addr(tmem, quarter, C::S_COL + grp * 64 + c * 16), wp);
-          tmem_st16(tmem_addr(tmem, quarter, C::DP_COL + grp * 64 + c * 16), wd);
         }
-        tmem_st_wait();
-        tc_fence_before();
-        mbar_arrive(&bars->pds_ready[grp]);
+        // ---- dS phase: dS^T = P^T (dP^T - D) (unscaled; the dK drain applies 1/sqrt(hd))
+        uint32_t wkeep[16];
+        mbar_wait(&bars->dp_full, g & 1);
+        tc_fence_after();
+        {
+#pragma unroll
+          for (int c = 0; c < 2; ++c) {
+            uint32_t ud[32];
+            tmem_ld32(tmem_addr(tmem, quarter, C::DP_COL + grp * 64 + c * 32), ud);
+            tmem_ld_wait();
+            const uint32_t va = vst + (grp * 64 + c * 32) * 4;
+            uint32_t wd[16];
+            dkv_ds_chunk(ud, pv, c * 32, va, wd);
+            if (p.dS) {  // dS^T chunk 0 -> the warp's stage now, chunk 1 kept: both stored after the arrive
+              if (c == 0)
+                warp_stage_rows_bf16(smem_u32(smem + C::STG_OFF + (warp - 2) * 2048), wd);
+              else
+#pragma unroll
+                for (int j = 0; j < 16; ++j) wkeep[j] = wd[j];
+            }
+            tmem_st16(tmem_addr(tmem, quarter, C::DP_COL + grp * 64 + c * 16), wd);
+          }
+          tmem_st_wait();
+          tc_fence_before();
+          mbar_arrive(&bars->ds_ready[grp]);
+        }
         if (tracer) { TLX(12 + grp, g) }
         __syncwarp();
         if (lane == 0) mbar_arrive(&bars->vec_empty[vs]);  // the warp's vector reads are done
