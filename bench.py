@@ -24,7 +24,7 @@ import time
 import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
-TRAFFIC_PROFILE = "r02_dram_traffic.json"  # per-class DRAM bytes per launch (scripts/traffic_summary.py)
+TRAFFIC_PROFILE = "r02b_dram_traffic.json"  # per-class DRAM bytes per launch (scripts/traffic_summary.py)
 sys.path.insert(0, ROOT)
 
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
@@ -374,7 +374,10 @@ def main():
     if local == 0:
         build.build(verbose=False)  # no-op when the shipped libcadet.so is current
     torch.cuda.set_device(local)
-    numa_cpus = bind_numa_local(local) if world > 1 else None  # N > 1: each rank's host memory on its GPU's node
+    # each rank's host threads and pinned inputs on its GPU's NUMA node (N = 1 too: the e2e leg's
+    # host -> device copies are the limit of that leg); the CPU oracle baseline gets the full affinity back
+    full_affinity = os.sched_getaffinity(0) if hasattr(os, "sched_getaffinity") else None
+    numa_cpus = bind_numa_local(local)
     group = None
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -609,6 +612,8 @@ def main():
         attn_view["dram_source"] = f"profiles/{TRAFFIC_PROFILE}"
     cpu = None
     if not args.no_cpu and world == 1:
+        if full_affinity:
+            os.sched_setaffinity(0, full_affinity)
         v, tokc, dt, desc = time_oracle(users, wl, 0)
         cpu = {"value": v, "unit": "tokens/s", "cores": cpu_cores(), "kind": "oracle", "sample": desc,
                "seconds": dt, "blas": blas_info()}
