@@ -37,7 +37,8 @@ def meta_of(cu, t, s, nc, n_static=None, flags=None):
 
 # ------------------------------------------------------------------ GEMM
 @pytest.mark.parametrize("a_mn,b_mn", [(0, 0), (0, 1), (1, 0), (1, 1)])
-@pytest.mark.parametrize("M,N,K", [(128, 128, 64), (304, 192, 200), (512, 512, 1024), (776, 768, 320)])
+@pytest.mark.parametrize("M,N,K", [(128, 128, 64), (304, 192, 200), (512, 512, 1024), (776, 768, 320),
+                                   (512, 352, 352), (4352, 352, 352)])  # ragged N on the 128-wide CTA-pair tiles
 def test_gemm_majors(ops, a_mn, b_mn, M, N, K):
     rng = np.random.default_rng(M + N + K)
     A = rng.standard_normal((M, K)).astype(np.float32)
