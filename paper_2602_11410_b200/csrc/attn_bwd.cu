@@ -358,11 +358,10 @@ CADET_DEV uint32_t dkv_prefix_mask(uint32_t vaddr, int key) {
   }
   return vis;
 }
-// Softmax phase of one 32-column chunk: P = exp2(S^T log2e / sqrt(hd) - LSE log2e) (LSE at vaddr), fp32 into
-// pv[o .. o + 32) and packed bf16 into wp; MASKED: invisible columns (vis bit clear) give exactly 0.
+// Softmax phase of one 32-column chunk: P = exp2(S^T log2e / sqrt(hd) - LSE log2e) (LSE at vaddr), packed
+// bf16 into wp; MASKED: invisible columns (vis bit clear) give exactly 0.
 template <bool MASKED>
-CADET_DEV void dkv_p_chunk(const uint32_t (&us)[32], uint32_t vaddr, uint32_t vis, float sl2, float (&pv)[64], int o,
-                           uint32_t (&wp)[16]) {
+CADET_DEV void dkv_p_chunk(const uint32_t (&us)[32], uint32_t vaddr, uint32_t vis, float sl2, uint32_t (&wp)[16]) {
   const float2 sl2v = make_float2(sl2, sl2), nlog2e = make_float2(-1.4426950408889634f, -1.4426950408889634f);
 #pragma unroll
   for (int i = 0; i < 32; i += 4) {
@@ -378,21 +377,22 @@ CADET_DEV void dkv_p_chunk(const uint32_t (&us)[32], uint32_t vaddr, uint32_t vi
     }
     const float2 p01 = ((i & 15) + 2 > 16 - BWD_NPOLY) ? exp2_poly3x2(x01) : make_float2(fast_exp2(x01.x), fast_exp2(x01.y));
     const float2 p23 = ((i & 15) + 4 > 16 - BWD_NPOLY) ? exp2_poly3x2(x23) : make_float2(fast_exp2(x23.x), fast_exp2(x23.y));
-    pv[o + i] = p01.x, pv[o + i + 1] = p01.y, pv[o + i + 2] = p23.x, pv[o + i + 3] = p23.y;
     wp[i >> 1] = pack_bf16(p01.x, p01.y);
     wp[(i >> 1) + 1] = pack_bf16(p23.x, p23.y);
   }
 }
-// dS phase of one chunk: dS^T = P^T (dP^T - D) (D at vaddr + 512), packed bf16 into wd
-CADET_DEV void dkv_ds_chunk(const uint32_t (&ud)[32], const float (&pv)[64], int o, uint32_t vaddr, uint32_t (&wd)[16]) {
+// dS phase of one chunk from the packed bf16 P^T (the values the dV MMA used): dS^T = P^T (dP^T - D)
+CADET_DEV void dkv_ds_chunk_pk(const uint32_t (&ud)[32], const uint32_t* pk, uint32_t vaddr, uint32_t (&wd)[16]) {
 #pragma unroll
   for (int i = 0; i < 32; i += 4) {
     const float4 d4 = lds_f4(vaddr + 512 + i * 4);
     const float2 dd01 = __fadd2_rn(make_float2(__uint_as_float(ud[i]), __uint_as_float(ud[i + 1])), make_float2(-d4.x, -d4.y));
     const float2 dd23 =
         __fadd2_rn(make_float2(__uint_as_float(ud[i + 2]), __uint_as_float(ud[i + 3])), make_float2(-d4.z, -d4.w));
-    const float2 s01 = __fmul2_rn(make_float2(pv[o + i], pv[o + i + 1]), dd01);
-    const float2 s23 = __fmul2_rn(make_float2(pv[o + i + 2], pv[o + i + 3]), dd23);
+    const uint32_t w0 = pk[i >> 1], w1 = pk[(i >> 1) + 1];
+    const float2 p01 = make_float2(__uint_as_float(w0 << 16), __uint_as_float(w0 & 0xFFFF0000u));
+    const float2 p23 = make_float2(__uint_as_float(w1 << 16), __uint_as_float(w1 & 0xFFFF0000u));
+    const float2 s01 = __fmul2_rn(p01, dd01), s23 = __fmul2_rn(p23, dd23);
     wd[i >> 1] = pack_bf16(s01.x, s01.y);
     wd[(i >> 1) + 1] = pack_bf16(s23.x, s23.y);
   }
@@ -680,32 +680,35 @@ __global__ void __launch_bounds__(352, 1)
         const bool full = (entry >> 30) & 1;
         const int qbase = t.sa + (entry & 0xFFFF) * 128 + grp * 64;
         // ---- softmax phase: P^T of this warpgroup's 64 columns (kept in fp32 for the dS phase)
-        float pv[64];
+        // P^T kept packed (bf16, the values the dV MMA multiplies) for the dS phase; both chunks' TMEM
+        // loads in flight before one wait in each phase (TMEM load latency is long while the tensor
+        // core is busy)
+        uint32_t pk[32];
         {
           PTM(tracer, 8)
+          uint32_t us0[32], us1[32];
+          tmem_ld32(tmem_addr(tmem, quarter, C::S_COL + grp * 64), us0);
+          tmem_ld32(tmem_addr(tmem, quarter, C::S_COL + grp * 64 + 32), us1);
+          tmem_ld_wait();
 #pragma unroll
           for (int c = 0; c < 2; ++c) {
-            uint32_t us[32];
-            tmem_ld32(tmem_addr(tmem, quarter, C::S_COL + grp * 64 + c * 32), us);
-            tmem_ld_wait();
             const uint32_t va = vst + (grp * 64 + c * 32) * 4;
             uint32_t wp[16];
             if (full) {
-              dkv_p_chunk<false>(us, va, 0u, sl2, pv, c * 32, wp);
+              dkv_p_chunk<false>(c == 0 ? us0 : us1, va, 0u, sl2, wp);
             } else {
-              // diagonal (key == q) and transposed pair (q == key + 1 with PAIR_PREV) columns of the chunk;
-              // columns past the sequence end (pad / next sequence rows of the stage) are never visible
               const int q0c = qbase + c * 32;
               const int dd = key - q0c;
               uint32_t extra = 0;
               if (key_valid && dd >= 0 && dd < 32) extra |= 1u << dd;
               if (ppn && dd + 1 >= 0 && dd + 1 < 32) extra |= 1u << (dd + 1);
-              const int nv = t.se - q0c;  // valid columns of the chunk
+              const int nv = t.se - q0c;
               const uint32_t colmask = nv >= 32 ? 0xFFFFFFFFu : (nv <= 0 ? 0u : ((1u << nv) - 1u));
               const uint32_t vis = (dkv_prefix_mask(va, key) | extra) & colmask & (key_valid ? 0xFFFFFFFFu : 0u);
-              dkv_p_chunk<true>(us, va, vis, sl2, pv, c * 32, wp);
+              dkv_p_chunk<true>(c == 0 ? us0 : us1, va, vis, sl2, wp);
             }
-            // P^T chunk c -> columns [16c, 16c + 16) of this half (only this thread's consumed S^T)
+#pragma unroll
+            for (int j = 0; j < 16; ++j) pk[c * 16 + j] = wp[j];
             tmem_st16(tmem_addr(tmem, quarter, C::S_COL + grp * 64 + c * 16), wp);
           }
           tmem_st_wait();
@@ -713,20 +716,20 @@ __global__ void __launch_bounds__(352, 1)
           mbar_arrive(&bars->p_ready[grp]);
           PTM(tracer, 9)
         }
-        // ---- dS phase: dS^T = P^T (dP^T - D) (unscaled; the dK drain applies 1/sqrt(hd))
         uint32_t wkeep[16];
         mbar_wait(&bars->dp_full, g & 1);
         tc_fence_after();
         {
+          uint32_t ud0[32], ud1[32];
+          tmem_ld32(tmem_addr(tmem, quarter, C::DP_COL + grp * 64), ud0);
+          tmem_ld32(tmem_addr(tmem, quarter, C::DP_COL + grp * 64 + 32), ud1);
+          tmem_ld_wait();
 #pragma unroll
           for (int c = 0; c < 2; ++c) {
-            uint32_t ud[32];
-            tmem_ld32(tmem_addr(tmem, quarter, C::DP_COL + grp * 64 + c * 32), ud);
-            tmem_ld_wait();
             const uint32_t va = vst + (grp * 64 + c * 32) * 4;
             uint32_t wd[16];
-            dkv_ds_chunk(ud, pv, c * 32, va, wd);
-            if (p.dS) {  // dS^T chunk 0 -> the warp's stage now, chunk 1 kept: both stored after the arrive
+            dkv_ds_chunk_pk(c == 0 ? ud0 : ud1, &pk[c * 16], va, wd);
+            if (p.dS) {
               if (c == 0)
                 warp_stage_rows_bf16(smem_u32(smem + C::STG_OFF + (warp - 2) * 2048), wd);
               else
