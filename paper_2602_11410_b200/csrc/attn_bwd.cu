@@ -779,6 +779,10 @@ __global__ void __launch_bounds__(352, 1)
           uint32_t u[32];
           tmem_ld32(tmem_addr(tmem, quarter, col0 + c * 32), u);
           tmem_ld_wait();
+          if (which == 1 && c + 2 >= G::HDP / 32) {  // this warp's last accumulator read: hand the
+            tc_fence_before();                        // accumulators to the next item's MMAs before
+            mbar_arrive(&bars->acc_free);             // the last stores
+          }
           const int ncol = min(32, p.hd - c * 32);
           if (!p.out_f32) {
             uint32_t wv[16];
@@ -796,8 +800,10 @@ __global__ void __launch_bounds__(352, 1)
           }
         }
       }
-      tc_fence_before();
-      mbar_arrive(&bars->acc_free);
+      if (grp >= G::HDP / 32) {  // (hd = 32: the second warpgroup holds no accumulator chunk)
+        tc_fence_before();
+        mbar_arrive(&bars->acc_free);
+      }
       PTM(tracer, 5)
       gq += t.n_it;
       t = tn;
