@@ -8,7 +8,9 @@
 //
 //   warp 0     : TMA producer: Q once, then K_j / V_j (single-buffered, 3-D [T][H][hd] maps)
 //   warp 1     : TMEM owner + tcgen05.mma issuer: S_j = Q K_j^T into TMEM; O += P_j V_j with
-//                P_j read from TMEM (TS form: P overwrites the consumed S columns as packed bf16)
+//                P_j read from TMEM (TS form: P overwrites the consumed S columns as packed bf16);
+//                by default each K tile runs as two 64-key halves with their own S buffers
+//                (PV_a(j), S_a(j+1), PV_b(j), S_b(j+1)), so one half's softmax overlaps the other's MMAs
 //   warps 2..5 : softmax, thread = query row: tcgen05.ld S, mask, online softmax with
 //                conditional rescaling (threshold 2^8), tcgen05.st P, O rescale, final O / l, LSE.
 // ~96 KB of shared memory and 256 TMEM columns per CTA, so two CTAs share an SM and one CTA's
@@ -50,6 +52,12 @@ __device__ unsigned long long g_phase_fwd[8192][16];
 #ifndef FWD1_NPOLY
 #define FWD1_NPOLY 4
 #endif
+// Each 128-key tile as two 64-key halves with their own S buffers and online-softmax steps, so one
+// half's softmax overlaps the other half's S / PV MMAs inside the CTA (C4 forward -7..-11 %, same-box
+// A/B); FWD_ONE_S builds the single-S variant (S -> softmax -> PV strictly in sequence per CTA).
+#ifndef FWD_ONE_S
+#define FWD_HALVES 1
+#endif
 template <int HD>
 struct FwdCfg {
   using G = HeadGeom<HD>;
@@ -65,6 +73,7 @@ struct FwdCfg {
 
 struct FwdBars {
   uint64_t q_full, k_full, k_empty, v_full, v_empty, s_full, p_full, pv_done;
+  uint64_t sh_full[2], ph_full[2], pvh_done[2];  // FWD_HALVES: per 64-key half of the tile
   uint32_t tmem_base;
 };
 
@@ -106,6 +115,11 @@ __global__ void __launch_bounds__(192, 2)
     mbar_init(&bars->s_full, 1);
     mbar_init(&bars->p_full, 128);
     mbar_init(&bars->pv_done, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&bars->sh_full[i], 1);
+      mbar_init(&bars->ph_full[i], 128);
+      mbar_init(&bars->pvh_done[i], 1);
+    }
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc<C::TMEM_COLS>(&bars->tmem_base);
@@ -149,6 +163,48 @@ __global__ void __launch_bounds__(192, 2)
 #endif
       mbar_wait(&bars->q_full, 0);
       FT_MARK(0)
+#ifdef FWD_HALVES
+      // each K tile as two 64-key halves with their own S buffers (S_a cols [0, 64), S_b [64, 128)), so the
+      // softmax of one half overlaps the other half's MMAs: PV_a(j), S_a(j+1), PV_b(j), S_b(j+1), ...
+      const uint32_t idesc_h = idesc_bf16(128, 64, 0, 0);
+      auto issue_s = [&](int hh) {  // S_hh = Q K[64 hh .. 64 hh + 64)^T
+#pragma unroll
+        for (int kk = 0; kk < G::HDP / 16; ++kk)
+          mma_bf16_ss(tmem + C::S_COL + hh * 64, kmajor_desc<HD>(sQ, kk), kmajor_desc<HD>(sK + hh * 64 * G::RB, kk),
+                      idesc_h, kk > 0 ? 1u : 0u);
+        mma_commit(&bars->sh_full[hh]);
+      };
+      if (n_kv > 0) {
+        mbar_wait(&bars->k_full, 0);
+        tc_fence_after();
+        issue_s(0);
+        issue_s(1);
+        mma_commit(&bars->k_empty);
+      }
+      for (int j = 0; j < n_kv; ++j) {
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          mbar_wait(&bars->ph_full[hh], j & 1);
+          if (hh == 0) mbar_wait(&bars->v_full, j & 1);
+          tc_fence_after();
+#pragma unroll
+          for (int kk = 0; kk < 64 / 16; ++kk)  // packed P of the half's keys at its first 32 columns
+            mma_bf16_ts(tmem + C::O_COL, tmem + C::S_COL + hh * 64 + kk * 8, mnmajor_desc<HD>(sV, hh * 4 + kk),
+                        idesc_o, (j > 0 || hh > 0 || kk > 0) ? 1u : 0u);
+          mma_commit(&bars->pvh_done[hh]);
+          if (hh == 1) mma_commit(&bars->v_empty);
+          if (j + 1 < n_kv) {
+            if (hh == 0) {
+              mbar_wait(&bars->k_full, (j + 1) & 1);
+              tc_fence_after();
+            }
+            issue_s(hh);  // over P_hh(j): after PV_hh(j) in issue order
+            if (hh == 1) mma_commit(&bars->k_empty);
+          }
+        }
+      }
+      if (n_kv > 0) mma_commit(&bars->pv_done);  // once: the epilogue waits parity 0
+#else
       for (int j = 0; j < n_kv; ++j) {
         // S_j: the tensor pipe executes in issue order, so S_j overwrites P_{j-1} only after PV_{j-1}
         // has read it; p_full(j-1) (waited below) guarantees the softmax finished with S_{j-1}.
@@ -172,6 +228,7 @@ __global__ void __launch_bounds__(192, 2)
         mma_commit(&bars->v_empty);
         mma_commit(&bars->pv_done);
       }
+#endif
     }
   } else {
     // ============================ softmax warps 2..5
@@ -189,6 +246,81 @@ __global__ void __launch_bounds__(192, 2)
     const uint32_t lane_save = lane;
 #define lane (threadIdx.x == 64 ? 0u : 1u)
 #endif
+#ifdef FWD_HALVES
+    // per tile j, the two 64-key halves as separate online-softmax steps (same running max / sum)
+    for (int j = 0; j < n_kv; ++j) {
+      const int k0 = sa + visit_tile(qi, j0 + j) * 128;
+      const bool partial = !valid || (e_r < k0 + 128);
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) {
+        mbar_wait(&bars->sh_full[hh], j & 1);
+        tc_fence_after();
+        uint32_t sv[2][32];
+        tmem_ld32(tmem_addr(tmem, quarter, C::S_COL + hh * 64), sv[0]);
+        tmem_ld32(tmem_addr(tmem, quarter, C::S_COL + hh * 64 + 32), sv[1]);
+        tmem_ld_wait();
+        if (partial) {
+#pragma unroll
+          for (int c = 0; c < 2; ++c) {
+            const uint32_t m = valid ? row_mask32(e_r, r, pp, k0 + hh * 64 + c * 32) : 0u;
+#pragma unroll
+            for (int q = 0; q < 32; ++q)
+              if (!((m >> q) & 1u)) sv[c][q] = __float_as_uint(-INFINITY);
+          }
+        }
+        float m0 = -INFINITY, m1 = -INFINITY;
+#pragma unroll
+        for (int q = 0; q < 32; q += 2) {
+          m0 = fmaxf(m0, fmaxf(__uint_as_float(sv[0][q]), __uint_as_float(sv[0][q + 1])));
+          m1 = fmaxf(m1, fmaxf(__uint_as_float(sv[1][q]), __uint_as_float(sv[1][q + 1])));
+        }
+        const float mx_s = fmaxf(m0, m1) * sl2;
+        float factor = 1.f;
+        bool rescale = false;
+        if (mx_s > m_used + 8.f) {  // conditional rescale (also the first finite max)
+          factor = (m_used == -INFINITY) ? 0.f : fast_exp2(m_used - mx_s);
+          m_used = mx_s;
+          rescale = true;
+        }
+        const float base = (m_used == -INFINITY) ? 0.f : m_used;
+        const float2 sl2v = make_float2(sl2, sl2), nbase = make_float2(-base, -base);
+        float2 rs2 = make_float2(0.f, 0.f);
+        uint32_t w[32];
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+#pragma unroll
+          for (int q = 0; q < 32; q += 2) {
+            const float2 x = __ffma2_rn(make_float2(__uint_as_float(sv[c][q]), __uint_as_float(sv[c][q + 1])), sl2v, nbase);
+            const float2 pp2 = ((q & 15) + 2 > 16 - FWD1_NPOLY) ? exp2_poly3x2(x) : make_float2(fast_exp2(x.x), fast_exp2(x.y));
+            rs2 = __fadd2_rn(rs2, pp2);
+            w[c * 16 + (q >> 1)] = pack_bf16(pp2.x, pp2.y);
+          }
+        tmem_st32(tmem_addr(tmem, quarter, C::S_COL + hh * 64), w);
+        // O rescale (rare): every earlier PV must be complete -- the other half's latest PV is the only one
+        // the S commit does not cover (PV_b(j-1) for half a, PV_a(j) for half b)
+        if (__any_sync(0xffffffffu, rescale) && (j > 0 || hh > 0)) {
+          if (hh == 0) mbar_wait(&bars->pvh_done[1], (j - 1) & 1);
+          else mbar_wait(&bars->pvh_done[0], j & 1);
+          tc_fence_after();
+          const float f = rescale ? factor : 1.f;
+#pragma unroll
+          for (int c = 0; c < G::HDP / 32; ++c) {
+            uint32_t u[32];
+            const uint32_t ta = tmem_addr(tmem, quarter, C::O_COL + c * 32);
+            tmem_ld32(ta, u);
+            tmem_ld_wait();
+#pragma unroll
+            for (int q = 0; q < 32; ++q) u[q] = __float_as_uint(__uint_as_float(u[q]) * f);
+            tmem_st32(ta, u);
+          }
+        }
+        tmem_st_wait();
+        tc_fence_before();
+        mbar_arrive(&bars->ph_full[hh]);
+        l = l * factor + (rs2.x + rs2.y);
+      }
+    }
+#else
     for (int j = 0; j < n_kv; ++j) {
       const int k0 = sa + visit_tile(qi, j0 + j) * 128;
       // s_full(j) also implies PV_{j-1} completed (commit tracks all prior tcgen05 ops)
@@ -283,13 +415,18 @@ __global__ void __launch_bounds__(192, 2)
       l = l * factor + (rs + rs2.x + rs2.y);
       FT_MARK(6)
     }
+#endif
 #ifdef CADET_PHASE_TIMING
 #undef lane
     (void)lane_save;
 #endif
     // ---- epilogue: O / l, LSE
     if (n_kv > 0) {
+#ifdef FWD_HALVES
+      mbar_wait(&bars->pv_done, 0);
+#else
       mbar_wait(&bars->pv_done, (n_kv - 1) & 1);
+#endif
       tc_fence_after();
     }
     if (S > 1) {  // split-KV partial: unnormalised O, the split's max (log2 units) and row sum
