@@ -49,8 +49,10 @@ __device__ unsigned long long g_phase_fwd[8192][16];
 #define PP_FLUSH(lo, hi)
 #endif
 
+// FWD1_NPOLY of every 16 exponentials on the FMA pipe (exp2_poly3x2): 4 helped the single-S kernel
+// (~3 %); with the 64-key halves the issue slots, not the MUFU pipe, bind and 0 is fastest
 #ifndef FWD1_NPOLY
-#define FWD1_NPOLY 4
+#define FWD1_NPOLY 0
 #endif
 // Each 128-key tile as two 64-key halves with their own S buffers and online-softmax steps, so one
 // half's softmax overlaps the other half's S / PV MMAs inside the CTA (C4 forward -7..-11 %, same-box
