@@ -447,7 +447,7 @@ template <int HD>
 __global__ void __launch_bounds__(352, 1)
     attn_bwd_dkv_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constant__ CUtensorMap mK,
                         const __grid_constant__ CUtensorMap mV, const __grid_constant__ CUtensorMap mdO,
-                        const AttnParams p) {
+                        const __grid_constant__ CUtensorMap mDSs, const AttnParams p) {
   using G = HeadGeom<HD>;
   using C = DkvCfg<HD>;
   if (threadIdx.x == 0) { TR(1, 0, gtime()); TR(1, 4, smid()); }
@@ -729,9 +729,12 @@ __global__ void __launch_bounds__(352, 1)
             const uint32_t va = vst + (grp * 64 + c * 32) * 4;
             uint32_t wd[16];
             dkv_ds_chunk_pk(c == 0 ? ud0 : ud1, &pk[c * 16], va, wd);
-            if (p.dS) {
-              if (c == 0)
+            if (p.dS) {  // chunk 0 -> the warp's stage now (after the previous TMA store read it), chunk 1 kept
+              if (c == 0) {
+                if (lane == 0) bulk_wait_read0();
+                __syncwarp();
                 warp_stage_rows_bf16(smem_u32(smem + C::STG_OFF + (warp - 2) * 2048), wd);
+              }
               else
 #pragma unroll
                 for (int j = 0; j < 16; ++j) wkeep[j] = wd[j];
@@ -750,14 +753,25 @@ __global__ void __launch_bounds__(352, 1)
           const int qt = entry & 0xFFFF;
           const int slot = ds_base + qt * (qt + 1) / 2;
           if (slot < p.ds_slots) {  // (a batch violating max_seqlen latches E_TOO_LONG; stay in bounds)
+            // the warp's 32 keys x 32 q chunks leave through TMA bulk tensor stores straight from the
+            // (64B-swizzled) stage: no LDS / STG by the warp, which moves on to the next q-tile
             const uint32_t stg = smem_u32(smem + C::STG_OFF + (warp - 2) * 2048);
-            __nv_bfloat16* dst =
-                reinterpret_cast<__nv_bfloat16*>(p.dS) + (((size_t)slot * 128 + quarter * 32) * p.H + t.h) * 128 + grp * 64;
-            // streaming (evict-first) stores: the dS^T tiles are read once, by the next kernel, from
-            // HBM anyway; keep L2 for the Q / dO tiles the other k-tiles re-read
-            warp_flush_rows_bf16<true>(stg, dst, (size_t)p.H * 128, 32, 32);
+            const int row = slot * 128 + quarter * 32;
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_3d(&mDSs, stg, grp * 64, t.h, row);
+              bulk_commit();
+              bulk_wait_read0();
+            }
+            __syncwarp();
             warp_stage_rows_bf16(stg, wkeep);
-            warp_flush_rows_bf16<true>(stg, dst + 32, (size_t)p.H * 128, 32, 32);
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_3d(&mDSs, stg, grp * 64 + 32, t.h, row);
+              bulk_commit();
+            }
           } else {
             __syncwarp();
           }
@@ -765,6 +779,8 @@ __global__ void __launch_bounds__(352, 1)
         if (tracer) { TLX(14 + grp, g) }
       }
       // dK, dV (thread = key row; each warpgroup writes half of the hd columns)
+      if (lane == 0) bulk_wait_read0();  // the stage is free of the last dS^T store
+      __syncwarp();
       PTM(tracer, 7)
       mbar_wait(&bars->mma_done, wi & 1);
       tc_fence_after();
@@ -811,6 +827,7 @@ __global__ void __launch_bounds__(352, 1)
       if (w2 < n_work) tn = dkv_work(p, w2);
     }
   }
+  if (warp >= 2 && warp < 10 && lane == 0) bulk_wait0();  // this warp's dS^T stores complete
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -1029,7 +1046,7 @@ static int num_sms_attn() {
 
 template <int HD>
 static cudaError_t bwd_hd(const CUtensorMap& mQ, const CUtensorMap& mK, const CUtensorMap& mV, const CUtensorMap& mdO,
-                          const CUtensorMap& mDS, const AttnParams& p, cudaStream_t st) {
+                          const CUtensorMap& mDS, const CUtensorMap& mDSs, const AttnParams& p, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(attn_bwd_dq_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1050,13 +1067,13 @@ static cudaError_t bwd_hd(const CUtensorMap& mQ, const CUtensorMap& mK, const CU
     ProfScope ps(PROF_ATTN_BWD, st, 2);
     if (p.dS) {  // two-pass: dK, dV and the dS^T tiles, then dQ from the tiles
       cudaError_t e = launch_pdl(attn_bwd_dkv_kernel<HD>, grid, DkvCfg<HD>::THREADS, DkvCfg<HD>::SMEM, st, mQ, mK, mV,
-                                 mdO, p);
+                                 mdO, mDSs, p);
       if (e == cudaSuccess) e = launch_pdl(attn_bwd_dq2_kernel<HD>, grid, Dq2Cfg<HD>::THREADS, Dq2Cfg<HD>::SMEM, st, mK, mDS, p);
       if (e != cudaSuccess) return e;
     } else {
       cudaError_t e = launch_pdl(attn_bwd_dq_kernel<HD>, grid, DqCfg<HD>::THREADS, DqCfg<HD>::SMEM, st, mQ, mK, mV, mdO, p);
       if (e == cudaSuccess)
-        e = launch_pdl(attn_bwd_dkv_kernel<HD>, grid, DkvCfg<HD>::THREADS, DkvCfg<HD>::SMEM, st, mQ, mK, mV, mdO, p);
+        e = launch_pdl(attn_bwd_dkv_kernel<HD>, grid, DkvCfg<HD>::THREADS, DkvCfg<HD>::SMEM, st, mQ, mK, mV, mdO, mDSs, p);
       if (e != cudaSuccess) return e;
     }
   }
@@ -1075,17 +1092,24 @@ cudaError_t attn_bwd_pre_launch(const void* O, const void* dO, float* D, float* 
 
 cudaError_t attn_bwd_launch(const void* Qr, const void* Kr, const void* V, const void* dO, const AttnParams& p,
                             cudaStream_t st) {
-  CUtensorMap mQ, mK, mV, mdO, mDS;
+  CUtensorMap mQ, mK, mV, mdO, mDS, mDSs;
   memset(&mDS, 0, sizeof(mDS));
+  memset(&mDSs, 0, sizeof(mDSs));
+  if (p.dS) {  // dS^T stores from the dK/dV kernel's 32 x 32 warp stages: [rows][H][128] bf16, 64B swizzle
+    uint64_t dims[3] = {128, (uint64_t)p.H, (uint64_t)p.ds_slots * 128};
+    uint64_t strides[2] = {128 * 2, (uint64_t)p.H * 128 * 2};
+    uint32_t box[3] = {32, 1, 32};
+    if (!encode_bf16_map(&mDSs, p.dS, 3, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_64B)) return cudaErrorInvalidValue;
+  }
   if (!make_head_map(&mQ, Qr, p.T, p.H, p.hd) || !make_head_map(&mK, Kr, p.T, p.H, p.hd) ||
       !make_head_map(&mV, V, p.T, p.H, p.hd) || !make_head_map(&mdO, dO, p.T, p.H, p.hd) ||
       (p.dS && !make_head_map(&mDS, p.dS, p.ds_slots * 128, p.H, 128)))
     return cudaErrorInvalidValue;
   switch ((p.hd + 31) / 32 * 32) {
-    case 32: return bwd_hd<32>(mQ, mK, mV, mdO, mDS, p, st);
-    case 64: return bwd_hd<64>(mQ, mK, mV, mdO, mDS, p, st);
-    case 96: return bwd_hd<96>(mQ, mK, mV, mdO, mDS, p, st);
-    case 128: return bwd_hd<128>(mQ, mK, mV, mdO, mDS, p, st);
+    case 32: return bwd_hd<32>(mQ, mK, mV, mdO, mDS, mDSs, p, st);
+    case 64: return bwd_hd<64>(mQ, mK, mV, mdO, mDS, mDSs, p, st);
+    case 96: return bwd_hd<96>(mQ, mK, mV, mdO, mDS, mDSs, p, st);
+    case 128: return bwd_hd<128>(mQ, mK, mV, mdO, mDS, mDSs, p, st);
     default: return cudaErrorInvalidValue;
   }
 }

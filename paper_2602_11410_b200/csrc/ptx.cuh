@@ -121,6 +121,17 @@ CADET_DEV void tma_load_3d(void* dst, const CUtensorMap* m, uint64_t* bar, int c
       : "memory");
 }
 
+// TMA store (shared -> global, bulk-group completion) and its group waits
+CADET_DEV void tma_store_3d(const CUtensorMap* m, uint32_t src_smem, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(m)),
+               "r"(src_smem), "r"(c0), "r"(c1), "r"(c2)
+               : "memory");
+}
+CADET_DEV void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+CADET_DEV void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+CADET_DEV void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
 // L2 eviction-priority policies for TMA loads: streamed-once data (evict_first) must not push out
 // tiles that other CTAs re-read (evict_last).
 CADET_DEV uint64_t l2_policy_evict_first() {
