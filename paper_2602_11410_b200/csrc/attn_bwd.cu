@@ -411,6 +411,9 @@ struct DkvCfg {
   static constexpr int VEC_OFF = DO_OFF + 2 * G::TILE_BYTES;
   static constexpr int VEC_BYTES = 2048;
   static constexpr int STG_OFF = VEC_OFF + VSTAGES * VEC_BYTES;  // [8 compute warps][2 KB] store transpose
+  // dS^T chunks by TMA bulk tensor stores from the stage (hd 128: -4..-7 % on C4) or by the warp's own
+  // LDS + STG (hd <= 96: the TMA variant measured +5 % on C3's attention backward)
+  static constexpr bool TMA_DS = HD == 128;
   static constexpr int BAR_OFF = STG_OFF + 8 * 2048;
   static constexpr int SMEM = BAR_OFF + 256 + 1024;
   // S^T/P^T half-buffers at [0,64) and [64,128); dP^T/dS^T at [128,192) and [192,256)
@@ -731,8 +734,10 @@ __global__ void __launch_bounds__(352, 1)
             dkv_ds_chunk_pk(c == 0 ? ud0 : ud1, &pk[c * 16], va, wd);
             if (p.dS) {  // chunk 0 -> the warp's stage now (after the previous TMA store read it), chunk 1 kept
               if (c == 0) {
-                if (lane == 0) bulk_wait_read0();
-                __syncwarp();
+                if (C::TMA_DS) {
+                  if (lane == 0) bulk_wait_read0();
+                  __syncwarp();
+                }
                 warp_stage_rows_bf16(smem_u32(smem + C::STG_OFF + (warp - 2) * 2048), wd);
               }
               else
@@ -756,21 +761,30 @@ __global__ void __launch_bounds__(352, 1)
             // the warp's 32 keys x 32 q chunks leave through TMA bulk tensor stores straight from the
             // (64B-swizzled) stage: no LDS / STG by the warp, which moves on to the next q-tile
             const uint32_t stg = smem_u32(smem + C::STG_OFF + (warp - 2) * 2048);
-            const int row = slot * 128 + quarter * 32;
-            fence_proxy_async_smem();
-            __syncwarp();
-            if (lane == 0) {
-              tma_store_3d(&mDSs, stg, grp * 64, t.h, row);
-              bulk_commit();
-              bulk_wait_read0();
-            }
-            __syncwarp();
-            warp_stage_rows_bf16(stg, wkeep);
-            fence_proxy_async_smem();
-            __syncwarp();
-            if (lane == 0) {
-              tma_store_3d(&mDSs, stg, grp * 64 + 32, t.h, row);
-              bulk_commit();
+            if (C::TMA_DS) {
+              const int row = slot * 128 + quarter * 32;
+              fence_proxy_async_smem();
+              __syncwarp();
+              if (lane == 0) {
+                tma_store_3d(&mDSs, stg, grp * 64, t.h, row);
+                bulk_commit();
+                bulk_wait_read0();
+              }
+              __syncwarp();
+              warp_stage_rows_bf16(stg, wkeep);
+              fence_proxy_async_smem();
+              __syncwarp();
+              if (lane == 0) {
+                tma_store_3d(&mDSs, stg, grp * 64 + 32, t.h, row);
+                bulk_commit();
+              }
+            } else {
+              __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(p.dS) +
+                                   (((size_t)slot * 128 + quarter * 32) * p.H + t.h) * 128 + grp * 64;
+              // streaming (evict-first) stores: the dS^T tiles are read once, by the next kernel
+              warp_flush_rows_bf16<true>(stg, dst, (size_t)p.H * 128, 32, 32);
+              warp_stage_rows_bf16(stg, wkeep);
+              warp_flush_rows_bf16<true>(stg, dst + 32, (size_t)p.H * 128, 32, 32);
             }
           } else {
             __syncwarp();
