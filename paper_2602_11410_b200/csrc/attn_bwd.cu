@@ -450,7 +450,8 @@ template <int HD>
 __global__ void __launch_bounds__(352, 1)
     attn_bwd_dkv_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constant__ CUtensorMap mK,
                         const __grid_constant__ CUtensorMap mV, const __grid_constant__ CUtensorMap mdO,
-                        const __grid_constant__ CUtensorMap mDSs, const AttnParams p) {
+                        const __grid_constant__ CUtensorMap mDSs, const __grid_constant__ CUtensorMap mDK,
+                        const __grid_constant__ CUtensorMap mDV, const AttnParams p) {
   using G = HeadGeom<HD>;
   using C = DkvCfg<HD>;
   if (threadIdx.x == 0) { TR(1, 0, gtime()); TR(1, 4, smid()); }
@@ -818,10 +819,27 @@ __global__ void __launch_bounds__(352, 1)
             uint32_t wv[16];
 #pragma unroll
             for (int j = 0; j < 16; ++j) wv[j] = pack_bf16(f * __uint_as_float(u[2 * j]), f * __uint_as_float(u[2 * j + 1]));
-            warp_store_rows_bf16(smem_u32(smem + C::STG_OFF + (warp - 2) * 2048), wv,
-                                 reinterpret_cast<__nv_bfloat16*>(out) + (size_t)(t.k0 + quarter * 32) * p.d +
-                                     (size_t)t.h * p.hd + c * 32,
-                                 p.d, t.keys_valid - (int)quarter * 32, ncol);
+            const uint32_t stg = smem_u32(smem + C::STG_OFF + (warp - 2) * 2048);
+            if (C::TMA_DS && t.keys_valid == 128 && p.dS) {  // full k-tile: TMA bulk store from the stage
+              if (lane == 0) bulk_wait_read0();
+              __syncwarp();
+              warp_stage_rows_bf16(stg, wv);
+              fence_proxy_async_smem();
+              __syncwarp();
+              if (lane == 0) {
+                tma_store_3d(which == 0 ? &mDK : &mDV, stg, c * 32, t.h, t.k0 + quarter * 32);
+                bulk_commit();
+              }
+            } else {
+              if (C::TMA_DS) {
+                if (lane == 0) bulk_wait_read0();
+                __syncwarp();
+              }
+              warp_store_rows_bf16(stg, wv,
+                                   reinterpret_cast<__nv_bfloat16*>(out) + (size_t)(t.k0 + quarter * 32) * p.d +
+                                       (size_t)t.h * p.hd + c * 32,
+                                   p.d, t.keys_valid - (int)quarter * 32, ncol);
+            }
           } else if (key_valid) {  // fp32 outputs (exactness mode): direct row stores
             float* o = reinterpret_cast<float*>(out) + (size_t)key * p.d + (size_t)t.h * p.hd + c * 32;
             for (int j = 0; j < ncol; j += 4)
@@ -1060,7 +1078,8 @@ static int num_sms_attn() {
 
 template <int HD>
 static cudaError_t bwd_hd(const CUtensorMap& mQ, const CUtensorMap& mK, const CUtensorMap& mV, const CUtensorMap& mdO,
-                          const CUtensorMap& mDS, const CUtensorMap& mDSs, const AttnParams& p, cudaStream_t st) {
+                          const CUtensorMap& mDS, const CUtensorMap& mDSs, const CUtensorMap& mDK, const CUtensorMap& mDV,
+                          const AttnParams& p, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(attn_bwd_dq_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1081,13 +1100,14 @@ static cudaError_t bwd_hd(const CUtensorMap& mQ, const CUtensorMap& mK, const CU
     ProfScope ps(PROF_ATTN_BWD, st, 2);
     if (p.dS) {  // two-pass: dK, dV and the dS^T tiles, then dQ from the tiles
       cudaError_t e = launch_pdl(attn_bwd_dkv_kernel<HD>, grid, DkvCfg<HD>::THREADS, DkvCfg<HD>::SMEM, st, mQ, mK, mV,
-                                 mdO, mDSs, p);
+                                 mdO, mDSs, mDK, mDV, p);
       if (e == cudaSuccess) e = launch_pdl(attn_bwd_dq2_kernel<HD>, grid, Dq2Cfg<HD>::THREADS, Dq2Cfg<HD>::SMEM, st, mK, mDS, p);
       if (e != cudaSuccess) return e;
     } else {
       cudaError_t e = launch_pdl(attn_bwd_dq_kernel<HD>, grid, DqCfg<HD>::THREADS, DqCfg<HD>::SMEM, st, mQ, mK, mV, mdO, p);
       if (e == cudaSuccess)
-        e = launch_pdl(attn_bwd_dkv_kernel<HD>, grid, DkvCfg<HD>::THREADS, DkvCfg<HD>::SMEM, st, mQ, mK, mV, mdO, mDSs, p);
+        e = launch_pdl(attn_bwd_dkv_kernel<HD>, grid, DkvCfg<HD>::THREADS, DkvCfg<HD>::SMEM, st, mQ, mK, mV, mdO, mDSs,
+                       mDK, mDV, p);
       if (e != cudaSuccess) return e;
     }
   }
@@ -1106,9 +1126,19 @@ cudaError_t attn_bwd_pre_launch(const void* O, const void* dO, float* D, float* 
 
 cudaError_t attn_bwd_launch(const void* Qr, const void* Kr, const void* V, const void* dO, const AttnParams& p,
                             cudaStream_t st) {
-  CUtensorMap mQ, mK, mV, mdO, mDS, mDSs;
+  CUtensorMap mQ, mK, mV, mdO, mDS, mDSs, mDK, mDV;
   memset(&mDS, 0, sizeof(mDS));
   memset(&mDSs, 0, sizeof(mDSs));
+  memset(&mDK, 0, sizeof(mDK));
+  memset(&mDV, 0, sizeof(mDV));
+  if (p.dS && p.hd == 128 && !p.out_f32) {  // dK / dV drains of full k-tiles by TMA stores: [T][H][128], 64B swizzle
+    uint64_t dims[3] = {(uint64_t)p.hd, (uint64_t)p.H, (uint64_t)p.T};
+    uint64_t strides[2] = {(uint64_t)p.hd * 2, (uint64_t)p.H * p.hd * 2};
+    uint32_t box[3] = {32, 1, 32};
+    if (!encode_bf16_map(&mDK, p.dK, 3, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_64B) ||
+        !encode_bf16_map(&mDV, p.dV, 3, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_64B))
+      return cudaErrorInvalidValue;
+  }
   if (p.dS) {  // dS^T stores from the dK/dV kernel's 32 x 32 warp stages: [rows][H][128] bf16, 64B swizzle
     uint64_t dims[3] = {128, (uint64_t)p.H, (uint64_t)p.ds_slots * 128};
     uint64_t strides[2] = {128 * 2, (uint64_t)p.H * 128 * 2};
@@ -1120,10 +1150,10 @@ cudaError_t attn_bwd_launch(const void* Qr, const void* Kr, const void* V, const
       (p.dS && !make_head_map(&mDS, p.dS, p.ds_slots * 128, p.H, 128)))
     return cudaErrorInvalidValue;
   switch ((p.hd + 31) / 32 * 32) {
-    case 32: return bwd_hd<32>(mQ, mK, mV, mdO, mDS, mDSs, p, st);
-    case 64: return bwd_hd<64>(mQ, mK, mV, mdO, mDS, mDSs, p, st);
-    case 96: return bwd_hd<96>(mQ, mK, mV, mdO, mDS, mDSs, p, st);
-    case 128: return bwd_hd<128>(mQ, mK, mV, mdO, mDS, mDSs, p, st);
+    case 32: return bwd_hd<32>(mQ, mK, mV, mdO, mDS, mDSs, mDK, mDV, p, st);
+    case 64: return bwd_hd<64>(mQ, mK, mV, mdO, mDS, mDSs, mDK, mDV, p, st);
+    case 96: return bwd_hd<96>(mQ, mK, mV, mdO, mDS, mDSs, mDK, mDV, p, st);
+    case 128: return bwd_hd<128>(mQ, mK, mV, mdO, mDS, mDSs, mDK, mDV, p, st);
     default: return cudaErrorInvalidValue;
   }
 }
