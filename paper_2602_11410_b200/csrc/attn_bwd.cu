@@ -358,15 +358,15 @@ CADET_DEV uint32_t dkv_prefix_mask(uint32_t vaddr, int key) {
   }
   return vis;
 }
-// Softmax phase of one 32-column chunk: P = exp2(S^T log2e / sqrt(hd) - LSE log2e) (LSE at vaddr), packed
+// Softmax phase of one 32-column chunk: P = exp2(S^T log2e / sqrt(hd) - LSE log2e) (-LSE log2e at vaddr), packed
 // bf16 into wp; MASKED: invisible columns (vis bit clear) give exactly 0.
 template <bool MASKED>
 CADET_DEV void dkv_p_chunk(const uint32_t (&us)[32], uint32_t vaddr, uint32_t vis, float sl2, uint32_t (&wp)[16]) {
-  const float2 sl2v = make_float2(sl2, sl2), nlog2e = make_float2(-1.4426950408889634f, -1.4426950408889634f);
+  const float2 sl2v = make_float2(sl2, sl2);
 #pragma unroll
   for (int i = 0; i < 32; i += 4) {
-    const float4 l4 = lds_f4(vaddr + i * 4);
-    const float2 nl01 = __fmul2_rn(make_float2(l4.x, l4.y), nlog2e), nl23 = __fmul2_rn(make_float2(l4.z, l4.w), nlog2e);
+    const float4 l4 = lds_f4(vaddr + i * 4);  // -LSE log2e, premultiplied by the vector loader
+    const float2 nl01 = make_float2(l4.x, l4.y), nl23 = make_float2(l4.z, l4.w);
     float2 x01 = __ffma2_rn(make_float2(__uint_as_float(us[i]), __uint_as_float(us[i + 1])), sl2v, nl01);
     float2 x23 = __ffma2_rn(make_float2(__uint_as_float(us[i + 2]), __uint_as_float(us[i + 3])), sl2v, nl23);
     if (MASKED) {
@@ -405,7 +405,7 @@ struct DkvCfg {
   static constexpr int V_OFF = K_OFF + G::TILE_BYTES;
   static constexpr int Q_OFF = V_OFF + G::TILE_BYTES;          // two stages
   static constexpr int DO_OFF = Q_OFF + 2 * G::TILE_BYTES;     // two stages
-  // VSTAGES stages of one q-tile's column vectors, written by the vector-loader warp: LSE [128] f32 at +0,
+  // VSTAGES stages of one q-tile's column vectors, written by the vector-loader warp: -LSE log2e [128] f32 at +0,
   // D [128] f32 at +512, kv_end [128] i32 at +1024, the visit-list entry at +1536
   static constexpr int VSTAGES = 4;
   static constexpr int VEC_OFF = DO_OFF + 2 * G::TILE_BYTES;
@@ -634,7 +634,7 @@ __global__ void __launch_bounds__(352, 1)
         for (int j = 0; j < 4; ++j) {
           const int q = q0 + j * 32 + lane;
           const bool v = q < t.se;
-          lv[j] = v ? p.lse[(size_t)t.h * p.T + q] : INFINITY;
+          lv[j] = v ? -1.4426950408889634f * p.lse[(size_t)t.h * p.T + q] : -INFINITY;  // -LSE log2e
           dv[j] = v ? p.D[(size_t)t.h * p.T + q] : 0.f;
           ev[j] = v ? p.plan.kv_end[q] : -1;
         }
