@@ -84,6 +84,32 @@ __device__ __forceinline__ void kb_to_seg(const KProb& q, int kb, int& seg, int&
   kk = kb;
 }
 
+// The k-block walk of one unit with the per-segment fields in registers: the producer / MMA loops
+// otherwise re-read them from parameter space after every mbarrier wait (the waits clobber memory),
+// a dependent chain of constant loads per k-block that made short-K GEMMs (d 352) issue-bound.
+struct SegCursor {
+  int seg, kk, left;  // left: k-blocks before the next segment (the last segment never advances)
+  uint32_t a_mn, b_mn;
+  __device__ __forceinline__ void load(const KProb& q) {
+    a_mn = (uint32_t)q.a_mn[seg];
+    b_mn = (uint32_t)q.b_mn[seg];
+  }
+  __device__ __forceinline__ void init(const KProb& q, int kb) {
+    kb_to_seg(q, kb, seg, kk);
+    left = seg + 1 < q.nseg ? q.kb[seg] - kk : 0x7fffffff;
+    load(q);
+  }
+  __device__ __forceinline__ void next(const KProb& q) {
+    ++kk;
+    if (--left == 0) {
+      ++seg;
+      kk = 0;
+      left = seg + 1 < q.nseg ? q.kb[seg] : 0x7fffffff;
+      load(q);
+    }
+  }
+};
+
 // ---------------------------------------------------------------- epilogue helpers
 // Epilogue mode sets (compile time): each GEMM launch instantiates only the epilogues of its
 // problems, so e.g. a plain store does not carry the gate + RoPE epilogue's registers.
@@ -485,26 +511,29 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_kernel(const __grid_cons
         const Unit U = decode_unit(P, u);
         const KProb& q = P.p[U.p];
         const int n0 = U.n0 * BN;
-        for (int kb = U.kb_lo; kb < U.kb_hi; ++kb, ++it) {
+        const int bke = q.tf32 ? BK / 2 : BK;  // a 128-byte K row: 64 bf16 / 32 fp32
+        SegCursor sc;
+        sc.init(q, U.kb_lo);
+        for (int kb = U.kb_lo; kb < U.kb_hi; ++kb, ++it, sc.next(q)) {
           const uint32_t stage = it % C::STAGES, use = it / C::STAGES;
           if (use > 0) mbar_wait(&empty[stage], (use - 1) & 1);
-          int seg, kk;
-          kb_to_seg(q, kb, seg, kk);
-          const int k0 = kk * (q.tf32 ? BK / 2 : BK);  // a 128-byte K row: 64 bf16 / 32 fp32
+          const int k0 = sc.kk * bke;
+          const CUtensorMap* mA = &P.mA[U.p][sc.seg];
+          const CUtensorMap* mB = &P.mB[U.p][sc.seg];
           uint8_t* sA = smem + stage * C::STAGE_BYTES;
           uint8_t* sB = sA + C::A_BYTES;
           mbar_expect_tx(&full[stage], C::STAGE_BYTES);
-          if (!q.a_mn[seg]) {
-            tma_load_2d(sA, &P.mA[U.p][seg], &full[stage], k0, U.m0);
+          if (!sc.a_mn) {
+            tma_load_2d(sA, mA, &full[stage], k0, U.m0);
           } else {
 #pragma unroll
-            for (int j = 0; j < BM / 64; ++j) tma_load_2d(sA + j * 8192, &P.mA[U.p][seg], &full[stage], U.m0 + 64 * j, k0);
+            for (int j = 0; j < BM / 64; ++j) tma_load_2d(sA + j * 8192, mA, &full[stage], U.m0 + 64 * j, k0);
           }
-          if (!q.b_mn[seg]) {
-            tma_load_2d(sB, &P.mB[U.p][seg], &full[stage], k0, n0);
+          if (!sc.b_mn) {
+            tma_load_2d(sB, mB, &full[stage], k0, n0);
           } else {
 #pragma unroll
-            for (int j = 0; j < BN / 64; ++j) tma_load_2d(sB + j * 8192, &P.mB[U.p][seg], &full[stage], n0 + 64 * j, k0);
+            for (int j = 0; j < BN / 64; ++j) tma_load_2d(sB + j * 8192, mB, &full[stage], n0 + 64 * j, k0);
           }
         }
       }
@@ -521,23 +550,25 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_kernel(const __grid_cons
         if (use > 0) mbar_wait(&tempty[buf], (use - 1) & 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + buf * BN;
-        for (int kb = U.kb_lo; kb < U.kb_hi; ++kb, ++it) {
+        const bool tf32 = q.tf32 != 0;
+        const uint32_t fmask = q.f16 ? ~((7u << 7) | (7u << 10)) : ~0u;  // F16: format 0
+        SegCursor sc;
+        sc.init(q, U.kb_lo);
+        for (int kb = U.kb_lo; kb < U.kb_hi; ++kb, ++it, sc.next(q)) {
           const uint32_t stage = it % C::STAGES, suse = it / C::STAGES;
           mbar_wait(&full[stage], suse & 1);
           tc_fence_after();
-          int seg, kk;
-          kb_to_seg(q, kb, seg, kk);
-          const uint32_t a_mn = q.a_mn[seg], b_mn = q.b_mn[seg];
+          const uint32_t a_mn = sc.a_mn, b_mn = sc.b_mn;
           const uint32_t sA = smem_u32(smem + stage * C::STAGE_BYTES);
           const uint32_t sB = sA + C::A_BYTES;
-          if (q.tf32) {  // K-major fp32 tiles: 4 x (K = 8) per 128-byte row, same 32-byte descriptor steps
+          if (tf32) {  // K-major fp32 tiles: 4 x (K = 8) per 128-byte row, same 32-byte descriptor steps
             const uint32_t idesc = idesc_tf32(BM, BN);
 #pragma unroll
             for (int k = 0; k < BK / 16; ++k)
               mma_tf32_ss(d_tmem, smem_desc(sA + k * 32, 16, 1024, SWZ_128B), smem_desc(sB + k * 32, 16, 1024, SWZ_128B),
                           idesc, (kb > U.kb_lo || k > 0) ? 1u : 0u);
           } else {
-            const uint32_t idesc = idesc_bf16(BM, BN, a_mn, b_mn) & (q.f16 ? ~((7u << 7) | (7u << 10)) : ~0u);  // F16: format 0
+            const uint32_t idesc = idesc_bf16(BM, BN, a_mn, b_mn) & fmask;
 #pragma unroll
             for (int k = 0; k < BK / 16; ++k) {
               const uint64_t ad = a_mn ? smem_desc(sA + k * 2048, 8192, 1024, SWZ_128B)
@@ -673,27 +704,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
         const KProb& q = P.p[U.p];
         const int n0 = U.n0 * BN + 128 * (int)rank;
         const int m0 = U.m0 + 128 * (int)rank;
-        for (int kb = U.kb_lo; kb < U.kb_hi; ++kb, ++it) {
+        SegCursor sc;
+        sc.init(q, U.kb_lo);
+        for (int kb = U.kb_lo; kb < U.kb_hi; ++kb, ++it, sc.next(q)) {
           const uint32_t stage = it % C::STAGES, use = it / C::STAGES;
           if (use > 0) mbar_wait(&empty[stage], (use - 1) & 1);
-          int seg, kk;
-          kb_to_seg(q, kb, seg, kk);
-          const int k0 = kk * BK;
+          const int k0 = sc.kk * BK;
+          const CUtensorMap* mA = &P.mA[U.p][sc.seg];
+          const CUtensorMap* mB = &P.mB[U.p][sc.seg];
           uint8_t* sA = smem + stage * C::STAGE_BYTES;
           uint8_t* sB = sA + C::A_BYTES;
           const uint32_t fb = mapa_shared(smem_u32(&full[stage]), 0);
           if (leader) mbar_expect_tx(&full[stage], 2 * C::STAGE_BYTES);
-          if (!q.a_mn[seg]) {
-            tma_load_2d_pair(sA, &P.mA[U.p][seg], fb, k0, m0);
+          if (!sc.a_mn) {
+            tma_load_2d_pair(sA, mA, fb, k0, m0);
           } else {
-            tma_load_2d_pair(sA, &P.mA[U.p][seg], fb, m0, k0);
-            tma_load_2d_pair(sA + 8192, &P.mA[U.p][seg], fb, m0 + 64, k0);
+            tma_load_2d_pair(sA, mA, fb, m0, k0);
+            tma_load_2d_pair(sA + 8192, mA, fb, m0 + 64, k0);
           }
-          if (!q.b_mn[seg]) {
-            tma_load_2d_pair(sB, &P.mB[U.p][seg], fb, k0, n0);
+          if (!sc.b_mn) {
+            tma_load_2d_pair(sB, mB, fb, k0, n0);
           } else {
-            tma_load_2d_pair(sB, &P.mB[U.p][seg], fb, n0, k0);
-            tma_load_2d_pair(sB + 8192, &P.mB[U.p][seg], fb, n0 + 64, k0);
+            tma_load_2d_pair(sB, mB, fb, n0, k0);
+            tma_load_2d_pair(sB + 8192, mB, fb, n0 + 64, k0);
           }
         }
       }
@@ -710,14 +743,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
         if (use > 0) mbar_wait(&tempty[buf], (use - 1) & 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + buf * BN;
-        for (int kb = U.kb_lo; kb < U.kb_hi; ++kb, ++it) {
+        const uint32_t fmask = q.f16 ? ~((7u << 7) | (7u << 10)) : ~0u;  // F16: format 0
+        SegCursor sc;
+        sc.init(q, U.kb_lo);
+        for (int kb = U.kb_lo; kb < U.kb_hi; ++kb, ++it, sc.next(q)) {
           const uint32_t stage = it % C::STAGES, suse = it / C::STAGES;
           mbar_wait(&full[stage], suse & 1);
           tc_fence_after();
-          int seg, kk;
-          kb_to_seg(q, kb, seg, kk);
-          const uint32_t a_mn = q.a_mn[seg], b_mn = q.b_mn[seg];
-          const uint32_t idesc = idesc_bf16(256, BN, a_mn, b_mn) & (q.f16 ? ~((7u << 7) | (7u << 10)) : ~0u);  // F16: format 0
+          const uint32_t a_mn = sc.a_mn, b_mn = sc.b_mn;
+          const uint32_t idesc = idesc_bf16(256, BN, a_mn, b_mn) & fmask;
           const uint32_t sA = smem_u32(smem + stage * C::STAGE_BYTES);
           const uint32_t sB = sA + C::A_BYTES;
 #pragma unroll
