@@ -595,23 +595,27 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_kernel(const __grid_cons
     for (int u = blockIdx.x; u < P.total_units; u += gridDim.x, ++tc) {
       const Unit U = decode_unit(P, u);
       const KProb& q = P.p[U.p];
+      // the epilogue parameters in registers for the whole tile (parameter-space reads would be
+      // repeated after every TMEM / barrier wait, which clobber memory)
+      const EpiParams e = q.epi;
+      const int qM = q.M, qN = q.N;
       const uint32_t buf = tc & 1, use = tc >> 1;
       mbar_wait(&tfull[buf], use & 1);
       tc_fence_after();
       const int row0 = U.m0 + quarter * 32;
       const int n0 = U.n0 * BN;
       // the primary epilogue input of slice c + 2 is requested before slice c is processed
-      const void* pb = epi_primary(q.epi);
+      const void* pb = epi_primary(e);
       uint4 g[4];
       auto issue = [&](int c) {
         const int n0c = n0 + c * 32;
-        if (c < BN / 32 && n0c < q.N && row0 < q.M && pb)
-          warp_ldg_rows_bf16(pb, (size_t)row0 * q.epi.ldo + n0c, q.epi.ldo, q.M - row0, g);
+        if (c < BN / 32 && n0c < qN && row0 < qM && pb)
+          warp_ldg_rows_bf16(pb, (size_t)row0 * e.ldo + n0c, e.ldo, qM - row0, g);
       };
       issue(half);
       for (int c = half; c < BN / 32; c += 2) {
         const int n0c = n0 + c * 32;
-        if (n0c >= q.N) break;
+        if (n0c >= qN) break;
         uint4 cur[4] = {g[0], g[1], g[2], g[3]};
         issue(c + 2);
         uint32_t r[32];
@@ -620,7 +624,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_kernel(const __grid_cons
         float v[32];
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-        run_epilogue_warp<MODES>(q.epi, row0, q.M, n0c, v, stg, pb ? cur : nullptr, U.ks);
+        run_epilogue_warp<MODES>(e, row0, qM, n0c, v, stg, pb ? cur : nullptr, U.ks);
       }
       tc_fence_before();
       __syncwarp();
@@ -780,23 +784,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
     for (int u = cid; u < P.total_units; u += ncl, ++tc) {
       const Unit U = decode_unit(P, u);
       const KProb& q = P.p[U.p];
+      // the epilogue parameters in registers for the whole tile (parameter-space reads would be
+      // repeated after every TMEM / barrier wait, which clobber memory)
+      const EpiParams e = q.epi;
+      const int qM = q.M, qN = q.N;
       const uint32_t buf = tc & 1, use = tc >> 1;
       mbar_wait(&tfull[buf], use & 1);
       tc_fence_after();
       const int row0 = U.m0 + 128 * (int)rank + quarter * 32;
       const int n0 = U.n0 * BN;
       // the primary epilogue input of slice c + 2 is requested before slice c is processed
-      const void* pb = epi_primary(q.epi);
+      const void* pb = epi_primary(e);
       uint4 g[4];
       auto issue = [&](int c) {
         const int n0c = n0 + c * 32;
-        if (c < BN / 32 && n0c < q.N && row0 < q.M && pb)
-          warp_ldg_rows_bf16(pb, (size_t)row0 * q.epi.ldo + n0c, q.epi.ldo, q.M - row0, g);
+        if (c < BN / 32 && n0c < qN && row0 < qM && pb)
+          warp_ldg_rows_bf16(pb, (size_t)row0 * e.ldo + n0c, e.ldo, qM - row0, g);
       };
       issue(half);
       for (int c = half; c < BN / 32; c += 2) {
         const int n0c = n0 + c * 32;
-        if (n0c >= q.N) break;
+        if (n0c >= qN) break;
         uint4 cur[4] = {g[0], g[1], g[2], g[3]};
         issue(c + 2);
         uint32_t r[32];
@@ -805,7 +813,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
         float v[32];
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-        run_epilogue_warp<MODES>(q.epi, row0, q.M, n0c, v, stg, pb ? cur : nullptr, U.ks);
+        run_epilogue_warp<MODES>(e, row0, qM, n0c, v, stg, pb ? cur : nullptr, U.ks);
       }
       tc_fence_before();
       __syncwarp();
