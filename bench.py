@@ -24,7 +24,7 @@ import time
 import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
-TRAFFIC_PROFILE = "r02b_dram_traffic.json"  # per-class DRAM bytes per launch (scripts/traffic_summary.py)
+TRAFFIC_PROFILE = "r02c_dram_traffic.json"  # per-class DRAM bytes per launch (scripts/traffic_summary.py)
 sys.path.insert(0, ROOT)
 
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
